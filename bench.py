@@ -1,0 +1,496 @@
+"""LoopServe hot-path benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], "C2"): Llama-3.1-8B attention shapes --
+32 layers, 32 q / 8 KV heads, d = 128, bf16 -- a 3-turn dialogue of 5000-token
+inputs, 128 decoded tokens per turn, LoopServe mode with the paper defaults
+alpha = 0.955, sample 0.1 / floor 32, KV budget B = 1024, n_d = 16, warmup 16,
+obs window 16. Synthetic structured Q/K/V generated on the
+device; Q/K/V of all layers (~6 GB) exceed L2, so no flush is needed.
+
+One step = one full dialogue: per turn the sparse prefill of every layer
+(K0 sampling, K1 scoring, K2-K4 selection, K5 sparse attention, decode seeds)
+and 128 compressed decode steps of every layer (K7/K8 events + K6).
+  value  = TTFT: mean sparse-prefill time of one turn block over all layers, ms
+  decode_tokens_per_s = decoded tokens / decode time
+Multi-GPU (torchrun): KV-head groups are split across ranks (all q-heads of a
+group on one rank, K/V never replicated) and each layer's attention output is
+all-gathered over NCCL (the head concat before W_O, model.py:259); time is the
+max over ranks ("strong" scaling: the dialogue is fixed).
+
+--impl reference: the reference algorithm's CPU implementation (the oracle
+port of oracle/, run with all host cores on a bounded sample of the same
+workload, extrapolated to the full dialogue; the reference itself is pure
+Python and cannot travel to the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill TTFT (ms) & decode tokens/s, Llama-3.1-8B attn shapes, 1/2/4/8 B200"
+
+CONFIGS = {
+    "c2": dict(workload="C2: Llama-3.1-8B attention (32q/8kv, d=128, bf16), 32 layers, 3 turns x 5000 tokens, "
+                        "128 decoded tokens/turn, alpha=0.955, B=1024, n_d=16, sparse prefill + compressed decode",
+               n_layers=32, n_q=32, n_kv=8, d=128, input_len=5000, n_turns=3, max_new=128, alpha=0.955,
+               budget=1024, interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),
+    "c1": dict(workload="C1: toy attention layer (8 heads MHA, d=64), 3 turns x 1000 tokens, alpha=0.9, B=256",
+               n_layers=1, n_q=8, n_kv=8, d=64, input_len=1000, n_turns=3, max_new=32, alpha=0.9, budget=256,
+               interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return dict(hbm=d["hbm_gbs"], tensor=d["bf16_tflops"], tensor_sus=d.get("bf16_tflops_sustained"),
+                    src="measured")
+    return dict(hbm=6650.0, tensor=1590.0, tensor_sus=1400.0, src="fallback")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ CPU baseline
+_CPU = {}
+
+
+def _cpu_unit(args):
+    """One (turn, head) of the sparse prefill on the oracle: sparsify_head +
+    masked_sparse_attention (session.py:135-152 / model.py:242-251)."""
+    turn, head = args
+    import numpy as np
+
+    from oracle.session import prefill_head
+
+    d = _CPU
+    ro, n_new = d["blocks"][turn]
+    n_total = ro + n_new
+    g = head // d["group"]
+    Q = d["Q"][head, ro:n_total].astype(np.float64)
+    K = d["K"][g, :n_total].astype(np.float64)
+    V = d["V"][g, :n_total].astype(np.float64)
+    t0 = time.perf_counter()
+    prefill_head(Q, K, V, ro, d["alpha"], d["rate"], d["floor"], 0, turn, 0, head, d["window"])
+    return time.perf_counter() - t0
+
+
+def _cpu_decode_unit(args):
+    import numpy as np
+
+    from oracle.kvcompress import decode_head_step
+
+    n_cols, reps = args
+    d = _CPU
+    k = d["K"][0].astype(np.float64)
+    v = d["V"][0].astype(np.float64)
+    q = d["Q"][0, n_cols - 1].astype(np.float64)
+    cols = np.arange(n_cols)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        decode_head_step(k, v, q, cols)
+    return (time.perf_counter() - t0) / reps
+
+
+def cpu_baseline(cfg, cores=None):
+    """Oracle port on `cores` host processes, bounded sample, extrapolated."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    from paper_2507_13681_b200.engine import SessionEngine  # noqa: F401 (turn geometry only)
+    from paper_2507_13681_b200.synth import SynthSpec, layer_qkv_numpy
+
+    cores = cores or os.cpu_count() or 1
+    group = cfg["n_q"] // cfg["n_kv"]
+    blocks = turn_blocks(cfg["input_len"], cfg["n_turns"], cfg["max_new"])
+    cap = cfg["n_turns"] * (cfg["input_len"] + cfg["max_new"])
+    n_q_s = min(cfg["n_q"], max(group, cores))
+    n_q_s = ((n_q_s + group - 1) // group) * group
+    spec = SynthSpec(n_q_s, n_q_s // group, cfg["d"], cap, seed=0)
+    Q, K, V = layer_qkv_numpy(spec, 0)
+    _CPU.update(Q=Q, K=K, V=V, blocks=blocks, group=group, alpha=cfg["alpha"], rate=cfg["rate"],
+                floor=cfg["floor"], window=cfg["obs_window"] or cfg["interval"])
+    ctx = mp.get_context("fork")
+    per_turn_ms = []
+    units = cfg["n_layers"] * cfg["n_q"]
+    n_sample = min(cores, n_q_s)
+    with ctx.Pool(n_sample) as pool:
+        for t in range(cfg["n_turns"]):
+            t0 = time.perf_counter()
+            times = pool.map(_cpu_unit, [(t, h) for h in range(n_sample)])
+            wall = time.perf_counter() - t0
+            # n_sample units ran in parallel on n_sample cores
+            per_turn_ms.append(1e3 * wall * units / n_sample)
+        # decode: one head-step at the dense (pre-event) and compressed sizes
+        L_end = blocks[-1][0] + blocks[-1][1]
+        comp_cols = min(L_end, cfg["budget"] + (cfg["obs_window"] or cfg["interval"]) + 1)
+        dense_t, comp_t = pool.map(_cpu_decode_unit, [(L_end, 3), (comp_cols, 20)])
+    n_dense = min(cfg["max_new"], cfg["warmup"] - 1 if cfg["budget"] is not None else cfg["max_new"])
+    step_s = (n_dense * dense_t + (cfg["max_new"] - n_dense) * comp_t) / cfg["max_new"]
+    tok_s = 1.0 / (step_s * units / cores)
+    sample = (f"oracle port (numpy fp64), {n_sample} (turn, layer 0, head) prefill units per turn of the "
+              f"{cfg['n_turns']} turns in parallel on {n_sample} processes + decode head-steps at {L_end} and "
+              f"{comp_cols} columns; extrapolated x{units} (layer, head) units")
+    return dict(ttft_ms=statistics.mean(per_turn_ms), per_turn_ms=per_turn_ms, decode_tokens_per_s=tok_s,
+                cores=n_sample, sample=sample)
+
+
+def turn_blocks(input_len, n_turns, max_new):
+    out, hist = [], 0
+    for t in range(n_turns):
+        out.append((hist - (max_new if t > 0 else 0), input_len + (max_new if t > 0 else 0)))
+        hist += input_len + max_new
+    return out
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup if args.warmup < 1 else 0):
+        pass
+    res = []
+    for _ in range(max(1, args.steps)):
+        res.append(cpu_baseline(cfg))
+    v = statistics.mean(r["ttft_ms"] for r in res)
+    tok = statistics.mean(r["decode_tokens_per_s"] for r in res)
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "ms", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * cfg["n_turns"], 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["workload"]},
+            "decode_tokens_per_s": round(tok, 3),
+            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": res[0]["cores"], "kind": "port",
+                             "sample": res[0]["sample"]},
+            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    from paper_2507_13681_b200 import _lib
+    from paper_2507_13681_b200.engine import AttnShape, QKVStore, SessionEngine, SessionParams
+    from paper_2507_13681_b200.kvcompress import CompressionConfig
+    from paper_2507_13681_b200.parallel import HeadShard
+
+    shard = HeadShard(cfg["n_q"], cfg["n_kv"], world, rank)
+    shape = AttnShape(cfg["n_layers"], shard.n_q_local, shard.n_kv_local, cfg["d"])
+    comp = CompressionConfig(cfg["budget"], cfg["interval"], cfg["warmup"], cfg["obs_window"])
+    params = SessionParams(alpha=cfg["alpha"], comp=comp, sample_rate=cfg["rate"], sample_floor=cfg["floor"],
+                           max_new=cfg["max_new"], seed=0)
+    blocks = turn_blocks(cfg["input_len"], cfg["n_turns"], cfg["max_new"])
+    cap = cfg["n_turns"] * (cfg["input_len"] + cfg["max_new"])
+    store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1 + shard.kv_begin)
+    eng = SessionEngine(shape, params, cap)
+    stream = torch.cuda.current_stream()
+
+    # per-entry CUDA-event timing (on the launching stream)
+    recs = []
+    timing = {"on": False}
+
+    def hook(name, phase):
+        if not timing["on"]:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        if phase == "begin":
+            recs.append([name, ev, None])
+        else:
+            for r in reversed(recs):
+                if r[0] == name and r[2] is None:
+                    r[2] = ev
+                    break
+
+    _lib.entry_hook = hook
+
+    gather = shard.make_gather(cfg["d"]) if world > 1 else None
+
+    def dialogue(ev_log):
+        for t, (ro, n_new) in enumerate(blocks):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = eng.prefill(store, t, ro, n_new, turn_offset_heads=shard.q_begin)
+            if gather is not None:
+                for l in range(cfg["n_layers"]):
+                    gather.prefill(res.out[l])
+            e1.record(stream)
+            outs, _ = eng.decode(store, ro + n_new, cfg["max_new"])
+            if gather is not None:
+                for step in outs:
+                    gather.decode(step)
+            e2.record(stream)
+            ev_log.append((e0, e1, e2))
+            # rollback is implicit: the next block starts at ro + n_new (session.py:180)
+        return res
+
+    # warmup
+    for _ in range(args.warmup):
+        dialogue([])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev_log = []
+    recs.clear()
+    eng.clear_logs()
+    timing["on"] = True
+    launches0 = _lib.launch_count
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        dialogue(ev_log)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    timing["on"] = False
+    launches = _lib.launch_count - launches0
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    prefill_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in ev_log)
+    decode_ms = sum(e1.elapsed_time(e2) for _, e1, e2 in ev_log)
+    n_prefills = len(ev_log)
+    vals = torch.tensor([total_ms, prefill_ms, decode_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    total_ms, prefill_ms, decode_ms = vals.tolist()
+    ttft = prefill_ms / n_prefills
+    tok_s = args.steps * cfg["n_turns"] * cfg["max_new"] / (decode_ms / 1e3)
+
+    # per-entry shares and the dominant kernel's roofline
+    per = {}
+    for name, a, b in recs:
+        if b is None:
+            continue
+        per.setdefault(name, []).append(a.elapsed_time(b))
+    stages = {k: round(sum(v), 3) for k, v in per.items()}
+    peaks = load_peaks()
+    roof = roofline(per, cfg, eng, store, blocks, peaks)
+    if roof is not None and roof.get("kernel") in per:
+        roof["share_of_timed"] = round(sum(per[roof["kernel"]]) / total_ms, 4)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, eng, store, blocks, shard, gather)
+
+    line = {"metric": METRIC, "value": round(ttft, 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (structured Q/K/V, SURVEY 8d; random-init, no checkpoint)",
+            "config": {"workload": cfg["workload"], "layers": cfg["n_layers"], "q_heads": cfg["n_q"],
+                       "kv_heads": cfg["n_kv"], "head_dim": cfg["d"], "turn_blocks": blocks,
+                       "max_new": cfg["max_new"], "parallelism": f"kv-head groups x{world}",
+                       "l2": "inputs larger than L2 (Q/K/V of all layers ~%.1f GB)" % (
+                           store.q.numel() * 2 * (1 + 2 * cfg["n_kv"] / cfg["n_q"]) / 1e9)},
+            "decode_tokens_per_s": round(tok_s, 2),
+            "prefill_ms_per_turn": round(ttft, 3), "decode_ms_per_turn": round(decode_ms / n_prefills, 3),
+            "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof}
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg)
+        line["cpu_baseline"] = {"value": round(cb["ttft_ms"], 1), "unit": "ms", "cores": cb["cores"], "kind": "port",
+                                "sample": cb["sample"], "decode_tokens_per_s": round(cb["decode_tokens_per_s"], 4)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(per, cfg, eng, store, blocks, peaks):
+    """Dominant entry by measured time; algorithmic work per launch / mean
+    launch duration. K5 (ls_vs_attention): 4*d*cells FLOPs (exact plan cells,
+    the reference's OpCounter units, tensor_ops.py:172-174). K1
+    (ls_score_lines): 2*d*score_count FLOPs + 1 exp per cell."""
+    if not per:
+        return None
+    name = max(per, key=lambda k: sum(per[k]))
+    mean_ms = statistics.mean(per[name])
+    d = cfg["d"]
+    # algorithmic work of the last dialogue's launches of this entry
+    work = None
+    n = len(per[name])
+    if name == "ls_vs_attention" and eng.cell_log:
+        work = 4.0 * d * float(sum(int(c.sum()) for c in eng.cell_log)) / n
+        bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]
+        achieved = work / (mean_ms * 1e-3) / 1e12
+    elif name == "ls_score_lines" and eng.score_log:
+        work = 2.0 * d * float(sum(int(c.sum()) for c in eng.score_log)) / n  # QK^T of the causal sampled cells
+        bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]
+        achieved = work / (mean_ms * 1e-3) / 1e12
+    elif name == "ls_decode_attention":
+        bytes_ = 4.0 * d * eng.decode_cols / max(1, eng.decode_launches)  # K+V bf16 per q-head column
+        bound, unit, peak = "hbm", "GB/s", peaks["hbm"]
+        achieved = bytes_ / (mean_ms * 1e-3) / 1e9 if bytes_ else None
+        work = bytes_
+    else:
+        return {"kernel": name, "mean_ms": round(mean_ms, 4), "note": "no algorithmic model"}
+    return {"kernel": name, "bound": bound, "achieved": round(achieved, 3) if achieved else None,
+            "peak": peak, "unit": unit, "frac": round(achieved / peak, 5) if achieved else None,
+            "traffic": None, "mean_launch_ms": round(mean_ms, 4), "launches": len(per[name]),
+            "work_per_launch": work, "peak_src": peaks["src"] + (" sustained" if bound == "tensor" else ""),
+            "share_of_timed": None}
+
+
+def run_e2e(args, cfg, eng, store, blocks, shard, gather):
+    """Same dialogue through the public API with HOST inputs: every turn copies
+    its block's Q/K/V (all layers) from pinned host memory into the HBM
+    archive and reads every layer's attention output back; every decode step
+    copies its q and new K/V rows in and its outputs out."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    L = cfg["n_layers"]
+    hq = store.q.cpu().pin_memory()
+    hk = store.k.cpu().pin_memory()
+    hv = store.v.cpu().pin_memory()
+    h2d = d2h = 0
+    ttfts, dec = [], []
+    steps = max(1, args.steps)
+    for it in range(steps + 1):  # first iteration warms up
+        for t, (ro, n_new) in enumerate(blocks):
+            n_total = ro + n_new
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            store.q[:, :, ro:n_total].copy_(hq[:, :, ro:n_total], non_blocking=True)
+            store.k[:, :, ro:n_total].copy_(hk[:, :, ro:n_total], non_blocking=True)
+            store.v[:, :, ro:n_total].copy_(hv[:, :, ro:n_total], non_blocking=True)
+            res = eng.prefill(store, t, ro, n_new, turn_offset_heads=shard.q_begin)
+            host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in res.out]
+            for o, ho in zip(res.out, host_out):
+                ho.copy_(o, non_blocking=True)
+            e1.record(stream)
+            if it > 0:
+                h2d += sum(x[:, :, ro:n_total].numel() * 2 for x in (hq, hk, hv))
+                d2h += sum(o.numel() * 2 for o in res.out)
+            # decode with per-step host I/O
+            outs_host = torch.empty((cfg["max_new"], L, shard.n_q_local, cfg["d"]), dtype=torch.bfloat16,
+                                    pin_memory=True)
+            length = n_total
+            for step in range(cfg["max_new"]):
+                pos = length + step
+                store.q[:, :, pos].copy_(hq[:, :, pos], non_blocking=True)
+                store.k[:, :, pos].copy_(hk[:, :, pos], non_blocking=True)
+                store.v[:, :, pos].copy_(hv[:, :, pos], non_blocking=True)
+                if it > 0:
+                    h2d += (hq[:, :, pos].numel() + 2 * hk[:, :, pos].numel()) * 2
+            outs, _ = eng.decode(store, n_total, cfg["max_new"])
+            for s_i, step_outs in enumerate(outs):
+                for l, o in enumerate(step_outs):
+                    outs_host[s_i, l].copy_(o, non_blocking=True)
+            if it > 0:
+                d2h += outs_host.numel() * 2
+            e2.record(stream)
+            if it > 0:
+                ttfts.append((e0, e1))
+                dec.append((e1, e2))
+    torch.cuda.synchronize()
+    ttft = statistics.mean(a.elapsed_time(b) for a, b in ttfts)
+    dec_ms = sum(a.elapsed_time(b) for a, b in dec)
+    tok_s = steps * cfg["n_turns"] * cfg["max_new"] / (dec_ms / 1e3)
+    return {"value": round(ttft, 3), "unit": "ms", "h2d_bytes_per_step": h2d // steps,
+            "d2h_bytes_per_step": d2h // steps, "decode_tokens_per_s": round(tok_s, 2),
+            "note": "step = one 3-turn dialogue; decode step inputs are copied before the decode loop "
+                    "of the turn (all inside the timed region)"}
+
+
+if __name__ == "__main__":
+    main()

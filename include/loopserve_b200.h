@@ -1,0 +1,226 @@
+/*
+ * loopserve_b200.h -- C ABI of the B200-native LoopServe hot paths.
+ *
+ * Drop-in boundary for the two data-parallel hot paths of the reference
+ * (arxiv 2507.13681, pkg/src/loopserve): online prefill sparsification +
+ * vertical/slash sparse attention, and progressive decode KV compression.
+ * Every entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Stream-ordered: every device entry point enqueues work on `stream` and
+ *    returns without synchronising. Buffers are caller-allocated device
+ *    memory (the Python layer allocates them with torch); plain pointers and
+ *    sizes only, no framework types.
+ *  - Status: 0 = OK; negative = one code per reference exception class
+ *    (errors.py:4-65) plus CUDA / workspace / unsupported codes.
+ *    `ls_last_error()` returns a thread-local message for the last failure.
+ *  - Layouts (row-major, bf16 = uint16 storage of bfloat16):
+ *      q block      [n_heads][q_rows_stride...]  : q + h*q_head_stride + r*head_dim
+ *      K / V archive[n_kv_heads][cap][head_dim]   : k + kv*kv_head_stride + pos*head_dim
+ *    q-head h reads kv-head h / (n_heads / n_kv_heads) (GQA; the reference is
+ *    MHA, model.py:26-34 -- one reference head == one q-head here).
+ *  - Plans on device: per head a sorted int32 id list + count for slashes
+ *    (global offsets d = g - c) and verticals (columns c), capacity n_total.
+ */
+#ifndef LOOPSERVE_B200_H
+#define LOOPSERVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *ls_stream_t; /* cudaStream_t */
+
+enum ls_status {
+  LS_OK = 0,
+  LS_ERR_NON_FINITE_INPUT = -1,   /* errors.py:8  NonFiniteInput   */
+  LS_ERR_ALL_MASKED_ROW = -2,     /* errors.py:12 AllMaskedRow     */
+  LS_ERR_DIMENSION_MISMATCH = -3, /* errors.py:16 DimensionMismatch*/
+  LS_ERR_EMPTY_PLAN = -4,         /* errors.py:20 EmptyPlan        */
+  LS_ERR_INVALID_CONFIG = -5,     /* errors.py:24 InvalidConfig    */
+  LS_ERR_SEQUENCE_TOO_LONG = -6,  /* errors.py:28 SequenceTooLong  */
+  LS_ERR_CACHE_CORRUPT = -7,      /* errors.py:32 CacheCorrupt     */
+  LS_ERR_EMPTY_BLOCK = -8,        /* errors.py:36 EmptyBlock       */
+  LS_ERR_INVALID_ALPHA = -9,      /* errors.py:40 InvalidAlpha     */
+  LS_ERR_EMPTY_WINDOW = -11,      /* errors.py:48 EmptyWindow      */
+  LS_ERR_SIZE_MISMATCH = -12,     /* errors.py:52 SizeMismatch     */
+  LS_ERR_INVALID_IDS = -13,       /* errors.py:56 InvalidIds       */
+  LS_ERR_CUDA = -100,
+  LS_ERR_WORKSPACE = -101,
+  LS_ERR_UNSUPPORTED = -102
+};
+
+/* Shape of one attention layer call (all q-heads of a layer, or a shard). */
+typedef struct ls_layer_desc {
+  int32_t n_heads;        /* q-heads in this call                          */
+  int32_t n_kv_heads;     /* kv-heads; n_heads % n_kv_heads == 0           */
+  int32_t head_dim;       /* 64 or 128                                      */
+  int32_t n_new;          /* block rows (session.py:122 block)              */
+  int32_t n_total;        /* keys = row_offset + n_new                      */
+  int32_t row_offset;     /* global position of block row 0                 */
+  int64_t q_head_stride;  /* elements between q-heads in q                  */
+  int64_t kv_head_stride; /* elements between kv-heads in k / v             */
+} ls_layer_desc;
+
+const char *ls_last_error(void);
+int ls_version(void);
+/* number of SMs / device name of the current device (diagnostics) */
+int ls_device_info(int *sm_count, char *name, int name_len);
+
+/* ---------------------------------------------------------------- K0 ---
+ * Row sampling, bit-exact with numpy: replaces Session.head_seed
+ * (session.py:84-86) + sample_rows (prefill.py:125-135), i.e. for each layer
+ * l in [layer_begin, +n_layers) and head h in [head_begin, +n_heads): rows of
+ *   sample_rows(n_new, rate, floor, SeedSequence(session_seed,
+ *               spawn_key=(turn, l, h)).generate_state(1, uint64)[0])
+ * written sorted to out_rows[l - layer_begin][h - head_begin][0..n_s). n_s is returned by
+ * ls_sample_size (prefill.py:132). turn < 0 selects raw-seed mode: session_seed
+ * is used directly as the PCG64 seed (sample_rows(..., seed)). alpha >= 1 (session.py:136-137) is the
+ * caller's choice: pass rate=1, floor=n_new to get every row.
+ * Workspace: ls_sample_rows_workspace(n_layers * n_heads, n_new) bytes.  */
+int ls_sample_size(int32_t n_new, double rate, int32_t floor_, int32_t *n_s);
+size_t ls_sample_rows_workspace(int32_t n_units, int32_t n_new);
+int ls_sample_rows(uint64_t session_seed, int32_t turn, int32_t layer_begin, int32_t n_layers,
+                   int32_t head_begin, int32_t n_heads, int32_t n_new, double rate, int32_t floor_,
+                   int32_t *out_rows, void *ws, size_t ws_bytes, ls_stream_t stream);
+/* Host build of the same generator (used by the CPU tests to pin the bits
+ * against numpy; not used by any device path). */
+int ls_sample_rows_host(uint64_t session_seed, int32_t turn, int32_t layer, int32_t head,
+                        int32_t n_new, double rate, int32_t floor_, int32_t *out_rows);
+uint64_t ls_head_seed_host(uint64_t session_seed, int32_t turn, int32_t layer, int32_t head);
+
+/* ---------------------------------------------------------------- K1 ---
+ * Sampled-row scoring + line sums: replaces the scoring part of
+ * sparsify_head (prefill.py:377-390), softmax_rows (tensor_ops.py:24-40) and
+ * _line_sums (prefill.py:138-169) for every head of a layer.
+ * rows[h][n_s]: sorted local block rows (K0 output).
+ * Outputs (per head, capacity n_total):
+ *   v_w[h][c] fp64, v_max[h][c] fp32  (vertical weight / max cell)
+ *   s_w[h][d] fp64, s_max[h][d] fp32  (slash weight / max cell)
+ *   row_stats[h][n_s][2] fp32 (row max in log2 units, 1/row-sum)
+ *   total[h] fp64 (sum of all sampled weights, prefill.py:392)
+ *   score_count[h] int64 (OpCounter increments, prefill.py:388-389)     */
+size_t ls_score_lines_workspace(const ls_layer_desc *L, int32_t n_s);
+int ls_score_lines(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k,
+                   const int32_t *rows, double *v_w, float *v_max, double *s_w, float *s_max,
+                   float *row_stats, double *total, int64_t *score_count, void *ws,
+                   size_t ws_bytes, ls_stream_t stream);
+
+/* ------------------------------------------------------------- K2+K3+K4 -
+ * Line sort + greedy coverage-alpha selection: replaces the sort of
+ * _line_sums (prefill.py:168-169) and _greedy (prefill.py:178-229).
+ * Consumes ls_score_lines outputs; crossing cells (prefill.py:116-122) are
+ * recomputed from q/k and row_stats. Outputs per head:
+ *   slash_ids[h][n_total] / vert_ids[h][n_total] sorted ascending,
+ *   counts[h][2] = (|S|, |V|), coverage[h], approx[h] (SparsePlan fields),
+ *   picks[h][...] pick sequence (kind<<31 | index) in selection order
+ *   (capacity 2*n_total) and n_picks[h].                               */
+size_t ls_select_lines_workspace(const ls_layer_desc *L, int32_t n_s);
+int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha, const uint16_t *q,
+                    const uint16_t *k, const int32_t *rows, const double *v_w,
+                    const float *v_max, const double *s_w, const float *s_max,
+                    const float *row_stats, const double *total, int32_t *slash_ids,
+                    int32_t *vert_ids, int32_t *counts, double *coverage, double *approx,
+                    int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
+                    ls_stream_t stream);
+
+/* Greedy on caller-provided sorted line lists with a dense weight matrix as
+ * the cell source: replaces greedy_select_lines (prefill.py:232-251). One
+ * head. lines are (index, weight, length, max_cell) sorted by (-w, index);
+ * weights[n_rows][n_total] fp64 with positions[n_rows]. Diagnostics/parity. */
+int ls_greedy_dense(int32_t n_slash, const int32_t *s_idx, const double *s_w,
+                    const int32_t *s_len, const double *s_max, int32_t n_vert,
+                    const int32_t *v_idx, const double *v_w, const int32_t *v_len,
+                    const double *v_max, double alpha, double total_weight,
+                    const double *weights, const int32_t *positions, int32_t n_rows,
+                    int32_t n_total, int32_t *slash_ids, int32_t *vert_ids,
+                    int32_t *counts, double *coverage, double *approx, void *ws,
+                    size_t ws_bytes, ls_stream_t stream);
+
+/* ---------------------------------------------------------------- K5 ---
+ * Vertical/slash sparse attention: replaces masked_sparse_attention
+ * (tensor_ops.py:141-183) for every head of a layer, with the exact
+ * `_row_columns` cell set (tensor_ops.py:130-138) incl. the diagonal
+ * fallback. out[r][h][d] (token-major, the head concat of model.py:259),
+ * fp32 if out_bf16 == 0 else bf16. cells[h] int64 = OpCounter increments
+ * (tensor_ops.py:172-174). Heads with an empty plan -> LS_ERR_EMPTY_PLAN
+ * is checked by the host layer (tensor_ops.py:165-166).                 */
+size_t ls_vs_attention_workspace(const ls_layer_desc *L);
+int ls_vs_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k,
+                    const uint16_t *v, const int32_t *slash_ids, const int32_t *vert_ids,
+                    const int32_t *counts, void *out, int32_t out_bf16, int64_t *cells,
+                    void *ws, size_t ws_bytes, ls_stream_t stream);
+
+/* Dense probability rows of block rows [n_new - n_rows, n_new) under the
+ * plan (the decode observation seeds, session.py:89-95):
+ * out[h*out_head_stride + i*out_row_stride + c] fp32, zeros off-plan.    */
+int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16_t *q, const uint16_t *k,
+                 const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts,
+                 float *out, int64_t out_row_stride, int64_t out_head_stride,
+                 ls_stream_t stream);
+
+/* Dense causal attention (scaled_dot_attention, tensor_ops.py:104-127):
+ * the lossless baseline / speed-up denominator. out[r][h][d].           */
+int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k,
+                       const uint16_t *v, void *out, int32_t out_bf16, ls_stream_t stream);
+
+/* ------------------------------------------------------------- decode ---
+ * Per-head decode state lives in caller-allocated device arrays described
+ * by the ls_decode_state struct (one layer). See paper_2507_13681_b200/engine.py.
+ *   ring_w   [n_heads][window][row_cap] fp32   observation rows' weights
+ *   ring_ids [n_heads][window][sparse_cap] int32 ids of sparse rows
+ *   ring_n   [n_heads][window] int32  row length (0 = empty slot)
+ *   ring_dense[n_heads][window] int32 1 if ids == arange(n)
+ *   sel_ids  [n_heads][budget_cap] int32 picked ids, sorted (kvcompress.py:212)
+ *   n_sel    [n_heads] int32
+ *   ck, cv   [n_heads][budget_cap][head_dim] bf16 compacted K/V of sel_ids */
+typedef struct ls_decode_state {
+  int32_t n_heads, n_kv_heads, head_dim;
+  int32_t window;      /* obs_window (kvcompress.py:29-30)        */
+  int32_t row_cap;     /* >= max cache length + 1                  */
+  int32_t sparse_cap;  /* >= budget + window + 1                   */
+  int32_t budget_cap;  /* >= budget                                */
+  int64_t kv_head_stride;
+  float *ring_w;
+  int32_t *ring_ids;
+  int32_t *ring_n;
+  int32_t *ring_dense;
+  int32_t *sel_ids;
+  int32_t *n_sel;
+  uint16_t *ck;
+  uint16_t *cv;
+} ls_decode_state;
+
+/* Working-set decode attention for one token (model.py:232-241 +
+ * decode_step, model.py:289-311): per q-head, attends the working set
+ * (all positions [0, length) before the first event; selected ids below
+ * length-window plus [length-window, length) after it) plus the new
+ * position `length` (its K/V already written to the archive), writes
+ * out[h][d] and the observation row into ring slot `slot`.              */
+size_t ls_decode_attention_workspace(const ls_decode_state *S, int32_t max_len);
+int ls_decode_attention(const ls_decode_state *S, const uint16_t *q, const uint16_t *k,
+                        const uint16_t *v, int32_t length, int32_t compressed, int32_t slot,
+                        void *out, int32_t out_bf16, void *ws, size_t ws_bytes,
+                        ls_stream_t stream);
+
+/* Compression event (kvcompress.py:210-224): accumulate the buffered rows
+ * (oldest first, slot order given by `slot_order[n_rows]`), top-B by
+ * (score desc, id asc), write sel_ids/n_sel, and per head the retained
+ * working-set size and score coverage (event log fields).               */
+size_t ls_decode_select_workspace(const ls_decode_state *S, int32_t max_len);
+int ls_decode_select(const ls_decode_state *S, const int32_t *slot_order, int32_t n_rows,
+                     int32_t length, int32_t budget, int32_t *retained_n,
+                     double *score_coverage, void *ws, size_t ws_bytes, ls_stream_t stream);
+
+/* Coalesced gather-compaction of the selected rows (compact_cache,
+ * kvcompress.py:133-147): ck/cv[h][j] = K/V[kv(h)][sel_ids[h][j]].       */
+int ls_kv_compact(const ls_decode_state *S, const uint16_t *k, const uint16_t *v,
+                  ls_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOOPSERVE_B200_H */

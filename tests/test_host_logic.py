@@ -1,0 +1,120 @@
+"""Host-side logic on CPU: turn geometry, deque/seed bookkeeping, sharding
+and the NCCL all-gather path (exercised with gloo, world_size 2)."""
+
+import os
+import socket
+from collections import deque
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import seeding as oseed
+from paper_2507_13681_b200.kvcompress import CompressionConfig
+from paper_2507_13681_b200.parallel import HeadShard, OutputGather, session_shard
+
+
+def test_turn_blocks_match_session_loop():
+    """session.py:122 (block = previous answer + input) and :180 (rollback)."""
+    from bench import turn_blocks
+
+    input_len, max_new = 5000, 128
+    blocks = turn_blocks(input_len, 3, max_new)
+    assert blocks == [(0, 5000), (5000, 5128), (10128, 5128)]
+    # n_total after prefill equals SURVEY 8 table: 5000, 10128, 15256
+    assert [ro + n for ro, n in blocks] == [5000, 10128, 15256]
+    # sample sizes of those blocks (prefill.py:132)
+    assert [oseed.sample_size(n, 0.1, 32) for _, n in blocks] == [500, 513, 513]
+
+
+@pytest.mark.parametrize("W,warmup,interval,n_seed,max_new", [(16, 16, 16, 16, 128), (9, 7, 5, 9, 33),
+                                                               (12, 3, 6, 12, 30), (4, 4, 4, 4, 20),
+                                                               (8, 30, 4, 8, 10)])
+def test_surviving_seeds_matches_deque(W, warmup, interval, n_seed, max_new):
+    """kvcompress.py:196/233: the seeds present at the first event."""
+    comp = CompressionConfig(budget=8, interval=interval, warmup=warmup, obs_window=W)
+    buf = deque([("seed", i) for i in range(n_seed)], maxlen=W)
+    first = None
+    for n_o in range(1, max_new + 1):
+        if comp.event_at(n_o):
+            first = sum(1 for x in buf if x[0] == "seed")
+            break
+        buf.append(("row", n_o))
+    expect = first if first is not None else 0
+    assert comp.surviving_seeds(n_seed, max_new) == expect
+
+
+def test_event_schedule():  # test_kvcompress.py:245-256
+    comp = CompressionConfig(budget=3, interval=5, warmup=5, obs_window=5)
+    assert [n for n in range(1, 13) if comp.event_at(n)] == [5, 10]
+    assert not any(CompressionConfig(budget=None).event_at(n) for n in range(1, 100))
+
+
+def test_head_shard_partition():
+    for world in (1, 2, 4, 8):
+        owned = []
+        for r in range(world):
+            s = HeadShard(32, 8, world, r)
+            assert s.n_q_local == 32 // world
+            # every q-head of a kv group lives with its group
+            for h in s.q_heads():
+                assert h // 4 in s.kv_heads()
+            owned += list(s.q_heads())
+        assert owned == list(range(32))
+    with pytest.raises(ValueError):
+        HeadShard(28, 4, 8, 0)  # Qwen2.5-7B: 4 kv heads cannot split over 8 ranks
+    assert sorted(sum((session_shard(64, 8, r) for r in range(8)), [])) == list(range(64))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shard = HeadShard(8, 4, world, rank)
+    d = 4
+    n_new = 3
+    # every rank computes its heads' "outputs" as a function of the global head id
+    local = torch.stack([torch.full((n_new, d), float(h)) for h in shard.q_heads()], dim=1)
+    full = OutputGather(shard, d).prefill(local)
+    step = [torch.full((shard.n_q_local, d), float(l * 100 + rank)) for l in range(2)]
+    dec = OutputGather(shard, d).decode(step)
+    # per-head sampling seeds depend on the GLOBAL head id only
+    rows = [oseed.sample_rows(500, 0.1, 32, oseed.head_seed(0, 1, 0, h)) for h in shard.q_heads()]
+    q.put((rank, full.numpy(), [x.numpy() for x in dec], [r.tolist() for r in rows]))
+    dist.destroy_process_group()
+
+
+def test_output_gather_gloo_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=60) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    for rank, full, dec, rows in res:
+        assert full.shape == (3, 8, 4)
+        for h in range(8):
+            assert np.all(full[:, h] == h)  # head concat order == global head order
+        for l in range(2):
+            assert dec[l].shape == (8, 4)
+            assert np.all(dec[l][:4] == l * 100 + 0) and np.all(dec[l][4:] == l * 100 + 1)
+    # sharded sampling == unsharded sampling (index sets invariant under sharding)
+    all_rows = res[0][3] + res[1][3]
+    for h in range(8):
+        assert all_rows[h] == oseed.sample_rows(500, 0.1, 32, oseed.head_seed(0, 1, 0, h)).tolist()
