@@ -109,8 +109,9 @@ def test_sparsify_plans_match_reference(cuda_lib, golden, name):
         outcome = check_plan(oplan, dev_plans[h], seqs[h], sl_w, vt_w)
         outcomes.append(outcome)
         if outcome == "identical":
-            assert dev_plans[h].achieved_coverage == pytest.approx(hc["coverage"], abs=1e-5)
-            assert dev_plans[h].approx_sum == pytest.approx(hc["approx"], abs=1e-4)
+            # fp32 P vs fp64: sums over up to 2*n_total picks, so relative
+            assert dev_plans[h].achieved_coverage == pytest.approx(hc["coverage"], rel=1e-5, abs=1e-5)
+            assert dev_plans[h].approx_sum == pytest.approx(hc["approx"], rel=1e-5, abs=1e-4)
         assert dev_plans[h].total_weight == pytest.approx(hc["total"], abs=1e-4)
         assert int(score_count[h]) == hc["score_count"]
     assert outcomes.count("identical") >= len(outcomes) - 1, outcomes
