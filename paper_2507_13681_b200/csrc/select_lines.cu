@@ -100,145 +100,20 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_lines_kernel(const double *
   }
 }
 
-// ---------------------------------------------------------------- K3a chain
-struct Stage {
-  int32_t idx[CHUNK];
-  int32_t len[CHUNK];
-  double w[CHUNK];
-  double mx[CHUNK];
-};
-
-__global__ void __launch_bounds__(128) chain_kernel(Lists L, int n_total, double alpha, const double *total,
-                                                    Picks P, int cap) {
-  __shared__ Stage st[2];  // 0 slash, 1 vertical
-  __shared__ int s_base[2], s_stop;
-  __shared__ int s_idx_sh, v_idx_sh, n_pick_sh;
-  __shared__ double ol_s_sh, ol_v_sh, approx_sh;
-  const int h = blockIdx.x;
-  const double T = total[h];
-  const double target = alpha * T;
-  const int64_t lb = static_cast<int64_t>(h) * 2 * n_total;
-  const int64_t pb = static_cast<int64_t>(h) * cap;
-  if (threadIdx.x == 0) {
-    s_idx_sh = v_idx_sh = n_pick_sh = 0;
-    ol_s_sh = ol_v_sh = approx_sh = 0.0;
-    s_base[0] = s_base[1] = -1;
-    s_stop = 0;
-  }
-  __syncthreads();
-  while (true) {
-    // (re)stage whichever list's cursor left its chunk
-    for (int kind = 0; kind < 2; ++kind) {
-      const int cur = kind == 0 ? s_idx_sh : v_idx_sh;
-      const int want = (cur / CHUNK) * CHUNK;
-      if (want != s_base[kind] && cur < n_total) {
-        for (int i = threadIdx.x; i < CHUNK; i += blockDim.x) {
-          int o = want + i;
-          if (o < n_total) {
-            int64_t g = lb + static_cast<int64_t>(kind) * n_total + o;
-            st[kind].idx[i] = L.idx[g];
-            st[kind].len[i] = L.len[g];
-            st[kind].w[i] = L.w[g];
-            st[kind].mx[i] = L.mx[g];
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int kind = 0; kind < 2; ++kind) {
-        const int cur = kind == 0 ? s_idx_sh : v_idx_sh;
-        s_base[kind] = (cur / CHUNK) * CHUNK;
-      }
-      int s_idx = s_idx_sh, v_idx = v_idx_sh, n = n_pick_sh;
-      double ol_s = ol_s_sh, ol_v = ol_v_sh, approx = approx_sh;
-      const int s_end = s_base[0] + CHUNK, v_end = s_base[1] + CHUNK;
-      int stop = 0;
-      while (true) {
-        if (!(approx < target - EPS)) {  // exact is checked by finalize
-          stop = 1;
-          break;
-        }
-        const bool has_s = s_idx < n_total, has_v = v_idx < n_total;
-        if (!has_s && !has_v) {
-          stop = 1;
-          break;
-        }
-        if (n >= cap) {
-          stop = 1;
-          break;
-        }
-        if ((has_s && s_idx >= s_end) || (has_v && v_idx >= v_end)) break;  // restage
-        bool take_slash;
-        double ws = 0, wv = 0;
-        int ls_ = 0, lv = 0;
-        if (has_s) {
-          ws = st[0].w[s_idx - s_base[0]];
-          ls_ = st[0].len[s_idx - s_base[0]];
-        }
-        if (has_v) {
-          wv = st[1].w[v_idx - s_base[1]];
-          lv = st[1].len[v_idx - s_base[1]];
-        }
-        if (!has_s) {
-          take_slash = false;
-        } else if (!has_v) {
-          take_slash = true;
-        } else {
-          // prefill.py:206-208, |V| = v_idx, |S| = s_idx
-          const int den_s = max(1, ls_ - v_idx);
-          const int den_v = max(1, lv - s_idx);
-          const double gain_s = (ws - ol_v) / static_cast<double>(den_s);
-          const double gain_v = (wv - ol_s) / static_cast<double>(den_v);
-          take_slash = gain_s >= gain_v;
-        }
-        if (take_slash) {
-          approx += ws - ol_v;
-          ol_s += st[0].mx[s_idx - s_base[0]];
-          P.code[pb + n] = st[0].idx[s_idx - s_base[0]];
-          P.other[pb + n] = v_idx;
-          P.w[pb + n] = ws;
-          ++s_idx;
-        } else {
-          approx += wv - ol_s;
-          ol_v += st[1].mx[v_idx - s_base[1]];
-          P.code[pb + n] = st[1].idx[v_idx - s_base[1]] | static_cast<int32_t>(0x80000000u);
-          P.other[pb + n] = s_idx;
-          P.w[pb + n] = wv;
-          ++v_idx;
-        }
-        P.approx[pb + n] = approx;
-        ++n;
-      }
-      s_idx_sh = s_idx;
-      v_idx_sh = v_idx;
-      n_pick_sh = n;
-      ol_s_sh = ol_s;
-      ol_v_sh = ol_v;
-      approx_sh = approx;
-      s_stop = stop;
-    }
-    __syncthreads();
-    if (s_stop) break;
-  }
-  if (threadIdx.x == 0) P.n[h] = n_pick_sh;
-}
-
-// ------------------------------------------------------------ K3b crossings
+// ------------------------------------------------------- crossing cells
 // Cell source 1: recompute P[r, c] from q, k and K1 row statistics.
 struct RecomputeCells {
   const uint16_t *q, *k;
-  const int32_t *rows;
   const int32_t *row_of;  // [H][n_total] sampled row index of position g, or -1
   const float *row_stats;
   int n_s, n_total, row_offset, d, group;
   int64_t q_head_stride, kv_head_stride;
   float scale_log2;
 
-  __device__ __forceinline__ double cell(int h, int g, int c) const {
-    if (g >= n_total) return 0.0;
-    const int r = row_of[static_cast<int64_t>(h) * n_total + g];
-    if (r < 0) return 0.0;
+  __device__ __forceinline__ int row(int h, int g) const {
+    return g < n_total ? row_of[static_cast<int64_t>(h) * n_total + g] : -1;
+  }
+  __device__ __forceinline__ double value(int h, int r, int g, int c) const {
     const uint16_t *qr = q + static_cast<int64_t>(h) * q_head_stride + static_cast<int64_t>(g - row_offset) * d;
     const uint16_t *kr = k + static_cast<int64_t>(h / group) * kv_head_stride + static_cast<int64_t>(c) * d;
     float acc = 0.f;
@@ -261,85 +136,200 @@ struct DenseCells {
   const double *weights;  // [n_rows][n_total]
   const int32_t *row_of;  // [n_total]
   int n_total;
-  __device__ __forceinline__ double cell(int /*h*/, int g, int c) const {
-    if (g >= n_total) return 0.0;
-    const int r = row_of[g];
-    if (r < 0) return 0.0;
+  __device__ __forceinline__ int row(int /*h*/, int g) const { return g < n_total ? row_of[g] : -1; }
+  __device__ __forceinline__ double value(int /*h*/, int r, int /*g*/, int c) const {
     return weights[static_cast<int64_t>(r) * n_total + c];
   }
 };
 
-template <typename Cells>
-__global__ void __launch_bounds__(256) cross_kernel(Lists L, int n_total, Picks P, int cap, Cells cells) {
-  __shared__ double vals[8][32];
-  const int h = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = P.n[h];
-  const int64_t pb = static_cast<int64_t>(h) * cap;
-  const int64_t lb = static_cast<int64_t>(h) * 2 * n_total;
-  for (int t = blockIdx.x * 8 + warp; t < n; t += gridDim.x * 8) {
-    const int32_t code = P.code[pb + t];
-    const bool is_vert = code < 0;
-    const int idx = code & 0x7fffffff;
-    const int n_other = P.other[pb + t];
-    const int32_t *other = L.idx + lb + static_cast<int64_t>(is_vert ? 0 : 1) * n_total;  // picked-in-order prefix
-    double sum = 0.0;  // python sum() starts at 0, adds in selection order
-    for (int j0 = 0; j0 < n_other; j0 += 32) {
-      const int j = j0 + lane;
-      double v = 0.0;
-      if (j < n_other) {
-        const int o = other[j];
-        // slash pick d=idx crosses vertical c=o at g=c+d; vertical pick c=idx crosses slash d=o
-        v = is_vert ? cells.cell(h, idx + o, idx) : cells.cell(h, o + idx, o);
-      }
-      vals[warp][lane] = v;
-      __syncwarp();
-      if (lane == 0) {
-        const int m = min(32, n_other - j0);
-        for (int i = 0; i < m; ++i) sum += vals[warp][i];
-      }
-      __syncwarp();
-    }
-    if (lane == 0) P.cross[pb + t] = sum;
-  }
+// ------------------------------------------------------------ K3 greedy
+// One CTA per head. Rounds of: (A) thread 0 advances the decision chain by up
+// to PCH picks (prefill.py:195-220, approx-only decisions), (B) every warp
+// sums the crossing cells of some of the new picks with the other kind's
+// already-picked prefix, in selection order (prefill.py:211, 217), (C) thread
+// 0 replays exact += w - cross in order and applies the reference's dual
+// termination test (prefill.py:195). Stops at the first pick count where
+// approx or exact reaches alpha*T - eps, or when both lists are exhausted.
+struct Stage {
+  int32_t idx[CHUNK];
+  int32_t len[CHUNK];
+  double w[CHUNK];
+  double mx[CHUNK];
+};
+
+constexpr int PCH = 64;             // picks per round
+constexpr int G_THREADS = 512;      // 16 warps
+constexpr int G_WARPS = G_THREADS / 32;
+
+// gain_s >= gain_v with gain = num / den (prefill.py:206-208). Decided by
+// cross-multiplication unless the two sides are within 1e-13 relative, in
+// which case the reference's own fp64 divisions decide (bit-identical result).
+__device__ __forceinline__ bool take_slash_decision(double a, int ds, double b, int dv) {
+  const double x = a * static_cast<double>(dv);
+  const double y = b * static_cast<double>(ds);
+  const double diff = x - y;
+  const double mag = fmax(fabs(x), fabs(y));
+  if (fabs(diff) > 1e-13 * mag) return diff > 0.0;
+  return a / static_cast<double>(ds) >= b / static_cast<double>(dv);
 }
 
-// ------------------------------------------------------------ K3c finalize
-__global__ void finalize_kernel(Picks P, int cap, double alpha, const double *total, int32_t *n_final,
-                                double *coverage, double *approx_out) {
-  const int h = blockIdx.x, lane = threadIdx.x;
+template <typename Cells>
+__global__ void __launch_bounds__(G_THREADS) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
+                                                            Picks P, int cap, Cells cells, int32_t *n_final,
+                                                            double *coverage, double *approx_out) {
+  __shared__ Stage st[2];  // 0 slash, 1 vertical
+  __shared__ int c_code[PCH], c_other[PCH];
+  __shared__ double c_w[PCH], c_approx[PCH], c_cross[PCH];
+  __shared__ double vals[G_WARPS][32];
+  __shared__ int s_base[2], s_idx_sh, v_idx_sh, n_sh, n_chunk, done, exhausted;
+  __shared__ double ol_s_sh, ol_v_sh, approx_sh, exact_sh;
+  const int h = blockIdx.x;
   const double T = total[h];
   const double target = alpha * T;
-  const int n = P.n[h];
+  const int64_t lb = static_cast<int64_t>(h) * 2 * n_total;
   const int64_t pb = static_cast<int64_t>(h) * cap;
-  double exact = 0.0, approx = 0.0;
-  int t_stop = -1;
-  if (!(0.0 < target - EPS)) t_stop = 0;  // loop never entered (e.g. alpha = 0)
-  for (int t0 = 0; t0 < n && t_stop < 0; t0 += 32) {
-    const int t = t0 + lane;
-    double inc = 0.0, ap = 0.0;
-    if (t < n) {
-      inc = P.w[pb + t] - P.cross[pb + t];
-      ap = P.approx[pb + t];
-    }
-    const int m = min(32, n - t0);
-    for (int i = 0; i < m; ++i) {
-      const double in = __shfl_sync(0xffffffffu, inc, i);
-      const double a = __shfl_sync(0xffffffffu, ap, i);
-      exact += in;  // prefill.py:211 / 217
-      approx = a;
-      if (!(approx < target - EPS && exact < target - EPS)) {
-        t_stop = t0 + i + 1;
-        break;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    s_idx_sh = v_idx_sh = n_sh = 0;
+    ol_s_sh = ol_v_sh = approx_sh = exact_sh = 0.0;
+    s_base[0] = s_base[1] = -1;
+    done = !(0.0 < target - EPS);  // the while condition fails before any pick
+    exhausted = 0;
+  }
+  __syncthreads();
+  while (!done) {
+    // (re)stage whichever list's cursor left its chunk
+    for (int kind = 0; kind < 2; ++kind) {
+      const int cur = kind == 0 ? s_idx_sh : v_idx_sh;
+      const int want = (cur / CHUNK) * CHUNK;
+      if (want != s_base[kind] && cur < n_total) {
+        for (int i = threadIdx.x; i < CHUNK; i += blockDim.x) {
+          const int o = want + i;
+          if (o < n_total) {
+            const int64_t g = lb + static_cast<int64_t>(kind) * n_total + o;
+            st[kind].idx[i] = L.idx[g];
+            st[kind].len[i] = L.len[g];
+            st[kind].w[i] = L.w[g];
+            st[kind].mx[i] = L.mx[g];
+          }
+        }
       }
     }
+    __syncthreads();
+    // (A) decision chain
+    if (threadIdx.x == 0) {
+      for (int kind = 0; kind < 2; ++kind) s_base[kind] = ((kind == 0 ? s_idx_sh : v_idx_sh) / CHUNK) * CHUNK;
+      int s_idx = s_idx_sh, v_idx = v_idx_sh, k = 0;
+      double ol_s = ol_s_sh, ol_v = ol_v_sh, approx = approx_sh;
+      const int s_end = s_base[0] + CHUNK, v_end = s_base[1] + CHUNK;
+      while (k < PCH) {
+        const bool has_s = s_idx < n_total, has_v = v_idx < n_total;
+        if (!has_s && !has_v) break;
+        if ((has_s && s_idx >= s_end) || (has_v && v_idx >= v_end)) break;  // restage first
+        bool take_slash;
+        const int so = s_idx - s_base[0], vo = v_idx - s_base[1];
+        if (!has_s) {
+          take_slash = false;
+        } else if (!has_v) {
+          take_slash = true;
+        } else {
+          // |V| = v_idx, |S| = s_idx (prefill.py:206-207)
+          take_slash = take_slash_decision(st[0].w[so] - ol_v, max(1, st[0].len[so] - v_idx),
+                                           st[1].w[vo] - ol_s, max(1, st[1].len[vo] - s_idx));
+        }
+        if (take_slash) {
+          approx += st[0].w[so] - ol_v;
+          ol_s += st[0].mx[so];
+          c_code[k] = st[0].idx[so];
+          c_other[k] = v_idx;
+          c_w[k] = st[0].w[so];
+          ++s_idx;
+        } else {
+          approx += st[1].w[vo] - ol_s;
+          ol_v += st[1].mx[vo];
+          c_code[k] = st[1].idx[vo] | static_cast<int32_t>(0x80000000u);
+          c_other[k] = s_idx;
+          c_w[k] = st[1].w[vo];
+          ++v_idx;
+        }
+        c_approx[k] = approx;
+        ++k;
+        // the reference re-tests the loop condition after every pick; stop the
+        // chain at the approx target (exact is applied in phase C)
+        if (!(approx < target - EPS)) break;
+      }
+      s_idx_sh = s_idx;
+      v_idx_sh = v_idx;
+      ol_s_sh = ol_s;
+      ol_v_sh = ol_v;
+      approx_sh = approx;
+      n_chunk = k;
+      exhausted = (s_idx >= n_total && v_idx >= n_total) ? 1 : 0;
+    }
+    __syncthreads();
+    const int nk = n_chunk;
+    // (B) crossing sums, one warp per new pick, selection order
+    for (int j = warp; j < nk; j += G_WARPS) {
+      const int32_t code = c_code[j];
+      const bool is_vert = code < 0;
+      const int idx = code & 0x7fffffff;
+      const int n_other = c_other[j];
+      const int32_t *other = L.idx + lb + static_cast<int64_t>(is_vert ? 0 : 1) * n_total;
+      double sum = 0.0;
+      for (int j0 = 0; j0 < n_other; j0 += 32) {
+        const int jj = j0 + lane;
+        double v = 0.0;
+        if (jj < n_other) {
+          const int o = other[jj];
+          // slash d=idx x vertical c=o at g=o+idx; vertical c=idx x slash d=o at g=idx+o
+          const int g = idx + o;
+          const int c = is_vert ? idx : o;
+          const int r = cells.row(h, g);
+          if (r >= 0) v = cells.value(h, r, g, c);
+        }
+        const unsigned any = __ballot_sync(0xffffffffu, v != 0.0);
+        if (any) {
+          vals[warp][lane] = v;
+          __syncwarp();
+          if (lane == 0) {
+            const int m = min(32, n_other - j0);
+            for (int i = 0; i < m; ++i) sum += vals[warp][i];  // python sum(): left to right
+          }
+          __syncwarp();
+        }
+      }
+      if (lane == 0) c_cross[j] = sum;
+    }
+    __syncthreads();
+    // (C) exact accumulator + dual termination, in order
+    if (threadIdx.x == 0) {
+      double exact = exact_sh;
+      int n = n_sh;
+      int stop = 0;
+      for (int j = 0; j < nk; ++j) {
+        exact += c_w[j] - c_cross[j];
+        P.code[pb + n] = c_code[j];
+        P.approx[pb + n] = c_approx[j];
+        ++n;
+        if (!(c_approx[j] < target - EPS && exact < target - EPS)) {
+          stop = 1;
+          approx_sh = c_approx[j];
+          break;
+        }
+      }
+      if (!stop && nk > 0) approx_sh = c_approx[nk - 1];
+      exact_sh = exact;
+      n_sh = n;
+      if (stop || exhausted || n >= cap) done = 1;
+    }
+    __syncthreads();
   }
-  if (t_stop < 0) t_stop = n;  // lists exhausted
-  if (lane == 0) {
-    n_final[h] = t_stop;
-    const double cov = T > 0 ? exact / T : 0.0;  // prefill.py:221
+  if (threadIdx.x == 0) {
+    P.n[h] = n_sh;
+    n_final[h] = n_sh;
+    const double cov = T > 0 ? exact_sh / T : 0.0;  // prefill.py:221
     coverage[h] = cov < 1.0 ? cov : 1.0;
-    approx_out[h] = approx;
+    approx_out[h] = n_sh > 0 ? approx_sh : 0.0;
   }
 }
 
@@ -458,8 +448,6 @@ inline size_t sort_smem() { return sizeof(typename BlockSort::TempStorage) + 4 *
 int run_tail(Work &w, int H, int n_total, double alpha, const double *total, int32_t *slash_ids,
              int32_t *vert_ids, int32_t *counts, double *coverage, double *approx, int32_t *picks_out,
              int32_t *n_picks_out, cudaStream_t st) {
-  finalize_kernel<<<H, 32, 0, st>>>(w.picks, w.cap, alpha, total, w.n_final, coverage, approx);
-  LS_LAUNCH_CHECK("finalize_kernel");
   LS_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * H * w.words, st));
   LS_CUDA(cudaMemsetAsync(w.vbits, 0, sizeof(uint32_t) * H * w.words, st));
   plan_bits_kernel<<<dim3(8, H), 256, 0, st>>>(w.picks, w.cap, w.n_final, n_total, w.words, w.sbits, w.vbits,
@@ -503,15 +491,12 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   sel::sort_lines_kernel<float><<<dim3(2, H), sel::SORT_THREADS, smem, st>>>(v_w, v_max, s_w, s_max, rows, n_s,
                                                                             n_total, L->row_offset, w.lists);
   LS_LAUNCH_CHECK("sort_lines_kernel");
-  sel::chain_kernel<<<H, 128, 0, st>>>(w.lists, n_total, alpha, total, w.picks, w.cap);
-  LS_LAUNCH_CHECK("chain_kernel");
   sel::row_of_kernel<<<dim3(ceil_div(n_total, 256), H), 256, 0, st>>>(rows, n_s, n_total, L->row_offset, w.row_of);
   sel::row_of_set_kernel<<<dim3(ceil_div(n_s, 256), H), 256, 0, st>>>(rows, n_s, n_total, L->row_offset, w.row_of);
   LS_LAUNCH_CHECK("row_of_kernel");
   sel::RecomputeCells cells;
   cells.q = q;
   cells.k = k;
-  cells.rows = rows;
   cells.row_of = w.row_of;
   cells.row_stats = row_stats;
   cells.n_s = n_s;
@@ -522,8 +507,9 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   cells.q_head_stride = L->q_head_stride;
   cells.kv_head_stride = L->kv_head_stride;
   cells.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
-  sel::cross_kernel<sel::RecomputeCells><<<dim3(32, H), 256, 0, st>>>(w.lists, n_total, w.picks, w.cap, cells);
-  LS_LAUNCH_CHECK("cross_kernel");
+  sel::greedy_kernel<sel::RecomputeCells><<<H, sel::G_THREADS, 0, st>>>(w.lists, n_total, alpha, total, w.picks,
+                                                                        w.cap, cells, w.n_final, coverage, approx);
+  LS_LAUNCH_CHECK("greedy_kernel");
   return sel::run_tail(w, H, n_total, alpha, total, slash_ids, vert_ids, counts, coverage, approx, picks, n_picks,
                        st);
 }
@@ -564,13 +550,12 @@ extern "C" int ls_greedy_dense(int32_t n_slash, const int32_t *s_idx, const doub
   sel::load_lists_kernel<<<8, 256, 0, st>>>(n_slash, s_idx, s_w, s_len, s_max, 0, n_total, w.lists);
   sel::load_lists_kernel<<<8, 256, 0, st>>>(n_vert, v_idx, v_w, v_len, v_max, 1, n_total, w.lists);
   LS_LAUNCH_CHECK("load_lists_kernel");
-  sel::chain_kernel<<<1, 128, 0, st>>>(w.lists, n_total, alpha, tot, w.picks, w.cap);
-  LS_LAUNCH_CHECK("chain_kernel");
   sel::row_of_kernel<<<dim3(ceil_div(n_total, 256), 1), 256, 0, st>>>(positions, n_rows, n_total, 0, w.row_of);
   sel::row_of_set_kernel<<<dim3(ceil_div(n_rows, 256), 1), 256, 0, st>>>(positions, n_rows, n_total, 0, w.row_of);
   sel::DenseCells cells{weights, w.row_of, n_total};
-  sel::cross_kernel<sel::DenseCells><<<dim3(32, 1), 256, 0, st>>>(w.lists, n_total, w.picks, w.cap, cells);
-  LS_LAUNCH_CHECK("cross_kernel");
+  sel::greedy_kernel<sel::DenseCells><<<1, sel::G_THREADS, 0, st>>>(w.lists, n_total, alpha, tot, w.picks, w.cap,
+                                                                    cells, w.n_final, coverage, approx);
+  LS_LAUNCH_CHECK("greedy_kernel");
   return sel::run_tail(w, 1, n_total, alpha, tot, slash_ids, vert_ids, counts, coverage, approx, nullptr, nullptr,
                        st);
 }
