@@ -62,6 +62,7 @@ SIGNATURES = {
                                   P, P, P, P, SZ, P]),
     "ls_vs_attention_workspace": (SZ, [LD]),
     "ls_vs_attention": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, SZ, P]),
+    "ls_vs_attention_simt": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, SZ, P]),
     "ls_plan_rows": (C.c_int, [LD, I32, P, P, P, P, P, P, I64, I64, P]),
     "ls_dense_attention": (C.c_int, [LD, P, P, P, P, I32, P]),
     "ls_decode_attention_workspace": (SZ, [DS, I32]),
@@ -103,8 +104,9 @@ def check(status: int, what: str = "") -> None:
 # CUDA kernels each C-ABI entry launches (memsets/memcpys not counted);
 # bench.py reports the sum over its timed region as `gpu_launches`.
 KERNELS_PER_CALL = {
-    "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 8, "ls_greedy_dense": 8,
-    "ls_vs_attention": 3, "ls_plan_rows": 3, "ls_dense_attention": 1, "ls_decode_attention": 2,
+    "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 6, "ls_greedy_dense": 6,
+    "ls_vs_attention": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 3, "ls_dense_attention": 1,
+    "ls_decode_attention": 2,
     "ls_decode_select": 1, "ls_kv_compact": 1,
 }
 launch_count = 0

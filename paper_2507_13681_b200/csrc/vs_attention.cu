@@ -375,9 +375,27 @@ int check_desc(const ls_layer_desc *L) {
 
 using namespace ls;
 
+namespace ls {
+size_t vs_attention_tc_workspace(const ls_layer_desc *L);
+int vs_attention_tc(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                    const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
+                    int32_t out_bf16, int64_t *cells, int dense, void *ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace ls
+
 extern "C" size_t ls_vs_attention_workspace(const ls_layer_desc *L) {
   const size_t words = (L->n_total + 31) / 32;
-  return 2 * static_cast<size_t>(L->n_heads) * words * 4 + 1024;
+  const size_t simt = 2 * static_cast<size_t>(L->n_heads) * words * 4 + 1024;
+  const size_t tcw = vs_attention_tc_workspace(L);
+  return simt > tcw ? simt : tcw;
+}
+
+extern "C" int ls_vs_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                               const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
+                               int32_t out_bf16, int64_t *cells, void *ws, size_t ws_bytes, ls_stream_t stream) {
+  int stc = k5::check_desc(L);
+  if (stc) return stc;
+  return vs_attention_tc(L, q, k, v, slash_ids, vert_ids, counts, out, out_bf16, cells, 0, ws, ws_bytes,
+                         static_cast<cudaStream_t>(stream));
 }
 
 static int build_bits(const ls_layer_desc *L, const int32_t *slash_ids, const int32_t *vert_ids,
@@ -391,9 +409,10 @@ static int build_bits(const ls_layer_desc *L, const int32_t *slash_ids, const in
   return LS_OK;
 }
 
-extern "C" int ls_vs_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
-                               const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
-                               int32_t out_bf16, int64_t *cells, void *ws, size_t ws_bytes, ls_stream_t stream) {
+extern "C" int ls_vs_attention_simt(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k,
+                                    const uint16_t *v, const int32_t *slash_ids, const int32_t *vert_ids,
+                                    const int32_t *counts, void *out, int32_t out_bf16, int64_t *cells, void *ws,
+                                    size_t ws_bytes, ls_stream_t stream) {
   int stc = k5::check_desc(L);
   if (stc) return stc;
   LS_REQUIRE(ws_bytes >= ls_vs_attention_workspace(L), LS_ERR_WORKSPACE, "vs_attention workspace too small");
@@ -458,28 +477,10 @@ extern "C" int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, con
   int stc = k5::check_desc(L);
   if (stc) return stc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k5::Params p;
-  k5::fill(p, L);
-  p.q = q;
-  p.k = k;
-  p.v = v;
-  p.slash_ids = p.vert_ids = nullptr;
-  p.counts = nullptr;
-  static uint32_t *dummy_bits = nullptr;
-  p.sbits = p.vbits = nullptr;
-  (void)dummy_bits;
-  p.out = out;
-  p.out_bf16 = out_bf16;
-  long long *cells = nullptr;
-  LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&cells), sizeof(long long) * L->n_heads, st));
-  LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(long long) * L->n_heads, st));
-  p.cells = cells;
-  p.dense = 1;
-  const size_t smem = k5::smem_bytes(L->head_dim);
-  LS_CUDA(cudaFuncSetAttribute(k5::vs_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
-  k5::vs_attention_kernel<<<dim3(ceil_div(L->n_new, k5::BM), L->n_heads), k5::THREADS, smem, st>>>(p);
-  LS_LAUNCH_CHECK("vs_attention_kernel(dense)");
+  int64_t *cells = nullptr;
+  LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&cells), sizeof(int64_t) * L->n_heads, st));
+  // dense mode touches every causal key block with the causal mask only (tensor-core path)
+  int s = vs_attention_tc(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, 1, nullptr, 0, st);
   LS_CUDA(cudaFreeAsync(cells, st));
-  return LS_OK;
+  return s;
 }

@@ -1,0 +1,502 @@
+// K5 (tensor-core path) -- vertical/slash sparse attention on tcgen05 / TMEM.
+//
+// Same contract as the CUDA-core kernel in vs_attention.cu (reference
+// masked_sparse_attention, tensor_ops.py:141-183 with `_row_columns`,
+// tensor_ops.py:130-138): per (head, 128-row q tile) the CTA walks
+//   * key blocks (BN = 128) touched by a selected slash, mask
+//     causal & (vbit[c] | sbit[g - c]), and
+//   * gathered tiles of selected verticals outside those blocks, mask causal,
+// with S = Q K^T and O_tile = P V on the 5th-gen tensor cores:
+//   Q, K, V, P staged in shared memory in the 128B-swizzled UMMA layouts
+//   (tc_common.cuh), K/V tiles double-buffered with cp.async (gathers are
+//   row-granular, so TMA tiled copies do not apply), accumulators in TMEM
+//   (S: 128 columns, O_tile: D columns), one elected thread issues
+//   tcgen05.mma and commits to an mbarrier; 128 softmax threads own one TMEM
+//   lane (= one q row) each: masked online softmax in fp32 (log2 domain),
+//   P rounded to bf16 into shared memory, O accumulated in registers.
+// Rows with no selected cell fall back to the diagonal (out = V[g]).
+// The per-row popcount of the mask is the OpCounter increment
+// (tensor_ops.py:172-174).
+
+#include "ls_common.cuh"
+#include "tc_common.cuh"
+
+namespace ls {
+namespace k5tc {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int THREADS = 128;
+constexpr int MAX_KB = 2048;  // key blocks per head (n_total <= 262144)
+
+struct Params {
+  const uint16_t *q, *k, *v;
+  const int32_t *slash_ids, *vert_ids, *counts;
+  const uint32_t *vbits;   // [H][words]
+  const uint32_t *rsbits;  // [H][words + 8] reversed slash bits: bit i = sbit[n_total-1-i]
+  int32_t *gather_ws;      // [n_qtiles * H][n_total]
+  int n_heads, group, n_new, n_total, row_offset, words, n_qtiles;
+  int64_t q_head_stride, kv_head_stride;
+  float scale_log2;
+  void *out;
+  int out_bf16;
+  long long *cells;
+  int dense;
+};
+
+template <int D>
+struct Smem {
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int P_BYTES = BM * BN * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K0 = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V0 = OFF_K0 + 2 * KV_BYTES;
+  static constexpr int OFF_P = OFF_V0 + 2 * KV_BYTES;
+  static constexpr int OFF_MISC = OFF_P + P_BYTES;
+  static constexpr int MISC_BYTES = 1024 + MAX_KB * 2 + 2 * BN * 4 + 64;
+  static constexpr int TOTAL = OFF_MISC + MISC_BYTES + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void *gptr, bool valid) {
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(gptr), "r"(n) : "memory");
+}
+
+// 128-bit window of a bit array starting at bit `s` (bits beyond the array read as 0 if padded)
+__device__ __forceinline__ void bit_window(const uint32_t *bits, int s, uint32_t *w) {
+  const int w0 = s >> 5, sh = s & 31;
+  uint32_t x[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) x[i] = __ldg(bits + w0 + i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = __funnelshift_r(x[i], x[i + 1], sh);
+}
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
+  extern __shared__ unsigned char smem_dyn[];
+  using L = Smem<D>;
+  unsigned char *smem =
+      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  unsigned char *misc = smem + L::OFF_MISC;
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(misc);          // [2]
+  uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(misc + 16);
+  int *sh_int = reinterpret_cast<int *>(misc + 32);              // scratch ints [32]
+  uint32_t *kb_bits = reinterpret_cast<uint32_t *>(misc + 256);  // [64] bitmap of touched key blocks
+  int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 1024);
+  int *gcols = reinterpret_cast<int *>(misc + 1024 + MAX_KB * 2);  // [2][BN] gathered columns per buffer
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = blockIdx.y, qt = blockIdx.x;
+  const int r0 = qt * BM;
+  const int nr = min(BM, p.n_new - r0);
+  const int g0 = p.row_offset + r0;
+  const int g_hi = g0 + nr - 1;
+  const int kv = h / p.group;
+  const uint16_t *qb = p.q + static_cast<int64_t>(h) * p.q_head_stride;
+  const uint16_t *kb = p.k + static_cast<int64_t>(kv) * p.kv_head_stride;
+  const uint16_t *vb = p.v + static_cast<int64_t>(kv) * p.kv_head_stride;
+  const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * p.words;
+  const uint32_t *rsbits = p.rsbits + static_cast<int64_t>(h) * (p.words + 8);
+  int32_t *gl = p.gather_ws + (static_cast<int64_t>(h) * p.n_qtiles + qt) * p.n_total;
+
+  // ---- TMEM allocation (warp 0), barriers
+  if (warp == 0) tc::tmem_alloc(tmem_base_sh, 256);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+  }
+  for (int i = tid; i < 64; i += THREADS) kb_bits[i] = 0u;
+  // ---- Q tile (K-major SW128) via cp.async
+  {
+    const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
+    constexpr int CH = D / 8;
+    for (int i = tid; i < BM * CH; i += THREADS) {
+      const int r = i / CH, c = i % CH;
+      const bool ok = r < nr;
+      cp_async16_zfill(qs + tc::sw128_offset(r, c, BM), qb + static_cast<int64_t>(ok ? r0 + r : 0) * D + c * 8,
+                           ok);
+    }
+    tc::cp_async_commit();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_base_sh;
+  const uint32_t tmem_s = tmem;        // columns [0, 128)
+  const uint32_t tmem_o = tmem + 128;  // columns [128, 128 + D)
+
+  // ---- tile list: touched key blocks, then gathered verticals
+  const int n_kb = g_hi / BN + 1;
+  const int n_sl = p.dense ? 0 : p.counts[h * 2 + 0];
+  const int n_vt = p.dense ? 0 : p.counts[h * 2 + 1];
+  const int32_t *S = p.slash_ids + static_cast<int64_t>(h) * p.n_total;
+  const int32_t *V = p.vert_ids + static_cast<int64_t>(h) * p.n_total;
+  if (p.dense) {
+    for (int b = tid; b < n_kb; b += THREADS) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
+  } else {
+    for (int i = tid; i < n_sl; i += THREADS) {
+      const int dd = S[i];
+      if (dd > g_hi) break;
+      const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
+      for (int b = c_lo / BN; b <= c_hi / BN; ++b) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int n = 0;
+    for (int w = 0; w < (n_kb + 31) / 32; ++w) {
+      uint32_t x = kb_bits[w];
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        if (w * 32 + b < n_kb) dense_list[n++] = static_cast<int16_t>(w * 32 + b);
+      }
+    }
+    sh_int[0] = n;
+  }
+  // gathered verticals (ascending): V entries <= g_hi whose block is untouched
+  int n_g = 0;
+  if (!p.dense && n_vt > 0) {
+    int v_end = 0;
+    {
+      int lo = 0, hi = n_vt;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (V[mid] <= g_hi)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      v_end = lo;
+    }
+    for (int base = 0; base < v_end; base += THREADS) {
+      const int i = base + tid;
+      const int c = i < v_end ? V[i] : 0;
+      const bool take = i < v_end && !((kb_bits[(c / BN) >> 5] >> ((c / BN) & 31)) & 1u);
+      const unsigned ball = __ballot_sync(0xffffffffu, take);
+      __syncthreads();
+      if (lane == 0) sh_int[8 + warp] = __popc(ball);
+      __syncthreads();
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += sh_int[8 + w];
+      const int tot = sh_int[8] + sh_int[9] + sh_int[10] + sh_int[11];
+      if (take) gl[n_g + before + __popc(ball & ((1u << lane) - 1u))] = c;
+      n_g += tot;
+    }
+  }
+  __syncthreads();
+  const int n_dense = sh_int[0];
+  const int n_tiles = n_dense + (n_g + BN - 1) / BN;
+
+  // ---- per-thread row state (thread = TMEM lane = q row)
+  const int row = tid;
+  const int my_g = g0 + row;
+  const bool row_ok = row < nr;
+  float m = -INFINITY, l = 0.f;
+  float o[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) o[i] = 0.f;
+  long long my_cells = 0;
+
+  constexpr uint32_t IDESC_S = tc::make_idesc(BM, BN, false, false);
+  constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, false, true);
+  const uint32_t q_s = tc::smem_u32(smem + L::OFF_Q);
+  const uint32_t p_s = tc::smem_u32(smem + L::OFF_P);
+
+  auto issue_load = [&](int i, int buf) {
+    const uint32_t ks = tc::smem_u32(smem + L::OFF_K0 + buf * L::KV_BYTES);
+    const uint32_t vs = tc::smem_u32(smem + L::OFF_V0 + buf * L::KV_BYTES);
+    int c;  // key of row `tid` of the tile
+    bool ok;
+    if (i < n_dense) {
+      c = dense_list[i] * BN + tid;
+      ok = c < p.n_total;
+    } else {
+      const int j = (i - n_dense) * BN + tid;
+      ok = j < n_g;
+      c = ok ? gl[j] : 0x7fffffff;
+    }
+    gcols[buf * BN + tid] = c;
+    const int cc = ok ? c : 0;
+    constexpr int CH = D / 8;
+#pragma unroll 4
+    for (int ch = 0; ch < CH; ++ch) {
+      const uint32_t off = tc::sw128_offset(tid, ch, BN);
+      cp_async16_zfill(ks + off, kb + static_cast<int64_t>(cc) * D + ch * 8, ok);
+      cp_async16_zfill(vs + off, vb + static_cast<int64_t>(cc) * D + ch * 8, ok);
+    }
+    tc::cp_async_commit();
+  };
+
+  if (n_tiles > 0) issue_load(0, 0);
+  uint32_t ph_s = 0, ph_o = 0;
+  for (int i = 0; i < n_tiles; ++i) {
+    const int buf = i & 1;
+    if (i + 1 < n_tiles) {
+      issue_load(i + 1, buf ^ 1);
+      tc::cp_async_wait<1>();
+    } else {
+      tc::cp_async_wait<0>();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    // S = Q K^T
+    if (tid == 0) {
+      const uint32_t ks = tc::smem_u32(smem + L::OFF_K0 + buf * L::KV_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t koff = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+        const uint64_t ad = tc::make_desc(q_s + koff, 16, 1024);
+        const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+        tc::mma_bf16(tmem_s, ad, bd, IDESC_S, kk > 0);
+      }
+      tc::mma_commit(&mbar[0]);
+    }
+    // mask of this row for this tile (overlaps the MMA)
+    const bool gathered = i >= n_dense;
+    uint32_t mk[4];
+    if (!row_ok) {
+      mk[0] = mk[1] = mk[2] = mk[3] = 0u;
+    } else if (!gathered) {
+      const int c0 = dense_list[i] * BN;
+      const int lim = my_g - c0;  // columns j <= lim are causal
+      if (p.dense) {
+        mk[0] = mk[1] = mk[2] = mk[3] = 0xffffffffu;
+      } else {
+        uint32_t vw[4], sw[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) vw[t] = (c0 / 32 + t < p.words) ? __ldg(vbits + c0 / 32 + t) : 0u;
+        bit_window(rsbits, p.n_total - 1 - my_g + c0, sw);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) mk[t] = vw[t] | sw[t];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int hi = lim - 32 * t;  // bits [0, hi] valid in word t
+        const uint32_t cm = hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u));
+        mk[t] &= cm;
+      }
+    } else {
+      // gathered columns ascending: causal prefix
+      const int *gc = gcols + buf * BN;
+      int lo = 0, hi = BN;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (gc[mid] <= my_g)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int nb = lo - 32 * t;
+        mk[t] = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
+      }
+    }
+    my_cells += __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
+
+    tc::mbar_wait(&mbar[0], ph_s);
+    ph_s ^= 1;
+    tc::fence_after_sync();
+    // pass 1: masked row max
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    float tmax = -INFINITY;
+#pragma unroll
+    for (int cch = 0; cch < 4; ++cch) {
+      float sv[32];
+      tc::tmem_ld32(tmem_s + lane_base + cch * 32, sv);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if ((mk[cch] >> j) & 1u) tmax = fmaxf(tmax, sv[j] * p.scale_log2);
+    }
+    const float m_new = fmaxf(m, tmax);
+    const float corr = (m_new == -INFINITY) ? 1.f : fast_exp2(m - m_new);
+    // pass 2: P = exp2(s - m_new) -> bf16 smem (K-major SW128), row sum
+    float lsum = 0.f;
+#pragma unroll
+    for (int cch = 0; cch < 4; ++cch) {
+      float sv[32];
+      tc::tmem_ld32(tmem_s + lane_base + cch * 32, sv);
+      tc::tmem_wait_ld();
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(sv[j] * p.scale_log2 - m_new) : 0.f;
+        const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(sv[j + 1] * p.scale_log2 - m_new) : 0.f;
+        lsum += a + b;
+        pk[j >> 1] = tc::pack_bf16(a, b);
+      }
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int chunk = cch * 4 + q4;  // 16-byte chunk index along keys
+        uint4 val = make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        *reinterpret_cast<uint4 *>(smem + L::OFF_P + tc::sw128_offset(row, chunk, BM)) = val;
+      }
+    }
+    l = l * corr + lsum;
+    m = m_new;
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    // O_tile = P V
+    if (tid == 0) {
+      const uint32_t vs = tc::smem_u32(smem + L::OFF_V0 + buf * L::KV_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BN / 16; ++kk) {
+        const uint64_t ad = tc::make_desc(p_s + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
+        tc::mma_bf16(tmem_o, ad, bd, IDESC_O, kk > 0);
+      }
+      tc::mma_commit(&mbar[1]);
+    }
+    tc::mbar_wait(&mbar[1], ph_o);
+    ph_o ^= 1;
+    tc::fence_after_sync();
+#pragma unroll
+    for (int cch = 0; cch < D / 32; ++cch) {
+      float ov[32];
+      tc::tmem_ld32(tmem_o + lane_base + cch * 32, ov);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) o[cch * 32 + j] = fmaf(o[cch * 32 + j], corr, ov[j]);
+    }
+    tc::fence_before_sync();
+  }
+
+  tc::cp_async_wait<0>();
+  // ---- epilogue
+  if (row_ok) {
+    const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * D;
+    if (l > 0.f) {
+      const float inv = 1.f / l;
+      if (p.out_bf16) {
+        uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + orow;
+#pragma unroll
+        for (int j = 0; j < D; j += 8) {
+          uint4 val = make_uint4(tc::pack_bf16(o[j] * inv, o[j + 1] * inv), tc::pack_bf16(o[j + 2] * inv, o[j + 3] * inv),
+                                 tc::pack_bf16(o[j + 4] * inv, o[j + 5] * inv), tc::pack_bf16(o[j + 6] * inv, o[j + 7] * inv));
+          *reinterpret_cast<uint4 *>(dst + j) = val;
+        }
+      } else {
+        float *dst = reinterpret_cast<float *>(p.out) + orow;
+#pragma unroll
+        for (int j = 0; j < D; j += 4)
+          *reinterpret_cast<float4 *>(dst + j) = make_float4(o[j] * inv, o[j + 1] * inv, o[j + 2] * inv, o[j + 3] * inv);
+      }
+    } else {  // diagonal fallback (tensor_ops.py:136-137)
+      for (int j = 0; j < D; ++j) {
+        const float val = bf2f(vb[static_cast<int64_t>(my_g) * D + j]);
+        if (p.out_bf16)
+          reinterpret_cast<uint16_t *>(p.out)[orow + j] = f2bf(val);
+        else
+          reinterpret_cast<float *>(p.out)[orow + j] = val;
+      }
+      my_cells += 1;
+    }
+  }
+  const long long cs = warp_sum_ll(my_cells);
+  if (lane == 0 && cs)
+    atomicAdd(reinterpret_cast<unsigned long long *>(p.cells + h), static_cast<unsigned long long>(cs));
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
+__global__ void vert_bits_kernel(const int32_t *vert_ids, const int32_t *counts, int n_total, int words,
+                                 uint32_t *vbits) {
+  const int h = blockIdx.y;
+  const int n = counts[h * 2 + 1];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = vert_ids[static_cast<int64_t>(h) * n_total + i];
+    atomicOr(vbits + static_cast<int64_t>(h) * words + (c >> 5), 1u << (c & 31));
+  }
+}
+
+// reversed slash bitmap: bit i = sbit[n_total - 1 - i]
+__global__ void reverse_bits_kernel(const int32_t *slash_ids, const int32_t *counts, int n_total, int words,
+                                    uint32_t *rsbits) {
+  const int h = blockIdx.y;
+  const int n = counts[h * 2];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = slash_ids[static_cast<int64_t>(h) * n_total + i];
+    const int x = n_total - 1 - d;
+    atomicOr(rsbits + static_cast<int64_t>(h) * (words + 8) + (x >> 5), 1u << (x & 31));
+  }
+}
+
+}  // namespace k5tc
+}  // namespace ls
+
+using namespace ls;
+
+namespace ls {
+size_t vs_attention_tc_workspace(const ls_layer_desc *L) {
+  const size_t words = (L->n_total + 31) / 32;
+  const size_t nqt = (L->n_new + k5tc::BM - 1) / k5tc::BM;
+  return static_cast<size_t>(L->n_heads) * (words * 4 + (words + 8) * 4) + nqt * L->n_heads * L->n_total * 4 + 4096;
+}
+
+int vs_attention_tc(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                    const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
+                    int32_t out_bf16, int64_t *cells, int dense, void *ws, size_t ws_bytes, cudaStream_t st) {
+  LS_REQUIRE(L->head_dim == 64 || L->head_dim == 128, LS_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  LS_REQUIRE((L->n_total + k5tc::BN - 1) / k5tc::BN <= k5tc::MAX_KB, LS_ERR_UNSUPPORTED, "n_total too large");
+  LS_REQUIRE(dense || ws_bytes >= vs_attention_tc_workspace(L), LS_ERR_WORKSPACE, "vs_attention workspace too small");
+  const int words = (L->n_total + 31) / 32;
+  const int nqt = (L->n_new + k5tc::BM - 1) / k5tc::BM;
+  Carver c(dense ? nullptr : ws, ws_bytes);  // dense mode reads no plan buffers
+  uint32_t *vbits = c.take<uint32_t>(static_cast<size_t>(L->n_heads) * words);
+  uint32_t *rsbits = c.take<uint32_t>(static_cast<size_t>(L->n_heads) * (words + 8));
+  int32_t *gather = c.take<int32_t>(static_cast<size_t>(nqt) * L->n_heads * L->n_total);
+  if (!dense) {
+    LS_CUDA(cudaMemsetAsync(vbits, 0, sizeof(uint32_t) * L->n_heads * words, st));
+    LS_CUDA(cudaMemsetAsync(rsbits, 0, sizeof(uint32_t) * L->n_heads * (words + 8), st));
+    k5tc::vert_bits_kernel<<<dim3(4, L->n_heads), 256, 0, st>>>(vert_ids, counts, L->n_total, words, vbits);
+    k5tc::reverse_bits_kernel<<<dim3(4, L->n_heads), 256, 0, st>>>(slash_ids, counts, L->n_total, words, rsbits);
+    LS_LAUNCH_CHECK("reverse_bits_kernel");
+  }
+  k5tc::Params p;
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.slash_ids = slash_ids;
+  p.vert_ids = vert_ids;
+  p.counts = counts;
+  p.vbits = vbits;
+  p.rsbits = rsbits;
+  p.gather_ws = gather;
+  p.n_heads = L->n_heads;
+  p.group = L->n_heads / L->n_kv_heads;
+  p.n_new = L->n_new;
+  p.n_total = L->n_total;
+  p.row_offset = L->row_offset;
+  p.words = words;
+  p.n_qtiles = nqt;
+  p.q_head_stride = L->q_head_stride;
+  p.kv_head_stride = L->kv_head_stride;
+  p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
+  p.out = out;
+  p.out_bf16 = out_bf16;
+  p.cells = reinterpret_cast<long long *>(cells);
+  p.dense = dense;
+  LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * L->n_heads, st));
+  dim3 grid(nqt, L->n_heads);
+  if (L->head_dim == 128) {
+    const int smem = k5tc::Smem<128>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k5tc::vs_attention_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k5tc::vs_attention_tc_kernel<128><<<grid, k5tc::THREADS, smem, st>>>(p);
+  } else {
+    const int smem = k5tc::Smem<64>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k5tc::vs_attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k5tc::vs_attention_tc_kernel<64><<<grid, k5tc::THREADS, smem, st>>>(p);
+  }
+  LS_LAUNCH_CHECK("vs_attention_tc_kernel");
+  return LS_OK;
+}
+}  // namespace ls

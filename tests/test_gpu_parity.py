@@ -310,3 +310,55 @@ def test_compact_cache_known_answer(cuda_lib):  # test_kvcompress.py:175-184
     out = kv.compact_cache(h, picked, recent_window=1)
     assert out.retained_ids.tolist() == [1, 3, 5]
     assert np.array_equal(out.keys, keys[[1, 3, 5]]) and np.array_equal(out.values, vals[[1, 3, 5]])
+
+
+# ------------------------------------------- tensor-core vs CUDA-core K5
+@pytest.mark.parametrize("d,n_q,n_kv,ro,n_new", [(128, 8, 2, 2048, 2048), (64, 4, 4, 700, 333),
+                                                 (128, 4, 1, 0, 1500)])
+def test_vs_attention_tc_matches_simt_and_oracle(cuda_lib, d, n_q, n_kv, ro, n_new):
+    import ctypes
+
+    from paper_2507_13681_b200 import _lib
+    from paper_2507_13681_b200.synth import layer_qkv_torch
+
+    n_total = ro + n_new
+    spec = SynthSpec(n_q, n_kv, d, n_total, seed=7)
+    Q, K, V = layer_qkv_torch(spec, 0)
+    qb = Q[:, ro:n_total].contiguous()
+    rows = pf.sample_rows_device(n_new, 0.1, 32, 3, 1, 0, 0, n_q)
+    plans = pf.sparsify_layer(qb, K, rows, 0.955, n_new, n_total, n_kv)
+    out_tc, cells_tc = tops.attention_layer(qb, K, V, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total,
+                                            n_kv, out_dtype=torch.float32)
+    L = pf.layer_desc(n_q, n_kv, d, n_new, n_total, qb.stride(0), K.stride(0))
+    out_s = torch.empty_like(out_tc)
+    cells_s = torch.empty_like(cells_tc)
+    n = _lib.lib().ls_vs_attention_workspace(ctypes.byref(L))
+    ws = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.call("ls_vs_attention_simt", ctypes.byref(L), qb.data_ptr(), K.data_ptr(), V.data_ptr(),
+              plans.slash_ids.data_ptr(), plans.vert_ids.data_ptr(), plans.counts.data_ptr(), out_s.data_ptr(), 0,
+              cells_s.data_ptr(), ws.data_ptr(), n, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(cells_tc, cells_s)
+    assert (out_tc - out_s).abs().max().item() <= 1e-2
+    hp = plans.to_host()
+    group = n_q // n_kv
+    for h in (0, n_q - 1):
+        Z, _, cells = oatt.masked_sparse_attention(qb[h].double().cpu().numpy(), K[h // group].double().cpu().numpy(),
+                                                   V[h // group].double().cpu().numpy(), hp[h].selected_slashes,
+                                                   hp[h].selected_verticals, ro)
+        assert cells == int(cells_tc[h])
+        assert np.abs(out_tc[:, h].double().cpu().numpy() - Z).max() <= ATOL
+
+
+def test_dense_attention_tc_layer(cuda_lib):
+    from paper_2507_13681_b200.synth import layer_qkv_torch
+
+    spec = SynthSpec(4, 2, 128, 1000, seed=9)
+    Q, K, V = layer_qkv_torch(spec, 0)
+    ro, n_new = 400, 600
+    qb = Q[:, ro:].contiguous()
+    out = tops.dense_attention_layer(qb, K, V, n_new, 1000, 2, out_dtype=torch.float32)
+    for h in (0, 3):
+        Zo, _ = oatt.scaled_dot_attention(qb[h].double().cpu().numpy(), K[h // 2].double().cpu().numpy(),
+                                          V[h // 2].double().cpu().numpy(), ro)
+        assert np.abs(out[:, h].double().cpu().numpy() - Zo).max() <= ATOL
