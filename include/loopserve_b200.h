@@ -108,6 +108,11 @@ int ls_score_lines(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
                    const int32_t *rows, double *v_w, float *v_max, double *s_w, float *s_max,
                    float *row_stats, double *total, int64_t *score_count, void *ws,
                    size_t ws_bytes, ls_stream_t stream);
+/* Same contract on CUDA cores (tests cross-check the tcgen05 kernel).    */
+int ls_score_lines_simt(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k,
+                        const int32_t *rows, double *v_w, float *v_max, double *s_w, float *s_max,
+                        float *row_stats, double *total, int64_t *score_count, void *ws,
+                        size_t ws_bytes, ls_stream_t stream);
 
 /* ------------------------------------------------------------- K2+K3+K4 -
  * Line sort + greedy coverage-alpha selection: replaces the sort of

@@ -55,6 +55,7 @@ SIGNATURES = {
     "ls_head_seed_host": (U64, [U64, I32, I32, I32]),
     "ls_score_lines_workspace": (SZ, [LD, I32]),
     "ls_score_lines": (C.c_int, [LD, I32, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "ls_score_lines_simt": (C.c_int, [LD, I32, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "ls_select_lines_workspace": (SZ, [LD, I32]),
     "ls_select_lines": (C.c_int, [LD, I32, F64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
                                   SZ, P]),
