@@ -18,7 +18,6 @@
 // tcgen05 path replaces the tile product, the reductions are shared.
 
 #include "ls_common.cuh"
-#include "tc_common.cuh"
 
 namespace ls {
 namespace k1 {
@@ -291,216 +290,6 @@ __global__ void total_kernel(const double *v_w, const int32_t *rows, int n_s, in
   }
 }
 
-// ------------------------------------------------------------------------
-// Tensor-core path: one CTA per (head, tile of TC_BM = 128 sampled rows).
-// The sampled q rows are gathered into a 128B-swizzled K-major smem tile, K
-// tiles (128 keys) stream through a cp.async double buffer, S = Qs K^T goes
-// to TMEM (double-buffered, 2 x 128 columns) so the MMA of tile t+1 overlaps
-// the softmax / reductions of tile t. Each of the 128 threads owns one TMEM
-// lane = one sampled row. Pass 1: online (max, sum); pass 2: P in fp32 to
-// shared memory, then the same deterministic fp64 vertical / slash
-// reductions as the CUDA-core path (rows ascending).
-constexpr int TC_BM = 128;
-constexpr int TC_BN = 128;
-constexpr int TC_LDP = TC_BN + 1;  // fp32 P row stride (bank-conflict free rows and columns)
-
-template <int D>
-struct TcSmem {
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + TC_BM * D * 2;
-  static constexpr int OFF_P = OFF_K + 2 * TC_BN * D * 2;
-  static constexpr int OFF_MISC = OFF_P + TC_BM * TC_LDP * 4;
-  static constexpr int TOTAL = OFF_MISC + 2048 + 1024;
-};
-
-__device__ __forceinline__ void zfill16(uint32_t saddr, const void *g, bool ok) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(ok ? 16 : 0) : "memory");
-}
-
-template <int D>
-__global__ void __launch_bounds__(128, 1) score_lines_tc_kernel(Params p) {
-  extern __shared__ unsigned char smem_dyn[];
-  using L = TcSmem<D>;
-  unsigned char *smem =
-      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);  // [2] S buffers
-  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
-  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);     // [128] row positions
-  float *Pf = reinterpret_cast<float *>(smem + L::OFF_P);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int h = blockIdx.y, rt = blockIdx.x;
-  const int r_begin = rt * TC_BM;
-  const int nr = min(TC_BM, p.n_s - r_begin);
-  const int32_t *rows_h = p.rows + static_cast<int64_t>(h) * p.n_s;
-  const uint16_t *qbase = p.q + static_cast<int64_t>(h) * p.q_head_stride;
-  const uint16_t *kbase = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
-  const int64_t part_off = (static_cast<int64_t>(h) * p.n_rt + rt) * p.n_total;
-  double *vpart = p.vpart + part_off;
-  float *vmaxp = p.vmaxp + part_off;
-  double *spart = p.spart + part_off;
-  float *smaxp = p.smaxp + part_off;
-
-  if (warp == 0) tc::tmem_alloc(tmem_sh, 256);
-  if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-  }
-  const int my_lr = tid < nr ? rows_h[r_begin + tid] : 0;
-  gs[tid] = tid < nr ? p.row_offset + my_lr : 0x7fffffff;
-  {  // gather the sampled q rows
-    const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
-#pragma unroll
-    for (int ch = 0; ch < D / 8; ++ch)
-      zfill16(qs + tc::sw128_offset(tid, ch, TC_BM), qbase + static_cast<int64_t>(my_lr) * D + ch * 8, tid < nr);
-    tc::cp_async_commit();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_sh;
-  const int g_first = gs[0];
-  const int g_last = gs[nr - 1];
-  const int my_g = gs[tid];
-  const bool row_ok = tid < nr;
-  for (int i = tid; i <= g_last; i += blockDim.x) {  // exclusive RMW accumulator
-    spart[i] = 0.0;
-    smaxp[i] = 0.f;
-  }
-  const int n_tiles = g_last / TC_BN + 1;
-  const uint32_t q_s = tc::smem_u32(smem + L::OFF_Q);
-  constexpr uint32_t IDESC = tc::make_idesc(TC_BM, TC_BN, false, false);
-  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-
-  auto load_k = [&](int t, int buf) {
-    const uint32_t ks = tc::smem_u32(smem + L::OFF_K + buf * TC_BN * D * 2);
-    const int c = t * TC_BN + tid;
-    const bool ok = c < p.n_total;
-#pragma unroll
-    for (int ch = 0; ch < D / 8; ++ch)
-      zfill16(ks + tc::sw128_offset(tid, ch, TC_BN), kbase + static_cast<int64_t>(ok ? c : 0) * D + ch * 8, ok);
-    tc::cp_async_commit();
-  };
-  auto issue_mma = [&](int buf) {  // S[buf] = Qs K[buf]^T
-    const uint32_t ks = tc::smem_u32(smem + L::OFF_K + buf * TC_BN * D * 2);
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const uint64_t ad = tc::make_desc(q_s + (kk >> 2) * (TC_BM * 128) + (kk & 3) * 32, 16, 1024);
-      const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (TC_BN * 128) + (kk & 3) * 32, 16, 1024);
-      tc::mma_bf16(tmem + buf * 128, ad, bd, IDESC, kk > 0);
-    }
-    tc::mma_commit(&mbar[buf]);
-  };
-
-  float m = -INFINITY, l = 0.f, linv = 0.f;
-  uint32_t ph[2] = {0u, 0u};
-  for (int pass = 0; pass < 2; ++pass) {
-    // prologue: tile 0 loaded and its MMA issued
-    load_k(0, 0);
-    tc::cp_async_wait<0>();
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    if (tid == 0) issue_mma(0);
-    for (int t = 0; t < n_tiles; ++t) {
-      const int buf = t & 1;
-      const int c0 = t * TC_BN;
-      if (t + 1 < n_tiles) load_k(t + 1, buf ^ 1);
-      tc::mbar_wait(&mbar[buf], ph[buf]);
-      ph[buf] ^= 1;
-      tc::fence_after_sync();
-      const int lim = my_g - c0;  // causal: column j valid iff j <= lim
-      if (pass == 0) {
-#pragma unroll
-        for (int cch = 0; cch < 4; ++cch) {
-          float sv[32];
-          tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv);
-          tc::tmem_wait_ld();
-          if (row_ok) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (cch * 32 + j <= lim) {
-                const float s = sv[j] * p.scale_log2;
-                if (s > m) {
-                  l = l * fast_exp2(m - s) + 1.f;
-                  m = s;
-                } else {
-                  l += fast_exp2(s - m);
-                }
-              }
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int cch = 0; cch < 4; ++cch) {
-          float sv[32];
-          tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int jj = cch * 32 + j;
-            Pf[tid * TC_LDP + jj] = (row_ok && jj <= lim) ? fast_exp2(sv[j] * p.scale_log2 - m) * linv : 0.f;
-          }
-        }
-      }
-      // next tile's K landed -> its MMA overlaps this tile's reductions
-      if (t + 1 < n_tiles) tc::cp_async_wait<0>();
-      tc::fence_proxy_async();
-      tc::fence_before_sync();
-      __syncthreads();
-      tc::fence_after_sync();
-      if (t + 1 < n_tiles && tid == 0) issue_mma(buf ^ 1);
-      if (pass == 1) {
-        // verticals: thread per column, rows ascending (prefill.py:141-142)
-        {
-          const int c = c0 + tid;
-          if (c < p.n_total) {
-            double sw = 0.0;
-            float mx = 0.f;
-            for (int r = 0; r < nr; ++r) {
-              const float v = Pf[r * TC_LDP + tid];
-              sw += static_cast<double>(v);
-              mx = fmaxf(mx, v);
-            }
-            vpart[c] = sw;
-            vmaxp[c] = mx;
-          }
-        }
-        // slashes: thread owns diagonal d, rows ascending (prefill.py:149-157)
-        const int d_lo = max(0, g_first - (c0 + TC_BN - 1));
-        const int d_hi = g_last - c0;
-        for (int dd = d_lo + tid; dd <= d_hi; dd += blockDim.x) {
-          const int glo = c0 + dd, ghi = c0 + dd + TC_BN - 1;
-          int r = lower_bound_dev(gs, nr, glo);
-          if (r >= nr || gs[r] > ghi) continue;
-          double sw = spart[dd];
-          float mx = smaxp[dd];
-          for (; r < nr && gs[r] <= ghi; ++r) {
-            const float v = Pf[r * TC_LDP + (gs[r] - dd - c0)];
-            sw += static_cast<double>(v);
-            mx = fmaxf(mx, v);
-          }
-          spart[dd] = sw;
-          smaxp[dd] = mx;
-        }
-        __syncthreads();  // Pf reused by the next tile
-      }
-    }
-    if (pass == 0) {
-      linv = (l > 0.f) ? 1.f / l : 0.f;
-      if (row_ok) {
-        float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + r_begin + tid) * 2;
-        rs[0] = m;
-        rs[1] = linv;
-      }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 256);
-}
-
 inline size_t smem_bytes(int d) {
   int ld = d + 1;
   return static_cast<size_t>(BM * ld + BN * ld + BM * (BN + 1)) * 4 + BM * 16 + 64;
@@ -517,8 +306,15 @@ static size_t score_ws(const ls_layer_desc *L, int32_t n_s, int bm) {
   return per * (8 + 4 + 8 + 4) + 4 * 256 + 4096;
 }
 
+namespace ls {
+size_t score_lines_tc_workspace(const ls_layer_desc *L, int32_t n_s);
+int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
+                   double *v_w, float *v_max, double *s_w, float *s_max, float *row_stats, double *total,
+                   int64_t *score_count, void *ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace ls
+
 extern "C" size_t ls_score_lines_workspace(const ls_layer_desc *L, int32_t n_s) {
-  const size_t a = score_ws(L, n_s, k1::BM), b = score_ws(L, n_s, k1::TC_BM);
+  const size_t a = score_ws(L, n_s, k1::BM), b = score_lines_tc_workspace(L, n_s);
   return a > b ? a : b;
 }
 
@@ -533,7 +329,9 @@ static int score_lines_impl(const ls_layer_desc *L, int32_t n_s, const uint16_t 
              LS_ERR_DIMENSION_MISMATCH, "row_offset must equal n_total - n_new >= 0");
   LS_REQUIRE(ws_bytes >= ls_score_lines_workspace(L, n_s), LS_ERR_WORKSPACE, "score_lines workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int bm = tensor_cores ? k1::TC_BM : k1::BM;
+  if (tensor_cores)
+    return score_lines_tc(L, n_s, q, k, rows, v_w, v_max, s_w, s_max, row_stats, total, score_count, ws, ws_bytes, st);
+  const int bm = k1::BM;
   const int n_rt = ceil_div(n_s, bm);
   Carver c(ws, ws_bytes);
   const size_t per = static_cast<size_t>(L->n_heads) * n_rt * L->n_total;
@@ -556,18 +354,7 @@ static int score_lines_impl(const ls_layer_desc *L, int32_t n_s, const uint16_t 
   p.kv_head_stride = L->kv_head_stride;
   p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
   p.row_stats = row_stats;
-  if (tensor_cores) {
-    if (L->head_dim == 128) {
-      const int smem = k1::TcSmem<128>::TOTAL;
-      LS_CUDA(cudaFuncSetAttribute(k1::score_lines_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k1::score_lines_tc_kernel<128><<<dim3(n_rt, L->n_heads), 128, smem, st>>>(p);
-    } else {
-      const int smem = k1::TcSmem<64>::TOTAL;
-      LS_CUDA(cudaFuncSetAttribute(k1::score_lines_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k1::score_lines_tc_kernel<64><<<dim3(n_rt, L->n_heads), 128, smem, st>>>(p);
-    }
-    LS_LAUNCH_CHECK("score_lines_tc_kernel");
-  } else {
+  {
     const size_t smem = k1::smem_bytes(L->head_dim);
     LS_CUDA(cudaFuncSetAttribute(k1::score_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));

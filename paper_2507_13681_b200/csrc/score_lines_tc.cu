@@ -1,0 +1,476 @@
+// K1 (tensor-core path) -- sampled-row scoring and line sums on tcgen05.
+//
+// Replaces the scoring part of sparsify_head (reference prefill.py:377-390),
+// softmax_rows (tensor_ops.py:24-40) and _line_sums (prefill.py:138-169).
+//
+// Work grid: (key chunk of CHUNK columns, tile of 128 sampled rows, head).
+//   k1_stats   : S = Qs K^T per 128-key tile on tcgen05 (TMEM double-
+//                buffered so tile t+1's MMA overlaps tile t's math), online
+//                (max, sum) per row and chunk -> partial stats.
+//   k1_lines   : combines the chunk stats of its rows in chunk order, then
+//                recomputes S, P = exp2(s - m) / l (fp32) into shared memory
+//                and reduces it: vertical sums (column, rows in order, fp64)
+//                and slash sums (thread owns d = g - c, rows in order, fp64,
+//                accumulated over the chunk in shared memory).
+// Partials of different CTAs are merged with 64-bit integer atomics on a
+// 2^-40 fixed-point scale: integer addition is associative, so the result is
+// bit-identical whatever the CTA schedule (the reference's determinism
+// contract), and the quantisation (<= 2^-41 per partial) is
+// far below the fp32 error of P itself. Maxima use integer atomicMax on the
+// (non-negative) float bits.
+
+#include "ls_common.cuh"
+#include "tc_common.cuh"
+
+namespace ls {
+namespace k1tc {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int CHUNK = 1024;        // key columns per CTA
+constexpr int LDP = BN + 1;        // fp32 P row stride
+constexpr int ACC_CAP = 4096;      // shared slash accumulator (diagonals per chunk)
+constexpr double FIX = 1099511627776.0;  // 2^40
+constexpr double UNFIX = 1.0 / 1099511627776.0;
+
+struct Params {
+  const uint16_t *q;
+  const uint16_t *k;
+  const int32_t *rows;
+  int n_heads, group, n_s, n_total, row_offset, n_rt, n_chunks;
+  int64_t q_head_stride, kv_head_stride;
+  float scale_log2;
+  float2 *pstats;  // [H][n_rt][n_chunks][BM]
+  unsigned long long *vfix, *sfix;  // [H][n_total]
+  unsigned int *vmaxb, *smaxb;      // [H][n_total]
+  float *row_stats;                 // [H][n_s][2]
+};
+
+template <int D>
+struct StatsSmem {
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = BM * D * 2;
+  static constexpr int OFF_MISC = OFF_K + 2 * BN * D * 2;
+  static constexpr int TOTAL = OFF_MISC + 1024 + 1024;
+};
+
+template <int D>
+struct LinesSmem {
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = BM * D * 2;
+  static constexpr int OFF_P = OFF_K + 2 * BN * D * 2;
+  static constexpr int OFF_ACC = OFF_P + BM * LDP * 4;         // double[ACC_CAP]
+  static constexpr int OFF_ACCM = OFF_ACC + ACC_CAP * 8;       // float[ACC_CAP]
+  static constexpr int OFF_MISC = OFF_ACCM + ACC_CAP * 4;
+  static constexpr int TOTAL = OFF_MISC + 4096 + 1024;
+};
+
+__device__ __forceinline__ void zfill16(uint32_t saddr, const void *g, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(ok ? 16 : 0) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long to_fix(double x) {
+  return static_cast<unsigned long long>(__double2ll_rn(x * FIX));
+}
+
+// shared prologue: TMEM, barriers, row positions, gathered Q tile
+template <int D>
+__device__ __forceinline__ void setup(const Params &p, unsigned char *smem, int off_misc, int h, int rt, int &nr,
+                                      int *gs, uint64_t *mbar, uint32_t *tmem_sh) {
+  const int tid = threadIdx.x;
+  const int r_begin = rt * BM;
+  nr = min(BM, p.n_s - r_begin);
+  if ((tid >> 5) == 0) tc::tmem_alloc(tmem_sh, 256);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+  }
+  const int32_t *rows_h = p.rows + static_cast<int64_t>(h) * p.n_s;
+  if (tid < BM) {
+    const int lr = tid < nr ? rows_h[r_begin + tid] : 0;
+    gs[tid] = tid < nr ? p.row_offset + lr : 0x7fffffff;
+    const uint16_t *qrow = p.q + static_cast<int64_t>(h) * p.q_head_stride + static_cast<int64_t>(lr) * D;
+    const uint32_t qs = tc::smem_u32(smem);
+#pragma unroll
+    for (int ch = 0; ch < D / 8; ++ch) zfill16(qs + tc::sw128_offset(tid, ch, BM), qrow + ch * 8, tid < nr);
+  }
+  tc::cp_async_commit();
+  (void)off_misc;
+}
+
+template <int D>
+__device__ __forceinline__ void load_k(const Params &p, unsigned char *smem, int off_k, const uint16_t *kbase, int c0,
+                                       int buf) {
+  // 128 key rows; threads >= 128 help when blockDim is 256
+  const uint32_t ks = tc::smem_u32(smem + off_k + buf * BN * D * 2);
+  constexpr int CH = D / 8;
+  for (int i = threadIdx.x; i < BN * CH; i += blockDim.x) {
+    const int r = i / CH, ch = i % CH;
+    const int c = c0 + r;
+    const bool ok = c < p.n_total;
+    zfill16(ks + tc::sw128_offset(r, ch, BN), kbase + static_cast<int64_t>(ok ? c : 0) * D + ch * 8, ok);
+  }
+  tc::cp_async_commit();
+}
+
+template <int D>
+__device__ __forceinline__ void issue_s(unsigned char *smem, int off_k, uint32_t tmem, int buf, uint64_t *mbar) {
+  constexpr uint32_t IDESC = tc::make_idesc(BM, BN, false, false);
+  const uint32_t qs = tc::smem_u32(smem);
+  const uint32_t ks = tc::smem_u32(smem + off_k + buf * BN * D * 2);
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    const uint64_t ad = tc::make_desc(qs + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
+    const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+    tc::mma_bf16(tmem + buf * 128, ad, bd, IDESC, kk > 0);
+  }
+  tc::mma_commit(&mbar[buf]);
+}
+
+__device__ __forceinline__ void cta_sync_tc() {
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+// ------------------------------------------------------------- pass 1
+template <int D>
+__global__ void __launch_bounds__(128) k1_stats_kernel(Params p) {
+  extern __shared__ unsigned char smem_dyn[];
+  using L = StatsSmem<D>;
+  unsigned char *smem =
+      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
+  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);
+  const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  float2 *ps = p.pstats + ((static_cast<int64_t>(h) * p.n_rt + rt) * p.n_chunks + ck) * BM;
+  // chunk bounds against this row tile's causal extent
+  const int r_last = min(p.n_s, (rt + 1) * BM) - 1;
+  const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
+  const int c_begin = ck * CHUNK;
+  if (c_begin > g_last) {
+    ps[tid] = make_float2(-INFINITY, 0.f);
+    return;
+  }
+  const int c_end = min(c_begin + CHUNK, g_last + 1);
+  int nr;
+  setup<D>(p, smem, L::OFF_MISC, h, rt, nr, gs, mbar, tmem_sh);
+  const uint16_t *kbase = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
+  const int n_tiles = (c_end - c_begin + BN - 1) / BN;
+  load_k<D>(p, smem, L::OFF_K, kbase, c_begin, 0);
+  tc::cp_async_wait<0>();
+  cta_sync_tc();
+  const uint32_t tmem = *tmem_sh;
+  if (tid == 0) issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+  const int my_g = gs[tid];
+  const bool row_ok = tid < nr;
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  float m = -INFINITY, l = 0.f;
+  uint32_t ph0 = 0, ph1 = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const int buf = t & 1;
+    const int c0 = c_begin + t * BN;
+    if (t + 1 < n_tiles) load_k<D>(p, smem, L::OFF_K, kbase, c0 + BN, buf ^ 1);
+    tc::mbar_wait(&mbar[buf], buf ? ph1 : ph0);
+    if (buf) ph1 ^= 1; else ph0 ^= 1;
+    tc::fence_after_sync();
+    const int lim = min(my_g, c_end - 1) - c0;
+#pragma unroll
+    for (int cch = 0; cch < 4; ++cch) {
+      float sv[32];
+      tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv);
+      tc::tmem_wait_ld();
+      if (row_ok) {
+        float tm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (cch * 32 + j <= lim) tm = fmaxf(tm, sv[j]);
+        if (tm != -INFINITY) {
+          const float mn = fmaxf(m, tm * p.scale_log2);
+          float acc = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (cch * 32 + j <= lim) acc += fast_exp2(sv[j] * p.scale_log2 - mn);
+          l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
+          m = mn;
+        }
+      }
+    }
+    if (t + 1 < n_tiles) tc::cp_async_wait<0>();
+    cta_sync_tc();
+    if (t + 1 < n_tiles && tid == 0) issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+  }
+  ps[tid] = make_float2(row_ok ? m : -INFINITY, row_ok ? l : 0.f);
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
+// ------------------------------------------------------------- pass 2
+template <int D>
+__global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
+  extern __shared__ unsigned char smem_dyn[];
+  using L = LinesSmem<D>;
+  unsigned char *smem =
+      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
+  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);              // [128]
+  float *m_sh = reinterpret_cast<float *>(smem + L::OFF_MISC + 64 + 512);  // [128]
+  float *li_sh = m_sh + BM;                                                 // [128]
+  double *colp = reinterpret_cast<double *>(smem + L::OFF_MISC + 2048);     // [2][128]
+  float *colm = reinterpret_cast<float *>(smem + L::OFF_MISC + 2048 + 2048);  // [2][128]
+  float *Pf = reinterpret_cast<float *>(smem + L::OFF_P);
+  double *acc = reinterpret_cast<double *>(smem + L::OFF_ACC);
+  float *accm = reinterpret_cast<float *>(smem + L::OFF_ACCM);
+  const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int r_last = min(p.n_s, (rt + 1) * BM) - 1;
+  const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
+  const int c_begin = ck * CHUNK;
+  if (c_begin > g_last) return;
+  const int c_end = min(c_begin + CHUNK, g_last + 1);
+  int nr;
+  setup<D>(p, smem, L::OFF_MISC, h, rt, nr, gs, mbar, tmem_sh);
+  const uint16_t *kbase = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
+  // combine the chunk statistics of this CTA's rows (chunk order: deterministic)
+  if (tid < BM) {
+    float m = -INFINITY, l = 0.f;
+    const float2 *ps = p.pstats + (static_cast<int64_t>(h) * p.n_rt + rt) * p.n_chunks * BM + tid;
+    for (int c = 0; c < p.n_chunks; ++c) {
+      const float2 v = ps[static_cast<int64_t>(c) * BM];
+      if (v.x == -INFINITY) continue;
+      const float mn = fmaxf(m, v.x);
+      l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
+      m = mn;
+    }
+    m_sh[tid] = m;
+    li_sh[tid] = l > 0.f ? 1.f / l : 0.f;
+    if (ck == 0 && tid < nr) {
+      float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + rt * BM + tid) * 2;
+      rs[0] = m;
+      rs[1] = l > 0.f ? 1.f / l : 0.f;
+    }
+  }
+  const int n_tiles = (c_end - c_begin + BN - 1) / BN;
+  load_k<D>(p, smem, L::OFF_K, kbase, c_begin, 0);
+  tc::cp_async_wait<0>();
+  cta_sync_tc();
+  const uint32_t tmem = *tmem_sh;
+  if (tid == 0) issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+  const int g_first = gs[0];
+  const int g_hi = gs[nr - 1];
+  // slash accumulator window of the chunk: d in [d_base, d_base + width)
+  const int d_base = max(0, g_first - (c_end - 1));
+  const int width = g_hi - c_begin - d_base + 1;
+  const bool smem_acc = width <= ACC_CAP;
+  if (smem_acc)
+    for (int i = tid; i < width; i += blockDim.x) {
+      acc[i] = 0.0;
+      accm[i] = 0.f;
+    }
+  // TMEM reads: warp w -> lanes 32*(w%4), columns [64*(w/4), +64)
+  const int row = (warp & 3) * 32 + (tid & 31);
+  const int col_half = warp >> 2;
+  const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  uint32_t ph0 = 0, ph1 = 0;
+  unsigned long long *sfix = p.sfix + static_cast<int64_t>(h) * p.n_total;
+  unsigned int *smaxb = p.smaxb + static_cast<int64_t>(h) * p.n_total;
+  for (int t = 0; t < n_tiles; ++t) {
+    const int buf = t & 1;
+    const int c0 = c_begin + t * BN;
+    if (t + 1 < n_tiles) load_k<D>(p, smem, L::OFF_K, kbase, c0 + BN, buf ^ 1);
+    tc::mbar_wait(&mbar[buf], buf ? ph1 : ph0);
+    if (buf) ph1 ^= 1; else ph0 ^= 1;
+    tc::fence_after_sync();
+    {
+      const int g = gs[row];
+      const bool ok = row < nr;
+      const int lim = min(g, c_end - 1) - c0;
+      const float mr = m_sh[row], li = li_sh[row];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int cbase = col_half * 64 + half * 32;
+        float sv[32];
+        tc::tmem_ld32(tmem + buf * 128 + lane_base + cbase, sv);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          Pf[row * LDP + cbase + j] = (ok && cbase + j <= lim) ? fast_exp2(sv[j] * p.scale_log2 - mr) * li : 0.f;
+      }
+    }
+    if (t + 1 < n_tiles) tc::cp_async_wait<0>();
+    cta_sync_tc();
+    if (t + 1 < n_tiles && tid == 0) issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+    // vertical partials: two threads per column (row halves), combined in order
+    {
+      const int j = tid & (BN - 1), hf = tid >> 7;
+      double sw = 0.0;
+      float mx = 0.f;
+      const int r0 = hf * 64, r1 = min(nr, r0 + 64);
+      for (int r = r0; r < r1; ++r) {
+        const float v = Pf[r * LDP + j];
+        sw += static_cast<double>(v);
+        mx = fmaxf(mx, v);
+      }
+      colp[hf * BN + j] = sw;
+      colm[hf * BN + j] = mx;
+    }
+    // slash partials: thread owns diagonal d, rows ascending
+    {
+      // cells of this chunk have d >= d_base (columns beyond c_end are not ours)
+      const int d_lo = max(d_base, g_first - (c0 + BN - 1));
+      const int d_hi = g_hi - c0;
+      for (int dd = d_lo + tid; dd <= d_hi; dd += blockDim.x) {
+        const int glo = c0 + dd, ghi = c0 + dd + BN - 1;
+        int r = lower_bound_dev(gs, nr, glo);
+        if (r >= nr || gs[r] > ghi) continue;
+        double sw = smem_acc ? acc[dd - d_base] : 0.0;
+        float mx = smem_acc ? accm[dd - d_base] : 0.f;
+        for (; r < nr && gs[r] <= ghi; ++r) {
+          const float v = Pf[r * LDP + (gs[r] - dd - c0)];
+          sw += static_cast<double>(v);
+          mx = fmaxf(mx, v);
+        }
+        if (smem_acc) {
+          acc[dd - d_base] = sw;
+          accm[dd - d_base] = mx;
+        } else if (sw > 0.0) {
+          atomicAdd(sfix + dd, to_fix(sw));
+          atomicMax(smaxb + dd, __float_as_uint(mx));
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < BN) {
+      const int c = c0 + tid;
+      if (c < c_end) {
+        const double sw = colp[tid] + colp[BN + tid];
+        const float mx = fmaxf(colm[tid], colm[BN + tid]);
+        if (sw > 0.0) atomicAdd(p.vfix + static_cast<int64_t>(h) * p.n_total + c, to_fix(sw));
+        if (mx > 0.f) atomicMax(p.vmaxb + static_cast<int64_t>(h) * p.n_total + c, __float_as_uint(mx));
+      }
+    }
+    __syncthreads();  // Pf / colp reused by the next tile
+  }
+  if (smem_acc)
+    for (int i = tid; i < width; i += blockDim.x) {
+      if (acc[i] > 0.0) atomicAdd(sfix + d_base + i, to_fix(acc[i]));
+      if (accm[i] > 0.f) atomicMax(smaxb + d_base + i, __float_as_uint(accm[i]));
+    }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
+// fixed point -> fp64 line weights; total = exact integer sum of the verticals
+__global__ void k1_finish_kernel(const unsigned long long *vfix, const unsigned int *vmaxb,
+                                 const unsigned long long *sfix, const unsigned int *smaxb, const int32_t *rows,
+                                 int n_s, int n_total, int row_offset, double *v_w, float *v_max, double *s_w,
+                                 float *s_max, double *total, int64_t *score_count) {
+  __shared__ unsigned long long red[32];
+  __shared__ long long redc[32];
+  const int h = blockIdx.x;
+  unsigned long long sum = 0;
+  long long cnt = 0;
+  for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
+    const int64_t o = static_cast<int64_t>(h) * n_total + i;
+    const unsigned long long vf = vfix[o];
+    sum += vf;
+    v_w[o] = static_cast<double>(vf) * UNFIX;
+    v_max[o] = __uint_as_float(vmaxb[o]);
+    s_w[o] = static_cast<double>(sfix[o]) * UNFIX;
+    s_max[o] = __uint_as_float(smaxb[o]);
+  }
+  for (int r = threadIdx.x; r < n_s; r += blockDim.x) {
+    const long long g = row_offset + rows[static_cast<int64_t>(h) * n_s + r];
+    cnt += min(g, static_cast<long long>(n_total - 1)) + 1;  // prefill.py:386-389
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = sum;
+    redc[threadIdx.x >> 5] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    long long c = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      s += red[i];
+      c += redc[i];
+    }
+    total[h] = static_cast<double>(s) * UNFIX;
+    score_count[h] = c;
+  }
+}
+
+}  // namespace k1tc
+
+size_t score_lines_tc_workspace(const ls_layer_desc *L, int32_t n_s) {
+  const size_t n_rt = (n_s + k1tc::BM - 1) / k1tc::BM;
+  const size_t n_ch = (L->n_total + k1tc::CHUNK - 1) / k1tc::CHUNK;
+  const size_t H = L->n_heads;
+  return H * n_rt * n_ch * k1tc::BM * sizeof(float2) + H * L->n_total * (8 + 8 + 4 + 4) + 6 * 256 + 4096;
+}
+
+int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
+                   double *v_w, float *v_max, double *s_w, float *s_max, float *row_stats, double *total,
+                   int64_t *score_count, void *ws, size_t ws_bytes, cudaStream_t st) {
+  LS_REQUIRE(ws_bytes >= score_lines_tc_workspace(L, n_s), LS_ERR_WORKSPACE, "score_lines workspace too small");
+  k1tc::Params p;
+  p.q = q;
+  p.k = k;
+  p.rows = rows;
+  p.n_heads = L->n_heads;
+  p.group = L->n_heads / L->n_kv_heads;
+  p.n_s = n_s;
+  p.n_total = L->n_total;
+  p.row_offset = L->row_offset;
+  p.n_rt = (n_s + k1tc::BM - 1) / k1tc::BM;
+  p.n_chunks = (L->n_total + k1tc::CHUNK - 1) / k1tc::CHUNK;
+  p.q_head_stride = L->q_head_stride;
+  p.kv_head_stride = L->kv_head_stride;
+  p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
+  p.row_stats = row_stats;
+  Carver c(ws, ws_bytes);
+  const size_t H = L->n_heads;
+  p.pstats = c.take<float2>(H * p.n_rt * p.n_chunks * k1tc::BM);
+  p.vfix = c.take<unsigned long long>(H * L->n_total);
+  p.sfix = c.take<unsigned long long>(H * L->n_total);
+  p.vmaxb = c.take<unsigned int>(H * L->n_total);
+  p.smaxb = c.take<unsigned int>(H * L->n_total);
+  LS_CUDA(cudaMemsetAsync(p.vfix, 0, H * L->n_total * 8, st));
+  LS_CUDA(cudaMemsetAsync(p.sfix, 0, H * L->n_total * 8, st));
+  LS_CUDA(cudaMemsetAsync(p.vmaxb, 0, H * L->n_total * 4, st));
+  LS_CUDA(cudaMemsetAsync(p.smaxb, 0, H * L->n_total * 4, st));
+  dim3 grid(p.n_chunks, p.n_rt, L->n_heads);
+  if (L->head_dim == 128) {
+    const int s1 = k1tc::StatsSmem<128>::TOTAL, s2 = k1tc::LinesSmem<128>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+    k1tc::k1_stats_kernel<128><<<grid, 128, s1, st>>>(p);
+    LS_LAUNCH_CHECK("k1_stats_kernel");
+    k1tc::k1_lines_kernel<128><<<grid, 256, s2, st>>>(p);
+  } else {
+    const int s1 = k1tc::StatsSmem<64>::TOTAL, s2 = k1tc::LinesSmem<64>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+    k1tc::k1_stats_kernel<64><<<grid, 128, s1, st>>>(p);
+    LS_LAUNCH_CHECK("k1_stats_kernel");
+    k1tc::k1_lines_kernel<64><<<grid, 256, s2, st>>>(p);
+  }
+  LS_LAUNCH_CHECK("k1_lines_kernel");
+  k1tc::k1_finish_kernel<<<L->n_heads, 512, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
+                                                     L->row_offset, v_w, v_max, s_w, s_max, total, score_count);
+  LS_LAUNCH_CHECK("k1_finish_kernel");
+  return LS_OK;
+}
+
+}  // namespace ls
