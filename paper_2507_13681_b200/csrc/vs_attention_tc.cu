@@ -26,7 +26,7 @@ namespace k5tc {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int THREADS = 128;
+constexpr int THREADS = 256;  // two warpgroups split S / O columns of the same 128 rows
 constexpr int MAX_KB = 2048;  // key blocks per head (n_total <= 262144)
 
 struct Params {
@@ -54,7 +54,7 @@ struct Smem {
   static constexpr int OFF_V0 = OFF_K0 + 2 * KV_BYTES;
   static constexpr int OFF_P = OFF_V0 + 2 * KV_BYTES;
   static constexpr int OFF_MISC = OFF_P + P_BYTES;
-  static constexpr int MISC_BYTES = 1024 + MAX_KB * 2 + 2 * BN * 4 + 64;
+  static constexpr int MISC_BYTES = 1536 + MAX_KB * 2 + 2 * BN * 4 + BM * 4 + 64;
   static constexpr int TOTAL = OFF_MISC + MISC_BYTES + 1024;  // + alignment slack
 };
 
@@ -77,17 +77,22 @@ template <int D>
 __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = Smem<D>;
+  constexpr int DH = D / 2;  // O columns per warpgroup
   unsigned char *smem =
       reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   unsigned char *misc = smem + L::OFF_MISC;
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(misc);          // [2]
-  uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(misc + 16);
-  int *sh_int = reinterpret_cast<int *>(misc + 32);              // scratch ints [32]
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(misc);          // [0,1] S buffers, [2] O
+  uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(misc + 32);
+  int *sh_int = reinterpret_cast<int *>(misc + 64);              // scratch ints [32]
   uint32_t *kb_bits = reinterpret_cast<uint32_t *>(misc + 256);  // [64] bitmap of touched key blocks
-  int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 1024);
-  int *gcols = reinterpret_cast<int *>(misc + 1024 + MAX_KB * 2);  // [2][BN] gathered columns per buffer
+  float *pmax = reinterpret_cast<float *>(misc + 512);           // [2][128] partial row maxima
+  int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 1536);
+  int *gcols = reinterpret_cast<int *>(misc + 1536 + MAX_KB * 2);  // [2][BN] columns per buffer
+  float *lsum_sh = reinterpret_cast<float *>(misc + 1536 + MAX_KB * 2 + 2 * BN * 4);  // [128]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wg = warp >> 2;          // column half of S / O handled by this thread
+  const int row = (warp & 3) * 32 + lane;  // TMEM lane = q row
   const int h = blockIdx.y, qt = blockIdx.x;
   const int r0 = qt * BM;
   const int nr = min(BM, p.n_new - r0);
@@ -101,22 +106,21 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   const uint32_t *rsbits = p.rsbits + static_cast<int64_t>(h) * (p.words + 8);
   int32_t *gl = p.gather_ws + (static_cast<int64_t>(h) * p.n_qtiles + qt) * p.n_total;
 
-  // ---- TMEM allocation (warp 0), barriers
-  if (warp == 0) tc::tmem_alloc(tmem_base_sh, 256);
+  // ---- TMEM (S double buffer + O tile), barriers, Q tile
+  if (warp == 0) tc::tmem_alloc(tmem_base_sh, 512);
   if (tid == 0) {
     tc::mbar_init(&mbar[0], 1);
     tc::mbar_init(&mbar[1], 1);
+    tc::mbar_init(&mbar[2], 1);
   }
   for (int i = tid; i < 64; i += THREADS) kb_bits[i] = 0u;
-  // ---- Q tile (K-major SW128) via cp.async
   {
     const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
     constexpr int CH = D / 8;
     for (int i = tid; i < BM * CH; i += THREADS) {
       const int r = i / CH, c = i % CH;
       const bool ok = r < nr;
-      cp_async16_zfill(qs + tc::sw128_offset(r, c, BM), qb + static_cast<int64_t>(ok ? r0 + r : 0) * D + c * 8,
-                           ok);
+      cp_async16_zfill(qs + tc::sw128_offset(r, c, BM), qb + static_cast<int64_t>(ok ? r0 + r : 0) * D + c * 8, ok);
     }
     tc::cp_async_commit();
   }
@@ -124,8 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_base_sh;
-  const uint32_t tmem_s = tmem;        // columns [0, 128)
-  const uint32_t tmem_o = tmem + 128;  // columns [128, 128 + D)
+  const uint32_t tmem_o = tmem + 256;  // columns [256, 256 + D)
 
   // ---- tile list: touched key blocks, then gathered verticals
   const int n_kb = g_hi / BN + 1;
@@ -156,21 +159,17 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
     }
     sh_int[0] = n;
   }
-  // gathered verticals (ascending): V entries <= g_hi whose block is untouched
-  int n_g = 0;
+  int n_g = 0;  // gathered verticals (ascending): V entries <= g_hi whose block is untouched
   if (!p.dense && n_vt > 0) {
-    int v_end = 0;
-    {
-      int lo = 0, hi = n_vt;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (V[mid] <= g_hi)
-          lo = mid + 1;
-        else
-          hi = mid;
-      }
-      v_end = lo;
+    int lo = 0, hi = n_vt;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (V[mid] <= g_hi)
+        lo = mid + 1;
+      else
+        hi = mid;
     }
+    const int v_end = lo;
     for (int base = 0; base < v_end; base += THREADS) {
       const int i = base + tid;
       const int c = i < v_end ? V[i] : 0;
@@ -179,9 +178,11 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
       __syncthreads();
       if (lane == 0) sh_int[8 + warp] = __popc(ball);
       __syncthreads();
-      int before = 0;
-      for (int w = 0; w < warp; ++w) before += sh_int[8 + w];
-      const int tot = sh_int[8] + sh_int[9] + sh_int[10] + sh_int[11];
+      int before = 0, tot = 0;
+      for (int w = 0; w < THREADS / 32; ++w) {
+        if (w < warp) before += sh_int[8 + w];
+        tot += sh_int[8 + w];
+      }
       if (take) gl[n_g + before + __popc(ball & ((1u << lane) - 1u))] = c;
       n_g += tot;
     }
@@ -190,98 +191,89 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   const int n_dense = sh_int[0];
   const int n_tiles = n_dense + (n_g + BN - 1) / BN;
 
-  // ---- per-thread row state (thread = TMEM lane = q row)
-  const int row = tid;
   const int my_g = g0 + row;
   const bool row_ok = row < nr;
   float m = -INFINITY, l = 0.f;
-  float o[D];
+  float o[DH];
 #pragma unroll
-  for (int i = 0; i < D; ++i) o[i] = 0.f;
+  for (int i = 0; i < DH; ++i) o[i] = 0.f;
   long long my_cells = 0;
 
   constexpr uint32_t IDESC_S = tc::make_idesc(BM, BN, false, false);
   constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, false, true);
   const uint32_t q_s = tc::smem_u32(smem + L::OFF_Q);
   const uint32_t p_s = tc::smem_u32(smem + L::OFF_P);
+  const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
 
+  // K / V rows of tile i into buffer `buf` (two threads per key row: K and V)
   auto issue_load = [&](int i, int buf) {
-    const uint32_t ks = tc::smem_u32(smem + L::OFF_K0 + buf * L::KV_BYTES);
-    const uint32_t vs = tc::smem_u32(smem + L::OFF_V0 + buf * L::KV_BYTES);
-    int c;  // key of row `tid` of the tile
+    const int r = tid & (BN - 1);
+    const bool is_v = tid >= BN;
+    int c;
     bool ok;
     if (i < n_dense) {
-      c = dense_list[i] * BN + tid;
+      c = dense_list[i] * BN + r;
       ok = c < p.n_total;
     } else {
-      const int j = (i - n_dense) * BN + tid;
+      const int j = (i - n_dense) * BN + r;
       ok = j < n_g;
       c = ok ? gl[j] : 0x7fffffff;
     }
-    gcols[buf * BN + tid] = c;
+    if (!is_v) gcols[buf * BN + r] = c;
     const int cc = ok ? c : 0;
+    const uint32_t dst = tc::smem_u32(smem + (is_v ? L::OFF_V0 : L::OFF_K0) + buf * L::KV_BYTES);
+    const uint16_t *src = (is_v ? vb : kb) + static_cast<int64_t>(cc) * D;
     constexpr int CH = D / 8;
-#pragma unroll 4
-    for (int ch = 0; ch < CH; ++ch) {
-      const uint32_t off = tc::sw128_offset(tid, ch, BN);
-      cp_async16_zfill(ks + off, kb + static_cast<int64_t>(cc) * D + ch * 8, ok);
-      cp_async16_zfill(vs + off, vb + static_cast<int64_t>(cc) * D + ch * 8, ok);
-    }
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch) cp_async16_zfill(dst + tc::sw128_offset(r, ch, BN), src + ch * 8, ok);
     tc::cp_async_commit();
   };
-
-  if (n_tiles > 0) issue_load(0, 0);
-  uint32_t ph_s = 0, ph_o = 0;
-  for (int i = 0; i < n_tiles; ++i) {
-    const int buf = i & 1;
-    if (i + 1 < n_tiles) {
-      issue_load(i + 1, buf ^ 1);
-      tc::cp_async_wait<1>();
-    } else {
-      tc::cp_async_wait<0>();
+  auto issue_s = [&](int buf) {  // S[buf] = Q K[buf]^T (thread 0)
+    const uint32_t ks = tc::smem_u32(smem + L::OFF_K0 + buf * L::KV_BYTES);
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint64_t ad = tc::make_desc(q_s + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
+      const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+      tc::mma_bf16(tmem + buf * 128, ad, bd, IDESC_S, kk > 0);
     }
+    tc::mma_commit(&mbar[buf]);
+  };
+
+  uint32_t ph_s0 = 0, ph_s1 = 0, ph_o = 0;
+  if (n_tiles > 0) {
+    issue_load(0, 0);
+    tc::cp_async_wait<0>();
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    // S = Q K^T
-    if (tid == 0) {
-      const uint32_t ks = tc::smem_u32(smem + L::OFF_K0 + buf * L::KV_BYTES);
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t koff = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-        const uint64_t ad = tc::make_desc(q_s + koff, 16, 1024);
-        const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
-        tc::mma_bf16(tmem_s, ad, bd, IDESC_S, kk > 0);
-      }
-      tc::mma_commit(&mbar[0]);
-    }
-    // mask of this row for this tile (overlaps the MMA)
+    if (tid == 0) issue_s(0);
+    if (n_tiles > 1) issue_load(1, 1);
+  }
+  for (int i = 0; i < n_tiles; ++i) {
+    const int buf = i & 1;
+    // ---- mask of (row, this thread's 64 columns) -- overlaps the S MMA
     const bool gathered = i >= n_dense;
-    uint32_t mk[4];
+    uint32_t mk[2];
     if (!row_ok) {
-      mk[0] = mk[1] = mk[2] = mk[3] = 0u;
+      mk[0] = mk[1] = 0u;
     } else if (!gathered) {
-      const int c0 = dense_list[i] * BN;
-      const int lim = my_g - c0;  // columns j <= lim are causal
+      const int c0 = dense_list[i] * BN + wg * 64;
+      const int lim = my_g - c0;
       if (p.dense) {
-        mk[0] = mk[1] = mk[2] = mk[3] = 0xffffffffu;
+        mk[0] = mk[1] = 0xffffffffu;
       } else {
-        uint32_t vw[4], sw[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) vw[t] = (c0 / 32 + t < p.words) ? __ldg(vbits + c0 / 32 + t) : 0u;
+        uint32_t sw[4];
         bit_window(rsbits, p.n_total - 1 - my_g + c0, sw);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) mk[t] = vw[t] | sw[t];
+        for (int t = 0; t < 2; ++t) mk[t] = ((c0 / 32 + t < p.words) ? __ldg(vbits + c0 / 32 + t) : 0u) | sw[t];
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int hi = lim - 32 * t;  // bits [0, hi] valid in word t
-        const uint32_t cm = hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u));
-        mk[t] &= cm;
+      for (int t = 0; t < 2; ++t) {
+        const int hi = lim - 32 * t;
+        mk[t] &= hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u));
       }
     } else {
-      // gathered columns ascending: causal prefix
       const int *gc = gcols + buf * BN;
       int lo = 0, hi = BN;
       while (lo < hi) {
@@ -292,59 +284,65 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
           hi = mid;
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int nb = lo - 32 * t;
+      for (int t = 0; t < 2; ++t) {
+        const int nb = lo - wg * 64 - 32 * t;
         mk[t] = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
       }
     }
-    my_cells += __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
-
-    tc::mbar_wait(&mbar[0], ph_s);
-    ph_s ^= 1;
+    my_cells += __popc(mk[0]) + __popc(mk[1]);
+    // ---- S ready
+    if (buf) {
+      tc::mbar_wait(&mbar[1], ph_s1);
+      ph_s1 ^= 1;
+    } else {
+      tc::mbar_wait(&mbar[0], ph_s0);
+      ph_s0 ^= 1;
+    }
     tc::fence_after_sync();
-    // pass 1: masked row max
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t s_addr = tmem + buf * 128 + lane_base + wg * 64;
     float tmax = -INFINITY;
 #pragma unroll
-    for (int cch = 0; cch < 4; ++cch) {
+    for (int cch = 0; cch < 2; ++cch) {
       float sv[32];
-      tc::tmem_ld32(tmem_s + lane_base + cch * 32, sv);
+      tc::tmem_ld32(s_addr + cch * 32, sv);
       tc::tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if ((mk[cch] >> j) & 1u) tmax = fmaxf(tmax, sv[j] * p.scale_log2);
+      for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, ((mk[cch] >> j) & 1u) ? sv[j] : -INFINITY);
     }
-    const float m_new = fmaxf(m, tmax);
+    pmax[wg * BM + row] = tmax;
+    __syncthreads();
+    const float tm = fmaxf(pmax[row], pmax[BM + row]);
+    const float m_new = fmaxf(m, tm == -INFINITY ? -INFINITY : tm * p.scale_log2);
     const float corr = (m_new == -INFINITY) ? 1.f : fast_exp2(m - m_new);
-    // pass 2: P = exp2(s - m_new) -> bf16 smem (K-major SW128), row sum
     float lsum = 0.f;
 #pragma unroll
-    for (int cch = 0; cch < 4; ++cch) {
+    for (int cch = 0; cch < 2; ++cch) {
       float sv[32];
-      tc::tmem_ld32(tmem_s + lane_base + cch * 32, sv);
+      tc::tmem_ld32(s_addr + cch * 32, sv);
       tc::tmem_wait_ld();
       uint32_t pk[16];
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(sv[j] * p.scale_log2 - m_new) : 0.f;
-        const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(sv[j + 1] * p.scale_log2 - m_new) : 0.f;
+        const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(fmaf(sv[j], p.scale_log2, -m_new)) : 0.f;
+        const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[j + 1], p.scale_log2, -m_new)) : 0.f;
         lsum += a + b;
         pk[j >> 1] = tc::pack_bf16(a, b);
       }
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
-        const int chunk = cch * 4 + q4;  // 16-byte chunk index along keys
-        uint4 val = make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-        *reinterpret_cast<uint4 *>(smem + L::OFF_P + tc::sw128_offset(row, chunk, BM)) = val;
+        const int chunk = wg * 8 + cch * 4 + q4;  // 16-byte chunk along keys
+        *reinterpret_cast<uint4 *>(smem + L::OFF_P + tc::sw128_offset(row, chunk, BM)) =
+            make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
       }
     }
     l = l * corr + lsum;
     m = m_new;
+    // next tile's K/V must have landed before its S MMA is issued
+    if (i + 1 < n_tiles) tc::cp_async_wait<0>();
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    // O_tile = P V
     if (tid == 0) {
       const uint32_t vs = tc::smem_u32(smem + L::OFF_V0 + buf * L::KV_BYTES);
 #pragma unroll
@@ -353,51 +351,62 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
         const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
         tc::mma_bf16(tmem_o, ad, bd, IDESC_O, kk > 0);
       }
-      tc::mma_commit(&mbar[1]);
+      tc::mma_commit(&mbar[2]);
+      if (i + 1 < n_tiles) issue_s(buf ^ 1);  // queued behind PV: overlaps the O update below
     }
-    tc::mbar_wait(&mbar[1], ph_o);
+    tc::mbar_wait(&mbar[2], ph_o);
     ph_o ^= 1;
     tc::fence_after_sync();
 #pragma unroll
-    for (int cch = 0; cch < D / 32; ++cch) {
+    for (int cch = 0; cch < DH / 32; ++cch) {
       float ov[32];
-      tc::tmem_ld32(tmem_o + lane_base + cch * 32, ov);
+      tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
       tc::tmem_wait_ld();
 #pragma unroll
       for (int j = 0; j < 32; ++j) o[cch * 32 + j] = fmaf(o[cch * 32 + j], corr, ov[j]);
     }
     tc::fence_before_sync();
+    // K/V buffer `buf` is free (S(i) and PV(i) done): prefetch tile i + 2
+    if (i + 2 < n_tiles) issue_load(i + 2, buf);
   }
-
   tc::cp_async_wait<0>();
-  // ---- epilogue
+
+  // ---- epilogue: l = sum of both halves
+  lsum_sh[row] = 0.f;
+  __syncthreads();
+  if (wg == 1) lsum_sh[row] = l;
+  __syncthreads();
+  const float l_tot = l + (wg == 0 ? lsum_sh[row] : 0.f);
+  __syncthreads();
+  if (wg == 0) lsum_sh[row] = l_tot;
+  __syncthreads();
+  const float l_all = lsum_sh[row];
   if (row_ok) {
-    const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * D;
-    if (l > 0.f) {
-      const float inv = 1.f / l;
+    const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * D + wg * DH;
+    if (l_all > 0.f) {
+      const float inv = 1.f / l_all;
       if (p.out_bf16) {
         uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + orow;
 #pragma unroll
-        for (int j = 0; j < D; j += 8) {
-          uint4 val = make_uint4(tc::pack_bf16(o[j] * inv, o[j + 1] * inv), tc::pack_bf16(o[j + 2] * inv, o[j + 3] * inv),
-                                 tc::pack_bf16(o[j + 4] * inv, o[j + 5] * inv), tc::pack_bf16(o[j + 6] * inv, o[j + 7] * inv));
-          *reinterpret_cast<uint4 *>(dst + j) = val;
-        }
+        for (int j = 0; j < DH; j += 8)
+          *reinterpret_cast<uint4 *>(dst + j) =
+              make_uint4(tc::pack_bf16(o[j] * inv, o[j + 1] * inv), tc::pack_bf16(o[j + 2] * inv, o[j + 3] * inv),
+                         tc::pack_bf16(o[j + 4] * inv, o[j + 5] * inv), tc::pack_bf16(o[j + 6] * inv, o[j + 7] * inv));
       } else {
         float *dst = reinterpret_cast<float *>(p.out) + orow;
 #pragma unroll
-        for (int j = 0; j < D; j += 4)
+        for (int j = 0; j < DH; j += 4)
           *reinterpret_cast<float4 *>(dst + j) = make_float4(o[j] * inv, o[j + 1] * inv, o[j + 2] * inv, o[j + 3] * inv);
       }
     } else {  // diagonal fallback (tensor_ops.py:136-137)
-      for (int j = 0; j < D; ++j) {
-        const float val = bf2f(vb[static_cast<int64_t>(my_g) * D + j]);
+      for (int j = 0; j < DH; ++j) {
+        const float val = bf2f(vb[static_cast<int64_t>(my_g) * D + wg * DH + j]);
         if (p.out_bf16)
           reinterpret_cast<uint16_t *>(p.out)[orow + j] = f2bf(val);
         else
           reinterpret_cast<float *>(p.out)[orow + j] = val;
       }
-      my_cells += 1;
+      if (wg == 0) my_cells += 1;
     }
   }
   const long long cs = warp_sum_ll(my_cells);
@@ -405,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
     atomicAdd(reinterpret_cast<unsigned long long *>(p.cells + h), static_cast<unsigned long long>(cs));
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
 __global__ void vert_bits_kernel(const int32_t *vert_ids, const int32_t *counts, int n_total, int words,

@@ -52,7 +52,7 @@ def test_score_lines_tc_vs_simt_vs_oracle(cuda_lib, d, n_q, n_kv, ro, n_new, rat
     assert torch.equal(tc["cnt"], si["cnt"])
     for key in ("v_w", "s_w"):
         scale = si[key].abs().max().item()
-        assert (tc[key] - si[key]).abs().max().item() <= 2e-6 * max(1.0, scale), key
+        assert (tc[key] - si[key]).abs().max().item() <= 1e-5 * max(1.0, scale), key
     for key in ("v_max", "s_max"):
         assert (tc[key] - si[key]).abs().max().item() <= 2e-6, key
     # oracle on one head
