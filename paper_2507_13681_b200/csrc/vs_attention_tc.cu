@@ -28,6 +28,7 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int THREADS = 256;  // two warpgroups split S / O columns of the same 128 rows
 constexpr int MAX_KB = 2048;  // key blocks per head (n_total <= 262144)
+constexpr int DENSE_SLASHES = 3;  // slashes crossing a key block before it goes to the tensor cores
 
 struct Params {
   const uint16_t *q, *k, *v;
@@ -54,7 +55,7 @@ struct Smem {
   static constexpr int OFF_V0 = OFF_K0 + 2 * KV_BYTES;
   static constexpr int OFF_P = OFF_V0 + 2 * KV_BYTES;
   static constexpr int OFF_MISC = OFF_P + P_BYTES;
-  static constexpr int MISC_BYTES = 1536 + MAX_KB * 2 + 2 * BN * 4 + BM * 4 + 64;
+  static constexpr int MISC_BYTES = 1536 + MAX_KB * 2 + 2 * BN * 4 + BM * 4 + MAX_KB * 4 + 64;
   static constexpr int TOTAL = OFF_MISC + MISC_BYTES + 1024;  // + alignment slack
 };
 
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 1536);
   int *gcols = reinterpret_cast<int *>(misc + 1536 + MAX_KB * 2);  // [2][BN] columns per buffer
   float *lsum_sh = reinterpret_cast<float *>(misc + 1536 + MAX_KB * 2 + 2 * BN * 4);  // [128]
+  int *blk_cnt = reinterpret_cast<int *>(misc + 1536 + MAX_KB * 2 + 2 * BN * 4 + BM * 4);  // [MAX_KB]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = warp >> 2;          // column half of S / O handled by this thread
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   const uint16_t *vb = p.v + static_cast<int64_t>(kv) * p.kv_head_stride;
   const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * p.words;
   const uint32_t *rsbits = p.rsbits + static_cast<int64_t>(h) * (p.words + 8);
-  int32_t *gl = p.gather_ws + (static_cast<int64_t>(h) * p.n_qtiles + qt) * p.n_total;
+  int32_t *gl = p.gather_ws + (static_cast<int64_t>(h) * p.n_qtiles + qt) * 2 * p.n_total;
 
   // ---- TMEM (S double buffer + O tile), barriers, Q tile
   if (warp == 0) tc::tmem_alloc(tmem_base_sh, 512);
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
     tc::mbar_init(&mbar[2], 1);
   }
   for (int i = tid; i < 64; i += THREADS) kb_bits[i] = 0u;
+  for (int i = tid; i < MAX_KB; i += THREADS) blk_cnt[i] = 0;
   {
     const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
     constexpr int CH = D / 8;
@@ -139,12 +142,17 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   if (p.dense) {
     for (int b = tid; b < n_kb; b += THREADS) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
   } else {
+    // a key block goes to the tensor cores when >= DENSE_SLASHES slashes cross it;
+    // the other slash cells take the CUDA-core diagonal path below
     for (int i = tid; i < n_sl; i += THREADS) {
       const int dd = S[i];
       if (dd > g_hi) break;
       const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
-      for (int b = c_lo / BN; b <= c_hi / BN; ++b) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
+      for (int b = c_lo / BN; b <= c_hi / BN; ++b) atomicAdd(&blk_cnt[b], 1);
     }
+    __syncthreads();
+    for (int b = tid; b < n_kb; b += THREADS)
+      if (blk_cnt[b] >= DENSE_SLASHES) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
   }
   __syncthreads();
   if (tid == 0) {
@@ -185,6 +193,34 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
       }
       if (take) gl[n_g + before + __popc(ball & ((1u << lane) - 1u))] = c;
       n_g += tot;
+    }
+  }
+  // diagonal slashes: selected slashes crossing at least one non-tensor block
+  int32_t *sl = gl + p.n_total;
+  int n_diag = 0;
+  if (!p.dense) {
+    for (int base = 0; base < n_sl; base += THREADS) {
+      const int i = base + tid;
+      bool take = false;
+      int dd = 0;
+      if (i < n_sl) {
+        dd = S[i];
+        if (dd <= g_hi) {
+          const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
+          for (int b = c_lo / BN; b <= c_hi / BN; ++b) take |= !((kb_bits[b >> 5] >> (b & 31)) & 1u);
+        }
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, take);
+      __syncthreads();
+      if (lane == 0) sh_int[8 + warp] = __popc(ball);
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int w = 0; w < THREADS / 32; ++w) {
+        if (w < warp) before += sh_int[8 + w];
+        tot += sh_int[8 + w];
+      }
+      if (take) sl[n_diag + before + __popc(ball & ((1u << lane) - 1u))] = dd;
+      n_diag += tot;
     }
   }
   __syncthreads();
@@ -371,6 +407,83 @@ __global__ void __launch_bounds__(THREADS, 1) vs_attention_tc_kernel(Params p) {
   }
   tc::cp_async_wait<0>();
 
+  // ---- diagonal slash cells on CUDA cores: cells of `sl` slashes whose column
+  // is in a non-tensor block and is not a selected vertical (those cells were
+  // covered above). Thread (row, wg) owns half of the head dim; the partial
+  // dot products of a batch of DB slashes are exchanged through shared memory.
+  if (n_diag > 0) {
+    constexpr int DB = 8;
+    float *part = reinterpret_cast<float *>(smem + L::OFF_P);  // [2][DB][BM] (P buffer is free now)
+    float qf[DH];
+#pragma unroll
+    for (int c8 = 0; c8 < DH / 8; ++c8) {
+      const uint4 u =
+          *reinterpret_cast<const uint4 *>(smem + L::OFF_Q + tc::sw128_offset(row, wg * (DH / 8) + c8, BM));
+      bf16x8_to_f32(u, qf + c8 * 8);
+    }
+    for (int base = 0; base < n_diag; base += DB) {
+      int cj[DB];
+      bool vj[DB];
+#pragma unroll
+      for (int j = 0; j < DB; ++j) {
+        const int idx = base + j;
+        const int c = my_g - (idx < n_diag ? sl[idx] : 0x3fffffff);
+        bool v = row_ok && idx < n_diag && c >= 0;
+        if (v) {
+          const int b = c / BN;
+          v = !((kb_bits[b >> 5] >> (b & 31)) & 1u) && !((__ldg(vbits + (c >> 5)) >> (c & 31)) & 1u);
+        }
+        cj[j] = c;
+        vj[j] = v;
+        float acc = 0.f;
+        if (v) {
+          const uint16_t *kr = kb + static_cast<int64_t>(c) * D + wg * DH;
+#pragma unroll
+          for (int c8 = 0; c8 < DH / 8; ++c8) {
+            float f[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4 *>(kr + c8 * 8), f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = fmaf(qf[c8 * 8 + e], f[e], acc);
+          }
+        }
+        part[(wg * DB + j) * BM + row] = acc;
+      }
+      __syncthreads();
+      float sc[DB];
+      float bmax = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < DB; ++j) {
+        sc[j] = vj[j] ? (part[j * BM + row] + part[(DB + j) * BM + row]) * p.scale_log2 : -INFINITY;
+        bmax = fmaxf(bmax, sc[j]);
+      }
+      __syncthreads();  // `part` is rewritten by the next batch
+      if (bmax != -INFINITY) {
+        const float m_new = fmaxf(m, bmax);
+        const float corr = fast_exp2(m - m_new);  // 0 when m == -inf
+        float lsum = 0.f;
+#pragma unroll
+        for (int i = 0; i < DH; ++i) o[i] *= corr;
+#pragma unroll
+        for (int j = 0; j < DB; ++j) {
+          if (!vj[j]) continue;
+          const float pj = fast_exp2(sc[j] - m_new);
+          lsum += pj;
+          const uint16_t *vr = vb + static_cast<int64_t>(cj[j]) * D + wg * DH;
+#pragma unroll
+          for (int c8 = 0; c8 < DH / 8; ++c8) {
+            float f[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4 *>(vr + c8 * 8), f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[c8 * 8 + e] = fmaf(pj, f[e], o[c8 * 8 + e]);
+          }
+          if (wg == 0) my_cells += 1;
+        }
+        l = l * corr + (wg == 0 ? lsum : 0.f);  // each cell's p is counted once (warpgroup 0)
+        m = m_new;
+      }
+    }
+  }
+
   // ---- epilogue: l = sum of both halves
   lsum_sh[row] = 0.f;
   __syncthreads();
@@ -448,7 +561,7 @@ namespace ls {
 size_t vs_attention_tc_workspace(const ls_layer_desc *L) {
   const size_t words = (L->n_total + 31) / 32;
   const size_t nqt = (L->n_new + k5tc::BM - 1) / k5tc::BM;
-  return static_cast<size_t>(L->n_heads) * (words * 4 + (words + 8) * 4) + nqt * L->n_heads * L->n_total * 4 + 4096;
+  return static_cast<size_t>(L->n_heads) * (words * 4 + (words + 8) * 4) + 2 * nqt * L->n_heads * L->n_total * 4 + 4096;
 }
 
 int vs_attention_tc(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
@@ -462,7 +575,7 @@ int vs_attention_tc(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   Carver c(dense ? nullptr : ws, ws_bytes);  // dense mode reads no plan buffers
   uint32_t *vbits = c.take<uint32_t>(static_cast<size_t>(L->n_heads) * words);
   uint32_t *rsbits = c.take<uint32_t>(static_cast<size_t>(L->n_heads) * (words + 8));
-  int32_t *gather = c.take<int32_t>(static_cast<size_t>(nqt) * L->n_heads * L->n_total);
+  int32_t *gather = c.take<int32_t>(2 * static_cast<size_t>(nqt) * L->n_heads * L->n_total);
   if (!dense) {
     LS_CUDA(cudaMemsetAsync(vbits, 0, sizeof(uint32_t) * L->n_heads * words, st));
     LS_CUDA(cudaMemsetAsync(rsbits, 0, sizeof(uint32_t) * L->n_heads * (words + 8), st));

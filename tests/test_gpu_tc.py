@@ -54,7 +54,7 @@ def test_score_lines_tc_vs_simt_vs_oracle(cuda_lib, d, n_q, n_kv, ro, n_new, rat
         scale = si[key].abs().max().item()
         assert (tc[key] - si[key]).abs().max().item() <= 1e-5 * max(1.0, scale), key
     for key in ("v_max", "s_max"):
-        assert (tc[key] - si[key]).abs().max().item() <= 2e-6, key
+        assert (tc[key] - si[key]).abs().max().item() <= 1e-5 * max(1.0, si[key].abs().max().item()), key
     # oracle on one head
     group = n_q // n_kv
     h = n_q - 1
