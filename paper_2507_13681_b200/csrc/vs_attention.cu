@@ -376,8 +376,8 @@ int check_desc(const ls_layer_desc *L) {
 using namespace ls;
 
 namespace ls {
-size_t vs_attention_tc_workspace(const ls_layer_desc *L);
-int vs_attention_tc(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+size_t vs_attention_ws_workspace(const ls_layer_desc *L);
+int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
                     const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
                     int32_t out_bf16, int64_t *cells, int dense, void *ws, size_t ws_bytes, cudaStream_t st);
 }  // namespace ls
@@ -385,7 +385,7 @@ int vs_attention_tc(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
 extern "C" size_t ls_vs_attention_workspace(const ls_layer_desc *L) {
   const size_t words = (L->n_total + 31) / 32;
   const size_t simt = 2 * static_cast<size_t>(L->n_heads) * words * 4 + 1024;
-  const size_t tcw = vs_attention_tc_workspace(L);
+  const size_t tcw = vs_attention_ws_workspace(L);
   return simt > tcw ? simt : tcw;
 }
 
@@ -394,7 +394,7 @@ extern "C" int ls_vs_attention(const ls_layer_desc *L, const uint16_t *q, const 
                                int32_t out_bf16, int64_t *cells, void *ws, size_t ws_bytes, ls_stream_t stream) {
   int stc = k5::check_desc(L);
   if (stc) return stc;
-  return vs_attention_tc(L, q, k, v, slash_ids, vert_ids, counts, out, out_bf16, cells, 0, ws, ws_bytes,
+  return vs_attention_ws(L, q, k, v, slash_ids, vert_ids, counts, out, out_bf16, cells, 0, ws, ws_bytes,
                          static_cast<cudaStream_t>(stream));
 }
 
@@ -480,7 +480,7 @@ extern "C" int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, con
   int64_t *cells = nullptr;
   LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&cells), sizeof(int64_t) * L->n_heads, st));
   // dense mode touches every causal key block with the causal mask only (tensor-core path)
-  int s = vs_attention_tc(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, 1, nullptr, 0, st);
+  int s = vs_attention_ws(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, 1, nullptr, 0, st);
   LS_CUDA(cudaFreeAsync(cells, st));
   return s;
 }

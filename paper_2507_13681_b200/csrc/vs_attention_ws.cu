@@ -1,0 +1,691 @@
+// K5 (production path) -- warp-specialized vertical/slash sparse attention.
+//
+// Contract: reference masked_sparse_attention (tensor_ops.py:141-183) with the
+// exact `_row_columns` cell set (tensor_ops.py:130-138) and the diagonal
+// fallback, for every q-head of a layer; per-row cell counts = OpCounter
+// increments (tensor_ops.py:172-174).
+//
+// One CTA per (head, 128-row q tile), 10 warps:
+//   warp 8  (1 thread) TMA producer: every operand tile arrives by
+//           cp.async.bulk.tensor (128B swizzle, zero fill out of range) into a
+//           2-stage K/V ring; signals `full`, waits `empty`.
+//   warp 9  (1 thread) MMA issuer: S(i) = Q K(i)^T into a double-buffered
+//           TMEM S, then O += P(i-1) V(i-1) into a TMEM O accumulator
+//           (tcgen05.mma kind::f16, bf16 -> fp32), commits to mbarriers.
+//   warps 0-7 softmax: thread (row, half) owns one TMEM lane and 64 of the
+//           128 S columns; masked online softmax in the log2 domain with lazy
+//           rescaling of the TMEM O (only when the running max grows by 2^8),
+//           P to shared memory in the UMMA K-major layout.
+// Tile kinds, in order:
+//   dense    : key block [128b, 128b+128) crossed by >= DENSE_SLASHES selected
+//              slashes; mask causal & (vbit | sbit)              (tensor cores)
+//   gathered : 128 consecutive entries of the head's compacted selected
+//              verticals (K/V rows gathered once per call by a pre-kernel);
+//              mask causal & column not in a dense block          (tensor cores)
+//   diagonal : one selected slash d whose cells fall outside dense blocks: the
+//              contiguous key range [g0-d, g0-d+128) is TMA-loaded and each
+//              row's single cell (key g-d) is computed on CUDA cores (the cell
+//              is skipped when its column is a selected vertical, already
+//              counted by the gathered tiles).
+// No cell is counted twice; every cell of every row is covered.
+
+#include <cuda.h>
+
+#include "ls_common.cuh"
+#include "tc_common.cuh"
+
+namespace ls {
+namespace k5ws {
+
+constexpr int BM = 128, BN = 128;
+constexpr int N_SOFT = 256;           // softmax threads (8 warps)
+constexpr int THREADS = N_SOFT + 64;  // + producer warp + MMA warp
+constexpr int MAX_KB = 2048;
+constexpr int DENSE_SLASHES = 3;
+constexpr float RESCALE_LOG2 = 8.f;  // lazy rescale threshold (factor 256)
+
+struct Params {
+  const int32_t *slash_ids, *vert_ids, *counts;
+  const uint32_t *vbits, *rsbits;
+  int32_t *diag_ws;  // [H * n_qtiles][n_total]
+  const uint16_t *v;  // archive V (diagonal fallback reads)
+  int n_heads, group, n_new, n_total, row_offset, words, n_qtiles, dense;
+  int64_t kv_head_stride;
+  float scale_log2;
+  void *out;
+  int out_bf16;
+  long long *cells;
+};
+
+template <int D>
+struct Smem {
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = Q_BYTES;                 // 2 stages
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;    // 2 stages
+  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
+  static constexpr int OFF_MISC = OFF_P + BM * BN * 2;
+  // misc: barriers 256 | ints 256 | kb_bits 256 | pmax 1024 | pd 1024 | lx 512 | gcols 1024 | dense_list 4096 | blk_cnt 8192
+  static constexpr int MISC_BYTES = 256 + 256 + 256 + 1024 + 1024 + 512 + 1024 + MAX_KB * 2 + MAX_KB * 4;
+  static constexpr int TOTAL = OFF_MISC + MISC_BYTES + 1024;
+};
+
+struct Bars {
+  uint64_t full[2], empty[2], s_full[2], s_empty[2], p_full, pv_done, q_full;
+};
+
+__device__ __forceinline__ bool bit_of(const uint32_t *b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
+
+__device__ __forceinline__ void bit_window(const uint32_t *bits, int s, uint32_t *w, int n) {
+  const int w0 = s >> 5, sh = s & 31;
+  uint32_t x[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) x[i] = __ldg(bits + w0 + i);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) w[i] = __funnelshift_r(x[i], x[i + 1], sh);
+  (void)n;
+}
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+    vs_attention_ws_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                           const __grid_constant__ CUtensorMap tm_vc, Params p) {
+  extern __shared__ unsigned char smem_dyn[];
+  using L = Smem<D>;
+  constexpr int DH = D / 2;
+  unsigned char *smem = tc::align1024(smem_dyn);
+  unsigned char *misc = smem + L::OFF_MISC;
+  Bars *bars = reinterpret_cast<Bars *>(misc);
+  int *sh_int = reinterpret_cast<int *>(misc + 256);                   // [64]
+  uint32_t *kb_bits = reinterpret_cast<uint32_t *>(misc + 512);        // [64]
+  float *pmax = reinterpret_cast<float *>(misc + 768);                 // [2][128]
+  float *pd = reinterpret_cast<float *>(misc + 1792);                  // [2][128]
+  float *lx = reinterpret_cast<float *>(misc + 2816);                  // [128]
+  int *gcols = reinterpret_cast<int *>(misc + 3328);                   // [2][128]
+  int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 4352);      // [MAX_KB]
+  int *blk_cnt = reinterpret_cast<int *>(misc + 4352 + MAX_KB * 2);   // [MAX_KB]
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(misc + 256 + 252);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = blockIdx.y, qt = blockIdx.x;
+  const int r0 = qt * BM;
+  const int nr = min(BM, p.n_new - r0);
+  const int g0 = p.row_offset + r0;
+  const int g_hi = g0 + nr - 1;
+  const int kv = h / p.group;
+  const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * p.words;
+  const uint32_t *rsbits = p.rsbits + static_cast<int64_t>(h) * (p.words + 8);
+  int32_t *sl = p.diag_ws + (static_cast<int64_t>(h) * p.n_qtiles + qt) * p.n_total;
+
+  if (warp == 0) tc::tmem_alloc(tmem_sh, 512);
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&bars->full[s], 1);
+      tc::mbar_init(&bars->empty[s], 1);
+      tc::mbar_init(&bars->s_full[s], 1);
+      tc::mbar_init(&bars->s_empty[s], 1);
+    }
+    tc::mbar_init(&bars->p_full, 1);
+    tc::mbar_init(&bars->pv_done, 1);
+    tc::mbar_init(&bars->q_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 64; i += THREADS) kb_bits[i] = 0u;
+  for (int i = tid; i < MAX_KB; i += THREADS) blk_cnt[i] = 0;
+  __syncthreads();
+
+  // ---- tile lists (all threads)
+  const int n_kb = g_hi / BN + 1;
+  const int n_sl = p.dense ? 0 : p.counts[h * 2 + 0];
+  const int n_vt = p.dense ? 0 : p.counts[h * 2 + 1];
+  const int32_t *S = p.slash_ids + static_cast<int64_t>(h) * p.n_total;
+  const int32_t *Vl = p.vert_ids + static_cast<int64_t>(h) * p.n_total;
+  if (p.dense) {
+    for (int b = tid; b < n_kb; b += THREADS) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
+  } else {
+    for (int i = tid; i < n_sl; i += THREADS) {
+      const int dd = S[i];
+      if (dd > g_hi) break;
+      const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
+      for (int b = c_lo / BN; b <= c_hi / BN; ++b) atomicAdd(&blk_cnt[b], 1);
+    }
+    __syncthreads();
+    for (int b = tid; b < n_kb; b += THREADS)
+      if (blk_cnt[b] >= DENSE_SLASHES) atomicOr(&kb_bits[b >> 5], 1u << (b & 31));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int n = 0;
+    for (int w = 0; w < (n_kb + 31) / 32; ++w) {
+      uint32_t x = kb_bits[w];
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        if (w * 32 + b < n_kb) dense_list[n++] = static_cast<int16_t>(w * 32 + b);
+      }
+    }
+    sh_int[0] = n;
+    int lo = 0, hi = n_vt;  // verticals <= g_hi
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (Vl[mid] <= g_hi)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    sh_int[1] = lo;
+  }
+  int n_diag = 0;
+  if (!p.dense) {
+    for (int base = 0; base < n_sl; base += THREADS) {
+      const int i = base + tid;
+      bool take = false;
+      int dd = 0;
+      if (i < n_sl) {
+        dd = S[i];
+        if (dd <= g_hi) {
+          const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
+          for (int b = c_lo / BN; b <= c_hi / BN; ++b) take |= !bit_of(kb_bits, b);
+        }
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, take);
+      __syncthreads();
+      if (lane == 0) sh_int[8 + warp] = __popc(ball);
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int w = 0; w < THREADS / 32; ++w) {
+        if (w < warp) before += sh_int[8 + w];
+        tot += sh_int[8 + w];
+      }
+      if (take) sl[n_diag + before + __popc(ball & ((1u << lane) - 1u))] = dd;
+      n_diag += tot;
+    }
+  }
+  __syncthreads();
+  const int n_dense = sh_int[0];
+  const int v_end = sh_int[1];
+  const int n_gt = (v_end + BN - 1) / BN;
+  const int n_tc = n_dense + n_gt;
+  const int n_all = n_tc + n_diag;
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_sh;
+  const uint32_t tmem_o = tmem + 256;
+
+  if (warp == 8) {
+    // =================================================== TMA producer
+    if (lane == 0) {
+      tc::prefetch_tmap(&tm_q);
+      tc::prefetch_tmap(&tm_k);
+      tc::prefetch_tmap(&tm_v);
+      tc::prefetch_tmap(&tm_kc);
+      tc::prefetch_tmap(&tm_vc);
+      tc::mbar_expect_tx(&bars->q_full, L::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < D / 64; ++a)
+        tc::tma_load_3d(tc::smem_u32(smem + L::OFF_Q + a * BM * 128), &tm_q, &bars->q_full, a * 64, r0, h);
+      for (int t = 0; t < n_all; ++t) {
+        const int s = t & 1;
+        tc::mbar_wait(&bars->empty[s], ((t >> 1) & 1) ^ 1);
+        tc::mbar_expect_tx(&bars->full[s], 2 * L::KV_BYTES);
+        const CUtensorMap *mk, *mv;
+        int row, hh;
+        if (t < n_dense) {
+          mk = &tm_k, mv = &tm_v, row = dense_list[t] * BN, hh = kv;
+        } else if (t < n_tc) {
+          mk = &tm_kc, mv = &tm_vc, row = (t - n_dense) * BN, hh = h;
+        } else {
+          mk = &tm_k, mv = &tm_v, row = g0 - sl[t - n_tc], hh = kv;
+        }
+        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
+        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + s * L::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < D / 64; ++a) {
+          tc::tma_load_3d(ks + a * BN * 128, mk, &bars->full[s], a * 64, row, hh);
+          tc::tma_load_3d(vs + a * BN * 128, mv, &bars->full[s], a * 64, row, hh);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // =================================================== MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = tc::make_idesc(BM, BN, false, false);
+      constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, false, true);
+      const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
+      const uint32_t ps = tc::smem_u32(smem + L::OFF_P);
+      tc::mbar_wait(&bars->q_full, 0);
+      auto issue_pv = [&](int j) {  // O += P(j) V(j)
+        tc::mbar_wait(&bars->p_full, j & 1);
+        tc::fence_after_sync();
+        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (j & 1) * L::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t ad = tc::make_desc(ps + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
+          tc::mma_bf16(tmem_o, ad, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(&bars->pv_done);
+        tc::mma_commit(&bars->empty[j & 1]);
+      };
+      for (int i = 0; i < n_tc; ++i) {
+        const int s = i & 1;
+        tc::mbar_wait(&bars->full[s], (i >> 1) & 1);
+        tc::mbar_wait(&bars->s_empty[s], ((i >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = tc::make_desc(qs + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+          tc::mma_bf16(tmem + s * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&bars->s_full[s]);
+        if (i > 0) issue_pv(i - 1);
+      }
+      if (n_tc > 0) issue_pv(n_tc - 1);
+    }
+  } else {
+    // =================================================== softmax warps
+    const int wg = warp >> 2;
+    const int row = (warp & 3) * 32 + lane;
+    const int my_g = g0 + row;
+    const bool row_ok = row < nr;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float m_ref = -INFINITY, l = 0.f;
+    long long my_cells = 0;
+    for (int i = 0; i < n_tc; ++i) {
+      const int s = i & 1;
+      const bool gathered = i >= n_dense;
+      uint32_t mk[2];
+      if (gathered) {  // stage this tile's 128 vertical columns
+        if (wg == 0) {
+          const int idx = (i - n_dense) * BN + row;
+          gcols[s * BN + row] = idx < v_end ? Vl[idx] : 0x7fffffff;
+        }
+        tc::named_sync(1, N_SOFT);
+        const int *gc = gcols + s * BN + wg * 64;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          uint32_t w = 0;
+#pragma unroll 8
+          for (int j = 0; j < 32; ++j) {
+            const int c = gc[t * 32 + j];
+            const bool ok = row_ok && c <= my_g && !bit_of(kb_bits, c / BN);
+            w |= ok ? (1u << j) : 0u;
+          }
+          mk[t] = w;
+        }
+      } else {
+        const int c0 = dense_list[i] * BN + wg * 64;
+        const int lim = my_g - c0;
+        if (p.dense || !row_ok) {
+          mk[0] = mk[1] = 0xffffffffu;  // (rows past the block are cleared below)
+        } else {
+          uint32_t sw[2];
+          bit_window(rsbits, p.n_total - 1 - my_g + c0, sw, 2);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) mk[t] = ((c0 / 32 + t < p.words) ? __ldg(vbits + c0 / 32 + t) : 0u) | sw[t];
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int hi = lim - 32 * t;
+          mk[t] &= (!row_ok) ? 0u : (hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u)));
+        }
+      }
+      my_cells += __popc(mk[0]) + __popc(mk[1]);
+      tc::mbar_wait(&bars->s_full[s], (i >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t s_addr = tmem + s * 128 + lane_base + wg * 64;
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch) {
+        float sv[32];
+        tc::tmem_ld32(s_addr + cch * 32, sv);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, ((mk[cch] >> j) & 1u) ? sv[j] : -INFINITY);
+      }
+      pmax[wg * BM + row] = tmax;
+      tc::named_sync(1, N_SOFT);
+      const float tm = fmaxf(pmax[row], pmax[BM + row]);
+      const float m_tile = tm == -INFINITY ? -INFINITY : tm * p.scale_log2;
+      // previous PV must be done before P is overwritten or O is rescaled
+      if (i > 0) {
+        tc::mbar_wait(&bars->pv_done, (i - 1) & 1);
+        tc::fence_after_sync();
+      }
+      if (m_tile > m_ref + RESCALE_LOG2) {
+        if (m_ref != -INFINITY) {  // O holds data scaled by exp2(-m_ref)
+          const float corr = fast_exp2(m_ref - m_tile);
+#pragma unroll
+          for (int cch = 0; cch < DH / 32; ++cch) {
+            float ov[32];
+            tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ov[j] *= corr;
+            tc::tmem_st32(tmem_o + lane_base + wg * DH + cch * 32, ov);
+          }
+          tc::tmem_wait_st();
+          l *= corr;
+        }
+        m_ref = m_tile;
+      }
+      float lsum = 0.f;
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch) {
+        float sv[32];
+        tc::tmem_ld32(s_addr + cch * 32, sv);
+        tc::tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(fmaf(sv[j], p.scale_log2, -m_ref)) : 0.f;
+          const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[j + 1], p.scale_log2, -m_ref)) : 0.f;
+          lsum += a + b;
+          pk[j >> 1] = tc::pack_bf16(a, b);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int chunk = wg * 8 + cch * 4 + q4;
+          *reinterpret_cast<uint4 *>(smem + L::OFF_P + tc::sw128_offset(row, chunk, BM)) =
+              make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        }
+      }
+      l += lsum;
+      tc::fence_before_sync();
+      tc::fence_proxy_async();
+      tc::named_sync(1, N_SOFT);
+      if (tid == 0) {
+        tc::mbar_arrive(&bars->s_empty[s]);
+        tc::mbar_arrive(&bars->p_full);
+      }
+    }
+    // O (TMEM) -> registers, relative to m_ref
+    float o[DH];
+    if (n_tc > 0) {
+      tc::mbar_wait(&bars->pv_done, (n_tc - 1) & 1);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int cch = 0; cch < DH / 32; ++cch) {
+        float ov[32];
+        tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[cch * 32 + j] = ov[j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < DH; ++j) o[j] = 0.f;
+    }
+    // ---- diagonal slash tiles on CUDA cores
+    if (n_diag > 0) {
+      float qf[DH];
+      tc::mbar_wait(&bars->q_full, 0);
+#pragma unroll
+      for (int c8 = 0; c8 < DH / 8; ++c8)
+        bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_Q + tc::sw128_offset(row, wg * (DH / 8) + c8, BM)),
+                      qf + c8 * 8);
+      for (int t = n_tc; t < n_all; ++t) {
+        const int s = t & 1;
+        const int dd = sl[t - n_tc];
+        const int c = my_g - dd;
+        bool v = row_ok && c >= 0;
+        if (v) v = !bit_of(kb_bits, c / BN) && !bit_of(vbits, c);
+        tc::mbar_wait(&bars->full[s], (t >> 1) & 1);
+        float acc = 0.f;
+        if (v) {  // key c sits at row `row` of the staged range [g0 - d, g0 - d + 128)
+#pragma unroll
+          for (int c8 = 0; c8 < DH / 8; ++c8) {
+            float f[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_K + s * L::KV_BYTES +
+                                                           tc::sw128_offset(row, wg * (DH / 8) + c8, BN)),
+                          f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = fmaf(qf[c8 * 8 + e], f[e], acc);
+          }
+        }
+        pd[wg * BM + row] = acc;
+        tc::named_sync(1, N_SOFT);
+        if (v) {
+          const float sc = (pd[row] + pd[BM + row]) * p.scale_log2;
+          if (sc > m_ref + RESCALE_LOG2) {
+            const float corr = fast_exp2(m_ref - sc);  // 0 when m_ref == -inf
+#pragma unroll
+            for (int j = 0; j < DH; ++j) o[j] *= corr;
+            l *= corr;
+            m_ref = sc;
+          }
+          const float pj = fast_exp2(sc - m_ref);
+          if (wg == 0) {
+            l += pj;
+            my_cells += 1;
+          }
+#pragma unroll
+          for (int c8 = 0; c8 < DH / 8; ++c8) {
+            float f[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_V + s * L::KV_BYTES +
+                                                           tc::sw128_offset(row, wg * (DH / 8) + c8, BN)),
+                          f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[c8 * 8 + e] = fmaf(pj, f[e], o[c8 * 8 + e]);
+          }
+        }
+        tc::named_sync(1, N_SOFT);  // stage and pd consumed
+        if (tid == 0) tc::mbar_arrive(&bars->empty[s]);
+      }
+    }
+    // ---- epilogue: both halves agree on m_ref; l = l(wg0) + l(wg1)
+    if (wg == 1) lx[row] = l;
+    tc::named_sync(1, N_SOFT);
+    if (wg == 0) lx[row] = l + lx[row];
+    tc::named_sync(1, N_SOFT);
+    const float l_all = lx[row];
+    if (row_ok) {
+      const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * D + wg * DH;
+      if (l_all > 0.f) {
+        const float inv = 1.f / l_all;
+        if (p.out_bf16) {
+          uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + orow;
+#pragma unroll
+          for (int j = 0; j < DH; j += 8)
+            *reinterpret_cast<uint4 *>(dst + j) =
+                make_uint4(tc::pack_bf16(o[j] * inv, o[j + 1] * inv), tc::pack_bf16(o[j + 2] * inv, o[j + 3] * inv),
+                           tc::pack_bf16(o[j + 4] * inv, o[j + 5] * inv), tc::pack_bf16(o[j + 6] * inv, o[j + 7] * inv));
+        } else {
+          float *dst = reinterpret_cast<float *>(p.out) + orow;
+#pragma unroll
+          for (int j = 0; j < DH; j += 4)
+            *reinterpret_cast<float4 *>(dst + j) = make_float4(o[j] * inv, o[j + 1] * inv, o[j + 2] * inv, o[j + 3] * inv);
+        }
+      } else {  // diagonal fallback (tensor_ops.py:136-137)
+        const uint16_t *vrow = p.v + static_cast<int64_t>(kv) * p.kv_head_stride + static_cast<int64_t>(my_g) * D + wg * DH;
+        for (int j = 0; j < DH; ++j) {
+          const float val = bf2f(vrow[j]);
+          if (p.out_bf16)
+            reinterpret_cast<uint16_t *>(p.out)[orow + j] = f2bf(val);
+          else
+            reinterpret_cast<float *>(p.out)[orow + j] = val;
+        }
+        if (wg == 0) my_cells += 1;
+      }
+    }
+    const long long cs = warp_sum_ll(my_cells);
+    if (lane == 0 && cs)
+      atomicAdd(reinterpret_cast<unsigned long long *>(p.cells + h), static_cast<unsigned long long>(cs));
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+// compacted selected verticals: kc/vc[h][j] = K/V[kv(h)][vert_ids[h][j]], rows
+// [n_vt, round_up(n_vt, 128)) zeroed so that padded tile rows are finite
+__global__ void gather_verticals_kernel(const uint16_t *k, const uint16_t *v, const int32_t *vert_ids,
+                                        const int32_t *counts, int n_total, int group, int64_t kv_head_stride,
+                                        int d, uint16_t *kc, uint16_t *vc) {
+  const int h = blockIdx.y;
+  const int n = counts[h * 2 + 1];
+  const int n_pad = (n + 127) / 128 * 128;
+  const int vec = d / 8;
+  const uint4 *ks = reinterpret_cast<const uint4 *>(k + static_cast<int64_t>(h / group) * kv_head_stride);
+  const uint4 *vs = reinterpret_cast<const uint4 *>(v + static_cast<int64_t>(h / group) * kv_head_stride);
+  uint4 *kd = reinterpret_cast<uint4 *>(kc + static_cast<int64_t>(h) * n_total * d);
+  uint4 *vd = reinterpret_cast<uint4 *>(vc + static_cast<int64_t>(h) * n_total * d);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad * vec; i += gridDim.x * blockDim.x) {
+    const int j = i / vec, e = i % vec;
+    if (j >= n_total) break;
+    if (j < n) {
+      const int64_t src = static_cast<int64_t>(vert_ids[static_cast<int64_t>(h) * n_total + j]) * vec + e;
+      kd[i] = ks[src];
+      vd[i] = vs[src];
+    } else {
+      kd[i] = make_uint4(0, 0, 0, 0);
+      vd[i] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+__global__ void vert_bits_kernel(const int32_t *vert_ids, const int32_t *counts, int n_total, int words,
+                                 uint32_t *vbits) {
+  const int h = blockIdx.y;
+  const int n = counts[h * 2 + 1];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = vert_ids[static_cast<int64_t>(h) * n_total + i];
+    atomicOr(vbits + static_cast<int64_t>(h) * words + (c >> 5), 1u << (c & 31));
+  }
+}
+
+__global__ void reverse_bits_kernel(const int32_t *slash_ids, const int32_t *counts, int n_total, int words,
+                                    uint32_t *rsbits) {
+  const int h = blockIdx.y;
+  const int n = counts[h * 2];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = slash_ids[static_cast<int64_t>(h) * n_total + i];
+    const int x = n_total - 1 - d;
+    atomicOr(rsbits + static_cast<int64_t>(h) * (words + 8) + (x >> 5), 1u << (x & 31));
+  }
+}
+
+}  // namespace k5ws
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// bf16 [heads][rows][d] with explicit strides; box = 64 columns x 128 rows
+int make_tmap_bf16_3d(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
+                      int64_t head_stride_el) {
+  EncodeTiledFn fn = encode_fn();
+  LS_REQUIRE(fn != nullptr, LS_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride_el * 2), static_cast<cuuint64_t>(head_stride_el * 2)};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LS_REQUIRE(r == CUDA_SUCCESS, LS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return LS_OK;
+}
+
+size_t vs_attention_ws_workspace(const ls_layer_desc *L) {
+  const size_t words = (L->n_total + 31) / 32;
+  const size_t nqt = (L->n_new + k5ws::BM - 1) / k5ws::BM;
+  const size_t H = L->n_heads;
+  return H * (words * 4 + (words + 8) * 4) + nqt * H * L->n_total * 4 +
+         2 * H * (static_cast<size_t>(L->n_total) + 128) * L->head_dim * 2 + 8 * 256;
+}
+
+int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                    const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
+                    int32_t out_bf16, int64_t *cells, int dense, void *ws, size_t ws_bytes, cudaStream_t st) {
+  LS_REQUIRE(L->head_dim == 64 || L->head_dim == 128, LS_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  LS_REQUIRE((L->n_total + k5ws::BN - 1) / k5ws::BN <= k5ws::MAX_KB, LS_ERR_UNSUPPORTED, "n_total too large");
+  LS_REQUIRE(dense || ws_bytes >= vs_attention_ws_workspace(L), LS_ERR_WORKSPACE, "vs_attention workspace too small");
+  const int H = L->n_heads, d = L->head_dim;
+  const int words = (L->n_total + 31) / 32;
+  const int nqt = (L->n_new + k5ws::BM - 1) / k5ws::BM;
+  Carver c(ws, ws_bytes);
+  uint32_t *vbits = c.take<uint32_t>(static_cast<size_t>(H) * words);
+  uint32_t *rsbits = c.take<uint32_t>(static_cast<size_t>(H) * (words + 8));
+  int32_t *diag = c.take<int32_t>(static_cast<size_t>(nqt) * H * L->n_total);
+  const size_t vcap = static_cast<size_t>(L->n_total) + 128;
+  uint16_t *kc = c.take<uint16_t>(static_cast<size_t>(H) * vcap * d);
+  uint16_t *vc = c.take<uint16_t>(static_cast<size_t>(H) * vcap * d);
+  if (!dense) {
+    LS_CUDA(cudaMemsetAsync(vbits, 0, sizeof(uint32_t) * H * words, st));
+    LS_CUDA(cudaMemsetAsync(rsbits, 0, sizeof(uint32_t) * H * (words + 8), st));
+    k5ws::vert_bits_kernel<<<dim3(4, H), 256, 0, st>>>(vert_ids, counts, L->n_total, words, vbits);
+    k5ws::reverse_bits_kernel<<<dim3(4, H), 256, 0, st>>>(slash_ids, counts, L->n_total, words, rsbits);
+    k5ws::gather_verticals_kernel<<<dim3(32, H), 256, 0, st>>>(k, v, vert_ids, counts, static_cast<int>(vcap),
+                                                               H / L->n_kv_heads, L->kv_head_stride, d, kc, vc);
+    LS_LAUNCH_CHECK("vs_attention_ws prep");
+  }
+  CUtensorMap tq, tk, tv, tkc, tvc;
+  int s;
+  if ((s = make_tmap_bf16_3d(&tq, q, d, L->n_new, H, d, L->q_head_stride))) return s;
+  if ((s = make_tmap_bf16_3d(&tk, k, d, L->n_total, L->n_kv_heads, d, L->kv_head_stride))) return s;
+  if ((s = make_tmap_bf16_3d(&tv, v, d, L->n_total, L->n_kv_heads, d, L->kv_head_stride))) return s;
+  if (dense) {  // no gathered tiles: any valid map will do
+    tkc = tk;
+    tvc = tv;
+  } else {
+    if ((s = make_tmap_bf16_3d(&tkc, kc, d, static_cast<int64_t>(vcap), H, d, static_cast<int64_t>(vcap) * d)))
+      return s;
+    if ((s = make_tmap_bf16_3d(&tvc, vc, d, static_cast<int64_t>(vcap), H, d, static_cast<int64_t>(vcap) * d)))
+      return s;
+  }
+  k5ws::Params p;
+  p.slash_ids = slash_ids;
+  p.vert_ids = vert_ids;
+  p.counts = counts;
+  p.vbits = vbits;
+  p.rsbits = rsbits;
+  p.diag_ws = diag;
+  p.v = v;
+  p.n_heads = H;
+  p.group = H / L->n_kv_heads;
+  p.n_new = L->n_new;
+  p.n_total = L->n_total;
+  p.row_offset = L->row_offset;
+  p.words = words;
+  p.n_qtiles = nqt;
+  p.dense = dense;
+  p.kv_head_stride = L->kv_head_stride;
+  p.scale_log2 = kLog2e / sqrtf(static_cast<float>(d));
+  p.out = out;
+  p.out_bf16 = out_bf16;
+  p.cells = reinterpret_cast<long long *>(cells);
+  LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * H, st));
+  dim3 grid(nqt, H);
+  if (d == 128) {
+    const int smem = k5ws::Smem<128>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k5ws::vs_attention_ws_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k5ws::vs_attention_ws_kernel<128><<<grid, k5ws::THREADS, smem, st>>>(tq, tk, tv, tkc, tvc, p);
+  } else {
+    const int smem = k5ws::Smem<64>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k5ws::vs_attention_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k5ws::vs_attention_ws_kernel<64><<<grid, k5ws::THREADS, smem, st>>>(tq, tk, tv, tkc, tvc, p);
+  }
+  LS_LAUNCH_CHECK("vs_attention_ws_kernel");
+  return LS_OK;
+}
+
+}  // namespace ls
