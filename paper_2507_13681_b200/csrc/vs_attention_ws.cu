@@ -525,19 +525,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 // compacted selected verticals: kc/vc[h][j] = K/V[kv(h)][vert_ids[h][j]], rows
 // [n_vt, round_up(n_vt, 128)) zeroed so that padded tile rows are finite
 __global__ void gather_verticals_kernel(const uint16_t *k, const uint16_t *v, const int32_t *vert_ids,
-                                        const int32_t *counts, int n_total, int group, int64_t kv_head_stride,
-                                        int d, uint16_t *kc, uint16_t *vc) {
+                                        const int32_t *counts, int n_total, int vcap, int group,
+                                        int64_t kv_head_stride, int d, uint16_t *kc, uint16_t *vc) {
   const int h = blockIdx.y;
   const int n = counts[h * 2 + 1];
-  const int n_pad = (n + 127) / 128 * 128;
+  const int n_pad = min((n + 127) / 128 * 128, vcap);
   const int vec = d / 8;
   const uint4 *ks = reinterpret_cast<const uint4 *>(k + static_cast<int64_t>(h / group) * kv_head_stride);
   const uint4 *vs = reinterpret_cast<const uint4 *>(v + static_cast<int64_t>(h / group) * kv_head_stride);
-  uint4 *kd = reinterpret_cast<uint4 *>(kc + static_cast<int64_t>(h) * n_total * d);
-  uint4 *vd = reinterpret_cast<uint4 *>(vc + static_cast<int64_t>(h) * n_total * d);
+  uint4 *kd = reinterpret_cast<uint4 *>(kc + static_cast<int64_t>(h) * vcap * d);
+  uint4 *vd = reinterpret_cast<uint4 *>(vc + static_cast<int64_t>(h) * vcap * d);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad * vec; i += gridDim.x * blockDim.x) {
     const int j = i / vec, e = i % vec;
-    if (j >= n_total) break;
     if (j < n) {
       const int64_t src = static_cast<int64_t>(vert_ids[static_cast<int64_t>(h) * n_total + j]) * vec + e;
       kd[i] = ks[src];
@@ -634,8 +633,9 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
     LS_CUDA(cudaMemsetAsync(rsbits, 0, sizeof(uint32_t) * H * (words + 8), st));
     k5ws::vert_bits_kernel<<<dim3(4, H), 256, 0, st>>>(vert_ids, counts, L->n_total, words, vbits);
     k5ws::reverse_bits_kernel<<<dim3(4, H), 256, 0, st>>>(slash_ids, counts, L->n_total, words, rsbits);
-    k5ws::gather_verticals_kernel<<<dim3(32, H), 256, 0, st>>>(k, v, vert_ids, counts, static_cast<int>(vcap),
-                                                               H / L->n_kv_heads, L->kv_head_stride, d, kc, vc);
+    k5ws::gather_verticals_kernel<<<dim3(32, H), 256, 0, st>>>(k, v, vert_ids, counts, L->n_total,
+                                                               static_cast<int>(vcap), H / L->n_kv_heads,
+                                                               L->kv_head_stride, d, kc, vc);
     LS_LAUNCH_CHECK("vs_attention_ws prep");
   }
   CUtensorMap tq, tk, tv, tkc, tvc;
