@@ -68,15 +68,27 @@ __device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Waits for phase `parity` of an mbarrier; traps after ~10 s so a pipeline
+// bug surfaces as a launch error instead of a hung device.
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
-  asm volatile(
-      "{\n\t.reg .pred done;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-      "@!done bra WAIT_%=;\n\t}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
+  if (mbar_try_wait(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
 }
 
 // ------------------------------------------------------------ TMEM

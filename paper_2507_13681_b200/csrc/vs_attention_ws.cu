@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mk = &tm_k, mv = &tm_v, row = dense_list[t] * BN, hh = kv;
         } else if (t < n_tc) {
           mk = &tm_kc, mv = &tm_vc, row = (t - n_dense) * BN, hh = h;
-        } else {
-          mk = &tm_k, mv = &tm_v, row = g0 - sl[t - n_tc], hh = kv;
+        } else {  // diagonal range start, clamped at 0 (no negative TMA coordinates)
+          mk = &tm_k, mv = &tm_v, row = max(0, g0 - sl[t - n_tc]), hh = kv;
         }
         const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
         const uint32_t vs = tc::smem_u32(smem + L::OFF_V + s * L::KV_BYTES);
@@ -433,16 +433,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = t & 1;
         const int dd = sl[t - n_tc];
         const int c = my_g - dd;
+        const int kr = c - max(0, g0 - dd);  // row of key c in the staged range
         bool v = row_ok && c >= 0;
         if (v) v = !bit_of(kb_bits, c / BN) && !bit_of(vbits, c);
         tc::mbar_wait(&bars->full[s], (t >> 1) & 1);
         float acc = 0.f;
-        if (v) {  // key c sits at row `row` of the staged range [g0 - d, g0 - d + 128)
+        if (v) {
 #pragma unroll
           for (int c8 = 0; c8 < DH / 8; ++c8) {
             float f[8];
             bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_K + s * L::KV_BYTES +
-                                                           tc::sw128_offset(row, wg * (DH / 8) + c8, BN)),
+                                                           tc::sw128_offset(kr, wg * (DH / 8) + c8, BN)),
                           f);
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc = fmaf(qf[c8 * 8 + e], f[e], acc);
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int c8 = 0; c8 < DH / 8; ++c8) {
             float f[8];
             bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_V + s * L::KV_BYTES +
-                                                           tc::sw128_offset(row, wg * (DH / 8) + c8, BN)),
+                                                           tc::sw128_offset(kr, wg * (DH / 8) + c8, BN)),
                           f);
 #pragma unroll
             for (int e = 0; e < 8; ++e) o[c8 * 8 + e] = fmaf(pj, f[e], o[c8 * 8 + e]);
