@@ -67,6 +67,9 @@ typedef struct ls_layer_desc {
 
 const char *ls_last_error(void);
 int ls_version(void);
+/* Debugging: host-mapped int buffer where the pipelined kernels record the
+ * progress of each role per CTA (NULL disables). */
+int ls_debug_set_buffer(void *host_mapped);
 /* number of SMs / device name of the current device (diagnostics) */
 int ls_device_info(int *sm_count, char *name, int name_len);
 

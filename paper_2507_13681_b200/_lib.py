@@ -47,6 +47,7 @@ DS = C.POINTER(DecodeStateDesc)
 SIGNATURES = {
     "ls_last_error": (C.c_char_p, []),
     "ls_version": (C.c_int, []),
+    "ls_debug_set_buffer": (C.c_int, [P]),
     "ls_device_info": (C.c_int, [C.POINTER(C.c_int), C.c_char_p, C.c_int]),
     "ls_sample_size": (C.c_int, [I32, F64, I32, C.POINTER(I32)]),
     "ls_sample_rows_workspace": (SZ, [I32, I32]),

@@ -55,7 +55,19 @@ struct Params {
   void *out;
   int out_bf16;
   long long *cells;
+  int *dbg;  // optional host-mapped progress record [CTA][16] (ls_debug_set_buffer)
 };
+
+// progress note of a role (0 producer, 1 MMA, 2 softmax, 3 tile counts) before a wait
+#define KDBG(role, tile, code)                                                          \
+  do {                                                                                  \
+    if (p.dbg) {                                                                        \
+      volatile int *d_ = p.dbg + (blockIdx.y * gridDim.x + blockIdx.x) * 16 + (role)*4; \
+      d_[0] = (tile);                                                                   \
+      d_[1] = (code);                                                                   \
+      __threadfence_system();                                                           \
+    }                                                                                   \
+  } while (0)
 
 template <int D>
 struct Smem {
@@ -209,6 +221,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n_gt = (v_end + BN - 1) / BN;
   const int n_tc = n_dense + n_gt;
   const int n_all = n_tc + n_diag;
+  if (tid == 0 && p.dbg) {
+    volatile int *d_ = p.dbg + (blockIdx.y * gridDim.x + blockIdx.x) * 16 + 12;
+    d_[0] = n_dense;
+    d_[1] = n_gt;
+    d_[2] = n_diag;
+    d_[3] = 1;
+  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -229,6 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tma_load_3d(tc::smem_u32(smem + L::OFF_Q + a * BM * 128), &tm_q, &bars->q_full, a * 64, r0, h);
       for (int t = 0; t < n_all; ++t) {
         const int s = t & 1;
+        KDBG(0, t, 1);
         tc::mbar_wait(&bars->empty[s], ((t >> 1) & 1) ^ 1);
         tc::mbar_expect_tx(&bars->full[s], 2 * L::KV_BYTES);
         const CUtensorMap *mk, *mv;
@@ -256,8 +276,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, false, true);
       const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
       const uint32_t ps = tc::smem_u32(smem + L::OFF_P);
+      KDBG(1, -1, 2);
       tc::mbar_wait(&bars->q_full, 0);
       auto issue_pv = [&](int j) {  // O += P(j) V(j)
+        KDBG(1, j, 3);
         tc::mbar_wait(&bars->p_full, j & 1);
         tc::fence_after_sync();
         const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (j & 1) * L::KV_BYTES);
@@ -272,7 +294,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       for (int i = 0; i < n_tc; ++i) {
         const int s = i & 1;
+        KDBG(1, i, 4);
         tc::mbar_wait(&bars->full[s], (i >> 1) & 1);
+        KDBG(1, i, 5);
         tc::mbar_wait(&bars->s_empty[s], ((i >> 1) & 1) ^ 1);
         tc::fence_after_sync();
         const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
@@ -336,6 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       my_cells += __popc(mk[0]) + __popc(mk[1]);
+      if (tid == 0) KDBG(2, i, 6);
       tc::mbar_wait(&bars->s_full[s], (i >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t s_addr = tmem + s * 128 + lane_base + wg * 64;
@@ -354,6 +379,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float m_tile = tm == -INFINITY ? -INFINITY : tm * p.scale_log2;
       // previous PV must be done before P is overwritten or O is rescaled
       if (i > 0) {
+        if (tid == 0) KDBG(2, i, 7);
         tc::mbar_wait(&bars->pv_done, (i - 1) & 1);
         tc::fence_after_sync();
       }
@@ -407,6 +433,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // O (TMEM) -> registers, relative to m_ref
     float o[DH];
     if (n_tc > 0) {
+      if (tid == 0) KDBG(2, n_tc, 8);
       tc::mbar_wait(&bars->pv_done, (n_tc - 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
@@ -436,6 +463,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int kr = c - max(0, g0 - dd);  // row of key c in the staged range
         bool v = row_ok && c >= 0;
         if (v) v = !bit_of(kb_bits, c / BN) && !bit_of(vbits, c);
+        if (tid == 0) KDBG(2, t, 10);
         tc::mbar_wait(&bars->full[s], (t >> 1) & 1);
         float acc = 0.f;
         if (v) {
@@ -573,6 +601,8 @@ __global__ void reverse_bits_kernel(const int32_t *slash_ids, const int32_t *cou
 }  // namespace k5ws
 
 // ------------------------------------------------------------------ host
+static int *g_debug_buffer = nullptr;
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -674,6 +704,7 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   p.out = out;
   p.out_bf16 = out_bf16;
   p.cells = reinterpret_cast<long long *>(cells);
+  p.dbg = g_debug_buffer;
   LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * H, st));
   dim3 grid(nqt, H);
   if (d == 128) {
@@ -690,3 +721,8 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
 }
 
 }  // namespace ls
+
+extern "C" int ls_debug_set_buffer(void *host_mapped) {
+  ls::g_debug_buffer = static_cast<int *>(host_mapped);
+  return LS_OK;
+}

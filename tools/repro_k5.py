@@ -25,9 +25,22 @@ rows = pf.sample_rows_device(n_new, 0.1, 32, 3, 1, 0, 0, n_q)
 plans = pf.sparsify_layer(qb, K, rows, 0.955, n_new, n_total, n_kv)
 torch.cuda.synchronize()
 print("plans ok", plans.counts.cpu().tolist())
-out_tc, cells_tc = tops.attention_layer(qb, K, V, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total,
-                                        n_kv, out_dtype=torch.float32)
-torch.cuda.synchronize()
+n_cta = ((n_new + 127) // 128) * n_q
+dbg = torch.full((n_cta * 16,), -7, dtype=torch.int32).pin_memory()
+if os.environ.get("LS_DEBUG"):
+    _lib.lib().ls_debug_set_buffer(dbg.data_ptr())
+try:
+    out_tc, cells_tc = tops.attention_layer(qb, K, V, plans.slash_ids, plans.vert_ids, plans.counts, n_new,
+                                            n_total, n_kv, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+except Exception as e:  # noqa: BLE001
+    print("FAILED:", e)
+    d = dbg.view(n_cta, 4, 4).tolist()
+    names = ["producer", "mma", "softmax", "counts"]
+    for i, rec in enumerate(d):
+        print("cta", i, {names[r]: rec[r][:2] if r < 3 else rec[r] for r in range(4)})
+    sys.exit(1)
+_lib.lib().ls_debug_set_buffer(None)
 L = pf.layer_desc(n_q, n_kv, d, n_new, n_total, qb.stride(0), K.stride(0))
 out_s = torch.empty_like(out_tc)
 cells_s = torch.empty_like(cells_tc)
