@@ -383,21 +383,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_wait(&bars->pv_done, (i - 1) & 1);
         tc::fence_after_sync();
       }
-      if (m_tile > m_ref + RESCALE_LOG2) {
-        if (m_ref != -INFINITY) {  // O holds data scaled by exp2(-m_ref)
-          const float corr = fast_exp2(m_ref - m_tile);
+      const bool need = m_tile > m_ref + RESCALE_LOG2;
+      // TMEM ld/st are .sync.aligned: the whole warp rescales if any row needs it
+      if (__any_sync(0xffffffffu, need && m_ref != -INFINITY && i > 0)) {
+        const float corr = (need && m_ref != -INFINITY) ? fast_exp2(m_ref - m_tile) : 1.f;
 #pragma unroll
-          for (int cch = 0; cch < DH / 32; ++cch) {
-            float ov[32];
-            tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
-            tc::tmem_wait_ld();
+        for (int cch = 0; cch < DH / 32; ++cch) {
+          float ov[32];
+          tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
+          tc::tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) ov[j] *= corr;
-            tc::tmem_st32(tmem_o + lane_base + wg * DH + cch * 32, ov);
-          }
-          tc::tmem_wait_st();
-          l *= corr;
+          for (int j = 0; j < 32; ++j) ov[j] *= corr;
+          tc::tmem_st32(tmem_o + lane_base + wg * DH + cch * 32, ov);
         }
+        tc::tmem_wait_st();
+      }
+      if (need) {
+        if (m_ref != -INFINITY) l *= fast_exp2(m_ref - m_tile);
         m_ref = m_tile;
       }
       float lsum = 0.f;
