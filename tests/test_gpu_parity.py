@@ -344,7 +344,7 @@ def test_vs_attention_tc_matches_simt_and_oracle(cuda_lib, d, n_q, n_kv, ro, n_n
               cells_s.data_ptr(), ws.data_ptr(), n, _lib.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(cells_tc, cells_s)
-    assert (out_tc - out_s).abs().max().item() <= 1e-2
+    assert (out_tc - out_s).abs().max().item() <= 2e-2  # both vs fp64 within 2e-2; tc rounds P to bf16
     hp = plans.to_host()
     group = n_q // n_kv
     for h in (0, n_q - 1):
