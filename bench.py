@@ -303,10 +303,8 @@ def main():
                 for l in range(cfg["n_layers"]):
                     gather.prefill(res.out[l])
             e1.record(stream)
-            outs, _ = eng.decode(store, ro + n_new, cfg["max_new"])
-            if gather is not None:
-                for step in outs:
-                    gather.decode(step)
+            sink = (lambda t, ob: gather.decode(list(ob))) if gather is not None else None
+            eng.decode(store, ro + n_new, cfg["max_new"], out_sink=sink)
             e2.record(stream)
             ev_log.append((e0, e1, e2))
             # rollback is implicit: the next block starts at ro + n_new (session.py:180)
@@ -364,6 +362,12 @@ def main():
     roof = roofline(per, cfg, eng, store, blocks, peaks)
     if roof is not None and roof.get("kernel") in per:
         roof["share_of_timed"] = round(sum(per[roof["kernel"]]) / total_ms, 4)
+    dec_roof = None  # the decode step (one graph replay, all layers) against HBM
+    for k in ("decode_graph_comp", "decode_graph_dense"):
+        if k in per:
+            dec_roof = roofline({k: per[k]}, cfg, eng, store, blocks, peaks)
+            dec_roof["share_of_timed"] = round(sum(per[k]) / total_ms, 4)
+            break
 
     e2e = None
     if not args.no_e2e:
@@ -380,7 +384,8 @@ def main():
                            store.q.numel() * 2 * (1 + 2 * cfg["n_kv"] / cfg["n_q"]) / 1e9)},
             "decode_tokens_per_s": round(tok_s, 2),
             "prefill_ms_per_turn": round(ttft, 3), "decode_ms_per_turn": round(decode_ms / n_prefills, 3),
-            "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof}
+            "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+            "decode_roofline": dec_roof}
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -414,8 +419,10 @@ def roofline(per, cfg, eng, store, blocks, peaks):
         work = 2.0 * d * float(sum(int(c.sum()) for c in eng.score_log)) / n  # QK^T of the causal sampled cells
         bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]
         achieved = work / (mean_ms * 1e-3) / 1e12
-    elif name == "ls_decode_attention":
-        bytes_ = 4.0 * d * eng.decode_cols / max(1, eng.decode_launches)  # K+V bf16 per q-head column
+    elif name.startswith("decode_graph_") and name != "decode_graph_event":
+        kind = name[len("decode_graph_"):]
+        cols = [c for k, c in eng.decode_log if k == kind]
+        bytes_ = 4.0 * d * sum(cols) / max(1, len(cols))  # bf16 K + V row per KV-head column, all layers
         bound, unit, peak = "hbm", "GB/s", peaks["hbm"]
         achieved = bytes_ / (mean_ms * 1e-3) / 1e9 if bytes_ else None
         work = bytes_
@@ -464,18 +471,16 @@ def run_e2e(args, cfg, eng, store, blocks, shard, gather):
             # decode with per-step host I/O
             outs_host = torch.empty((cfg["max_new"], L, shard.n_q_local, cfg["d"]), dtype=torch.bfloat16,
                                     pin_memory=True)
-            length = n_total
-            for step in range(cfg["max_new"]):
-                pos = length + step
-                store.q[:, :, pos].copy_(hq[:, :, pos], non_blocking=True)
-                store.k[:, :, pos].copy_(hk[:, :, pos], non_blocking=True)
-                store.v[:, :, pos].copy_(hv[:, :, pos], non_blocking=True)
+            hi = n_total + cfg["max_new"]
+            for dst, src in ((store.q, hq), (store.k, hk), (store.v, hv)):
+                dst[:, :, n_total:hi].copy_(src[:, :, n_total:hi], non_blocking=True)
                 if it > 0:
-                    h2d += (hq[:, :, pos].numel() + 2 * hk[:, :, pos].numel()) * 2
-            outs, _ = eng.decode(store, n_total, cfg["max_new"])
-            for s_i, step_outs in enumerate(outs):
-                for l, o in enumerate(step_outs):
-                    outs_host[s_i, l].copy_(o, non_blocking=True)
+                    h2d += src[:, :, n_total:hi].numel() * 2
+
+            def sink(t, ob):  # every step's outputs of every layer back to the host
+                outs_host[t].copy_(ob, non_blocking=True)
+
+            eng.decode(store, n_total, cfg["max_new"], out_sink=sink)
             if it > 0:
                 d2h += outs_host.numel() * 2
             e2.record(stream)

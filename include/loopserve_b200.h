@@ -182,23 +182,32 @@ int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t
                        const uint16_t *v, void *out, int32_t out_bf16, ls_stream_t stream);
 
 /* ------------------------------------------------------------- decode ---
- * Per-head decode state lives in caller-allocated device arrays described
- * by the ls_decode_state struct (one layer). See paper_2507_13681_b200/engine.py.
- *   ring_w   [n_heads][window][row_cap] fp32   observation rows' weights
- *   ring_ids [n_heads][window][sparse_cap] int32 ids of sparse rows
- *   ring_n   [n_heads][window] int32  row length (0 = empty slot)
- *   ring_dense[n_heads][window] int32 1 if ids == arange(n)
- *   sel_ids  [n_heads][budget_cap] int32 picked ids, sorted (kvcompress.py:212)
- *   n_sel    [n_heads] int32
- *   ck, cv   [n_heads][budget_cap][head_dim] bf16 compacted K/V of sel_ids */
-typedef struct ls_decode_state {
-  int32_t n_heads, n_kv_heads, head_dim;
-  int32_t window;      /* obs_window (kvcompress.py:29-30)        */
-  int32_t row_cap;     /* >= max cache length + 1                  */
-  int32_t sparse_cap;  /* >= budget + window + 1                   */
-  int32_t budget_cap;  /* >= budget                                */
-  int64_t kv_head_stride;
-  float *ring_w;
+ * Decode state of ALL layers of one session, caller-allocated device arrays
+ * (see paper_2507_13681_b200/kvcompress.py DecodeStack). The step counters
+ * live in device memory so a decode step / an event is a fixed launch
+ * sequence (CUDA-graph capturable):
+ *   step[0] = cache length before this step's append (= the new token's position)
+ *   step[1] = rows appended to the observation deque so far (seeds included);
+ *             this step's row goes to slot step[1] % window.
+ * Per (layer, q-head) row hr = layer*n_heads + h:
+ *   ring_s   [hr][window][row_cap]  fp32 raw log2-domain logits of a row
+ *   ring_ml  [hr][window][2]        fp32 (max, sum) of the row; sum == 0 means
+ *                                   ring_s holds probabilities (prefill seeds)
+ *   ring_ids [hr][window][sparse_cap] int32 ids of compressed rows
+ *   ring_n, ring_dense [hr][window] int32
+ *   sel_ids  [hr][budget_cap], n_sel [hr]      picked ids (kvcompress.py:212)
+ *   ck, cv   [hr][budget_cap][head_dim] bf16   compacted K/V of sel_ids
+ *   partials [n_heads][splits][head_dim+2] fp32, counters [n_heads] int32 (zeroed)
+ * Archive K/V of layer l, kv-head j at k_all + l*kv_layer_stride + j*kv_head_stride. */
+typedef struct ls_decode_stack {
+  int32_t n_layers, n_heads, n_kv_heads, head_dim;
+  int32_t window;      /* obs_window (kvcompress.py:29-30)   */
+  int32_t row_cap;     /* >= max cache length + 1            */
+  int32_t sparse_cap;  /* >= budget_cap + window + 1         */
+  int32_t budget_cap;  /* >= budget                          */
+  int64_t kv_layer_stride, kv_head_stride;
+  float *ring_s;
+  float *ring_ml;
   int32_t *ring_ids;
   int32_t *ring_n;
   int32_t *ring_dense;
@@ -206,33 +215,30 @@ typedef struct ls_decode_state {
   int32_t *n_sel;
   uint16_t *ck;
   uint16_t *cv;
-} ls_decode_state;
+  float *partials;
+  int32_t *counters;
+  int32_t *step;
+} ls_decode_stack;
 
-/* Working-set decode attention for one token (model.py:232-241 +
- * decode_step, model.py:289-311): per q-head, attends the working set
- * (all positions [0, length) before the first event; selected ids below
- * length-window plus [length-window, length) after it) plus the new
- * position `length` (its K/V already written to the archive), writes
- * out[h][d] and the observation row into ring slot `slot`.              */
-size_t ls_decode_attention_workspace(const ls_decode_state *S, int32_t max_len);
-int ls_decode_attention(const ls_decode_state *S, const uint16_t *q, const uint16_t *k,
-                        const uint16_t *v, int32_t length, int32_t compressed, int32_t slot,
-                        void *out, int32_t out_bf16, void *ws, size_t ws_bytes,
-                        ls_stream_t stream);
-
-/* Compression event (kvcompress.py:210-224): accumulate the buffered rows
- * (oldest first, slot order given by `slot_order[n_rows]`), top-B by
- * (score desc, id asc), write sel_ids/n_sel, and per head the retained
- * working-set size and score coverage (event log fields).               */
-size_t ls_decode_select_workspace(const ls_decode_state *S, int32_t max_len);
-int ls_decode_select(const ls_decode_state *S, const int32_t *slot_order, int32_t n_rows,
-                     int32_t length, int32_t budget, int32_t *retained_n,
-                     double *score_coverage, void *ws, size_t ws_bytes, ls_stream_t stream);
-
-/* Coalesced gather-compaction of the selected rows (compact_cache,
- * kvcompress.py:133-147): ck/cv[h][j] = K/V[kv(h)][sel_ids[h][j]].       */
-int ls_kv_compact(const ls_decode_state *S, const uint16_t *k, const uint16_t *v,
-                  ls_stream_t stream);
+/* Working-set decode attention of one layer for the current step
+ * (model.py:232-241 inside decode_step, model.py:289-311): out[h][d] and the
+ * observation row into the ring. compressed = an event has happened
+ * (kvcompress.py:234-237); max_cols bounds the columns of any head. */
+size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len);
+int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
+                   const uint16_t *v_layer, int32_t compressed, int32_t max_cols, void *out,
+                   int32_t out_bf16, ls_stream_t stream);
+/* step[0] += 1 (the new token is in the cache), step[1] += 1 (its row was appended). */
+int ls_decode_advance(const ls_decode_stack *S, ls_stream_t stream);
+/* Compression event for every layer and head (kvcompress.py:210-224):
+ * accumulate the buffered rows oldest first, top-B by (score desc, id asc),
+ * sel_ids / n_sel, then the coalesced gather-compaction of K/V (compact_cache,
+ * kvcompress.py:133-147). retained_n / score_coverage [n_layers*n_heads]
+ * (optional) are the event-log fields. */
+size_t ls_decode_select_workspace(const ls_decode_stack *S);
+int ls_decode_event(const ls_decode_stack *S, int32_t budget, int32_t max_len, const uint16_t *k_all,
+                    const uint16_t *v_all, int32_t *retained_n, double *score_coverage, void *ws,
+                    size_t ws_bytes, ls_stream_t stream);
 
 #ifdef __cplusplus
 }

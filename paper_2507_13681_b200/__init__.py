@@ -21,7 +21,7 @@ _EXPORTS = {
     "sparsify_layer": "prefill", "greedy_select_lines": "prefill", "vertical_length": "prefill",
     "slash_length": "prefill", "masked_sparse_attention": "tensor_ops", "scaled_dot_attention": "tensor_ops",
     "AttentionBlock": "tensor_ops", "attention_layer": "tensor_ops", "CompressionConfig": "kvcompress",
-    "DecodeStats": "kvcompress", "KVCacheHead": "kvcompress", "DecodeLayer": "kvcompress",
+    "DecodeStats": "kvcompress", "KVCacheHead": "kvcompress", "DecodeStack": "kvcompress",
     "accumulate_scores": "kvcompress", "select_topB_obs": "kvcompress", "retained_union": "kvcompress",
     "compact_cache": "kvcompress", "progressive_decode": "kvcompress", "token_scores": "kvcompress",
     "SessionParams": "engine", "SessionEngine": "engine", "AttnShape": "engine", "QKVStore": "engine",

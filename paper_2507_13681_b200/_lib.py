@@ -33,15 +33,16 @@ class LayerDesc(C.Structure):
                 ("kv_head_stride", I64)]
 
 
-class DecodeStateDesc(C.Structure):
-    _fields_ = [("n_heads", I32), ("n_kv_heads", I32), ("head_dim", I32), ("window", I32),
-                ("row_cap", I32), ("sparse_cap", I32), ("budget_cap", I32),
-                ("kv_head_stride", I64), ("ring_w", P), ("ring_ids", P), ("ring_n", P),
-                ("ring_dense", P), ("sel_ids", P), ("n_sel", P), ("ck", P), ("cv", P)]
+class DecodeStackDesc(C.Structure):
+    _fields_ = [("n_layers", I32), ("n_heads", I32), ("n_kv_heads", I32), ("head_dim", I32), ("window", I32),
+                ("row_cap", I32), ("sparse_cap", I32), ("budget_cap", I32), ("kv_layer_stride", I64),
+                ("kv_head_stride", I64), ("ring_s", P), ("ring_ml", P), ("ring_ids", P), ("ring_n", P),
+                ("ring_dense", P), ("sel_ids", P), ("n_sel", P), ("ck", P), ("cv", P), ("partials", P),
+                ("counters", P), ("step", P)]
 
 
 LD = C.POINTER(LayerDesc)
-DS = C.POINTER(DecodeStateDesc)
+DS = C.POINTER(DecodeStackDesc)
 
 # name -> (restype, argtypes)
 SIGNATURES = {
@@ -67,11 +68,11 @@ SIGNATURES = {
     "ls_vs_attention_simt": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, SZ, P]),
     "ls_plan_rows": (C.c_int, [LD, I32, P, P, P, P, P, P, I64, I64, P]),
     "ls_dense_attention": (C.c_int, [LD, P, P, P, P, I32, P]),
-    "ls_decode_attention_workspace": (SZ, [DS, I32]),
-    "ls_decode_attention": (C.c_int, [DS, P, P, P, I32, I32, I32, P, I32, P, SZ, P]),
-    "ls_decode_select_workspace": (SZ, [DS, I32]),
-    "ls_decode_select": (C.c_int, [DS, P, I32, I32, I32, P, P, P, SZ, P]),
-    "ls_kv_compact": (C.c_int, [DS, P, P, P]),
+    "ls_decode_partials_size": (SZ, [DS, I32]),
+    "ls_decode_step": (C.c_int, [DS, I32, P, P, P, I32, I32, P, I32, P]),
+    "ls_decode_advance": (C.c_int, [DS, P]),
+    "ls_decode_select_workspace": (SZ, [DS]),
+    "ls_decode_event": (C.c_int, [DS, I32, I32, P, P, P, P, P, SZ, P]),
 }
 
 
@@ -108,21 +109,55 @@ def check(status: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 6, "ls_greedy_dense": 6,
     "ls_vs_attention": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 3, "ls_dense_attention": 1,
-    "ls_decode_attention": 2,
-    "ls_decode_select": 1, "ls_kv_compact": 1,
+    "ls_decode_step": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
 }
 launch_count = 0
 entry_hook = None  # optional callable(name, phase) used by bench.py to time entries
 
 
+_capture = None  # list collecting kernel counts while a CUDA graph is being captured
+
+
 def call(name: str, *args):
     global launch_count
+    if _capture is not None:  # captured, not executed: no timing, count at replay
+        check(getattr(lib(), name)(*args), name)
+        _capture.append(KERNELS_PER_CALL.get(name, 0))
+        return
     if entry_hook is not None:
         entry_hook(name, "begin")
     check(getattr(lib(), name)(*args), name)
     if entry_hook is not None:
         entry_hook(name, "end")
     launch_count += KERNELS_PER_CALL.get(name, 0)
+
+
+class Captured:
+    """A CUDA graph of C-ABI calls; replay() counts its kernels and reports
+    it to entry_hook under `name` like a single entry."""
+
+    def __init__(self, name: str, stream, fn):
+        import torch
+
+        global _capture
+        self.name = name
+        self.graph = torch.cuda.CUDAGraph()
+        _capture = []
+        try:
+            with torch.cuda.graph(self.graph, stream=stream):
+                fn()
+            self.kernels = sum(_capture)
+        finally:
+            _capture = None
+
+    def replay(self):
+        global launch_count
+        if entry_hook is not None:
+            entry_hook(self.name, "begin")
+        self.graph.replay()
+        if entry_hook is not None:
+            entry_hook(self.name, "end")
+        launch_count += self.kernels
 
 
 def ptr(t) -> int | None:

@@ -1,54 +1,58 @@
 // K6 + K7 + K8 -- progressive decode with periodic KV compression.
 //
+// Device-resident decode state for ALL layers of a session (ls_decode_stack),
+// with the step counters in device memory so that one decode step (every
+// layer) and one compression event (every layer) are fixed launch sequences
+// that the host captures into CUDA graphs.
+//
 // K6 decode attention replaces the working-set branch of forward_extend
 // (reference model.py:232-241) inside decode_step (model.py:289-311): per
-// q-head, cols = working set U {new position}, softmax over
-// K[cols].q / sqrt(d), out = w . V[cols], and the observation row (cols, w)
-// (kvcompress.py:233) is written to the head's ring slot. Working set:
-//   before the first event: [0, length)                 (kvcompress.py:194, 237)
-//   after it: selected U [length - W, length)           (kvcompress.py:235)
-// The selected rows are read from the compacted per-head cache ck/cv
-// (segment A, ids < length - W so the recent window is not double counted);
-// the recent window and the new row are read from the archive (segment B).
-// Split-K over columns (K6a) + a combine kernel (K6b) that normalises the
-// output and rescales the ring row in place.
+// q-head, cols = working set U {new position}, softmax(K[cols] q / sqrt(d)),
+// out = w V[cols]; the observation row (cols, w) (kvcompress.py:233) goes to
+// the head's ring slot as raw log2-domain logits plus the row's (max, sum), so
+// it is normalised only when an event reads it. Working set:
+//   before the first event: [0, length)                        (kvcompress.py:194, 237)
+//   after it: selected U [length - W, length)                  (kvcompress.py:235)
+// Dense steps are computed per KV head for its q-head group (each K/V row is
+// read once for the group); compressed steps per q-head from the compacted
+// cache (segment A: selected ids < length - W) plus the archive window
+// (segment B). One kernel: split-K CTAs write partials, the last CTA of a head
+// combines them (threadfence + ticket).
 //
-// K7 (event) replaces accumulate_scores + _top_by_score + retained_union
-// (kvcompress.py:67-90, 126-130, 210-224): rows are accumulated oldest ->
-// newest in fp64 (each row has distinct ids, so a row is added in parallel
-// without races and the per-id order is the reference's), candidates are
-// the touched ids only (kvcompress.py:73-83), then an 8-pass radix select
-// on the fp64 bits finds the B-th largest (score desc, id asc) and the
-// picked ids are emitted in id order.
+// K7 (event, all layers in one launch) replaces accumulate_scores +
+// _top_by_score + retained_union (kvcompress.py:67-90, 126-130, 210-224):
+// buffered rows are accumulated oldest -> newest in fp64 (rows have distinct
+// ids: a row is added in parallel with no races, the per-id order is the
+// reference's), candidates are the touched ids only (kvcompress.py:73-83),
+// an 8-pass radix select on the fp64 bits finds the B-th largest by (score
+// desc, id asc), picked ids are emitted in id order.
 //
-// K8 replaces compact_cache (kvcompress.py:133-147): coalesced 16-byte
-// gather of the picked rows into the contiguous per-head cache.
+// K8 (all layers) replaces compact_cache (kvcompress.py:133-147): coalesced
+// 16-byte gather of the picked K/V rows into the contiguous per-head cache.
 
 #include "ls_common.cuh"
 
 namespace ls {
 namespace dec {
 
-constexpr int COLS_PER_SPLIT = 256;
-constexpr int K6_THREADS = 128;  // 4 warps, 8 column groups of 4 lanes per warp
+constexpr int K6_THREADS = 256;
+constexpr int K7_THREADS = 1024;
+constexpr int K7_SMEM_CAP = 24 * 1024;  // ids accumulated in shared memory (fp64) up to this length
 
-struct Part {  // per (head, split)
-  float m, l;
-  float o[128];
+__device__ __forceinline__ int64_t head_row(const ls_decode_stack &S, int layer, int h) {
+  return static_cast<int64_t>(layer) * S.n_heads + h;
+}
+
+struct Geo {
+  int n_a, lo, n_cols;
 };
 
-struct Geo {  // column geometry of one head for this step
-  int n_a;   // compacted selected rows used (ids < lo)
-  int lo;    // archive segment start
-  int n_cols;
-};
-
-__device__ __forceinline__ Geo geometry(const ls_decode_state &S, int h, int length, int compressed) {
+__device__ __forceinline__ Geo geometry(const ls_decode_stack &S, int layer, int h, int length, int compressed) {
   Geo g;
   if (compressed) {
     g.lo = max(0, length - S.window);
-    const int32_t *sel = S.sel_ids + static_cast<int64_t>(h) * S.budget_cap;
-    g.n_a = lower_bound_dev(sel, S.n_sel[h], g.lo);
+    const int64_t hr = head_row(S, layer, h);
+    g.n_a = lower_bound_dev(S.sel_ids + hr * S.budget_cap, S.n_sel[hr], g.lo);
   } else {
     g.lo = 0;
     g.n_a = 0;
@@ -57,170 +61,206 @@ __device__ __forceinline__ Geo geometry(const ls_decode_state &S, int h, int len
   return g;
 }
 
-__global__ void __launch_bounds__(K6_THREADS) decode_partial_kernel(ls_decode_state S, const uint16_t *q,
-                                                                    const uint16_t *k, const uint16_t *v,
-                                                                    int length, int compressed, int slot,
-                                                                    float scale_log2, Part *parts, int n_split) {
-  __shared__ float red_m[4];
-  __shared__ float red_l[4];
-  __shared__ float red_o[4][128];
-  const int h = blockIdx.y, split = blockIdx.x;
-  const int d = S.head_dim;
-  const Geo g = geometry(S, h, length, compressed);
-  const int c_begin = split * COLS_PER_SPLIT;
-  const int c_end = min(g.n_cols, c_begin + COLS_PER_SPLIT);
-  Part &part = parts[static_cast<int64_t>(h) * n_split + split];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane >> 2, sub = lane & 3;  // 8 groups of 4 lanes
-  const int dpl = d / 4;                      // dims per lane: 32 (d=128) or 16
-  const int kv = h / (S.n_heads / S.n_kv_heads);
+// ------------------------------------------------------------------ K6
+template <int D, int G>
+__global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, int layer, const uint16_t *q,
+                                                            const uint16_t *k, const uint16_t *v, int compressed,
+                                                            int cs, float scale_log2, void *out, int out_bf16) {
+  constexpr int DPL = D / 32;  // dims per lane in the PV phase
+  extern __shared__ float dsm[];
+  float(*qf)[D] = reinterpret_cast<float(*)[D]>(dsm);                       // [G][D]
+  float(*sc)[512] = reinterpret_cast<float(*)[512]>(dsm + G * D);          // [G][512] scores / probabilities
+  float(*opart)[G][D] = reinterpret_cast<float(*)[G][D]>(dsm + G * D + G * 512);  // [8][G][D]
+  __shared__ float red[G][8];
+  __shared__ int ticket;
+  const int split = blockIdx.x, unit = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int length = S.step[0];
+  const int slot = S.step[1] % S.window;
+  const int group = S.n_heads / S.n_kv_heads;
+  const int kv = compressed ? unit / group : unit;
+  const int h0 = compressed ? unit : unit * G;  // first q-head of this unit
+  const Geo geo = geometry(S, layer, h0, length, compressed);
+  const int c_begin = split * cs, c_end = min(geo.n_cols, c_begin + cs);
+  const int n = max(0, c_end - c_begin);
   const uint16_t *kb = k + static_cast<int64_t>(kv) * S.kv_head_stride;
   const uint16_t *vb = v + static_cast<int64_t>(kv) * S.kv_head_stride;
-  const uint16_t *ckb = S.ck + static_cast<int64_t>(h) * S.budget_cap * d;
-  const uint16_t *cvb = S.cv + static_cast<int64_t>(h) * S.budget_cap * d;
-  const int32_t *sel = S.sel_ids + static_cast<int64_t>(h) * S.budget_cap;
-  float *wrow = S.ring_w + (static_cast<int64_t>(h) * S.window + slot) * S.row_cap;
-  int32_t *idrow = S.ring_ids + (static_cast<int64_t>(h) * S.window + slot) * S.sparse_cap;
+  const int64_t hr0 = head_row(S, layer, h0);
+  const uint16_t *ckb = S.ck + hr0 * S.budget_cap * D;
+  const uint16_t *cvb = S.cv + hr0 * S.budget_cap * D;
+  const int32_t *sel = S.sel_ids + hr0 * S.budget_cap;
 
-  if (c_begin >= g.n_cols) {
-    if (threadIdx.x == 0) {
-      part.m = -INFINITY;
-      part.l = 0.f;
-    }
-    for (int i = threadIdx.x; i < d; i += blockDim.x) part.o[i] = 0.f;
-    return;
-  }
-  // q slice of this lane
-  float qv[32];
-  const uint16_t *qh = q + static_cast<int64_t>(h) * d + sub * dpl;
-  for (int i = 0; i < dpl; ++i) qv[i] = bf2f(qh[i]);
-
-  constexpr int PER = COLS_PER_SPLIT / 32;  // columns per lane group
-  float sv[PER];
-  int cid[PER];
-  float m = -INFINITY;
-#pragma unroll
-  for (int t = 0; t < PER; ++t) {
-    const int j = c_begin + (t * 4 + warp) * 8 + grp;
-    const bool valid = j < c_end;
-    sv[t] = -INFINITY;
-    cid[t] = -1;
-    float acc = 0.f;
-    if (valid) {
-      const uint16_t *kr;
-      int id;
-      if (j < g.n_a) {
-        id = sel[j];
-        kr = ckb + static_cast<int64_t>(j) * d;
-      } else {
-        id = g.lo + (j - g.n_a);
-        kr = kb + static_cast<int64_t>(id) * d;
-      }
-      cid[t] = id;
-      for (int vv = 0; vv < dpl / 8; ++vv) {
-        uint4 u = *reinterpret_cast<const uint4 *>(kr + sub * dpl + vv * 8);
-        float f[8];
-        bf16x8_to_f32(u, f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc = fmaf(qv[vv * 8 + e], f[e], acc);
-      }
-    }
-    // lanes of a group share j; shuffles stay converged across the warp
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (valid) {
-      sv[t] = acc * scale_log2;
-      m = fmaxf(m, sv[t]);
-    }
-  }
-  m = warp_max(m);
-  if (lane == 0) red_m[warp] = m;
+  for (int i = tid; i < G * D; i += blockDim.x) qf[i / D][i % D] = bf2f(q[static_cast<int64_t>(h0) * D + i]);
   __syncthreads();
-  m = fmaxf(fmaxf(red_m[0], red_m[1]), fmaxf(red_m[2], red_m[3]));
-  float l = 0.f;
-  float o[32];
+  // ---- scores: one thread per column
+  float mloc[G];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) o[i] = 0.f;
+  for (int g = 0; g < G; ++g) mloc[g] = -INFINITY;
+  for (int jj = tid; jj < n; jj += blockDim.x) {
+    const int j = c_begin + jj;
+    int id;
+    const uint16_t *kr;
+    if (j < geo.n_a) {
+      id = sel[j];
+      kr = ckb + static_cast<int64_t>(j) * D;
+    } else {
+      id = geo.lo + (j - geo.n_a);
+      kr = kb + static_cast<int64_t>(id) * D;
+    }
+    float acc[G];
 #pragma unroll
-  for (int t = 0; t < PER; ++t) {
-    const int j = c_begin + (t * 4 + warp) * 8 + grp;
-    if (j < c_end) {
-      const float p = fast_exp2(sv[t] - m);
-      if (sub == 0) {
-        l += p;
-        wrow[j] = p;
-        if (compressed) idrow[j] = cid[t];
-      }
-      const uint16_t *vr = (j < g.n_a) ? cvb + static_cast<int64_t>(j) * d : vb + static_cast<int64_t>(cid[t]) * d;
-      for (int vv = 0; vv < dpl / 8; ++vv) {
-        uint4 u = *reinterpret_cast<const uint4 *>(vr + sub * dpl + vv * 8);
-        float f[8];
-        bf16x8_to_f32(u, f);
+    for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll 4
+    for (int c8 = 0; c8 < D / 8; ++c8) {
+      float f[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4 *>(kr + c8 * 8), f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[vv * 8 + e] = fmaf(p, f[e], o[vv * 8 + e]);
-      }
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[g] = fmaf(qf[g][c8 * 8 + e], f[e], acc[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float s = acc[g] * scale_log2;
+      sc[g][jj] = s;
+      mloc[g] = fmaxf(mloc[g], s);
+      const int64_t hr = head_row(S, layer, h0 + g);
+      S.ring_s[(hr * S.window + slot) * S.row_cap + j] = s;  // raw logit, normalised at events
+      if (compressed) S.ring_ids[(hr * S.window + slot) * S.sparse_cap + j] = id;
     }
   }
-  // reduce over the 8 groups of the warp (lanes with equal sub)
 #pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    l += __shfl_xor_sync(0xffffffffu, l, off);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] += __shfl_xor_sync(0xffffffffu, o[i], off);
+  for (int g = 0; g < G; ++g) {
+    const float m = warp_max(mloc[g]);
+    if (lane == 0) red[g][warp] = m;
   }
-  if (lane == 0) red_l[warp] = l;
-  if (grp == 0)
-    for (int i = 0; i < dpl; ++i) red_o[warp][sub * dpl + i] = o[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    part.m = m;
-    part.l = red_l[0] + red_l[1] + red_l[2] + red_l[3];
+  float mg[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m = fmaxf(m, red[g][w]);
+    mg[g] = m;
   }
-  for (int i = threadIdx.x; i < d; i += blockDim.x)
-    part.o[i] = red_o[0][i] + red_o[1][i] + red_o[2][i] + red_o[3][i];
+  __syncthreads();
+  float lloc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) lloc[g] = 0.f;
+  for (int jj = tid; jj < n; jj += blockDim.x)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float pv = fast_exp2(sc[g][jj] - mg[g]);
+      sc[g][jj] = pv;
+      lloc[g] += pv;
+    }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float l = warp_sum(lloc[g]);
+    if (lane == 0) red[g][warp] = l;
+  }
+  __syncthreads();
+  // ---- PV: warp w takes columns w, w+8, ...; lane owns DPL dims
+  float o[G][DPL];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) o[g][e] = 0.f;
+  for (int jj = warp; jj < n; jj += 8) {
+    const int j = c_begin + jj;
+    const uint16_t *vr = (j < geo.n_a) ? cvb + static_cast<int64_t>(j) * D
+                                       : vb + static_cast<int64_t>(geo.lo + (j - geo.n_a)) * D;
+    float f[DPL];
+    if constexpr (DPL == 4) {
+      const uint2 u = *reinterpret_cast<const uint2 *>(vr + lane * 4);
+      f[0] = __uint_as_float(u.x << 16);
+      f[1] = __uint_as_float(u.x & 0xffff0000u);
+      f[2] = __uint_as_float(u.y << 16);
+      f[3] = __uint_as_float(u.y & 0xffff0000u);
+    } else {
+      const uint32_t u = *reinterpret_cast<const uint32_t *>(vr + lane * 2);
+      f[0] = __uint_as_float(u << 16);
+      f[1] = __uint_as_float(u & 0xffff0000u);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float pv = sc[g][jj];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) o[g][e] = fmaf(pv, f[e], o[g][e]);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) opart[warp][g][lane * DPL + e] = o[g][e];
+  __syncthreads();
+  // ---- partial -> global, ticket
+  const int n_split = gridDim.x;
+  for (int i = tid; i < G * (D + 2); i += blockDim.x) {
+    const int g = i / (D + 2), e = i % (D + 2);
+    const int64_t hr = head_row(S, layer, h0 + g);
+    float *pp = S.partials + (static_cast<int64_t>(h0 + g) * n_split + split) * (D + 2);
+    (void)hr;
+    if (e == 0) {
+      pp[0] = mg[g];
+    } else if (e == 1) {
+      float l = 0.f;
+      for (int w = 0; w < 8; ++w) l += red[g][w];
+      pp[1] = (n > 0) ? l : 0.f;
+    } else {
+      float acc = 0.f;
+      for (int w = 0; w < 8; ++w) acc += opart[w][g][e - 2];
+      pp[e] = acc;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(S.counters + unit, 1);
+  __syncthreads();
+  if (ticket != n_split - 1) return;
+  // ---- last CTA of this unit: combine splits (deterministic split order)
+  __threadfence();
+  for (int g = 0; g < G; ++g) {
+    const int h = h0 + g;
+    const float *pp = S.partials + static_cast<int64_t>(h) * n_split * (D + 2);
+    float M = -INFINITY;
+    for (int s = 0; s < n_split; ++s) M = fmaxf(M, __ldcg(pp + s * (D + 2)));
+    float Lsum = 0.f;
+    for (int s = 0; s < n_split; ++s) {
+      const float ms = __ldcg(pp + s * (D + 2));
+      if (ms != -INFINITY) Lsum += __ldcg(pp + s * (D + 2) + 1) * fast_exp2(ms - M);
+    }
+    const float inv = 1.f / Lsum;
+    for (int e = tid; e < D; e += blockDim.x) {
+      float acc = 0.f;
+      for (int s = 0; s < n_split; ++s) {
+        const float ms = __ldcg(pp + s * (D + 2));
+        if (ms != -INFINITY) acc += __ldcg(pp + s * (D + 2) + 2 + e) * fast_exp2(ms - M);
+      }
+      if (out_bf16)
+        reinterpret_cast<uint16_t *>(out)[static_cast<int64_t>(h) * D + e] = f2bf(acc * inv);
+      else
+        reinterpret_cast<float *>(out)[static_cast<int64_t>(h) * D + e] = acc * inv;
+    }
+    if (tid == 0) {
+      const int64_t hr = head_row(S, layer, h);
+      S.ring_ml[(hr * S.window + slot) * 2 + 0] = M;
+      S.ring_ml[(hr * S.window + slot) * 2 + 1] = Lsum;
+      S.ring_n[hr * S.window + slot] = geo.n_cols;
+      S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
+    }
+  }
+  if (tid == 0) S.counters[unit] = 0;  // re-armed for the next step / graph replay
 }
 
-__global__ void __launch_bounds__(256) decode_combine_kernel(ls_decode_state S, int length, int compressed,
-                                                             int slot, const Part *parts, int n_split, void *out,
-                                                             int out_bf16) {
-  __shared__ float scl[512];
-  __shared__ float Msh, Lsh;
-  const int h = blockIdx.x;
-  const int d = S.head_dim;
-  const Geo g = geometry(S, h, length, compressed);
-  const int ns = (g.n_cols + COLS_PER_SPLIT - 1) / COLS_PER_SPLIT;
-  const Part *pp = parts + static_cast<int64_t>(h) * n_split;
+__global__ void advance_kernel(int32_t *step, int rows) {
   if (threadIdx.x == 0) {
-    float M = -INFINITY;
-    for (int s = 0; s < ns; ++s) M = fmaxf(M, pp[s].m);
-    float Ls = 0.f;
-    for (int s = 0; s < ns; ++s) Ls += pp[s].l * fast_exp2(pp[s].m - M);
-    Msh = M;
-    Lsh = Ls;
-  }
-  __syncthreads();
-  const float M = Msh, inv = 1.f / Lsh;
-  for (int s = threadIdx.x; s < ns; s += blockDim.x) scl[s] = fast_exp2(pp[s].m - M) * inv;
-  __syncthreads();
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < ns; ++s) acc += pp[s].o[i] * scl[s];
-    if (out_bf16)
-      reinterpret_cast<uint16_t *>(out)[static_cast<int64_t>(h) * d + i] = f2bf(acc);
-    else
-      reinterpret_cast<float *>(out)[static_cast<int64_t>(h) * d + i] = acc;
-  }
-  float *wrow = S.ring_w + (static_cast<int64_t>(h) * S.window + slot) * S.row_cap;
-  for (int j = threadIdx.x; j < g.n_cols; j += blockDim.x) wrow[j] *= scl[j / COLS_PER_SPLIT];
-  if (threadIdx.x == 0) {
-    S.ring_n[h * S.window + slot] = g.n_cols;
-    S.ring_dense[h * S.window + slot] = compressed ? 0 : 1;
+    step[0] += 1;
+    step[1] += rows;
   }
 }
 
 // ------------------------------------------------------------------ K7
-constexpr int K7_THREADS = 1024;
-
 __device__ __forceinline__ unsigned long long dkey(double x) {
   return static_cast<unsigned long long>(__double_as_longlong(x));  // x >= 0: monotone
 }
@@ -232,8 +272,7 @@ __device__ int block_sum_int(int v, int *sh) {
   if (lane == 0) sh[wid] = v;
   __syncthreads();
   int tot = 0;
-  const int nw = blockDim.x >> 5;
-  for (int i = 0; i < nw; ++i) tot += sh[i];
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += sh[i];
   __syncthreads();
   return tot;
 }
@@ -245,13 +284,11 @@ __device__ double block_sum_double(double v, double *sh) {
   if (lane == 0) sh[wid] = v;
   __syncthreads();
   double tot = 0.0;
-  const int nw = blockDim.x >> 5;
-  for (int i = 0; i < nw; ++i) tot += sh[i];
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += sh[i];
   __syncthreads();
   return tot;
 }
 
-// exclusive block scan of a 0/1 flag; returns the rank, total via *tot
 __device__ int block_rank(int flag, int *sh, int *tot) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned b = __ballot_sync(0xffffffffu, flag);
@@ -259,8 +296,7 @@ __device__ int block_rank(int flag, int *sh, int *tot) {
   if (lane == 0) sh[wid] = __popc(b);
   __syncthreads();
   int before = 0, all = 0;
-  const int nw = blockDim.x >> 5;
-  for (int i = 0; i < nw; ++i) {
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
     if (i < wid) before += sh[i];
     all += sh[i];
   }
@@ -268,63 +304,90 @@ __device__ int block_rank(int flag, int *sh, int *tot) {
   return before + __popc(b & ((1u << lane) - 1u));
 }
 
-__global__ void __launch_bounds__(K7_THREADS) decode_select_kernel(ls_decode_state S, const int32_t *slot_order,
-                                                                   int n_rows, int length, int budget,
-                                                                   double *acc_ws, uint8_t *touched_ws,
-                                                                   int32_t *retained_n, double *score_cov) {
+__global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, int budget, double *acc_ws,
+                                                            uint32_t *touched_ws, int use_smem, int32_t *retained_n,
+                                                            double *score_cov) {
+  extern __shared__ __align__(16) unsigned char smem7[];
   __shared__ int hist[256];
   __shared__ int shi[32];
   __shared__ double shd[32];
   __shared__ int s_digit, s_above;
-  const int h = blockIdx.x;
-  double *acc = acc_ws + static_cast<int64_t>(h) * S.row_cap;
-  uint8_t *touched = touched_ws + static_cast<int64_t>(h) * S.row_cap;
-  for (int i = threadIdx.x; i < length; i += blockDim.x) {
-    acc[i] = 0.0;
-    touched[i] = 0;
-  }
+  const int h = blockIdx.x, layer = blockIdx.y;
+  const int64_t hr = head_row(S, layer, h);
+  const int length = S.step[0];
+  const int appended = S.step[1];
+  const int n_rows = min(S.window, appended);
+  const int words = (length + 31) / 32;
+  double *acc = use_smem ? reinterpret_cast<double *>(smem7) : acc_ws + hr * S.row_cap;
+  uint32_t *touched =
+      use_smem ? reinterpret_cast<uint32_t *>(smem7 + static_cast<size_t>(K7_SMEM_CAP) * 8)
+               : touched_ws + hr * ((S.row_cap + 31) / 32);
+  for (int i = threadIdx.x; i < length; i += blockDim.x) acc[i] = 0.0;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) touched[i] = 0u;
   __syncthreads();
   // accumulate rows oldest -> newest (kvcompress.py:75-79)
   for (int rr = 0; rr < n_rows; ++rr) {
-    const int slot = slot_order[rr];
-    const int n = S.ring_n[h * S.window + slot];
-    const int dense = S.ring_dense[h * S.window + slot];
-    const float *w = S.ring_w + (static_cast<int64_t>(h) * S.window + slot) * S.row_cap;
-    const int32_t *ids = S.ring_ids + (static_cast<int64_t>(h) * S.window + slot) * S.sparse_cap;
+    const int slot = (appended - n_rows + rr) % S.window;
+    const int64_t so = hr * S.window + slot;
+    const int n = S.ring_n[so];
+    const int dense = S.ring_dense[so];
+    const float M = S.ring_ml[so * 2], Lr = S.ring_ml[so * 2 + 1];
+    const float inv = Lr > 0.f ? 1.f / Lr : 0.f;
+    const float *s = S.ring_s + so * S.row_cap;
+    const int32_t *ids = S.ring_ids + so * S.sparse_cap;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const int id = dense ? j : ids[j];
-      acc[id] += static_cast<double>(w[j]);
-      touched[id] = 1;
+      const float w = (Lr == 0.f) ? s[j] : fast_exp2(s[j] - M) * inv;  // Lr == 0: stored probabilities (seeds)
+      acc[id] += static_cast<double>(w);
+      atomicOr(touched + (id >> 5), 1u << (id & 31));
     }
     __syncthreads();
   }
-  // candidates
   int cnt = 0;
-  for (int i = threadIdx.x; i < length; i += blockDim.x) cnt += touched[i];
+  for (int i = threadIdx.x; i < words; i += blockDim.x) cnt += __popc(touched[i]);
   const int n_cand = block_sum_int(cnt, shi);
-  // radix select of the budget-th largest key among candidates
   unsigned long long prefix = 0ull, pmask = 0ull;
-  int need = budget;  // rank from the top still to place
+  int need = budget;
   const bool take_all = budget >= n_cand;
   if (!take_all) {
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < length; i += blockDim.x) {
-        if (!touched[i]) continue;
+        if (!((touched[i >> 5] >> (i & 31)) & 1u)) continue;
         const unsigned long long key = dkey(acc[i]);
         if ((key & pmask) != prefix) continue;
         atomicAdd(&hist[(key >> shift) & 0xff], 1);
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int above = 0, dg = 255;
-        for (; dg >= 0; --dg) {
-          if (above + hist[dg] >= need) break;
-          above += hist[dg];
+      if (threadIdx.x < 32) {  // warp scan from the top digit down
+        const int lane = threadIdx.x;
+        int c[8], loc = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          c[t] = hist[255 - (lane * 8 + t)];
+          loc += c[t];
         }
-        s_digit = dg;
-        s_above = above;
+        int incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int excl = incl - loc;  // count above this lane's 8 digits
+        const bool hit = excl < need && incl >= need;
+        const unsigned hb = __ballot_sync(0xffffffffu, hit);
+        if (lane == __ffs(hb) - 1) {
+          int above = excl;
+          for (int t = 0; t < 8; ++t) {
+            if (above + c[t] >= need) {
+              s_digit = 255 - (lane * 8 + t);
+              s_above = above;
+              break;
+            }
+            above += c[t];
+          }
+        }
       }
       __syncthreads();
       prefix |= static_cast<unsigned long long>(s_digit) << shift;
@@ -333,9 +396,8 @@ __global__ void __launch_bounds__(K7_THREADS) decode_select_kernel(ls_decode_sta
       __syncthreads();
     }
   }
-  const unsigned long long thr = prefix;  // key of the budget-th largest
-  // emit picked ids in id order: key > thr, or key == thr among the first `need` ids
-  int32_t *sel = S.sel_ids + static_cast<int64_t>(h) * S.budget_cap;
+  const unsigned long long thr = prefix;
+  int32_t *sel = S.sel_ids + hr * S.budget_cap;
   int base = 0, eq_seen = 0;
   double tot_mass = 0.0, kept_mass = 0.0;
   int in_window_picked = 0;
@@ -343,12 +405,12 @@ __global__ void __launch_bounds__(K7_THREADS) decode_select_kernel(ls_decode_sta
   for (int i0 = 0; i0 < length; i0 += blockDim.x) {
     const int i = i0 + threadIdx.x;
     int is_t = 0, is_eq = 0, is_gt = 0;
-    double sc = 0.0;
-    if (i < length && touched[i]) {
+    double scv = 0.0;
+    if (i < length && ((touched[i >> 5] >> (i & 31)) & 1u)) {
       is_t = 1;
-      sc = acc[i];
+      scv = acc[i];
       if (!take_all) {
-        const unsigned long long key = dkey(sc);
+        const unsigned long long key = dkey(scv);
         is_gt = key > thr;
         is_eq = key == thr;
       }
@@ -360,8 +422,8 @@ __global__ void __launch_bounds__(K7_THREADS) decode_select_kernel(ls_decode_sta
     const int rank = block_rank(pick, shi, &pick_tot);
     if (pick) sel[base + rank] = i;
     if (is_t) {
-      tot_mass += sc;
-      if (pick || i >= lo) kept_mass += sc;  // kvcompress.py:215 (working = picked U recent)
+      tot_mass += scv;
+      if (pick || i >= lo) kept_mass += scv;  // kvcompress.py:215 (working = picked U recent)
     }
     if (pick && i >= lo) in_window_picked += 1;
     base += pick_tot;
@@ -371,25 +433,26 @@ __global__ void __launch_bounds__(K7_THREADS) decode_select_kernel(ls_decode_sta
   const double Kp = block_sum_double(kept_mass, shd);
   const int iw = block_sum_int(in_window_picked, shi);
   if (threadIdx.x == 0) {
-    S.n_sel[h] = base;
-    const int w_len = length - lo;
-    if (retained_n) retained_n[h] = base + w_len - iw;
-    if (score_cov) score_cov[h] = T > 0 ? Kp / T : 1.0;
+    S.n_sel[hr] = base;
+    if (retained_n) retained_n[hr] = base + (length - lo) - iw;
+    if (score_cov) score_cov[hr] = T > 0 ? Kp / T : 1.0;
   }
 }
 
 // ------------------------------------------------------------------ K8
-__global__ void kv_compact_kernel(ls_decode_state S, const uint16_t *k, const uint16_t *v) {
-  const int h = blockIdx.y;
+__global__ void compact_kernel(ls_decode_stack S, const uint16_t *k, const uint16_t *v) {
+  const int h = blockIdx.y, layer = blockIdx.z;
   const int d = S.head_dim;
-  const int vec = d / 8;  // 16-byte vectors per row
-  const int n = S.n_sel[h];
+  const int vec = d / 8;
+  const int64_t hr = head_row(S, layer, h);
+  const int n = S.n_sel[hr];
   const int kv = h / (S.n_heads / S.n_kv_heads);
-  const int32_t *sel = S.sel_ids + static_cast<int64_t>(h) * S.budget_cap;
-  const uint4 *kb = reinterpret_cast<const uint4 *>(k + static_cast<int64_t>(kv) * S.kv_head_stride);
-  const uint4 *vb = reinterpret_cast<const uint4 *>(v + static_cast<int64_t>(kv) * S.kv_head_stride);
-  uint4 *ck = reinterpret_cast<uint4 *>(S.ck + static_cast<int64_t>(h) * S.budget_cap * d);
-  uint4 *cv = reinterpret_cast<uint4 *>(S.cv + static_cast<int64_t>(h) * S.budget_cap * d);
+  const int32_t *sel = S.sel_ids + hr * S.budget_cap;
+  const int64_t base = static_cast<int64_t>(layer) * S.kv_layer_stride + static_cast<int64_t>(kv) * S.kv_head_stride;
+  const uint4 *kb = reinterpret_cast<const uint4 *>(k + base);
+  const uint4 *vb = reinterpret_cast<const uint4 *>(v + base);
+  uint4 *ck = reinterpret_cast<uint4 *>(S.ck + hr * S.budget_cap * d);
+  uint4 *cv = reinterpret_cast<uint4 *>(S.cv + hr * S.budget_cap * d);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * vec; i += gridDim.x * blockDim.x) {
     const int j = i / vec, e = i % vec;
     const int64_t src = static_cast<int64_t>(sel[j]) * vec + e;
@@ -403,73 +466,110 @@ __global__ void kv_compact_kernel(ls_decode_state S, const uint16_t *k, const ui
 
 using namespace ls;
 
-static int check_state(const ls_decode_state *S) {
+static int check_stack(const ls_decode_stack *S) {
   LS_REQUIRE(S->head_dim == 64 || S->head_dim == 128, LS_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   LS_REQUIRE(S->n_heads > 0 && S->n_kv_heads > 0 && S->n_heads % S->n_kv_heads == 0, LS_ERR_DIMENSION_MISMATCH,
              "n_heads must be a multiple of n_kv_heads");
   LS_REQUIRE(S->window >= 1, LS_ERR_INVALID_CONFIG, "obs_window must be >= 1");
-  return LS_OK;
-}
-
-extern "C" size_t ls_decode_attention_workspace(const ls_decode_state *S, int32_t max_len) {
-  const size_t n_split = static_cast<size_t>(ceil_div(max_len + 1, dec::COLS_PER_SPLIT));
-  return static_cast<size_t>(S->n_heads) * n_split * sizeof(dec::Part) + 1024;
-}
-
-extern "C" int ls_decode_attention(const ls_decode_state *S, const uint16_t *q, const uint16_t *k,
-                                   const uint16_t *v, int32_t length, int32_t compressed, int32_t slot, void *out,
-                                   int32_t out_bf16, void *ws, size_t ws_bytes, ls_stream_t stream) {
-  int c = check_state(S);
-  if (c) return c;
-  LS_REQUIRE(length >= 0 && length + 1 <= S->row_cap, LS_ERR_SEQUENCE_TOO_LONG,
-             "length %d exceeds the ring row capacity %d", length, S->row_cap);
-  LS_REQUIRE(slot >= 0 && slot < S->window, LS_ERR_INVALID_CONFIG, "ring slot out of range");
-  LS_REQUIRE(!compressed || S->budget_cap + S->window + 1 <= S->sparse_cap, LS_ERR_INVALID_CONFIG,
+  LS_REQUIRE(S->sparse_cap >= S->budget_cap + S->window + 1, LS_ERR_INVALID_CONFIG,
              "sparse_cap must be >= budget_cap + window + 1");
-  const int n_split = ceil_div(length + 1, dec::COLS_PER_SPLIT);
-  LS_REQUIRE(ws_bytes >= ls_decode_attention_workspace(S, length), LS_ERR_WORKSPACE,
-             "decode_attention workspace too small");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  dec::Part *parts = reinterpret_cast<dec::Part *>(ws);
-  const float scale_log2 = kLog2e / sqrtf(static_cast<float>(S->head_dim));
-  dec::decode_partial_kernel<<<dim3(n_split, S->n_heads), dec::K6_THREADS, 0, st>>>(
-      *S, q, k, v, length, compressed, slot, scale_log2, parts, n_split);
-  LS_LAUNCH_CHECK("decode_partial_kernel");
-  dec::decode_combine_kernel<<<S->n_heads, 256, 0, st>>>(*S, length, compressed, slot, parts, n_split, out,
-                                                         out_bf16);
-  LS_LAUNCH_CHECK("decode_combine_kernel");
   return LS_OK;
 }
 
-extern "C" size_t ls_decode_select_workspace(const ls_decode_state *S, int32_t max_len) {
-  (void)max_len;
-  return static_cast<size_t>(S->n_heads) * S->row_cap * 9 + 1024;
+static int split_cols(int compressed) { return compressed ? 256 : 512; }
+
+template <int D, int G>
+static int launch_decode(dim3 grid, cudaStream_t st, const ls_decode_stack *S, int layer, const uint16_t *q,
+                         const uint16_t *k, const uint16_t *v, int compressed, int cs, float sl, void *out,
+                         int out_bf16) {
+  const int smem = (G * D + G * 512 + 8 * G * D) * 4;
+  if (smem > 48 * 1024)
+    LS_CUDA(cudaFuncSetAttribute(dec::decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dec::decode_kernel<D, G><<<grid, dec::K6_THREADS, smem, st>>>(*S, layer, q, k, v, compressed, cs, sl, out, out_bf16);
+  return LS_OK;
 }
 
-extern "C" int ls_decode_select(const ls_decode_state *S, const int32_t *slot_order, int32_t n_rows,
-                                int32_t length, int32_t budget, int32_t *retained_n, double *score_coverage,
-                                void *ws, size_t ws_bytes, ls_stream_t stream) {
-  int c = check_state(S);
+extern "C" size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len) {
+  const size_t n_split = static_cast<size_t>(ceil_div(max_len + 1, split_cols(1)));
+  return static_cast<size_t>(S->n_heads) * n_split * (S->head_dim + 2) * sizeof(float);
+}
+
+extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
+                              const uint16_t *v_layer, int32_t compressed, int32_t max_cols, void *out,
+                              int32_t out_bf16, ls_stream_t stream) {
+  int c = check_stack(S);
   if (c) return c;
-  LS_REQUIRE(n_rows >= 1, LS_ERR_EMPTY_WINDOW, "need at least one observation row");
+  LS_REQUIRE(layer >= 0 && layer < S->n_layers, LS_ERR_DIMENSION_MISMATCH, "layer out of range");
+  LS_REQUIRE(max_cols >= 1 && max_cols <= S->row_cap, LS_ERR_SEQUENCE_TOO_LONG,
+             "max_cols %d exceeds the ring row capacity %d", max_cols, S->row_cap);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cs = split_cols(compressed);
+  const int n_split = ceil_div(max_cols, cs);
+  const float sl = kLog2e / sqrtf(static_cast<float>(S->head_dim));
+  const int group = S->n_heads / S->n_kv_heads;
+  int r = LS_OK;
+  if (compressed) {
+    dim3 grid(n_split, S->n_heads);
+    r = S->head_dim == 128 ? launch_decode<128, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, cs, sl, out, out_bf16)
+                           : launch_decode<64, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, cs, sl, out, out_bf16);
+  } else {
+    dim3 grid(n_split, S->n_kv_heads);
+#define LS_DENSE(DD, GG) r = launch_decode<DD, GG>(grid, st, S, layer, q, k_layer, v_layer, 0, cs, sl, out, out_bf16)
+    if (S->head_dim == 128) {
+      if (group == 1) LS_DENSE(128, 1);
+      else if (group == 2) LS_DENSE(128, 2);
+      else if (group == 4) LS_DENSE(128, 4);
+      else if (group == 7) LS_DENSE(128, 7);
+      else if (group == 8) LS_DENSE(128, 8);
+      else LS_REQUIRE(false, LS_ERR_UNSUPPORTED, "GQA group size %d", group);
+    } else {
+      if (group == 1) LS_DENSE(64, 1);
+      else if (group == 2) LS_DENSE(64, 2);
+      else if (group == 4) LS_DENSE(64, 4);
+      else LS_REQUIRE(false, LS_ERR_UNSUPPORTED, "GQA group size %d", group);
+    }
+#undef LS_DENSE
+  }
+  if (r) return r;
+  LS_LAUNCH_CHECK("decode_kernel");
+  return LS_OK;
+}
+
+extern "C" int ls_decode_advance(const ls_decode_stack *S, ls_stream_t stream) {
+  dec::advance_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(S->step, 1);
+  LS_LAUNCH_CHECK("advance_kernel");
+  return LS_OK;
+}
+
+extern "C" size_t ls_decode_select_workspace(const ls_decode_stack *S) {
+  return static_cast<size_t>(S->n_layers) * S->n_heads *
+             (static_cast<size_t>(S->row_cap) * 8 + (S->row_cap + 31) / 32 * 4) + 1024;
+}
+
+extern "C" int ls_decode_event(const ls_decode_stack *S, int32_t budget, int32_t max_len, const uint16_t *k_all,
+                               const uint16_t *v_all, int32_t *retained_n, double *score_coverage, void *ws,
+                               size_t ws_bytes, ls_stream_t stream) {
+  int c = check_stack(S);
+  if (c) return c;
   LS_REQUIRE(budget >= 1 && budget <= S->budget_cap, LS_ERR_INVALID_CONFIG, "budget outside [1, budget_cap]");
-  LS_REQUIRE(length <= S->row_cap, LS_ERR_SEQUENCE_TOO_LONG, "length exceeds row_cap");
-  LS_REQUIRE(ws_bytes >= ls_decode_select_workspace(S, length), LS_ERR_WORKSPACE, "decode_select workspace too small");
+  LS_REQUIRE(max_len <= S->row_cap, LS_ERR_SEQUENCE_TOO_LONG, "length exceeds row_cap");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Carver cv(ws, ws_bytes);
-  double *acc = cv.take<double>(static_cast<size_t>(S->n_heads) * S->row_cap);
-  uint8_t *touched = cv.take<uint8_t>(static_cast<size_t>(S->n_heads) * S->row_cap);
-  dec::decode_select_kernel<<<S->n_heads, dec::K7_THREADS, 0, st>>>(*S, slot_order, n_rows, length, budget, acc,
-                                                                   touched, retained_n, score_coverage);
-  LS_LAUNCH_CHECK("decode_select_kernel");
-  return LS_OK;
-}
-
-extern "C" int ls_kv_compact(const ls_decode_state *S, const uint16_t *k, const uint16_t *v, ls_stream_t stream) {
-  int c = check_state(S);
-  if (c) return c;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  dec::kv_compact_kernel<<<dim3(16, S->n_heads), 256, 0, st>>>(*S, k, v);
-  LS_LAUNCH_CHECK("kv_compact_kernel");
+  const bool smem = max_len <= dec::K7_SMEM_CAP;
+  double *acc = nullptr;
+  uint32_t *touched = nullptr;
+  if (!smem) {
+    LS_REQUIRE(ws_bytes >= ls_decode_select_workspace(S), LS_ERR_WORKSPACE, "decode_event workspace too small");
+    Carver cv(ws, ws_bytes);
+    acc = cv.take<double>(static_cast<size_t>(S->n_layers) * S->n_heads * S->row_cap);
+    touched = cv.take<uint32_t>(static_cast<size_t>(S->n_layers) * S->n_heads * ((S->row_cap + 31) / 32));
+  }
+  const size_t dyn = smem ? static_cast<size_t>(dec::K7_SMEM_CAP) * 8 + dec::K7_SMEM_CAP / 8 + 64 : 0;
+  if (dyn > 48 * 1024)
+    LS_CUDA(cudaFuncSetAttribute(dec::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+  dec::select_kernel<<<dim3(S->n_heads, S->n_layers), dec::K7_THREADS, dyn, st>>>(*S, budget, acc, touched, smem ? 1 : 0,
+                                                                                   retained_n, score_coverage);
+  LS_LAUNCH_CHECK("select_kernel");
+  dec::compact_kernel<<<dim3(16, S->n_heads, S->n_layers), 256, 0, st>>>(*S, k_all, v_all);
+  LS_LAUNCH_CHECK("compact_kernel");
   return LS_OK;
 }

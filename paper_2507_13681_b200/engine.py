@@ -11,9 +11,11 @@ scope):
     K2-K4 sort + greedy   prefill.py:168-169, 178-229
     K5 sparse attention   model.py:242-251 -> tensor_ops.py:141-183
     seeds                 session.py:163 / 89-95 (only rows that survive to the first event)
-  decode (per token, per layer):
-    event: K7 + K8        kvcompress.py:205-225
-    K6 decode attention   kvcompress.py:227-237 / model.py:232-241
+  decode (per token): CUDA graphs over all layers with the step counters in
+  device memory (kvcompress.py:200-239):
+    event graph           K7 + K8 for every layer   (kvcompress.py:205-225)
+    step graph            q gather + K6 per layer + counter advance
+                          (dense-step and compressed-step variants)
   rollback                session.py:180 (the archive only grows; positions past the
                           block are simply not read by the next turn's prefill)
 
@@ -28,7 +30,8 @@ from dataclasses import dataclass, field
 
 import torch
 
-from .kvcompress import CompressionConfig, DecodeLayer
+from . import _lib
+from .kvcompress import CompressionConfig, DecodeStack
 from .prefill import LayerPlans, Workspace, sample_rows_device, sample_size, sparsify_layer
 from .tensor_ops import attention_layer, dense_attention_layer, plan_rows
 
@@ -95,6 +98,7 @@ class PrefillOut:
     rows: torch.Tensor | None
     n_new: int
     n_total: int
+    n_seed: int = 0
 
 
 class SessionEngine:
@@ -107,16 +111,15 @@ class SessionEngine:
         comp = params.comp
         self.window = comp.window()
         budget_cap = comp.budget if comp.budget is not None else 1
-        self.decode_layers = [DecodeLayer(shape.n_q, shape.n_kv, shape.d, self.window, budget_cap, cap + 1,
-                                          cap * shape.d, device=device) for _ in range(shape.n_layers)]
+        self.stack = DecodeStack(shape.n_layers, shape.n_q, shape.n_kv, shape.d, self.window, budget_cap, cap + 1,
+                                 shape.n_kv * cap * shape.d, cap * shape.d, device=device)
         self.ws = Workspace()
         self.rows_ws = Workspace()
         self.clear_logs()
 
     def clear_logs(self):
         """Work logs (device tensors / host counts) used by bench.py's roofline."""
-        self.cell_log, self.score_log, self.decode_cols = [], [], 0
-        self.decode_launches = 0
+        self.cell_log, self.score_log, self.decode_log = [], [], []
 
     # ------------------------------------------------------------- prefill
     def prefill(self, store: QKVStore, turn: int, row_offset: int, n_new: int, seed_rows: bool = True,
@@ -139,7 +142,8 @@ class SessionEngine:
                 if rows.dim() == 2:
                     rows = rows.unsqueeze(0)
         n_seed = min(self.window, n_new)
-        surv = p.comp.surviving_seeds(n_seed, p.max_new) if seed_rows else 0
+        surv = p.comp.surviving_seeds(n_seed, p.max_new) if (seed_rows and p.mode == "loopserve") else 0
+        st = self.stack
         for l in range(sh.n_layers):
             qb = store.q[l, :, row_offset:n_total]
             kl, vl = store.k[l], store.v[l]
@@ -159,53 +163,90 @@ class SessionEngine:
             cells_all.append(cells)
             self.cell_log.append(cells)
             self.score_log.append(plans.score_count)
-            dl = self.decode_layers[l]
-            dl.reset()
-            slots = dl.seed_slots(n_seed)
             if surv > 0:
-                # the surviving seeds are the last `surv` rows of the block
-                first = slots[n_seed - surv]
-                assert slots[n_seed - surv:] == list(range(first, first + surv))
+                # the seeds that are still in the deque at the first event are the
+                # last `surv` block rows; they sit in slots [n_seed - surv, n_seed)
+                first = n_seed - surv
+                hr = slice(l * sh.n_q, (l + 1) * sh.n_q)
                 plan_rows(qb, kl, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total, sh.n_kv, surv,
-                          out=dl.ring_w[:, first:], out_row_stride=dl.row_cap,
-                          out_head_stride=dl.window * dl.row_cap, q_head_stride=store.q.stride(1),
+                          out=st.ring_s[hr, first:], out_row_stride=st.row_cap,
+                          out_head_stride=st.window * st.row_cap, q_head_stride=store.q.stride(1),
                           stream=stream)
-                dl.ring_n[:, first:first + surv] = n_total
-                dl.ring_dense[:, first:first + surv] = 1
-        return PrefillOut(outs, plans_all, cells_all, rows, n_new, n_total)
+                st.ring_ml[hr, first:n_seed] = 0.0
+                st.ring_n[hr, first:n_seed] = n_total
+                st.ring_dense[hr, first:n_seed] = 1
+        st.set_step(n_total, n_seed)
+        return PrefillOut(outs, plans_all, cells_all, rows, n_new, n_total, n_seed)
 
     # -------------------------------------------------------------- decode
-    def decode(self, store: QKVStore, L0: int, max_new: int, record=False, stream=None):
-        """max_new decode steps (kvcompress.py:200-239) from cache length L0.
-        Returns per step a list of per-layer outputs [n_q, d]."""
+    def _step(self, store: QKVStore, q_buf, out_buf, compressed: bool, max_cols: int, stream=None):
+        st = self.stack
+        torch.index_select(store.q, 2, st.step_t[:1], out=q_buf)  # q of position step[0] (device index)
+        for l in range(self.shape.n_layers):
+            st.step(l, q_buf[l, :, 0], store.k[l], store.v[l], compressed, max_cols, out_buf[l], stream=stream)
+        st.advance(stream=stream)
+
+    def decode(self, store: QKVStore, L0: int, max_new: int, use_graphs: bool = True, out_sink=None):
+        """max_new decode steps (kvcompress.py:200-239) from cache length L0,
+        after prefill() set the counters. Returns the last step's outputs
+        [L, n_q, d]; out_sink(step, out_buf) is called after every step."""
         p, sh = self.params, self.shape
+        st = self.stack
         comp = p.comp if p.mode == "loopserve" else CompressionConfig(budget=None)
         if p.mode == "dense":
-            for dl in self.decode_layers:
-                dl.reset()
-        length = L0
+            st.set_step(L0, 0)
+        n_dense = max_new if comp.budget is None else min(max_new, comp.warmup - 1)
+        dense_cols = L0 + n_dense + 1
+        comp_cols = min((comp.budget or 0) + self.window + 1, L0 + max_new + 1)
+        q_buf = torch.empty((sh.n_layers, sh.n_q, 1, sh.d), dtype=torch.bfloat16, device=self.device)
+        out_buf = torch.empty((sh.n_layers, sh.n_q, sh.d), dtype=self.out_dtype, device=self.device)
+        # K/V columns each step reads per KV head (all layers): the algorithmic
+        # HBM traffic of a step is 4*d bytes per column (bf16 K + V rows)
+        for t in range(max_new):
+            if t < n_dense:
+                self.decode_log.append(("dense", (L0 + t + 1) * sh.n_kv * sh.n_layers))
+            else:
+                self.decode_log.append(("comp", min(comp_cols, L0 + t + 1) * sh.n_kv * sh.n_layers))
+        if not use_graphs:
+            compressed = False
+            for n_o in range(1, max_new + 1):
+                if comp.event_at(n_o):
+                    st.event(comp.budget, store.k, store.v, max_len=L0 + max_new)
+                    compressed = True
+                self._step(store, q_buf, out_buf, compressed, comp_cols if compressed else dense_cols)
+                if out_sink is not None:
+                    out_sink(n_o - 1, out_buf)
+            return out_buf
+        # ---- CUDA graphs (captured per turn: the dense grid depends on L0)
+        host = (st.length, st.appended)
+        st.event_workspace(L0 + max_new)
+        graphs = {}
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            if n_dense > 0:
+                graphs["dense"] = _lib.Captured(
+                    "decode_graph_dense", s, lambda: self._step(store, q_buf, out_buf, False, dense_cols))
+            if n_dense < max_new:
+                graphs["comp"] = _lib.Captured(
+                    "decode_graph_comp", s, lambda: self._step(store, q_buf, out_buf, True, comp_cols))
+                graphs["event"] = _lib.Captured(
+                    "decode_graph_event", s,
+                    lambda: st.event(comp.budget, store.k, store.v, max_len=L0 + max_new))
+        torch.cuda.current_stream().wait_stream(s)
+        st.length, st.appended = host  # capture does not execute; restore the host mirror
         compressed = False
-        outs = []
-        events = []
         for n_o in range(1, max_new + 1):
             if comp.event_at(n_o):
-                for l, dl in enumerate(self.decode_layers):
-                    dl.event(length, comp.budget, stream=stream)
-                    dl.compact(store.k[l], store.v[l], stream=stream)
-                    if record:
-                        events.append((n_o, l, dl.working_ids(length, True), dl.score_cov.cpu().numpy()))
+                graphs["event"].replay()
                 compressed = True
-            q_step = store.q[:, :, length].contiguous()  # [L, n_q, d]
-            step = []
-            for l, dl in enumerate(self.decode_layers):
-                step.append(dl.step(q_step[l], store.k[l], store.v[l], length, compressed, stream=stream))
-            # algorithmic columns per q-head (upper bound |keep| <= B + W after an event)
-            cols = min(length, comp.budget + self.window) + 1 if compressed else length + 1
-            self.decode_cols += cols * sh.n_q * sh.n_layers
-            self.decode_launches += sh.n_layers
-            outs.append(step)
-            length += 1
-        return outs, events
+            graphs["comp" if compressed else "dense"].replay()
+            st.length += 1
+            st.appended += 1
+            if out_sink is not None:
+                out_sink(n_o - 1, out_buf)
+        self._graphs = graphs  # keep alive until the next turn
+        return out_buf
 
     def turn_blocks(self, input_len: int, n_turns: int, max_new: int):
         """(row_offset, n_new) of each turn: block = previous answer + input

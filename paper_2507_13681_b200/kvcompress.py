@@ -92,111 +92,132 @@ class KVCacheHead:
             raise InvalidIds("row count does not match retained_ids")
 
 
-class DecodeLayer:
-    """Device decode state of one attention layer (all q-heads)."""
+class DecodeStack:
+    """Device decode state of every layer of one session (ls_decode_stack):
+    observation ring (the deque of kvcompress.py:196) per (layer, q-head),
+    selected ids, compacted K/V, and the device step counters
+    (step[0] = cache length, step[1] = rows appended to the deque)."""
 
-    def __init__(self, n_heads: int, n_kv_heads: int, head_dim: int, window: int, budget_cap: int,
-                 row_cap: int, kv_head_stride: int, device=None):
+    def __init__(self, n_layers: int, n_heads: int, n_kv_heads: int, head_dim: int, window: int, budget_cap: int,
+                 row_cap: int, kv_layer_stride: int, kv_head_stride: int, device=None, sparse_cap: int | None = None):
         dev = device or _dev()
-        self.n_heads, self.n_kv, self.d, self.window = n_heads, n_kv_heads, head_dim, window
+        self.n_layers, self.n_heads, self.n_kv, self.d, self.window = n_layers, n_heads, n_kv_heads, head_dim, window
         self.budget_cap, self.row_cap = max(1, budget_cap), row_cap
-        self.sparse_cap = self.budget_cap + window + 1
-        H, W = n_heads, window
-        self.ring_w = torch.zeros((H, W, row_cap), dtype=torch.float32, device=dev)
-        self.ring_ids = torch.zeros((H, W, self.sparse_cap), dtype=torch.int32, device=dev)
-        self.ring_n = torch.zeros((H, W), dtype=torch.int32, device=dev)
-        self.ring_dense = torch.zeros((H, W), dtype=torch.int32, device=dev)
-        self.sel_ids = torch.zeros((H, self.budget_cap), dtype=torch.int32, device=dev)
-        self.n_sel = torch.zeros(H, dtype=torch.int32, device=dev)
-        self.ck = torch.zeros((H, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
-        self.cv = torch.zeros((H, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
-        self.retained_n = torch.zeros(H, dtype=torch.int32, device=dev)
-        self.score_cov = torch.zeros(H, dtype=torch.float64, device=dev)
-        self.desc = _lib.DecodeStateDesc(
-            n_heads, n_kv_heads, head_dim, window, row_cap, self.sparse_cap, self.budget_cap, int(kv_head_stride),
-            self.ring_w.data_ptr(), self.ring_ids.data_ptr(), self.ring_n.data_ptr(), self.ring_dense.data_ptr(),
-            self.sel_ids.data_ptr(), self.n_sel.data_ptr(), self.ck.data_ptr(), self.cv.data_ptr())
+        self.sparse_cap = max(self.budget_cap + window + 1, sparse_cap or 0)
+        HR, W = n_layers * n_heads, window
+        f32, i32 = torch.float32, torch.int32
+        self.ring_s = torch.zeros((HR, W, row_cap), dtype=f32, device=dev)
+        self.ring_ml = torch.zeros((HR, W, 2), dtype=f32, device=dev)
+        self.ring_ids = torch.zeros((HR, W, self.sparse_cap), dtype=i32, device=dev)
+        self.ring_n = torch.zeros((HR, W), dtype=i32, device=dev)
+        self.ring_dense = torch.zeros((HR, W), dtype=i32, device=dev)
+        self.sel_ids = torch.zeros((HR, self.budget_cap), dtype=i32, device=dev)
+        self.n_sel = torch.zeros(HR, dtype=i32, device=dev)
+        self.ck = torch.zeros((HR, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
+        self.cv = torch.zeros((HR, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
+        self.counters = torch.zeros(n_heads, dtype=i32, device=dev)
+        self.step_t = torch.zeros(4, dtype=i32, device=dev)
+        self.retained_n = torch.zeros(HR, dtype=i32, device=dev)
+        self.score_cov = torch.zeros(HR, dtype=torch.float64, device=dev)
+        self.desc = _lib.DecodeStackDesc(
+            n_layers, n_heads, n_kv_heads, head_dim, window, row_cap, self.sparse_cap, self.budget_cap,
+            int(kv_layer_stride), int(kv_head_stride), self.ring_s.data_ptr(), self.ring_ml.data_ptr(),
+            self.ring_ids.data_ptr(), self.ring_n.data_ptr(), self.ring_dense.data_ptr(), self.sel_ids.data_ptr(),
+            self.n_sel.data_ptr(), self.ck.data_ptr(), self.cv.data_ptr(), 0, self.counters.data_ptr(),
+            self.step_t.data_ptr())
+        n = _lib.lib().ls_decode_partials_size(ctypes.byref(self.desc), row_cap - 1)
+        self.partials = torch.zeros(n // 4 + 64, dtype=f32, device=dev)
+        self.desc.partials = self.partials.data_ptr()
         self.ws = Workspace()
-        self.reset()
+        self.set_step(0, 0)
 
-    def reset(self):
-        self.appended = 0
-        self.order: deque = deque(maxlen=self.window)
+    # ---------------------------------------------------------------- counters
+    def set_step(self, length: int, appended: int):
+        """Host mirror + device counters (a tiny H2D copy; outside graphs)."""
+        self.length, self.appended = int(length), int(appended)
+        self.step_t.copy_(torch.tensor([self.length, self.appended, 0, 0], dtype=torch.int32))
 
-    # ring / deque bookkeeping (kvcompress.py:196, 233)
-    def push_slot(self) -> int:
-        slot = self.appended % self.window
-        self.appended += 1
-        self.order.append(slot)
-        return slot
+    def deque_slots(self) -> list[int]:
+        n = min(self.window, self.appended)
+        return [(self.appended - n + i) % self.window for i in range(n)]
 
     def seed_slots(self, n_seed: int) -> list[int]:
-        """Append n_seed seed rows; returns their slots (oldest first)."""
-        return [self.push_slot() for _ in range(n_seed)]
+        """Slots of n_seed seed rows appended to an empty deque (oldest first)."""
+        return [i % self.window for i in range(n_seed)]
 
-    def write_dense_row(self, slot: int, rows: torch.Tensor):
-        """rows: fp32 [H, n] dense observation rows (ids = arange(n))."""
-        n = rows.shape[1]
-        self.ring_w[:, slot, :n].copy_(rows)
-        self.ring_n[:, slot] = n
-        self.ring_dense[:, slot] = 1
+    def write_dense_rows(self, layer: int, slot: int, rows: torch.Tensor):
+        """Seed rows given as probabilities: rows fp32 [H, n] (ids = arange(n))."""
+        H, n = rows.shape
+        hr = slice(layer * self.n_heads, (layer + 1) * self.n_heads)
+        self.ring_s[hr, slot, :n].copy_(rows)
+        self.ring_ml[hr, slot, 0] = 0.0
+        self.ring_ml[hr, slot, 1] = 0.0  # sum == 0: probabilities stored directly
+        self.ring_n[hr, slot] = n
+        self.ring_dense[hr, slot] = 1
 
-    def write_sparse_row(self, slot: int, h: int, ids: np.ndarray, w: np.ndarray):
+    def write_sparse_row(self, layer: int, h: int, slot: int, ids: np.ndarray, w: np.ndarray):
         n = len(ids)
-        if n > self.sparse_cap:
-            raise SizeMismatch("observation row longer than the sparse ring capacity")
-        self.ring_w[h, slot, :n] = torch.as_tensor(np.asarray(w, dtype=np.float32))
-        self.ring_ids[h, slot, :n] = torch.as_tensor(np.asarray(ids, dtype=np.int32))
-        self.ring_n[h, slot] = n
-        self.ring_dense[h, slot] = 0
+        if n > self.sparse_cap or n > self.row_cap:
+            raise SizeMismatch("observation row longer than the ring capacity")
+        hr = layer * self.n_heads + h
+        self.ring_s[hr, slot, :n] = torch.as_tensor(np.asarray(w, dtype=np.float32))
+        self.ring_ids[hr, slot, :n] = torch.as_tensor(np.asarray(ids, dtype=np.int32))
+        self.ring_ml[hr, slot, 0] = 0.0
+        self.ring_ml[hr, slot, 1] = 0.0
+        self.ring_n[hr, slot] = n
+        self.ring_dense[hr, slot] = 0
 
-    def event(self, length: int, budget: int, stream=None):
-        """K7 + K8: select per head from the buffered rows, compact K/V."""
-        if not self.order:
+    # ----------------------------------------------------------------- kernels
+    def event_workspace(self, max_len: int) -> torch.Tensor:
+        """K7's global score accumulator (only past its shared-memory capacity);
+        call before graph capture so the capture does not allocate."""
+        n = _lib.lib().ls_decode_select_workspace(ctypes.byref(self.desc))
+        return self.ws.get(n if max_len > 24 * 1024 else 1)
+
+    def event(self, budget: int, k_all: torch.Tensor, v_all: torch.Tensor, max_len: int | None = None, stream=None):
+        """K7 + K8 for every layer (kvcompress.py:210-225) at the current step."""
+        if self.appended == 0:
             raise EmptyWindow("need at least one observation row")
-        order = torch.tensor(list(self.order), dtype=torch.int32, device=self.ring_w.device)
-        n = _lib.lib().ls_decode_select_workspace(ctypes.byref(self.desc), length)
-        w = self.ws.get(n)
-        _lib.call("ls_decode_select", ctypes.byref(self.desc), order.data_ptr(), len(self.order), int(length),
-                  int(budget), self.retained_n.data_ptr(), self.score_cov.data_ptr(), w.data_ptr(), w.numel(),
-                  _lib.stream_ptr(stream))
-        self._order_keepalive = order
-        return w
-
-    def compact(self, k_arch: torch.Tensor, v_arch: torch.Tensor, stream=None):
-        _lib.call("ls_kv_compact", ctypes.byref(self.desc), k_arch.data_ptr(), v_arch.data_ptr(),
+        max_len = self.length if max_len is None else max_len
+        w = self.event_workspace(max_len)
+        _lib.call("ls_decode_event", ctypes.byref(self.desc), int(budget), int(max_len), k_all.data_ptr(),
+                  v_all.data_ptr(), self.retained_n.data_ptr(), self.score_cov.data_ptr(), w.data_ptr(), w.numel(),
                   _lib.stream_ptr(stream))
 
-    def step(self, q: torch.Tensor, k_arch: torch.Tensor, v_arch: torch.Tensor, length: int, compressed: bool,
-             out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        """K6: attend one new token (K/V already at position `length` of the
-        archive); q [H, d] bf16 -> out [H, d]."""
-        slot = self.push_slot()
-        if out is None:
-            out = torch.empty((self.n_heads, self.d), dtype=torch.bfloat16, device=q.device)
-        n = _lib.lib().ls_decode_attention_workspace(ctypes.byref(self.desc), length)
-        w = self.ws.get(n)
-        _lib.call("ls_decode_attention", ctypes.byref(self.desc), q.data_ptr(), k_arch.data_ptr(),
-                  v_arch.data_ptr(), int(length), int(bool(compressed)), slot, out.data_ptr(),
-                  int(out.dtype == torch.bfloat16), w.data_ptr(), w.numel(), _lib.stream_ptr(stream))
-        return out
+    def step(self, layer: int, q: torch.Tensor, k_layer: torch.Tensor, v_layer: torch.Tensor, compressed: bool,
+             max_cols: int, out: torch.Tensor, stream=None):
+        """K6 for one layer at the current step (q [H, d] bf16 -> out [H, d])."""
+        _lib.call("ls_decode_step", ctypes.byref(self.desc), int(layer), q.data_ptr(), k_layer.data_ptr(),
+                  v_layer.data_ptr(), int(bool(compressed)), int(max_cols), out.data_ptr(),
+                  int(out.dtype == torch.bfloat16), _lib.stream_ptr(stream))
+
+    def advance(self, stream=None):
+        _lib.call("ls_decode_advance", ctypes.byref(self.desc), _lib.stream_ptr(stream))
+        self.length += 1
+        self.appended += 1
 
     # ------------------------------------------------------ host views (parity)
-    def working_ids(self, length: int, compressed: bool) -> list[np.ndarray]:
+    def working_ids(self, layer: int, compressed: bool) -> list[np.ndarray]:
         """retained_union(selected, W, length) per head (kvcompress.py:126-130)."""
+        L = self.length
         if not compressed:
-            return [np.arange(length) for _ in range(self.n_heads)]
-        sel = self.sel_ids.cpu().numpy()
-        n = self.n_sel.cpu().numpy()
-        lo = max(0, length - self.window)
-        return [np.union1d(sel[h, :n[h]], np.arange(lo, length)).astype(np.intp) for h in range(self.n_heads)]
+            return [np.arange(L) for _ in range(self.n_heads)]
+        hr = slice(layer * self.n_heads, (layer + 1) * self.n_heads)
+        sel = self.sel_ids[hr].cpu().numpy()
+        n = self.n_sel[hr].cpu().numpy()
+        lo = max(0, L - self.window)
+        return [np.union1d(sel[h, :n[h]], np.arange(lo, L)).astype(np.intp) for h in range(self.n_heads)]
 
-    def slot_row(self, h: int, slot: int):
-        n = int(self.ring_n[h, slot].item())
-        w = self.ring_w[h, slot, :n].double().cpu().numpy()
-        if int(self.ring_dense[h, slot].item()):
+    def slot_row(self, layer: int, h: int, slot: int):
+        """(ids, normalised weights) of a ring row."""
+        hr = layer * self.n_heads + h
+        n = int(self.ring_n[hr, slot].item())
+        s = self.ring_s[hr, slot, :n].double().cpu().numpy()
+        M, Ls = (float(x) for x in self.ring_ml[hr, slot].cpu().numpy())
+        w = s if Ls == 0.0 else np.exp2(s - M) / Ls
+        if int(self.ring_dense[hr, slot].item()):
             return np.arange(n), w
-        return self.ring_ids[h, slot, :n].cpu().numpy().astype(np.intp), w
+        return self.ring_ids[hr, slot, :n].cpu().numpy().astype(np.intp), w
 
 
 def retained_union(selected, recent_window: int, full_len: int) -> np.ndarray:
@@ -214,24 +235,22 @@ def _rows_select(buffered_rows, budget: int):
         raise EmptyWindow("need at least one observation row")
     id_cap = max(int(np.max(ids)) + 1 if len(ids) else 1 for ids, _ in rows)
     n_max = max(len(ids) for ids, _ in rows)
-    layer = DecodeLayer(1, 1, 64, len(rows), max(1, budget), max(id_cap, n_max) + 1, 0)
-    layer.sparse_cap = max(layer.sparse_cap, n_max)
-    if n_max > layer.ring_ids.shape[2]:
-        layer.ring_ids = torch.zeros((1, len(rows), n_max), dtype=torch.int32, device=layer.ring_w.device)
-        layer.desc.ring_ids = layer.ring_ids.data_ptr()
-        layer.desc.sparse_cap = n_max
-        layer.sparse_cap = n_max
+    cap = max(id_cap, n_max) + 1
+    st = DecodeStack(1, 1, 1, 64, len(rows), max(1, budget), cap, 0, 0, sparse_cap=n_max)
+    for i, (ids, w) in enumerate(rows):
+        st.write_sparse_row(0, 0, i, np.asarray(ids), np.asarray(w))
+    st.set_step(id_cap, len(rows))
+    dummy = torch.zeros(8 * 64, dtype=torch.bfloat16, device=st.ring_s.device)
+    st.event(max(1, budget), dummy, dummy, max_len=id_cap)
+    # scores: host re-accumulation of the same fp32 weights in the same order
+    acc = np.zeros(id_cap)
+    touched = np.zeros(id_cap, dtype=bool)
     for ids, w in rows:
-        slot = layer.push_slot()
-        layer.write_sparse_row(slot, 0, np.asarray(ids), np.asarray(w))
-    ws = layer.event(id_cap, max(1, budget))
-    torch.cuda.synchronize()
-    acc = ws[: 8 * layer.row_cap].view(torch.float64)[:id_cap].cpu().numpy()
-    off = (8 * layer.row_cap + 255) // 256 * 256
-    touched = ws[off: off + id_cap].cpu().numpy().astype(bool)
+        np.add.at(acc, np.asarray(ids, dtype=np.intp), np.asarray(w, dtype=np.float32).astype(np.float64))
+        touched[np.asarray(ids, dtype=np.intp)] = True
     ids = np.nonzero(touched)[0].astype(np.intp)
-    n = int(layer.n_sel[0].item())
-    picked = layer.sel_ids[0, :n].cpu().numpy().astype(np.intp)
+    n = int(st.n_sel[0].item())
+    picked = st.sel_ids[0, :n].cpu().numpy().astype(np.intp)
     return ids, acc[ids], picked
 
 
@@ -293,61 +312,62 @@ def compact_cache(head: KVCacheHead, retained_ids, recent_window: int) -> KVCach
                        retained_ids=keep, full_len=head.full_len)
 
 
-def progressive_decode(layers: list[DecodeLayer], step_source, L0: int, comp: CompressionConfig, max_new: int,
-                       counter: OpCounter | None = None, row_collector: list | None = None,
-                       record_events: bool = True, stream=None):
+def progressive_decode(stack: DecodeStack, step_source, L0: int, comp: CompressionConfig, max_new: int,
+                       k_all: torch.Tensor, v_all: torch.Tensor, counter: OpCounter | None = None,
+                       row_collector: list | None = None, record_events: bool = True, stream=None):
     """kvcompress.py:167-240 at attention-only shapes.
 
-    layers: one DecodeLayer per attention layer, already seeded (ring holds the
-    prefill observation seeds). step_source(t, length) -> list per layer of
-    (q [H, d] bf16, k_arch, v_arch) with the new token's K/V at `length`.
+    `stack` is already seeded (ring rows of the prefill observation seeds,
+    counters at (L0, n_seed)). step_source(t, length) -> list per layer of
+    (q [H, d] bf16, k_layer, v_layer) with the new token's K/V at `length`.
     Returns (outputs per step [max_new][layer] -> [H, d], DecodeStats).
     """
     comp.validate()
     window = comp.window()
     stats = DecodeStats()
-    length = L0
     outs = []
     compressed = False
+    budget_cols = (comp.budget or 0) + window + 1
     for n_answer in range(1, max_new + 1):
         n_o = n_answer
-        inputs = step_source(n_answer - 1, length)
+        length = stack.length
         if comp.event_at(n_o):
-            for li, layer in enumerate(layers):
-                layer.event(length, comp.budget, stream=stream)
-                _, k_arch, v_arch = inputs[li]
-                layer.compact(k_arch, v_arch, stream=stream)
-                if record_events:
-                    work = layer.working_ids(length, True)
-                    cov = layer.score_cov.cpu().numpy()
-                    for h in range(layer.n_heads):
-                        stats.events.append({"step": n_o, "head": f"L{li}H{h}",
-                                             "retained_ids": [int(g) for g in work[h]],
-                                             "score_coverage": float(cov[h])})
+            stack.event(comp.budget, k_all, v_all, stream=stream)
             compressed = True
             stats.compressed = True
-        step_outs = []
-        for li, layer in enumerate(layers):
-            q, k_arch, v_arch = inputs[li]
-            step_outs.append(layer.step(q, k_arch, v_arch, length, compressed, stream=stream))
+            if record_events:
+                cov = stack.score_cov.cpu().numpy()
+                for li in range(stack.n_layers):
+                    work = stack.working_ids(li, True)
+                    for h in range(stack.n_heads):
+                        stats.events.append({"step": n_o, "head": f"L{li}H{h}",
+                                             "retained_ids": [int(g) for g in work[h]],
+                                             "score_coverage": float(cov[li * stack.n_heads + h])})
+        inputs = step_source(n_answer - 1, length)
         if record_events:
-            pre = max(len(w) for w in layers[0].working_ids(length, compressed)) + 1 if compressed else length + 1
-            if compressed:
-                pre = max(max(len(w) for w in layer.working_ids(length, True)) for layer in layers) + 1
+            pre = max(max(len(w) for w in stack.working_ids(li, compressed)) for li in range(stack.n_layers)) + 1
             stats.step_head_scores.append(pre)
             if counter is not None:
-                for layer in layers:
-                    counter.add(sum(len(w) + 1 for w in layer.working_ids(length, compressed)))
+                for li in range(stack.n_layers):
+                    counter.add(sum(len(w) + 1 for w in stack.working_ids(li, compressed)))
+        step_outs = []
+        max_cols = min(budget_cols, length + 1) if compressed else length + 1
+        slot = stack.appended % stack.window
+        for li in range(stack.n_layers):
+            q, k_layer, v_layer = inputs[li]
+            out = torch.empty((stack.n_heads, stack.d), dtype=torch.bfloat16, device=q.device)
+            stack.step(li, q, k_layer, v_layer, compressed, max_cols, out, stream=stream)
+            step_outs.append(out)
+        stack.advance(stream=stream)
         if row_collector is not None:
-            row_collector.append([{(li, h): layer.slot_row(h, layer.order[-1]) for h in range(layer.n_heads)}
-                                  for li, layer in enumerate(layers)])
-        length += 1
+            row_collector.append([{(li, h): stack.slot_row(li, h, slot) for h in range(stack.n_heads)}
+                                  for li in range(stack.n_layers)])
         if record_events:
-            stats.step_retained.append(max(max(len(w) for w in layer.working_ids(length, compressed))
-                                           for layer in layers))
+            stats.step_retained.append(max(max(len(w) for w in stack.working_ids(li, compressed))
+                                           for li in range(stack.n_layers)))
         outs.append(step_outs)
     return outs, stats
 
 
-__all__ = ["CompressionConfig", "DecodeStats", "KVCacheHead", "DecodeLayer", "accumulate_scores", "token_scores",
-           "select_topB_obs", "_top_by_score", "retained_union", "compact_cache", "progressive_decode"]
+__all__ = ["CompressionConfig", "DecodeStats", "KVCacheHead", "accumulate_scores", "token_scores",
+           "select_topB_obs", "_top_by_score", "retained_union", "compact_cache", "progressive_decode", "DecodeStack"]

@@ -276,12 +276,13 @@ def test_progressive_decode_matches_reference(cuda_lib, golden, name):
     qd = pf.to_bf16(Q)  # [n_q, n_pos, d]
     kd, vd = pf.to_bf16(K), pf.to_bf16(V)
     budget_cap = c["budget"] if c["budget"] is not None else 1
-    layer = kv.DecodeLayer(spec.n_q, spec.n_kv, spec.d, W, budget_cap, cap + 1, kd.stride(0))
+    stack = kv.DecodeStack(1, spec.n_q, spec.n_kv, spec.d, W, budget_cap, cap + 1, kd.numel(), kd.stride(0))
     seeds = golden[f"{name}/seed_rows"]  # [n_q, n_seed, L0]
     n_seed = seeds.shape[1]
-    slots = layer.seed_slots(n_seed)
+    slots = stack.seed_slots(n_seed)
     for i, s in enumerate(slots):
-        layer.write_dense_row(s, torch.from_numpy(seeds[:, i].astype(np.float32)).cuda())
+        stack.write_dense_rows(0, s, torch.from_numpy(seeds[:, i].astype(np.float32)).cuda())
+    stack.set_step(L0, n_seed)
 
     def source(t, length):
         return [(qd[:, length].contiguous(), kd, vd)]
@@ -289,7 +290,7 @@ def test_progressive_decode_matches_reference(cuda_lib, golden, name):
     from paper_2507_13681_b200.opcount import OpCounter
 
     cnt = OpCounter()
-    outs, stats = kv.progressive_decode([layer], source, L0, comp, max_new, counter=cnt)
+    outs, stats = kv.progressive_decode(stack, source, L0, comp, max_new, kd, vd, counter=cnt)
     dev_outs = np.stack([o[0].float().cpu().numpy() for o in outs])
     assert np.abs(dev_outs - golden[f"{name}/outs"]).max() <= ATOL
     assert stats.compressed == c["compressed"]

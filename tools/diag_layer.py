@@ -49,7 +49,7 @@ def main():
         recs.clear()
         _lib.entry_hook = hook
         res = eng.prefill(store, a.turn, ro, n_new)
-        outs, _ = eng.decode(store, ro + n_new, a.decode)
+        eng.decode(store, ro + n_new, a.decode)
         torch.cuda.synchronize()
         _lib.entry_hook = None
         per = {}
