@@ -118,3 +118,26 @@ def test_output_gather_gloo_two_ranks():
     all_rows = res[0][3] + res[1][3]
     for h in range(8):
         assert all_rows[h] == oseed.sample_rows(500, 0.1, 32, oseed.head_seed(0, 1, 0, h)).tolist()
+
+
+def test_dropin_rebinds_reference_names():
+    """dropin.install() rebinds the reference's import-time name bindings
+    (session.py:37, model.py:20) in the calling modules and restores them."""
+    import types
+
+    from paper_2507_13681_b200 import dropin, prefill, tensor_ops
+
+    orig = object()
+    mods = {}
+    for (mod_name, attr) in dropin.PATCHES:
+        m = mods.setdefault(mod_name, types.ModuleType(mod_name))
+        setattr(m, attr, orig)
+    done = dropin.install(mods)
+    try:
+        assert sorted(done) == sorted(f"{m}.{a}" for m, a in dropin.PATCHES)
+        assert mods["loopserve.session"].sparsify_head is prefill.sparsify_head
+        assert mods["loopserve.model"].masked_sparse_attention is tensor_ops.masked_sparse_attention
+        assert mods["loopserve.model"].scaled_dot_attention is tensor_ops.scaled_dot_attention
+    finally:
+        dropin.uninstall()
+    assert all(getattr(mods[m], a) is orig for m, a in dropin.PATCHES)

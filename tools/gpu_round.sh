@@ -1,0 +1,26 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench (both arms), ncu launch list and
+# full captures of the top kernels. Each stage is bounded by its own timeout.
+# usage: tools/gpu_round.sh [stages...]   stages: tests smoke bench ref launches full
+set -u
+OUT=gpurun_out
+mkdir -p $OUT
+STAGES="${@:-tests smoke bench launches full}"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
+python -c 'import __graft_entry__ as g; g.build()' > $OUT/build.log 2>&1 || { tail -30 $OUT/build.log; exit 1; }
+for s in $STAGES; do
+  case $s in
+    tests)  timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/tests_gpu.log 2>&1; echo "tests rc=$?"; tail -3 $OUT/tests_gpu.log;;
+    smoke)  timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > $OUT/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.log;;
+    bench)  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json; tail -5 $OUT/bench.err;;
+    benchq) timeout 600 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json; tail -5 $OUT/bench.err;;
+    ref)    timeout 900 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?"; cat $OUT/bench_ref.json; tail -3 $OUT/bench_ref.err;;
+    launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+                --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+                > $OUT/launches.log 2>&1; echo "launches rc=$?"; tail -2 $OUT/launches.log;;
+    full)   for k in vs_attention_ws_kernel score_lines_kernel decode_kernel compact_kernel select_kernel; do
+              timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 40 -c 2 \
+                -o $OUT/prof_$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+                > $OUT/prof_$k.log 2>&1; echo "full $k rc=$?"; done;;
+  esac
+done
