@@ -30,12 +30,15 @@
 // K8 (all layers) replaces compact_cache (kvcompress.py:133-147): coalesced
 // 16-byte gather of the picked K/V rows into the contiguous per-head cache.
 
+#include <algorithm>
+
 #include "ls_common.cuh"
+#include "tc_common.cuh"
 
 namespace ls {
 namespace dec {
 
-constexpr int K6_THREADS = 256;
+constexpr int K6_THREADS = 128;
 constexpr int K7_THREADS = 1024;
 constexpr int K7_SMEM_CAP = 24 * 1024;  // ids accumulated in shared memory (fp64) up to this length
 
@@ -62,27 +65,61 @@ __device__ __forceinline__ Geo geometry(const ls_decode_stack &S, int layer, int
 }
 
 // ------------------------------------------------------------------ K6
+// Split-K over columns: CTA (split, unit) owns a contiguous column range and
+// streams it in tiles of K6_TILE rows. K and V tiles are staged in shared
+// memory with cp.async (16-B chunks, double-buffered, zero-filled past the
+// range), so every HBM byte is requested once, coalesced, with two tiles in
+// flight per CTA and several CTAs per SM. Scores: 8 lanes per row (16 B
+// chunks, conflict-free quarter-warp phases), q in registers, shuffle
+// reduction; the raw log2 logits go to the ring (coalesced, 64 per head).
+// Online softmax per CTA across its tiles; PV: warp w owns 16 rows of a tile,
+// lane owns D/32 dims. The last CTA of a unit combines the splits in split
+// order (deterministic).
+constexpr int K6_TILE = 64;
+constexpr int K6_STAGES = 2;
+constexpr int K6_MAX_SPLIT = 256;
+
+__device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void *g, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(valid ? 16 : 0) : "memory");
+}
+
+template <int D>
+constexpr int k6_smem_bytes(int G) {
+  return 2 * K6_STAGES * K6_TILE * D * 2 + 2 * G * K6_TILE * 4;
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, int layer, const uint16_t *q,
                                                             const uint16_t *k, const uint16_t *v, int compressed,
-                                                            int cs, float scale_log2, void *out, int out_bf16) {
-  constexpr int DPL = D / 32;  // dims per lane in the PV phase
-  extern __shared__ float dsm[];
-  float(*qf)[D] = reinterpret_cast<float(*)[D]>(dsm);                       // [G][D]
-  float(*sc)[512] = reinterpret_cast<float(*)[512]>(dsm + G * D);          // [G][512] scores / probabilities
-  float(*opart)[G][D] = reinterpret_cast<float(*)[G][D]>(dsm + G * D + G * 512);  // [8][G][D]
-  __shared__ float red[G][8];
+                                                            float scale_log2, void *out, int out_bf16) {
+  constexpr int ROW_B = D * 2;
+  constexpr int CH = D / 8;                 // 16-B chunks per row
+  constexpr int CPL = CH / 8;               // chunks per lane in the score phase (8 lanes per row)
+  constexpr int TILE_B = K6_TILE * ROW_B;
+  constexpr int DPL = D / 32;               // dims per lane in the PV phase
+  constexpr int GS = G < 4 ? G : 4;         // heads per score pass (register bound)
+  constexpr int NSUB = (G + GS - 1) / GS;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  unsigned char *kt = dsm;
+  unsigned char *vt = dsm + K6_STAGES * TILE_B;
+  float *ps = reinterpret_cast<float *>(dsm + 2 * K6_STAGES * TILE_B);  // [G][TILE] raw log2 scores
+  float *pp = ps + G * K6_TILE;                                        // [G][TILE] probabilities
+  float *ored = reinterpret_cast<float *>(dsm);                        // [4][G][D] (aliases the tiles at the end)
+  __shared__ float wsp[K6_MAX_SPLIT], lsp[K6_MAX_SPLIT];
   __shared__ int ticket;
-  const int split = blockIdx.x, unit = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  const int split = blockIdx.x, unit = blockIdx.y, n_split = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, seg = lane & 7;
   const int length = S.step[0];
   const int slot = S.step[1] % S.window;
   const int group = S.n_heads / S.n_kv_heads;
   const int kv = compressed ? unit / group : unit;
-  const int h0 = compressed ? unit : unit * G;  // first q-head of this unit
+  const int h0 = compressed ? unit : unit * G;
   const Geo geo = geometry(S, layer, h0, length, compressed);
-  const int c_begin = split * cs, c_end = min(geo.n_cols, c_begin + cs);
-  const int n = max(0, c_end - c_begin);
+  const int per = ((geo.n_cols + n_split - 1) / n_split + K6_TILE - 1) / K6_TILE * K6_TILE;
+  const int c_begin = min(geo.n_cols, split * per);
+  const int c_end = min(geo.n_cols, c_begin + per);
+  const int n_tiles = (c_end - c_begin + K6_TILE - 1) / K6_TILE;
   const uint16_t *kb = k + static_cast<int64_t>(kv) * S.kv_head_stride;
   const uint16_t *vb = v + static_cast<int64_t>(kv) * S.kv_head_stride;
   const int64_t hr0 = head_row(S, layer, h0);
@@ -90,153 +127,205 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   const uint16_t *cvb = S.cv + hr0 * S.budget_cap * D;
   const int32_t *sel = S.sel_ids + hr0 * S.budget_cap;
 
-  for (int i = tid; i < G * D; i += blockDim.x) qf[i / D][i % D] = bf2f(q[static_cast<int64_t>(h0) * D + i]);
-  __syncthreads();
-  // ---- scores: one thread per column
-  float mloc[G];
+  auto issue = [&](int t) {
+    const int st = t % K6_STAGES;
+    const int c0 = c_begin + t * K6_TILE;
+    const uint32_t ks = tc::smem_u32(kt + st * TILE_B), vs = tc::smem_u32(vt + st * TILE_B);
 #pragma unroll
-  for (int g = 0; g < G; ++g) mloc[g] = -INFINITY;
-  for (int jj = tid; jj < n; jj += blockDim.x) {
-    const int j = c_begin + jj;
-    int id;
-    const uint16_t *kr;
-    if (j < geo.n_a) {
-      id = sel[j];
-      kr = ckb + static_cast<int64_t>(j) * D;
-    } else {
-      id = geo.lo + (j - geo.n_a);
-      kr = kb + static_cast<int64_t>(id) * D;
+    for (int it = 0; it < K6_TILE * CH / K6_THREADS; ++it) {
+      const int i = tid + it * K6_THREADS;
+      const int r = i / CH, c = i % CH;
+      const int j = c0 + r;
+      const bool ok = j < c_end;
+      int64_t off;
+      const uint16_t *kbase, *vbase;
+      if (j < geo.n_a) {
+        off = static_cast<int64_t>(j) * D;
+        kbase = ckb, vbase = cvb;
+      } else {
+        off = static_cast<int64_t>(ok ? geo.lo + (j - geo.n_a) : 0) * D;
+        kbase = kb, vbase = vb;
+      }
+      cp_async16_zfill(ks + r * ROW_B + c * 16, kbase + off + c * 8, ok);
+      cp_async16_zfill(vs + r * ROW_B + c * 16, vbase + off + c * 8, ok);
     }
-    float acc[G];
+    tc::cp_async_commit();
+  };
+
+  if (n_tiles > 0) issue(0);
+
+  // q of the first head sub-group stays in registers (dims of this lane's chunks)
+  float qr[GS][CPL * 8];
+  auto load_q = [&](int gb) {
 #pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = 0.f;
-#pragma unroll 4
-    for (int c8 = 0; c8 < D / 8; ++c8) {
-      float f[8];
-      bf16x8_to_f32(*reinterpret_cast<const uint4 *>(kr + c8 * 8), f);
+    for (int g = 0; g < GS; ++g)
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[g] = fmaf(qf[g][c8 * 8 + e], f[e], acc[g]);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float s = acc[g] * scale_log2;
-      sc[g][jj] = s;
-      mloc[g] = fmaxf(mloc[g], s);
-      const int64_t hr = head_row(S, layer, h0 + g);
-      S.ring_s[(hr * S.window + slot) * S.row_cap + j] = s;  // raw logit, normalised at events
-      if (compressed) S.ring_ids[(hr * S.window + slot) * S.sparse_cap + j] = id;
-    }
-  }
+      for (int m = 0; m < CPL; ++m) {
+        const int hh = min(h0 + gb + g, h0 + G - 1);
+        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4 *>(q + static_cast<int64_t>(hh) * D + (seg + 8 * m) * 8)),
+                      &qr[g][m * 8]);
+      }
+  };
+  if (NSUB == 1) load_q(0);
+
+  float m_run[G], l_run[G], o[G][DPL];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const float m = warp_max(mloc[g]);
-    if (lane == 0) red[g][warp] = m;
-  }
-  __syncthreads();
-  float mg[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    float m = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) m = fmaxf(m, red[g][w]);
-    mg[g] = m;
-  }
-  __syncthreads();
-  float lloc[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) lloc[g] = 0.f;
-  for (int jj = tid; jj < n; jj += blockDim.x)
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float pv = fast_exp2(sc[g][jj] - mg[g]);
-      sc[g][jj] = pv;
-      lloc[g] += pv;
-    }
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float l = warp_sum(lloc[g]);
-    if (lane == 0) red[g][warp] = l;
-  }
-  __syncthreads();
-  // ---- PV: warp w takes columns w, w+8, ...; lane owns DPL dims
-  float o[G][DPL];
-#pragma unroll
-  for (int g = 0; g < G; ++g)
+    m_run[g] = -INFINITY;
+    l_run[g] = 0.f;
 #pragma unroll
     for (int e = 0; e < DPL; ++e) o[g][e] = 0.f;
-  for (int jj = warp; jj < n; jj += 8) {
-    const int j = c_begin + jj;
-    const uint16_t *vr = (j < geo.n_a) ? cvb + static_cast<int64_t>(j) * D
-                                       : vb + static_cast<int64_t>(geo.lo + (j - geo.n_a)) * D;
-    float f[DPL];
-    if constexpr (DPL == 4) {
-      const uint2 u = *reinterpret_cast<const uint2 *>(vr + lane * 4);
-      f[0] = __uint_as_float(u.x << 16);
-      f[1] = __uint_as_float(u.x & 0xffff0000u);
-      f[2] = __uint_as_float(u.y << 16);
-      f[3] = __uint_as_float(u.y & 0xffff0000u);
+  }
+
+  for (int t = 0; t < n_tiles; ++t) {
+    const int st = t % K6_STAGES;
+    const int c0 = c_begin + t * K6_TILE;
+    if (t + 1 < n_tiles) {
+      issue(t + 1);
+      tc::cp_async_wait<1>();
     } else {
-      const uint32_t u = *reinterpret_cast<const uint32_t *>(vr + lane * 2);
-      f[0] = __uint_as_float(u << 16);
-      f[1] = __uint_as_float(u & 0xffff0000u);
+      tc::cp_async_wait<0>();
+    }
+    __syncthreads();
+    const unsigned char *ktile = kt + st * TILE_B;
+    // ---- scores
+#pragma unroll
+    for (int sb = 0; sb < NSUB; ++sb) {
+      if (NSUB > 1) load_q(sb * GS);
+#pragma unroll
+      for (int it = 0; it < K6_TILE / 16; ++it) {
+        const int r = warp * (K6_TILE / 4) + it * 4 + (lane >> 3);
+        float acc[GS];
+#pragma unroll
+        for (int g = 0; g < GS; ++g) acc[g] = 0.f;
+#pragma unroll
+        for (int m = 0; m < CPL; ++m) {
+          float f[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4 *>(ktile + r * ROW_B + (seg + 8 * m) * 16), f);
+#pragma unroll
+          for (int g = 0; g < GS; ++g)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[g] = fmaf(qr[g][m * 8 + e], f[e], acc[g]);
+        }
+#pragma unroll
+        for (int g = 0; g < GS; ++g) {
+          acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 1);
+          acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 2);
+          acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 4);
+        }
+        if (seg == 0) {
+#pragma unroll
+          for (int g = 0; g < GS; ++g)
+            if (sb * GS + g < G) ps[(sb * GS + g) * K6_TILE + r] = (c0 + r < c_end) ? acc[g] * scale_log2 : -INFINITY;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- ring rows (raw log2 logits, normalised at events) + online softmax
+    if (tid < K6_TILE && c0 + tid < c_end) {
+      const int j = c0 + tid;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int64_t hr = head_row(S, layer, h0 + g);
+        S.ring_s[(hr * S.window + slot) * S.row_cap + j] = ps[g * K6_TILE + tid];
+        if (compressed) S.ring_ids[(hr * S.window + slot) * S.sparse_cap + j] = j < geo.n_a ? sel[j] : geo.lo + (j - geo.n_a);
+      }
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float pv = sc[g][jj];
+      const float a = ps[g * K6_TILE + lane], b = ps[g * K6_TILE + 32 + lane];
+      const float m_new = fmaxf(m_run[g], warp_max(fmaxf(a, b)));
+      const float corr = m_run[g] == -INFINITY ? 0.f : fast_exp2(m_run[g] - m_new);
+      const float pa = a == -INFINITY ? 0.f : fast_exp2(a - m_new);
+      const float pb = b == -INFINITY ? 0.f : fast_exp2(b - m_new);
+      l_run[g] = l_run[g] * corr + warp_sum(pa + pb);
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) o[g][e] = fmaf(pv, f[e], o[g][e]);
+      for (int e = 0; e < DPL; ++e) o[g][e] *= corr;
+      m_run[g] = m_new;
+      // this warp's rows [16 warp, 16 warp + 16): row r < 32 sits in lane r of a, else lane r - 32 of b
+      const int r = warp * 16 + (lane & 15);
+      if ((lane >> 4) == (warp & 1)) pp[g * K6_TILE + r] = (warp < 2) ? pa : pb;
     }
+    __syncwarp();
+    // ---- PV over this warp's 16 rows
+    const unsigned char *vtile = vt + st * TILE_B;
+#pragma unroll 4
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = warp * 16 + rr;
+      float f[DPL];
+      if constexpr (DPL == 4) {
+        const uint2 u = *reinterpret_cast<const uint2 *>(vtile + r * ROW_B + lane * 8);
+        f[0] = __uint_as_float(u.x << 16);
+        f[1] = __uint_as_float(u.x & 0xffff0000u);
+        f[2] = __uint_as_float(u.y << 16);
+        f[3] = __uint_as_float(u.y & 0xffff0000u);
+      } else {
+        const uint32_t u = *reinterpret_cast<const uint32_t *>(vtile + r * ROW_B + lane * 4);
+        f[0] = __uint_as_float(u << 16);
+        f[1] = __uint_as_float(u & 0xffff0000u);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float pv = pp[g * K6_TILE + r];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[g][e] = fmaf(pv, f[e], o[g][e]);
+      }
+    }
+    __syncthreads();  // stage st and ps/pp are reused by tile t + 2 / t + 1
   }
+
+  // ---- cross-warp reduce -> this split's partial
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) opart[warp][g][lane * DPL + e] = o[g][e];
+    for (int e = 0; e < DPL; ++e) ored[(warp * G + g) * D + lane * DPL + e] = o[g][e];
   __syncthreads();
-  // ---- partial -> global, ticket
-  const int n_split = gridDim.x;
-  for (int i = tid; i < G * (D + 2); i += blockDim.x) {
+  for (int i = tid; i < G * (D + 2); i += K6_THREADS) {
     const int g = i / (D + 2), e = i % (D + 2);
-    const int64_t hr = head_row(S, layer, h0 + g);
-    float *pp = S.partials + (static_cast<int64_t>(h0 + g) * n_split + split) * (D + 2);
-    (void)hr;
+    float *pg = S.partials + (static_cast<int64_t>(h0 + g) * n_split + split) * (D + 2);
+    float val;
     if (e == 0) {
-      pp[0] = mg[g];
+      val = m_run[g];
     } else if (e == 1) {
-      float l = 0.f;
-      for (int w = 0; w < 8; ++w) l += red[g][w];
-      pp[1] = (n > 0) ? l : 0.f;
+      val = l_run[g];
     } else {
-      float acc = 0.f;
-      for (int w = 0; w < 8; ++w) acc += opart[w][g][e - 2];
-      pp[e] = acc;
+      val = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) val += ored[(w * G + g) * D + e - 2];
     }
+    pg[e] = val;
   }
   __threadfence();
   __syncthreads();
   if (tid == 0) ticket = atomicAdd(S.counters + unit, 1);
   __syncthreads();
   if (ticket != n_split - 1) return;
-  // ---- last CTA of this unit: combine splits (deterministic split order)
+  // ---- last CTA of this unit: combine the splits in split order
   __threadfence();
   for (int g = 0; g < G; ++g) {
     const int h = h0 + g;
-    const float *pp = S.partials + static_cast<int64_t>(h) * n_split * (D + 2);
-    float M = -INFINITY;
-    for (int s = 0; s < n_split; ++s) M = fmaxf(M, __ldcg(pp + s * (D + 2)));
-    float Lsum = 0.f;
-    for (int s = 0; s < n_split; ++s) {
-      const float ms = __ldcg(pp + s * (D + 2));
-      if (ms != -INFINITY) Lsum += __ldcg(pp + s * (D + 2) + 1) * fast_exp2(ms - M);
+    const float *pg = S.partials + static_cast<int64_t>(h) * n_split * (D + 2);
+    for (int s = tid; s < n_split; s += K6_THREADS) {
+      wsp[s] = __ldcg(pg + s * (D + 2));
+      lsp[s] = __ldcg(pg + s * (D + 2) + 1);
     }
+    __syncthreads();
+    float M = -INFINITY;
+    for (int s = 0; s < n_split; ++s) M = fmaxf(M, wsp[s]);
+    __syncthreads();
+    for (int s = tid; s < n_split; s += K6_THREADS) {
+      const float w = wsp[s] == -INFINITY ? 0.f : fast_exp2(wsp[s] - M);
+      wsp[s] = w;
+      lsp[s] *= w;
+    }
+    __syncthreads();
+    float Lsum = 0.f;
+    for (int s = 0; s < n_split; ++s) Lsum += lsp[s];
     const float inv = 1.f / Lsum;
-    for (int e = tid; e < D; e += blockDim.x) {
+    for (int e = tid; e < D; e += K6_THREADS) {
       float acc = 0.f;
-      for (int s = 0; s < n_split; ++s) {
-        const float ms = __ldcg(pp + s * (D + 2));
-        if (ms != -INFINITY) acc += __ldcg(pp + s * (D + 2) + 2 + e) * fast_exp2(ms - M);
-      }
+#pragma unroll 16
+      for (int s = 0; s < n_split; ++s) acc = fmaf(wsp[s], __ldcg(pg + s * (D + 2) + 2 + e), acc);
       if (out_bf16)
         reinterpret_cast<uint16_t *>(out)[static_cast<int64_t>(h) * D + e] = f2bf(acc * inv);
       else
@@ -249,6 +338,7 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
       S.ring_n[hr * S.window + slot] = geo.n_cols;
       S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
     }
+    __syncthreads();
   }
   if (tid == 0) S.counters[unit] = 0;  // re-armed for the next step / graph replay
 }
@@ -476,22 +566,35 @@ static int check_stack(const ls_decode_stack *S) {
   return LS_OK;
 }
 
-static int split_cols(int compressed) { return compressed ? 256 : 512; }
+// split count: enough CTAs to cover the SMs a few times, never more than
+// the tiles of the longest row
+static int decode_splits(int units, int max_cols) {
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const int target = n_sm * 3;
+  const int tiles = ceil_div(max_cols, dec::K6_TILE);
+  return std::max(1, std::min({ceil_div(target, units), tiles, dec::K6_MAX_SPLIT}));
+}
 
 template <int D, int G>
 static int launch_decode(dim3 grid, cudaStream_t st, const ls_decode_stack *S, int layer, const uint16_t *q,
-                         const uint16_t *k, const uint16_t *v, int compressed, int cs, float sl, void *out,
-                         int out_bf16) {
-  const int smem = (G * D + G * 512 + 8 * G * D) * 4;
+                         const uint16_t *k, const uint16_t *v, int compressed, float sl, void *out, int out_bf16) {
+  const int smem = dec::k6_smem_bytes<D>(G);
+  static_assert(dec::k6_smem_bytes<D>(G) >= 4 * G * D * 4, "reduction buffer must fit in the tile buffers");
   if (smem > 48 * 1024)
     LS_CUDA(cudaFuncSetAttribute(dec::decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dec::decode_kernel<D, G><<<grid, dec::K6_THREADS, smem, st>>>(*S, layer, q, k, v, compressed, cs, sl, out, out_bf16);
+  dec::decode_kernel<D, G><<<grid, dec::K6_THREADS, smem, st>>>(*S, layer, q, k, v, compressed, sl, out, out_bf16);
   return LS_OK;
 }
 
 extern "C" size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len) {
-  const size_t n_split = static_cast<size_t>(ceil_div(max_len + 1, split_cols(1)));
-  return static_cast<size_t>(S->n_heads) * n_split * (S->head_dim + 2) * sizeof(float);
+  (void)max_len;
+  return static_cast<size_t>(S->n_heads) * dec::K6_MAX_SPLIT * (S->head_dim + 2) * sizeof(float);
 }
 
 extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
@@ -503,18 +606,16 @@ extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uin
   LS_REQUIRE(max_cols >= 1 && max_cols <= S->row_cap, LS_ERR_SEQUENCE_TOO_LONG,
              "max_cols %d exceeds the ring row capacity %d", max_cols, S->row_cap);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int cs = split_cols(compressed);
-  const int n_split = ceil_div(max_cols, cs);
   const float sl = kLog2e / sqrtf(static_cast<float>(S->head_dim));
   const int group = S->n_heads / S->n_kv_heads;
   int r = LS_OK;
   if (compressed) {
-    dim3 grid(n_split, S->n_heads);
-    r = S->head_dim == 128 ? launch_decode<128, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, cs, sl, out, out_bf16)
-                           : launch_decode<64, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, cs, sl, out, out_bf16);
+    dim3 grid(decode_splits(S->n_heads, max_cols), S->n_heads);
+    r = S->head_dim == 128 ? launch_decode<128, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16)
+                           : launch_decode<64, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16);
   } else {
-    dim3 grid(n_split, S->n_kv_heads);
-#define LS_DENSE(DD, GG) r = launch_decode<DD, GG>(grid, st, S, layer, q, k_layer, v_layer, 0, cs, sl, out, out_bf16)
+    dim3 grid(decode_splits(S->n_kv_heads, max_cols), S->n_kv_heads);
+#define LS_DENSE(DD, GG) r = launch_decode<DD, GG>(grid, st, S, layer, q, k_layer, v_layer, 0, sl, out, out_bf16)
     if (S->head_dim == 128) {
       if (group == 1) LS_DENSE(128, 1);
       else if (group == 2) LS_DENSE(128, 2);

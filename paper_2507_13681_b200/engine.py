@@ -200,13 +200,15 @@ class SessionEngine:
         comp_cols = min((comp.budget or 0) + self.window + 1, L0 + max_new + 1)
         q_buf = torch.empty((sh.n_layers, sh.n_q, 1, sh.d), dtype=torch.bfloat16, device=self.device)
         out_buf = torch.empty((sh.n_layers, sh.n_q, sh.d), dtype=self.out_dtype, device=self.device)
-        # K/V columns each step reads per KV head (all layers): the algorithmic
-        # HBM traffic of a step is 4*d bytes per column (bf16 K + V rows)
+        # K/V rows each step reads (all layers), 4*d bytes each (bf16 K + V):
+        # dense steps read each archive row once per KV head (the q-group
+        # shares it); compressed steps read each q-head's own compacted cache
+        # (per-q-head kept sets) plus the recent window
         for t in range(max_new):
             if t < n_dense:
                 self.decode_log.append(("dense", (L0 + t + 1) * sh.n_kv * sh.n_layers))
             else:
-                self.decode_log.append(("comp", min(comp_cols, L0 + t + 1) * sh.n_kv * sh.n_layers))
+                self.decode_log.append(("comp", min(comp_cols, L0 + t + 1) * sh.n_q * sh.n_layers))
         if not use_graphs:
             compressed = False
             for n_o in range(1, max_new + 1):
