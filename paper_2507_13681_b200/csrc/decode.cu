@@ -50,12 +50,27 @@ struct Geo {
   int n_a, lo, n_cols;
 };
 
+// first index i in [0, n) with a[i] >= x, all threads of the block together:
+// two dependent global round trips (128 strided samples, then one bucket)
+// instead of log2(n) for a single-thread binary search
+__device__ __forceinline__ int block_lower_bound(const int32_t *a, int n, int x) {
+  const int nt = blockDim.x;
+  const int stride = (n + nt - 1) / nt;
+  const int t = threadIdx.x;
+  const int c1 = __syncthreads_count(t * stride < n && __ldg(a + t * stride) < x);
+  if (c1 == 0) return 0;
+  const int start = (c1 - 1) * stride;
+  const int c2 = __syncthreads_count(t < stride && start + t < n && __ldg(a + start + t) < x);
+  return start + c2;
+}
+
+// geometry of a q-head's working set at this step (called by every thread)
 __device__ __forceinline__ Geo geometry(const ls_decode_stack &S, int layer, int h, int length, int compressed) {
   Geo g;
   if (compressed) {
     g.lo = max(0, length - S.window);
     const int64_t hr = head_row(S, layer, h);
-    g.n_a = lower_bound_dev(S.sel_ids + hr * S.budget_cap, S.n_sel[hr], g.lo);
+    g.n_a = block_lower_bound(S.sel_ids + hr * S.budget_cap, S.n_sel[hr], g.lo);
   } else {
     g.lo = 0;
     g.n_a = 0;
@@ -105,7 +120,6 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   float *ps = reinterpret_cast<float *>(dsm + 2 * K6_STAGES * TILE_B);  // [G][TILE] raw log2 scores
   float *pp = ps + G * K6_TILE;                                        // [G][TILE] probabilities
   float *ored = reinterpret_cast<float *>(dsm);                        // [4][G][D] (aliases the tiles at the end)
-  __shared__ float wsp[K6_MAX_SPLIT], lsp[K6_MAX_SPLIT];
   __shared__ int ticket;
 
   const int split = blockIdx.x, unit = blockIdx.y, n_split = gridDim.x;
@@ -300,45 +314,56 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   if (tid == 0) ticket = atomicAdd(S.counters + unit, 1);
   __syncthreads();
   if (ticket != n_split - 1) return;
-  // ---- last CTA of this unit: combine the splits in split order
+  // ---- last CTA of this unit: combine the splits in split order, all G heads
+  // at once (the tile buffers are free: [G][n_split] weights and sums there)
   __threadfence();
-  for (int g = 0; g < G; ++g) {
-    const int h = h0 + g;
-    const float *pg = S.partials + static_cast<int64_t>(h) * n_split * (D + 2);
-    for (int s = tid; s < n_split; s += K6_THREADS) {
-      wsp[s] = __ldcg(pg + s * (D + 2));
-      lsp[s] = __ldcg(pg + s * (D + 2) + 1);
+  float *wsg = reinterpret_cast<float *>(dsm);       // [G][n_split] max, then weight
+  float *lsg = wsg + G * n_split;                     // [G][n_split] sum, then weighted sum
+  float *mg = lsg + G * n_split;                      // [G] max, [G] total
+  const float *pbase = S.partials + static_cast<int64_t>(h0) * n_split * (D + 2);
+  for (int i = tid; i < G * n_split; i += K6_THREADS) {
+    wsg[i] = __ldcg(pbase + static_cast<int64_t>(i) * (D + 2));
+    lsg[i] = __ldcg(pbase + static_cast<int64_t>(i) * (D + 2) + 1);
+  }
+  __syncthreads();
+  for (int g = warp; g < G; g += K6_THREADS / 32) {
+    float m = -INFINITY;
+    for (int s = lane; s < n_split; s += 32) m = fmaxf(m, wsg[g * n_split + s]);
+    m = warp_max(m);
+    float l = 0.f;
+    for (int s = lane; s < n_split; s += 32) {
+      const float ms = wsg[g * n_split + s];
+      const float w = ms == -INFINITY ? 0.f : fast_exp2(ms - m);
+      wsg[g * n_split + s] = w;
+      l += lsg[g * n_split + s] * w;
     }
-    __syncthreads();
-    float M = -INFINITY;
-    for (int s = 0; s < n_split; ++s) M = fmaxf(M, wsp[s]);
-    __syncthreads();
-    for (int s = tid; s < n_split; s += K6_THREADS) {
-      const float w = wsp[s] == -INFINITY ? 0.f : fast_exp2(wsp[s] - M);
-      wsp[s] = w;
-      lsp[s] *= w;
+    l = warp_sum(l);
+    if (lane == 0) {
+      mg[g] = m;
+      mg[G + g] = l;
     }
-    __syncthreads();
-    float Lsum = 0.f;
-    for (int s = 0; s < n_split; ++s) Lsum += lsp[s];
-    const float inv = 1.f / Lsum;
-    for (int e = tid; e < D; e += K6_THREADS) {
-      float acc = 0.f;
-#pragma unroll 16
-      for (int s = 0; s < n_split; ++s) acc = fmaf(wsp[s], __ldcg(pg + s * (D + 2) + 2 + e), acc);
-      if (out_bf16)
-        reinterpret_cast<uint16_t *>(out)[static_cast<int64_t>(h) * D + e] = f2bf(acc * inv);
-      else
-        reinterpret_cast<float *>(out)[static_cast<int64_t>(h) * D + e] = acc * inv;
-    }
-    if (tid == 0) {
-      const int64_t hr = head_row(S, layer, h);
-      S.ring_ml[(hr * S.window + slot) * 2 + 0] = M;
-      S.ring_ml[(hr * S.window + slot) * 2 + 1] = Lsum;
-      S.ring_n[hr * S.window + slot] = geo.n_cols;
-      S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
-    }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int i = tid; i < G * D; i += K6_THREADS) {
+    const int g = i / D, e = i % D;
+    const float *pg = pbase + static_cast<int64_t>(g) * n_split * (D + 2) + 2 + e;
+    const float *wg = wsg + g * n_split;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int s = 0; s < n_split; ++s) acc = fmaf(wg[s], __ldcg(pg + s * (D + 2)), acc);
+    const float r = acc / mg[G + g];
+    const int64_t oi = static_cast<int64_t>(h0 + g) * D + e;
+    if (out_bf16)
+      reinterpret_cast<uint16_t *>(out)[oi] = f2bf(r);
+    else
+      reinterpret_cast<float *>(out)[oi] = r;
+  }
+  if (tid < G) {
+    const int64_t hr = head_row(S, layer, h0 + tid);
+    S.ring_ml[(hr * S.window + slot) * 2 + 0] = mg[tid];
+    S.ring_ml[(hr * S.window + slot) * 2 + 1] = mg[G + tid];
+    S.ring_n[hr * S.window + slot] = geo.n_cols;
+    S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
   }
   if (tid == 0) S.counters[unit] = 0;  // re-armed for the next step / graph replay
 }
@@ -586,6 +611,7 @@ static int launch_decode(dim3 grid, cudaStream_t st, const ls_decode_stack *S, i
                          const uint16_t *k, const uint16_t *v, int compressed, float sl, void *out, int out_bf16) {
   const int smem = dec::k6_smem_bytes<D>(G);
   static_assert(dec::k6_smem_bytes<D>(G) >= 4 * G * D * 4, "reduction buffer must fit in the tile buffers");
+  static_assert(dec::k6_smem_bytes<D>(G) >= (2 * G * dec::K6_MAX_SPLIT + 2 * G) * 4, "combine buffers must fit");
   if (smem > 48 * 1024)
     LS_CUDA(cudaFuncSetAttribute(dec::decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dec::decode_kernel<D, G><<<grid, dec::K6_THREADS, smem, st>>>(*S, layer, q, k, v, compressed, sl, out, out_bf16);

@@ -446,6 +446,20 @@ extern "C" int ls_vs_attention_simt(const ls_layer_desc *L, const uint16_t *q, c
   return LS_OK;
 }
 
+// stream-ordered scratch: keep the default pool's memory across syncs so the
+// per-call cudaMallocAsync is a pool hit, not a fresh mapping
+static void keep_pool_memory() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
+
 extern "C" int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16_t *q, const uint16_t *k,
                             const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, float *out,
                             int64_t out_row_stride, int64_t out_head_stride, ls_stream_t stream) {
@@ -456,6 +470,7 @@ extern "C" int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int words = (L->n_total + 31) / 32;
   uint32_t *bits = nullptr;
+  keep_pool_memory();
   LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&bits), sizeof(uint32_t) * 2 * L->n_heads * words, st));
   uint32_t *sbits = bits, *vbits = bits + static_cast<size_t>(L->n_heads) * words;
   int s = build_bits(L, slash_ids, vert_ids, counts, sbits, vbits, st);
@@ -478,6 +493,7 @@ extern "C" int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, con
   if (stc) return stc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t *cells = nullptr;
+  keep_pool_memory();
   LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&cells), sizeof(int64_t) * L->n_heads, st));
   // dense mode touches every causal key block with the causal mask only (tensor-core path)
   int s = vs_attention_ws(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, 1, nullptr, 0, st);

@@ -36,6 +36,7 @@ from .prefill import LayerPlans, Workspace, sample_rows_device, sample_size, spa
 from .tensor_ops import attention_layer, dense_attention_layer, plan_rows
 
 MODES = ("dense", "loopserve")
+GRAPH_BUCKET = 1024  # column-bound bucket of the captured decode graphs
 
 
 @dataclass(frozen=True)
@@ -115,6 +116,10 @@ class SessionEngine:
                                  shape.n_kv * cap * shape.d, cap * shape.d, device=device)
         self.ws = Workspace()
         self.rows_ws = Workspace()
+        self.stack.event_workspace(self.stack.row_cap)  # fixed before any graph captures it
+        self._q_buf = torch.empty((shape.n_layers, shape.n_q, 1, shape.d), dtype=torch.bfloat16, device=device)
+        self._out_buf = torch.empty((shape.n_layers, shape.n_q, shape.d), dtype=out_dtype, device=device)
+        self._graphs = {}
         self.clear_logs()
 
     def clear_logs(self):
@@ -186,6 +191,23 @@ class SessionEngine:
             st.step(l, q_buf[l, :, 0], store.k[l], store.v[l], compressed, max_cols, out_buf[l], stream=stream)
         st.advance(stream=stream)
 
+    def _graph(self, key, name, fn):
+        """CUDA graph of a fixed launch sequence, captured once per key (the
+        kernels read the cache length and deque position from the device step
+        counters, so a graph serves every step and turn of its shape bucket)."""
+        g = self._graphs.get(key)
+        if g is None:
+            st = self.stack
+            host = (st.length, st.appended)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                g = _lib.Captured(name, s, fn)
+            torch.cuda.current_stream().wait_stream(s)
+            st.length, st.appended = host  # capture does not execute; restore the host mirror
+            self._graphs[key] = g
+        return g
+
     def decode(self, store: QKVStore, L0: int, max_new: int, use_graphs: bool = True, out_sink=None):
         """max_new decode steps (kvcompress.py:200-239) from cache length L0,
         after prefill() set the counters. Returns the last step's outputs
@@ -196,10 +218,11 @@ class SessionEngine:
         if p.mode == "dense":
             st.set_step(L0, 0)
         n_dense = max_new if comp.budget is None else min(max_new, comp.warmup - 1)
-        dense_cols = L0 + n_dense + 1
+        # grid sizes come from column bounds; bucket them so graphs are reused
+        dense_cols = min(st.row_cap, -(-(L0 + n_dense + 1) // GRAPH_BUCKET) * GRAPH_BUCKET)
         comp_cols = min((comp.budget or 0) + self.window + 1, L0 + max_new + 1)
-        q_buf = torch.empty((sh.n_layers, sh.n_q, 1, sh.d), dtype=torch.bfloat16, device=self.device)
-        out_buf = torch.empty((sh.n_layers, sh.n_q, sh.d), dtype=self.out_dtype, device=self.device)
+        ev_len = min(st.row_cap, -(-(L0 + max_new) // GRAPH_BUCKET) * GRAPH_BUCKET)
+        q_buf, out_buf = self._q_buf, self._out_buf
         # K/V rows each step reads (all layers), 4*d bytes each (bf16 K + V):
         # dense steps read each archive row once per KV head (the q-group
         # shares it); compressed steps read each q-head's own compacted cache
@@ -213,30 +236,22 @@ class SessionEngine:
             compressed = False
             for n_o in range(1, max_new + 1):
                 if comp.event_at(n_o):
-                    st.event(comp.budget, store.k, store.v, max_len=L0 + max_new)
+                    st.event(comp.budget, store.k, store.v, max_len=ev_len)
                     compressed = True
                 self._step(store, q_buf, out_buf, compressed, comp_cols if compressed else dense_cols)
                 if out_sink is not None:
                     out_sink(n_o - 1, out_buf)
             return out_buf
-        # ---- CUDA graphs (captured per turn: the dense grid depends on L0)
-        host = (st.length, st.appended)
-        st.event_workspace(L0 + max_new)
+        sk = id(store)
         graphs = {}
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            if n_dense > 0:
-                graphs["dense"] = _lib.Captured(
-                    "decode_graph_dense", s, lambda: self._step(store, q_buf, out_buf, False, dense_cols))
-            if n_dense < max_new:
-                graphs["comp"] = _lib.Captured(
-                    "decode_graph_comp", s, lambda: self._step(store, q_buf, out_buf, True, comp_cols))
-                graphs["event"] = _lib.Captured(
-                    "decode_graph_event", s,
-                    lambda: st.event(comp.budget, store.k, store.v, max_len=L0 + max_new))
-        torch.cuda.current_stream().wait_stream(s)
-        st.length, st.appended = host  # capture does not execute; restore the host mirror
+        if n_dense > 0:
+            graphs["dense"] = self._graph(("dense", sk, dense_cols), "decode_graph_dense",
+                                          lambda: self._step(store, q_buf, out_buf, False, dense_cols))
+        if n_dense < max_new:
+            graphs["comp"] = self._graph(("comp", sk, comp_cols), "decode_graph_comp",
+                                         lambda: self._step(store, q_buf, out_buf, True, comp_cols))
+            graphs["event"] = self._graph(("event", sk, comp.budget, ev_len), "decode_graph_event",
+                                          lambda: st.event(comp.budget, store.k, store.v, max_len=ev_len))
         compressed = False
         for n_o in range(1, max_new + 1):
             if comp.event_at(n_o):
@@ -247,7 +262,6 @@ class SessionEngine:
             st.appended += 1
             if out_sink is not None:
                 out_sink(n_o - 1, out_buf)
-        self._graphs = graphs  # keep alive until the next turn
         return out_buf
 
     def turn_blocks(self, input_len: int, n_turns: int, max_new: int):
