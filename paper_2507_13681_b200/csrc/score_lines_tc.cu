@@ -28,8 +28,10 @@ namespace k1tc {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int CHUNK = 1024;        // key columns per CTA
-constexpr int LDP = BN + 1;        // fp32 P row stride
-constexpr int ACC_CAP = 4096;      // shared slash accumulator (diagonals per chunk)
+constexpr int LDP = BN + 4;        // fp32 P row stride (16-B rows: conflict-free STS.128 / column LDS)
+constexpr int ACC_CAP = 3072;      // shared slash accumulator (diagonals per chunk)
+constexpr int RP_CAP = 2048;       // row-pointer table: first sampled row at or after a position
+constexpr int LINES_THREADS = 512; // 16 warps: 4 per TMEM lane quadrant
 constexpr double FIX = 1099511627776.0;  // 2^40
 constexpr double UNFIX = 1.0 / 1099511627776.0;
 
@@ -61,8 +63,9 @@ struct LinesSmem {
   static constexpr int OFF_P = OFF_K + 2 * BN * D * 2;
   static constexpr int OFF_ACC = OFF_P + BM * LDP * 4;         // double[ACC_CAP]
   static constexpr int OFF_ACCM = OFF_ACC + ACC_CAP * 8;       // float[ACC_CAP]
-  static constexpr int OFF_MISC = OFF_ACCM + ACC_CAP * 4;
-  static constexpr int TOTAL = OFF_MISC + 4096 + 1024;
+  static constexpr int OFF_RP = OFF_ACCM + ACC_CAP * 4;        // int[RP_CAP] row pointer by position
+  static constexpr int OFF_MISC = OFF_RP + RP_CAP * 4;  // barriers | gs | m | 1/l | colp [4][128] f64 | colm [4][128]
+  static constexpr int TOTAL = OFF_MISC + 2048 + 4096 + 2048 + 1024;
 };
 
 __device__ __forceinline__ void zfill16(uint32_t saddr, const void *g, bool ok) {
@@ -183,7 +186,17 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(Params p) {
       float sv[32];
       tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv);
       tc::tmem_wait_ld();
-      if (row_ok) {
+      if (row_ok && lim >= cch * 32 + 31) {  // whole chunk causal: no masking
+        float tm = sv[0];
+#pragma unroll
+        for (int j = 1; j < 32; ++j) tm = fmaxf(tm, sv[j]);
+        const float mn = fmaxf(m, tm * p.scale_log2);
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
+        l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
+        m = mn;
+      } else if (row_ok) {
         float tm = -INFINITY;
 #pragma unroll
         for (int j = 0; j < 32; ++j)
@@ -210,8 +223,15 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(Params p) {
 }
 
 // ------------------------------------------------------------- pass 2
+// 16 warps. Per 128-key tile: P = exp2(s - m) / l (fp32) from TMEM into
+// shared memory (warp w: TMEM lanes of quadrant w % 4, 32 columns of block
+// w / 4); vertical partials by 4 threads per column (32 rows each, fp64, in
+// row order); slash partials by thread-owns-diagonal, rows ascending, with
+// the first contributing row read from a position -> row table instead of a
+// binary search; per-tile slash sums (<= ~13 cells) in fp32, accumulated per
+// chunk in fp64 shared memory.
 template <int D>
-__global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
+__global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = LinesSmem<D>;
   unsigned char *smem =
@@ -221,13 +241,14 @@ __global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
   int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);              // [128]
   float *m_sh = reinterpret_cast<float *>(smem + L::OFF_MISC + 64 + 512);  // [128]
   float *li_sh = m_sh + BM;                                                 // [128]
-  double *colp = reinterpret_cast<double *>(smem + L::OFF_MISC + 2048);     // [2][128]
-  float *colm = reinterpret_cast<float *>(smem + L::OFF_MISC + 2048 + 2048);  // [2][128]
+  double *colp = reinterpret_cast<double *>(smem + L::OFF_MISC + 2048);         // [4][128]
+  float *colm = reinterpret_cast<float *>(smem + L::OFF_MISC + 2048 + 4096);    // [4][128]
   float *Pf = reinterpret_cast<float *>(smem + L::OFF_P);
   double *acc = reinterpret_cast<double *>(smem + L::OFF_ACC);
   float *accm = reinterpret_cast<float *>(smem + L::OFF_ACCM);
+  int *rp = reinterpret_cast<int *>(smem + L::OFF_RP);
   const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r_last = min(p.n_s, (rt + 1) * BM) - 1;
   const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
   const int c_begin = ck * CHUNK;
@@ -263,19 +284,29 @@ __global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
   if (tid == 0) issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
   const int g_first = gs[0];
   const int g_hi = gs[nr - 1];
+  // position -> first sampled row at or after it, for positions [g_first, g_hi]
+  const int rp_span = g_hi - g_first + 1;
+  const bool use_rp = rp_span <= RP_CAP;
+  if (use_rp)
+    for (int x = tid; x < rp_span; x += LINES_THREADS) rp[x] = lower_bound_dev(gs, nr, g_first + x);
   // slash accumulator window of the chunk: d in [d_base, d_base + width)
   const int d_base = max(0, g_first - (c_end - 1));
   const int width = g_hi - c_begin - d_base + 1;
   const bool smem_acc = width <= ACC_CAP;
   if (smem_acc)
-    for (int i = tid; i < width; i += blockDim.x) {
+    for (int i = tid; i < width; i += LINES_THREADS) {
       acc[i] = 0.0;
       accm[i] = 0.f;
     }
-  // TMEM reads: warp w -> lanes 32*(w%4), columns [64*(w/4), +64)
-  const int row = (warp & 3) * 32 + (tid & 31);
-  const int col_half = warp >> 2;
+  __syncthreads();
+  // TMEM reads: warp w -> lanes 32*(w%4), columns [32*(w/4), +32)
+  const int row = (warp & 3) * 32 + lane;
+  const int cblk = (warp >> 2) * 32;
   const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  const int my_g = gs[row];
+  const bool row_ok = row < nr;
+  // P = exp2(s * scale - m) / l = exp2(s * scale - (m + log2 l))
+  const float mr = li_sh[row] > 0.f ? m_sh[row] - __log2f(li_sh[row]) : INFINITY;
   uint32_t ph0 = 0, ph1 = 0;
   unsigned long long *sfix = p.sfix + static_cast<int64_t>(h) * p.n_total;
   unsigned int *smaxb = p.smaxb + static_cast<int64_t>(h) * p.n_total;
@@ -287,59 +318,71 @@ __global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
     if (buf) ph1 ^= 1; else ph0 ^= 1;
     tc::fence_after_sync();
     {
-      const int g = gs[row];
-      const bool ok = row < nr;
-      const int lim = min(g, c_end - 1) - c0;
-      const float mr = m_sh[row], li = li_sh[row];
+      const int lim = min(my_g, c_end - 1) - c0 - cblk;  // last valid column of this thread's 32
+      float sv[32];
+      tc::tmem_ld32(tmem + buf * 128 + lane_base + cblk, sv);
+      tc::tmem_wait_ld();
+      float4 *prow = reinterpret_cast<float4 *>(Pf + row * LDP + cblk);
+      if (row_ok && lim >= 31) {
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int cbase = col_half * 64 + half * 32;
-        float sv[32];
-        tc::tmem_ld32(tmem + buf * 128 + lane_base + cbase, sv);
-        tc::tmem_wait_ld();
+        for (int j = 0; j < 32; j += 4)
+          prow[j / 4] = make_float4(fast_exp2(fmaf(sv[j], p.scale_log2, -mr)), fast_exp2(fmaf(sv[j + 1], p.scale_log2, -mr)),
+                                    fast_exp2(fmaf(sv[j + 2], p.scale_log2, -mr)), fast_exp2(fmaf(sv[j + 3], p.scale_log2, -mr)));
+      } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          Pf[row * LDP + cbase + j] = (ok && cbase + j <= lim) ? fast_exp2(sv[j] * p.scale_log2 - mr) * li : 0.f;
+        for (int j = 0; j < 32; j += 4) {
+          float e[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            e[u] = (row_ok && j + u <= lim) ? fast_exp2(fmaf(sv[j + u], p.scale_log2, -mr)) : 0.f;
+          prow[j / 4] = make_float4(e[0], e[1], e[2], e[3]);
+        }
       }
     }
     if (t + 1 < n_tiles) tc::cp_async_wait<0>();
     cta_sync_tc();
     if (t + 1 < n_tiles && tid == 0) issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
-    // vertical partials: two threads per column (row halves), combined in order
+    // vertical partials: four threads per column (32-row quarters)
     {
-      const int j = tid & (BN - 1), hf = tid >> 7;
+      const int j = tid & (BN - 1), qq = tid >> 7;
       double sw = 0.0;
       float mx = 0.f;
-      const int r0 = hf * 64, r1 = min(nr, r0 + 64);
+      const int r0 = qq * 32, r1 = min(nr, r0 + 32);
       for (int r = r0; r < r1; ++r) {
         const float v = Pf[r * LDP + j];
         sw += static_cast<double>(v);
         mx = fmaxf(mx, v);
       }
-      colp[hf * BN + j] = sw;
-      colm[hf * BN + j] = mx;
+      colp[qq * BN + j] = sw;
+      colm[qq * BN + j] = mx;
     }
     // slash partials: thread owns diagonal d, rows ascending
     {
-      // cells of this chunk have d >= d_base (columns beyond c_end are not ours)
       const int d_lo = max(d_base, g_first - (c0 + BN - 1));
       const int d_hi = g_hi - c0;
-      for (int dd = d_lo + tid; dd <= d_hi; dd += blockDim.x) {
-        const int glo = c0 + dd, ghi = c0 + dd + BN - 1;
-        int r = lower_bound_dev(gs, nr, glo);
-        if (r >= nr || gs[r] > ghi) continue;
-        double sw = smem_acc ? acc[dd - d_base] : 0.0;
-        float mx = smem_acc ? accm[dd - d_base] : 0.f;
-        for (; r < nr && gs[r] <= ghi; ++r) {
-          const float v = Pf[r * LDP + (gs[r] - dd - c0)];
-          sw += static_cast<double>(v);
+      for (int dd = d_lo + tid; dd <= d_hi; dd += LINES_THREADS) {
+        const int glo = c0 + dd, ghi = min(c0 + dd + BN - 1, g_hi);
+        int r, r_end;
+        if (use_rp) {
+          r = rp[max(glo, g_first) - g_first];
+          r_end = ghi + 1 <= g_hi ? rp[ghi + 1 - g_first] : nr;
+        } else {
+          r = lower_bound_dev(gs, nr, glo);
+          r_end = lower_bound_dev(gs, nr, ghi + 1);
+        }
+        float sw = 0.f, mx = 0.f;
+        const float *pcol = Pf - dd - c0;
+#pragma unroll 4
+        for (; r < r_end; ++r) {
+          const float v = pcol[r * LDP + gs[r]];
+          sw += v;
           mx = fmaxf(mx, v);
         }
         if (smem_acc) {
-          acc[dd - d_base] = sw;
-          accm[dd - d_base] = mx;
-        } else if (sw > 0.0) {
-          atomicAdd(sfix + dd, to_fix(sw));
+          acc[dd - d_base] += static_cast<double>(sw);
+          accm[dd - d_base] = fmaxf(accm[dd - d_base], mx);
+        } else if (sw > 0.f) {
+          atomicAdd(sfix + dd, to_fix(static_cast<double>(sw)));
           atomicMax(smaxb + dd, __float_as_uint(mx));
         }
       }
@@ -348,8 +391,8 @@ __global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
     if (tid < BN) {
       const int c = c0 + tid;
       if (c < c_end) {
-        const double sw = colp[tid] + colp[BN + tid];
-        const float mx = fmaxf(colm[tid], colm[BN + tid]);
+        const double sw = ((colp[tid] + colp[BN + tid]) + colp[2 * BN + tid]) + colp[3 * BN + tid];
+        const float mx = fmaxf(fmaxf(colm[tid], colm[BN + tid]), fmaxf(colm[2 * BN + tid], colm[3 * BN + tid]));
         if (sw > 0.0) atomicAdd(p.vfix + static_cast<int64_t>(h) * p.n_total + c, to_fix(sw));
         if (mx > 0.f) atomicMax(p.vmaxb + static_cast<int64_t>(h) * p.n_total + c, __float_as_uint(mx));
       }
@@ -357,7 +400,7 @@ __global__ void __launch_bounds__(256) k1_lines_kernel(Params p) {
     __syncthreads();  // Pf / colp reused by the next tile
   }
   if (smem_acc)
-    for (int i = tid; i < width; i += blockDim.x) {
+    for (int i = tid; i < width; i += LINES_THREADS) {
       if (acc[i] > 0.0) atomicAdd(sfix + d_base + i, to_fix(acc[i]));
       if (accm[i] > 0.f) atomicMax(smaxb + d_base + i, __float_as_uint(accm[i]));
     }
@@ -457,14 +500,14 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
     k1tc::k1_stats_kernel<128><<<grid, 128, s1, st>>>(p);
     LS_LAUNCH_CHECK("k1_stats_kernel");
-    k1tc::k1_lines_kernel<128><<<grid, 256, s2, st>>>(p);
+    k1tc::k1_lines_kernel<128><<<grid, k1tc::LINES_THREADS, s2, st>>>(p);
   } else {
     const int s1 = k1tc::StatsSmem<64>::TOTAL, s2 = k1tc::LinesSmem<64>::TOTAL;
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
     k1tc::k1_stats_kernel<64><<<grid, 128, s1, st>>>(p);
     LS_LAUNCH_CHECK("k1_stats_kernel");
-    k1tc::k1_lines_kernel<64><<<grid, 256, s2, st>>>(p);
+    k1tc::k1_lines_kernel<64><<<grid, k1tc::LINES_THREADS, s2, st>>>(p);
   }
   LS_LAUNCH_CHECK("k1_lines_kernel");
   k1tc::k1_finish_kernel<<<L->n_heads, 512, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
