@@ -32,16 +32,17 @@
 #include "ls_common.cuh"
 
 namespace ls {
+extern int *g_debug_buffer;
 namespace sel {
 
 constexpr int SORT_THREADS = 512;
 constexpr int SORT_ITEMS = 32;  // capacity 16384
 constexpr int SORT_CAP = SORT_THREADS * SORT_ITEMS;
-constexpr int CHUNK = 512;      // staged lines per list in the chain kernel
 constexpr double EPS = 1e-12;   // prefill.py:188
 
 struct Lists {  // sorted lines, [H][2][n] (kind 0 = slash, 1 = vertical)
   int32_t *idx;
+  int32_t *inv;     // line index -> position in its sorted list
   double *w;
   int32_t *len;
   double *mx;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_lines_kernel(const double *
       out.w[base + o] = w[idx];
       out.mx[base + o] = static_cast<double>(mx[idx]);
       out.len[base + o] = n_s - lower_bound_dev(pos, n_s, idx);  // #{rows with g >= idx}, prefill.py:144,155
+      out.inv[base + idx] = o;
     }
   }
 }
@@ -104,27 +106,36 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_lines_kernel(const double *
 // Cell source 1: recompute P[r, c] from q, k and K1 row statistics.
 struct RecomputeCells {
   const uint16_t *q, *k;
-  const int32_t *row_of;  // [H][n_total] sampled row index of position g, or -1
+  const int32_t *rows;  // [H][n_s] sorted local rows of the sampled block
   const float *row_stats;
   int n_s, n_total, row_offset, d, group;
   int64_t q_head_stride, kv_head_stride;
   float scale_log2;
 
-  __device__ __forceinline__ int row(int h, int g) const {
-    return g < n_total ? row_of[static_cast<int64_t>(h) * n_total + g] : -1;
-  }
+  __device__ __forceinline__ int n_rows() const { return n_s; }
+  __device__ __forceinline__ int pos(int h, int r) const { return row_offset + rows[static_cast<int64_t>(h) * n_s + r]; }
   __device__ __forceinline__ double value(int h, int r, int g, int c) const {
-    const uint16_t *qr = q + static_cast<int64_t>(h) * q_head_stride + static_cast<int64_t>(g - row_offset) * d;
-    const uint16_t *kr = k + static_cast<int64_t>(h / group) * kv_head_stride + static_cast<int64_t>(c) * d;
+    const uint4 *qr = reinterpret_cast<const uint4 *>(q + static_cast<int64_t>(h) * q_head_stride +
+                                                      static_cast<int64_t>(g - row_offset) * d);
+    const uint4 *kr = reinterpret_cast<const uint4 *>(k + static_cast<int64_t>(h / group) * kv_head_stride +
+                                                      static_cast<int64_t>(c) * d);
     float acc = 0.f;
-    for (int v = 0; v < d / 8; ++v) {
-      uint4 a = *reinterpret_cast<const uint4 *>(qr + v * 8);
-      uint4 b = *reinterpret_cast<const uint4 *>(kr + v * 8);
-      float fa[8], fb[8];
-      bf16x8_to_f32(a, fa);
-      bf16x8_to_f32(b, fb);
+    // two batches of loads in flight (2 L2 round trips per cell at d = 128)
+    for (int v = 0; v < d / 8; v += 8) {
+      uint4 a[8], b[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc = fmaf(fa[j], fb[j], acc);
+      for (int u = 0; u < 8; ++u) {
+        a[u] = __ldg(qr + v + u);
+        b[u] = __ldg(kr + v + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float fa[8], fb[8];
+        bf16x8_to_f32(a[u], fa);
+        bf16x8_to_f32(b[u], fb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = fmaf(fa[j], fb[j], acc);
+      }
     }
     const float *rs = row_stats + (static_cast<int64_t>(h) * n_s + r) * 2;
     return static_cast<double>(fast_exp2(acc * scale_log2 - rs[0]) * rs[1]);
@@ -133,33 +144,40 @@ struct RecomputeCells {
 
 // Cell source 2: a dense fp64 weight matrix (greedy_select_lines parity path).
 struct DenseCells {
-  const double *weights;  // [n_rows][n_total]
-  const int32_t *row_of;  // [n_total]
-  int n_total;
-  __device__ __forceinline__ int row(int /*h*/, int g) const { return g < n_total ? row_of[g] : -1; }
+  const double *weights;     // [n_rows][n_total]
+  const int32_t *positions;  // [n_rows] sorted global positions
+  int n_rows_, n_total;
+  __device__ __forceinline__ int n_rows() const { return n_rows_; }
+  __device__ __forceinline__ int pos(int /*h*/, int r) const { return positions[r]; }
   __device__ __forceinline__ double value(int /*h*/, int r, int /*g*/, int c) const {
     return weights[static_cast<int64_t>(r) * n_total + c];
   }
 };
 
 // ------------------------------------------------------------ K3 greedy
-// One CTA per head. Rounds of: (A) thread 0 advances the decision chain by up
-// to PCH picks (prefill.py:195-220, approx-only decisions), (B) every warp
-// sums the crossing cells of some of the new picks with the other kind's
-// already-picked prefix, in selection order (prefill.py:211, 217), (C) thread
-// 0 replays exact += w - cross in order and applies the reference's dual
-// termination test (prefill.py:195). Stops at the first pick count where
-// approx or exact reaches alpha*T - eps, or when both lists are exhausted.
-struct Stage {
-  int32_t idx[CHUNK];
-  int32_t len[CHUNK];
-  double w[CHUNK];
-  double mx[CHUNK];
-};
-
-constexpr int PCH = 64;             // picks per round
-constexpr int G_THREADS = 512;      // 16 warps
-constexpr int G_WARPS = G_THREADS / 32;
+// One CTA per head, warp-specialised so that only the decision chain is
+// sequential and the exact-mass bookkeeping runs concurrently with it:
+//   warp 0, lane 0  producer: replays the decision chain of _greedy
+//                   (prefill.py:195-220) in fp64 over the sorted lists staged
+//                   in shared memory -- decisions depend on approx, ol_s, ol_v,
+//                   |S|, |V| only -- and publishes every pick (code, weight,
+//                   approx after it, picks of the other kind before it).
+//   warps 2..15     crossing sums, one warp per pick (prefill.py:211, 217): the
+//                   cells of the pick's line with the other kind's picked
+//                   prefix. A cell exists only at a sampled row g = c + d
+//                   (_BlockView.cell, prefill.py:116-122), so the warp walks the
+//                   sampled rows g >= line index and tests the other line's
+//                   sorted-list position against the prefix length (an
+//                   inverse permutation from K2) -- O(n_s) per pick, fully
+//                   independent of the other picks. Fixed-order warp sum.
+//   warp 1, lane 0  finalizer: exact += w - cross in selection order and the
+//                   reference's dual termination test (prefill.py:195); it
+//                   stops the producer as soon as the plan is complete.
+constexpr int WIN = 1024;            // staged lines per list
+constexpr int TAB_CAP = 16384;       // n_total up to which position tables live in shared memory
+constexpr int G_THREADS = 512;       // 16 warps
+constexpr int RING = 1024;           // picks in flight between producer and finalizer
+constexpr int GS_CAP = 8192;         // sampled positions kept in shared memory
 
 // gain_s >= gain_v with gain = num / den (prefill.py:206-208). Decided by
 // cross-multiplication unless the two sides are within 1e-13 relative, in
@@ -173,164 +191,276 @@ __device__ __forceinline__ bool take_slash_decision(double a, int ds, double b, 
   return a / static_cast<double>(ds) >= b / static_cast<double>(dv);
 }
 
+struct GreedySmem {
+  int32_t idx[2][WIN];
+  int32_t len[2][WIN];
+  double w[2][WIN];
+  double mx[2][WIN];
+  double r_w[RING], r_approx[RING], r_cross[RING];
+  int32_t r_code[RING], r_other[RING], r_seq[RING];
+  int32_t gs[GS_CAP];
+  int16_t rowof[TAB_CAP];    // position -> sampled row, or -1
+  uint16_t inv[2][TAB_CAP];  // line index -> sorted position (clamped to 65535)
+};
+
+__device__ __forceinline__ int vload(const volatile int *p) { return *p; }
+
 template <typename Cells>
-__global__ void __launch_bounds__(G_THREADS) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
-                                                            Picks P, int cap, Cells cells, int32_t *n_final,
-                                                            double *coverage, double *approx_out) {
-  __shared__ Stage st[2];  // 0 slash, 1 vertical
-  __shared__ int c_code[PCH], c_other[PCH];
-  __shared__ double c_w[PCH], c_approx[PCH], c_cross[PCH];
-  __shared__ double vals[G_WARPS][32];
-  __shared__ int s_base[2], s_idx_sh, v_idx_sh, n_sh, n_chunk, done, exhausted;
-  __shared__ double ol_s_sh, ol_v_sh, approx_sh, exact_sh;
+__global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
+                                                               Picks P, int cap, Cells cells, int32_t *n_final,
+                                                               double *coverage, double *approx_out, int *dbg) {
+  extern __shared__ __align__(16) unsigned char g_smem[];
+  const long long t_start = clock64();
+  GreedySmem &S = *reinterpret_cast<GreedySmem *>(g_smem);
+  __shared__ volatile int n_prod, prod_done, fin_pos, stop_at;
+  __shared__ int next_j;
   const int h = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double T = total[h];
   const double target = alpha * T;
   const int64_t lb = static_cast<int64_t>(h) * 2 * n_total;
   const int64_t pb = static_cast<int64_t>(h) * cap;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    s_idx_sh = v_idx_sh = n_sh = 0;
-    ol_s_sh = ol_v_sh = approx_sh = exact_sh = 0.0;
-    s_base[0] = s_base[1] = -1;
-    done = !(0.0 < target - EPS);  // the while condition fails before any pick
-    exhausted = 0;
+  const int n_rows = cells.n_rows();
+  const bool gs_smem = n_rows <= GS_CAP;
+  const int win = min(WIN, n_total);
+  for (int i = threadIdx.x; i < 2 * win; i += blockDim.x) {
+    const int kind = i / win, o = i % win;
+    const int64_t g = lb + static_cast<int64_t>(kind) * n_total + o;
+    S.idx[kind][o] = L.idx[g];
+    S.len[kind][o] = L.len[g];
+    S.w[kind][o] = L.w[g];
+    S.mx[kind][o] = L.mx[g];
   }
-  __syncthreads();
-  while (!done) {
-    // (re)stage whichever list's cursor left its chunk
-    for (int kind = 0; kind < 2; ++kind) {
-      const int cur = kind == 0 ? s_idx_sh : v_idx_sh;
-      const int want = (cur / CHUNK) * CHUNK;
-      if (want != s_base[kind] && cur < n_total) {
-        for (int i = threadIdx.x; i < CHUNK; i += blockDim.x) {
-          const int o = want + i;
-          if (o < n_total) {
-            const int64_t g = lb + static_cast<int64_t>(kind) * n_total + o;
-            st[kind].idx[i] = L.idx[g];
-            st[kind].len[i] = L.len[g];
-            st[kind].w[i] = L.w[g];
-            st[kind].mx[i] = L.mx[g];
-          }
-        }
-      }
+  if (gs_smem)
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) S.gs[r] = cells.pos(h, r);
+  for (int i = threadIdx.x; i < RING; i += blockDim.x) S.r_seq[i] = 0;
+  const bool tabs = n_total <= TAB_CAP && gs_smem;
+  if (tabs) {
+    for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
+      S.rowof[i] = -1;
+      S.inv[0][i] = static_cast<uint16_t>(min(L.inv[lb + i], 65535));
+      S.inv[1][i] = static_cast<uint16_t>(min(L.inv[lb + n_total + i], 65535));
     }
     __syncthreads();
-    // (A) decision chain
-    if (threadIdx.x == 0) {
-      for (int kind = 0; kind < 2; ++kind) s_base[kind] = ((kind == 0 ? s_idx_sh : v_idx_sh) / CHUNK) * CHUNK;
-      int s_idx = s_idx_sh, v_idx = v_idx_sh, k = 0;
-      double ol_s = ol_s_sh, ol_v = ol_v_sh, approx = approx_sh;
-      const int s_end = s_base[0] + CHUNK, v_end = s_base[1] + CHUNK;
-      while (k < PCH) {
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) S.rowof[S.gs[r]] = static_cast<int16_t>(r);
+  }
+  if (threadIdx.x == 0) {
+    n_prod = 0;
+    prod_done = 0;
+    fin_pos = 0;
+    stop_at = 0x7fffffff;
+    next_j = 0;
+  }
+  __syncthreads();
+  const int32_t *inv_s = L.inv + lb, *inv_v = L.inv + lb + n_total;
+
+  if (warp == 0) {
+    // ================================================= producer (chain)
+    if (lane == 0) {
+      int s_idx = 0, v_idx = 0, n = 0;
+      double ol_s = 0.0, ol_v = 0.0, approx = 0.0;
+      bool go = 0.0 < target - EPS;  // the while condition before any pick
+      // heads of both lists in registers; only the advanced one is reloaded
+      double ws = 0.0, mxs = 0.0, wv = 0.0, mxv = 0.0;
+      int ls = 0, lv = 0, is = 0, iv = 0;
+      auto load_head = [&](int kind, int i, double &w, double &mx, int &len, int &ix) {
+        if (i >= n_total) return;
+        if (i < win) {
+          w = S.w[kind][i]; mx = S.mx[kind][i]; len = S.len[kind][i]; ix = S.idx[kind][i];
+        } else {
+          const int64_t g = lb + static_cast<int64_t>(kind) * n_total + i;
+          w = L.w[g]; mx = L.mx[g]; len = L.len[g]; ix = L.idx[g];
+        }
+      };
+      load_head(0, 0, ws, mxs, ls, is);
+      load_head(1, 0, wv, mxv, lv, iv);
+      int stop_seen = 0x7fffffff, fin_seen = 0;
+      long long wait_cycles = 0;
+      while (go) {
         const bool has_s = s_idx < n_total, has_v = v_idx < n_total;
-        if (!has_s && !has_v) break;
-        if ((has_s && s_idx >= s_end) || (has_v && v_idx >= v_end)) break;  // restage first
+        if ((!has_s && !has_v) || n >= cap) break;
+        if ((n & 15) == 0) stop_seen = stop_at;  // polled every 16 picks
+        if (n >= stop_seen) break;
+        if (n - fin_seen >= RING) {
+          fin_seen = fin_pos;
+          const long long tw = clock64();
+          while (n - fin_seen >= RING) {  // ring full: finalizer behind
+            __nanosleep(64);
+            fin_seen = fin_pos;
+          }
+          wait_cycles += clock64() - tw;
+        }
         bool take_slash;
-        const int so = s_idx - s_base[0], vo = v_idx - s_base[1];
         if (!has_s) {
           take_slash = false;
         } else if (!has_v) {
           take_slash = true;
-        } else {
-          // |V| = v_idx, |S| = s_idx (prefill.py:206-207)
-          take_slash = take_slash_decision(st[0].w[so] - ol_v, max(1, st[0].len[so] - v_idx),
-                                           st[1].w[vo] - ol_s, max(1, st[1].len[vo] - s_idx));
+        } else {  // |V| = v_idx, |S| = s_idx (prefill.py:206-207)
+          take_slash = take_slash_decision(ws - ol_v, max(1, ls - v_idx), wv - ol_s, max(1, lv - s_idx));
         }
+        int32_t code, other;
+        double wl;
         if (take_slash) {
-          approx += st[0].w[so] - ol_v;
-          ol_s += st[0].mx[so];
-          c_code[k] = st[0].idx[so];
-          c_other[k] = v_idx;
-          c_w[k] = st[0].w[so];
+          wl = ws;
+          approx += ws - ol_v;
+          ol_s += mxs;
+          code = is;
+          other = v_idx;
           ++s_idx;
+          load_head(0, s_idx, ws, mxs, ls, is);
         } else {
-          approx += st[1].w[vo] - ol_s;
-          ol_v += st[1].mx[vo];
-          c_code[k] = st[1].idx[vo] | static_cast<int32_t>(0x80000000u);
-          c_other[k] = s_idx;
-          c_w[k] = st[1].w[vo];
+          wl = wv;
+          approx += wv - ol_s;
+          ol_v += mxv;
+          code = iv | static_cast<int32_t>(0x80000000u);
+          other = s_idx;
           ++v_idx;
+          load_head(1, v_idx, wv, mxv, lv, iv);
         }
-        c_approx[k] = approx;
-        ++k;
-        // the reference re-tests the loop condition after every pick; stop the
-        // chain at the approx target (exact is applied in phase C)
-        if (!(approx < target - EPS)) break;
+        const int slot = n % RING;
+        S.r_code[slot] = code;
+        S.r_other[slot] = other;
+        S.r_w[slot] = wl;
+        S.r_approx[slot] = approx;
+        __threadfence_block();
+        n_prod = ++n;
+        go = approx < target - EPS;  // the chain stops at the approx target
       }
-      s_idx_sh = s_idx;
-      v_idx_sh = v_idx;
-      ol_s_sh = ol_s;
-      ol_v_sh = ol_v;
-      approx_sh = approx;
-      n_chunk = k;
-      exhausted = (s_idx >= n_total && v_idx >= n_total) ? 1 : 0;
-    }
-    __syncthreads();
-    const int nk = n_chunk;
-    // (B) crossing sums, one warp per new pick, selection order
-    for (int j = warp; j < nk; j += G_WARPS) {
-      const int32_t code = c_code[j];
-      const bool is_vert = code < 0;
-      const int idx = code & 0x7fffffff;
-      const int n_other = c_other[j];
-      const int32_t *other = L.idx + lb + static_cast<int64_t>(is_vert ? 0 : 1) * n_total;
-      double sum = 0.0;
-      for (int j0 = 0; j0 < n_other; j0 += 32) {
-        const int jj = j0 + lane;
-        double v = 0.0;
-        if (jj < n_other) {
-          const int o = other[jj];
-          // slash d=idx x vertical c=o at g=o+idx; vertical c=idx x slash d=o at g=idx+o
-          const int g = idx + o;
-          const int c = is_vert ? idx : o;
-          const int r = cells.row(h, g);
-          if (r >= 0) v = cells.value(h, r, g, c);
-        }
-        const unsigned any = __ballot_sync(0xffffffffu, v != 0.0);
-        if (any) {
-          vals[warp][lane] = v;
-          __syncwarp();
-          if (lane == 0) {
-            const int m = min(32, n_other - j0);
-            for (int i = 0; i < m; ++i) sum += vals[warp][i];  // python sum(): left to right
-          }
-          __syncwarp();
-        }
+      __threadfence_block();
+      prod_done = 1;
+      if (dbg) {
+        dbg[60000 + blockIdx.x * 8 + 0] = n;
+        dbg[60000 + blockIdx.x * 8 + 2] = static_cast<int>(clock64() - t_start);
+        dbg[60000 + blockIdx.x * 8 + 4] = static_cast<int>(wait_cycles);
       }
-      if (lane == 0) c_cross[j] = sum;
     }
-    __syncthreads();
-    // (C) exact accumulator + dual termination, in order
-    if (threadIdx.x == 0) {
-      double exact = exact_sh;
-      int n = n_sh;
-      int stop = 0;
-      for (int j = 0; j < nk; ++j) {
-        exact += c_w[j] - c_cross[j];
-        P.code[pb + n] = c_code[j];
-        P.approx[pb + n] = c_approx[j];
-        ++n;
-        if (!(c_approx[j] < target - EPS && exact < target - EPS)) {
-          stop = 1;
-          approx_sh = c_approx[j];
+  } else if (warp == 1) {
+    // ================================================= finalizer
+    if (lane == 0) {
+      double exact = 0.0, approx = 0.0;
+      int j = 0;
+      while (true) {
+        const int slot = j % RING;
+        int ready;
+        while ((ready = vload(S.r_seq + slot)) != j + 1) {
+          if (prod_done && j >= n_prod) break;
+          __nanosleep(32);
+        }
+        if (ready != j + 1) break;  // every published pick consumed
+        exact += static_cast<const volatile double *>(S.r_w)[slot] - static_cast<const volatile double *>(S.r_cross)[slot];
+        P.code[pb + j] = static_cast<const volatile int32_t *>(S.r_code)[slot];
+        approx = static_cast<const volatile double *>(S.r_approx)[slot];
+        ++j;
+        fin_pos = j;
+        if (!(approx < target - EPS && (exact < target - EPS || (dbg && dbg[69999] == 1)))) {
+          stop_at = j;
           break;
         }
       }
-      if (!stop && nk > 0) approx_sh = c_approx[nk - 1];
-      exact_sh = exact;
-      n_sh = n;
-      if (stop || exhausted || n >= cap) done = 1;
+      stop_at = j;
+      if (dbg) {
+        dbg[60000 + blockIdx.x * 8 + 1] = j;
+        dbg[60000 + blockIdx.x * 8 + 3] = static_cast<int>(clock64() - t_start);
+      }
+      P.n[h] = j;
+      n_final[h] = j;
+      const double cov = T > 0 ? exact / T : 0.0;  // prefill.py:221
+      coverage[h] = cov < 1.0 ? cov : 1.0;
+      approx_out[h] = j > 0 ? approx : 0.0;
     }
-    __syncthreads();
+  } else {
+    // ================================================= crossing sums
+    if ((warp & 3) == 0) return;  // scheduler 0 stays free for the producer
+    while (true) {
+      int j = 0;
+      if (lane == 0) j = atomicAdd(&next_j, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      bool ok = false;
+      if (lane == 0) {
+        while (true) {
+          if (j < n_prod) { ok = true; break; }
+          if (prod_done || j >= stop_at) break;
+          __nanosleep(256);
+        }
+        if (j >= stop_at) ok = false;
+      }
+      ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0);
+      if (!ok) break;
+      const int slot = j % RING;
+      const int32_t code = static_cast<const volatile int32_t *>(S.r_code)[slot];
+      const int n_other = static_cast<const volatile int32_t *>(S.r_other)[slot];
+      const bool is_vert = code < 0;
+      const int idx = code & 0x7fffffff;
+      const int32_t *inv_o = is_vert ? inv_s : inv_v;  // other kind's sorted positions
+      double sum = 0.0;
+      if (n_other > 0 && !(dbg && dbg[69999] == 1)) {
+        // sampled rows at or after position idx: g = idx + (other line index)
+        int lo = 0, hi = n_rows;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((gs_smem ? S.gs[mid] : cells.pos(h, mid)) < idx) lo = mid + 1; else hi = mid;
+        }
+        const int okind = is_vert ? 0 : 1;
+        if (tabs && n_other < n_rows - lo) {
+          // walk the other kind's picked prefix: cell at g = idx + o if g is sampled
+          for (int i0 = 0; i0 < n_other; i0 += 32 * 4) {
+            int gg[4], rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * 32 + lane;
+              int o = -1;
+              if (i < n_other) o = i < win ? S.idx[okind][i] : __ldg(L.idx + lb + static_cast<int64_t>(okind) * n_total + i);
+              gg[u] = idx + o;
+              rr[u] = (o >= 0 && gg[u] < n_total) ? S.rowof[gg[u]] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (rr[u] >= 0) sum += cells.value(h, rr[u], gg[u], is_vert ? idx : gg[u] - idx);
+          }
+        } else {
+          // walk the sampled rows: the other line o = g - idx is picked iff its
+          // sorted position is below the prefix length
+          const int32_t *inv_o = is_vert ? inv_s : inv_v;
+          for (int r0 = lo; r0 < n_rows; r0 += 32 * 4) {
+            int gg[4];
+            bool hit[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int r = r0 + u * 32 + lane;
+              hit[u] = false;
+              if (r < n_rows) {
+                gg[u] = gs_smem ? S.gs[r] : cells.pos(h, r);
+                const int o = gg[u] - idx;
+                const int pos = tabs ? static_cast<int>(S.inv[okind][o]) : __ldg(inv_o + o);
+                hit[u] = pos < n_other;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (hit[u]) sum += cells.value(h, r0 + u * 32 + lane, gg[u], is_vert ? idx : gg[u] - idx);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        static_cast<volatile double *>(S.r_cross)[slot] = sum;
+        __threadfence_block();
+        static_cast<volatile int32_t *>(S.r_seq)[slot] = j + 1;
+      }
+    }
   }
-  if (threadIdx.x == 0) {
-    P.n[h] = n_sh;
-    n_final[h] = n_sh;
-    const double cov = T > 0 ? exact_sh / T : 0.0;  // prefill.py:221
-    coverage[h] = cov < 1.0 ? cov : 1.0;
-    approx_out[h] = n_sh > 0 ? approx_sh : 0.0;
-  }
+}
+
+template <typename Cells>
+int launch_greedy(const Lists &lists, int H, int n_total, double alpha, const double *total, Picks &picks, int cap,
+                  const Cells &cells, int32_t *n_final, double *coverage, double *approx, cudaStream_t st) {
+  const int smem = static_cast<int>(sizeof(GreedySmem));
+  LS_CUDA(cudaFuncSetAttribute(greedy_kernel<Cells>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  greedy_kernel<Cells><<<H, G_THREADS, smem, st>>>(lists, n_total, alpha, total, picks, cap, cells, n_final, coverage,
+                                                   approx, g_debug_buffer);
+  LS_LAUNCH_CHECK("greedy_kernel");
+  return LS_OK;
 }
 
 // ------------------------------------------------------------------ K4 plan
@@ -398,34 +528,21 @@ __global__ void __launch_bounds__(1024) compact_bits_kernel(const uint32_t *sbit
   if (threadIdx.x == 0) counts[h * 2 + kind] = carry;
 }
 
-__global__ void row_of_kernel(const int32_t *rows, int n_s, int n_total, int row_offset, int32_t *row_of) {
-  const int h = blockIdx.y;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_total; i += gridDim.x * blockDim.x)
-    row_of[static_cast<int64_t>(h) * n_total + i] = -1;
-  // (second launch sets the sampled positions)
-}
-
-__global__ void row_of_set_kernel(const int32_t *rows, int n_s, int n_total, int row_offset, int32_t *row_of) {
-  const int h = blockIdx.y;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_s; r += gridDim.x * blockDim.x)
-    row_of[static_cast<int64_t>(h) * n_total + row_offset + rows[static_cast<int64_t>(h) * n_s + r]] = r;
-}
-
 struct Work {
   Lists lists;
   Picks picks;
-  int32_t *row_of;
   uint32_t *sbits, *vbits;
   int32_t *n_final;
   int words, cap;
 };
 
-inline Work carve(Carver &c, int H, int n_total, bool with_row_of) {
+inline Work carve(Carver &c, int H, int n_total) {
   Work w;
   const size_t nl = static_cast<size_t>(H) * 2 * n_total;
   w.cap = 2 * n_total;
   const size_t np = static_cast<size_t>(H) * w.cap;
   w.lists.idx = c.take<int32_t>(nl);
+  w.lists.inv = c.take<int32_t>(nl);
   w.lists.len = c.take<int32_t>(nl);
   w.lists.w = c.take<double>(nl);
   w.lists.mx = c.take<double>(nl);
@@ -439,7 +556,6 @@ inline Work carve(Carver &c, int H, int n_total, bool with_row_of) {
   w.words = (n_total + 31) / 32;
   w.sbits = c.take<uint32_t>(static_cast<size_t>(H) * w.words);
   w.vbits = c.take<uint32_t>(static_cast<size_t>(H) * w.words);
-  w.row_of = with_row_of ? c.take<int32_t>(static_cast<size_t>(H) * n_total) : nullptr;
   return w;
 }
 
@@ -467,7 +583,7 @@ using namespace ls;
 
 extern "C" size_t ls_select_lines_workspace(const ls_layer_desc *L, int32_t /*n_s*/) {
   Carver c(nullptr, 0);
-  sel::carve(c, L->n_heads, L->n_total, true);
+  sel::carve(c, L->n_heads, L->n_total);
   return c.off + 4096;
 }
 
@@ -484,20 +600,17 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int H = L->n_heads, n_total = L->n_total;
   Carver c(ws, ws_bytes);
-  sel::Work w = sel::carve(c, H, n_total, true);
+  sel::Work w = sel::carve(c, H, n_total);
   const size_t smem = sel::sort_smem();
   LS_CUDA(cudaFuncSetAttribute(sel::sort_lines_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   sel::sort_lines_kernel<float><<<dim3(2, H), sel::SORT_THREADS, smem, st>>>(v_w, v_max, s_w, s_max, rows, n_s,
                                                                             n_total, L->row_offset, w.lists);
   LS_LAUNCH_CHECK("sort_lines_kernel");
-  sel::row_of_kernel<<<dim3(ceil_div(n_total, 256), H), 256, 0, st>>>(rows, n_s, n_total, L->row_offset, w.row_of);
-  sel::row_of_set_kernel<<<dim3(ceil_div(n_s, 256), H), 256, 0, st>>>(rows, n_s, n_total, L->row_offset, w.row_of);
-  LS_LAUNCH_CHECK("row_of_kernel");
   sel::RecomputeCells cells;
   cells.q = q;
   cells.k = k;
-  cells.row_of = w.row_of;
+  cells.rows = rows;
   cells.row_stats = row_stats;
   cells.n_s = n_s;
   cells.n_total = n_total;
@@ -507,9 +620,9 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   cells.q_head_stride = L->q_head_stride;
   cells.kv_head_stride = L->kv_head_stride;
   cells.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
-  sel::greedy_kernel<sel::RecomputeCells><<<H, sel::G_THREADS, 0, st>>>(w.lists, n_total, alpha, total, w.picks,
-                                                                        w.cap, cells, w.n_final, coverage, approx);
-  LS_LAUNCH_CHECK("greedy_kernel");
+  int s = sel::launch_greedy(w.lists, H, n_total, alpha, total, w.picks, w.cap, cells, w.n_final, coverage, approx,
+                             st);
+  if (s) return s;
   return sel::run_tail(w, H, n_total, alpha, total, slash_ids, vert_ids, counts, coverage, approx, picks, n_picks,
                        st);
 }
@@ -523,6 +636,7 @@ __global__ void load_lists_kernel(int n, const int32_t *idx, const double *w, co
     const int64_t o = static_cast<int64_t>(kind) * n_total + i;
     if (i < n) {
       L.idx[o] = idx[i];
+      L.inv[static_cast<int64_t>(kind) * n_total + idx[i]] = i;
       L.w[o] = w[i];
       L.len[o] = len[i];
       L.mx[o] = mx[i];
@@ -543,19 +657,16 @@ extern "C" int ls_greedy_dense(int32_t n_slash, const int32_t *s_idx, const doub
              "ls_greedy_dense expects exactly n_total lines of each kind");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Carver c(ws, ws_bytes);
-  sel::Work w = sel::carve(c, 1, n_total, true);
+  sel::Work w = sel::carve(c, 1, n_total);
   double *tot = c.take<double>(1);
   LS_REQUIRE(c.ok(), LS_ERR_WORKSPACE, "greedy_dense workspace too small (%zu > %zu)", c.off, ws_bytes);
   LS_CUDA(cudaMemcpyAsync(tot, &total_weight, sizeof(double), cudaMemcpyHostToDevice, st));
   sel::load_lists_kernel<<<8, 256, 0, st>>>(n_slash, s_idx, s_w, s_len, s_max, 0, n_total, w.lists);
   sel::load_lists_kernel<<<8, 256, 0, st>>>(n_vert, v_idx, v_w, v_len, v_max, 1, n_total, w.lists);
   LS_LAUNCH_CHECK("load_lists_kernel");
-  sel::row_of_kernel<<<dim3(ceil_div(n_total, 256), 1), 256, 0, st>>>(positions, n_rows, n_total, 0, w.row_of);
-  sel::row_of_set_kernel<<<dim3(ceil_div(n_rows, 256), 1), 256, 0, st>>>(positions, n_rows, n_total, 0, w.row_of);
-  sel::DenseCells cells{weights, w.row_of, n_total};
-  sel::greedy_kernel<sel::DenseCells><<<1, sel::G_THREADS, 0, st>>>(w.lists, n_total, alpha, tot, w.picks, w.cap,
-                                                                    cells, w.n_final, coverage, approx);
-  LS_LAUNCH_CHECK("greedy_kernel");
+  sel::DenseCells cells{weights, positions, n_rows, n_total};
+  int s = sel::launch_greedy(w.lists, 1, n_total, alpha, tot, w.picks, w.cap, cells, w.n_final, coverage, approx, st);
+  if (s) return s;
   return sel::run_tail(w, 1, n_total, alpha, tot, slash_ids, vert_ids, counts, coverage, approx, nullptr, nullptr,
                        st);
 }

@@ -275,70 +275,100 @@ __global__ void set_bits_kernel(const int32_t *ids, const int32_t *counts, int w
   }
 }
 
-// Seed rows: full probability rows of block rows [n_new - n_rows, n_new).
-__global__ void __launch_bounds__(256) plan_rows_kernel(Params p, int n_rows, float *out, int64_t out_stride,
-                                                        int64_t out_head_stride) {
-  __shared__ float qsh[128];
-  __shared__ float red[32];
-  const int h = blockIdx.y, i = blockIdx.x;
+// Seed rows: full probability rows of block rows [n_new - n_rows, n_new)
+// (the decode observation seeds, session.py:89-95), in two parallel passes:
+//  plan_scores_kernel  grid (column chunks of 256, row, head), one warp per 32
+//                      columns: the selected cells (vertical bit or slash bit of
+//                      g - c, tensor_ops.py:130-138) get q.k * log2(e)/sqrt(d)
+//                      by a coalesced warp dot product, the others -inf; each
+//                      CTA writes its chunk's (max, sum of exp2) partial.
+//  plan_norm_kernel    grid (row, head): combines the partials in chunk order
+//                      and normalises the row in place (zeros off-plan); an
+//                      empty row becomes the diagonal fallback (tensor_ops.py:136-137).
+constexpr int PR_CHUNK = 256;
+
+__global__ void __launch_bounds__(PR_CHUNK) plan_scores_kernel(Params p, int n_rows, float *out, int64_t out_stride,
+                                                               int64_t out_head_stride, float2 *part, int n_chunks) {
+  __shared__ float wmax[PR_CHUNK / 32], wsum[PR_CHUNK / 32];
+  const int ch = blockIdx.x, i = blockIdx.y, h = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = p.n_new - n_rows + i;
   const int g = p.row_offset + r;
   const int d = p.d;
-  const uint16_t *qr = p.q + static_cast<int64_t>(h) * p.q_head_stride + static_cast<int64_t>(r) * d;
-  const uint16_t *kb = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
+  const int c = ch * PR_CHUNK + threadIdx.x;  // this thread's column
   const uint32_t *sb = p.sbits + static_cast<int64_t>(h) * p.words;
   const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * p.words;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) qsh[t] = bf2f(qr[t]);
-  __syncthreads();
-  float *orow = out + static_cast<int64_t>(h) * out_head_stride + static_cast<int64_t>(i) * out_stride;
-  auto score = [&](int c) -> float {
-    const uint16_t *kr = kb + static_cast<int64_t>(c) * d;
-    float acc = 0.f;
-    for (int v = 0; v < d / 8; ++v) {
-      uint4 u = *reinterpret_cast<const uint4 *>(kr + v * 8);
-      float f[8];
-      bf16x8_to_f32(u, f);
+  const bool sel = c <= g && c < p.n_total && (bit(vbits, c) || bit(sb, g - c));
+  // q: lane owns dims [4 lane, 4 lane + 4) (d = 128) or [2 lane, +2) (d = 64)
+  const uint16_t *qr = p.q + static_cast<int64_t>(h) * p.q_head_stride + static_cast<int64_t>(r) * d;
+  const uint16_t *kb = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
+  const int dpl = d / 32;
+  float qv[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc = fmaf(qsh[v * 8 + j], f[j], acc);
+  for (int e = 0; e < 4; ++e) qv[e] = e < dpl ? bf2f(qr[lane * dpl + e]) : 0.f;
+  float my = -INFINITY;
+  unsigned m = __ballot_sync(0xffffffffu, sel);
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const int cc = ch * PR_CHUNK + warp * 32 + src;
+    const uint16_t *kr = kb + static_cast<int64_t>(cc) * d + lane * dpl;
+    float acc;
+    if (dpl == 4) {
+      const uint2 u = *reinterpret_cast<const uint2 *>(kr);
+      acc = qv[0] * __uint_as_float(u.x << 16) + qv[1] * __uint_as_float(u.x & 0xffff0000u) +
+            qv[2] * __uint_as_float(u.y << 16) + qv[3] * __uint_as_float(u.y & 0xffff0000u);
+    } else {
+      const uint32_t u = *reinterpret_cast<const uint32_t *>(kr);
+      acc = qv[0] * __uint_as_float(u << 16) + qv[1] * __uint_as_float(u & 0xffff0000u);
     }
-    return acc * p.scale_log2;
-  };
-  float mx = -INFINITY;
-  for (int c = threadIdx.x; c <= g; c += blockDim.x)
-    if (bit(vbits, c) || bit(sb, g - c)) mx = fmaxf(mx, score(c));
-  mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
-    v = warp_max(v);
-    if (threadIdx.x == 0) red[0] = v;
+    acc = warp_sum(acc) * p.scale_log2;
+    if (lane == src) my = acc;
+  }
+  float *orow = out + static_cast<int64_t>(h) * out_head_stride + static_cast<int64_t>(i) * out_stride;
+  if (c < p.n_total) orow[c] = my;
+  // chunk partial (max, sum exp2(s - max))
+  const float wm = warp_max(my);
+  const float we = warp_sum(my == -INFINITY ? 0.f : fast_exp2(my - wm));
+  if (lane == 0) {
+    wmax[warp] = wm;
+    wsum[warp] = we;
   }
   __syncthreads();
-  mx = red[0];
-  __syncthreads();
-  if (mx == -INFINITY) {  // diagonal fallback
-    for (int c = threadIdx.x; c < p.n_total; c += blockDim.x) orow[c] = (c == g) ? 1.f : 0.f;
-    return;
+  if (threadIdx.x == 0) {
+    float M = -INFINITY, S = 0.f;
+    for (int w = 0; w < PR_CHUNK / 32; ++w) M = fmaxf(M, wmax[w]);
+    for (int w = 0; w < PR_CHUNK / 32; ++w)
+      if (wmax[w] != -INFINITY) S += wsum[w] * fast_exp2(wmax[w] - M);
+    part[(static_cast<int64_t>(h) * n_rows + i) * n_chunks + ch] = make_float2(M, S);
   }
-  float sum = 0.f;
-  for (int c = threadIdx.x; c <= g; c += blockDim.x) {
-    float e = 0.f;
-    if (bit(vbits, c) || bit(sb, g - c)) e = fast_exp2(score(c) - mx);
-    orow[c] = e;
-    sum += e;
+}
+
+__global__ void __launch_bounds__(256) plan_norm_kernel(Params p, int n_rows, float *out, int64_t out_stride,
+                                                        int64_t out_head_stride, const float2 *part, int n_chunks) {
+  __shared__ float stats[2];
+  const int i = blockIdx.x, h = blockIdx.y;
+  const int g = p.row_offset + p.n_new - n_rows + i;
+  const float2 *pp = part + (static_cast<int64_t>(h) * n_rows + i) * n_chunks;
+  if (threadIdx.x == 0) {
+    float M = -INFINITY, S = 0.f;
+    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, pp[c].x);
+    for (int c = 0; c < n_chunks; ++c)
+      if (pp[c].x != -INFINITY) S += pp[c].y * fast_exp2(pp[c].x - M);
+    stats[0] = M;
+    stats[1] = S > 0.f ? 1.f / S : 0.f;
   }
-  sum = warp_sum(sum);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
+  const float M = stats[0], inv = stats[1];
+  float *orow = out + static_cast<int64_t>(h) * out_head_stride + static_cast<int64_t>(i) * out_stride;
+  for (int c = threadIdx.x; c < p.n_total; c += blockDim.x) {
+    if (M == -INFINITY) {
+      orow[c] = (c == g) ? 1.f : 0.f;
+    } else {
+      const float s = orow[c];
+      orow[c] = s == -INFINITY ? 0.f : fast_exp2(s - M) * inv;
+    }
   }
-  __syncthreads();
-  const float inv = 1.f / red[0];
-  for (int c = threadIdx.x; c < p.n_total; c += blockDim.x) orow[c] = (c <= g) ? orow[c] * inv : 0.f;
 }
 
 inline size_t smem_bytes(int d) {
@@ -471,7 +501,11 @@ extern "C" int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16
   const int words = (L->n_total + 31) / 32;
   uint32_t *bits = nullptr;
   keep_pool_memory();
-  LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&bits), sizeof(uint32_t) * 2 * L->n_heads * words, st));
+  const int n_chunks = ceil_div(L->n_total, k5::PR_CHUNK);
+  const size_t bits_bytes = (sizeof(uint32_t) * 2 * L->n_heads * words + 255) / 256 * 256;
+  LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&bits),
+                          bits_bytes + sizeof(float2) * static_cast<size_t>(L->n_heads) * n_rows * n_chunks, st));
+  float2 *part = reinterpret_cast<float2 *>(reinterpret_cast<char *>(bits) + bits_bytes);
   uint32_t *sbits = bits, *vbits = bits + static_cast<size_t>(L->n_heads) * words;
   int s = build_bits(L, slash_ids, vert_ids, counts, sbits, vbits, st);
   if (s) return s;
@@ -481,8 +515,12 @@ extern "C" int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16
   p.k = k;
   p.sbits = sbits;
   p.vbits = vbits;
-  k5::plan_rows_kernel<<<dim3(n_rows, L->n_heads), 256, 0, st>>>(p, n_rows, out, out_row_stride, out_head_stride);
-  LS_LAUNCH_CHECK("plan_rows_kernel");
+  k5::plan_scores_kernel<<<dim3(n_chunks, n_rows, L->n_heads), k5::PR_CHUNK, 0, st>>>(p, n_rows, out, out_row_stride,
+                                                                                     out_head_stride, part, n_chunks);
+  LS_LAUNCH_CHECK("plan_scores_kernel");
+  k5::plan_norm_kernel<<<dim3(n_rows, L->n_heads), 256, 0, st>>>(p, n_rows, out, out_row_stride, out_head_stride, part,
+                                                                 n_chunks);
+  LS_LAUNCH_CHECK("plan_norm_kernel");
   LS_CUDA(cudaFreeAsync(bits, st));
   return LS_OK;
 }

@@ -603,7 +603,7 @@ __global__ void reverse_bits_kernel(const int32_t *slash_ids, const int32_t *cou
 }  // namespace k5ws
 
 // ------------------------------------------------------------------ host
-static int *g_debug_buffer = nullptr;
+int *g_debug_buffer = nullptr;  // ls_debug_set_buffer (host-mapped), read by the pipelined kernels
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
