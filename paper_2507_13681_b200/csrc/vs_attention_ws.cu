@@ -22,12 +22,12 @@
 //   gathered : 128 consecutive entries of the head's compacted selected
 //              verticals (K/V rows gathered once per call by a pre-kernel);
 //              mask causal & column not in a dense block          (tensor cores)
-//   diagonal : one selected slash d whose cells fall outside dense blocks: the
-//              contiguous key range [g0-d, g0-d+128) is TMA-loaded and each
-//              row's single cell (key g-d) is computed on CUDA cores (the cell
-//              is skipped when its column is a selected vertical, already
-//              counted by the gathered tiles).
-// No cell is counted twice; every cell of every row is covered.
+//   window   : the key ranges [g0-d, g_hi-d] of selected slashes whose cells
+//              fall outside dense blocks, merged and covered by disjoint
+//              128-key windows at unaligned starts (tensor cores); mask
+//              causal & sbit & !vbit & column not in a dense block.
+// No cell is counted twice (windows are disjoint and skip dense-block and
+// vertical columns); every cell of every row is covered.
 
 #include <cuda.h>
 
@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   float *lx = reinterpret_cast<float *>(misc + 2816);                  // [128]
   int *gcols = reinterpret_cast<int *>(misc + 3328);                   // [2][128]
   int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 4352);      // [MAX_KB]
-  int *blk_cnt = reinterpret_cast<int *>(misc + 4352 + MAX_KB * 2);   // [MAX_KB]
+  int *blk_cnt = reinterpret_cast<int *>(misc + 4352 + MAX_KB * 2);   // [MAX_KB] slash counts, then window starts
+  int *wins = blk_cnt;
   uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(misc + 256 + 252);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int g0 = p.row_offset + r0;
   const int g_hi = g0 + nr - 1;
   const int kv = h / p.group;
-  const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * p.words;
+  const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * (p.words + 8);
   const uint32_t *rsbits = p.rsbits + static_cast<int64_t>(h) * (p.words + 8);
   int32_t *sl = p.diag_ws + (static_cast<int64_t>(h) * p.n_qtiles + qt) * p.n_total;
 
@@ -215,17 +216,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       n_diag += tot;
     }
   }
+  __syncthreads();  // (blk_cnt is free from here: it becomes the window list)
+  if (tid == 0) {
+    // isolated slashes in descending d = ascending key start; merge their key
+    // ranges and cover them with disjoint 128-key windows
+    int n_win = 0, covered = -1;
+    for (int i = n_diag - 1; i >= 0; --i) {
+      const int dd = sl[i];
+      const int lo = max(0, g0 - dd), hi = g_hi - dd;
+      if (hi <= covered) continue;
+      for (int w = max(lo, covered + 1); w <= hi && n_win < MAX_KB; w += BN) {
+        wins[n_win++] = w;
+        covered = w + BN - 1;
+      }
+    }
+    sh_int[2] = n_win;
+  }
   __syncthreads();
   const int n_dense = sh_int[0];
   const int v_end = sh_int[1];
   const int n_gt = (v_end + BN - 1) / BN;
   const int n_tc = n_dense + n_gt;
-  const int n_all = n_tc + n_diag;
+  const int n_win = sh_int[2];
+  const int n_all = n_tc + n_win;
   if (tid == 0 && p.dbg) {
     volatile int *d_ = p.dbg + (blockIdx.y * gridDim.x + blockIdx.x) * 16 + 12;
     d_[0] = n_dense;
     d_[1] = n_gt;
-    d_[2] = n_diag;
+    d_[2] = n_win;
     d_[3] = 1;
   }
   tc::fence_before_sync();
@@ -257,8 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mk = &tm_k, mv = &tm_v, row = dense_list[t] * BN, hh = kv;
         } else if (t < n_tc) {
           mk = &tm_kc, mv = &tm_vc, row = (t - n_dense) * BN, hh = h;
-        } else {  // diagonal range start, clamped at 0 (no negative TMA coordinates)
-          mk = &tm_k, mv = &tm_v, row = max(0, g0 - sl[t - n_tc]), hh = kv;
+        } else {  // window start (>= 0)
+          mk = &tm_k, mv = &tm_v, row = wins[t - n_tc], hh = kv;
         }
         const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
         const uint32_t vs = tc::smem_u32(smem + L::OFF_V + s * L::KV_BYTES);
@@ -292,7 +310,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mma_commit(&bars->pv_done);
         tc::mma_commit(&bars->empty[j & 1]);
       };
-      for (int i = 0; i < n_tc; ++i) {
+      for (int i = 0; i < n_all; ++i) {
         const int s = i & 1;
         KDBG(1, i, 4);
         tc::mbar_wait(&bars->full[s], (i >> 1) & 1);
@@ -309,7 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mma_commit(&bars->s_full[s]);
         if (i > 0) issue_pv(i - 1);
       }
-      if (n_tc > 0) issue_pv(n_tc - 1);
+      if (n_all > 0) issue_pv(n_all - 1);
     }
   } else {
     // =================================================== softmax warps
@@ -320,27 +338,62 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     float m_ref = -INFINITY, l = 0.f;
     long long my_cells = 0;
-    for (int i = 0; i < n_tc; ++i) {
+    for (int i = 0; i < n_all; ++i) {
       const int s = i & 1;
-      const bool gathered = i >= n_dense;
+      const bool gathered = i >= n_dense && i < n_tc;
       uint32_t mk[2];
-      if (gathered) {  // stage this tile's 128 vertical columns
+      if (i >= n_tc) {  // window: slash cells outside dense blocks and verticals
+        const int c0 = wins[i - n_tc] + wg * 64;
+        if (!row_ok) {
+          mk[0] = mk[1] = 0u;
+        } else {
+          uint32_t sw[2], vw[2];
+          bit_window(rsbits, p.n_total - 1 - my_g + c0, sw, 2);
+          bit_window(vbits, c0, vw, 2);
+          // columns of this thread's 64 that fall in dense blocks
+          const int b1 = c0 / BN, split = (b1 + 1) * BN - c0;  // columns [0, split) in block b1
+          const uint64_t lo_mask = split >= 64 ? ~0ull : ((1ull << split) - 1ull);
+          uint64_t dm = 0ull;
+          if (bit_of(kb_bits, b1)) dm |= lo_mask;
+          if (split < 64 && b1 + 1 < MAX_KB && bit_of(kb_bits, b1 + 1)) dm |= ~lo_mask;
+          const int lim = my_g - c0;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int hi = lim - 32 * t;
+            const uint32_t causal = hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u));
+            mk[t] = sw[t] & ~vw[t] & ~static_cast<uint32_t>(dm >> (32 * t)) & causal;
+          }
+        }
+      } else if (gathered) {
+        // stage this tile's 128 vertical columns (sorted ascending) and the
+        // tile-wide mask of columns outside dense blocks; a row's causal part
+        // is then a prefix: columns <= g
+        uint32_t *cm = reinterpret_cast<uint32_t *>(pd) + s * 4;
         if (wg == 0) {
           const int idx = (i - n_dense) * BN + row;
-          gcols[s * BN + row] = idx < v_end ? Vl[idx] : 0x7fffffff;
+          const int c = idx < v_end ? Vl[idx] : 0x7fffffff;
+          gcols[s * BN + row] = c;
+          const unsigned b = __ballot_sync(0xffffffffu, c != 0x7fffffff && !bit_of(kb_bits, c / BN));
+          if (lane == 0) cm[warp & 3] = b;
         }
         tc::named_sync(1, N_SOFT);
-        const int *gc = gcols + s * BN + wg * 64;
+        const int *gc = gcols + s * BN;
+        int n_le;  // gathered columns <= my_g
+        if (gc[BN - 1] <= g0) {
+          n_le = BN;
+        } else {
+          int lo = 0, hi = BN;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (gc[mid] <= my_g) lo = mid + 1; else hi = mid;
+          }
+          n_le = lo;
+        }
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          uint32_t w = 0;
-#pragma unroll 8
-          for (int j = 0; j < 32; ++j) {
-            const int c = gc[t * 32 + j];
-            const bool ok = row_ok && c <= my_g && !bit_of(kb_bits, c / BN);
-            w |= ok ? (1u << j) : 0u;
-          }
-          mk[t] = w;
+          const int hi = n_le - (wg * 64 + t * 32);  // columns of this word below n_le
+          const uint32_t causal = hi >= 32 ? 0xffffffffu : (hi <= 0 ? 0u : ((1u << hi) - 1u));
+          mk[t] = row_ok ? (cm[wg * 2 + t] & causal) : 0u;
         }
       } else {
         const int c0 = dense_list[i] * BN + wg * 64;
@@ -365,13 +418,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::fence_after_sync();
       const uint32_t s_addr = tmem + s * 128 + lane_base + wg * 64;
       float tmax = -INFINITY;
+      float sv[2][32];
+      bool live[2];
 #pragma unroll
       for (int cch = 0; cch < 2; ++cch) {
-        float sv[32];
-        tc::tmem_ld32(s_addr + cch * 32, sv);
-        tc::tmem_wait_ld();
+        live[cch] = __any_sync(0xffffffffu, mk[cch] != 0u);  // warp-uniform: TMEM loads are .sync.aligned
+        if (live[cch]) {
+          tc::tmem_ld32(s_addr + cch * 32, sv[cch]);
+          tc::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, ((mk[cch] >> j) & 1u) ? sv[j] : -INFINITY);
+          for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, ((mk[cch] >> j) & 1u) ? sv[cch][j] : -INFINITY);
+        }
       }
       pmax[wg * BM + row] = tmax;
       tc::named_sync(1, N_SOFT);
@@ -405,16 +462,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       float lsum = 0.f;
 #pragma unroll
       for (int cch = 0; cch < 2; ++cch) {
-        float sv[32];
-        tc::tmem_ld32(s_addr + cch * 32, sv);
-        tc::tmem_wait_ld();
         uint32_t pk[16];
+        if (live[cch]) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(fmaf(sv[j], p.scale_log2, -m_ref)) : 0.f;
-          const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[j + 1], p.scale_log2, -m_ref)) : 0.f;
-          lsum += a + b;
-          pk[j >> 1] = tc::pack_bf16(a, b);
+          for (int j = 0; j < 32; j += 2) {
+            const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(fmaf(sv[cch][j], p.scale_log2, -m_ref)) : 0.f;
+            const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[cch][j + 1], p.scale_log2, -m_ref)) : 0.f;
+            lsum += a + b;
+            pk[j >> 1] = tc::pack_bf16(a, b);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = 0u;
         }
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -434,9 +493,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     // O (TMEM) -> registers, relative to m_ref
     float o[DH];
-    if (n_tc > 0) {
-      if (tid == 0) KDBG(2, n_tc, 8);
-      tc::mbar_wait(&bars->pv_done, (n_tc - 1) & 1);
+    if (n_all > 0) {
+      if (tid == 0) KDBG(2, n_all, 8);
+      tc::mbar_wait(&bars->pv_done, (n_all - 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
       for (int cch = 0; cch < DH / 32; ++cch) {
@@ -449,65 +508,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
 #pragma unroll
       for (int j = 0; j < DH; ++j) o[j] = 0.f;
-    }
-    // ---- diagonal slash tiles on CUDA cores
-    if (n_diag > 0) {
-      float qf[DH];
-      tc::mbar_wait(&bars->q_full, 0);
-#pragma unroll
-      for (int c8 = 0; c8 < DH / 8; ++c8)
-        bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_Q + tc::sw128_offset(row, wg * (DH / 8) + c8, BM)),
-                      qf + c8 * 8);
-      for (int t = n_tc; t < n_all; ++t) {
-        const int s = t & 1;
-        const int dd = sl[t - n_tc];
-        const int c = my_g - dd;
-        const int kr = c - max(0, g0 - dd);  // row of key c in the staged range
-        bool v = row_ok && c >= 0;
-        if (v) v = !bit_of(kb_bits, c / BN) && !bit_of(vbits, c);
-        if (tid == 0) KDBG(2, t, 10);
-        tc::mbar_wait(&bars->full[s], (t >> 1) & 1);
-        float acc = 0.f;
-        if (v) {
-#pragma unroll
-          for (int c8 = 0; c8 < DH / 8; ++c8) {
-            float f[8];
-            bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_K + s * L::KV_BYTES +
-                                                           tc::sw128_offset(kr, wg * (DH / 8) + c8, BN)),
-                          f);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc = fmaf(qf[c8 * 8 + e], f[e], acc);
-          }
-        }
-        pd[wg * BM + row] = acc;
-        tc::named_sync(1, N_SOFT);
-        if (v) {
-          const float sc = (pd[row] + pd[BM + row]) * p.scale_log2;
-          if (sc > m_ref + RESCALE_LOG2) {
-            const float corr = fast_exp2(m_ref - sc);  // 0 when m_ref == -inf
-#pragma unroll
-            for (int j = 0; j < DH; ++j) o[j] *= corr;
-            l *= corr;
-            m_ref = sc;
-          }
-          const float pj = fast_exp2(sc - m_ref);
-          if (wg == 0) {
-            l += pj;
-            my_cells += 1;
-          }
-#pragma unroll
-          for (int c8 = 0; c8 < DH / 8; ++c8) {
-            float f[8];
-            bf16x8_to_f32(*reinterpret_cast<const uint4 *>(smem + L::OFF_V + s * L::KV_BYTES +
-                                                           tc::sw128_offset(kr, wg * (DH / 8) + c8, BN)),
-                          f);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[c8 * 8 + e] = fmaf(pj, f[e], o[c8 * 8 + e]);
-          }
-        }
-        tc::named_sync(1, N_SOFT);  // stage and pd consumed
-        if (tid == 0) tc::mbar_arrive(&bars->empty[s]);
-      }
     }
     // ---- epilogue: both halves agree on m_ref; l = l(wg0) + l(wg1)
     if (wg == 1) lx[row] = l;
@@ -585,7 +585,7 @@ __global__ void vert_bits_kernel(const int32_t *vert_ids, const int32_t *counts,
   const int n = counts[h * 2 + 1];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int c = vert_ids[static_cast<int64_t>(h) * n_total + i];
-    atomicOr(vbits + static_cast<int64_t>(h) * words + (c >> 5), 1u << (c & 31));
+    atomicOr(vbits + static_cast<int64_t>(h) * (words + 8) + (c >> 5), 1u << (c & 31));
   }
 }
 
@@ -641,7 +641,7 @@ size_t vs_attention_ws_workspace(const ls_layer_desc *L) {
   const size_t words = (L->n_total + 31) / 32;
   const size_t nqt = (L->n_new + k5ws::BM - 1) / k5ws::BM;
   const size_t H = L->n_heads;
-  return H * (words * 4 + (words + 8) * 4) + nqt * H * L->n_total * 4 +
+  return H * ((words + 8) * 4 + (words + 8) * 4) + nqt * H * L->n_total * 4 +
          2 * H * (static_cast<size_t>(L->n_total) + 128) * L->head_dim * 2 + 8 * 256;
 }
 
@@ -655,14 +655,14 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   const int words = (L->n_total + 31) / 32;
   const int nqt = (L->n_new + k5ws::BM - 1) / k5ws::BM;
   Carver c(ws, ws_bytes);
-  uint32_t *vbits = c.take<uint32_t>(static_cast<size_t>(H) * words);
+  uint32_t *vbits = c.take<uint32_t>(static_cast<size_t>(H) * (words + 8));
   uint32_t *rsbits = c.take<uint32_t>(static_cast<size_t>(H) * (words + 8));
   int32_t *diag = c.take<int32_t>(static_cast<size_t>(nqt) * H * L->n_total);
   const size_t vcap = static_cast<size_t>(L->n_total) + 128;
   uint16_t *kc = c.take<uint16_t>(static_cast<size_t>(H) * vcap * d);
   uint16_t *vc = c.take<uint16_t>(static_cast<size_t>(H) * vcap * d);
   if (!dense) {
-    LS_CUDA(cudaMemsetAsync(vbits, 0, sizeof(uint32_t) * H * words, st));
+    LS_CUDA(cudaMemsetAsync(vbits, 0, sizeof(uint32_t) * H * (words + 8), st));
     LS_CUDA(cudaMemsetAsync(rsbits, 0, sizeof(uint32_t) * H * (words + 8), st));
     k5ws::vert_bits_kernel<<<dim3(4, H), 256, 0, st>>>(vert_ids, counts, L->n_total, words, vbits);
     k5ws::reverse_bits_kernel<<<dim3(4, H), 256, 0, st>>>(slash_ids, counts, L->n_total, words, rsbits);
