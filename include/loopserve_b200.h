@@ -197,7 +197,10 @@ int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t
  *   ring_n, ring_dense [hr][window] int32
  *   sel_ids  [hr][budget_cap], n_sel [hr]      picked ids (kvcompress.py:212)
  *   ck, cv   [hr][budget_cap][head_dim] bf16   compacted K/V of sel_ids
- *   partials [n_heads][splits][head_dim+2] fp32, counters [n_heads] int32 (zeroed)
+ *   partials, counters: unused since the split-K combine moved to distributed
+ *                                   shared memory (kept for layout stability; may be NULL)
+ *   n_a      [hr] int32  picked ids below the recent window at the current step
+ *                        (written by ls_decode_event, advanced by ls_decode_advance)
  * Archive K/V of layer l, kv-head j at k_all + l*kv_layer_stride + j*kv_head_stride. */
 typedef struct ls_decode_stack {
   int32_t n_layers, n_heads, n_kv_heads, head_dim;
@@ -218,6 +221,7 @@ typedef struct ls_decode_stack {
   float *partials;
   int32_t *counters;
   int32_t *step;
+  int32_t *n_a;
 } ls_decode_stack;
 
 /* Working-set decode attention of one layer for the current step
@@ -228,7 +232,8 @@ size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len);
 int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
                    const uint16_t *v_layer, int32_t compressed, int32_t max_cols, void *out,
                    int32_t out_bf16, ls_stream_t stream);
-/* step[0] += 1 (the new token is in the cache), step[1] += 1 (its row was appended). */
+/* step[0] += 1 (the new token is in the cache), step[1] += 1 (its row was appended);
+ * n_a follows the window start. */
 int ls_decode_advance(const ls_decode_stack *S, ls_stream_t stream);
 /* Compression event for every layer and head (kvcompress.py:210-224):
  * accumulate the buffered rows oldest first, top-B by (score desc, id asc),

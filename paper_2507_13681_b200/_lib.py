@@ -38,7 +38,7 @@ class DecodeStackDesc(C.Structure):
                 ("row_cap", I32), ("sparse_cap", I32), ("budget_cap", I32), ("kv_layer_stride", I64),
                 ("kv_head_stride", I64), ("ring_s", P), ("ring_ml", P), ("ring_ids", P), ("ring_n", P),
                 ("ring_dense", P), ("sel_ids", P), ("n_sel", P), ("ck", P), ("cv", P), ("partials", P),
-                ("counters", P), ("step", P)]
+                ("counters", P), ("step", P), ("n_a", P)]
 
 
 LD = C.POINTER(LayerDesc)

@@ -32,6 +32,9 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 #include "ls_common.cuh"
 #include "tc_common.cuh"
 
@@ -69,8 +72,7 @@ __device__ __forceinline__ Geo geometry(const ls_decode_stack &S, int layer, int
   Geo g;
   if (compressed) {
     g.lo = max(0, length - S.window);
-    const int64_t hr = head_row(S, layer, h);
-    g.n_a = block_lower_bound(S.sel_ids + hr * S.budget_cap, S.n_sel[hr], g.lo);
+    g.n_a = S.n_a[head_row(S, layer, h)];  // kept current by the event and advance kernels
   } else {
     g.lo = 0;
     g.n_a = 0;
@@ -93,6 +95,10 @@ __device__ __forceinline__ Geo geometry(const ls_decode_stack &S, int layer, int
 constexpr int K6_TILE = 64;
 constexpr int K6_STAGES = 2;
 constexpr int K6_MAX_SPLIT = 256;
+constexpr int K6_MAX_CLUSTER = 16;  // splits of a unit = one thread-block cluster
+// G <= 4: 16-CTA clusters (non-portable); larger q-groups: 8 (the gather
+// area + cross-warp buffers must fit in the tile buffers)
+__host__ __device__ constexpr int k6_max_cluster(int G) { return G > 4 ? 8 : K6_MAX_CLUSTER; }
 
 __device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void *g, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(valid ? 16 : 0) : "memory");
@@ -100,7 +106,7 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void *g, 
 
 template <int D>
 constexpr int k6_smem_bytes(int G) {
-  return 2 * K6_STAGES * K6_TILE * D * 2 + 2 * G * K6_TILE * 4;
+  return 2 * K6_STAGES * K6_TILE * D * 2 + 2 * G * K6_TILE * 4 + (G * K6_MAX_CLUSTER + 2 * G) * 4;
 }
 
 template <int D, int G>
@@ -119,10 +125,9 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   unsigned char *vt = dsm + K6_STAGES * TILE_B;
   float *ps = reinterpret_cast<float *>(dsm + 2 * K6_STAGES * TILE_B);  // [G][TILE] raw log2 scores
   float *pp = ps + G * K6_TILE;                                        // [G][TILE] probabilities
-  float *ored = reinterpret_cast<float *>(dsm);                        // [4][G][D] (aliases the tiles at the end)
-  __shared__ int ticket;
-
-  const int split = blockIdx.x, unit = blockIdx.y, n_split = gridDim.x;
+  // [4][G][D] cross-warp reduction, in the tile buffers after the gather area
+  float *ored = reinterpret_cast<float *>(dsm) + k6_max_cluster(G) * G * (D + 2);
+  const int split = blockIdx.x, unit = blockIdx.y, n_split = gridDim.x;  // cluster = the unit's splits
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, seg = lane & 7;
   const int length = S.step[0];
   const int slot = S.step[1] % S.window;
@@ -288,15 +293,21 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
     __syncthreads();  // stage st and ps/pp are reused by tile t + 2 / t + 1
   }
 
-  // ---- cross-warp reduce -> this split's partial
+  // ---- cross-warp reduce -> this split's partial, in this CTA's shared memory
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
     for (int e = 0; e < DPL; ++e) ored[(warp * G + g) * D + lane * DPL + e] = o[g][e];
   __syncthreads();
+  // ---- the unit's splits form one thread-block cluster: every split pushes
+  // its partial (max, sum, o) into rank 0's shared memory (fire-and-forget
+  // DSMEM stores), rank 0 combines them in split order
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();  // rank 0's tile buffers are free: its loop is done
+  float *gather = reinterpret_cast<float *>(dsm);                       // [n_split][G][D + 2] in rank 0
+  float *dst = cluster.map_shared_rank(gather, 0) + split * G * (D + 2);
   for (int i = tid; i < G * (D + 2); i += K6_THREADS) {
     const int g = i / (D + 2), e = i % (D + 2);
-    float *pg = S.partials + (static_cast<int64_t>(h0 + g) * n_split + split) * (D + 2);
     float val;
     if (e == 0) {
       val = m_run[g];
@@ -307,73 +318,67 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
 #pragma unroll
       for (int w = 0; w < 4; ++w) val += ored[(w * G + g) * D + e - 2];
     }
-    pg[e] = val;
+    dst[i] = val;
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) ticket = atomicAdd(S.counters + unit, 1);
-  __syncthreads();
-  if (ticket != n_split - 1) return;
-  // ---- last CTA of this unit: combine the splits in split order, all G heads
-  // at once (the tile buffers are free: [G][n_split] weights and sums there)
-  __threadfence();
-  float *wsg = reinterpret_cast<float *>(dsm);       // [G][n_split] max, then weight
-  float *lsg = wsg + G * n_split;                     // [G][n_split] sum, then weighted sum
-  float *mg = lsg + G * n_split;                      // [G] max, [G] total
-  const float *pbase = S.partials + static_cast<int64_t>(h0) * n_split * (D + 2);
-  for (int i = tid; i < G * n_split; i += K6_THREADS) {
-    wsg[i] = __ldcg(pbase + static_cast<int64_t>(i) * (D + 2));
-    lsg[i] = __ldcg(pbase + static_cast<int64_t>(i) * (D + 2) + 1);
-  }
-  __syncthreads();
-  for (int g = warp; g < G; g += K6_THREADS / 32) {
-    float m = -INFINITY;
-    for (int s = lane; s < n_split; s += 32) m = fmaxf(m, wsg[g * n_split + s]);
-    m = warp_max(m);
-    float l = 0.f;
-    for (int s = lane; s < n_split; s += 32) {
-      const float ms = wsg[g * n_split + s];
-      const float w = ms == -INFINITY ? 0.f : fast_exp2(ms - m);
-      wsg[g * n_split + s] = w;
-      l += lsg[g * n_split + s] * w;
+  cluster.sync();  // partials visible in rank 0
+  if (split == 0) {
+    float *wsc = reinterpret_cast<float *>(dsm + 2 * K6_STAGES * TILE_B) + 2 * G * K6_TILE;  // [G][n_split] weights
+    float *mg = wsc + G * K6_MAX_CLUSTER;                                                   // [2G] max, total
+    if (tid < G) {
+      const int g = tid;
+      float M = -INFINITY;
+      for (int r = 0; r < n_split; ++r) M = fmaxf(M, gather[(r * G + g) * (D + 2)]);
+      float Lsum = 0.f;
+      for (int r = 0; r < n_split; ++r) {
+        const float *pr = gather + (r * G + g) * (D + 2);
+        const float w = pr[0] == -INFINITY ? 0.f : fast_exp2(pr[0] - M);
+        wsc[g * K6_MAX_CLUSTER + r] = w;
+        Lsum += pr[1] * w;
+      }
+      mg[g] = M;
+      mg[G + g] = Lsum;
     }
-    l = warp_sum(l);
-    if (lane == 0) {
-      mg[g] = m;
-      mg[G + g] = l;
+    __syncthreads();
+    for (int i = tid; i < G * D; i += K6_THREADS) {
+      const int g = i / D, e = i % D;
+      float acc = 0.f;
+      for (int r = 0; r < n_split; ++r) acc = fmaf(wsc[g * K6_MAX_CLUSTER + r], gather[(r * G + g) * (D + 2) + 2 + e], acc);
+      const float res = acc / mg[G + g];
+      const int64_t oi = static_cast<int64_t>(h0 + g) * D + e;
+      if (out_bf16)
+        reinterpret_cast<uint16_t *>(out)[oi] = f2bf(res);
+      else
+        reinterpret_cast<float *>(out)[oi] = res;
+    }
+    if (tid < G) {
+      const int64_t hr = head_row(S, layer, h0 + tid);
+      S.ring_ml[(hr * S.window + slot) * 2 + 0] = mg[tid];
+      S.ring_ml[(hr * S.window + slot) * 2 + 1] = mg[G + tid];
+      S.ring_n[hr * S.window + slot] = geo.n_cols;
+      S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
     }
   }
-  __syncthreads();
-  for (int i = tid; i < G * D; i += K6_THREADS) {
-    const int g = i / D, e = i % D;
-    const float *pg = pbase + static_cast<int64_t>(g) * n_split * (D + 2) + 2 + e;
-    const float *wg = wsg + g * n_split;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int s = 0; s < n_split; ++s) acc = fmaf(wg[s], __ldcg(pg + s * (D + 2)), acc);
-    const float r = acc / mg[G + g];
-    const int64_t oi = static_cast<int64_t>(h0 + g) * D + e;
-    if (out_bf16)
-      reinterpret_cast<uint16_t *>(out)[oi] = f2bf(r);
-    else
-      reinterpret_cast<float *>(out)[oi] = r;
-  }
-  if (tid < G) {
-    const int64_t hr = head_row(S, layer, h0 + tid);
-    S.ring_ml[(hr * S.window + slot) * 2 + 0] = mg[tid];
-    S.ring_ml[(hr * S.window + slot) * 2 + 1] = mg[G + tid];
-    S.ring_n[hr * S.window + slot] = geo.n_cols;
-    S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
-  }
-  if (tid == 0) S.counters[unit] = 0;  // re-armed for the next step / graph replay
 }
 
-__global__ void advance_kernel(int32_t *step, int rows) {
-  if (threadIdx.x == 0) {
-    step[0] += 1;
-    step[1] += rows;
+// step[0] += 1, step[1] += rows; and the working-set split point n_a of every
+// (layer, q-head) follows the window start lo = max(0, length - W) one up
+// (an id equal to the old lo moves below the window)
+__global__ void advance_kernel(ls_decode_stack S, int rows) {
+  const int length = S.step[0];
+  for (int hr = blockIdx.x * blockDim.x + threadIdx.x; hr < S.n_layers * S.n_heads; hr += gridDim.x * blockDim.x) {
+    const int lo_old = max(0, length - S.window), lo_new = max(0, length + 1 - S.window);
+    if (lo_new != lo_old) {
+      const int na = S.n_a[hr];
+      if (na < S.n_sel[hr] && S.sel_ids[static_cast<int64_t>(hr) * S.budget_cap + na] == lo_old) S.n_a[hr] = na + 1;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    S.step[0] = length + 1;
+    S.step[1] += rows;
   }
 }
+
 
 // ------------------------------------------------------------------ K7
 __device__ __forceinline__ unsigned long long dkey(double x) {
@@ -547,6 +552,13 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   const double T = block_sum_double(tot_mass, shd);
   const double Kp = block_sum_double(kept_mass, shd);
   const int iw = block_sum_int(in_window_picked, shi);
+  {
+    // working-set split point for this step: picked ids below the window start
+    int below = 0;
+    for (int j = threadIdx.x; j < base; j += blockDim.x) below += sel[j] < lo ? 1 : 0;
+    below = block_sum_int(below, shi);
+    if (threadIdx.x == 0) S.n_a[hr] = below;
+  }
   if (threadIdx.x == 0) {
     S.n_sel[hr] = base;
     if (retained_n) retained_n[hr] = base + (length - lo) - iw;
@@ -591,36 +603,49 @@ static int check_stack(const ls_decode_stack *S) {
   return LS_OK;
 }
 
-// split count: enough CTAs to cover the SMs a few times, never more than
-// the tiles of the longest row
-static int decode_splits(int units, int max_cols) {
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm <= 0) n_sm = 148;
-  }
-  const int target = n_sm * 3;
-  const int tiles = ceil_div(max_cols, dec::K6_TILE);
-  return std::max(1, std::min({ceil_div(target, units), tiles, dec::K6_MAX_SPLIT}));
-}
-
+// split count = cluster size: the splits of a unit combine through DSMEM.
+// 16 (non-portable) when the device accepts it, else 8; never more than the
+// tiles of the longest row.
 template <int D, int G>
-static int launch_decode(dim3 grid, cudaStream_t st, const ls_decode_stack *S, int layer, const uint16_t *q,
-                         const uint16_t *k, const uint16_t *v, int compressed, float sl, void *out, int out_bf16) {
+static int launch_decode(int units, int max_cols, cudaStream_t st, const ls_decode_stack *S, int layer,
+                         const uint16_t *q, const uint16_t *k, const uint16_t *v, int compressed, float sl, void *out,
+                         int out_bf16) {
   const int smem = dec::k6_smem_bytes<D>(G);
-  static_assert(dec::k6_smem_bytes<D>(G) >= 4 * G * D * 4, "reduction buffer must fit in the tile buffers");
-  static_assert(dec::k6_smem_bytes<D>(G) >= (2 * G * dec::K6_MAX_SPLIT + 2 * G) * 4, "combine buffers must fit");
-  if (smem > 48 * 1024)
-    LS_CUDA(cudaFuncSetAttribute(dec::decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dec::decode_kernel<D, G><<<grid, dec::K6_THREADS, smem, st>>>(*S, layer, q, k, v, compressed, sl, out, out_bf16);
+  static_assert(2 * dec::K6_STAGES * dec::K6_TILE * D * 2 >= (4 * G * D + dec::k6_max_cluster(G) * G * (D + 2)) * 4,
+                "gather + reduction buffers must fit in the tile buffers");
+  static int max_cluster = 0;
+  if (!max_cluster) {
+    max_cluster = 8;
+    if (dec::k6_max_cluster(G) > 8 &&
+        cudaFuncSetAttribute(dec::decode_kernel<D, G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+      max_cluster = dec::k6_max_cluster(G);
+    cudaGetLastError();
+  }
+  LS_CUDA(cudaFuncSetAttribute(dec::decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // compressed steps: 8-CTA clusters (enough splits for ~1K columns, best
+  // co-scheduling); dense steps stream the whole archive: up to 16
+  const int cl = compressed ? std::min(8, max_cluster) : max_cluster;
+  const int n_split = std::max(1, std::min(cl, ceil_div(max_cols, dec::K6_TILE)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_split, units, 1);
+  cfg.blockDim = dim3(dec::K6_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = n_split;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_kernel<D, G>, *S, layer, q, k, v, compressed, sl, out, out_bf16));
   return LS_OK;
 }
 
 extern "C" size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len) {
   (void)max_len;
-  return static_cast<size_t>(S->n_heads) * dec::K6_MAX_SPLIT * (S->head_dim + 2) * sizeof(float);
+  (void)S;  // splits combine through distributed shared memory: no global partials
+  return 0;
 }
 
 extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
@@ -636,12 +661,12 @@ extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uin
   const int group = S->n_heads / S->n_kv_heads;
   int r = LS_OK;
   if (compressed) {
-    dim3 grid(decode_splits(S->n_heads, max_cols), S->n_heads);
-    r = S->head_dim == 128 ? launch_decode<128, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16)
-                           : launch_decode<64, 1>(grid, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16);
+    r = S->head_dim == 128
+            ? launch_decode<128, 1>(S->n_heads, max_cols, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16)
+            : launch_decode<64, 1>(S->n_heads, max_cols, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16);
   } else {
-    dim3 grid(decode_splits(S->n_kv_heads, max_cols), S->n_kv_heads);
-#define LS_DENSE(DD, GG) r = launch_decode<DD, GG>(grid, st, S, layer, q, k_layer, v_layer, 0, sl, out, out_bf16)
+#define LS_DENSE(DD, GG) \
+  r = launch_decode<DD, GG>(S->n_kv_heads, max_cols, st, S, layer, q, k_layer, v_layer, 0, sl, out, out_bf16)
     if (S->head_dim == 128) {
       if (group == 1) LS_DENSE(128, 1);
       else if (group == 2) LS_DENSE(128, 2);
@@ -663,7 +688,7 @@ extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uin
 }
 
 extern "C" int ls_decode_advance(const ls_decode_stack *S, ls_stream_t stream) {
-  dec::advance_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(S->step, 1);
+  dec::advance_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(*S, 1);
   LS_LAUNCH_CHECK("advance_kernel");
   return LS_OK;
 }

@@ -117,6 +117,7 @@ class DecodeStack:
         self.cv = torch.zeros((HR, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
         self.counters = torch.zeros(n_heads, dtype=i32, device=dev)
         self.step_t = torch.zeros(4, dtype=i32, device=dev)
+        self.n_a = torch.zeros(HR, dtype=i32, device=dev)
         self.retained_n = torch.zeros(HR, dtype=i32, device=dev)
         self.score_cov = torch.zeros(HR, dtype=torch.float64, device=dev)
         self.desc = _lib.DecodeStackDesc(
@@ -124,10 +125,7 @@ class DecodeStack:
             int(kv_layer_stride), int(kv_head_stride), self.ring_s.data_ptr(), self.ring_ml.data_ptr(),
             self.ring_ids.data_ptr(), self.ring_n.data_ptr(), self.ring_dense.data_ptr(), self.sel_ids.data_ptr(),
             self.n_sel.data_ptr(), self.ck.data_ptr(), self.cv.data_ptr(), 0, self.counters.data_ptr(),
-            self.step_t.data_ptr())
-        n = _lib.lib().ls_decode_partials_size(ctypes.byref(self.desc), row_cap - 1)
-        self.partials = torch.zeros(n // 4 + 64, dtype=f32, device=dev)
-        self.desc.partials = self.partials.data_ptr()
+            self.step_t.data_ptr(), self.n_a.data_ptr())
         self.ws = Workspace()
         self.set_step(0, 0)
 
