@@ -232,6 +232,17 @@ size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len);
 int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
                    const uint16_t *v_layer, int32_t compressed, int32_t max_cols, void *out,
                    int32_t out_bf16, ls_stream_t stream);
+/* Same step with q read from the layer's Q archive at position step[0]
+ * (q_layer + h*q_head_stride + step[0]*head_dim): no per-step q gather, so a
+ * decode step of every layer is one launch per layer. flags: LS_DECODE_PDL
+ * launches it as a programmatic dependent of the previous kernel on the stream
+ * (its K/V tile prefetch overlaps that kernel's tail; q and all writes wait
+ * for it, as the next layer of a full model would). */
+#define LS_DECODE_PDL 1
+int ls_decode_step_archive(const ls_decode_stack *S, int32_t layer, const uint16_t *q_layer,
+                           int64_t q_head_stride, const uint16_t *k_layer, const uint16_t *v_layer,
+                           int32_t compressed, int32_t max_cols, void *out, int32_t out_bf16, int32_t flags,
+                           ls_stream_t stream);
 /* step[0] += 1 (the new token is in the cache), step[1] += 1 (its row was appended);
  * n_a follows the window start. */
 int ls_decode_advance(const ls_decode_stack *S, ls_stream_t stream);

@@ -111,8 +111,9 @@ constexpr int k6_smem_bytes(int G) {
 
 template <int D, int G>
 __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, int layer, const uint16_t *q,
+                                                            int64_t q_head_stride, int q_from_archive,
                                                             const uint16_t *k, const uint16_t *v, int compressed,
-                                                            float scale_log2, void *out, int out_bf16) {
+                                                            float scale_log2, void *out, int out_bf16, int pdl) {
   constexpr int ROW_B = D * 2;
   constexpr int CH = D / 8;                 // 16-B chunks per row
   constexpr int CPL = CH / 8;               // chunks per lane in the score phase (8 lanes per row)
@@ -172,6 +173,12 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   };
 
   if (n_tiles > 0) issue(0);
+  // programmatic dependent launch: the archive / compacted-cache tiles above
+  // do not depend on the previous kernel; q (the previous layer's output in a
+  // full model) and every write below do
+  if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // q of this step: [H][D] buffer, or the Q archive at position `length`
+  const uint16_t *qbase = q_from_archive ? q + static_cast<int64_t>(length) * D : q;
 
   // q of the first head sub-group stays in registers (dims of this lane's chunks)
   float qr[GS][CPL * 8];
@@ -181,7 +188,8 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
 #pragma unroll
       for (int m = 0; m < CPL; ++m) {
         const int hh = min(h0 + gb + g, h0 + G - 1);
-        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4 *>(q + static_cast<int64_t>(hh) * D + (seg + 8 * m) * 8)),
+        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4 *>(qbase + static_cast<int64_t>(hh) * q_head_stride +
+                                                            (seg + 8 * m) * 8)),
                       &qr[g][m * 8]);
       }
   };
@@ -293,6 +301,7 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
     __syncthreads();  // stage st and ps/pp are reused by tile t + 2 / t + 1
   }
 
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next layer may start its prologue
   // ---- cross-warp reduce -> this split's partial, in this CTA's shared memory
 #pragma unroll
   for (int g = 0; g < G; ++g)
@@ -608,8 +617,8 @@ static int check_stack(const ls_decode_stack *S) {
 // tiles of the longest row.
 template <int D, int G>
 static int launch_decode(int units, int max_cols, cudaStream_t st, const ls_decode_stack *S, int layer,
-                         const uint16_t *q, const uint16_t *k, const uint16_t *v, int compressed, float sl, void *out,
-                         int out_bf16) {
+                         const uint16_t *q, int64_t q_head_stride, int q_from_archive, const uint16_t *k,
+                         const uint16_t *v, int compressed, float sl, void *out, int out_bf16, int pdl) {
   const int smem = dec::k6_smem_bytes<D>(G);
   static_assert(2 * dec::K6_STAGES * dec::K6_TILE * D * 2 >= (4 * G * D + dec::k6_max_cluster(G) * G * (D + 2)) * 4,
                 "gather + reduction buffers must fit in the tile buffers");
@@ -631,14 +640,17 @@ static int launch_decode(int units, int max_cols, cudaStream_t st, const ls_deco
   cfg.blockDim = dim3(dec::K6_THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = n_split;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_kernel<D, G>, *S, layer, q, k, v, compressed, sl, out, out_bf16));
+  cfg.numAttrs = pdl ? 2 : 1;
+  LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_kernel<D, G>, *S, layer, q, q_head_stride, q_from_archive, k, v,
+                             compressed, sl, out, out_bf16, pdl));
   return LS_OK;
 }
 
@@ -648,9 +660,9 @@ extern "C" size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_
   return 0;
 }
 
-extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
-                              const uint16_t *v_layer, int32_t compressed, int32_t max_cols, void *out,
-                              int32_t out_bf16, ls_stream_t stream) {
+static int decode_step_impl(const ls_decode_stack *S, int32_t layer, const uint16_t *q, int64_t q_head_stride,
+                            int q_from_archive, const uint16_t *k_layer, const uint16_t *v_layer, int32_t compressed,
+                            int32_t max_cols, void *out, int32_t out_bf16, int pdl, ls_stream_t stream) {
   int c = check_stack(S);
   if (c) return c;
   LS_REQUIRE(layer >= 0 && layer < S->n_layers, LS_ERR_DIMENSION_MISMATCH, "layer out of range");
@@ -660,13 +672,14 @@ extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uin
   const float sl = kLog2e / sqrtf(static_cast<float>(S->head_dim));
   const int group = S->n_heads / S->n_kv_heads;
   int r = LS_OK;
+#define LS_ARGS q, q_head_stride, q_from_archive, k_layer, v_layer
   if (compressed) {
     r = S->head_dim == 128
-            ? launch_decode<128, 1>(S->n_heads, max_cols, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16)
-            : launch_decode<64, 1>(S->n_heads, max_cols, st, S, layer, q, k_layer, v_layer, 1, sl, out, out_bf16);
+            ? launch_decode<128, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, 1, sl, out, out_bf16, pdl)
+            : launch_decode<64, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, 1, sl, out, out_bf16, pdl);
   } else {
 #define LS_DENSE(DD, GG) \
-  r = launch_decode<DD, GG>(S->n_kv_heads, max_cols, st, S, layer, q, k_layer, v_layer, 0, sl, out, out_bf16)
+  r = launch_decode<DD, GG>(S->n_kv_heads, max_cols, st, S, layer, LS_ARGS, 0, sl, out, out_bf16, pdl)
     if (S->head_dim == 128) {
       if (group == 1) LS_DENSE(128, 1);
       else if (group == 2) LS_DENSE(128, 2);
@@ -682,9 +695,25 @@ extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uin
     }
 #undef LS_DENSE
   }
+#undef LS_ARGS
   if (r) return r;
   LS_LAUNCH_CHECK("decode_kernel");
   return LS_OK;
+}
+
+extern "C" int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, const uint16_t *k_layer,
+                              const uint16_t *v_layer, int32_t compressed, int32_t max_cols, void *out,
+                              int32_t out_bf16, ls_stream_t stream) {
+  return decode_step_impl(S, layer, q, S->head_dim, 0, k_layer, v_layer, compressed, max_cols, out, out_bf16, 0,
+                          stream);
+}
+
+extern "C" int ls_decode_step_archive(const ls_decode_stack *S, int32_t layer, const uint16_t *q_layer,
+                                      int64_t q_head_stride, const uint16_t *k_layer, const uint16_t *v_layer,
+                                      int32_t compressed, int32_t max_cols, void *out, int32_t out_bf16,
+                                      int32_t flags, ls_stream_t stream) {
+  return decode_step_impl(S, layer, q_layer, q_head_stride, 1, k_layer, v_layer, compressed, max_cols, out, out_bf16,
+                          (flags & LS_DECODE_PDL) ? 1 : 0, stream);
 }
 
 extern "C" int ls_decode_advance(const ls_decode_stack *S, ls_stream_t stream) {

@@ -185,10 +185,13 @@ class SessionEngine:
 
     # -------------------------------------------------------------- decode
     def _step(self, store: QKVStore, q_buf, out_buf, compressed: bool, max_cols: int, stream=None):
+        """One decode step of every layer: K6 per layer reading q from the Q
+        archive at the device cache length, each launched as a programmatic
+        dependent of the previous layer's kernel, then the counter advance."""
         st = self.stack
-        torch.index_select(store.q, 2, st.step_t[:1], out=q_buf)  # q of position step[0] (device index)
         for l in range(self.shape.n_layers):
-            st.step(l, q_buf[l, :, 0], store.k[l], store.v[l], compressed, max_cols, out_buf[l], stream=stream)
+            st.step_archive(l, store.q[l], store.k[l], store.v[l], compressed, max_cols, out_buf[l], pdl=True,
+                            stream=stream)
         st.advance(stream=stream)
 
     def _graph(self, key, name, fn):

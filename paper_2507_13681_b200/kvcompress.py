@@ -189,6 +189,16 @@ class DecodeStack:
                   v_layer.data_ptr(), int(bool(compressed)), int(max_cols), out.data_ptr(),
                   int(out.dtype == torch.bfloat16), _lib.stream_ptr(stream))
 
+    def step_archive(self, layer: int, q_layer: torch.Tensor, k_layer: torch.Tensor, v_layer: torch.Tensor,
+                     compressed: bool, max_cols: int, out: torch.Tensor, pdl: bool = True, stream=None):
+        """K6 for one layer with q read from the layer's Q archive [H, cap, d]
+        at the current cache length (no per-step q gather); pdl: programmatic
+        dependent launch after the previous kernel on the stream."""
+        _lib.call("ls_decode_step_archive", ctypes.byref(self.desc), int(layer), q_layer.data_ptr(),
+                  int(q_layer.stride(0)), k_layer.data_ptr(), v_layer.data_ptr(), int(bool(compressed)),
+                  int(max_cols), out.data_ptr(), int(out.dtype == torch.bfloat16), 1 if pdl else 0,
+                  _lib.stream_ptr(stream))
+
     def advance(self, stream=None):
         _lib.call("ls_decode_advance", ctypes.byref(self.desc), _lib.stream_ptr(stream))
         self.length += 1
