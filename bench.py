@@ -184,28 +184,32 @@ def cpu_baseline(cfg, cores=None):
     _CPU.update(Q=Q, K=K, V=V, blocks=blocks, group=group, alpha=cfg["alpha"], rate=cfg["rate"],
                 floor=cfg["floor"], window=cfg["obs_window"] or cfg["interval"])
     ctx = mp.get_context("fork")
-    per_turn_ms = []
     units = cfg["n_layers"] * cfg["n_q"]
-    n_sample = min(cores, n_q_s)
-    with ctx.Pool(n_sample) as pool:
-        for t in range(cfg["n_turns"]):
-            t0 = time.perf_counter()
-            times = pool.map(_cpu_unit, [(t, h) for h in range(n_sample)])
-            wall = time.perf_counter() - t0
-            # n_sample units ran in parallel on n_sample cores
-            per_turn_ms.append(1e3 * wall * units / n_sample)
+    n_t = cfg["n_turns"]
+    # one round: (turn, head) units spread over the turns, one per process, so
+    # a round takes about one turn-3 unit of wall time (bounded sample)
+    per_turn_heads = max(1, min(n_q_s, cores // n_t))
+    work = [(t, h) for h in range(per_turn_heads) for t in range(n_t)]
+    n_sample = len(work)
+    with ctx.Pool(min(cores, n_sample)) as pool:
+        times = pool.map(_cpu_unit, work)
         # decode: one head-step at the dense (pre-event) and compressed sizes
         L_end = blocks[-1][0] + blocks[-1][1]
         comp_cols = min(L_end, cfg["budget"] + (cfg["obs_window"] or cfg["interval"]) + 1)
         dense_t, comp_t = pool.map(_cpu_decode_unit, [(L_end, 3), (comp_cols, 20)])
+    n_proc = min(cores, n_sample)
+    # per-unit core time x units / cores in parallel = the turn's TTFT on this host
+    per_turn_ms = [1e3 * statistics.mean(tt for (t, _), tt in zip(work, times) if t == turn) * units / n_proc
+                   for turn in range(n_t)]
     n_dense = min(cfg["max_new"], cfg["warmup"] - 1 if cfg["budget"] is not None else cfg["max_new"])
     step_s = (n_dense * dense_t + (cfg["max_new"] - n_dense) * comp_t) / cfg["max_new"]
-    tok_s = 1.0 / (step_s * units / cores)
-    sample = (f"oracle port (numpy fp64), {n_sample} (turn, layer 0, head) prefill units per turn of the "
-              f"{cfg['n_turns']} turns in parallel on {n_sample} processes + decode head-steps at {L_end} and "
-              f"{comp_cols} columns; extrapolated x{units} (layer, head) units")
+    tok_s = 1.0 / (step_s * units / n_proc)
+    sample = (f"oracle port (numpy fp64): {per_turn_heads} (layer 0, head) prefill units of each of the {n_t} turns "
+              f"({n_sample} units in parallel on {n_proc} processes) + decode head-steps at {L_end} and "
+              f"{comp_cols} columns; per-unit core time extrapolated to {units} (layer, head) units on "
+              f"{n_proc} cores")
     return dict(ttft_ms=statistics.mean(per_turn_ms), per_turn_ms=per_turn_ms, decode_tokens_per_s=tok_s,
-                cores=n_sample, sample=sample)
+                cores=n_proc, sample=sample)
 
 
 def turn_blocks(input_len, n_turns, max_new):

@@ -58,7 +58,7 @@ def launches(path, top=30):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in data:
         if len(r) <= vi:
