@@ -58,6 +58,16 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a_desc, uint6
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// D (TMEM) += A (TMEM, K-major: lane = row, 32-bit columns = K pairs) * B (smem descriptor)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
                : "memory");
@@ -86,8 +96,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
   if (mbar_try_wait(a, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait(a, parity)) {
-    if (clock64() - t0 > 20000000000LL) __trap();
+  for (uint32_t k = 1;; ++k) {
+    if (mbar_try_wait(a, parity)) return;
+    if ((k & 255) == 0 && clock64() - t0 > 20000000000LL) __trap();
   }
 }
 

@@ -76,15 +76,14 @@ struct Smem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = Q_BYTES;                 // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;    // 2 stages
-  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
-  static constexpr int OFF_MISC = OFF_P + BM * BN * 2;
+  static constexpr int OFF_MISC = OFF_V + 2 * KV_BYTES;  // (P lives in TMEM, aliasing its S buffer)
   // misc: barriers 256 | ints 256 | kb_bits 256 | pmax 1024 | pd 1024 | lx 512 | gcols 1024 | dense_list 4096 | blk_cnt 8192
   static constexpr int MISC_BYTES = 256 + 256 + 256 + 1024 + 1024 + 512 + 1024 + MAX_KB * 2 + MAX_KB * 4;
   static constexpr int TOTAL = OFF_MISC + MISC_BYTES + 1024;
 };
 
 struct Bars {
-  uint64_t full[2], empty[2], s_full[2], s_empty[2], p_full, pv_done, q_full;
+  uint64_t full[2], empty[2], s_full[2], p_full[2], pv_done[2], q_full;
 };
 
 __device__ __forceinline__ bool bit_of(const uint32_t *b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
@@ -138,10 +137,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(&bars->full[s], 1);
       tc::mbar_init(&bars->empty[s], 1);
       tc::mbar_init(&bars->s_full[s], 1);
-      tc::mbar_init(&bars->s_empty[s], 1);
+      tc::mbar_init(&bars->p_full[s], 1);
+      tc::mbar_init(&bars->pv_done[s], 1);
     }
-    tc::mbar_init(&bars->p_full, 1);
-    tc::mbar_init(&bars->pv_done, 1);
     tc::mbar_init(&bars->q_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -293,29 +291,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t IDESC_S = tc::make_idesc(BM, BN, false, false);
       constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, false, true);
       const uint32_t qs = tc::smem_u32(smem + L::OFF_Q);
-      const uint32_t ps = tc::smem_u32(smem + L::OFF_P);
       KDBG(1, -1, 2);
       tc::mbar_wait(&bars->q_full, 0);
-      auto issue_pv = [&](int j) {  // O += P(j) V(j)
+      auto issue_pv = [&](int j) {  // O += P(j) V(j), P(j) bf16 in TMEM over S(j)
         KDBG(1, j, 3);
-        tc::mbar_wait(&bars->p_full, j & 1);
+        tc::mbar_wait(&bars->p_full[j & 1], (j >> 1) & 1);
         tc::fence_after_sync();
         const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (j & 1) * L::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t ad = tc::make_desc(ps + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
-          tc::mma_bf16(tmem_o, ad, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_bf16_ts(tmem_o, tmem + (j & 1) * 128 + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        tc::mma_commit(&bars->pv_done);
+        tc::mma_commit(&bars->pv_done[j & 1]);
         tc::mma_commit(&bars->empty[j & 1]);
       };
+      // S(i) may overwrite P(i-2) in its buffer: PV(i-2) was issued before it
+      // and the tensor pipe executes one thread's MMAs in order
       for (int i = 0; i < n_all; ++i) {
         const int s = i & 1;
         KDBG(1, i, 4);
         tc::mbar_wait(&bars->full[s], (i >> 1) & 1);
         KDBG(1, i, 5);
-        tc::mbar_wait(&bars->s_empty[s], ((i >> 1) & 1) ^ 1);
         tc::fence_after_sync();
         const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
 #pragma unroll
@@ -434,15 +431,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::named_sync(1, N_SOFT);
       const float tm = fmaxf(pmax[row], pmax[BM + row]);
       const float m_tile = tm == -INFINITY ? -INFINITY : tm * p.scale_log2;
-      // previous PV must be done before P is overwritten or O is rescaled
-      if (i > 0) {
-        if (tid == 0) KDBG(2, i, 7);
-        tc::mbar_wait(&bars->pv_done, (i - 1) & 1);
-        tc::fence_after_sync();
-      }
       const bool need = m_tile > m_ref + RESCALE_LOG2;
-      // TMEM ld/st are .sync.aligned: the whole warp rescales if any row needs it
+      // TMEM ld/st are .sync.aligned: the whole warp rescales if any row needs it,
+      // after PV(i-1) has landed in O (PV(i) waits for this tile's p_full)
       if (__any_sync(0xffffffffu, need && m_ref != -INFINITY && i > 0)) {
+        if (tid == 0) KDBG(2, i, 7);
+        tc::mbar_wait(&bars->pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        tc::fence_after_sync();
         const float corr = (need && m_ref != -INFINITY) ? fast_exp2(m_ref - m_tile) : 1.f;
 #pragma unroll
         for (int cch = 0; cch < DH / 32; ++cch) {
@@ -460,42 +455,35 @@ __global__ void __launch_bounds__(THREADS, 1)
         m_ref = m_tile;
       }
       float lsum = 0.f;
+      uint32_t pk[32];  // this thread's 64 bf16 of P(i): TMEM columns s*128 + wg*32 + [0, 32)
 #pragma unroll
       for (int cch = 0; cch < 2; ++cch) {
-        uint32_t pk[16];
         if (live[cch]) {
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(fmaf(sv[cch][j], p.scale_log2, -m_ref)) : 0.f;
             const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[cch][j + 1], p.scale_log2, -m_ref)) : 0.f;
             lsum += a + b;
-            pk[j >> 1] = tc::pack_bf16(a, b);
+            pk[cch * 16 + (j >> 1)] = tc::pack_bf16(a, b);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = 0u;
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int chunk = wg * 8 + cch * 4 + q4;
-          *reinterpret_cast<uint4 *>(smem + L::OFF_P + tc::sw128_offset(row, chunk, BM)) =
-              make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+          for (int j = 0; j < 16; ++j) pk[cch * 16 + j] = 0u;
         }
       }
+      // (every S read of this tile finished before the max exchange barrier)
+      tc::tmem_st32(tmem + s * 128 + lane_base + wg * 32, reinterpret_cast<const float *>(pk));
+      tc::tmem_wait_st();
       l += lsum;
       tc::fence_before_sync();
-      tc::fence_proxy_async();
       tc::named_sync(1, N_SOFT);
-      if (tid == 0) {
-        tc::mbar_arrive(&bars->s_empty[s]);
-        tc::mbar_arrive(&bars->p_full);
-      }
+      if (tid == 0) tc::mbar_arrive(&bars->p_full[s]);
     }
     // O (TMEM) -> registers, relative to m_ref
     float o[DH];
     if (n_all > 0) {
       if (tid == 0) KDBG(2, n_all, 8);
-      tc::mbar_wait(&bars->pv_done, (n_all - 1) & 1);
+      tc::mbar_wait(&bars->pv_done[(n_all - 1) & 1], ((n_all - 1) >> 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
       for (int cch = 0; cch < DH / 32; ++cch) {
