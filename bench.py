@@ -63,6 +63,19 @@ def parse():
     return ap.parse_args()
 
 
+def _load_traffic():
+    """profiles/ncu_traffic.json: dram bytes per launch of the timed entries,
+    from one ncu --set full capture (tools/ncu_traffic.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
+NCU_TRAFFIC = _load_traffic()
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -366,6 +379,10 @@ def main():
     roof = roofline(per, cfg, eng, store, blocks, peaks)
     if roof is not None and roof.get("kernel") in per:
         roof["share_of_timed"] = round(sum(per[roof["kernel"]]) / total_ms, 4)
+    pre_roof = None  # the sparse-attention kernel (K5) against the tensor pipe
+    if "ls_vs_attention" in per:
+        pre_roof = roofline({"ls_vs_attention": per["ls_vs_attention"]}, cfg, eng, store, blocks, peaks)
+        pre_roof["share_of_timed"] = round(sum(per["ls_vs_attention"]) / total_ms, 4)
     dec_roof = None  # the decode step (one graph replay, all layers) against HBM
     for k in ("decode_graph_comp", "decode_graph_dense"):
         if k in per:
@@ -389,7 +406,7 @@ def main():
             "decode_tokens_per_s": round(tok_s, 2),
             "prefill_ms_per_turn": round(ttft, 3), "decode_ms_per_turn": round(decode_ms / n_prefills, 3),
             "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-            "decode_roofline": dec_roof}
+            "decode_roofline": dec_roof, "prefill_roofline": pre_roof}
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -411,6 +428,7 @@ def roofline(per, cfg, eng, store, blocks, peaks):
         return None
     name = max(per, key=lambda k: sum(per[k]))
     mean_ms = statistics.mean(per[name])
+    extra = {}
     d = cfg["d"]
     # algorithmic work of the last dialogue's launches of this entry
     work = None
@@ -419,6 +437,11 @@ def roofline(per, cfg, eng, store, blocks, peaks):
         work = 4.0 * d * float(sum(int(c.sum()) for c in eng.cell_log)) / n
         bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]
         achieved = work / (mean_ms * 1e-3) / 1e12
+        if eng.tile_log:  # executed 128x128 tiles: the tensor pipe's actual work
+            ex = 4.0 * d * 128 * 128 * float(sum(int(t.sum()) for t in eng.tile_log)) / n
+            extra = {"executed_tflops": round(ex / (mean_ms * 1e-3) / 1e12, 3),
+                     "executed_frac": round(ex / (mean_ms * 1e-3) / 1e12 / peak, 5),
+                     "algorithmic_over_executed": round(work / ex, 4)}
     elif name == "ls_score_lines" and eng.score_log:
         work = 2.0 * d * float(sum(int(c.sum()) for c in eng.score_log)) / n  # QK^T of the causal sampled cells
         bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]
@@ -432,11 +455,17 @@ def roofline(per, cfg, eng, store, blocks, peaks):
         work = bytes_
     else:
         return {"kernel": name, "mean_ms": round(mean_ms, 4), "note": "no algorithmic model"}
-    return {"kernel": name, "bound": bound, "achieved": round(achieved, 3) if achieved else None,
+    res = {"kernel": name, "bound": bound, "achieved": round(achieved, 3) if achieved else None,
             "peak": peak, "unit": unit, "frac": round(achieved / peak, 5) if achieved else None,
             "traffic": None, "mean_launch_ms": round(mean_ms, 4), "launches": len(per[name]),
             "work_per_launch": work, "peak_src": peaks["src"] + (" sustained" if bound == "tensor" else ""),
             "share_of_timed": None}
+    res.update(extra)
+    tr = NCU_TRAFFIC.get(name)
+    if tr:  # dram bytes per launch from the committed ncu --set full capture
+        res["traffic"] = tr["dram_bytes_per_launch"]
+        res["traffic_src"] = tr["source"]
+    return res
 
 
 def run_e2e(args, cfg, eng, store, blocks, shard, gather):

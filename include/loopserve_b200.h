@@ -161,6 +161,12 @@ int ls_vs_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
                     const uint16_t *v, const int32_t *slash_ids, const int32_t *vert_ids,
                     const int32_t *counts, void *out, int32_t out_bf16, int64_t *cells,
                     void *ws, size_t ws_bytes, ls_stream_t stream);
+/* Same, also counting the 128x128 tensor-core tiles each head executed
+ * (tiles[h] int64, the executed-FLOP denominator of the K5 roofline).    */
+int ls_vs_attention_ex(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k,
+                       const uint16_t *v, const int32_t *slash_ids, const int32_t *vert_ids,
+                       const int32_t *counts, void *out, int32_t out_bf16, int64_t *cells,
+                       int64_t *tiles, void *ws, size_t ws_bytes, ls_stream_t stream);
 /* Same contract on CUDA cores (FFMA, no tensor cores): the cross-check the
  * GPU tests compare the tcgen05 kernel against at full sizes.           */
 int ls_vs_attention_simt(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k,

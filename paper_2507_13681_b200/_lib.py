@@ -66,6 +66,7 @@ SIGNATURES = {
     "ls_vs_attention_workspace": (SZ, [LD]),
     "ls_vs_attention": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, SZ, P]),
     "ls_vs_attention_simt": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, SZ, P]),
+    "ls_vs_attention_ex": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, P, SZ, P]),
     "ls_plan_rows": (C.c_int, [LD, I32, P, P, P, P, P, P, I64, I64, P]),
     "ls_dense_attention": (C.c_int, [LD, P, P, P, P, I32, P]),
     "ls_decode_partials_size": (SZ, [DS, I32]),
@@ -109,7 +110,7 @@ def check(status: int, what: str = "") -> None:
 # bench.py reports the sum over its timed region as `gpu_launches`.
 KERNELS_PER_CALL = {
     "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 4, "ls_greedy_dense": 5,
-    "ls_vs_attention": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
+    "ls_vs_attention": 3, "ls_vs_attention_ex": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
     "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
 }
 launch_count = 0

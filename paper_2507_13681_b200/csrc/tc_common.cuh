@@ -82,10 +82,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}\n"
       : "=r"(ok)
-      : "r"(a), "r"(parity), "r"(0x989680u)  // suspend-time hint (ns): sleep in the barrier, not in a spin
+      : "r"(a), "r"(parity)
       : "memory");
   return ok != 0;
 }

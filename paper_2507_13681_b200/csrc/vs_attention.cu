@@ -409,7 +409,8 @@ namespace ls {
 size_t vs_attention_ws_workspace(const ls_layer_desc *L);
 int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
                     const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
-                    int32_t out_bf16, int64_t *cells, int dense, void *ws, size_t ws_bytes, cudaStream_t st);
+                    int32_t out_bf16, int64_t *cells, int64_t *tiles, int dense, void *ws, size_t ws_bytes,
+                    cudaStream_t st);
 }  // namespace ls
 
 extern "C" size_t ls_vs_attention_workspace(const ls_layer_desc *L) {
@@ -424,7 +425,17 @@ extern "C" int ls_vs_attention(const ls_layer_desc *L, const uint16_t *q, const 
                                int32_t out_bf16, int64_t *cells, void *ws, size_t ws_bytes, ls_stream_t stream) {
   int stc = k5::check_desc(L);
   if (stc) return stc;
-  return vs_attention_ws(L, q, k, v, slash_ids, vert_ids, counts, out, out_bf16, cells, 0, ws, ws_bytes,
+  return vs_attention_ws(L, q, k, v, slash_ids, vert_ids, counts, out, out_bf16, cells, nullptr, 0, ws, ws_bytes,
+                         static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int ls_vs_attention_ex(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                  const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts,
+                                  void *out, int32_t out_bf16, int64_t *cells, int64_t *tiles, void *ws,
+                                  size_t ws_bytes, ls_stream_t stream) {
+  int stc = k5::check_desc(L);
+  if (stc) return stc;
+  return vs_attention_ws(L, q, k, v, slash_ids, vert_ids, counts, out, out_bf16, cells, tiles, 0, ws, ws_bytes,
                          static_cast<cudaStream_t>(stream));
 }
 
@@ -534,7 +545,7 @@ extern "C" int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, con
   keep_pool_memory();
   LS_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&cells), sizeof(int64_t) * L->n_heads, st));
   // dense mode touches every causal key block with the causal mask only (tensor-core path)
-  int s = vs_attention_ws(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, 1, nullptr, 0, st);
+  int s = vs_attention_ws(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, nullptr, 1, nullptr, 0, st);
   LS_CUDA(cudaFreeAsync(cells, st));
   return s;
 }

@@ -55,6 +55,7 @@ struct Params {
   void *out;
   int out_bf16;
   long long *cells;
+  long long *tiles;  // optional: tensor-core tiles executed per head (NULL: not counted)
   int *dbg;  // optional host-mapped progress record [CTA][16] (ls_debug_set_buffer)
 };
 
@@ -535,6 +536,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const long long cs = warp_sum_ll(my_cells);
     if (lane == 0 && cs)
       atomicAdd(reinterpret_cast<unsigned long long *>(p.cells + h), static_cast<unsigned long long>(cs));
+    if (tid == 0 && p.tiles && n_all)
+      atomicAdd(reinterpret_cast<unsigned long long *>(p.tiles + h), static_cast<unsigned long long>(n_all));
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -635,7 +638,8 @@ size_t vs_attention_ws_workspace(const ls_layer_desc *L) {
 
 int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
                     const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
-                    int32_t out_bf16, int64_t *cells, int dense, void *ws, size_t ws_bytes, cudaStream_t st) {
+                    int32_t out_bf16, int64_t *cells, int64_t *tiles, int dense, void *ws, size_t ws_bytes,
+                    cudaStream_t st) {
   LS_REQUIRE(L->head_dim == 64 || L->head_dim == 128, LS_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   LS_REQUIRE((L->n_total + k5ws::BN - 1) / k5ws::BN <= k5ws::MAX_KB, LS_ERR_UNSUPPORTED, "n_total too large");
   LS_REQUIRE(dense || ws_bytes >= vs_attention_ws_workspace(L), LS_ERR_WORKSPACE, "vs_attention workspace too small");
@@ -694,8 +698,10 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   p.out = out;
   p.out_bf16 = out_bf16;
   p.cells = reinterpret_cast<long long *>(cells);
+  p.tiles = reinterpret_cast<long long *>(tiles);
   p.dbg = g_debug_buffer;
   LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * H, st));
+  if (tiles) LS_CUDA(cudaMemsetAsync(tiles, 0, sizeof(int64_t) * H, st));
   dim3 grid(nqt, H);
   if (d == 128) {
     const int smem = k5ws::Smem<128>::TOTAL;

@@ -124,7 +124,7 @@ class SessionEngine:
 
     def clear_logs(self):
         """Work logs (device tensors / host counts) used by bench.py's roofline."""
-        self.cell_log, self.score_log, self.decode_log = [], [], []
+        self.cell_log, self.score_log, self.decode_log, self.tile_log = [], [], [], []
 
     # ------------------------------------------------------------- prefill
     def prefill(self, store: QKVStore, turn: int, row_offset: int, n_new: int, seed_rows: bool = True,
@@ -160,9 +160,11 @@ class SessionEngine:
                 continue
             plans: LayerPlans = sparsify_layer(qb, kl, rows[l], p.alpha, n_new, n_total, sh.n_kv,
                                                q_head_stride=store.q.stride(1), ws=self.ws, stream=stream)
+            tiles = torch.empty(sh.n_q, dtype=torch.int64, device=self.device)
             out, cells = attention_layer(qb, kl, vl, plans.slash_ids, plans.vert_ids, plans.counts, n_new,
                                          n_total, sh.n_kv, out_dtype=self.out_dtype,
-                                         q_head_stride=store.q.stride(1), ws=self.ws, stream=stream)
+                                         q_head_stride=store.q.stride(1), ws=self.ws, stream=stream, tiles=tiles)
+            self.tile_log.append(tiles)
             outs.append(out)
             plans_all.append(plans)
             cells_all.append(cells)

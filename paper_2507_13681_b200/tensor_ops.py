@@ -97,8 +97,9 @@ def plan_tensors(plan, n_total: int, device):
 def attention_layer(q_block: torch.Tensor, k: torch.Tensor, v: torch.Tensor, slash_ids, vert_ids, counts,
                     n_new: int, n_total: int, n_kv_heads: int, out: torch.Tensor | None = None,
                     out_dtype=torch.bfloat16, q_head_stride=None, kv_head_stride=None,
-                    ws: Workspace | None = None, stream=None):
-    """K5 for every q-head of a layer -> (out [n_new, H, d], cells [H])."""
+                    ws: Workspace | None = None, stream=None, tiles: torch.Tensor | None = None):
+    """K5 for every q-head of a layer -> (out [n_new, H, d], cells [H]); with
+    `tiles` (int64 [H]) also the 128x128 tensor-core tiles each head executed."""
     H = counts.shape[0]
     d = q_block.shape[-1]
     dev = q_block.device
@@ -111,9 +112,15 @@ def attention_layer(q_block: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sla
     ws = ws or Workspace()
     n = _lib.lib().ls_vs_attention_workspace(C_ref(L))
     w = ws.get(n)
-    _lib.call("ls_vs_attention", C_ref(L), q_block.data_ptr(), k.data_ptr(), v.data_ptr(), slash_ids.data_ptr(),
-              vert_ids.data_ptr(), counts.data_ptr(), out.data_ptr(), int(out.dtype == torch.bfloat16),
-              cells.data_ptr(), w.data_ptr(), w.numel(), _lib.stream_ptr(stream))
+    if tiles is None:
+        _lib.call("ls_vs_attention", C_ref(L), q_block.data_ptr(), k.data_ptr(), v.data_ptr(), slash_ids.data_ptr(),
+                  vert_ids.data_ptr(), counts.data_ptr(), out.data_ptr(), int(out.dtype == torch.bfloat16),
+                  cells.data_ptr(), w.data_ptr(), w.numel(), _lib.stream_ptr(stream))
+    else:
+        _lib.call("ls_vs_attention_ex", C_ref(L), q_block.data_ptr(), k.data_ptr(), v.data_ptr(),
+                  slash_ids.data_ptr(), vert_ids.data_ptr(), counts.data_ptr(), out.data_ptr(),
+                  int(out.dtype == torch.bfloat16), cells.data_ptr(), tiles.data_ptr(), w.data_ptr(), w.numel(),
+                  _lib.stream_ptr(stream))
     return out, cells
 
 
