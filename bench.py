@@ -380,9 +380,10 @@ def main():
     if roof is not None and roof.get("kernel") in per:
         roof["share_of_timed"] = round(sum(per[roof["kernel"]]) / total_ms, 4)
     pre_roof = None  # the sparse-attention kernel (K5) against the tensor pipe
-    if "ls_vs_attention" in per:
-        pre_roof = roofline({"ls_vs_attention": per["ls_vs_attention"]}, cfg, eng, store, blocks, peaks)
-        pre_roof["share_of_timed"] = round(sum(per["ls_vs_attention"]) / total_ms, 4)
+    k5 = next((k for k in ("ls_vs_attention_ex", "ls_vs_attention") if k in per), None)
+    if k5 is not None:
+        pre_roof = roofline({k5: per[k5]}, cfg, eng, store, blocks, peaks)
+        pre_roof["share_of_timed"] = round(sum(per[k5]) / total_ms, 4)
     dec_roof = None  # the decode step (one graph replay, all layers) against HBM
     for k in ("decode_graph_comp", "decode_graph_dense"):
         if k in per:
@@ -433,7 +434,7 @@ def roofline(per, cfg, eng, store, blocks, peaks):
     # algorithmic work of the last dialogue's launches of this entry
     work = None
     n = len(per[name])
-    if name == "ls_vs_attention" and eng.cell_log:
+    if name in ("ls_vs_attention", "ls_vs_attention_ex") and eng.cell_log:
         work = 4.0 * d * float(sum(int(c.sum()) for c in eng.cell_log)) / n
         bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]
         achieved = work / (mean_ms * 1e-3) / 1e12
@@ -461,7 +462,7 @@ def roofline(per, cfg, eng, store, blocks, peaks):
             "work_per_launch": work, "peak_src": peaks["src"] + (" sustained" if bound == "tensor" else ""),
             "share_of_timed": None}
     res.update(extra)
-    tr = NCU_TRAFFIC.get(name)
+    tr = NCU_TRAFFIC.get("ls_vs_attention" if name.startswith("ls_vs_attention") else name)
     if tr:  # dram bytes per launch from the committed ncu --set full capture
         res["traffic"] = tr["dram_bytes_per_launch"]
         res["traffic_src"] = tr["source"]
