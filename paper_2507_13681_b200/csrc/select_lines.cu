@@ -343,7 +343,10 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         const int slot = j % RING;
         int ready;
         while ((ready = vload(S.r_seq + slot)) != j + 1) {
-          if (prod_done && j >= n_prod) break;
+          if (prod_done) {
+            __threadfence_block();
+            if (j >= n_prod) break;
+          }
           __nanosleep(32);
         }
         if (ready != j + 1) break;  // every published pick consumed
@@ -379,7 +382,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       if (lane == 0) {
         while (true) {
           if (j < n_prod) { ok = true; break; }
-          if (prod_done || j >= stop_at) break;
+          if (j >= stop_at) break;
+          if (prod_done) {  // the last n_prod store precedes prod_done: re-read it after the flag
+            __threadfence_block();
+            ok = j < n_prod;
+            break;
+          }
           __nanosleep(256);
         }
         if (j >= stop_at) ok = false;

@@ -424,8 +424,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (live[cch]) {
           tc::tmem_ld32(s_addr + cch * 32, sv[cch]);
           tc::tmem_wait_ld();
+          // masked cells become -inf once; max and exp then run unmasked
+          // (exp2(-inf) = 0); whole-chunk-valid rows skip the masking
+          const uint32_t m = mk[cch];
+          if (m != 0xffffffffu) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, ((mk[cch] >> j) & 1u) ? sv[cch][j] : -INFINITY);
+            for (int j = 0; j < 32; ++j) sv[cch][j] = ((m >> j) & 1u) ? sv[cch][j] : -INFINITY;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, sv[cch][j]);
         }
       }
       pmax[wg * BM + row] = tmax;
@@ -459,11 +466,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t pk[32];  // this thread's 64 bf16 of P(i): TMEM columns s*128 + wg*32 + [0, 32)
 #pragma unroll
       for (int cch = 0; cch < 2; ++cch) {
-        if (live[cch]) {
+        // a row with no valid cell so far (m_ref = -inf) has P = 0 (and no NaN)
+        if (live[cch] && m_ref != -INFINITY) {
+          const float nm = -m_ref;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float a = ((mk[cch] >> j) & 1u) ? fast_exp2(fmaf(sv[cch][j], p.scale_log2, -m_ref)) : 0.f;
-            const float b = ((mk[cch] >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[cch][j + 1], p.scale_log2, -m_ref)) : 0.f;
+            const float a = fast_exp2(fmaf(sv[cch][j], p.scale_log2, nm));
+            const float b = fast_exp2(fmaf(sv[cch][j + 1], p.scale_log2, nm));
             lsum += a + b;
             pk[cch * 16 + (j >> 1)] = tc::pack_bf16(a, b);
           }
