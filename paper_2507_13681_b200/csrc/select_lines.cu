@@ -205,6 +205,12 @@ struct GreedySmem {
 
 __device__ __forceinline__ int vload(const volatile int *p) { return *p; }
 
+// spin-wait guard: a protocol bug surfaces as a launch error after ~10 s
+// instead of a hung device
+__device__ __forceinline__ void spin_guard(long long t0) {
+  if (clock64() - t0 > 20000000000LL) __trap();
+}
+
 template <typename Cells>
 __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
                                                                Picks P, int cap, Cells cells, int32_t *n_final,
@@ -287,6 +293,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
           while (n - fin_seen >= RING) {  // ring full: finalizer behind
             __nanosleep(64);
             fin_seen = fin_pos;
+            spin_guard(tw);
           }
           wait_cycles += clock64() - tw;
         }
@@ -342,7 +349,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       while (true) {
         const int slot = j % RING;
         int ready;
+        const long long tw = clock64();
         while ((ready = vload(S.r_seq + slot)) != j + 1) {
+          spin_guard(tw);
           if (prod_done) {
             __threadfence_block();
             if (j >= n_prod) break;
@@ -380,7 +389,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       j = __shfl_sync(0xffffffffu, j, 0);
       bool ok = false;
       if (lane == 0) {
+        const long long tw = clock64();
         while (true) {
+          spin_guard(tw);
           if (j < n_prod) { ok = true; break; }
           if (j >= stop_at) break;
           if (prod_done) {  // the last n_prod store precedes prod_done: re-read it after the flag
