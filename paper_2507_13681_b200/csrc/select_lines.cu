@@ -206,10 +206,17 @@ struct GreedySmem {
 __device__ __forceinline__ int vload(const volatile int *p) { return *p; }
 
 // spin-wait guard: a protocol bug surfaces as a launch error after ~10 s
-// instead of a hung device
-__device__ __forceinline__ void spin_guard(long long t0) {
-  if (clock64() - t0 > 20000000000LL) __trap();
-}
+// instead of a hung device (the clock is read once every 1024 polls)
+struct SpinGuard {
+  long long t0 = -1;
+  unsigned n = 0;
+  __device__ __forceinline__ void tick() {
+    if ((++n & 1023u) != 0u) return;
+    const long long now = clock64();
+    if (t0 < 0) t0 = now;
+    else if (now - t0 > 20000000000LL) __trap();
+  }
+};
 
 template <typename Cells>
 __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
@@ -290,10 +297,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         if (n - fin_seen >= RING) {
           fin_seen = fin_pos;
           const long long tw = clock64();
+          SpinGuard guard;
           while (n - fin_seen >= RING) {  // ring full: finalizer behind
             __nanosleep(64);
             fin_seen = fin_pos;
-            spin_guard(tw);
+            guard.tick();
           }
           wait_cycles += clock64() - tw;
         }
@@ -349,9 +357,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       while (true) {
         const int slot = j % RING;
         int ready;
-        const long long tw = clock64();
+        SpinGuard guard;
         while ((ready = vload(S.r_seq + slot)) != j + 1) {
-          spin_guard(tw);
+          guard.tick();
           if (prod_done) {
             __threadfence_block();
             if (j >= n_prod) break;
@@ -389,9 +397,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       j = __shfl_sync(0xffffffffu, j, 0);
       bool ok = false;
       if (lane == 0) {
-        const long long tw = clock64();
+        SpinGuard guard;
         while (true) {
-          spin_guard(tw);
+          guard.tick();
           if (j < n_prod) { ok = true; break; }
           if (j >= stop_at) break;
           if (prod_done) {  // the last n_prod store precedes prod_done: re-read it after the flag
