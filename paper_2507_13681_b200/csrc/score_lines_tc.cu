@@ -19,8 +19,16 @@
 // far below the fp32 error of P itself. Maxima use integer atomicMax on the
 // (non-negative) float bits.
 
+#include <cuda.h>
+
 #include "ls_common.cuh"
 #include "tc_common.cuh"
+
+namespace ls {
+// bf16 [heads][rows][d] tensor map, box 64 columns x 128 rows, 128-B swizzle (vs_attention_ws.cu)
+int make_tmap_bf16_3d(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
+                      int64_t head_stride_el);
+}
 
 namespace ls {
 namespace k1tc {
@@ -53,7 +61,7 @@ struct StatsSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = BM * D * 2;
   static constexpr int OFF_MISC = OFF_K + 2 * BN * D * 2;
-  static constexpr int TOTAL = OFF_MISC + 1024 + 1024;
+  static constexpr int TOTAL = OFF_MISC + 1024 + 64 + 1024;  // (+ TMA / s_empty barriers at MISC + 1024)
 };
 
 template <int D>
@@ -116,6 +124,16 @@ __device__ __forceinline__ void load_k(const Params &p, unsigned char *smem, int
   tc::cp_async_commit();
 }
 
+// K rows [c0, c0 + 128) of kv head `kv` by TMA (rows past n_total read as zero)
+template <int D>
+__device__ __forceinline__ void tma_k(const CUtensorMap *tm, unsigned char *smem, int off_k, int buf, uint64_t *full,
+                                      int c0, int kv) {
+  tc::mbar_expect_tx(full, BN * D * 2);
+  const uint32_t ks = tc::smem_u32(smem + off_k + buf * BN * D * 2);
+#pragma unroll
+  for (int a = 0; a < D / 64; ++a) tc::tma_load_3d(ks + a * BN * 128, tm, full, a * 64, c0, kv);
+}
+
 template <int D>
 __device__ __forceinline__ void issue_s(unsigned char *smem, int off_k, uint32_t tmem, int buf, uint64_t *mbar) {
   constexpr uint32_t IDESC = tc::make_idesc(BM, BN, false, false);
@@ -138,15 +156,21 @@ __device__ __forceinline__ void cta_sync_tc() {
 }
 
 // ------------------------------------------------------------- pass 1
+// K tiles arrive by TMA (thread 0), S = Qs K^T double-buffered in TMEM:
+// S(t+1) is issued before the threads process S(t), and a buffer is reused
+// once all 128 threads have read it (s_empty, count 128) -- no CTA barrier
+// per tile.
 template <int D>
-__global__ void __launch_bounds__(128) k1_stats_kernel(Params p) {
+__global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = StatsSmem<D>;
   unsigned char *smem =
       reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);          // s_full[2] (setup)
   uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
   int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC + 1024);   // [2] TMA
+  uint64_t *s_empty = full + 2;                                             // [2] count 128
   const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5;
   float2 *ps = p.pstats + ((static_cast<int64_t>(h) * p.n_rt + rt) * p.n_chunks + ck) * BM;
@@ -159,62 +183,79 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(Params p) {
     return;
   }
   const int c_end = min(c_begin + CHUNK, g_last + 1);
-  int nr;
-  setup<D>(p, smem, L::OFF_MISC, h, rt, nr, gs, mbar, tmem_sh);
-  const uint16_t *kbase = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
+  const int kv = h / p.group;
   const int n_tiles = (c_end - c_begin + BN - 1) / BN;
-  load_k<D>(p, smem, L::OFF_K, kbase, c_begin, 0);
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&full[b], 1);
+      tc::mbar_init(&s_empty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tc::prefetch_tmap(&tm_k);
+    for (int t = 0; t < 2 && t < n_tiles; ++t) tma_k<D>(&tm_k, smem, L::OFF_K, t, &full[t], c_begin + t * BN, kv);
+  }
+  int nr;
+  setup<D>(p, smem, L::OFF_MISC, h, rt, nr, gs, mbar, tmem_sh);  // Q rows (cp.async), TMEM, s_full barriers
   tc::cp_async_wait<0>();
   cta_sync_tc();
   const uint32_t tmem = *tmem_sh;
-  if (tid == 0) issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+  if (tid == 0) {
+    tc::mbar_wait(&full[0], 0);
+    issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+  }
   const int my_g = gs[tid];
   const bool row_ok = tid < nr;
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
   float m = -INFINITY, l = 0.f;
-  uint32_t ph0 = 0, ph1 = 0;
   for (int t = 0; t < n_tiles; ++t) {
     const int buf = t & 1;
     const int c0 = c_begin + t * BN;
-    if (t + 1 < n_tiles) load_k<D>(p, smem, L::OFF_K, kbase, c0 + BN, buf ^ 1);
-    tc::mbar_wait(&mbar[buf], buf ? ph1 : ph0);
-    if (buf) ph1 ^= 1; else ph0 ^= 1;
-    tc::fence_after_sync();
-    const int lim = min(my_g, c_end - 1) - c0;
-#pragma unroll
-    for (int cch = 0; cch < 4; ++cch) {
-      float sv[32];
-      tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv);
-      tc::tmem_wait_ld();
-      if (row_ok && lim >= cch * 32 + 31) {  // whole chunk causal: no masking
-        float tm = sv[0];
-#pragma unroll
-        for (int j = 1; j < 32; ++j) tm = fmaxf(tm, sv[j]);
-        const float mn = fmaxf(m, tm * p.scale_log2);
-        float acc = 0.f;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
-        l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
-        m = mn;
-      } else if (row_ok) {
-        float tm = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cch * 32 + j <= lim) tm = fmaxf(tm, sv[j]);
-        if (tm != -INFINITY) {
-          const float mn = fmaxf(m, tm * p.scale_log2);
-          float acc = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (cch * 32 + j <= lim) acc += fast_exp2(sv[j] * p.scale_log2 - mn);
-          l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
-          m = mn;
-        }
-      }
+    if (tid == 0 && t + 1 < n_tiles) {  // S(t+1) behind S(t): its buffer was read by every thread at t-1
+      tc::mbar_wait(&full[buf ^ 1], ((t + 1) >> 1) & 1);
+      if (t >= 1) tc::mbar_wait(&s_empty[buf ^ 1], ((t - 1) >> 1) & 1);
+      tc::fence_after_sync();
+      issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
     }
-    if (t + 1 < n_tiles) tc::cp_async_wait<0>();
-    cta_sync_tc();
-    if (t + 1 < n_tiles && tid == 0) issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+    tc::mbar_wait(&mbar[buf], (t >> 1) & 1);
+    tc::fence_after_sync();
+    if (tid == 0 && t + 2 < n_tiles)  // S(t) is done with K stage `buf`
+      tma_k<D>(&tm_k, smem, L::OFF_K, buf, &full[buf], c0 + 2 * BN, kv);
+    const int lim = min(my_g, c_end - 1) - c0;
+    float sv[128];
+#pragma unroll
+    for (int cch = 0; cch < 4; ++cch) tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv + cch * 32);
+    tc::tmem_wait_ld();
+    tc::fence_before_sync();
+    tc::mbar_arrive(&s_empty[buf]);
+    if (row_ok && lim >= 127) {  // whole tile causal: no masking
+      float t4[4] = {sv[0], sv[1], sv[2], sv[3]};
+#pragma unroll
+      for (int j = 4; j < 128; j += 4) {
+        t4[0] = fmaxf(t4[0], sv[j]);
+        t4[1] = fmaxf(t4[1], sv[j + 1]);
+        t4[2] = fmaxf(t4[2], sv[j + 2]);
+        t4[3] = fmaxf(t4[3], sv[j + 3]);
+      }
+      const float tm = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+      const float mn = fmaxf(m, tm * p.scale_log2);
+      float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < 128; ++j) a4[j & 3] += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
+      l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + ((a4[0] + a4[1]) + (a4[2] + a4[3]));
+      m = mn;
+    } else if (row_ok && lim >= 0) {
+      float tm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 128; ++j)
+        if (j <= lim) tm = fmaxf(tm, sv[j]);
+      const float mn = fmaxf(m, tm * p.scale_log2);
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 128; ++j)
+        if (j <= lim) acc += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
+      l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
+      m = mn;
+    }
   }
   ps[tid] = make_float2(row_ok ? m : -INFINITY, row_ok ? l : 0.f);
   tc::fence_before_sync();
@@ -231,7 +272,7 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(Params p) {
 // binary search; per-tile slash sums (<= ~13 cells) in fp32, accumulated per
 // chunk in fp64 shared memory.
 template <int D>
-__global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(Params p) {
+__global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = LinesSmem<D>;
   unsigned char *smem =
@@ -277,11 +318,23 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(Params p) {
     }
   }
   const int n_tiles = (c_end - c_begin + BN - 1) / BN;
-  load_k<D>(p, smem, L::OFF_K, kbase, c_begin, 0);
+  uint64_t *kfull = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC + 32);  // [2] TMA K stages
+  const int kvh = h / p.group;
+  if (tid == 0) {
+    tc::mbar_init(&kfull[0], 1);
+    tc::mbar_init(&kfull[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tc::prefetch_tmap(&tm_k);
+    tma_k<D>(&tm_k, smem, L::OFF_K, 0, &kfull[0], c_begin, kvh);
+  }
+  (void)kbase;
   tc::cp_async_wait<0>();
   cta_sync_tc();
   const uint32_t tmem = *tmem_sh;
-  if (tid == 0) issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+  if (tid == 0) {
+    tc::mbar_wait(&kfull[0], 0);
+    issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+  }
   const int g_first = gs[0];
   const int g_hi = gs[nr - 1];
   // position -> first sampled row at or after it, for positions [g_first, g_hi]
@@ -313,7 +366,8 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(Params p) {
   for (int t = 0; t < n_tiles; ++t) {
     const int buf = t & 1;
     const int c0 = c_begin + t * BN;
-    if (t + 1 < n_tiles) load_k<D>(p, smem, L::OFF_K, kbase, c0 + BN, buf ^ 1);
+    if (t + 1 < n_tiles && tid == 0)  // stage buf^1 held K(t-1), consumed by S(t-1)
+      tma_k<D>(&tm_k, smem, L::OFF_K, buf ^ 1, &kfull[buf ^ 1], c0 + BN, kvh);
     tc::mbar_wait(&mbar[buf], buf ? ph1 : ph0);
     if (buf) ph1 ^= 1; else ph0 ^= 1;
     tc::fence_after_sync();
@@ -339,9 +393,11 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(Params p) {
         }
       }
     }
-    if (t + 1 < n_tiles) tc::cp_async_wait<0>();
     cta_sync_tc();
-    if (t + 1 < n_tiles && tid == 0) issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+    if (t + 1 < n_tiles && tid == 0) {
+      tc::mbar_wait(&kfull[buf ^ 1], ((t + 1) >> 1) & 1);
+      issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+    }
     // vertical partials: four threads per column (32-row quarters)
     {
       const int j = tid & (BN - 1), qq = tid >> 7;
@@ -494,20 +550,23 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
   LS_CUDA(cudaMemsetAsync(p.vmaxb, 0, H * L->n_total * 4, st));
   LS_CUDA(cudaMemsetAsync(p.smaxb, 0, H * L->n_total * 4, st));
   dim3 grid(p.n_chunks, p.n_rt, L->n_heads);
+  CUtensorMap tmk;
+  int st_map = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride);
+  if (st_map) return st_map;
   if (L->head_dim == 128) {
     const int s1 = k1tc::StatsSmem<128>::TOTAL, s2 = k1tc::LinesSmem<128>::TOTAL;
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    k1tc::k1_stats_kernel<128><<<grid, 128, s1, st>>>(p);
+    k1tc::k1_stats_kernel<128><<<grid, 128, s1, st>>>(tmk, p);
     LS_LAUNCH_CHECK("k1_stats_kernel");
-    k1tc::k1_lines_kernel<128><<<grid, k1tc::LINES_THREADS, s2, st>>>(p);
+    k1tc::k1_lines_kernel<128><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
   } else {
     const int s1 = k1tc::StatsSmem<64>::TOTAL, s2 = k1tc::LinesSmem<64>::TOTAL;
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    k1tc::k1_stats_kernel<64><<<grid, 128, s1, st>>>(p);
+    k1tc::k1_stats_kernel<64><<<grid, 128, s1, st>>>(tmk, p);
     LS_LAUNCH_CHECK("k1_stats_kernel");
-    k1tc::k1_lines_kernel<64><<<grid, k1tc::LINES_THREADS, s2, st>>>(p);
+    k1tc::k1_lines_kernel<64><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
   }
   LS_LAUNCH_CHECK("k1_lines_kernel");
   k1tc::k1_finish_kernel<<<L->n_heads, 512, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
