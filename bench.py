@@ -284,7 +284,7 @@ def main():
                            max_new=cfg["max_new"], seed=0)
     blocks = turn_blocks(cfg["input_len"], cfg["n_turns"], cfg["max_new"])
     cap = cfg["n_turns"] * (cfg["input_len"] + cfg["max_new"])
-    store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1 + shard.kv_begin)
+    store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1, kv_offset=shard.kv_begin)
     eng = SessionEngine(shape, params, cap)
     stream = torch.cuda.current_stream()
 

@@ -78,11 +78,12 @@ class QKVStore:
         self.v = v if v is not None else torch.empty((L, shape.n_kv, cap, d), dtype=torch.bfloat16, device=device)
 
     @staticmethod
-    def synthetic(shape: AttnShape, cap: int, n_ref: int | None = None, seed: int = 0, device="cuda"):
+    def synthetic(shape: AttnShape, cap: int, n_ref: int | None = None, seed: int = 0, device="cuda",
+                  kv_offset: int = 0):
         from .synth import SynthSpec, layer_qkv_torch
 
         st = QKVStore(shape, cap, device)
-        spec = SynthSpec(shape.n_q, shape.n_kv, shape.d, cap, n_ref=n_ref, seed=seed)
+        spec = SynthSpec(shape.n_q, shape.n_kv, shape.d, cap, n_ref=n_ref, seed=seed, kv_offset=kv_offset)
         for l in range(shape.n_layers):
             q, k, v = layer_qkv_torch(spec, l, device=device)
             st.q[l].copy_(q)

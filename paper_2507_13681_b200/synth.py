@@ -45,6 +45,7 @@ class SynthSpec:
     n_ref: int | None = None  # calibration length (defaults to n_pos)
     structured: bool = True
     seed: int = 0
+    kv_offset: int = 0    # global index of local kv-head 0 (head-sharded runs draw the same data)
 
     def boosts(self):
         n_ref = self.n_ref or self.n_pos
@@ -110,34 +111,43 @@ def layer_qkv_numpy(spec: SynthSpec, layer: int):
 
 def layer_qkv_torch(spec: SynthSpec, layer: int, device="cuda"):
     """Device generator, same formula (different random numbers): bf16 tensors
-    Q [n_q, n_pos, d], K/V [n_kv, n_pos, d]."""
+    Q [n_q, n_pos, d], K/V [n_kv, n_pos, d]. Every (layer, global kv head)
+    has its own generator, so a head-sharded rank (kv_offset = its first kv
+    head) draws exactly the heads an unsharded run would."""
     import torch
 
     d, n = spec.d, spec.n_pos
     group = spec.n_q // spec.n_kv
     b_loc, b_hot, b_sink = spec.boosts()
     n_ref = spec.n_ref or n
-    gen = torch.Generator(device=device)
-    gen.manual_seed((spec.seed * 1_000_003 + layer * 7919 + 17) & 0x7FFFFFFFFFFFFFFF)
-    K = torch.randn((spec.n_kv, n, d), generator=gen, device=device, dtype=torch.float32)
-    V = torch.randn((spec.n_kv, n, d), generator=gen, device=device, dtype=torch.float32)
-    Q = torch.randn((spec.n_q, n, d), generator=gen, device=device, dtype=torch.float32)
-    if spec.structured:
-        nf = min(2 * N_FEAT, d - 1)
-        p = torch.arange(n, device=device, dtype=torch.float64)
-        a = math.sqrt(b_loc * math.sqrt(d) / N_FEAT)
-        for g in range(spec.n_kv):
+    nf = min(2 * N_FEAT, d - 1)
+    p = torch.arange(n, device=device, dtype=torch.float64)
+    a = math.sqrt(b_loc * math.sqrt(d) / N_FEAT)
+    Q = torch.empty((spec.n_q, n, d), device=device, dtype=torch.bfloat16)
+    K = torch.empty((spec.n_kv, n, d), device=device, dtype=torch.bfloat16)
+    V = torch.empty((spec.n_kv, n, d), device=device, dtype=torch.bfloat16)
+    for g in range(spec.n_kv):
+        gg = spec.kv_offset + g
+        gen = torch.Generator(device=device)
+        gen.manual_seed((spec.seed * 1_000_003 + layer * 7919 + gg * 104_729 + 17) & 0x7FFFFFFFFFFFFFFF)
+        k = torch.randn((n, d), generator=gen, device=device, dtype=torch.float32)
+        v = torch.randn((n, d), generator=gen, device=device, dtype=torch.float32)
+        q = torch.randn((group, n, d), generator=gen, device=device, dtype=torch.float32)
+        if spec.structured:
             omega = torch.rand(N_FEAT, generator=gen, device=device, dtype=torch.float64) * (math.pi - 0.5) + 0.5
             ang = p[:, None] * omega[None, :]
             ph = (torch.cat([torch.cos(ang), torch.sin(ang)], dim=1) * a).to(torch.float32)[:, :nf]
-            K[g, :, :nf] += ph
-            Q[g * group:(g + 1) * group, :, :nf] += ph[None]
+            k[:, :nf] += ph
+            q[:, :, :nf] += ph[None]
             perm = torch.randperm(max(n_ref - 1, 1), generator=gen, device=device)[:N_HOT] + 1
             perm = perm[perm < n]
-            K[g, perm, d - 1] += b_hot * math.sqrt(d) / S_Q
-            K[g, 0, d - 1] += b_sink * math.sqrt(d) / S_Q
-        Q[:, :, d - 1] += S_Q
-    return Q.to(torch.bfloat16), K.to(torch.bfloat16), V.to(torch.bfloat16)
+            k[perm, d - 1] += b_hot * math.sqrt(d) / S_Q
+            k[0, d - 1] += b_sink * math.sqrt(d) / S_Q
+            q[:, :, d - 1] += S_Q
+        K[g] = k.to(torch.bfloat16)
+        V[g] = v.to(torch.bfloat16)
+        Q[g * group:(g + 1) * group] = q.to(torch.bfloat16)
+    return Q, K, V
 
 
 def checksum(*arrays) -> str:
