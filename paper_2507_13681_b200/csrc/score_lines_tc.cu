@@ -61,7 +61,7 @@ struct StatsSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = BM * D * 2;
   static constexpr int OFF_MISC = OFF_K + 2 * BN * D * 2;
-  static constexpr int TOTAL = OFF_MISC + 1024 + 64 + 1024;  // (+ TMA / s_empty barriers at MISC + 1024)
+  static constexpr int TOTAL = OFF_MISC + 1024 + 64 + 1024 + 1024;  // (+ TMA / s_empty barriers, halves' (m, l))
 };
 
 template <int D>
@@ -156,12 +156,15 @@ __device__ __forceinline__ void cta_sync_tc() {
 }
 
 // ------------------------------------------------------------- pass 1
-// K tiles arrive by TMA (thread 0), S = Qs K^T double-buffered in TMEM:
-// S(t+1) is issued before the threads process S(t), and a buffer is reused
-// once all 128 threads have read it (s_empty, count 128) -- no CTA barrier
-// per tile.
+// 256 threads, two per sampled row (TMEM lane = row, warps 0-3 columns 0-63,
+// warps 4-7 columns 64-127), each with its own online (max, sum) over its
+// half of every tile, merged once at the end. K tiles arrive by TMA (thread
+// 0), S = Qs K^T double-buffered in TMEM: S(t+1) is issued before the threads
+// process S(t), and a buffer is reused once all threads have read it
+// (s_empty, count 256) -- no CTA barrier per tile.
+constexpr int STATS_THREADS = 256;
 template <int D>
-__global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
+__global__ void __launch_bounds__(STATS_THREADS) k1_stats_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = StatsSmem<D>;
   unsigned char *smem =
@@ -170,16 +173,18 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ C
   uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
   int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC + 1024);   // [2] TMA
-  uint64_t *s_empty = full + 2;                                             // [2] count 128
+  uint64_t *s_empty = full + 2;                                             // [2] count STATS_THREADS
+  float2 *half = reinterpret_cast<float2 *>(smem + L::OFF_MISC + 1024 + 64);  // [128] second half's (m, l)
   const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int row = tid & (BM - 1), hc = tid >> 7;  // column half
   float2 *ps = p.pstats + ((static_cast<int64_t>(h) * p.n_rt + rt) * p.n_chunks + ck) * BM;
   // chunk bounds against this row tile's causal extent
   const int r_last = min(p.n_s, (rt + 1) * BM) - 1;
   const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
   const int c_begin = ck * CHUNK;
   if (c_begin > g_last) {
-    ps[tid] = make_float2(-INFINITY, 0.f);
+    if (tid < BM) ps[tid] = make_float2(-INFINITY, 0.f);
     return;
   }
   const int c_end = min(c_begin + CHUNK, g_last + 1);
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ C
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&full[b], 1);
-      tc::mbar_init(&s_empty[b], 128);
+      tc::mbar_init(&s_empty[b], STATS_THREADS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tc::prefetch_tmap(&tm_k);
@@ -203,9 +208,9 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ C
     tc::mbar_wait(&full[0], 0);
     issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
   }
-  const int my_g = gs[tid];
-  const bool row_ok = tid < nr;
-  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  const int my_g = gs[row];
+  const bool row_ok = row < nr;
+  const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
   float m = -INFINITY, l = 0.f;
   for (int t = 0; t < n_tiles; ++t) {
     const int buf = t & 1;
@@ -220,17 +225,17 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ C
     tc::fence_after_sync();
     if (tid == 0 && t + 2 < n_tiles)  // S(t) is done with K stage `buf`
       tma_k<D>(&tm_k, smem, L::OFF_K, buf, &full[buf], c0 + 2 * BN, kv);
-    const int lim = min(my_g, c_end - 1) - c0;
-    float sv[128];
-#pragma unroll
-    for (int cch = 0; cch < 4; ++cch) tc::tmem_ld32(tmem + buf * 128 + lane_base + cch * 32, sv + cch * 32);
+    const int lim = min(my_g, c_end - 1) - c0 - 64 * hc;  // last valid column of this thread's 64
+    float sv[64];
+    tc::tmem_ld32(tmem + buf * 128 + lane_base + 64 * hc, sv);
+    tc::tmem_ld32(tmem + buf * 128 + lane_base + 64 * hc + 32, sv + 32);
     tc::tmem_wait_ld();
     tc::fence_before_sync();
     tc::mbar_arrive(&s_empty[buf]);
-    if (row_ok && lim >= 127) {  // whole tile causal: no masking
+    if (row_ok && lim >= 63) {  // whole half-tile causal: no masking
       float t4[4] = {sv[0], sv[1], sv[2], sv[3]};
 #pragma unroll
-      for (int j = 4; j < 128; j += 4) {
+      for (int j = 4; j < 64; j += 4) {
         t4[0] = fmaxf(t4[0], sv[j]);
         t4[1] = fmaxf(t4[1], sv[j + 1]);
         t4[2] = fmaxf(t4[2], sv[j + 2]);
@@ -240,24 +245,34 @@ __global__ void __launch_bounds__(128) k1_stats_kernel(const __grid_constant__ C
       const float mn = fmaxf(m, tm * p.scale_log2);
       float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int j = 0; j < 128; ++j) a4[j & 3] += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
+      for (int j = 0; j < 64; ++j) a4[j & 3] += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
       l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + ((a4[0] + a4[1]) + (a4[2] + a4[3]));
       m = mn;
     } else if (row_ok && lim >= 0) {
       float tm = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < 128; ++j)
+      for (int j = 0; j < 64; ++j)
         if (j <= lim) tm = fmaxf(tm, sv[j]);
       const float mn = fmaxf(m, tm * p.scale_log2);
       float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < 128; ++j)
+      for (int j = 0; j < 64; ++j)
         if (j <= lim) acc += fast_exp2(fmaf(sv[j], p.scale_log2, -mn));
       l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
       m = mn;
     }
   }
-  ps[tid] = make_float2(row_ok ? m : -INFINITY, row_ok ? l : 0.f);
+  // merge the two column halves of each row (half 0 + half 1, fixed order)
+  if (hc == 1) half[row] = make_float2(m, l);
+  __syncthreads();
+  if (hc == 0) {
+    const float2 o = half[row];
+    const float mn = fmaxf(m, o.x);
+    float lt = 0.f;
+    if (m != -INFINITY) lt += l * fast_exp2(m - mn);
+    if (o.x != -INFINITY) lt += o.y * fast_exp2(o.x - mn);
+    ps[row] = make_float2(row_ok ? mn : -INFINITY, row_ok ? lt : 0.f);
+  }
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
@@ -557,14 +572,14 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
     const int s1 = k1tc::StatsSmem<128>::TOTAL, s2 = k1tc::LinesSmem<128>::TOTAL;
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    k1tc::k1_stats_kernel<128><<<grid, 128, s1, st>>>(tmk, p);
+    k1tc::k1_stats_kernel<128><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
     LS_LAUNCH_CHECK("k1_stats_kernel");
     k1tc::k1_lines_kernel<128><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
   } else {
     const int s1 = k1tc::StatsSmem<64>::TOTAL, s2 = k1tc::LinesSmem<64>::TOTAL;
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    k1tc::k1_stats_kernel<64><<<grid, 128, s1, st>>>(tmk, p);
+    k1tc::k1_stats_kernel<64><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
     LS_LAUNCH_CHECK("k1_stats_kernel");
     k1tc::k1_lines_kernel<64><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
   }
