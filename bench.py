@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
     return ap.parse_args()
 
 
@@ -391,6 +392,8 @@ def main():
             dec_roof["share_of_timed"] = round(sum(per[k]) / total_ms, 4)
             break
 
+    dense = None if args.no_dense else dense_baseline(cfg, store, blocks, shard, ttft)
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, eng, store, blocks, shard, gather)
@@ -407,7 +410,7 @@ def main():
             "decode_tokens_per_s": round(tok_s, 2),
             "prefill_ms_per_turn": round(ttft, 3), "decode_ms_per_turn": round(decode_ms / n_prefills, 3),
             "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-            "decode_roofline": dec_roof, "prefill_roofline": pre_roof}
+            "decode_roofline": dec_roof, "prefill_roofline": pre_roof, "dense_baseline": dense}
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -467,6 +470,39 @@ def roofline(per, cfg, eng, store, blocks, peaks):
         res["traffic"] = tr["dram_bytes_per_launch"]
         res["traffic_src"] = tr["source"]
     return res
+
+
+def dense_baseline(cfg, store, blocks, shard, sparse_ttft):
+    """the same turn blocks through dense causal attention
+    (scaled_dot_attention, tensor_ops.py:104-127; K5 in dense mode) -- the
+    speed-up denominator of the sparse prefill. Outside the timed region, one
+    pass after a warm-up, CUDA events on the launching stream."""
+    import torch
+
+    from paper_2507_13681_b200.engine import AttnShape, SessionEngine, SessionParams
+    from paper_2507_13681_b200.kvcompress import CompressionConfig
+
+    shape = AttnShape(cfg["n_layers"], shard.n_q_local, shard.n_kv_local, cfg["d"])
+    cap = store.cap
+    eng = SessionEngine(shape, SessionParams(mode="dense", comp=CompressionConfig(budget=None),
+                                             max_new=cfg["max_new"]), cap)
+    stream = torch.cuda.current_stream()
+    ro, n_new = blocks[0]
+    eng.prefill(store, 0, ro, n_new)  # warm-up
+    per_turn = []
+    for t, (ro, n_new) in enumerate(blocks):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.prefill(store, t, ro, n_new)
+        e1.record(stream)
+        per_turn.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in per_turn]
+    dense_cells = sum(n * ro + n * (n + 1) // 2 for ro, n in blocks) * shard.n_q_local * cfg["n_layers"]
+    tflops = 4.0 * cfg["d"] * dense_cells / (sum(ms) * 1e-3) / 1e12
+    return {"ttft_ms_per_turn": [round(x, 3) for x in ms], "ttft_ms": round(statistics.mean(ms), 3),
+            "sparse_speedup": round(statistics.mean(ms) / sparse_ttft, 3), "dense_tflops": round(tflops, 1),
+            "note": "dense causal attention of the same turn blocks (K5 dense mode, all layers), one pass"}
 
 
 def run_e2e(args, cfg, eng, store, blocks, shard, gather):

@@ -44,6 +44,7 @@ namespace dec {
 constexpr int K6_THREADS = 128;
 constexpr int K7_THREADS = 1024;
 constexpr int K7_SMEM_CAP = 24 * 1024;  // ids accumulated in shared memory (fp64) up to this length
+constexpr int K7_CAND_CAP = 4096;       // touched ids listed in shared memory (radix + ranking over the list)
 
 __device__ __forceinline__ int64_t head_row(const ls_decode_stack &S, int layer, int h) {
   return static_cast<int64_t>(layer) * S.n_heads + h;
@@ -418,6 +419,27 @@ __device__ double block_sum_double(double v, double *sh) {
   return tot;
 }
 
+// exclusive prefix of v over the block (thread order); *tot = block total
+__device__ int block_excl_scan(int v, int *sh, int *tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) sh[wid] = incl;
+  __syncthreads();
+  int before = 0, all = 0;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+    if (i < wid) before += sh[i];
+    all += sh[i];
+  }
+  *tot = all;
+  return before + incl - v;
+}
+
 __device__ int block_rank(int flag, int *sh, int *tot) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned b = __ballot_sync(0xffffffffu, flag);
@@ -475,6 +497,27 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   int cnt = 0;
   for (int i = threadIdx.x; i < words; i += blockDim.x) cnt += __popc(touched[i]);
   const int n_cand = block_sum_int(cnt, shi);
+  // after the first event only ~B + W ids are touched: list them (id order)
+  // and run the radix passes and the ranking over the list, not all positions
+  int32_t *cand = reinterpret_cast<int32_t *>(smem7 + static_cast<size_t>(K7_SMEM_CAP) * 8 + K7_SMEM_CAP / 8 + 64);
+  const bool use_list = use_smem && n_cand <= K7_CAND_CAP;
+  if (use_list) {
+    int base_c = 0;
+    for (int w0 = 0; w0 < words; w0 += blockDim.x) {
+      const int w = w0 + threadIdx.x;
+      uint32_t x = w < words ? touched[w] : 0u;
+      int tot;
+      int pos = base_c + block_excl_scan(__popc(x), shi, &tot);
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        cand[pos++] = w * 32 + b;
+      }
+      base_c += tot;
+    }
+    __syncthreads();
+  }
+  const int n_iter = use_list ? n_cand : length;  // loop domain: list entries or positions
   unsigned long long prefix = 0ull, pmask = 0ull;
   int need = budget;
   const bool take_all = budget >= n_cand;
@@ -482,8 +525,9 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
-      for (int i = threadIdx.x; i < length; i += blockDim.x) {
-        if (!((touched[i >> 5] >> (i & 31)) & 1u)) continue;
+      for (int k = threadIdx.x; k < n_iter; k += blockDim.x) {
+        const int i = use_list ? cand[k] : k;
+        if (!use_list && !((touched[i >> 5] >> (i & 31)) & 1u)) continue;
         const unsigned long long key = dkey(acc[i]);
         if ((key & pmask) != prefix) continue;
         atomicAdd(&hist[(key >> shift) & 0xff], 1);
@@ -531,11 +575,12 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   double tot_mass = 0.0, kept_mass = 0.0;
   int in_window_picked = 0;
   const int lo = max(0, length - S.window);
-  for (int i0 = 0; i0 < length; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
+  for (int i0 = 0; i0 < n_iter; i0 += blockDim.x) {
+    const int k = i0 + threadIdx.x;
+    const int i = use_list ? (k < n_iter ? cand[k] : length) : k;
     int is_t = 0, is_eq = 0, is_gt = 0;
     double scv = 0.0;
-    if (i < length && ((touched[i >> 5] >> (i & 31)) & 1u)) {
+    if (i < length && (use_list || ((touched[i >> 5] >> (i & 31)) & 1u))) {
       is_t = 1;
       scv = acc[i];
       if (!take_all) {
@@ -744,7 +789,8 @@ extern "C" int ls_decode_event(const ls_decode_stack *S, int32_t budget, int32_t
     acc = cv.take<double>(static_cast<size_t>(S->n_layers) * S->n_heads * S->row_cap);
     touched = cv.take<uint32_t>(static_cast<size_t>(S->n_layers) * S->n_heads * ((S->row_cap + 31) / 32));
   }
-  const size_t dyn = smem ? static_cast<size_t>(dec::K7_SMEM_CAP) * 8 + dec::K7_SMEM_CAP / 8 + 64 : 0;
+  const size_t dyn =
+      smem ? static_cast<size_t>(dec::K7_SMEM_CAP) * 8 + dec::K7_SMEM_CAP / 8 + 64 + dec::K7_CAND_CAP * 4 : 0;
   if (dyn > 48 * 1024)
     LS_CUDA(cudaFuncSetAttribute(dec::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
   dec::select_kernel<<<dim3(S->n_heads, S->n_layers), dec::K7_THREADS, dyn, st>>>(*S, budget, acc, touched, smem ? 1 : 0,

@@ -15,7 +15,7 @@ for s in $STAGES; do
     tests)  timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/tests_gpu.log 2>&1; echo "tests rc=$?"; tail -3 $OUT/tests_gpu.log;;
     smoke)  timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > $OUT/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.log;;
     bench)  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json; tail -5 $OUT/bench.err;;
-    benchq) timeout 600 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json; tail -5 $OUT/bench.err;;
+    benchq) timeout 600 python bench.py --no-cpu-baseline --no-dense > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json; tail -5 $OUT/bench.err;;
     ref)    timeout 900 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?"; cat $OUT/bench_ref.json; tail -3 $OUT/bench_ref.err;;
     launches) timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:$OURS" -c 15000 --csv \
                 --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
