@@ -89,20 +89,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA/ALU pipes (FA4-style relief for the 16/clk/SM
-// MUFU unit): x = n + f, f in [-0.5, 0.5], 2^f by a degree-3 least-squares
-// polynomial (max relative error 1.4e-4), n added to the exponent field;
-// x < -125 (incl. -inf) gives 0.
-__device__ __forceinline__ float exp2_poly(float x) {
-  const float xc = fmaxf(x, -125.f);
-  const float t = xc + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low mantissa bits
-  const float f = xc - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05502927f, f, 0.24225698f), f, 0.69325305f), f, 0.99995134f);
-  const int n = __float_as_int(t) - 0x4B400000;
-  const float r = __int_as_float(__float_as_int(p) + (n << 23));
-  return x < -125.f ? 0.f : r;
-}
-
 // first index i in [0, n) with a[i] >= x (a sorted ascending)
 template <typename T>
 __device__ __forceinline__ int lower_bound_dev(const T *a, int n, T x) {

@@ -472,9 +472,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (live[cch] && m_ref != -INFINITY) {
           const float nm = -m_ref;
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {  // half the exps on MUFU, half on the FMA pipe
+          for (int j = 0; j < 32; j += 2) {
             const float a = fast_exp2(fmaf(sv[cch][j], p.scale_log2, nm));
-            const float b = exp2_poly(fmaf(sv[cch][j + 1], p.scale_log2, nm));
+            const float b = fast_exp2(fmaf(sv[cch][j + 1], p.scale_log2, nm));
             lsum += a + b;
             pk[cch * 16 + (j >> 1)] = tc::pack_bf16(a, b);
           }
