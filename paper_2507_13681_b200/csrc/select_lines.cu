@@ -269,78 +269,152 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
 
   if (warp == 0) {
     // ================================================= producer (chain)
-    if (lane == 0) {
-      int s_idx = 0, v_idx = 0, n = 0;
-      double ol_s = 0.0, ol_v = 0.0, approx = 0.0;
-      bool go = 0.0 < target - EPS;  // the while condition before any pick
-      // heads of both lists in registers; only the advanced one is reloaded
-      double ws = 0.0, mxs = 0.0, wv = 0.0, mxv = 0.0;
-      int ls = 0, lv = 0, is = 0, iv = 0;
-      auto load_head = [&](int kind, int i, double &w, double &mx, int &len, int &ix) {
-        if (i >= n_total) return;
-        if (i < win) {
-          w = S.w[kind][i]; mx = S.mx[kind][i]; len = S.len[kind][i]; ix = S.idx[kind][i];
-        } else {
-          const int64_t g = lb + static_cast<int64_t>(kind) * n_total + i;
-          w = L.w[g]; mx = L.mx[g]; len = L.len[g]; ix = L.idx[g];
-        }
-      };
-      load_head(0, 0, ws, mxs, ls, is);
-      load_head(1, 0, wv, mxv, lv, iv);
-      int stop_seen = 0x7fffffff, fin_seen = 0;
-      long long wait_cycles = 0;
-      while (go) {
-        const bool has_s = s_idx < n_total, has_v = v_idx < n_total;
-        if ((!has_s && !has_v) || n >= cap) break;
-        if ((n & 15) == 0) stop_seen = stop_at;  // polled every 16 picks
-        if (n >= stop_seen) break;
-        if (n - fin_seen >= RING) {
-          fin_seen = fin_pos;
-          const long long tw = clock64();
-          SpinGuard guard;
-          while (n - fin_seen >= RING) {  // ring full: finalizer behind
-            __nanosleep(64);
-            fin_seen = fin_pos;
-            guard.tick();
-          }
-          wait_cycles += clock64() - tw;
-        }
-        bool take_slash;
-        if (!has_s) {
-          take_slash = false;
-        } else if (!has_v) {
-          take_slash = true;
-        } else {  // |V| = v_idx, |S| = s_idx (prefill.py:206-207)
-          take_slash = take_slash_decision(ws - ol_v, max(1, ls - v_idx), wv - ol_s, max(1, lv - s_idx));
-        }
-        int32_t code, other;
-        double wl;
-        if (take_slash) {
-          wl = ws;
-          approx += ws - ol_v;
-          ol_s += mxs;
-          code = is;
-          other = v_idx;
-          ++s_idx;
-          load_head(0, s_idx, ws, mxs, ls, is);
-        } else {
-          wl = wv;
-          approx += wv - ol_s;
-          ol_v += mxv;
-          code = iv | static_cast<int32_t>(0x80000000u);
-          other = s_idx;
-          ++v_idx;
-          load_head(1, v_idx, wv, mxv, lv, iv);
-        }
-        const int slot = n % RING;
-        S.r_code[slot] = code;
-        S.r_other[slot] = other;
-        S.r_w[slot] = wl;
-        S.r_approx[slot] = approx;
-        __threadfence_block();
-        n_prod = ++n;
-        go = approx < target - EPS;  // the chain stops at the approx target
+    // Run speculation: most picks come in runs of one kind. While kind R is
+    // being picked, the other kind's head, ol_other, and its count are
+    // fixed, and the R-side state after j more R picks follows from
+    // sequential folds over the next R heads. Each round the warp evaluates
+    // the decisions for the next K picks of kind R in parallel (lane j = "j R
+    // picks taken"), the folds being computed redundantly by every lane in
+    // the reference's order (bit-identical approx / ol), then takes the
+    // longest prefix of R picks plus the O pick that breaks the run.
+    int s_idx = 0, v_idx = 0, n = 0, R = 1, K = 8;
+    double ol_s = 0.0, ol_v = 0.0, approx = 0.0;
+    bool go = 0.0 < target - EPS;  // the while condition before any pick
+    int stop_seen = 0x7fffffff, fin_seen = 0;
+    long long wait_cycles = 0;
+    auto head = [&](int kind, int i, double &w, double &mx, int &len, int &ix) {
+      if (i >= n_total) {
+        w = 0.0; mx = 0.0; len = 0; ix = 0;
+      } else if (i < win) {
+        w = S.w[kind][i]; mx = S.mx[kind][i]; len = S.len[kind][i]; ix = S.idx[kind][i];
+      } else {
+        const int64_t g = lb + static_cast<int64_t>(kind) * n_total + i;
+        w = L.w[g]; mx = L.mx[g]; len = L.len[g]; ix = L.idx[g];
       }
+    };
+    while (go) {
+      if ((s_idx >= n_total && v_idx >= n_total) || n >= cap) break;
+      stop_seen = __shfl_sync(0xffffffffu, lane == 0 ? stop_at : 0, 0);  // one read: the warp must agree
+      if (n >= stop_seen) break;
+      int stopped = 0;
+      if (lane == 0 && n + 33 - fin_seen > RING) {
+        fin_seen = fin_pos;
+        const long long tw = clock64();
+        SpinGuard guard;
+        while (n + 33 - fin_seen > RING) {  // ring full: finalizer behind
+          if (stop_at <= n) {  // the finalizer has stopped the plan: it will not free the ring
+            stopped = 1;
+            break;
+          }
+          __nanosleep(64);
+          fin_seen = fin_pos;
+          guard.tick();
+        }
+        wait_cycles += clock64() - tw;
+      }
+      if (__shfl_sync(0xffffffffu, stopped, 0)) break;
+      fin_seen = __shfl_sync(0xffffffffu, fin_seen, 0);
+      const int O = 1 - R;
+      const int base_R = R ? v_idx : s_idx, base_O = R ? s_idx : v_idx;
+      double wR, mxR, wO, mxO;
+      int lR, iR, lO, iO;
+      head(R, base_R + lane, wR, mxR, lR, iR);
+      head(O, base_O, wO, mxO, lO, iO);
+      const double olR0 = R ? ol_v : ol_s, olO = R ? ol_s : ol_v;
+      // folds in reference order: state before R pick j (ol_R, approx)
+      double my_ol = olR0, my_ap = approx, ol_run = olR0, ap_run = approx;
+      for (int i = 0; i < K; ++i) {
+        if (lane == i) { my_ol = ol_run; my_ap = ap_run; }
+        const double wi = __shfl_sync(0xffffffffu, wR, i);
+        const double mi = __shfl_sync(0xffffffffu, mxR, i);
+        ap_run += wi - olO;  // approx += w - ol_other (prefill.py:210, 216)
+        ol_run += mi;        // ol_R += max_cell (prefill.py:212, 218)
+      }
+      // decision at (j = lane) R picks taken
+      const int sj = R ? s_idx : s_idx + lane, vj = R ? v_idx + lane : v_idx;
+      const bool has_s = sj < n_total, has_v = vj < n_total;
+      bool take_slash;
+      if (!has_s) {
+        take_slash = false;
+      } else if (!has_v) {
+        take_slash = true;
+      } else if (R) {  // vertical run: slash side fixed, ol_v = my_ol
+        take_slash = take_slash_decision(wO - my_ol, max(1, lO - vj), wR - olO, max(1, lR - sj));
+      } else {         // slash run: vertical side fixed, ol_s = my_ol
+        take_slash = take_slash_decision(wR - olO, max(1, lR - vj), wO - my_ol, max(1, lO - sj));
+      }
+      const bool exists = has_s || has_v;
+      const bool takes_R = exists && (take_slash == (R == 0));
+      const double ap_after = my_ap + (wR - olO);  // approx after this R pick
+      const bool stops = takes_R && !(ap_after < target - EPS);
+      // run = leading lanes (< K) taking R; cut after the first approx stop, at cap
+      const unsigned not_r = __ballot_sync(0xffffffffu, !takes_R || lane >= K);
+      int f = not_r ? __ffs(not_r) - 1 : 32;
+      const unsigned st_b = __ballot_sync(0xffffffffu, stops && lane < f);
+      bool chain_end = false;
+      if (st_b) {
+        f = __ffs(st_b);
+        chain_end = true;
+      }
+      if (n + f >= cap) {
+        f = cap - n;
+        chain_end = true;
+      }
+      if (lane < f) {  // publish the R picks
+        const int slot = (n + lane) % RING;
+        S.r_code[slot] = R ? (iR | static_cast<int32_t>(0x80000000u)) : iR;
+        S.r_other[slot] = base_O;
+        S.r_w[slot] = wR;
+        S.r_approx[slot] = ap_after;
+      }
+      // state after the f R picks (lane f's "before" state)
+      const double ol_f = __shfl_sync(0xffffffffu, my_ol, f & 31);
+      const double ap_f = __shfl_sync(0xffffffffu, my_ap, f & 31);
+      const bool run_broke = !chain_end && f < K;           // lane f decided for O
+      const bool o_exists = R ? (s_idx < n_total) : (v_idx < n_total);
+      const bool exists_f = __shfl_sync(0xffffffffu, exists ? 1 : 0, f & 31);
+      double ol_R = f == 0 ? olR0 : (f < 32 ? ol_f : ol_run), ap = f == 0 ? approx : (f < 32 ? ap_f : ap_run);
+      if (f == K && K < 32) {  // whole window taken: fold state after K picks
+        ol_R = ol_run;
+        ap = ap_run;
+      }
+      int np = f;
+      bool o_pick = run_broke && o_exists && exists_f;
+      if (o_pick) {  // the O pick that breaks the run (ol_R, |R| after the f R picks)
+        ap += wO - ol_R;
+        if (lane == 0) {
+          const int slot = (n + f) % RING;
+          S.r_code[slot] = O ? (iO | static_cast<int32_t>(0x80000000u)) : iO;
+          S.r_other[slot] = base_R + f;
+          S.r_w[slot] = wO;
+          S.r_approx[slot] = ap;
+        }
+        np = f + 1;
+        if (!(ap < target - EPS)) chain_end = true;
+      }
+      __syncwarp();
+      n += np;
+      if (lane == 0) {
+        __threadfence_block();
+        n_prod = n;
+      }
+      // advance the state
+      if (R) { v_idx += f; ol_v = ol_R; } else { s_idx += f; ol_s = ol_R; }
+      if (o_pick) {
+        if (R) { ++s_idx; ol_s += mxO; } else { ++v_idx; ol_v += mxO; }
+      }
+      approx = ap;
+      if (chain_end || np == 0) go = false;
+      if (!(approx < target - EPS)) go = false;
+      // next window: keep speculating on R while its runs are long
+      if (f >= 2) {
+        K = f >= K ? min(32, 2 * K) : max(4, min(32, 2 * f + 2));
+      } else {
+        R = 1 - R;
+        K = 4;
+      }
+    }
+    if (lane == 0) {
       __threadfence_block();
       prod_done = 1;
       if (dbg) {
