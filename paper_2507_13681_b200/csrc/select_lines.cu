@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
     }
   } else {
     // ================================================= crossing sums
-    if ((warp & 3) == 0) return;  // scheduler 0 stays free for the producer
+    // (warps 4, 8, 12 share the producer's scheduler: they are consumers too)
     while (true) {
       int j = 0;
       if (lane == 0) j = atomicAdd(&next_j, 1);
