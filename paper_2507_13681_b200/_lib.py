@@ -109,7 +109,7 @@ def check(status: int, what: str = "") -> None:
 # CUDA kernels each C-ABI entry launches (memsets/memcpys not counted);
 # bench.py reports the sum over its timed region as `gpu_launches`.
 KERNELS_PER_CALL = {
-    "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 4, "ls_greedy_dense": 5,
+    "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 5, "ls_greedy_dense": 5,
     "ls_vs_attention": 3, "ls_vs_attention_ex": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
     "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
 }

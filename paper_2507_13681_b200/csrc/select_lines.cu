@@ -27,7 +27,10 @@
 //       (prefill.py:195), coverage = min(exact / T, 1) (prefill.py:221-222).
 // K4: picks -> sorted slash / vertical id lists via bitmaps.
 
+#include <algorithm>
+
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 #include "ls_common.cuh"
 
@@ -100,6 +103,54 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_lines_kernel(const double *
       out.inv[base + idx] = o;
     }
   }
+}
+
+// K2 (device-wide): every (head, kind) list of a layer sorted at once by one
+// stable LSD radix sort over composite keys
+//   (segment << 50) | (2^50 - 1 - fixed point weight)
+// K1's line weights are exact multiples of 2^-40 below 2^10, so the 50-bit
+// fixed-point integer orders them exactly; ties keep index order (stable).
+// The whole GPU sorts, and n_total is not bounded by one SM's shared memory.
+constexpr int FIX_BITS = 50;
+
+__global__ void sort_keys_kernel(const double *v_w, const double *s_w, int H, int n_total,
+                                 unsigned long long *keys, int32_t *vals) {
+  const int64_t n = static_cast<int64_t>(2) * H * n_total;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t seg = i / n_total;  // h * 2 + kind
+    const int idx = static_cast<int>(i - seg * n_total);
+    const int h = static_cast<int>(seg >> 1), kind = static_cast<int>(seg & 1);
+    const double w = (kind == 0 ? s_w : v_w)[static_cast<int64_t>(h) * n_total + idx];
+    const unsigned long long fix = static_cast<unsigned long long>(w * 1099511627776.0);
+    keys[i] = (static_cast<unsigned long long>(seg) << FIX_BITS) | (((1ull << FIX_BITS) - 1ull) - fix);
+    vals[i] = idx;
+  }
+}
+
+template <typename MaxT>
+__global__ void sort_scatter_kernel(const unsigned long long *keys_sorted, const int32_t *vals_sorted,
+                                    const double *v_w, const MaxT *v_max, const double *s_w, const MaxT *s_max,
+                                    const int32_t *rows, int n_s, int n_total, int row_offset, int H, Lists out) {
+  extern __shared__ int pos_sh[];  // sampled positions of this head
+  const int h = blockIdx.y;
+  for (int r = threadIdx.x; r < n_s; r += blockDim.x) pos_sh[r] = row_offset + rows[static_cast<int64_t>(h) * n_s + r];
+  __syncthreads();
+  for (int kind = 0; kind < 2; ++kind) {
+    const int64_t base = (static_cast<int64_t>(h) * 2 + kind) * n_total;
+    const double *w = (kind == 0 ? s_w : v_w) + static_cast<int64_t>(h) * n_total;
+    const MaxT *mx = (kind == 0 ? s_max : v_max) + static_cast<int64_t>(h) * n_total;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n_total; o += gridDim.x * blockDim.x) {
+      const int idx = vals_sorted[base + o];
+      out.idx[base + o] = idx;
+      out.w[base + o] = w[idx];
+      out.mx[base + o] = static_cast<double>(mx[idx]);
+      out.len[base + o] = n_s - lower_bound_dev(pos_sh, n_s, idx);  // #{rows with g >= idx}, prefill.py:144,155
+      out.inv[base + idx] = o;
+    }
+  }
+  (void)keys_sorted;
+  (void)H;
 }
 
 // ------------------------------------------------------- crossing cells
@@ -662,6 +713,34 @@ inline Work carve(Carver &c, int H, int n_total) {
 
 inline size_t sort_smem() { return sizeof(typename BlockSort::TempStorage) + 4 * 16384 + 64; }
 
+inline size_t radix_temp_bytes(int H, int n_total) {
+  size_t bytes = 0;
+  const int n = 2 * H * n_total;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const unsigned long long *>(nullptr),
+                                  static_cast<unsigned long long *>(nullptr), static_cast<const int32_t *>(nullptr),
+                                  static_cast<int32_t *>(nullptr), n, 0, 64);
+  return bytes;
+}
+
+struct SortWork {
+  unsigned long long *k_in, *k_out;
+  int32_t *v_in, *v_out;
+  void *temp;
+  size_t temp_bytes;
+};
+
+inline SortWork carve_sort(Carver &c, int H, int n_total) {
+  SortWork w;
+  const size_t n = static_cast<size_t>(2) * H * n_total;
+  w.k_in = c.take<unsigned long long>(n);
+  w.k_out = c.take<unsigned long long>(n);
+  w.v_in = c.take<int32_t>(n);
+  w.v_out = c.take<int32_t>(n);
+  w.temp_bytes = radix_temp_bytes(H, n_total);
+  w.temp = c.take<unsigned char>(w.temp_bytes);
+  return w;
+}
+
 int run_tail(Work &w, int H, int n_total, double alpha, const double *total, int32_t *slash_ids,
              int32_t *vert_ids, int32_t *counts, double *coverage, double *approx, int32_t *picks_out,
              int32_t *n_picks_out, cudaStream_t st) {
@@ -685,6 +764,7 @@ using namespace ls;
 extern "C" size_t ls_select_lines_workspace(const ls_layer_desc *L, int32_t /*n_s*/) {
   Carver c(nullptr, 0);
   sel::carve(c, L->n_heads, L->n_total);
+  sel::carve_sort(c, L->n_heads, L->n_total);
   return c.off + 4096;
 }
 
@@ -695,19 +775,27 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
                                double *approx, int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
                                ls_stream_t stream) {
   LS_REQUIRE(alpha >= 0.0 && alpha <= 1.0, LS_ERR_INVALID_ALPHA, "alpha=%g outside [0, 1]", alpha);
-  LS_REQUIRE(L->n_total <= sel::SORT_CAP, LS_ERR_UNSUPPORTED, "n_total=%d exceeds the in-SM sort capacity %d",
-             L->n_total, sel::SORT_CAP);
+  LS_REQUIRE(2 * L->n_heads < (1 << (64 - sel::FIX_BITS)), LS_ERR_UNSUPPORTED, "too many heads for the sort key");
   LS_REQUIRE(ws_bytes >= ls_select_lines_workspace(L, n_s), LS_ERR_WORKSPACE, "select_lines workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int H = L->n_heads, n_total = L->n_total;
   Carver c(ws, ws_bytes);
   sel::Work w = sel::carve(c, H, n_total);
-  const size_t smem = sel::sort_smem();
-  LS_CUDA(cudaFuncSetAttribute(sel::sort_lines_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
-  sel::sort_lines_kernel<float><<<dim3(2, H), sel::SORT_THREADS, smem, st>>>(v_w, v_max, s_w, s_max, rows, n_s,
-                                                                            n_total, L->row_offset, w.lists);
-  LS_LAUNCH_CHECK("sort_lines_kernel");
+  sel::SortWork sw = sel::carve_sort(c, H, n_total);
+  {
+    const int n = 2 * H * n_total;
+    int seg_bits = 1;
+    while ((1 << seg_bits) < 2 * H) ++seg_bits;
+    sel::sort_keys_kernel<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(v_w, s_w, H, n_total, sw.k_in, sw.v_in);
+    LS_LAUNCH_CHECK("sort_keys_kernel");
+    size_t tb = sw.temp_bytes;
+    LS_CUDA(cub::DeviceRadixSort::SortPairs(sw.temp, tb, sw.k_in, sw.k_out, sw.v_in, sw.v_out, n, 0,
+                                            sel::FIX_BITS + seg_bits, st));
+    const int smem_pos = n_s * 4;
+    sel::sort_scatter_kernel<float><<<dim3(std::max(1, std::min(ceil_div(n_total, 256), 16)), H), 256, smem_pos, st>>>(
+        sw.k_out, sw.v_out, v_w, v_max, s_w, s_max, rows, n_s, n_total, L->row_offset, H, w.lists);
+    LS_LAUNCH_CHECK("sort_scatter_kernel");
+  }
   sel::RecomputeCells cells;
   cells.q = q;
   cells.k = k;

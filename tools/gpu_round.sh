@@ -6,7 +6,7 @@ set -u
 OUT=gpurun_out
 mkdir -p $OUT
 STAGES="${@:-tests smoke bench launches full}"
-OURS='^(sample_rows|k1_|score_lines|sort_lines|greedy|chain_kernel|cross_kernel|finalize_kernel|load_lists|row_of|set_bits|compact_bits|plan_bits|vert_bits|reverse_bits|gather_vert|vs_attention|plan_rows|plan_scores|plan_norm|decode_kernel|advance_kernel|select_kernel|compact_kernel|total_kernel|reduce_kernel)'
+OURS='^(sample_rows|k1_|score_lines|sort_lines|sort_keys|sort_scatter|greedy|chain_kernel|cross_kernel|finalize_kernel|load_lists|row_of|set_bits|compact_bits|plan_bits|vert_bits|reverse_bits|gather_vert|vs_attention|plan_rows|plan_scores|plan_norm|decode_kernel|advance_kernel|select_kernel|compact_kernel|total_kernel|reduce_kernel)'
 
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
 python -c 'import __graft_entry__ as g; g.build()' > $OUT/build.log 2>&1 || { tail -30 $OUT/build.log; exit 1; }
