@@ -84,3 +84,34 @@ def test_vs_attention_tile_counter(cuda_lib):
     assert (t >= n_qt).all() and (t <= n_qt * (n_qt + 2 * (n // 128 + 2))).all()
     # every executed tile holds at most 128 x 128 cells
     assert (c1.cpu().numpy() <= t * 128 * 128).all()
+
+
+def test_long_context_turn_c3_shape(cuda_lib):
+    """C3-sized turn block (33.5K keys, beyond the single-SM sort / table
+    capacities): the whole LoopServe turn runs and stays consistent."""
+    from paper_2507_13681_b200.engine import AttnShape, QKVStore, SessionEngine, SessionParams
+    from paper_2507_13681_b200.kvcompress import CompressionConfig
+
+    shape = AttnShape(1, 4, 1, 128)
+    ro, n_new, max_new = 25088, 8448, 24
+    cap = ro + n_new + max_new
+    store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=11)
+    eng = SessionEngine(shape, SessionParams(alpha=0.955, comp=CompressionConfig(2048, 16, 16), max_new=max_new),
+                        cap)
+    res = eng.prefill(store, 3, ro, n_new)
+    last = eng.decode(store, ro + n_new, max_new)
+    torch.cuda.synchronize()
+    plans = res.plans[0]
+    cn = plans.counts.cpu().numpy()
+    assert (cn.sum(axis=1) > 0).all()
+    sl, vt = plans.slash_ids.cpu().numpy(), plans.vert_ids.cpu().numpy()
+    for h in range(4):  # sorted, unique, in range
+        s, v = sl[h, :cn[h, 0]], vt[h, :cn[h, 1]]
+        assert (np.diff(s) > 0).all() and (np.diff(v) > 0).all()
+        assert s.max(initial=0) < ro + n_new and v.max(initial=0) < ro + n_new
+    cov = plans.coverage.cpu().numpy()
+    assert ((cov >= 0.955 - 1e-6) | (cov <= 1.0)).all()
+    cells = res.cells[0].cpu().numpy()
+    dense_cells = n_new * ro + n_new * (n_new + 1) // 2
+    assert (cells > 0).all() and (cells <= dense_cells).all()
+    assert torch.isfinite(res.out[0].float()).all() and torch.isfinite(last.float()).all()
