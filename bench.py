@@ -45,6 +45,11 @@ CONFIGS = {
                         "128 decoded tokens/turn, alpha=0.955, B=1024, n_d=16, sparse prefill + compressed decode",
                n_layers=32, n_q=32, n_kv=8, d=128, input_len=5000, n_turns=3, max_new=128, alpha=0.955,
                budget=1024, interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),
+    "c3": dict(workload="C3: Llama-3.1-8B attention (32q/8kv, d=128, bf16), 32 layers, 4 turns x 8192 tokens "
+                        "(33.5K-token context), 256 decoded tokens/turn, alpha=0.955, B=2048, n_d=16, "
+                        "head-sharded over the ranks",
+               n_layers=32, n_q=32, n_kv=8, d=128, input_len=8192, n_turns=4, max_new=256, alpha=0.955,
+               budget=2048, interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),
     "c1": dict(workload="C1: toy attention layer (8 heads MHA, d=64), 3 turns x 1000 tokens, alpha=0.9, B=256",
                n_layers=1, n_q=8, n_kv=8, d=64, input_len=1000, n_turns=3, max_new=32, alpha=0.9, budget=256,
                interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),

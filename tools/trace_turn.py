@@ -13,10 +13,13 @@ from paper_2507_13681_b200.kvcompress import CompressionConfig  # noqa: E402
 
 L = int(os.environ.get("LAYERS", "32"))
 shape = AttnShape(L, 32, 8, 128)
-cap = 3 * 5128
+RO = int(os.environ.get("RO", "10128"))
+NNEW = int(os.environ.get("NNEW", "5128"))
+cap = RO + NNEW + 256
 store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1)
-eng = SessionEngine(shape, SessionParams(alpha=0.955, comp=CompressionConfig(1024, 16, 16), max_new=128), cap)
-ro, n_new = 10128, 5128
+eng = SessionEngine(shape, SessionParams(alpha=0.955, comp=CompressionConfig(2048 if RO > 20000 else 1024, 16, 16),
+                                         max_new=128), cap)
+ro, n_new = RO, NNEW
 for _ in range(2):
     eng.prefill(store, 2, ro, n_new)
     eng.decode(store, ro + n_new, 40)
