@@ -31,6 +31,7 @@
 // 16-byte gather of the picked K/V rows into the contiguous per-head cache.
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -134,8 +135,10 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   const int length = S.step[0];
   const int slot = S.step[1] % S.window;
   const int group = S.n_heads / S.n_kv_heads;
-  const int kv = compressed ? unit / group : unit;
-  const int h0 = compressed ? unit : unit * G;
+  // units: q-heads when G == 1 (compressed steps, and dense steps split per
+  // q-head for parallelism), else kv-heads with their G q-heads
+  const int kv = G == 1 ? unit / group : unit;
+  const int h0 = G == 1 ? unit : unit * G;
   const Geo geo = geometry(S, layer, h0, length, compressed);
   const int per = ((geo.n_cols + n_split - 1) / n_split + K6_TILE - 1) / K6_TILE * K6_TILE;
   const int c_begin = min(geo.n_cols, split * per);
@@ -718,10 +721,13 @@ static int decode_step_impl(const ls_decode_stack *S, int32_t layer, const uint1
   const int group = S->n_heads / S->n_kv_heads;
   int r = LS_OK;
 #define LS_ARGS q, q_head_stride, q_from_archive, k_layer, v_layer
-  if (compressed) {
+  // dense steps: one unit per kv-head with its whole q-group (each K/V row read
+  // once); LS_DECODE_DENSE_PER_HEAD=1 splits them per q-head (measured slower)
+  const bool per_head = compressed || getenv("LS_DECODE_DENSE_PER_HEAD") != nullptr;
+  if (per_head) {
     r = S->head_dim == 128
-            ? launch_decode<128, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, 1, sl, out, out_bf16, pdl)
-            : launch_decode<64, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, 1, sl, out, out_bf16, pdl);
+            ? launch_decode<128, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl)
+            : launch_decode<64, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl);
   } else {
 #define LS_DENSE(DD, GG) \
   r = launch_decode<DD, GG>(S->n_kv_heads, max_cols, st, S, layer, LS_ARGS, 0, sl, out, out_bf16, pdl)
