@@ -203,8 +203,10 @@ int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t
  *   ring_n, ring_dense [hr][window] int32
  *   sel_ids  [hr][budget_cap], n_sel [hr]      picked ids (kvcompress.py:212)
  *   ck, cv   [hr][budget_cap][head_dim] bf16   compacted K/V of sel_ids
- *   partials, counters: unused since the split-K combine moved to distributed
- *                                   shared memory (kept for layout stability; may be NULL)
+ *   partials [ls_decode_partials_size() bytes] fp32 split-K partials of a decode step
+ *   counters [n_heads] int32, zeroed once: per-unit tickets (the last split combines)
+ *                      Both may be NULL: splits then combine inside one thread-block
+ *                      cluster (at most 16 splits per unit).
  *   n_a      [hr] int32  picked ids below the recent window at the current step
  *                        (written by ls_decode_event, advanced by ls_decode_advance)
  * Archive K/V of layer l, kv-head j at k_all + l*kv_layer_stride + j*kv_head_stride. */

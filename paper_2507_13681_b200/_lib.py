@@ -14,7 +14,7 @@ import threading
 from .errors import STATUS, NativeError, NativeLibraryMissing
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libloopserve_b200.so")
+LIB_PATH = os.environ.get("LS_LIB_PATH") or os.path.join(HERE, "libloopserve_b200.so")  # override: A/B builds
 
 _lock = threading.Lock()
 _lib = None

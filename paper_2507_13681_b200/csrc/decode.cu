@@ -30,6 +30,8 @@
 // K8 (all layers) replaces compact_cache (kvcompress.py:133-147): coalesced
 // 16-byte gather of the picked K/V rows into the contiguous per-head cache.
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -40,6 +42,7 @@ namespace cg = cooperative_groups;
 #include "tc_common.cuh"
 
 namespace ls {
+extern int *g_debug_buffer;  // ls_debug_set_buffer (host-mapped): per-CTA timeline records
 namespace dec {
 
 constexpr int K6_THREADS = 128;
@@ -373,6 +376,452 @@ __global__ void __launch_bounds__(K6_THREADS) decode_kernel(ls_decode_stack S, i
   }
 }
 
+// ------------------------------------------------------------------ K6 (tensor-core form)
+// The same step on the tensor pipe: at decode shapes the CUDA-core form above
+// spends ~0.25 warp-instructions per HBM byte (scalar dot products, shuffle
+// reductions, per-row softmax) and is issue-bound at ~1.4 TB/s. Here a tile
+// of 64 K/V rows arrives by TMA (128-B swizzle, one elected producer lane,
+// NST-deep mbarrier ring) and each of the 4 consumer warps owns 16 rows:
+//   S = Q K^T : mma.m16n8k16 bf16 -> fp32, A = the unit's q-heads (rows >= G
+//               zero), B = K rows by ldmatrix (K row-major == B col-major);
+//   online softmax per warp in registers (quad shuffles), raw log2 logits to
+//   the ring; P (bf16) is reused as the A fragment of
+//   O += P V    : mma.m16n8k16, B = V rows by ldmatrix.trans.
+// ~0.02 warp-instructions per byte. mma.sync (not tcgen05) on purpose: M is
+// the q-group (<= 8 rows), the kernel is HBM-bound and the tensor pipe idles.
+// Warps merge in shared memory (fixed order), splits through global partials
+// and a per-unit ticket (the last CTA combines in split order).
+constexpr int KM_MAX_SPLIT = 64;  // splits of a unit (global partials)
+
+struct KmMaps {
+  CUtensorMap ck, cv, k, v;  // compacted cache [hr][budget_cap][D]; archive [kv][rows][D] (box 64 x 64)
+};
+
+constexpr int KM_GATHER_B = 8192;  // cluster combine: [n_split][G][D + 2] partials in rank 0
+
+// NW consumer warps x 16 rows = one tile of TILE K/V rows; NG such warp
+// groups take alternate tiles (ping-pong); + one producer warp
+template <int D, int NST, int NW, int NG>
+struct KmSmem {
+  static constexpr int TILE = 16 * NW;
+  static constexpr int TILE_B = TILE * D * 2;  // one K or V tile, [D / 64][TILE rows][128 B] swizzled
+  static constexpr int OFF_V = NST * TILE_B;
+  static constexpr int OFF_BAR = 2 * NST * TILE_B;   // full[S], empty[S]
+  static constexpr int OFF_MG = OFF_BAR + 16 * NST;  // [2][8] (M, L) of the CTA / combine weights
+  static constexpr int OFF_W = OFF_MG + 2 * 8 * 4;   // [8][KM_MAX_SPLIT] split weights
+  static constexpr int OFF_GATHER = (OFF_W + 8 * KM_MAX_SPLIT * 4 + 15) / 16 * 16;
+  static constexpr int TOTAL = OFF_GATHER + KM_GATHER_B + 1024;  // + alignment slack
+  // after the tile loop the stage buffers hold the warp merge: m[W][8], l[W][8], o[W][8][D]
+  static_assert((3 * NW * NG * 8 + NW * NG * 8 * D + 8) * 4 <= 2 * NST * TILE_B, "merge area");
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t *r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t *r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// D += A B, m16n8k16 bf16 -> fp32; A rows 8-15 are zero here (a1 = a3 = 0)
+__device__ __forceinline__ void mma_16816(float *d, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+// byte offset of 16-B chunk c of tile row r in a [D / 64][TILE][128 B] 128-B-swizzled tile
+template <int TILE>
+__device__ __forceinline__ uint32_t km_off(int r, int c) {
+  return static_cast<uint32_t>((c >> 3) * (TILE * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+struct KmTile {
+  int seg_a;  // 1: compacted cache rows, 0: archive rows
+  int row0;   // first source row (compacted index, or archive position)
+  int valid;  // rows of the tile inside the working set
+  int j0;     // working-set column of the tile's row 0
+};
+// working set = [compacted 0, n_a) ++ archive [lo, lo + n_cols - n_a); tiles never straddle the two
+template <int KM_TILE>
+__device__ __forceinline__ KmTile km_tile(int t, int t_a, const Geo &geo) {
+  KmTile x;
+  if (t < t_a) {
+    x.seg_a = 1;
+    x.row0 = t * KM_TILE;
+    x.valid = min(KM_TILE, geo.n_a - x.row0);
+    x.j0 = x.row0;
+  } else {
+    const int b = (t - t_a) * KM_TILE;
+    x.seg_a = 0;
+    x.row0 = geo.lo + b;
+    x.valid = min(KM_TILE, geo.n_cols - geo.n_a - b);
+    x.j0 = geo.n_a + b;
+  }
+  return x;
+}
+
+template <int D, int G, int NST, int NW, int NG>
+__global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __grid_constant__ KmMaps maps, ls_decode_stack S,
+                                                                int layer, const uint16_t *q, int64_t q_head_stride,
+                                                                int q_from_archive, int compressed, float scale_log2,
+                                                                void *out, int out_bf16, int pdl, int ccombine,
+                                                                int *dbg) {
+  static_assert(G <= 8, "q-group rows live in rows 0-7 of the m16 tile");
+  auto gtime = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return static_cast<int>(t & 0x7fffffffull);
+  };
+  // the next layer's CTAs may launch at once: they only prefetch K/V before
+  // their griddepcontrol.wait, which returns when this grid has completed
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  int *rec = dbg ? dbg + (static_cast<int64_t>(layer) * 256 + blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
+  if (rec && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    rec[0] = static_cast<int>(smid);
+    rec[1] = gtime();
+  }
+  // a stage is only ever consumed by one warp group, so every group waits the
+  // phases of its stages in order (a group running two phases ahead on a
+  // shared barrier would see the older phase's parity as complete)
+  static_assert(NST % NG == 0, "stages per warp group");
+  using L = KmSmem<D, NST, NW, NG>;
+  constexpr int KM_TILE = L::TILE, KM_WARPS = NW * NG, KM_THREADS = (NW * NG + 1) * 32;
+  constexpr int NT = D / 8;  // n-tiles of 8 dims in O
+  extern __shared__ unsigned char km_dyn[];
+  unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(km_dyn) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + L::OFF_BAR);
+  uint64_t *empty = full + NST;
+  float *mg = reinterpret_cast<float *>(sm + L::OFF_MG);
+  float *wsc = reinterpret_cast<float *>(sm + L::OFF_W);
+  __shared__ int is_last;
+  const int split = blockIdx.x, unit = blockIdx.y, n_split = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int length = S.step[0];
+  const int slot = S.step[1] % S.window;
+  const int group = S.n_heads / S.n_kv_heads;
+  const int kv = G == 1 ? unit / group : unit;
+  const int h0 = G == 1 ? unit : unit * G;
+  const Geo geo = geometry(S, layer, h0, length, compressed);
+  const int t_a = (geo.n_a + KM_TILE - 1) / KM_TILE;
+  const int t_all = t_a + (geo.n_cols - geo.n_a + KM_TILE - 1) / KM_TILE;
+  const int t_begin = static_cast<int>(static_cast<int64_t>(t_all) * split / n_split);
+  const int t_end = static_cast<int>(static_cast<int64_t>(t_all) * (split + 1) / n_split);
+  const int n_my = t_end - t_begin;
+  const int64_t hr0 = head_row(S, layer, h0);
+
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], NW);  // the warps of the group that consumes the stage
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == KM_WARPS) {
+    // ---- producer: TMA K and V tiles of this split (independent of the previous kernel)
+    if (lane == 0 && n_my > 0) {
+      tc::prefetch_tmap(&maps.k);
+      tc::prefetch_tmap(&maps.v);
+      for (int i = 0; i < n_my; ++i) {
+        const int st = i % NST;
+        if (i >= NST) tc::mbar_wait(&empty[st], ((i / NST) - 1) & 1);
+        const KmTile x = km_tile<KM_TILE>(t_begin + i, t_a, geo);
+        tc::mbar_expect_tx(&full[st], 2 * L::TILE_B);
+        const uint32_t ks = tc::smem_u32(sm + st * L::TILE_B), vs = tc::smem_u32(sm + L::OFF_V + st * L::TILE_B);
+        const CUtensorMap *mk = x.seg_a ? &maps.ck : &maps.k;
+        const CUtensorMap *mv = x.seg_a ? &maps.cv : &maps.v;
+        const int z = x.seg_a ? static_cast<int>(hr0) : kv;
+#pragma unroll
+        for (int a = 0; a < D / 64; ++a) {
+          tc::tma_load_3d(ks + a * KM_TILE * 128, mk, &full[st], a * 64, x.row0, z);
+          tc::tma_load_3d(vs + a * KM_TILE * 128, mv, &full[st], a * 64, x.row0, z);
+        }
+      }
+    }
+    if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  } else {
+    // ---- consumers
+    if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int g = lane >> 2, t4 = lane & 3;
+    const bool hv = g < G;
+    const uint16_t *qbase = q_from_archive ? q + static_cast<int64_t>(length) * D : q;
+    uint32_t qa[D / 16][2];
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint16_t *qp = qbase + static_cast<int64_t>(h0 + (hv ? g : 0)) * q_head_stride + kk * 16 + 2 * t4;
+      qa[kk][0] = hv ? __ldg(reinterpret_cast<const uint32_t *>(qp)) : 0u;
+      qa[kk][1] = hv ? __ldg(reinterpret_cast<const uint32_t *>(qp + 8)) : 0u;
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run = -INFINITY, l_part = 0.f;
+    const int wr0 = (warp % NW) * 16, grp = warp / NW;
+    const int64_t hr_g = head_row(S, layer, h0 + (hv ? g : 0));
+    float *ring_row = S.ring_s + (hr_g * S.window + slot) * S.row_cap;
+    const int m8 = lane >> 3, r8 = lane & 7;
+    for (int i = grp; i < n_my; i += NG) {
+      const int st = i % NST;
+      const KmTile x = km_tile<KM_TILE>(t_begin + i, t_a, geo);
+      // this tile's working-set ids (ring_ids of compressed rows), fetched before the data wait
+      int id = 0;
+      if (compressed && lane < 16 && wr0 + lane < x.valid)
+        id = x.seg_a ? __ldg(S.sel_ids + hr0 * S.budget_cap + x.row0 + wr0 + lane) : x.row0 + wr0 + lane;
+      tc::mbar_wait(&full[st], (i / NST) & 1);
+      if (rec && tid == 0 && i == 0) rec[2] = gtime();
+      const uint32_t ks = tc::smem_u32(sm + st * L::TILE_B), vs = tc::smem_u32(sm + L::OFF_V + st * L::TILE_B);
+      if (x.valid < wr0 + 16) {
+        // rows past the working set hold other (finite or not) data: zero this warp's V rows (P = 0 there)
+        unsigned char *vt = sm + L::OFF_V + st * L::TILE_B;
+        for (int e = lane; e < 16 * (D / 8); e += 32) {
+          const int r = wr0 + e / (D / 8), c = e % (D / 8);
+          if (r >= x.valid) *reinterpret_cast<uint4 *>(vt + km_off<KM_TILE>(r, c)) = make_uint4(0, 0, 0, 0);
+        }
+        tc::fence_proxy_async();  // the stage is refilled by TMA (async proxy) later
+        __syncwarp();
+      }
+      // S = Q K^T over this warp's 16 rows: n-tile 0 = rows wr0..+7, 1 = wr0+8..+15
+      // (all fragment loads first, then the MMAs in two independent chains per n-tile)
+      uint32_t fb[D / 16][4];
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) ldsm_x4(fb[kk], ks + km_off<KM_TILE>(wr0 + (m8 >> 1) * 8 + r8, 2 * kk + (m8 & 1)));
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      float sd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int kk = 0; kk < D / 16; kk += 2) {
+        mma_16816(sc[0], qa[kk][0], qa[kk][1], fb[kk][0], fb[kk][1]);
+        mma_16816(sc[1], qa[kk][0], qa[kk][1], fb[kk][2], fb[kk][3]);
+        mma_16816(sd[0], qa[kk + 1][0], qa[kk + 1][1], fb[kk + 1][0], fb[kk + 1][1]);
+        mma_16816(sd[1], qa[kk + 1][0], qa[kk + 1][1], fb[kk + 1][2], fb[kk + 1][3]);
+      }
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[n][e] += sd[n][e];
+      // V fragments in flight while the softmax runs
+#pragma unroll
+      for (int np = 0; np < D / 16; ++np)
+        ldsm_x4_t(fb[np], vs + km_off<KM_TILE>(wr0 + (m8 & 1) * 8 + r8, 2 * np + (m8 >> 1)));
+      // logits (log2 units); rows past the working set -> -inf
+      float xs[2][2];
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wr0 + n * 8 + 2 * t4 + e;
+          xs[n][e] = r < x.valid ? sc[n][e] * scale_log2 : -INFINITY;
+          tmax = fmaxf(tmax, xs[n][e]);
+        }
+      // raw logits to the ring (head g, columns j0 + r)
+      if (hv) {
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const int r = wr0 + n * 8 + 2 * t4;
+          if (r < x.valid) ring_row[x.j0 + r] = xs[n][0];
+          if (r + 1 < x.valid) ring_row[x.j0 + r + 1] = xs[n][1];
+        }
+      }
+      if (compressed && lane < 16 && wr0 + lane < x.valid) {
+        const int r = wr0 + lane;
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+          S.ring_ids[(head_row(S, layer, h0 + gg) * S.window + slot) * S.sparse_cap + x.j0 + r] = id;
+      }
+      // online softmax of this warp's rows (row g of the quad)
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+      const float m_new = fmaxf(m_run, tmax);
+      float p[2][2];
+      float corr = 1.f;
+      if (m_new == -INFINITY || !hv) {
+        p[0][0] = p[0][1] = p[1][0] = p[1][1] = 0.f;
+      } else {
+        corr = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) p[n][e] = xs[n][e] == -INFINITY ? 0.f : fast_exp2(xs[n][e] - m_new);
+        m_run = m_new;
+      }
+      l_part = l_part * corr + ((p[0][0] + p[0][1]) + (p[1][0] + p[1][1]));
+      if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          o[n][0] *= corr;
+          o[n][1] *= corr;
+        }
+      }
+      const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]), pa2 = pack_bf16(p[1][0], p[1][1]);
+      // O += P V: B = V rows wr0..+15 (k) x 16 dims per ldmatrix.x4.trans
+#pragma unroll
+      for (int np = 0; np < D / 16; ++np) {
+        mma_16816(o[2 * np], pa0, pa2, fb[np][0], fb[np][1]);
+        mma_16816(o[2 * np + 1], pa0, pa2, fb[np][2], fb[np][3]);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[st]);
+    }
+    if (rec && tid == 0) {
+      rec[3] = gtime();
+      rec[5] = n_my;
+    }
+    // quad sum of the row's softmax denominator
+    l_part += __shfl_xor_sync(0xffffffffu, l_part, 1);
+    l_part += __shfl_xor_sync(0xffffffffu, l_part, 2);
+    __syncthreads();  // (A) every warp is done with the stage buffers
+    float *wm = reinterpret_cast<float *>(sm);  // [W][8]
+    float *wl = wm + KM_WARPS * 8;              // [W][8]
+    float *wo = wl + KM_WARPS * 8;              // [W][8][D]
+    if (hv) {
+      if (t4 == 0) {
+        wm[warp * 8 + g] = m_run;
+        wl[warp * 8 + g] = l_part;
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<float2 *>(wo + (warp * 8 + g) * D + n * 8 + 2 * t4) = make_float2(o[n][0], o[n][1]);
+    }
+  }
+  if (warp == KM_WARPS) __syncthreads();  // (A) for the producer warp
+  __syncthreads();                        // (B) warp partials written
+  // ---- this CTA's partial (M, L, O) per head, warps merged in order -> global
+  {
+    float *wm = reinterpret_cast<float *>(sm);
+    float *wl = wm + KM_WARPS * 8;
+    float *wo = wl + KM_WARPS * 8;
+    float *part = S.partials + static_cast<int64_t>(unit) * n_split * G * (D + 2);
+    float *gl = reinterpret_cast<float *>(sm + L::OFF_GATHER);  // rank 0's gather area (cluster mode)
+    float *dst = part + split * G * (D + 2);
+    cg::cluster_group cluster = cg::this_cluster();
+    if (ccombine) dst = cluster.map_shared_rank(gl, 0) + split * G * (D + 2);
+    // per-warp scale factors once per head, then every element is an unrolled
+    // sum of independent shared loads
+    float *wsw = wo + KM_WARPS * 8 * D;  // [W][8]
+    float *wM = wsw + KM_WARPS * 8;      // [8]
+    if (tid < G) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < KM_WARPS; ++w) M = fmaxf(M, wm[w * 8 + tid]);
+#pragma unroll
+      for (int w = 0; w < KM_WARPS; ++w) {
+        const float mw = wm[w * 8 + tid];
+        wsw[w * 8 + tid] = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+      }
+      wM[tid] = M;
+    }
+    __syncthreads();
+    for (int i = tid; i < G * (D + 2); i += KM_THREADS) {
+      const int gg = i / (D + 2), e = i % (D + 2);
+      float acc = 0.f;
+      if (e > 0) {
+#pragma unroll
+        for (int w = 0; w < KM_WARPS; ++w)
+          acc = fmaf(wsw[w * 8 + gg], e == 1 ? wl[w * 8 + gg] : wo[(w * 8 + gg) * D + e - 2], acc);
+      }
+      dst[i] = e == 0 ? wM[gg] : acc;
+    }
+    if (rec && tid == 0) rec[4] = gtime();
+    if (ccombine) {
+      // DSMEM pushes -> rank 0 (the gather area is outside the stage buffers: one cluster barrier)
+      cluster.sync();
+      if (split != 0) return;
+      part = gl;
+    } else {
+      __threadfence();
+      if (rec && tid == 0) rec[8] = gtime();
+      __syncthreads();
+      if (tid == 0) is_last = atomicAdd(S.counters + unit, 1) == n_split - 1;
+      if (rec && tid == 0) rec[9] = gtime();
+      __syncthreads();
+      if (!is_last) return;
+      __threadfence();
+      if (rec && tid == 0) rec[10] = gtime();
+      // every split's partial into shared memory in one round of independent
+      // L2 loads (the combine below would otherwise chain n_split round trips)
+      const int n_el = n_split * G * (D + 2);
+      if (n_el * 4 <= 2 * NST * L::TILE_B) {
+        float *stg = reinterpret_cast<float *>(sm);
+        constexpr int B = 16;  // independent loads in flight per thread
+        for (int i0 = tid; i0 < n_el; i0 += KM_THREADS * B) {
+          float v[B];
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const int i = i0 + u * KM_THREADS;
+            v[u] = i < n_el ? __ldcg(part + i) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const int i = i0 + u * KM_THREADS;
+            if (i < n_el) stg[i] = v[u];
+          }
+        }
+        __syncthreads();
+        part = stg;
+      }
+    }
+    if (rec && tid == 0) rec[7] = gtime();
+    // ---- last CTA of the unit (or cluster rank 0): combine the splits in split order
+    const bool in_smem = __isShared(part);
+    auto ldp = [&](const float *x) { return in_smem ? *x : __ldcg(x); };  // shared or L2
+    for (int gg = warp; gg < G; gg += KM_WARPS + 1) {  // warp per head, lane r: splits r and r + 32
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+      if (lane < n_split) {
+        m0 = ldp(part + (lane * G + gg) * (D + 2));
+        l0 = ldp(part + (lane * G + gg) * (D + 2) + 1);
+      }
+      if (lane + 32 < n_split) {
+        m1 = ldp(part + ((lane + 32) * G + gg) * (D + 2));
+        l1 = ldp(part + ((lane + 32) * G + gg) * (D + 2) + 1);
+      }
+      const float M = warp_max(fmaxf(m0, m1));
+      const float w0 = m0 == -INFINITY ? 0.f : fast_exp2(m0 - M);
+      const float w1 = m1 == -INFINITY ? 0.f : fast_exp2(m1 - M);
+      if (lane < n_split) wsc[gg * KM_MAX_SPLIT + lane] = w0;
+      if (lane + 32 < n_split) wsc[gg * KM_MAX_SPLIT + lane + 32] = w1;
+      const float Lsum = warp_sum(fmaf(l0, w0, l1 * w1));
+      if (lane == 0) {
+        mg[gg] = M;
+        mg[8 + gg] = Lsum;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < G * D; i += KM_THREADS) {
+      const int gg = i / D, e = i % D;
+      float acc = 0.f;
+#pragma unroll 4
+      for (int r = 0; r < n_split; ++r)
+        acc = fmaf(wsc[gg * KM_MAX_SPLIT + r], ldp(part + (r * G + gg) * (D + 2) + 2 + e), acc);
+      const float res = acc / mg[8 + gg];
+      const int64_t oi = static_cast<int64_t>(h0 + gg) * D + e;
+      if (out_bf16)
+        reinterpret_cast<uint16_t *>(out)[oi] = f2bf(res);
+      else
+        reinterpret_cast<float *>(out)[oi] = res;
+    }
+    if (tid < G) {
+      const int64_t hr = head_row(S, layer, h0 + tid);
+      S.ring_ml[(hr * S.window + slot) * 2 + 0] = mg[tid];
+      S.ring_ml[(hr * S.window + slot) * 2 + 1] = mg[8 + tid];
+      S.ring_n[hr * S.window + slot] = geo.n_cols;
+      S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
+    }
+    if (tid == 0 && !ccombine) S.counters[unit] = 0;  // ticket re-armed for the next launch
+    if (rec && tid == 0) rec[6] = gtime();
+  }
+}
+
 // step[0] += 1, step[1] += rows; and the working-set split point n_a of every
 // (layer, q-head) follows the window start lo = max(0, length - W) one up
 // (an id equal to the old lo moves below the window)
@@ -702,10 +1151,111 @@ static int launch_decode(int units, int max_cols, cudaStream_t st, const ls_deco
   return LS_OK;
 }
 
+namespace ls {
+int make_tmap_bf16_3d_box(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
+                          int64_t head_stride_el, int box_rows);
+}
+
+template <int D, int G>
+static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_decode_stack *S, int layer,
+                             const uint16_t *q, int64_t q_head_stride, int q_from_archive, const uint16_t *k,
+                             const uint16_t *v, int compressed, float sl, void *out, int out_bf16, int pdl) {
+  LS_REQUIRE(S->partials != nullptr && S->counters != nullptr, LS_ERR_WORKSPACE,
+             "decode stack without partials / counters (see ls_decode_partials_size)");
+  // dense steps stream the archive: two groups of 4 consumer warps on
+  // alternate 64-row tiles, 4 stages, one CTA per SM; compressed steps (~17 x
+  // 64 rows per head): 4 warps, 3 stages, two CTAs per SM (the next layer's
+  // CTAs start their prefetch beside this layer's). Measured: tools/sweep_dec.sh
+  constexpr int NST_D = 4, NW_D = 4, NG_D = 2, NST_C = 3, NW_C = 4, NG_C = 1;
+  const int tile = compressed ? 16 * NW_C : 16 * NW_D;
+  dec::KmMaps maps;
+  const int HR = S->n_layers * S->n_heads;
+  const int64_t rows = S->kv_head_stride / D;
+  int r = make_tmap_bf16_3d_box(&maps.ck, S->ck, D, S->budget_cap, HR, D, static_cast<int64_t>(S->budget_cap) * D,
+                                tile);
+  if (!r) r = make_tmap_bf16_3d_box(&maps.cv, S->cv, D, S->budget_cap, HR, D,
+                                    static_cast<int64_t>(S->budget_cap) * D, tile);
+  if (!r) r = make_tmap_bf16_3d_box(&maps.k, k, D, rows, S->n_kv_heads, D, S->kv_head_stride, tile);
+  if (!r) r = make_tmap_bf16_3d_box(&maps.v, v, D, rows, S->n_kv_heads, D, S->kv_head_stride, tile);
+  if (r) return r;
+  constexpr int smem_d = dec::KmSmem<D, NST_D, NW_D, NG_D>::TOTAL, smem_c = dec::KmSmem<D, NST_C, NW_C, NG_C>::TOTAL;
+  static bool attr_set = false;
+  if (!attr_set) {
+    LS_CUDA(cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_d));
+    LS_CUDA(cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_c));
+    attr_set = true;
+  }
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  // splits: fill the resident CTA slots (2 per SM at this shared-memory size)
+  static const int env_split_dense = getenv("LS_K6_SPLIT_DENSE") ? atoi(getenv("LS_K6_SPLIT_DENSE")) : 0;
+  static const int env_split_comp = getenv("LS_K6_SPLIT_COMP") ? atoi(getenv("LS_K6_SPLIT_COMP")) : 0;
+  static const int env_cta_mult = getenv("LS_K6_CTAS_PER_SM") ? atoi(getenv("LS_K6_CTAS_PER_SM")) : 1;
+  static const bool env_no_cluster = getenv("LS_K6_NO_CLUSTER") != nullptr;
+  const int env_split = compressed ? env_split_comp : env_split_dense;
+  const int tiles = ceil_div(max_cols, tile) + 1;  // + the segment boundary
+  // dense: one CTA per SM; compressed: ~3 tiles per split (one cluster per unit)
+  int n_split = env_split > 0 ? env_split
+                : compressed ? std::min(8, ceil_div(tiles, 3))
+                             : std::max(1, env_cta_mult * n_sm / units);
+  n_split = std::max(1, std::min({n_split, tiles, dec::KM_MAX_SPLIT}));
+  // splits combine in rank 0's shared memory when they fit one portable cluster
+  const int ccombine = !env_no_cluster && n_split > 1 && n_split <= 8 &&
+                       n_split * G * (D + 2) * 4 <= dec::KM_GATHER_B;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_split, units, 1);
+  cfg.blockDim = dim3(32 * ((compressed ? NW_C * NG_C : NW_D * NG_D) + 1), 1, 1);
+  cfg.dynamicSmemBytes = compressed ? smem_c : smem_d;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (ccombine) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = n_split;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (compressed)
+    LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C>, maps, *S, layer, q, q_head_stride,
+                               q_from_archive, compressed, sl, out, out_bf16, pdl, ccombine, g_debug_buffer));
+  else
+    LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>, maps, *S, layer, q, q_head_stride,
+                               q_from_archive, compressed, sl, out, out_bf16, pdl, ccombine, g_debug_buffer));
+  return LS_OK;
+}
+
+// tensor-core K6 when the stack carries split-K partials; LS_K6_SIMT=1 selects
+// the CUDA-core form (cluster combine), kept as the cross-check
+template <int D, int G>
+static int launch_k6(int units, int max_cols, cudaStream_t st, const ls_decode_stack *S, int layer, const uint16_t *q,
+                     int64_t q_head_stride, int q_from_archive, const uint16_t *k, const uint16_t *v, int compressed,
+                     float sl, void *out, int out_bf16, int pdl) {
+  static const bool simt = getenv("LS_K6_SIMT") != nullptr;
+  if (!simt && S->partials != nullptr && S->counters != nullptr)
+    return launch_decode_mma<D, G>(units, max_cols, st, S, layer, q, q_head_stride, q_from_archive, k, v, compressed,
+                                   sl, out, out_bf16, pdl);
+  return launch_decode<D, G>(units, max_cols, st, S, layer, q, q_head_stride, q_from_archive, k, v, compressed, sl,
+                             out, out_bf16, pdl);
+}
+
 extern "C" size_t ls_decode_partials_size(const ls_decode_stack *S, int32_t max_len) {
-  (void)max_len;
-  (void)S;  // splits combine through distributed shared memory: no global partials
-  return 0;
+  (void)max_len;  // [unit][split][G][D + 2] floats: units x G = n_heads for every step kind
+  return S ? static_cast<size_t>(S->n_heads) * dec::KM_MAX_SPLIT * (S->head_dim + 2) * sizeof(float) : 0;
 }
 
 static int decode_step_impl(const ls_decode_stack *S, int32_t layer, const uint16_t *q, int64_t q_head_stride,
@@ -726,11 +1276,11 @@ static int decode_step_impl(const ls_decode_stack *S, int32_t layer, const uint1
   const bool per_head = compressed || getenv("LS_DECODE_DENSE_PER_HEAD") != nullptr;
   if (per_head) {
     r = S->head_dim == 128
-            ? launch_decode<128, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl)
-            : launch_decode<64, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl);
+            ? launch_k6<128, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl)
+            : launch_k6<64, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl);
   } else {
 #define LS_DENSE(DD, GG) \
-  r = launch_decode<DD, GG>(S->n_kv_heads, max_cols, st, S, layer, LS_ARGS, 0, sl, out, out_bf16, pdl)
+  r = launch_k6<DD, GG>(S->n_kv_heads, max_cols, st, S, layer, LS_ARGS, 0, sl, out, out_bf16, pdl)
     if (S->head_dim == 128) {
       if (group == 1) LS_DENSE(128, 1);
       else if (group == 2) LS_DENSE(128, 2);

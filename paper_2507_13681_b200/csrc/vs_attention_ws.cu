@@ -1110,13 +1110,20 @@ static EncodeTiledFn encode_fn() {
 }
 
 // bf16 [heads][rows][d] with explicit strides; box = 64 columns x 128 rows
+int make_tmap_bf16_3d_box(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
+                          int64_t head_stride_el, int box_rows);
 int make_tmap_bf16_3d(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
                       int64_t head_stride_el) {
+  return make_tmap_bf16_3d_box(m, base, d, rows, heads, row_stride_el, head_stride_el, 128);
+}
+
+int make_tmap_bf16_3d_box(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
+                          int64_t head_stride_el, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   LS_REQUIRE(fn != nullptr, LS_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride_el * 2), static_cast<cuuint64_t>(head_stride_el * 2)};
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

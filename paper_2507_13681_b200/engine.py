@@ -193,7 +193,9 @@ class SessionEngine:
         dependent of the previous layer's kernel, then the counter advance."""
         st = self.stack
         for l in range(self.shape.n_layers):
-            st.step_archive(l, store.q[l], store.k[l], store.v[l], compressed, max_cols, out_buf[l], pdl=True,
+            # layer 0 follows the counter advance (or an event) in full: its tile
+            # prefetch reads the step counters those kernels write
+            st.step_archive(l, store.q[l], store.k[l], store.v[l], compressed, max_cols, out_buf[l], pdl=l > 0,
                             stream=stream)
         st.advance(stream=stream)
 

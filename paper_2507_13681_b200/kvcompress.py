@@ -126,6 +126,10 @@ class DecodeStack:
             self.ring_ids.data_ptr(), self.ring_n.data_ptr(), self.ring_dense.data_ptr(), self.sel_ids.data_ptr(),
             self.n_sel.data_ptr(), self.ck.data_ptr(), self.cv.data_ptr(), 0, self.counters.data_ptr(),
             self.step_t.data_ptr(), self.n_a.data_ptr())
+        # split-K partials of the decode kernel (units x splits, combined by the last CTA of a unit)
+        n_part = int(_lib.lib().ls_decode_partials_size(ctypes.byref(self.desc), int(row_cap))) // 4
+        self.partials = torch.zeros(max(1, n_part), dtype=f32, device=dev)
+        self.desc.partials = self.partials.data_ptr()
         self.ws = Workspace()
         self.set_step(0, 0)
 

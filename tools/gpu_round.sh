@@ -20,6 +20,7 @@ for s in $STAGES; do
     launches) timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:$OURS" -c 15000 --csv \
                 --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
                 > $OUT/launches.log 2>&1; echo "launches rc=$?"; tail -2 $OUT/launches.log;;
+    kprof)  timeout 600 python tools/kprof.py > $OUT/kprof.log 2>&1; echo "kprof rc=$?"; cat $OUT/kprof.log | grep -v Warning | head -70;;
     prof)   timeout 600 python tools/prof_prefill.py > $OUT/prof_prefill.log 2>&1; echo "prof rc=$?"; head -40 $OUT/prof_prefill.log;;
     full)   for k in ${FULL_KERNELS:-vs_attention_ws_kernel k1_lines_kernel k1_stats_kernel decode_kernel select_kernel greedy_kernel}; do
               timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 40 -c 2 \
