@@ -302,7 +302,7 @@ def main():
         if not timing["on"]:
             return
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record(stream)
+        ev.record()  # the stream the entry runs on (head-group streams in prefill)
         if phase == "begin":
             recs.append([name, ev, None])
         else:

@@ -63,6 +63,9 @@ typedef struct ls_layer_desc {
   int32_t row_offset;     /* global position of block row 0                 */
   int64_t q_head_stride;  /* elements between q-heads in q                  */
   int64_t kv_head_stride; /* elements between kv-heads in k / v             */
+  int64_t out_row_stride; /* elements between attention-output rows; 0 =
+                             n_heads * head_dim (a head group writes its
+                             columns of the full [n_new][H][d] output)     */
 } ls_layer_desc;
 
 const char *ls_last_error(void);

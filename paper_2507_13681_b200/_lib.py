@@ -30,7 +30,7 @@ SZ = C.c_size_t
 class LayerDesc(C.Structure):
     _fields_ = [("n_heads", I32), ("n_kv_heads", I32), ("head_dim", I32), ("n_new", I32),
                 ("n_total", I32), ("row_offset", I32), ("q_head_stride", I64),
-                ("kv_head_stride", I64)]
+                ("kv_head_stride", I64), ("out_row_stride", I64)]
 
 
 class DecodeStackDesc(C.Structure):

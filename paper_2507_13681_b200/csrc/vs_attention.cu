@@ -33,6 +33,7 @@ struct Params {
   const int32_t *slash_ids, *vert_ids, *counts;
   const uint32_t *sbits, *vbits;  // [H][words]
   int n_heads, group, d, n_new, n_total, row_offset, words;
+  int64_t out_row_stride;
   int64_t q_head_stride, kv_head_stride;
   float scale_log2;
   void *out;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(THREADS) vs_attention_kernel(Params p) {
 
   // epilogue
   if (row_ok) {
-    const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * d;
+    const int64_t orow = static_cast<int64_t>(r0 + row) * p.out_row_stride + static_cast<int64_t>(h) * d;
     if (l > 0.f) {
       const float inv = 1.f / l;
       for (int i = 0; i < n_od; ++i) {
@@ -379,6 +380,7 @@ inline size_t smem_bytes(int d) {
 
 inline void fill(Params &p, const ls_layer_desc *L) {
   p.n_heads = L->n_heads;
+  p.out_row_stride = L->out_row_stride ? L->out_row_stride : static_cast<int64_t>(L->n_heads) * L->head_dim;
   p.group = L->n_heads / L->n_kv_heads;
   p.d = L->head_dim;
   p.n_new = L->n_new;

@@ -53,6 +53,7 @@ struct Params {
   const uint16_t *v;  // archive V (diagonal fallback reads)
   int n_heads, group, n_new, n_total, row_offset, words, n_qtiles, dense;
   int64_t kv_head_stride;
+  int64_t out_row_stride;  // elements between output rows
   float scale_log2;
   void *out;
   int out_bf16;
@@ -516,7 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::named_sync(1, N_SOFT);
     const float l_all = lx[row];
     if (row_ok) {
-      const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * D + wg * DH;
+      const int64_t orow = static_cast<int64_t>(r0 + row) * p.out_row_stride + static_cast<int64_t>(h) * D + wg * DH;
       if (l_all > 0.f) {
         const float inv = 1.f / l_all;
         if (p.out_bf16) {
@@ -990,7 +991,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       tc::fence_after_sync();
     }
     // (TMEM loads are .sync.aligned: every lane of the warp loads each chunk)
-    const int64_t orow = (static_cast<int64_t>(r0 + row) * p.n_heads + h) * D;
+    const int64_t orow = static_cast<int64_t>(r0 + row) * p.out_row_stride + static_cast<int64_t>(h) * D;
     const bool write_o = row_ok && l > 0.f;
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
@@ -1190,6 +1191,7 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   p.diag_ws = diag;
   p.v = v;
   p.n_heads = H;
+  p.out_row_stride = L->out_row_stride ? L->out_row_stride : static_cast<int64_t>(H) * d;
   p.group = H / L->n_kv_heads;
   p.n_new = L->n_new;
   p.n_total = L->n_total;

@@ -104,8 +104,15 @@ class PrefillOut:
 
 
 class SessionEngine:
+    """head_groups: the q-heads of a layer are processed as this many groups
+    of whole kv-head groups, each on its own stream, with the line scoring
+    (K1) of group g + 1 started only when group g's is done, so that group g's
+    selection (K2-K4: a latency-bound chain on one SM per head) and sparse
+    attention overlap the next groups' scoring. Layers stay sequential: all
+    groups of layer l finish before layer l + 1 starts."""
+
     def __init__(self, shape: AttnShape, params: SessionParams, cap: int, device="cuda",
-                 out_dtype=torch.bfloat16):
+                 out_dtype=torch.bfloat16, head_groups: int | None = None):
         params.validate()
         self.shape, self.params, self.cap = shape, params, cap
         self.device = device
@@ -121,6 +128,26 @@ class SessionEngine:
         self._q_buf = torch.empty((shape.n_layers, shape.n_q, 1, shape.d), dtype=torch.bfloat16, device=device)
         self._out_buf = torch.empty((shape.n_layers, shape.n_q, shape.d), dtype=out_dtype, device=device)
         self._graphs = {}
+        if head_groups is None:
+            import os
+            head_groups = int(os.environ.get("LS_HEAD_GROUPS", "1"))
+        if head_groups < 1 or shape.n_kv % head_groups:
+            raise ValueError(f"head_groups={head_groups} must divide n_kv={shape.n_kv}")
+        self.head_groups = head_groups
+        kv_per = shape.n_kv // head_groups
+        grp = shape.n_q // shape.n_kv
+        self._groups = [(g * kv_per * grp, (g + 1) * kv_per * grp, g * kv_per, (g + 1) * kv_per)
+                        for g in range(head_groups)]
+        if head_groups > 1 and str(device).startswith("cuda") and torch.cuda.is_available():
+            # K1 / K5 on normal-priority streams; the selection chains (few CTAs,
+            # latency-bound) on high-priority streams so their CTAs are
+            # dispatched ahead of the other groups' pending K1 / K5 CTAs
+            self._streams = [torch.cuda.Stream(device=device) for _ in range(head_groups)]
+            self._streams_hi = [torch.cuda.Stream(device=device, priority=-1) for _ in range(head_groups)]
+            self._gws = [Workspace() for _ in range(head_groups)]
+            self._ev_scored = [torch.cuda.Event() for _ in range(head_groups)]
+            self._ev_done = [torch.cuda.Event() for _ in range(head_groups)]
+            self._ev_start = torch.cuda.Event()
         self.clear_logs()
 
     def clear_logs(self):
@@ -159,32 +186,79 @@ class SessionEngine:
                 plans_all.append(None)
                 cells_all.append(None)
                 continue
-            plans: LayerPlans = sparsify_layer(qb, kl, rows[l], p.alpha, n_new, n_total, sh.n_kv,
-                                               q_head_stride=store.q.stride(1), ws=self.ws, stream=stream)
-            tiles = torch.empty(sh.n_q, dtype=torch.int64, device=self.device)
-            out, cells = attention_layer(qb, kl, vl, plans.slash_ids, plans.vert_ids, plans.counts, n_new,
-                                         n_total, sh.n_kv, out_dtype=self.out_dtype,
-                                         q_head_stride=store.q.stride(1), ws=self.ws, stream=stream, tiles=tiles)
+            if self.head_groups > 1:
+                plans, out, cells, tiles = self._layer_groups(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
+                                                              store.q.stride(1), stream)
+            else:
+                plans, out, cells, tiles = self._layer_group(l, 0, sh.n_q, 0, sh.n_kv, qb, kl, vl, rows[l], n_new,
+                                                             n_total, surv, n_seed, store.q.stride(1), None,
+                                                             self.ws, stream)
             self.tile_log.append(tiles)
             outs.append(out)
             plans_all.append(plans)
             cells_all.append(cells)
             self.cell_log.append(cells)
             self.score_log.append(plans.score_count)
-            if surv > 0:
-                # the seeds that are still in the deque at the first event are the
-                # last `surv` block rows; they sit in slots [n_seed - surv, n_seed)
-                first = n_seed - surv
-                hr = slice(l * sh.n_q, (l + 1) * sh.n_q)
-                plan_rows(qb, kl, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total, sh.n_kv, surv,
-                          out=st.ring_s[hr, first:], out_row_stride=st.row_cap,
-                          out_head_stride=st.window * st.row_cap, q_head_stride=store.q.stride(1),
-                          stream=stream)
-                st.ring_ml[hr, first:n_seed] = 0.0
-                st.ring_n[hr, first:n_seed] = n_total
-                st.ring_dense[hr, first:n_seed] = 1
         st.set_step(n_total, n_seed)
         return PrefillOut(outs, plans_all, cells_all, rows, n_new, n_total, n_seed)
+
+    def _layer_group(self, l, h0, h1, kv0, kv1, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs, out, ws,
+                     stream, on_scored=None, select_stream=None):
+        """K1-K5 (+ seed rows) of q-heads [h0, h1) of layer l, on `stream`."""
+        p, sh, st = self.params, self.shape, self.stack
+        n_kv = kv1 - kv0
+        qg, kg, vg = qb[h0:h1], kl[kv0:kv1], vl[kv0:kv1]
+        plans: LayerPlans = sparsify_layer(qg, kg, rows_l[h0:h1], p.alpha, n_new, n_total, n_kv, q_head_stride=qhs,
+                                           ws=ws, stream=stream, on_scored=on_scored, select_stream=select_stream)
+        tiles = torch.empty(h1 - h0, dtype=torch.int64, device=self.device)
+        out, cells = attention_layer(qg, kg, vg, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total, n_kv,
+                                     out=out, out_dtype=self.out_dtype, q_head_stride=qhs, ws=ws, stream=stream,
+                                     tiles=tiles)
+        if surv > 0:
+            # the seeds that are still in the deque at the first event are the
+            # last `surv` block rows; they sit in slots [n_seed - surv, n_seed)
+            first = n_seed - surv
+            hr = slice(l * sh.n_q + h0, l * sh.n_q + h1)
+            plan_rows(qg, kg, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total, n_kv, surv,
+                      out=st.ring_s[hr, first:], out_row_stride=st.row_cap, out_head_stride=st.window * st.row_cap,
+                      q_head_stride=qhs, stream=stream)
+            st.ring_ml[hr, first:n_seed] = 0.0
+            st.ring_n[hr, first:n_seed] = n_total
+            st.ring_dense[hr, first:n_seed] = 1
+        return plans, out, cells, tiles
+
+    def _layer_groups(self, l, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs, stream):
+        """One layer as head groups on their own streams, K1 of group g + 1
+        after K1 of group g; joined on the caller's stream."""
+        main = stream if stream is not None else torch.cuda.current_stream()
+        sh = self.shape
+        out = torch.empty((n_new, sh.n_q, sh.d), dtype=self.out_dtype, device=self.device)
+        self._ev_start.record(main)
+        parts = []
+        for g, (h0, h1, kv0, kv1) in enumerate(self._groups):
+            s = self._streams[g]
+            s.wait_event(self._ev_start)
+            if g > 0:
+                s.wait_event(self._ev_scored[g - 1])
+            ev = self._ev_scored[g]
+            with torch.cuda.stream(s):
+                res = self._layer_group(l, h0, h1, kv0, kv1, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs,
+                                        out[:, h0:h1], self._gws[g], s, on_scored=lambda s=s, ev=ev: ev.record(s),
+                                        select_stream=self._streams_hi[g])
+            self._ev_done[g].record(s)
+            parts.append(res)
+        for g in range(len(self._groups)):
+            main.wait_event(self._ev_done[g])
+        plans = LayerPlans.cat([r[0] for r in parts])
+        cells = torch.cat([r[2] for r in parts])
+        tiles = torch.cat([r[3] for r in parts])
+        for r in parts:  # group-stream tensors now read on the caller's stream
+            pl = r[0]
+            ts = [v for v in vars(pl).values() if isinstance(v, torch.Tensor)]
+            ts += list(getattr(pl, "line_arrays", ())) + [r[2], r[3]]
+            for t in ts:
+                t.record_stream(main)
+        return plans, out, cells, tiles
 
     # -------------------------------------------------------------- decode
     def _step(self, store: QKVStore, q_buf, out_buf, compressed: bool, max_cols: int, stream=None):

@@ -158,6 +158,19 @@ class LayerPlans:
     n_picks: torch.Tensor     # int32 [H]
     n_total: int
 
+    @staticmethod
+    def cat(parts: list["LayerPlans"]) -> "LayerPlans":
+        """Plans of consecutive head groups -> one layer's plans (head order)."""
+        if len(parts) == 1:
+            return parts[0]
+        f = lambda name: torch.cat([getattr(p, name) for p in parts])
+        out = LayerPlans(f("slash_ids"), f("vert_ids"), f("counts"), f("coverage"), f("approx"), f("total"),
+                         f("score_count"), f("picks"), f("n_picks"), parts[0].n_total)
+        if all(hasattr(p, "line_arrays") for p in parts):
+            out.line_arrays = tuple(torch.cat([p.line_arrays[i] for p in parts]) for i in range(4))
+            out.row_stats = torch.cat([p.row_stats for p in parts])
+        return out
+
     def to_host(self) -> list[SparsePlan]:
         sl, vt, cn = self.slash_ids.cpu().numpy(), self.vert_ids.cpu().numpy(), self.counts.cpu().numpy()
         cov, ap, tot = self.coverage.cpu().numpy(), self.approx.cpu().numpy(), self.total.cpu().numpy()
@@ -192,16 +205,20 @@ class Workspace:
         return self.buf
 
 
-def layer_desc(n_heads, n_kv_heads, d, n_new, n_total, q_head_stride, kv_head_stride):
+def layer_desc(n_heads, n_kv_heads, d, n_new, n_total, q_head_stride, kv_head_stride, out_row_stride=0):
     return _lib.LayerDesc(int(n_heads), int(n_kv_heads), int(d), int(n_new), int(n_total),
-                          int(n_total - n_new), int(q_head_stride), int(kv_head_stride))
+                          int(n_total - n_new), int(q_head_stride), int(kv_head_stride), int(out_row_stride))
 
 
 def sparsify_layer(q_block: torch.Tensor, k: torch.Tensor, rows: torch.Tensor, alpha: float,
                    n_new: int, n_total: int, n_kv_heads: int, q_head_stride: int | None = None,
                    kv_head_stride: int | None = None, ws: Workspace | None = None,
-                   stream=None) -> LayerPlans:
+                   stream=None, on_scored=None, select_stream=None) -> LayerPlans:
     """Batched sparsify_head for every q-head of a layer (K1 + K2-K4).
+    on_scored(): called once the line sums (K1) are enqueued, before the
+    selection (the engine's head-group pipeline records an event there).
+    select_stream: run the selection (K2-K4) there (ordered after K1 and
+    before anything later on `stream` by events).
 
     q_block: bf16, head h row r at q_block.data_ptr() + (h*q_head_stride + r*d)*2
     k:       bf16 archive, kv-head j position c at (j*kv_head_stride + c*d)*2
@@ -231,6 +248,13 @@ def sparsify_layer(q_block: torch.Tensor, k: torch.Tensor, rows: torch.Tensor, a
     _lib.call("ls_score_lines", C_ref(L), n_s, q_block.data_ptr(), k.data_ptr(), rows.data_ptr(),
               v_w.data_ptr(), v_max.data_ptr(), s_w.data_ptr(), s_max.data_ptr(), row_stats.data_ptr(),
               total.data_ptr(), score_count.data_ptr(), w1.data_ptr(), w1.numel(), sp)
+    if on_scored is not None:
+        on_scored()
+    if select_stream is not None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        select_stream.wait_event(ev)
+        sp = _lib.stream_ptr(select_stream)
     slash_ids = torch.empty((H, n_total), dtype=i32, device=dev)
     vert_ids = torch.empty((H, n_total), dtype=i32, device=dev)
     counts = torch.empty((H, 2), dtype=i32, device=dev)
@@ -245,6 +269,10 @@ def sparsify_layer(q_block: torch.Tensor, k: torch.Tensor, rows: torch.Tensor, a
               row_stats.data_ptr(), total.data_ptr(), slash_ids.data_ptr(), vert_ids.data_ptr(),
               counts.data_ptr(), coverage.data_ptr(), approx.data_ptr(), picks.data_ptr(),
               n_picks.data_ptr(), w2.data_ptr(), w2.numel(), sp)
+    if select_stream is not None:
+        ev = torch.cuda.Event()
+        ev.record(select_stream)
+        (stream if stream is not None else torch.cuda.current_stream()).wait_event(ev)
     plans = LayerPlans(slash_ids, vert_ids, counts, coverage, approx, total, score_count, picks,
                        n_picks, n_total)
     plans.line_arrays = (v_w, v_max, s_w, s_max)  # kept for diagnostics / parity tests

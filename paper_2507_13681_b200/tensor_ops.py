@@ -99,13 +99,15 @@ def attention_layer(q_block: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sla
                     out_dtype=torch.bfloat16, q_head_stride=None, kv_head_stride=None,
                     ws: Workspace | None = None, stream=None, tiles: torch.Tensor | None = None):
     """K5 for every q-head of a layer -> (out [n_new, H, d], cells [H]); with
-    `tiles` (int64 [H]) also the 128x128 tensor-core tiles each head executed."""
+    `tiles` (int64 [H]) also the 128x128 tensor-core tiles each head executed.
+    `out` may be a head-column view of a wider [n_new, H_all, d] output."""
     H = counts.shape[0]
     d = q_block.shape[-1]
     dev = q_block.device
     L = layer_desc(H, n_kv_heads, d, n_new, n_total,
                    q_block.stride(0) if q_head_stride is None else q_head_stride,
-                   k.stride(0) if kv_head_stride is None else kv_head_stride)
+                   k.stride(0) if kv_head_stride is None else kv_head_stride,
+                   out.stride(0) if out is not None else 0)
     if out is None:
         out = torch.empty((n_new, H, d), dtype=out_dtype, device=dev)
     cells = torch.empty(H, dtype=torch.int64, device=dev)
