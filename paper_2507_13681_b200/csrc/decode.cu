@@ -49,6 +49,8 @@ constexpr int K6_THREADS = 128;
 constexpr int K7_THREADS = 1024;
 constexpr int K7_SMEM_CAP = 24 * 1024;  // ids accumulated in shared memory (fp64) up to this length
 constexpr int K7_CAND_CAP = 4096;       // touched ids listed in shared memory (radix + ranking over the list)
+constexpr int K7_BITONIC = 2048;        // candidate lists up to this size are ranked by one bitonic sort
+constexpr int K7_RB = 8, K7_PF = 2;     // rows fetched per round, columns per thread per row
 
 __device__ __forceinline__ int64_t head_row(const ls_decode_stack &S, int layer, int h) {
   return static_cast<int64_t>(layer) * S.n_heads + h;
@@ -907,9 +909,15 @@ __device__ int block_rank(int flag, int *sh, int *tot) {
   return before + __popc(b & ((1u << lane) - 1u));
 }
 
+__device__ __forceinline__ int gtime32() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<int>(t & 0x7fffffffull);
+}
+
 __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, int budget, double *acc_ws,
                                                             uint32_t *touched_ws, int use_smem, int32_t *retained_n,
-                                                            double *score_cov) {
+                                                            double *score_cov, int *dbg) {
   extern __shared__ __align__(16) unsigned char smem7[];
   __shared__ int hist[256];
   __shared__ int shi[32];
@@ -925,27 +933,86 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   uint32_t *touched =
       use_smem ? reinterpret_cast<uint32_t *>(smem7 + static_cast<size_t>(K7_SMEM_CAP) * 8)
                : touched_ws + hr * ((S.row_cap + 31) / 32);
+  int *rec = (dbg && threadIdx.x == 0) ? dbg + (static_cast<int64_t>(layer) * gridDim.x + h) * 8 : nullptr;
+  if (rec) rec[0] = gtime32();
   for (int i = threadIdx.x; i < length; i += blockDim.x) acc[i] = 0.0;
   for (int i = threadIdx.x; i < words; i += blockDim.x) touched[i] = 0u;
   __syncthreads();
-  // accumulate rows oldest -> newest (kvcompress.py:75-79)
-  for (int rr = 0; rr < n_rows; ++rr) {
-    const int slot = (appended - n_rows + rr) % S.window;
-    const int64_t so = hr * S.window + slot;
-    const int n = S.ring_n[so];
-    const int dense = S.ring_dense[so];
-    const float M = S.ring_ml[so * 2], Lr = S.ring_ml[so * 2 + 1];
-    const float inv = Lr > 0.f ? 1.f / Lr : 0.f;
-    const float *s = S.ring_s + so * S.row_cap;
-    const int32_t *ids = S.ring_ids + so * S.sparse_cap;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const int id = dense ? j : ids[j];
-      const float w = (Lr == 0.f) ? s[j] : fast_exp2(s[j] - M) * inv;  // Lr == 0: stored probabilities (seeds)
-      acc[id] += static_cast<double>(w);
-      atomicOr(touched + (id >> 5), 1u << (id & 31));
+  if (rec) rec[1] = gtime32();
+  // accumulate rows oldest -> newest (kvcompress.py:75-79). Rows of up to
+  // K7_PF * blockDim columns (every compressed row) are fetched K7_RB rows at
+  // a time into registers (one round of independent loads), then added in row
+  // order; longer (dense) rows stream.
+  auto row_weight = [](float sv, float M, float Lr, float inv) {
+    return (Lr == 0.f) ? sv : fast_exp2(sv - M) * inv;  // Lr == 0: stored probabilities (seeds)
+  };
+  for (int r0 = 0; r0 < n_rows; r0 += K7_RB) {
+    const int nr = min(K7_RB, n_rows - r0);
+    // row metadata of the round (one round trip: slots are always valid indices)
+    int64_t so_r[K7_RB];
+    int n_r[K7_RB], dense_r[K7_RB];
+    float m_r[K7_RB], l_r[K7_RB];
+    int nmax = 0;
+#pragma unroll
+    for (int rr = 0; rr < K7_RB; ++rr) {
+      so_r[rr] = hr * S.window + (appended - n_rows + r0 + rr) % S.window;
+      n_r[rr] = __ldg(S.ring_n + so_r[rr]);
+      dense_r[rr] = __ldg(S.ring_dense + so_r[rr]);
+      m_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2);
+      l_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2 + 1);
     }
-    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < K7_RB; ++rr) {
+      if (rr >= nr) n_r[rr] = 0;
+      nmax = max(nmax, n_r[rr]);
+    }
+    if (nmax <= K7_PF * static_cast<int>(blockDim.x)) {
+      // the round's columns (second round trip), then the adds in row order
+      float sv_r[K7_RB][K7_PF];
+      int iv[K7_RB][K7_PF];
+#pragma unroll
+      for (int rr = 0; rr < K7_RB; ++rr)
+#pragma unroll
+        for (int e = 0; e < K7_PF; ++e) {
+          const int j = threadIdx.x + e * blockDim.x;
+          const bool ok = j < n_r[rr];
+          iv[rr][e] = !ok ? -1 : dense_r[rr] ? j : __ldg(S.ring_ids + so_r[rr] * S.sparse_cap + j);
+          sv_r[rr][e] = ok ? __ldg(S.ring_s + so_r[rr] * S.row_cap + j) : 0.f;
+        }
+#pragma unroll
+      for (int rr = 0; rr < K7_RB; ++rr) {
+        if (rr < nr) {
+          const float inv = l_r[rr] > 0.f ? 1.f / l_r[rr] : 0.f;
+#pragma unroll
+          for (int e = 0; e < K7_PF; ++e) {
+            const int id = iv[rr][e];
+            if (id >= 0) {
+              acc[id] += static_cast<double>(row_weight(sv_r[rr][e], m_r[rr], l_r[rr], inv));
+              atomicOr(touched + (id >> 5), 1u << (id & 31));
+            }
+          }
+          __syncthreads();
+        }
+      }
+    } else {
+      for (int rr = 0; rr < nr; ++rr) {
+        const int64_t so = hr * S.window + (appended - n_rows + r0 + rr) % S.window;
+        const int n = S.ring_n[so];
+        const int dense = S.ring_dense[so];
+        const float M = S.ring_ml[so * 2], Lr = S.ring_ml[so * 2 + 1];
+        const float inv = Lr > 0.f ? 1.f / Lr : 0.f;
+        const float *sr = S.ring_s + so * S.row_cap;
+        const int32_t *ids = S.ring_ids + so * S.sparse_cap;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+          const int id = dense ? j : ids[j];
+          acc[id] += static_cast<double>(row_weight(sr[j], M, Lr, inv));
+          atomicOr(touched + (id >> 5), 1u << (id & 31));
+        }
+        __syncthreads();
+      }
+    }
   }
+  if (rec) rec[2] = gtime32();
   int cnt = 0;
   for (int i = threadIdx.x; i < words; i += blockDim.x) cnt += __popc(touched[i]);
   const int n_cand = block_sum_int(cnt, shi);
@@ -969,11 +1036,59 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     }
     __syncthreads();
   }
+  if (rec) {
+    rec[3] = gtime32();
+    rec[7] = n_cand;
+  }
   const int n_iter = use_list ? n_cand : length;  // loop domain: list entries or positions
   unsigned long long prefix = 0ull, pmask = 0ull;
   int need = budget;
   const bool take_all = budget >= n_cand;
-  if (!take_all) {
+  // few candidates (every event after the first: ~B + W ids): one bitonic
+  // sort of (score desc, id asc) over the list instead of 8 radix passes
+  const bool bitonic = use_list && !take_all && n_cand <= K7_BITONIC;
+  double sc_reg[K7_BITONIC / K7_THREADS];
+  int *flag = nullptr;
+  if (bitonic) {
+#pragma unroll
+    for (int e = 0; e < K7_BITONIC / K7_THREADS; ++e) {
+      const int k = threadIdx.x + e * K7_THREADS;
+      sc_reg[e] = k < n_cand ? acc[cand[k]] : 0.0;
+    }
+    __syncthreads();  // the accumulator area is reused below
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(smem7);
+    int *sv = reinterpret_cast<int *>(smem7 + K7_BITONIC * 8);
+    flag = sv + K7_BITONIC;
+#pragma unroll
+    for (int e = 0; e < K7_BITONIC / K7_THREADS; ++e) {
+      const int k = threadIdx.x + e * K7_THREADS;
+      sk[k] = k < n_cand ? ~dkey(sc_reg[e]) : ~0ull;  // ascending key = descending score
+      sv[k] = k;                                      // list order = id order: ties by id
+      flag[k] = 0;
+    }
+    __syncthreads();
+    for (int size = 2; size <= K7_BITONIC; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < K7_BITONIC / 2; t += K7_THREADS) {
+          const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+          const bool up = (i & size) == 0;
+          const unsigned long long ki = sk[i], kj = sk[j];
+          const int vi = sv[i], vj = sv[j];
+          const bool gt = ki > kj || (ki == kj && vi > vj);
+          if (gt == up) {
+            sk[i] = kj;
+            sk[j] = ki;
+            sv[i] = vj;
+            sv[j] = vi;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int t = threadIdx.x; t < budget; t += K7_THREADS) flag[sv[t]] = 1;
+    __syncthreads();
+  }
+  if (!take_all && !bitonic) {
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
@@ -1021,6 +1136,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
       __syncthreads();
     }
   }
+  if (rec) rec[4] = gtime32();
   const unsigned long long thr = prefix;
   int32_t *sel = S.sel_ids + hr * S.budget_cap;
   int base = 0, eq_seen = 0;
@@ -1032,7 +1148,12 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     const int i = use_list ? (k < n_iter ? cand[k] : length) : k;
     int is_t = 0, is_eq = 0, is_gt = 0;
     double scv = 0.0;
-    if (i < length && (use_list || ((touched[i >> 5] >> (i & 31)) & 1u))) {
+    if (bitonic) {
+      if (k < n_cand) {
+        is_t = 1;
+        scv = sc_reg[i0 / K7_THREADS];
+      }
+    } else if (i < length && (use_list || ((touched[i >> 5] >> (i & 31)) & 1u))) {
       is_t = 1;
       scv = acc[i];
       if (!take_all) {
@@ -1043,7 +1164,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     }
     int eq_tot;
     const int eq_rank = block_rank(is_eq, shi, &eq_tot);
-    const int pick = take_all ? is_t : (is_gt || (is_eq && eq_seen + eq_rank < need));
+    const int pick = take_all ? is_t : bitonic ? (is_t && flag[k]) : (is_gt || (is_eq && eq_seen + eq_rank < need));
     int pick_tot;
     const int rank = block_rank(pick, shi, &pick_tot);
     if (pick) sel[base + rank] = i;
@@ -1055,6 +1176,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     base += pick_tot;
     eq_seen += eq_tot;
   }
+  if (rec) rec[5] = gtime32();
   const double T = block_sum_double(tot_mass, shd);
   const double Kp = block_sum_double(kept_mass, shd);
   const int iw = block_sum_int(in_window_picked, shi);
@@ -1070,6 +1192,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     if (retained_n) retained_n[hr] = base + (length - lo) - iw;
     if (score_cov) score_cov[hr] = T > 0 ? Kp / T : 1.0;
   }
+  if (rec) rec[6] = gtime32();
 }
 
 // ------------------------------------------------------------------ K8
@@ -1350,7 +1473,7 @@ extern "C" int ls_decode_event(const ls_decode_stack *S, int32_t budget, int32_t
   if (dyn > 48 * 1024)
     LS_CUDA(cudaFuncSetAttribute(dec::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
   dec::select_kernel<<<dim3(S->n_heads, S->n_layers), dec::K7_THREADS, dyn, st>>>(*S, budget, acc, touched, smem ? 1 : 0,
-                                                                                   retained_n, score_coverage);
+                                                                                   retained_n, score_coverage, g_debug_buffer);
   LS_LAUNCH_CHECK("select_kernel");
   dec::compact_kernel<<<dim3(16, S->n_heads, S->n_layers), 256, 0, st>>>(*S, k_all, v_all);
   LS_LAUNCH_CHECK("compact_kernel");

@@ -115,3 +115,33 @@ def test_long_context_turn_c3_shape(cuda_lib):
     dense_cells = n_new * ro + n_new * (n_new + 1) // 2
     assert (cells > 0).all() and (cells <= dense_cells).all()
     assert torch.isfinite(res.out[0].float()).all() and torch.isfinite(last.float()).all()
+
+
+def test_head_group_pipeline_identical(cuda_lib):
+    """Prefill as head groups on their own streams (each group writing its
+    head columns of the shared output through out_row_stride) gives the
+    one-launch-per-layer results bit for bit: every kernel is per head."""
+    from paper_2507_13681_b200.engine import AttnShape, QKVStore, SessionEngine, SessionParams
+    from paper_2507_13681_b200.kvcompress import CompressionConfig
+
+    shape = AttnShape(2, 8, 4, 128)
+    n_new = 900
+    store = QKVStore.synthetic(shape, n_new + 16, n_ref=n_new + 16, seed=7)
+    res = []
+    for hg in (1, 2, 4):
+        eng = SessionEngine(shape, SessionParams(alpha=0.9, comp=CompressionConfig(64, 8, 8), max_new=16, seed=3),
+                            n_new + 16, head_groups=hg)
+        r = eng.prefill(store, 0, 0, n_new)
+        torch.cuda.synchronize()
+        res.append((r, eng.stack.ring_s.clone()))
+    (r1, ring1) = res[0]
+    for r, ring in res[1:]:
+        for l in range(shape.n_layers):
+            assert torch.equal(r.out[l], r1.out[l])
+            assert torch.equal(r.plans[l].counts, r1.plans[l].counts)
+            cn = r1.plans[l].counts.cpu()
+            for h in range(shape.n_q):  # id lists are valid up to their counts
+                assert torch.equal(r.plans[l].slash_ids[h, :cn[h, 0]], r1.plans[l].slash_ids[h, :cn[h, 0]])
+                assert torch.equal(r.plans[l].vert_ids[h, :cn[h, 1]], r1.plans[l].vert_ids[h, :cn[h, 1]])
+            assert torch.equal(r.cells[l], r1.cells[l])
+        assert torch.equal(ring, ring1)  # seed rows

@@ -60,15 +60,20 @@ def launches(path, top=30):
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     agg = collections.defaultdict(lambda: [0, 0.0])
+    n_setup = 0
     for r in data:
         if len(r) <= vi:
+            continue
+        if r[ki].startswith("at_cuda_detail") or "at_cuda_detail::" in r[ki][:40]:
+            n_setup += 1  # torch's own sorts (synthetic-data setup), not the path
             continue
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "")[:70]
         agg[name][0] += 1
         agg[name][1] += v
     tot = sum(x[1] for x in agg.values())
-    print(f"{len(data)} launches, {tot / 1e3:.3f} ms serialised (cold-cache) device time")
+    print(f"{sum(x[0] for x in agg.values())} launches, {tot / 1e3:.3f} ms serialised (cold-cache) device time"
+          f" ({n_setup} torch setup launches of the synthetic store excluded)")
     print("| kernel | launches | total ms | mean us | share |")
     print("|---|---|---|---|---|")
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
