@@ -505,9 +505,22 @@ def dense_baseline(cfg, store, blocks, shard, sparse_ttft):
     ms = [a.elapsed_time(b) for a, b in per_turn]
     dense_cells = sum(n * ro + n * (n + 1) // 2 for ro, n in blocks) * shard.n_q_local * cfg["n_layers"]
     tflops = 4.0 * cfg["d"] * dense_cells / (sum(ms) * 1e-3) / 1e12
+    # full-cache decode (decode_step without working sets, model.py:301-306): every
+    # step attends to the whole archive; after the last turn's prefill
+    ro, n_new = blocks[-1]
+    eng.decode(store, ro + n_new, cfg["max_new"])  # graphs captured + warm
+    eng.prefill(store, len(blocks) - 1, ro, n_new)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eng.decode(store, ro + n_new, cfg["max_new"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dec_ms = e0.elapsed_time(e1)
     return {"ttft_ms_per_turn": [round(x, 3) for x in ms], "ttft_ms": round(statistics.mean(ms), 3),
             "sparse_speedup": round(statistics.mean(ms) / sparse_ttft, 3), "dense_tflops": round(tflops, 1),
-            "note": "dense causal attention of the same turn blocks (K5 dense mode, all layers), one pass"}
+            "decode_tokens_per_s_last_turn": round(cfg["max_new"] / (dec_ms * 1e-3), 2),
+            "note": "dense causal attention of the same turn blocks (K5 dense mode, all layers), one pass; "
+                    "full-cache decode (no compression) of the last turn's max_new tokens"}
 
 
 def run_e2e(args, cfg, eng, store, blocks, shard, gather):

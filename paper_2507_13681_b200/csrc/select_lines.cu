@@ -170,7 +170,7 @@ struct RecomputeCells {
                                                       static_cast<int64_t>(g - row_offset) * d);
     const uint4 *kr = reinterpret_cast<const uint4 *>(k + static_cast<int64_t>(h / group) * kv_head_stride +
                                                       static_cast<int64_t>(c) * d);
-    float acc = 0.f;
+    float acc4[4] = {0.f, 0.f, 0.f, 0.f};  // four independent FMA chains
     // two batches of loads in flight (2 L2 round trips per cell at d = 128)
     for (int v = 0; v < d / 8; v += 8) {
       uint4 a[8], b[8];
@@ -185,9 +185,10 @@ struct RecomputeCells {
         bf16x8_to_f32(a[u], fa);
         bf16x8_to_f32(b[u], fb);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc = fmaf(fa[j], fb[j], acc);
+        for (int j = 0; j < 8; ++j) acc4[j & 3] = fmaf(fa[j], fb[j], acc4[j & 3]);
       }
     }
+    const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
     const float *rs = row_stats + (static_cast<int64_t>(h) * n_s + r) * 2;
     return static_cast<double>(fast_exp2(acc * scale_log2 - rs[0]) * rs[1]);
   }
@@ -227,7 +228,9 @@ struct DenseCells {
 constexpr int WIN = 1024;            // staged lines per list
 constexpr int TAB_CAP = 16384;       // n_total up to which position tables live in shared memory
 constexpr int G_THREADS = 512;       // 16 warps
-constexpr int RING = 1024;           // picks in flight between producer and finalizer
+constexpr int RING = 1024;           // pick slots between producer and finalizer
+constexpr int AHEAD = 256;           // the producer runs at most this far ahead of the finalizer: picks
+                                     // past the plan's end cost crossing sums for nothing
 constexpr int GS_CAP = 8192;         // sampled positions kept in shared memory
 
 // gain_s >= gain_v with gain = num / den (prefill.py:206-208). Decided by
@@ -252,6 +255,7 @@ struct GreedySmem {
   int32_t gs[GS_CAP];
   int16_t rowof[TAB_CAP];    // position -> sampled row, or -1
   uint16_t inv[2][TAB_CAP];  // line index -> sorted position (clamped to 65535)
+  int32_t hitq[G_THREADS / 32][64];  // per consumer warp: sampled rows of crossing cells awaiting a value
 };
 
 __device__ __forceinline__ int vload(const volatile int *p) { return *p; }
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
   GreedySmem &S = *reinterpret_cast<GreedySmem *>(g_smem);
   __shared__ volatile int n_prod, prod_done, fin_pos, stop_at;
   __shared__ int next_j;
+  __shared__ unsigned long long busy_cyc;  // diagnostics: consumer cycles spent on crossing sums
   const int h = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double T = total[h];
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
     fin_pos = 0;
     stop_at = 0x7fffffff;
     next_j = 0;
+    busy_cyc = 0ull;
   }
   __syncthreads();
   const int32_t *inv_s = L.inv + lb, *inv_v = L.inv + lb + n_total;
@@ -348,11 +354,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       stop_seen = __shfl_sync(0xffffffffu, lane == 0 ? stop_at : 0, 0);  // one read: the warp must agree
       if (n >= stop_seen) break;
       int stopped = 0;
-      if (lane == 0 && n + 33 - fin_seen > RING) {
+      if (lane == 0 && n + 33 - fin_seen > AHEAD) {
         fin_seen = fin_pos;
         const long long tw = clock64();
         SpinGuard guard;
-        while (n + 33 - fin_seen > RING) {  // ring full: finalizer behind
+        while (n + 33 - fin_seen > AHEAD) {  // far enough ahead: wait for the finalizer
           if (stop_at <= n) {  // the finalizer has stopped the plan: it will not free the ring
             stopped = 1;
             break;
@@ -374,12 +380,26 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       const double olR0 = R ? ol_v : ol_s, olO = R ? ol_s : ol_v;
       // folds in reference order: state before R pick j (ol_R, approx)
       double my_ol = olR0, my_ap = approx, ol_run = olR0, ap_run = approx;
-      for (int i = 0; i < K; ++i) {
-        if (lane == i) { my_ol = ol_run; my_ap = ap_run; }
-        const double wi = __shfl_sync(0xffffffffu, wR, i);
-        const double mi = __shfl_sync(0xffffffffu, mxR, i);
-        ap_run += wi - olO;  // approx += w - ol_other (prefill.py:210, 216)
-        ol_run += mi;        // ol_R += max_cell (prefill.py:212, 218)
+      if (base_R + K <= win) {
+        // window in shared memory: broadcast loads (issued ahead of the fold)
+        // instead of shuffles; the fold itself is the same sequential fp64 chain
+        const double *wp = S.w[R] + base_R, *mp = S.mx[R] + base_R;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i < K) {
+            if (lane == i) { my_ol = ol_run; my_ap = ap_run; }
+            ap_run += wp[i] - olO;  // approx += w - ol_other (prefill.py:210, 216)
+            ol_run += mp[i];        // ol_R += max_cell (prefill.py:212, 218)
+          }
+        }
+      } else {
+        for (int i = 0; i < K; ++i) {
+          if (lane == i) { my_ol = ol_run; my_ap = ap_run; }
+          const double wi = __shfl_sync(0xffffffffu, wR, i);
+          const double mi = __shfl_sync(0xffffffffu, mxR, i);
+          ap_run += wi - olO;  // approx += w - ol_other (prefill.py:210, 216)
+          ol_run += mi;        // ol_R += max_cell (prefill.py:212, 218)
+        }
       }
       // decision at (j = lane) R picks taken
       const int sj = R ? s_idx : s_idx + lane, vj = R ? v_idx + lane : v_idx;
@@ -479,9 +499,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
     if (lane == 0) {
       double exact = 0.0, approx = 0.0;
       int j = 0;
+      long long fwait = 0;
       while (true) {
         const int slot = j % RING;
         int ready;
+        const long long tw0 = clock64();
         SpinGuard guard;
         while ((ready = vload(S.r_seq + slot)) != j + 1) {
           guard.tick();
@@ -491,6 +513,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
           }
           __nanosleep(32);
         }
+        fwait += clock64() - tw0;
         if (ready != j + 1) break;  // every published pick consumed
         exact += static_cast<const volatile double *>(S.r_w)[slot] - static_cast<const volatile double *>(S.r_cross)[slot];
         P.code[pb + j] = static_cast<const volatile int32_t *>(S.r_code)[slot];
@@ -506,6 +529,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       if (dbg) {
         dbg[60000 + blockIdx.x * 8 + 1] = j;
         dbg[60000 + blockIdx.x * 8 + 3] = static_cast<int>(clock64() - t_start);
+        dbg[60000 + blockIdx.x * 8 + 5] = static_cast<int>(fwait);
+        dbg[60000 + blockIdx.x * 8 + 6] = static_cast<int>(busy_cyc / 16);
       }
       P.n[h] = j;
       n_final[h] = j;
@@ -515,7 +540,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
     }
   } else {
     // ================================================= crossing sums
-    // (warps 4, 8, 12 share the producer's scheduler: they are consumers too)
+    // (warps 4, 8, 12 share the producer's scheduler: they are consumers too;
+    // measured: idling them starves the finalizer)
     while (true) {
       int j = 0;
       if (lane == 0) j = atomicAdd(&next_j, 1);
@@ -538,6 +564,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       }
       ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0);
       if (!ok) break;
+      const long long tb0 = clock64();
       const int slot = j % RING;
       const int32_t code = static_cast<const volatile int32_t *>(S.r_code)[slot];
       const int n_other = static_cast<const volatile int32_t *>(S.r_other)[slot];
@@ -553,45 +580,60 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
           if ((gs_smem ? S.gs[mid] : cells.pos(h, mid)) < idx) lo = mid + 1; else hi = mid;
         }
         const int okind = is_vert ? 0 : 1;
+        // crossing cells are sparse among the walked candidates: queue their
+        // sampled rows and evaluate them 32 at a time, one per lane, so each
+        // cell recompute (two L2 round trips) runs with the whole warp busy
+        int *q = S.hitq[warp];
+        int qn = 0;
+        const unsigned lt = (1u << lane) - 1u;
+        auto eval = [&](int n) {  // value of queue entries [0, n), lane i takes entry i
+          const bool act = lane < n;
+          const int r = act ? q[lane] : 0;
+          const int g = act ? (gs_smem ? S.gs[r] : cells.pos(h, r)) : 0;
+          if (act) sum += cells.value(h, r, g, is_vert ? idx : g - idx);
+        };
+        auto push = [&](bool hit, int r) {
+          const unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (hit) q[qn + __popc(b & lt)] = r;
+          qn += __popc(b);
+          __syncwarp();
+          if (qn >= 32) {
+            eval(32);
+            const int t = lane < qn - 32 ? q[32 + lane] : 0;
+            __syncwarp();
+            if (lane < qn - 32) q[lane] = t;
+            qn -= 32;
+            __syncwarp();
+          }
+        };
         if (tabs && n_other < n_rows - lo) {
           // walk the other kind's picked prefix: cell at g = idx + o if g is sampled
-          for (int i0 = 0; i0 < n_other; i0 += 32 * 4) {
-            int gg[4], rr[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int i = i0 + u * 32 + lane;
-              int o = -1;
-              if (i < n_other) o = i < win ? S.idx[okind][i] : __ldg(L.idx + lb + static_cast<int64_t>(okind) * n_total + i);
-              gg[u] = idx + o;
-              rr[u] = (o >= 0 && gg[u] < n_total) ? S.rowof[gg[u]] : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (rr[u] >= 0) sum += cells.value(h, rr[u], gg[u], is_vert ? idx : gg[u] - idx);
+          for (int i0 = 0; i0 < n_other; i0 += 32) {
+            const int i = i0 + lane;
+            int o = -1;
+            if (i < n_other) o = i < win ? S.idx[okind][i] : __ldg(L.idx + lb + static_cast<int64_t>(okind) * n_total + i);
+            const int g = idx + o;
+            const int r = (o >= 0 && g < n_total) ? S.rowof[g] : -1;
+            push(r >= 0, r);
           }
         } else {
           // walk the sampled rows: the other line o = g - idx is picked iff its
           // sorted position is below the prefix length
           const int32_t *inv_o = is_vert ? inv_s : inv_v;
-          for (int r0 = lo; r0 < n_rows; r0 += 32 * 4) {
-            int gg[4];
-            bool hit[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int r = r0 + u * 32 + lane;
-              hit[u] = false;
-              if (r < n_rows) {
-                gg[u] = gs_smem ? S.gs[r] : cells.pos(h, r);
-                const int o = gg[u] - idx;
-                const int pos = tabs ? static_cast<int>(S.inv[okind][o]) : __ldg(inv_o + o);
-                hit[u] = pos < n_other;
-              }
+          for (int r0 = lo; r0 < n_rows; r0 += 32) {
+            const int r = r0 + lane;
+            bool hit = false;
+            if (r < n_rows) {
+              const int g = gs_smem ? S.gs[r] : cells.pos(h, r);
+              const int o = g - idx;
+              const int pos = tabs ? static_cast<int>(S.inv[okind][o]) : __ldg(inv_o + o);
+              hit = pos < n_other;
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (hit[u]) sum += cells.value(h, r0 + u * 32 + lane, gg[u], is_vert ? idx : gg[u] - idx);
+            push(hit, r);
           }
         }
+        eval(qn);
+        __syncwarp();
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -599,6 +641,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         static_cast<volatile double *>(S.r_cross)[slot] = sum;
         __threadfence_block();
         static_cast<volatile int32_t *>(S.r_seq)[slot] = j + 1;
+        if (dbg) atomicAdd(&busy_cyc, static_cast<unsigned long long>(clock64() - tb0));
       }
     }
   }

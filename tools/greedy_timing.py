@@ -27,4 +27,6 @@ for t, (ro, n_new) in enumerate([(0, 5000), (5000, 5128), (10128, 5128), (10128,
     print(f"turn {t}: chain picks max {int(d[:, 0].max())} mean {float(d[:, 0].float().mean()):.0f}; "
           f"final picks max {int(d[:, 1].max())}; producer cycles max {int(d[:, 2].max())} "
           f"({float(d[:, 2].max()) / max(1, int(d[int(d[:, 2].argmax()), 0])):.0f}/pick); "
-          f"finalizer cycles max {int(d[:, 3].max())}; producer ring-full wait max {int(d[:, 4].max())}")
+          f"finalizer cycles max {int(d[:, 3].max())}; producer ring-full wait max {int(d[:, 4].max())}; "
+          f"finalizer wait (slowest head) {int(d[int(d[:, 3].argmax()), 5])}; consumer busy/16 (slowest head) "
+          f"{int(d[int(d[:, 3].argmax()), 6])} -> x16/13 warps = {int(d[int(d[:, 3].argmax()), 6]) * 16 // 13} per warp")
