@@ -156,10 +156,15 @@ class SessionEngine:
 
     # ------------------------------------------------------------- prefill
     def prefill(self, store: QKVStore, turn: int, row_offset: int, n_new: int, seed_rows: bool = True,
-                stream=None, turn_offset_heads: int = 0) -> PrefillOut:
+                stream=None, turn_offset_heads: int = 0, layer_ready=None, layer_done=None) -> PrefillOut:
         """Sparse prefill of one turn block for every layer. `turn_offset_heads`
         is the global index of local q-head 0 (head-sharded runs): sampling
-        seeds use global head ids (session.py:84-86)."""
+        seeds use global head ids (session.py:84-86).
+        layer_ready(l, stream): called before layer l's work is enqueued (a
+        caller streaming the block's Q/K/V in from the host makes `stream`
+        wait for layer l's rows there); layer_done(l, out, stream): called once
+        layer l's output is enqueued (e.g. to start its copy-out while the
+        next layer computes)."""
         p, sh = self.params, self.shape
         n_total = row_offset + n_new
         outs, plans_all, cells_all = [], [], []
@@ -177,7 +182,10 @@ class SessionEngine:
         n_seed = min(self.window, n_new)
         surv = p.comp.surviving_seeds(n_seed, p.max_new) if (seed_rows and p.mode == "loopserve") else 0
         st = self.stack
+        main = stream if stream is not None else torch.cuda.current_stream()
         for l in range(sh.n_layers):
+            if layer_ready is not None:
+                layer_ready(l, main)
             qb = store.q[l, :, row_offset:n_total]
             kl, vl = store.k[l], store.v[l]
             if p.mode == "dense":
@@ -185,6 +193,8 @@ class SessionEngine:
                                                   q_head_stride=store.q.stride(1), stream=stream))
                 plans_all.append(None)
                 cells_all.append(None)
+                if layer_done is not None:
+                    layer_done(l, outs[-1], main)
                 continue
             if self.head_groups > 1:
                 plans, out, cells, tiles = self._layer_groups(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
@@ -195,6 +205,8 @@ class SessionEngine:
                                                              self.ws, stream)
             self.tile_log.append(tiles)
             outs.append(out)
+            if layer_done is not None:
+                layer_done(l, out, main)
             plans_all.append(plans)
             cells_all.append(cells)
             self.cell_log.append(cells)
