@@ -207,7 +207,7 @@ int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t
  *   sel_ids  [hr][budget_cap], n_sel [hr]      picked ids (kvcompress.py:212)
  *   ck, cv   [hr][budget_cap][head_dim] bf16   compacted K/V of sel_ids
  *   partials [ls_decode_partials_size() bytes] fp32 split-K partials of a decode step
- *   counters [n_heads] int32, zeroed once: per-unit tickets (the last split combines)
+ *   counters [2 * n_heads] int32, zeroed once: per-unit split arrival / departure counts
  *                      Both may be NULL: splits then combine inside one thread-block
  *                      cluster (at most 16 splits per unit).
  *   n_a      [hr] int32  picked ids below the recent window at the current step

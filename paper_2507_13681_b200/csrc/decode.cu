@@ -399,7 +399,8 @@ struct KmMaps {
   CUtensorMap ck, cv, k, v;  // compacted cache [hr][budget_cap][D]; archive [kv][rows][D] (box 64 x 64)
 };
 
-constexpr int KM_GATHER_B = 8192;  // cluster combine: [n_split][G][D + 2] partials in rank 0
+// cluster combine: [n_split][G][D + 2] partials in rank 0 (dense variant: 16 splits x 8 heads)
+__host__ __device__ constexpr int km_gather_b(int NG) { return NG == 2 ? 16 * 8 * 130 * 4 : 8192; }
 
 // NW consumer warps x 16 rows = one tile of TILE K/V rows; NG such warp
 // groups take alternate tiles (ping-pong); + one producer warp
@@ -412,7 +413,8 @@ struct KmSmem {
   static constexpr int OFF_MG = OFF_BAR + 16 * NST;  // [2][8] (M, L) of the CTA / combine weights
   static constexpr int OFF_W = OFF_MG + 2 * 8 * 4;   // [8][KM_MAX_SPLIT] split weights
   static constexpr int OFF_GATHER = (OFF_W + 8 * KM_MAX_SPLIT * 4 + 15) / 16 * 16;
-  static constexpr int TOTAL = OFF_GATHER + KM_GATHER_B + 1024;  // + alignment slack
+  static constexpr int GATHER_B = km_gather_b(NG);
+  static constexpr int TOTAL = OFF_GATHER + GATHER_B + 1024;  // + alignment slack
   // after the tile loop the stage buffers hold the warp merge: m[W][8], l[W][8], o[W][8][D]
   static_assert((3 * NW * NG * 8 + NW * NG * 8 * D + 8) * 4 <= 2 * NST * TILE_B, "merge area");
 };
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     float *gl = reinterpret_cast<float *>(sm + L::OFF_GATHER);  // rank 0's gather area (cluster mode)
     float *dst = part + split * G * (D + 2);
     cg::cluster_group cluster = cg::this_cluster();
-    if (ccombine) dst = cluster.map_shared_rank(gl, 0) + split * G * (D + 2);
+    if (ccombine == 1) dst = cluster.map_shared_rank(gl, 0) + split * G * (D + 2);
     // per-warp scale factors once per head, then every element is an unrolled
     // sum of independent shared loads
     float *wsw = wo + KM_WARPS * 8 * D;  // [W][8]
@@ -735,11 +737,40 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       dst[i] = e == 0 ? wM[gg] : acc;
     }
     if (rec && tid == 0) rec[4] = gtime();
-    if (ccombine) {
+    int o_begin = 0, o_end = G * D;  // output elements this CTA writes
+    bool write_meta = true;
+    if (ccombine == 1) {
       // DSMEM pushes -> rank 0 (the gather area is outside the stage buffers: one cluster barrier)
       cluster.sync();
       if (split != 0) return;
       part = gl;
+    } else if (ccombine == 2) {
+      // every CTA of the grid is resident (checked at launch): all splits wait
+      // for the unit's last partial, then each combines its own slice of the
+      // outputs -- no single-CTA tail
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(S.counters + unit, 1);
+        const volatile int *arr = S.counters + unit;
+        long long t0 = -1;
+        unsigned n = 0;
+        while (*arr < n_split) {
+          __nanosleep(32);
+          if ((++n & 1023u) == 0u) {  // a protocol bug traps instead of hanging the device
+            const long long now = clock64();
+            if (t0 < 0) t0 = now;
+            else if (now - t0 > 20000000000LL) __trap();
+          }
+        }
+      }
+      __syncthreads();
+      __threadfence();
+      if (rec && tid == 0) rec[9] = gtime();
+      const int per = (G * D + n_split - 1) / n_split;
+      o_begin = min(G * D, split * per);
+      o_end = min(G * D, o_begin + per);
+      write_meta = split == 0;
     } else {
       __threadfence();
       if (rec && tid == 0) rec[8] = gtime();
@@ -756,6 +787,24 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       if (n_el * 4 <= 2 * NST * L::TILE_B) {
         float *stg = reinterpret_cast<float *>(sm);
         constexpr int B = 16;  // independent loads in flight per thread
+        if ((G * (D + 2)) % 4 == 0) {  // 16-B loads: every partial block is 16-B aligned
+          const float4 *src4 = reinterpret_cast<const float4 *>(part);
+          float4 *stg4 = reinterpret_cast<float4 *>(stg);
+          const int n4 = n_el / 4;
+          for (int i0 = tid; i0 < n4; i0 += KM_THREADS * B) {
+            float4 v[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+              const int i = i0 + u * KM_THREADS;
+              v[u] = i < n4 ? __ldcg(src4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+              const int i = i0 + u * KM_THREADS;
+              if (i < n4) stg4[i] = v[u];
+            }
+          }
+        } else
         for (int i0 = tid; i0 < n_el; i0 += KM_THREADS * B) {
           float v[B];
 #pragma unroll
@@ -799,10 +848,10 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       }
     }
     __syncthreads();
-    for (int i = tid; i < G * D; i += KM_THREADS) {
+    for (int i = o_begin + tid; i < o_end; i += KM_THREADS) {
       const int gg = i / D, e = i % D;
       float acc = 0.f;
-#pragma unroll 4
+#pragma unroll 8
       for (int r = 0; r < n_split; ++r)
         acc = fmaf(wsc[gg * KM_MAX_SPLIT + r], ldp(part + (r * G + gg) * (D + 2) + 2 + e), acc);
       const float res = acc / mg[8 + gg];
@@ -812,14 +861,23 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       else
         reinterpret_cast<float *>(out)[oi] = res;
     }
-    if (tid < G) {
+    if (write_meta && tid < G) {
       const int64_t hr = head_row(S, layer, h0 + tid);
       S.ring_ml[(hr * S.window + slot) * 2 + 0] = mg[tid];
       S.ring_ml[(hr * S.window + slot) * 2 + 1] = mg[8 + tid];
       S.ring_n[hr * S.window + slot] = geo.n_cols;
       S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
     }
-    if (tid == 0 && !ccombine) S.counters[unit] = 0;  // ticket re-armed for the next launch
+    if (ccombine == 0 && tid == 0) S.counters[unit] = 0;  // ticket re-armed for the next launch
+    if (ccombine == 2) {
+      // departures: the last CTA to leave re-arms both counters (every CTA has
+      // stopped polling the arrival count by then)
+      __syncthreads();
+      if (tid == 0 && atomicAdd(S.counters + S.n_heads + unit, 1) == n_split - 1) {
+        S.counters[unit] = 0;
+        S.counters[S.n_heads + unit] = 0;
+      }
+    }
     if (rec && tid == 0) rec[6] = gtime();
   }
 }
@@ -1330,8 +1388,38 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
                              : std::max(1, env_cta_mult * n_sm / units);
   n_split = std::max(1, std::min({n_split, tiles, dec::KM_MAX_SPLIT}));
   // splits combine in rank 0's shared memory when they fit one portable cluster
-  const int ccombine = !env_no_cluster && n_split > 1 && n_split <= 8 &&
-                       n_split * G * (D + 2) * 4 <= dec::KM_GATHER_B;
+  static const bool env_dense_cluster = getenv("LS_K6_DENSE_CLUSTER") != nullptr;
+  static int max_cl = 0;
+  if (!max_cl) {  // 16-CTA clusters need the non-portable opt-in
+    max_cl = 8;
+    if (cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+      max_cl = 16;
+    cudaGetLastError();
+  }
+  if (!compressed && env_dense_cluster && env_split <= 0) n_split = std::min(n_split, max_cl);
+  const int cl_cap = compressed ? 8 : max_cl;
+  const int gather_b = compressed ? dec::km_gather_b(NG_C) : dec::km_gather_b(NG_D);
+  int ccombine = !env_no_cluster && n_split > 1 && n_split <= cl_cap && n_split * G * (D + 2) * 4 <= gather_b;
+  if (!ccombine && n_split > 1) {
+    // all splits wait for each other only if every CTA of the grid is resident
+    static int resident_d = -1, resident_c = -1;
+    int &res = compressed ? resident_c : resident_d;
+    if (res < 0) {
+      int per_sm = 0;
+      if (compressed)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C>,
+                                                      32 * (NW_C * NG_C + 1), smem_c);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>,
+                                                      32 * (NW_D * NG_D + 1), smem_d);
+      cudaGetLastError();
+      res = per_sm * n_sm;
+    }
+    // (measured at C2: no faster than the last-CTA combine; LS_K6_ALL_CTA=1 selects it)
+    static const bool env_all_cta = getenv("LS_K6_ALL_CTA") != nullptr;
+    if (env_all_cta && n_split * units <= res) ccombine = 2;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_split, units, 1);
   cfg.blockDim = dim3(32 * ((compressed ? NW_C * NG_C : NW_D * NG_D) + 1), 1, 1);
@@ -1339,9 +1427,9 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (ccombine) {
+  if (ccombine == 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = n_split;
+    attr[na].val.clusterDim.x = n_split;  // (ccombine == 1 only)
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;

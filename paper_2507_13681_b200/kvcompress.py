@@ -115,7 +115,7 @@ class DecodeStack:
         self.n_sel = torch.zeros(HR, dtype=i32, device=dev)
         self.ck = torch.zeros((HR, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
         self.cv = torch.zeros((HR, self.budget_cap, head_dim), dtype=torch.bfloat16, device=dev)
-        self.counters = torch.zeros(n_heads, dtype=i32, device=dev)
+        self.counters = torch.zeros(2 * n_heads, dtype=i32, device=dev)  # split-K arrivals, departures
         self.step_t = torch.zeros(4, dtype=i32, device=dev)
         self.n_a = torch.zeros(HR, dtype=i32, device=dev)
         self.retained_n = torch.zeros(HR, dtype=i32, device=dev)

@@ -145,3 +145,18 @@ def test_head_group_pipeline_identical(cuda_lib):
                 assert torch.equal(r.plans[l].vert_ids[h, :cn[h, 1]], r1.plans[l].vert_ids[h, :cn[h, 1]])
             assert torch.equal(r.cells[l], r1.cells[l])
         assert torch.equal(ring, ring1)  # seed rows
+
+
+def test_prefill_layer_hooks(cuda_lib):
+    """layer_ready / layer_done bracket every layer in order and do not change
+    the results (bench.py's e2e streams Q/K/V in and outputs out through them)."""
+    eng, store, n_new, _ = _engine(n_layers=3)
+    ref = eng.prefill(store, 0, 0, n_new)
+    calls = []
+    res = eng.prefill(store, 0, 0, n_new, layer_ready=lambda l, s: calls.append(("ready", l)),
+                      layer_done=lambda l, o, s: calls.append(("done", l, o.data_ptr())))
+    torch.cuda.synchronize()
+    assert [c[:2] for c in calls] == [(k, l) for l in range(3) for k in ("ready", "done")]
+    for l in range(3):
+        assert calls[2 * l + 1][2] == res.out[l].data_ptr()
+        assert torch.equal(res.out[l], ref.out[l])
