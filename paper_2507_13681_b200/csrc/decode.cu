@@ -523,14 +523,21 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
   const int n_my = t_end - t_begin;
   const int64_t hr0 = head_row(S, layer, h0);
 
+  __shared__ __align__(8) uint64_t gbar;  // cluster combine: rank 0 receives the other splits' partials
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], NW);  // the warps of the group that consumes the stage
     }
+    if (ccombine == 1 && split == 0) tc::mbar_init(&gbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ccombine == 1 && split == 0)  // armed before any split can send (cluster barrier below)
+      tc::mbar_expect_tx(&gbar, static_cast<uint32_t>((n_split - 1) * G * (D + 2) * 4));
   }
   __syncthreads();
+  // cluster combine: this arrive (paired with the wait before the sends) orders
+  // rank 0's armed mbarrier before every split's st.async
+  if (ccombine == 1) asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
 
   if (warp == KM_WARPS) {
     // ---- producer: TMA K and V tiles of this split (independent of the previous kernel)
@@ -707,9 +714,13 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     float *wo = wl + KM_WARPS * 8;
     float *part = S.partials + static_cast<int64_t>(unit) * n_split * G * (D + 2);
     float *gl = reinterpret_cast<float *>(sm + L::OFF_GATHER);  // rank 0's gather area (cluster mode)
-    float *dst = part + split * G * (D + 2);
-    cg::cluster_group cluster = cg::this_cluster();
-    if (ccombine == 1) dst = cluster.map_shared_rank(gl, 0) + split * G * (D + 2);
+    float *dst = ccombine == 1 ? gl : part + split * G * (D + 2);  // rank 0 keeps its own partial locally
+    uint32_t rgl = 0, rbar = 0;
+    if (ccombine == 1) {
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rgl) : "r"(tc::smem_u32(gl)));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rbar) : "r"(tc::smem_u32(&gbar)));
+    }
     // per-warp scale factors once per head, then every element is an unrolled
     // sum of independent shared loads
     float *wsw = wo + KM_WARPS * 8 * D;  // [W][8]
@@ -734,15 +745,25 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
         for (int w = 0; w < KM_WARPS; ++w)
           acc = fmaf(wsw[w * 8 + gg], e == 1 ? wl[w * 8 + gg] : wo[(w * 8 + gg) * D + e - 2], acc);
       }
-      dst[i] = e == 0 ? wM[gg] : acc;
+      const float val = e == 0 ? wM[gg] : acc;
+      if (ccombine == 1 && split != 0)  // straight into rank 0's gather area, counted on its mbarrier
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                         rgl + 4u * static_cast<uint32_t>(split * G * (D + 2) + i)),
+                     "r"(__float_as_uint(val)), "r"(rbar)
+                     : "memory");
+      else
+        dst[i] = val;
     }
     if (rec && tid == 0) rec[4] = gtime();
     int o_begin = 0, o_end = G * D;  // output elements this CTA writes
     bool write_meta = true;
     if (ccombine == 1) {
-      // DSMEM pushes -> rank 0 (the gather area is outside the stage buffers: one cluster barrier)
-      cluster.sync();
+      // the other splits' partials arrive by st.async on rank 0's mbarrier: no
+      // cluster barrier (whose release would wait for every CTA's global stores)
       if (split != 0) return;
+      __syncthreads();  // rank 0's own partial
+      if (tid == 0) tc::mbar_wait(&gbar, 0);
+      __syncthreads();
       part = gl;
     } else if (ccombine == 2) {
       // every CTA of the grid is resident (checked at launch): all splits wait
