@@ -1368,7 +1368,13 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
   // alternate 64-row tiles, 4 stages, one CTA per SM; compressed steps (~17 x
   // 64 rows per head): 4 warps, 3 stages, two CTAs per SM (the next layer's
   // CTAs start their prefetch beside this layer's). Measured: tools/sweep_dec.sh
-  constexpr int NST_D = 4, NW_D = 4, NG_D = 2, NST_C = 3, NW_C = 4, NG_C = 1;
+#ifndef LS_K6_NST_C
+#define LS_K6_NST_C 3
+#endif
+#ifndef LS_K6_NG_C
+#define LS_K6_NG_C 1
+#endif
+  constexpr int NST_D = 4, NW_D = 4, NG_D = 2, NST_C = LS_K6_NST_C, NW_C = 4, NG_C = LS_K6_NG_C;
   const int tile = compressed ? 16 * NW_C : 16 * NW_D;
   dec::KmMaps maps;
   const int HR = S->n_layers * S->n_heads;

@@ -480,17 +480,26 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
-// fixed point -> fp64 line weights; total = exact integer sum of the verticals
-__global__ void k1_finish_kernel(const unsigned long long *vfix, const unsigned int *vmaxb,
+// fixed point -> fp64 line weights; total = exact integer sum of the verticals.
+// Grid (column chunk, head): every CTA converts its chunk and adds its integer
+// partial sums to the head's accumulators (integer addition: order-free, so
+// the result is bit-identical whatever the schedule); the head's last CTA
+// (ticket) writes total and the op count and re-arms the accumulators.
+constexpr int FIN_THREADS = 256;
+constexpr int FIN_CHUNK = 2048;
+__global__ void __launch_bounds__(FIN_THREADS) k1_finish_kernel(const unsigned long long *vfix, const unsigned int *vmaxb,
                                  const unsigned long long *sfix, const unsigned int *smaxb, const int32_t *rows,
                                  int n_s, int n_total, int row_offset, double *v_w, float *v_max, double *s_w,
-                                 float *s_max, double *total, int64_t *score_count) {
-  __shared__ unsigned long long red[32];
-  __shared__ long long redc[32];
-  const int h = blockIdx.x;
+                                 float *s_max, double *total, int64_t *score_count, unsigned long long *acc_tot,
+                                 unsigned long long *acc_cnt, unsigned int *ticket) {
+  __shared__ unsigned long long red[FIN_THREADS / 32];
+  __shared__ long long redc[FIN_THREADS / 32];
+  __shared__ int last;
+  const int ck = blockIdx.x, h = blockIdx.y;
+  const int c0 = ck * FIN_CHUNK, c1 = min(n_total, c0 + FIN_CHUNK);
   unsigned long long sum = 0;
   long long cnt = 0;
-  for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
+  for (int i = c0 + threadIdx.x; i < c1; i += FIN_THREADS) {
     const int64_t o = static_cast<int64_t>(h) * n_total + i;
     const unsigned long long vf = vfix[o];
     sum += vf;
@@ -499,9 +508,11 @@ __global__ void k1_finish_kernel(const unsigned long long *vfix, const unsigned 
     s_w[o] = static_cast<double>(sfix[o]) * UNFIX;
     s_max[o] = __uint_as_float(smaxb[o]);
   }
-  for (int r = threadIdx.x; r < n_s; r += blockDim.x) {
+  // op count (prefill.py:386-389): the sampled rows, split across the chunks
+  const int per = (n_s + gridDim.x - 1) / gridDim.x;
+  for (int r = ck * per + threadIdx.x; r < min(n_s, (ck + 1) * per); r += FIN_THREADS) {
     const long long g = row_offset + rows[static_cast<int64_t>(h) * n_s + r];
-    cnt += min(g, static_cast<long long>(n_total - 1)) + 1;  // prefill.py:386-389
+    cnt += min(g, static_cast<long long>(n_total - 1)) + 1;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -516,12 +527,23 @@ __global__ void k1_finish_kernel(const unsigned long long *vfix, const unsigned 
   if (threadIdx.x == 0) {
     unsigned long long s = 0;
     long long c = 0;
-    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+    for (int i = 0; i < FIN_THREADS / 32; ++i) {
       s += red[i];
       c += redc[i];
     }
-    total[h] = static_cast<double>(s) * UNFIX;
-    score_count[h] = c;
+    atomicAdd(acc_tot + h, s);
+    atomicAdd(acc_cnt + h, static_cast<unsigned long long>(c));
+    __threadfence();
+    last = atomicAdd(ticket + h, 1u) == gridDim.x - 1;
+    if (last) {
+      __threadfence();
+      const unsigned long long ts = atomicAdd(acc_tot + h, 0ull), tc = atomicAdd(acc_cnt + h, 0ull);
+      total[h] = static_cast<double>(ts) * UNFIX;
+      score_count[h] = static_cast<long long>(tc);
+      acc_tot[h] = 0ull;
+      acc_cnt[h] = 0ull;
+      ticket[h] = 0u;
+    }
   }
 }
 
@@ -531,7 +553,7 @@ size_t score_lines_tc_workspace(const ls_layer_desc *L, int32_t n_s) {
   const size_t n_rt = (n_s + k1tc::BM - 1) / k1tc::BM;
   const size_t n_ch = (L->n_total + k1tc::CHUNK - 1) / k1tc::CHUNK;
   const size_t H = L->n_heads;
-  return H * n_rt * n_ch * k1tc::BM * sizeof(float2) + H * L->n_total * (8 + 8 + 4 + 4) + 6 * 256 + 4096;
+  return H * n_rt * n_ch * k1tc::BM * sizeof(float2) + H * L->n_total * (8 + 8 + 4 + 4) + H * 24 + 8 * 256 + 4096;
 }
 
 int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
@@ -560,10 +582,12 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
   p.sfix = c.take<unsigned long long>(H * L->n_total);
   p.vmaxb = c.take<unsigned int>(H * L->n_total);
   p.smaxb = c.take<unsigned int>(H * L->n_total);
-  LS_CUDA(cudaMemsetAsync(p.vfix, 0, H * L->n_total * 8, st));
-  LS_CUDA(cudaMemsetAsync(p.sfix, 0, H * L->n_total * 8, st));
-  LS_CUDA(cudaMemsetAsync(p.vmaxb, 0, H * L->n_total * 4, st));
-  LS_CUDA(cudaMemsetAsync(p.smaxb, 0, H * L->n_total * 4, st));
+  unsigned long long *fin_tot = c.take<unsigned long long>(H);
+  unsigned long long *fin_cnt = c.take<unsigned long long>(H);
+  unsigned int *fin_tick = c.take<unsigned int>(H);
+  // line accumulators and finish counters are consecutive in the workspace (shared
+  // with other entries, so zeroed per call): one memset
+  LS_CUDA(cudaMemsetAsync(p.vfix, 0, reinterpret_cast<char *>(fin_tick + H) - reinterpret_cast<char *>(p.vfix), st));
   dim3 grid(p.n_chunks, p.n_rt, L->n_heads);
   CUtensorMap tmk;
   int st_map = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride);
@@ -584,8 +608,12 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
     k1tc::k1_lines_kernel<64><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
   }
   LS_LAUNCH_CHECK("k1_lines_kernel");
-  k1tc::k1_finish_kernel<<<L->n_heads, 512, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
-                                                     L->row_offset, v_w, v_max, s_w, s_max, total, score_count);
+  {
+    const dim3 fg((L->n_total + k1tc::FIN_CHUNK - 1) / k1tc::FIN_CHUNK, L->n_heads);
+    k1tc::k1_finish_kernel<<<fg, k1tc::FIN_THREADS, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
+                                                           L->row_offset, v_w, v_max, s_w, s_max, total, score_count,
+                                                           fin_tot, fin_cnt, fin_tick);
+  }
   LS_LAUNCH_CHECK("k1_finish_kernel");
   return LS_OK;
 }

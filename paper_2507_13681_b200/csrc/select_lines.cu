@@ -787,8 +787,9 @@ inline SortWork carve_sort(Carver &c, int H, int n_total) {
 int run_tail(Work &w, int H, int n_total, double alpha, const double *total, int32_t *slash_ids,
              int32_t *vert_ids, int32_t *counts, double *coverage, double *approx, int32_t *picks_out,
              int32_t *n_picks_out, cudaStream_t st) {
-  LS_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * H * w.words, st));
-  LS_CUDA(cudaMemsetAsync(w.vbits, 0, sizeof(uint32_t) * H * w.words, st));
+  // sbits and vbits are consecutive in the workspace: one memset
+  LS_CUDA(cudaMemsetAsync(w.sbits, 0, reinterpret_cast<char *>(w.vbits + static_cast<size_t>(H) * w.words) -
+                                          reinterpret_cast<char *>(w.sbits), st));
   plan_bits_kernel<<<dim3(8, H), 256, 0, st>>>(w.picks, w.cap, w.n_final, n_total, w.words, w.sbits, w.vbits,
                                                picks_out);
   LS_LAUNCH_CHECK("plan_bits_kernel");

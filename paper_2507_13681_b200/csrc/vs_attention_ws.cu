@@ -1159,8 +1159,9 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   uint16_t *kc = c.take<uint16_t>(static_cast<size_t>(H) * vcap * d);
   uint16_t *vc = c.take<uint16_t>(static_cast<size_t>(H) * vcap * d);
   if (!dense) {
-    LS_CUDA(cudaMemsetAsync(vbits, 0, sizeof(uint32_t) * H * (words + 8), st));
-    LS_CUDA(cudaMemsetAsync(rsbits, 0, sizeof(uint32_t) * H * (words + 8), st));
+    // vbits and rsbits are consecutive in the workspace: one memset
+    LS_CUDA(cudaMemsetAsync(vbits, 0, reinterpret_cast<char *>(rsbits + static_cast<size_t>(H) * (words + 8)) -
+                                          reinterpret_cast<char *>(vbits), st));
     k5ws::vert_bits_kernel<<<dim3(4, H), 256, 0, st>>>(vert_ids, counts, L->n_total, words, vbits);
     k5ws::reverse_bits_kernel<<<dim3(4, H), 256, 0, st>>>(slash_ids, counts, L->n_total, words, rsbits);
     k5ws::gather_verticals_kernel<<<dim3(32, H), 256, 0, st>>>(k, v, vert_ids, counts, L->n_total,
