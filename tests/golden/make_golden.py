@@ -146,6 +146,10 @@ DECODE_CASES = [
     ("decode_warmup_lt_window", dict(n_q=2, n_kv=2, d=128, n_pos=300 + 30, seed=23), 300, 30, 40, 6, 3, 12, 12),
     ("decode_nobudget", dict(n_q=2, n_kv=1, d=64, n_pos=64 + 20, seed=24), 64, 20, None, 4, 4, None, 4),
     ("decode_huge_budget", dict(n_q=2, n_kv=1, d=64, n_pos=64 + 20, seed=25), 64, 20, 10_000, 4, 4, None, 4),
+    # GQA groups 7 (Qwen2.5-7B) and 8 (Llama-70B) and a longer cache (several tiles per split)
+    ("decode_gqa7", dict(n_q=7, n_kv=1, d=128, n_pos=400 + 40, seed=26), 400, 40, 64, 8, 8, None, 8),
+    ("decode_gqa8", dict(n_q=8, n_kv=1, d=128, n_pos=700 + 48, seed=27), 700, 48, 96, 16, 16, None, 16),
+    ("decode_long", dict(n_q=4, n_kv=1, d=128, n_pos=1500 + 40, seed=28), 1500, 40, 300, 8, 8, None, 8),
 ]
 
 

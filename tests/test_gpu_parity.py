@@ -261,7 +261,7 @@ def test_topb_hand_cases(cuda_lib):  # test_kvcompress.py:94-111
 
 
 DECODE = ["decode_small", "decode_window_gt_interval", "decode_warmup_lt_window", "decode_nobudget",
-          "decode_huge_budget"]
+          "decode_huge_budget", "decode_gqa7", "decode_gqa8", "decode_long"]
 
 
 @pytest.mark.parametrize("name", DECODE)

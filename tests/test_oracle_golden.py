@@ -168,7 +168,7 @@ def test_prefill_oracle_matches_reference(golden, name):
 
 
 DECODE = ["decode_small", "decode_window_gt_interval", "decode_warmup_lt_window",
-          "decode_nobudget", "decode_huge_budget"]
+          "decode_nobudget", "decode_huge_budget", "decode_gqa7", "decode_gqa8", "decode_long"]
 
 
 @pytest.mark.parametrize("name", DECODE)
