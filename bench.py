@@ -398,6 +398,7 @@ def main():
             break
 
     dense = None if args.no_dense else dense_baseline(cfg, store, blocks, shard, ttft)
+    quality = None if args.no_dense else plan_quality(cfg, eng, store, blocks, shard)
 
     e2e = None
     if not args.no_e2e:
@@ -415,7 +416,8 @@ def main():
             "decode_tokens_per_s": round(tok_s, 2),
             "prefill_ms_per_turn": round(ttft, 3), "decode_ms_per_turn": round(decode_ms / n_prefills, 3),
             "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-            "decode_roofline": dec_roof, "prefill_roofline": pre_roof, "dense_baseline": dense}
+            "decode_roofline": dec_roof, "prefill_roofline": pre_roof, "dense_baseline": dense,
+            "plan_quality": quality}
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -521,6 +523,35 @@ def dense_baseline(cfg, store, blocks, shard, sparse_ttft):
             "decode_tokens_per_s_last_turn": round(cfg["max_new"] / (dec_ms * 1e-3), 2),
             "note": "dense causal attention of the same turn blocks (K5 dense mode, all layers), one pass; "
                     "full-cache decode (no compression) of the last turn's max_new tokens"}
+
+
+def plan_quality(cfg, eng, store, blocks, shard):
+    """full-block coverage (coverage_ratio, prefill.py:254-281,
+    on the device) of the last turn's sampled-row plans, first and last layer,
+    beside the greedy's own sampled-row coverage. Outside the timed region."""
+    import torch
+
+    from paper_2507_13681_b200.tensor_ops import plan_coverage_layer
+
+    t = len(blocks) - 1
+    ro, n_new = blocks[t]
+    n_total = ro + n_new
+    res = eng.prefill(store, t, ro, n_new, turn_offset_heads=shard.q_begin)
+    full, sampled = [], []
+    for l in (0, cfg["n_layers"] - 1):
+        p = res.plans[l]
+        cov = plan_coverage_layer(store.q[l, :, ro:n_total], store.k[l], store.v[l], p.slash_ids, p.vert_ids,
+                                  p.counts, n_new, n_total, shard.n_kv_local, q_head_stride=store.q.stride(1))
+        full.append(cov)
+        sampled.append(p.coverage)
+    full, sampled = torch.cat(full), torch.cat(sampled)
+    torch.cuda.synchronize()
+    return {"full_block_coverage_mean": round(float(full.mean()), 4),
+            "full_block_coverage_min": round(float(full.min()), 4),
+            "sampled_row_coverage_mean": round(float(sampled.mean()), 4),
+            "alpha": cfg["alpha"], "layers": [0, cfg["n_layers"] - 1], "turn": t + 1,
+            "note": "coverage_ratio of each q-head's plan over the block's dense causal attention (all rows) vs "
+                    "the greedy's coverage of the sampled rows it was built from"}
 
 
 def run_e2e(args, cfg, eng, store, blocks, shard, gather):

@@ -190,6 +190,19 @@ int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16_t *q, cons
 int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k,
                        const uint16_t *v, void *out, int32_t out_bf16, ls_stream_t stream);
 
+/* ----------------------------------------------------- plan diagnostics ---
+ * coverage_ratio (prefill.py:254-281) for every head of
+ * a layer: the fraction of the block's FULL causal attention mass (all n_new
+ * rows, dense softmax) covered by the plan's lines -- inclusion-exclusion over
+ * the single crossing cells == the mass of the union of plan cells. Runs K1's
+ * statistics pass over every row (dense normaliser) and K5 with per-row
+ * plan-cell normalisers; coverage[h] = mean_r 2^(lse_plan - lse_full).
+ * Workspace: ls_plan_coverage_workspace(L) bytes. */
+size_t ls_plan_coverage_workspace(const ls_layer_desc *L);
+int ls_plan_coverage(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                     const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts,
+                     double *coverage, void *ws, size_t ws_bytes, ls_stream_t stream);
+
 /* ------------------------------------------------------------- decode ---
  * Decode state of ALL layers of one session, caller-allocated device arrays
  * (see paper_2507_13681_b200/kvcompress.py DecodeStack). The step counters

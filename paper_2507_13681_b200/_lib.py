@@ -69,6 +69,8 @@ SIGNATURES = {
     "ls_vs_attention_ex": (C.c_int, [LD, P, P, P, P, P, P, P, I32, P, P, P, SZ, P]),
     "ls_plan_rows": (C.c_int, [LD, I32, P, P, P, P, P, P, I64, I64, P]),
     "ls_dense_attention": (C.c_int, [LD, P, P, P, P, I32, P]),
+    "ls_plan_coverage_workspace": (SZ, [LD]),
+    "ls_plan_coverage": (C.c_int, [LD, P, P, P, P, P, P, P, P, SZ, P]),
     "ls_decode_partials_size": (SZ, [DS, I32]),
     "ls_decode_step": (C.c_int, [DS, I32, P, P, P, I32, I32, P, I32, P]),
     "ls_decode_step_archive": (C.c_int, [DS, I32, P, I64, P, P, I32, I32, P, I32, I32, P]),
@@ -111,6 +113,7 @@ def check(status: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 5, "ls_greedy_dense": 5,
     "ls_vs_attention": 3, "ls_vs_attention_ex": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
+    "ls_plan_coverage": 7,
     "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
 }
 launch_count = 0

@@ -547,6 +547,23 @@ __global__ void __launch_bounds__(FIN_THREADS) k1_finish_kernel(const unsigned l
   }
 }
 
+// per sampled row: merge the chunk statistics in chunk order (as k1_lines does)
+// into log2-sum-exp2 = m + log2(l) over all causal columns (ls_plan_coverage)
+__global__ void row_lse_kernel(const float2 *pstats, int n_s, int n_rt, int n_chunks, float *lse) {
+  const int h = blockIdx.y, r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_s) return;
+  const float2 *ps = pstats + (static_cast<int64_t>(h) * n_rt + r / BM) * n_chunks * BM + (r % BM);
+  float m = -INFINITY, l = 0.f;
+  for (int c = 0; c < n_chunks; ++c) {
+    const float2 v = ps[static_cast<int64_t>(c) * BM];
+    if (v.x == -INFINITY) continue;
+    const float mn = fmaxf(m, v.x);
+    l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
+    m = mn;
+  }
+  lse[static_cast<int64_t>(h) * n_s + r] = l > 0.f ? m + __log2f(l) : -INFINITY;
+}
+
 }  // namespace k1tc
 
 size_t score_lines_tc_workspace(const ls_layer_desc *L, int32_t n_s) {
@@ -615,6 +632,46 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
                                                            fin_tot, fin_cnt, fin_tick);
   }
   LS_LAUNCH_CHECK("k1_finish_kernel");
+  return LS_OK;
+}
+
+// K1 pass 1 only, for the rows given: log2-sum-exp2 of every row over all its
+// causal columns (the dense softmax normaliser), [H][n_s]
+int score_row_lse(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
+                  float *lse, void *ws, size_t ws_bytes, cudaStream_t st) {
+  LS_REQUIRE(ws_bytes >= score_lines_tc_workspace(L, n_s), LS_ERR_WORKSPACE, "row_lse workspace too small");
+  k1tc::Params p{};
+  p.q = q;
+  p.k = k;
+  p.rows = rows;
+  p.n_heads = L->n_heads;
+  p.group = L->n_heads / L->n_kv_heads;
+  p.n_s = n_s;
+  p.n_total = L->n_total;
+  p.row_offset = L->row_offset;
+  p.n_rt = (n_s + k1tc::BM - 1) / k1tc::BM;
+  p.n_chunks = (L->n_total + k1tc::CHUNK - 1) / k1tc::CHUNK;
+  p.q_head_stride = L->q_head_stride;
+  p.kv_head_stride = L->kv_head_stride;
+  p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
+  Carver c(ws, ws_bytes);
+  p.pstats = c.take<float2>(static_cast<size_t>(L->n_heads) * p.n_rt * p.n_chunks * k1tc::BM);
+  dim3 grid(p.n_chunks, p.n_rt, L->n_heads);
+  CUtensorMap tmk;
+  int st_map = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride);
+  if (st_map) return st_map;
+  if (L->head_dim == 128) {
+    const int s1 = k1tc::StatsSmem<128>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    k1tc::k1_stats_kernel<128><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
+  } else {
+    const int s1 = k1tc::StatsSmem<64>::TOTAL;
+    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    k1tc::k1_stats_kernel<64><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
+  }
+  LS_LAUNCH_CHECK("k1_stats_kernel");
+  k1tc::row_lse_kernel<<<dim3((n_s + 255) / 256, L->n_heads), 256, 0, st>>>(p.pstats, n_s, p.n_rt, p.n_chunks, lse);
+  LS_LAUNCH_CHECK("row_lse_kernel");
   return LS_OK;
 }
 

@@ -412,7 +412,37 @@ size_t vs_attention_ws_workspace(const ls_layer_desc *L);
 int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
                     const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
                     int32_t out_bf16, int64_t *cells, int64_t *tiles, int dense, void *ws, size_t ws_bytes,
-                    cudaStream_t st);
+                    cudaStream_t st, float *row_lse = nullptr);
+size_t score_lines_tc_workspace(const ls_layer_desc *L, int32_t n_s);
+int score_row_lse(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
+                  float *lse, void *ws, size_t ws_bytes, cudaStream_t st);
+
+namespace cov {
+__global__ void iota_rows_kernel(int32_t *rows, int n) {
+  const int h = blockIdx.y;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    rows[static_cast<int64_t>(h) * n + r] = r;
+}
+// coverage[h] = (1/n) sum_r 2^(lse_plan[r] - lse_full[r]): the full-softmax mass
+// of each row's plan cells, averaged over the block's rows (every row sums to 1)
+__global__ void coverage_kernel(const float *lse_plan, const float *lse_full, int n, double *coverage) {
+  __shared__ double red[32];
+  const int h = blockIdx.x;
+  double sum = 0.0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const float lp = lse_plan[static_cast<int64_t>(h) * n + r], lf = lse_full[static_cast<int64_t>(h) * n + r];
+    if (lp != -INFINITY) sum += static_cast<double>(exp2f(fminf(lp - lf, 0.f)));
+  }
+  sum = warp_sum_d(sum);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    coverage[h] = n > 0 ? t / n : 0.0;
+  }
+}
+}  // namespace cov
 }  // namespace ls
 
 extern "C" size_t ls_vs_attention_workspace(const ls_layer_desc *L) {
@@ -550,4 +580,52 @@ extern "C" int ls_dense_attention(const ls_layer_desc *L, const uint16_t *q, con
   int s = vs_attention_ws(L, q, k, v, nullptr, nullptr, nullptr, out, out_bf16, cells, nullptr, 1, nullptr, 0, st);
   LS_CUDA(cudaFreeAsync(cells, st));
   return s;
+}
+
+// ------------------------------------------------------------ plan coverage
+// coverage_ratio (reference prefill.py:254-281) for every head of a layer: the
+// fraction of the block's full (dense, causal) attention mass that the plan's
+// lines cover, by inclusion-exclusion == the mass of the union of plan cells.
+// Per row: dense normaliser from K1's statistics pass over all rows, plan-cell
+// normaliser from K5 (row_lse), mass = 2^(lse_plan - lse_full).
+static size_t cov_align(size_t x) { return (x + 255) / 256 * 256; }
+
+extern "C" size_t ls_plan_coverage_workspace(const ls_layer_desc *L) {
+  const size_t H = L->n_heads, n = L->n_new;
+  return 3 * cov_align(H * n * 4) + cov_align(n * H * L->head_dim * 2) + cov_align(H * 8) +
+         cov_align(score_lines_tc_workspace(L, L->n_new)) + cov_align(ls_vs_attention_workspace(L)) + 1024;
+}
+
+extern "C" int ls_plan_coverage(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts,
+                                double *coverage, void *ws, size_t ws_bytes, ls_stream_t stream) {
+  int stc = k5::check_desc(L);
+  if (stc) return stc;
+  LS_REQUIRE(ws_bytes >= ls_plan_coverage_workspace(L), LS_ERR_WORKSPACE, "plan coverage workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int H = L->n_heads, n = L->n_new;
+  char *b = static_cast<char *>(ws);
+  int32_t *rows = reinterpret_cast<int32_t *>(b);
+  b += cov_align(static_cast<size_t>(H) * n * 4);
+  float *lse_full = reinterpret_cast<float *>(b);
+  b += cov_align(static_cast<size_t>(H) * n * 4);
+  float *lse_plan = reinterpret_cast<float *>(b);
+  b += cov_align(static_cast<size_t>(H) * n * 4);
+  void *out = b;
+  b += cov_align(static_cast<size_t>(n) * H * L->head_dim * 2);
+  int64_t *cells = reinterpret_cast<int64_t *>(b);
+  b += cov_align(static_cast<size_t>(H) * 8);
+  const size_t w1 = cov_align(score_lines_tc_workspace(L, n));
+  void *ws1 = b;
+  b += w1;
+  const size_t w2 = ls_vs_attention_workspace(L);
+  cov::iota_rows_kernel<<<dim3(8, H), 256, 0, st>>>(rows, n);
+  LS_LAUNCH_CHECK("iota_rows_kernel");
+  int r = score_row_lse(L, n, q, k, rows, lse_full, ws1, w1, st);
+  if (r) return r;
+  r = vs_attention_ws(L, q, k, v, slash_ids, vert_ids, counts, out, 1, cells, nullptr, 0, b, w2, st, lse_plan);
+  if (r) return r;
+  cov::coverage_kernel<<<H, 256, 0, st>>>(lse_plan, lse_full, n, coverage);
+  LS_LAUNCH_CHECK("coverage_kernel");
+  return LS_OK;
 }

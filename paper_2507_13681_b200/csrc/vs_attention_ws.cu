@@ -59,6 +59,7 @@ struct Params {
   int out_bf16;
   long long *cells;
   long long *tiles;  // optional: tensor-core tiles executed per head (NULL: not counted)
+  float *row_lse;    // optional [H][n_new]: log2-sum-exp2 of each row's plan cells (-inf: diagonal fallback)
   int *dbg;  // optional host-mapped progress record [CTA][16] (ls_debug_set_buffer)
 };
 
@@ -516,6 +517,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (wg == 0) lx[row] = l + lx[row];
     tc::named_sync(1, N_SOFT);
     const float l_all = lx[row];
+    if (row_ok && wg == 0 && p.row_lse)  // plan-cell mass of the row on the log2 scale (ls_plan_coverage)
+      p.row_lse[static_cast<int64_t>(h) * p.n_new + r0 + row] = l_all > 0.f ? m_ref + __log2f(l_all) : -INFINITY;
     if (row_ok) {
       const int64_t orow = static_cast<int64_t>(r0 + row) * p.out_row_stride + static_cast<int64_t>(h) * D + wg * DH;
       if (l_all > 0.f) {
@@ -1144,7 +1147,7 @@ size_t vs_attention_ws_workspace(const ls_layer_desc *L) {
 int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k, const uint16_t *v,
                     const int32_t *slash_ids, const int32_t *vert_ids, const int32_t *counts, void *out,
                     int32_t out_bf16, int64_t *cells, int64_t *tiles, int dense, void *ws, size_t ws_bytes,
-                    cudaStream_t st) {
+                    cudaStream_t st, float *row_lse) {
   LS_REQUIRE(L->head_dim == 64 || L->head_dim == 128, LS_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   LS_REQUIRE((L->n_total + k5ws::BN - 1) / k5ws::BN <= k5ws::MAX_KB, LS_ERR_UNSUPPORTED, "n_total too large");
   LS_REQUIRE(dense || ws_bytes >= vs_attention_ws_workspace(L), LS_ERR_WORKSPACE, "vs_attention workspace too small");
@@ -1206,12 +1209,13 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   p.out_bf16 = out_bf16;
   p.cells = reinterpret_cast<long long *>(cells);
   p.tiles = reinterpret_cast<long long *>(tiles);
+  p.row_lse = row_lse;
   p.dbg = g_debug_buffer;
   LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * H, st));
   if (tiles) LS_CUDA(cudaMemsetAsync(tiles, 0, sizeof(int64_t) * H, st));
   // the q-tile-pair ping-pong variant is opt-in (LS_K5_PP=1): measured slower
   // than the single-tile kernel on C2 (one softmax warp per scheduler per tile)
-  const bool pp = !dense && (L->n_total + k5ws::BN - 1) / k5ws::BN <= k5ws::PP_MAX_KB && getenv("LS_K5_PP");
+  const bool pp = !dense && !row_lse && (L->n_total + k5ws::BN - 1) / k5ws::BN <= k5ws::PP_MAX_KB && getenv("LS_K5_PP");
   if (pp) {  // q-tile pairs sharing K/V tiles, ping-pong on the tensor pipe
     dim3 grid((nqt + 1) / 2, H);
     if (d == 128) {

@@ -144,6 +144,37 @@ def plan_rows(q_block, k, slash_ids, vert_ids, counts, n_new, n_total, n_kv_head
     return out
 
 
+def plan_coverage_layer(q_block, k, v, slash_ids, vert_ids, counts, n_new, n_total, n_kv_heads,
+                        q_head_stride=None, kv_head_stride=None, ws: Workspace | None = None,
+                        stream=None) -> torch.Tensor:
+    """coverage_ratio (prefill.py:254-281) of every head's plan over the block's
+    full causal attention: fp64 [H] on the device."""
+    H = counts.shape[0]
+    d = q_block.shape[-1]
+    L = layer_desc(H, n_kv_heads, d, n_new, n_total,
+                   q_block.stride(0) if q_head_stride is None else q_head_stride,
+                   k.stride(0) if kv_head_stride is None else kv_head_stride)
+    cov = torch.empty(H, dtype=torch.float64, device=q_block.device)
+    ws = ws or Workspace()
+    w = ws.get(_lib.lib().ls_plan_coverage_workspace(C_ref(L)))
+    _lib.call("ls_plan_coverage", C_ref(L), q_block.data_ptr(), k.data_ptr(), v.data_ptr(), slash_ids.data_ptr(),
+              vert_ids.data_ptr(), counts.data_ptr(), cov.data_ptr(), w.data_ptr(), w.numel(),
+              _lib.stream_ptr(stream))
+    return cov
+
+
+def coverage_ratio(Q, K, V, plan, row_offset: int) -> float:
+    """prefill.coverage_ratio(block, plan) (prefill.py:254-257) for one head,
+    with the block given as its Q/K/V instead of a dense AttentionBlock: the
+    dense weights are never materialised."""
+    Qt, Kt, Vt = to_bf16(Q), to_bf16(K), to_bf16(V)
+    _check_qkv(Qt, Kt, Vt, row_offset)
+    n_new, n_total = Qt.shape[0], Kt.shape[0]
+    sl, vt, cn = plan_tensors(plan, n_total, Qt.device)
+    cov = plan_coverage_layer(Qt.unsqueeze(0), Kt.unsqueeze(0), Vt.unsqueeze(0), sl, vt, cn, n_new, n_total, 1)
+    return float(cov[0].item())
+
+
 def masked_sparse_attention(Q, K, V, plan, row_offset: int, counter: OpCounter | None = None,
                             return_weights: bool = False):
     """tensor_ops.py:141-183 on the device (one head). Returns numpy fp64 Z
@@ -201,4 +232,4 @@ def dense_attention_layer(q_block, k, v, n_new, n_total, n_kv_heads, out=None, o
 
 
 __all__ = ["AttentionBlock", "masked_sparse_attention", "scaled_dot_attention", "attention_layer",
-           "dense_attention_layer", "plan_rows", "plan_tensors", "math"]
+           "dense_attention_layer", "plan_rows", "plan_tensors", "plan_coverage_layer", "coverage_ratio", "math"]

@@ -368,3 +368,34 @@ def test_dense_attention_tc_layer(cuda_lib):
         Zo, _ = oatt.scaled_dot_attention(qb[h].double().cpu().numpy(), K[h // 2].double().cpu().numpy(),
                                           V[h // 2].double().cpu().numpy(), ro)
         assert np.abs(out[:, h].double().cpu().numpy() - Zo).max() <= ATOL
+
+
+# ------------------------------------------- plan coverage
+@pytest.mark.parametrize("d,n_q,n_kv,ro,n_new", [(128, 4, 1, 600, 500), (64, 4, 2, 0, 700)])
+def test_plan_coverage_matches_oracle(cuda_lib, d, n_q, n_kv, ro, n_new):
+    """ls_plan_coverage == coverage_ratio (prefill.py:254-281) of each head's
+    plan over the block's dense causal weights (inclusion-exclusion over the
+    crossing cells, fp64 oracle)."""
+    from oracle import prefill as opf
+    from paper_2507_13681_b200.synth import layer_qkv_torch
+
+    n_total = ro + n_new
+    spec = SynthSpec(n_q, n_kv, d, n_total, seed=9)
+    Q, K, V = layer_qkv_torch(spec, 0)
+    qb = Q[:, ro:n_total].contiguous()
+    rows = pf.sample_rows_device(n_new, 0.1, 32, 5, 1, 0, 0, n_q)
+    plans = pf.sparsify_layer(qb, K, rows, 0.9, n_new, n_total, n_kv)
+    cov = tops.plan_coverage_layer(qb, K, V, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total, n_kv)
+    torch.cuda.synchronize()
+    hp = plans.to_host()
+    group = n_q // n_kv
+    positions = ro + np.arange(n_new)
+    for h in range(n_q):
+        _, w = oatt.scaled_dot_attention(qb[h].double().cpu().numpy(), K[h // group].double().cpu().numpy(),
+                                         V[h // group].double().cpu().numpy(), ro)
+        ref = opf.coverage(w, positions, hp[h])
+        assert abs(float(cov[h]) - ref) <= 1e-4, (h, float(cov[h]), ref)
+    # one-head reference-shaped entry (block given as Q/K/V)
+    one = tops.coverage_ratio(qb[0].float().cpu().numpy(), K[0].float().cpu().numpy(), V[0].float().cpu().numpy(),
+                              hp[0], ro)
+    assert abs(one - float(cov[0])) <= 1e-6
