@@ -51,6 +51,7 @@ constexpr int K7_SMEM_CAP = 24 * 1024;  // ids accumulated in shared memory (fp6
 constexpr int K7_CAND_CAP = 4096;       // touched ids listed in shared memory (radix + ranking over the list)
 constexpr int K7_BITONIC = 2048;        // candidate lists up to this size are ranked by one bitonic sort
 constexpr int K7_RB = 8, K7_PF = 2;     // rows fetched per round, columns per thread per row
+constexpr int K7_DMAX = 64, K7_DCH = 8;   // dense-window fast path: rows, rows loaded per batch
 
 __device__ __forceinline__ int64_t head_row(const ls_decode_stack &S, int layer, int h) {
   return static_cast<int64_t>(layer) * S.n_heads + h;
@@ -979,13 +980,16 @@ __device__ int block_rank(int flag, int *sh, int *tot) {
   __syncthreads();
   if (lane == 0) sh[wid] = __popc(b);
   __syncthreads();
-  int before = 0, all = 0;
-  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
-    if (i < wid) before += sh[i];
-    all += sh[i];
+  // every warp scans the (<= 32) warp counts with shuffles: one shared load per lane
+  const int c = lane < static_cast<int>(blockDim.x >> 5) ? sh[lane] : 0;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  *tot = all;
-  return before + __popc(b & ((1u << lane) - 1u));
+  *tot = __shfl_sync(0xffffffffu, incl, 31);
+  return __shfl_sync(0xffffffffu, incl - c, wid) + __popc(b & ((1u << lane) - 1u));
 }
 
 __device__ __forceinline__ int gtime32() {
@@ -1012,7 +1016,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   uint32_t *touched =
       use_smem ? reinterpret_cast<uint32_t *>(smem7 + static_cast<size_t>(K7_SMEM_CAP) * 8)
                : touched_ws + hr * ((S.row_cap + 31) / 32);
-  int *rec = (dbg && threadIdx.x == 0) ? dbg + (static_cast<int64_t>(layer) * gridDim.x + h) * 8 : nullptr;
+  int *rec = (dbg && threadIdx.x == 0) ? dbg + (static_cast<int64_t>(layer) * gridDim.x + h) * 16 : nullptr;
   if (rec) rec[0] = gtime32();
   for (int i = threadIdx.x; i < length; i += blockDim.x) acc[i] = 0.0;
   for (int i = threadIdx.x; i < words; i += blockDim.x) touched[i] = 0u;
@@ -1025,7 +1029,55 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   auto row_weight = [](float sv, float M, float Lr, float inv) {
     return (Lr == 0.f) ? sv : fast_exp2(sv - M) * inv;  // Lr == 0: stored probabilities (seeds)
   };
-  for (int r0 = 0; r0 < n_rows; r0 += K7_RB) {
+  // every buffered row dense (the first event: seed rows + dense steps): id j is
+  // owned by one thread, which adds the rows in order from registers -- all of
+  // a chunk's row values are loaded at once and no block barrier runs per row
+  __shared__ int64_t d_so[K7_DMAX];
+  __shared__ int d_n[K7_DMAX], d_dense[K7_DMAX];
+  __shared__ float d_m[K7_DMAX], d_l[K7_DMAX], d_inv[K7_DMAX];
+  __shared__ int d_all;
+  if (threadIdx.x == 0) d_all = n_rows <= K7_DMAX;
+  __syncthreads();
+  if (threadIdx.x < n_rows && threadIdx.x < K7_DMAX) {
+    const int64_t so = hr * S.window + (appended - n_rows + static_cast<int>(threadIdx.x)) % S.window;
+    d_so[threadIdx.x] = so;
+    d_n[threadIdx.x] = S.ring_n[so];
+    d_m[threadIdx.x] = S.ring_ml[so * 2];
+    d_l[threadIdx.x] = S.ring_ml[so * 2 + 1];
+    d_inv[threadIdx.x] = d_l[threadIdx.x] > 0.f ? 1.f / d_l[threadIdx.x] : 0.f;
+    d_dense[threadIdx.x] = S.ring_dense[so];
+    if (!d_dense[threadIdx.x]) d_all = 0;
+  }
+  __syncthreads();
+  const bool all_dense = d_all != 0;
+  if (all_dense) {
+    int max_n = 0;
+    for (int rr = 0; rr < n_rows; ++rr) max_n = max(max_n, d_n[rr]);
+    for (int j = threadIdx.x; j < max_n; j += blockDim.x) {
+      double a = 0.0;
+      bool t = false;
+      for (int c0 = 0; c0 < n_rows; c0 += K7_DCH) {
+        float sv[K7_DCH];
+#pragma unroll
+        for (int u = 0; u < K7_DCH; ++u) {
+          const int rr = c0 + u;
+          sv[u] = (rr < n_rows && j < d_n[rr]) ? __ldg(S.ring_s + d_so[rr] * S.row_cap + j) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < K7_DCH; ++u) {
+          const int rr = c0 + u;
+          if (rr < n_rows && j < d_n[rr]) {
+            a += static_cast<double>(row_weight(sv[u], d_m[rr], d_l[rr], d_inv[rr]));
+            t = true;
+          }
+        }
+      }
+      acc[j] = a;  // == 0.0 + w_0 + w_1 + ... in row order, as the row-by-row adds
+      if (t) atomicOr(touched + (j >> 5), 1u << (j & 31));
+    }
+    __syncthreads();
+  }
+  for (int r0 = 0; r0 < (all_dense ? 0 : n_rows); r0 += K7_RB) {
     const int nr = min(K7_RB, n_rows - r0);
     // row metadata of the round (one round trip: slots are always valid indices)
     int64_t so_r[K7_RB];
@@ -1034,17 +1086,27 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     int nmax = 0;
 #pragma unroll
     for (int rr = 0; rr < K7_RB; ++rr) {
-      so_r[rr] = hr * S.window + (appended - n_rows + r0 + rr) % S.window;
-      n_r[rr] = __ldg(S.ring_n + so_r[rr]);
-      dense_r[rr] = __ldg(S.ring_dense + so_r[rr]);
-      m_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2);
-      l_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2 + 1);
+      const int R = r0 + rr;
+      if (R < K7_DMAX) {  // staged in shared memory above
+        so_r[rr] = d_so[R];
+        n_r[rr] = d_n[R];
+        dense_r[rr] = d_dense[R];
+        m_r[rr] = d_m[R];
+        l_r[rr] = d_l[R];
+      } else {
+        so_r[rr] = hr * S.window + (appended - n_rows + R) % S.window;
+        n_r[rr] = __ldg(S.ring_n + so_r[rr]);
+        dense_r[rr] = __ldg(S.ring_dense + so_r[rr]);
+        m_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2);
+        l_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2 + 1);
+      }
     }
 #pragma unroll
     for (int rr = 0; rr < K7_RB; ++rr) {
       if (rr >= nr) n_r[rr] = 0;
       nmax = max(nmax, n_r[rr]);
     }
+    if (rec && r0 == 0) rec[8] = gtime32();
     if (nmax <= K7_PF * static_cast<int>(blockDim.x)) {
       // the round's columns (second round trip), then the adds in row order
       float sv_r[K7_RB][K7_PF];
@@ -1058,6 +1120,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
           iv[rr][e] = !ok ? -1 : dense_r[rr] ? j : __ldg(S.ring_ids + so_r[rr] * S.sparse_cap + j);
           sv_r[rr][e] = ok ? __ldg(S.ring_s + so_r[rr] * S.row_cap + j) : 0.f;
         }
+      if (rec && r0 == 0) rec[9] = gtime32() + 0 * __float_as_int(sv_r[0][0]) + 0 * iv[0][0];
 #pragma unroll
       for (int rr = 0; rr < K7_RB; ++rr) {
         if (rr < nr) {
@@ -1371,10 +1434,16 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
 #ifndef LS_K6_NST_C
 #define LS_K6_NST_C 3
 #endif
+#ifndef LS_K6_NST_D
+#define LS_K6_NST_D 4
+#endif
+#ifndef LS_K6_NG_D
+#define LS_K6_NG_D 2
+#endif
 #ifndef LS_K6_NG_C
 #define LS_K6_NG_C 1
 #endif
-  constexpr int NST_D = 4, NW_D = 4, NG_D = 2, NST_C = LS_K6_NST_C, NW_C = 4, NG_C = LS_K6_NG_C;
+  constexpr int NST_D = LS_K6_NST_D, NW_D = 4, NG_D = LS_K6_NG_D, NST_C = LS_K6_NST_C, NW_C = 4, NG_C = LS_K6_NG_C;
   const int tile = compressed ? 16 * NW_C : 16 * NW_D;
   dec::KmMaps maps;
   const int HR = S->n_layers * S->n_heads;
