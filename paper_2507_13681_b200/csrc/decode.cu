@@ -684,6 +684,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&empty[st]);
+      if (rec && tid == 0 && i < 4) rec[11 + i] = gtime();
     }
     if (rec && tid == 0) {
       rec[3] = gtime();
