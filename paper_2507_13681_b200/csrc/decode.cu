@@ -405,9 +405,9 @@ __host__ __device__ constexpr int km_gather_b(int NG) { return NG == 2 ? 16 * 8 
 
 // NW consumer warps x 16 rows = one tile of TILE K/V rows; NG such warp
 // groups take alternate tiles (ping-pong); + one producer warp
-template <int D, int NST, int NW, int NG>
+template <int D, int NST, int NW, int NG, int RPW = 16>
 struct KmSmem {
-  static constexpr int TILE = 16 * NW;
+  static constexpr int TILE = RPW * NW;
   static constexpr int TILE_B = TILE * D * 2;  // one K or V tile, [D / 64][TILE rows][128 B] swizzled
   static constexpr int OFF_V = NST * TILE_B;
   static constexpr int OFF_BAR = 2 * NST * TILE_B;   // full[S], empty[S]
@@ -473,7 +473,7 @@ __device__ __forceinline__ KmTile km_tile(int t, int t_a, const Geo &geo) {
   return x;
 }
 
-template <int D, int G, int NST, int NW, int NG>
+template <int D, int G, int NST, int NW, int NG, int RPW>
 __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __grid_constant__ KmMaps maps, ls_decode_stack S,
                                                                 int layer, const uint16_t *q, int64_t q_head_stride,
                                                                 int q_from_archive, int compressed, float scale_log2,
@@ -499,7 +499,9 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
   // phases of its stages in order (a group running two phases ahead on a
   // shared barrier would see the older phase's parity as complete)
   static_assert(NST % NG == 0, "stages per warp group");
-  using L = KmSmem<D, NST, NW, NG>;
+  static_assert(RPW == 16 || RPW == 8, "rows per consumer warp");
+  constexpr int NTS = RPW / 8;  // n-tiles of 8 key rows per warp in S
+  using L = KmSmem<D, NST, NW, NG, RPW>;
   constexpr int KM_TILE = L::TILE, KM_WARPS = NW * NG, KM_THREADS = (NW * NG + 1) * 32;
   constexpr int NT = D / 8;  // n-tiles of 8 dims in O
   extern __shared__ unsigned char km_dyn[];
@@ -579,7 +581,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
 #pragma unroll
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_run = -INFINITY, l_part = 0.f;
-    const int wr0 = (warp % NW) * 16, grp = warp / NW;
+    const int wr0 = (warp % NW) * RPW, grp = warp / NW;
     const int64_t hr_g = head_row(S, layer, h0 + (hv ? g : 0));
     float *ring_row = S.ring_s + (hr_g * S.window + slot) * S.row_cap;
     const int m8 = lane >> 3, r8 = lane & 7;
@@ -588,48 +590,65 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       const KmTile x = km_tile<KM_TILE>(t_begin + i, t_a, geo);
       // this tile's working-set ids (ring_ids of compressed rows), fetched before the data wait
       int id = 0;
-      if (compressed && lane < 16 && wr0 + lane < x.valid)
+      if (compressed && lane < RPW && wr0 + lane < x.valid)
         id = x.seg_a ? __ldg(S.sel_ids + hr0 * S.budget_cap + x.row0 + wr0 + lane) : x.row0 + wr0 + lane;
       tc::mbar_wait(&full[st], (i / NST) & 1);
       if (rec && tid == 0 && i == 0) rec[2] = gtime();
       const uint32_t ks = tc::smem_u32(sm + st * L::TILE_B), vs = tc::smem_u32(sm + L::OFF_V + st * L::TILE_B);
-      if (x.valid < wr0 + 16) {
+      if (x.valid < wr0 + RPW) {
         // rows past the working set hold other (finite or not) data: zero this warp's V rows (P = 0 there)
         unsigned char *vt = sm + L::OFF_V + st * L::TILE_B;
-        for (int e = lane; e < 16 * (D / 8); e += 32) {
+        for (int e = lane; e < RPW * (D / 8); e += 32) {
           const int r = wr0 + e / (D / 8), c = e % (D / 8);
           if (r >= x.valid) *reinterpret_cast<uint4 *>(vt + km_off<KM_TILE>(r, c)) = make_uint4(0, 0, 0, 0);
         }
         tc::fence_proxy_async();  // the stage is refilled by TMA (async proxy) later
         __syncwarp();
       }
-      // S = Q K^T over this warp's 16 rows: n-tile 0 = rows wr0..+7, 1 = wr0+8..+15
+      // S = Q K^T over this warp's rows (n-tile n = rows wr0 + 8n .. +7)
       // (all fragment loads first, then the MMAs in two independent chains per n-tile)
       uint32_t fb[D / 16][4];
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) ldsm_x4(fb[kk], ks + km_off<KM_TILE>(wr0 + (m8 >> 1) * 8 + r8, 2 * kk + (m8 & 1)));
       float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       float sd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      if constexpr (RPW == 16) {
 #pragma unroll
-      for (int kk = 0; kk < D / 16; kk += 2) {
-        mma_16816(sc[0], qa[kk][0], qa[kk][1], fb[kk][0], fb[kk][1]);
-        mma_16816(sc[1], qa[kk][0], qa[kk][1], fb[kk][2], fb[kk][3]);
-        mma_16816(sd[0], qa[kk + 1][0], qa[kk + 1][1], fb[kk + 1][0], fb[kk + 1][1]);
-        mma_16816(sd[1], qa[kk + 1][0], qa[kk + 1][1], fb[kk + 1][2], fb[kk + 1][3]);
+        for (int kk = 0; kk < D / 16; ++kk) ldsm_x4(fb[kk], ks + km_off<KM_TILE>(wr0 + (m8 >> 1) * 8 + r8, 2 * kk + (m8 & 1)));
+#pragma unroll
+        for (int kk = 0; kk < D / 16; kk += 2) {
+          mma_16816(sc[0], qa[kk][0], qa[kk][1], fb[kk][0], fb[kk][1]);
+          mma_16816(sc[1], qa[kk][0], qa[kk][1], fb[kk][2], fb[kk][3]);
+          mma_16816(sd[0], qa[kk + 1][0], qa[kk + 1][1], fb[kk + 1][0], fb[kk + 1][1]);
+          mma_16816(sd[1], qa[kk + 1][0], qa[kk + 1][1], fb[kk + 1][2], fb[kk + 1][3]);
+        }
+      } else {
+        // 8 rows: one x4 load = the rows' chunks 4kp..4kp+3 = two k-steps of the one n-tile
+#pragma unroll
+        for (int kp = 0; kp < D / 32; ++kp) ldsm_x4(fb[kp], ks + km_off<KM_TILE>(wr0 + r8, 4 * kp + m8));
+#pragma unroll
+        for (int kp = 0; kp < D / 32; ++kp) {
+          mma_16816(sc[0], qa[2 * kp][0], qa[2 * kp][1], fb[kp][0], fb[kp][1]);
+          mma_16816(sd[0], qa[2 * kp + 1][0], qa[2 * kp + 1][1], fb[kp][2], fb[kp][3]);
+        }
       }
 #pragma unroll
-      for (int n = 0; n < 2; ++n)
+      for (int n = 0; n < NTS; ++n)
 #pragma unroll
         for (int e = 0; e < 4; ++e) sc[n][e] += sd[n][e];
       // V fragments in flight while the softmax runs
+      if constexpr (RPW == 16) {
 #pragma unroll
-      for (int np = 0; np < D / 16; ++np)
-        ldsm_x4_t(fb[np], vs + km_off<KM_TILE>(wr0 + (m8 & 1) * 8 + r8, 2 * np + (m8 >> 1)));
+        for (int np = 0; np < D / 16; ++np)
+          ldsm_x4_t(fb[np], vs + km_off<KM_TILE>(wr0 + (m8 & 1) * 8 + r8, 2 * np + (m8 >> 1)));
+      } else {
+        // 8 rows (k 0-7; k 8-15 of the m16n8k16 step are zero): x4.trans = 4 dim n-tiles
+#pragma unroll
+        for (int nq = 0; nq < D / 32; ++nq) ldsm_x4_t(fb[nq], vs + km_off<KM_TILE>(wr0 + r8, 4 * nq + m8));
+      }
       // logits (log2 units); rows past the working set -> -inf
-      float xs[2][2];
+      float xs[2][2] = {{-INFINITY, -INFINITY}, {-INFINITY, -INFINITY}};
       float tmax = -INFINITY;
 #pragma unroll
-      for (int n = 0; n < 2; ++n)
+      for (int n = 0; n < NTS; ++n)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = wr0 + n * 8 + 2 * t4 + e;
@@ -639,13 +658,13 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       // raw logits to the ring (head g, columns j0 + r)
       if (hv) {
 #pragma unroll
-        for (int n = 0; n < 2; ++n) {
+        for (int n = 0; n < NTS; ++n) {
           const int r = wr0 + n * 8 + 2 * t4;
           if (r < x.valid) ring_row[x.j0 + r] = xs[n][0];
           if (r + 1 < x.valid) ring_row[x.j0 + r + 1] = xs[n][1];
         }
       }
-      if (compressed && lane < 16 && wr0 + lane < x.valid) {
+      if (compressed && lane < RPW && wr0 + lane < x.valid) {
         const int r = wr0 + lane;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg)
@@ -664,7 +683,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
 #pragma unroll
         for (int n = 0; n < 2; ++n)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) p[n][e] = xs[n][e] == -INFINITY ? 0.f : fast_exp2(xs[n][e] - m_new);
+          for (int e = 0; e < 2; ++e) p[n][e] = (n >= NTS || xs[n][e] == -INFINITY) ? 0.f : fast_exp2(xs[n][e] - m_new);
         m_run = m_new;
       }
       l_part = l_part * corr + ((p[0][0] + p[0][1]) + (p[1][0] + p[1][1]));
@@ -676,11 +695,18 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
         }
       }
       const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]), pa2 = pack_bf16(p[1][0], p[1][1]);
-      // O += P V: B = V rows wr0..+15 (k) x 16 dims per ldmatrix.x4.trans
+      // O += P V (B = this warp's V rows)
+      if constexpr (RPW == 16) {
 #pragma unroll
-      for (int np = 0; np < D / 16; ++np) {
-        mma_16816(o[2 * np], pa0, pa2, fb[np][0], fb[np][1]);
-        mma_16816(o[2 * np + 1], pa0, pa2, fb[np][2], fb[np][3]);
+        for (int np = 0; np < D / 16; ++np) {
+          mma_16816(o[2 * np], pa0, pa2, fb[np][0], fb[np][1]);
+          mma_16816(o[2 * np + 1], pa0, pa2, fb[np][2], fb[np][3]);
+        }
+      } else {
+#pragma unroll
+        for (int nq = 0; nq < D / 32; ++nq)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) mma_16816(o[4 * nq + m], pa0, 0u, fb[nq][m], 0u);
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&empty[st]);
@@ -1444,8 +1470,13 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
 #ifndef LS_K6_NG_C
 #define LS_K6_NG_C 1
 #endif
-  constexpr int NST_D = LS_K6_NST_D, NW_D = 4, NG_D = LS_K6_NG_D, NST_C = LS_K6_NST_C, NW_C = 4, NG_C = LS_K6_NG_C;
-  const int tile = compressed ? 16 * NW_C : 16 * NW_D;
+#ifndef LS_K6_RPW_C
+#define LS_K6_RPW_C 16
+#endif
+  constexpr int RPW_C = LS_K6_RPW_C, RPW_D = 16;
+  constexpr int NST_D = LS_K6_NST_D, NW_D = 4, NG_D = LS_K6_NG_D, NST_C = LS_K6_NST_C, NW_C = 64 / RPW_C,
+                NG_C = LS_K6_NG_C;
+  const int tile = compressed ? RPW_C * NW_C : RPW_D * NW_D;
   dec::KmMaps maps;
   const int HR = S->n_layers * S->n_heads;
   const int64_t rows = S->kv_head_stride / D;
@@ -1456,12 +1487,12 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
   if (!r) r = make_tmap_bf16_3d_box(&maps.k, k, D, rows, S->n_kv_heads, D, S->kv_head_stride, tile);
   if (!r) r = make_tmap_bf16_3d_box(&maps.v, v, D, rows, S->n_kv_heads, D, S->kv_head_stride, tile);
   if (r) return r;
-  constexpr int smem_d = dec::KmSmem<D, NST_D, NW_D, NG_D>::TOTAL, smem_c = dec::KmSmem<D, NST_C, NW_C, NG_C>::TOTAL;
+  constexpr int smem_d = dec::KmSmem<D, NST_D, NW_D, NG_D, RPW_D>::TOTAL, smem_c = dec::KmSmem<D, NST_C, NW_C, NG_C, RPW_C>::TOTAL;
   static bool attr_set = false;
   if (!attr_set) {
-    LS_CUDA(cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LS_CUDA(cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D, RPW_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_d));
-    LS_CUDA(cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LS_CUDA(cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C, RPW_C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_c));
     attr_set = true;
   }
@@ -1489,7 +1520,7 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
   static int max_cl = 0;
   if (!max_cl) {  // 16-CTA clusters need the non-portable opt-in
     max_cl = 8;
-    if (cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>,
+    if (cudaFuncSetAttribute(dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D, RPW_D>,
                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
       max_cl = 16;
     cudaGetLastError();
@@ -1505,10 +1536,10 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
     if (res < 0) {
       int per_sm = 0;
       if (compressed)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C, RPW_C>,
                                                       32 * (NW_C * NG_C + 1), smem_c);
       else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D, RPW_D>,
                                                       32 * (NW_D * NG_D + 1), smem_d);
       cudaGetLastError();
       res = per_sm * n_sm;
@@ -1539,10 +1570,10 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
   cfg.attrs = attr;
   cfg.numAttrs = na;
   if (compressed)
-    LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C>, maps, *S, layer, q, q_head_stride,
+    LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_mma_kernel<D, G, NST_C, NW_C, NG_C, RPW_C>, maps, *S, layer, q, q_head_stride,
                                q_from_archive, compressed, sl, out, out_bf16, pdl, ccombine, g_debug_buffer));
   else
-    LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D>, maps, *S, layer, q, q_head_stride,
+    LS_CUDA(cudaLaunchKernelEx(&cfg, dec::decode_mma_kernel<D, G, NST_D, NW_D, NG_D, RPW_D>, maps, *S, layer, q, q_head_stride,
                                q_from_archive, compressed, sl, out, out_bf16, pdl, ccombine, g_debug_buffer));
   return LS_OK;
 }
