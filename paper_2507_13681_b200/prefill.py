@@ -280,6 +280,27 @@ def sparsify_layer(q_block: torch.Tensor, k: torch.Tensor, rows: torch.Tensor, a
     return plans
 
 
+def line_arrays_device(Qt: torch.Tensor, Kt: torch.Tensor, row_offset: int):
+    """Line weights of a block over ALL its rows (every row "sampled"), one
+    head: (v_w, s_w) fp64 numpy arrays of length n_total (K1 through the C ABI;
+    diagnostics such as metrics.recovery_curve)."""
+    n_new, n_total = Qt.shape[0], Kt.shape[0]
+    dev = Qt.device
+    rows = torch.arange(n_new, dtype=torch.int32, device=dev).unsqueeze(0)
+    L = layer_desc(1, 1, Qt.shape[-1], n_new, n_total, 0, 0)
+    f64, f32 = torch.float64, torch.float32
+    v_w, s_w = torch.empty(n_total, dtype=f64, device=dev), torch.empty(n_total, dtype=f64, device=dev)
+    v_max, s_max = torch.empty(n_total, dtype=f32, device=dev), torch.empty(n_total, dtype=f32, device=dev)
+    row_stats = torch.empty((n_new, 2), dtype=f32, device=dev)
+    total = torch.empty(1, dtype=f64, device=dev)
+    count = torch.empty(1, dtype=torch.int64, device=dev)
+    ws = Workspace().get(_lib.lib().ls_score_lines_workspace(C_ref(L), n_new))
+    _lib.call("ls_score_lines", C_ref(L), n_new, Qt.data_ptr(), Kt.data_ptr(), rows.data_ptr(), v_w.data_ptr(),
+              v_max.data_ptr(), s_w.data_ptr(), s_max.data_ptr(), row_stats.data_ptr(), total.data_ptr(),
+              count.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    return v_w.cpu().numpy(), s_w.cpu().numpy()
+
+
 def C_ref(x):
     import ctypes
 

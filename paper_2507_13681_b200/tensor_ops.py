@@ -18,6 +18,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+from types import SimpleNamespace
+
 import numpy as np
 import torch
 
@@ -175,6 +177,43 @@ def coverage_ratio(Q, K, V, plan, row_offset: int) -> float:
     return float(cov[0].item())
 
 
+def recovery_curve(qkv_per_head: dict, row_offset: int, etas) -> list[tuple[float, float]]:
+    """metrics.recovery_curve (metrics.py:71-96) with each head's block given
+    as its (Q, K, V) instead of a dense AttentionBlock: for each eta, the
+    head-averaged full-block coverage of the top floor(eta * 2 n_total) lines of
+    both kinds ranked together by (weight desc, kind, index). Line sums over ALL
+    block rows come from K1 (rows = every row), coverage from ls_plan_coverage;
+    only the ranking of the 2 n_total lines runs on the host (diagnostic path)."""
+    from .prefill import line_arrays_device  # noqa: PLC0415
+
+    curves = {float(e): [] for e in etas}
+    for Q, K, V in qkv_per_head.values():
+        Qt, Kt, Vt = to_bf16(Q), to_bf16(K), to_bf16(V)
+        _check_qkv(Qt, Kt, Vt, row_offset)
+        n_new, n_total = Qt.shape[0], Kt.shape[0]
+        v_w, s_w = line_arrays_device(Qt, Kt, row_offset)
+        # every row sampled: all n_total lines of each kind exist (prefill.py:159-167)
+        w = np.concatenate([s_w, v_w])
+        kind = np.concatenate([np.zeros(n_total, np.int8), np.ones(n_total, np.int8)])  # "slash" < "vertical"
+        idx = np.concatenate([np.arange(n_total), np.arange(n_total)])
+        order = np.lexsort((idx, kind, -w))
+        for eta in curves:
+            k = int(np.floor(eta * 2 * n_total + 1e-9))
+            chosen = order[:k]
+            sl = idx[chosen[kind[chosen] == 0]]
+            vt = idx[chosen[kind[chosen] == 1]]
+            plan = SimpleNamespace(selected_slashes=frozenset(int(x) for x in sl),
+                                   selected_verticals=frozenset(int(x) for x in vt))
+            if not plan.selected_slashes and not plan.selected_verticals:
+                curves[eta].append(0.0)
+                continue
+            sl_t, vt_t, cn = plan_tensors(plan, n_total, Qt.device)
+            cov = plan_coverage_layer(Qt.unsqueeze(0), Kt.unsqueeze(0), Vt.unsqueeze(0), sl_t, vt_t, cn, n_new,
+                                      n_total, 1)
+            curves[eta].append(float(cov[0].item()))
+    return [(eta, float(np.mean(r))) for eta, r in curves.items()]
+
+
 def masked_sparse_attention(Q, K, V, plan, row_offset: int, counter: OpCounter | None = None,
                             return_weights: bool = False):
     """tensor_ops.py:141-183 on the device (one head). Returns numpy fp64 Z
@@ -232,4 +271,4 @@ def dense_attention_layer(q_block, k, v, n_new, n_total, n_kv_heads, out=None, o
 
 
 __all__ = ["AttentionBlock", "masked_sparse_attention", "scaled_dot_attention", "attention_layer",
-           "dense_attention_layer", "plan_rows", "plan_tensors", "plan_coverage_layer", "coverage_ratio", "math"]
+           "dense_attention_layer", "plan_rows", "plan_tensors", "plan_coverage_layer", "coverage_ratio", "recovery_curve", "math"]

@@ -399,3 +399,35 @@ def test_plan_coverage_matches_oracle(cuda_lib, d, n_q, n_kv, ro, n_new):
     one = tops.coverage_ratio(qb[0].float().cpu().numpy(), K[0].float().cpu().numpy(), V[0].float().cpu().numpy(),
                               hp[0], ro)
     assert abs(one - float(cov[0])) <= 1e-6
+
+
+def test_recovery_curve_matches_oracle(cuda_lib):
+    """metrics.recovery_curve (metrics.py:71-96) on the device vs the oracle's
+    full-block line sums + ranking + inclusion-exclusion coverage."""
+    from paper_2507_13681_b200.synth import layer_qkv_torch
+
+    ro, n_new, d = 200, 300, 64
+    n_total = ro + n_new
+    spec = SynthSpec(2, 1, d, n_total, seed=13)
+    Q, K, V = layer_qkv_torch(spec, 0)
+    etas = [0.01, 0.05, 0.2]
+    heads = {h: (Q[h, ro:n_total].float().cpu().numpy(), K[0].float().cpu().numpy(), V[0].float().cpu().numpy())
+             for h in range(2)}
+    got = tops.recovery_curve(heads, ro, etas)
+    positions = ro + np.arange(n_new)
+    for (eta, val), eta_ref in zip(got, etas):
+        ratios = []
+        for qh, kh, vh in heads.values():
+            _, w = oatt.scaled_dot_attention(qh.astype(np.float64), kh.astype(np.float64), vh.astype(np.float64), ro)
+            a = opf.line_arrays(w, positions)
+            lines = [(-a["s_w"][i], 0, i) for i in range(len(a["s_w"])) if a["s_len"][i] > 0]
+            lines += [(-a["v_w"][i], 1, i) for i in range(len(a["v_w"])) if a["v_len"][i] > 0]
+            lines.sort()
+            k = int(np.floor(eta_ref * 2 * n_total + 1e-9))
+            chosen = lines[:k]
+            plan = type("P", (), {})()
+            plan.selected_slashes = frozenset(i for _, kd, i in chosen if kd == 0)
+            plan.selected_verticals = frozenset(i for _, kd, i in chosen if kd == 1)
+            ratios.append(opf.coverage(w, positions, plan))
+        assert eta == eta_ref
+        assert abs(val - float(np.mean(ratios))) <= 2e-3, (eta, val, float(np.mean(ratios)))
