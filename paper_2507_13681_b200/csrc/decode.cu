@@ -102,7 +102,6 @@ __device__ __forceinline__ Geo geometry(const ls_decode_stack &S, int layer, int
 // order (deterministic).
 constexpr int K6_TILE = 64;
 constexpr int K6_STAGES = 2;
-constexpr int K6_MAX_SPLIT = 256;
 constexpr int K6_MAX_CLUSTER = 16;  // splits of a unit = one thread-block cluster
 // G <= 4: 16-CTA clusters (non-portable); larger q-groups: 8 (the gather
 // area + cross-warp buffers must fit in the tile buffers)
