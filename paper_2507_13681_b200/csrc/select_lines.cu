@@ -192,6 +192,40 @@ struct RecomputeCells {
     const float *rs = row_stats + (static_cast<int64_t>(h) * n_s + r) * 2;
     return static_cast<double>(fast_exp2(acc * scale_log2 - rs[0]) * rs[1]);
   }
+  // 1/PARTS of the q . k dot product (dims [part * d/PARTS, +d/PARTS)), one batch of loads
+  template <int PARTS>
+  __device__ __forceinline__ float dot_part(int h, int g, int c, int part) const {
+    constexpr int MAXU = 16 / PARTS;  // 16-B chunks per lane at d = 128
+    const int nu = d / (8 * PARTS);
+    const uint4 *qr = reinterpret_cast<const uint4 *>(q + static_cast<int64_t>(h) * q_head_stride +
+                                                      static_cast<int64_t>(g - row_offset) * d) + part * nu;
+    const uint4 *kr = reinterpret_cast<const uint4 *>(k + static_cast<int64_t>(h / group) * kv_head_stride +
+                                                      static_cast<int64_t>(c) * d) + part * nu;
+    uint4 a[MAXU], b[MAXU];
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      if (u < nu) {
+        a[u] = __ldg(qr + u);
+        b[u] = __ldg(kr + u);
+      }
+    }
+    float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      if (u < nu) {
+        float fa[8], fb[8];
+        bf16x8_to_f32(a[u], fa);
+        bf16x8_to_f32(b[u], fb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc4[j & 3] = fmaf(fa[j], fb[j], acc4[j & 3]);
+      }
+    }
+    return (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+  }
+  __device__ __forceinline__ double finish(int h, int r, float dot, int, int) const {
+    const float *rs = row_stats + (static_cast<int64_t>(h) * n_s + r) * 2;
+    return static_cast<double>(fast_exp2(dot * scale_log2 - rs[0]) * rs[1]);
+  }
 };
 
 // Cell source 2: a dense fp64 weight matrix (greedy_select_lines parity path).
@@ -204,6 +238,9 @@ struct DenseCells {
   __device__ __forceinline__ double value(int /*h*/, int r, int /*g*/, int c) const {
     return weights[static_cast<int64_t>(r) * n_total + c];
   }
+  template <int PARTS>
+  __device__ __forceinline__ float dot_part(int, int, int, int) const { return 0.f; }
+  __device__ __forceinline__ double finish(int h, int r, float, int g, int c) const { return value(h, r, g, c); }
 };
 
 // ------------------------------------------------------------ K3 greedy
@@ -586,8 +623,21 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         int *q = S.hitq[warp];
         int qn = 0;
         const unsigned lt = (1u << lane) - 1u;
-        auto eval = [&](int n) {  // value of queue entries [0, n), lane i takes entry i
-          const bool act = lane < n;
+        auto eval = [&](int n) {  // value of queue entries [0, n)
+          if (n <= 8) {
+            // few cells (most vertical picks): four lanes per cell, a quarter of
+            // the dot product each -- one L2 round trip instead of two
+            const int e = lane >> 2, part = lane & 3;
+            const bool act = e < n;
+            const int r = act ? q[e] : 0;
+            const int g = act ? (gs_smem ? S.gs[r] : cells.pos(h, r)) : 0;
+            float dot = act ? cells.template dot_part<4>(h, g, is_vert ? idx : g - idx, part) : 0.f;
+            dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+            if (act && part == 0) sum += cells.finish(h, r, dot, g, is_vert ? idx : g - idx);
+            return;
+          }
+          const bool act = lane < n;  // lane i takes entry i
           const int r = act ? q[lane] : 0;
           const int g = act ? (gs_smem ? S.gs[r] : cells.pos(h, r)) : 0;
           if (act) sum += cells.value(h, r, g, is_vert ? idx : g - idx);
