@@ -264,7 +264,7 @@ struct DenseCells {
 //                   stops the producer as soon as the plan is complete.
 constexpr int WIN = 1024;            // staged lines per list
 constexpr int TAB_CAP = 16384;       // n_total up to which position tables live in shared memory
-constexpr int G_THREADS = 512;       // 16 warps
+constexpr int G_THREADS = 640;       // 20 warps
 constexpr int RING = 1024;           // pick slots between producer and finalizer
 constexpr int AHEAD = 256;           // the producer runs at most this far ahead of the finalizer: picks
                                      // past the plan's end cost crossing sums for nothing
