@@ -610,11 +610,23 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       const int32_t *inv_o = is_vert ? inv_s : inv_v;  // other kind's sorted positions
       double sum = 0.0;
       if (n_other > 0 && !(dbg && dbg[69999] == 1)) {
-        // sampled rows at or after position idx: g = idx + (other line index)
-        int lo = 0, hi = n_rows;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if ((gs_smem ? S.gs[mid] : cells.pos(h, mid)) < idx) lo = mid + 1; else hi = mid;
+        // sampled rows at or after position idx: g = idx + (other line index).
+        // Warp-wide 32-ary search: two probe rounds for n_rows <= 1024
+        int lo = 0;
+        {
+          int hi = n_rows;  // first row with g >= idx lies in [lo, hi]
+          while (hi - lo > 32) {
+            const int stp = (hi - lo + 31) / 32;
+            const int p = lo + lane * stp;
+            const bool lt = p < hi && (gs_smem ? S.gs[p] : cells.pos(h, p)) < idx;
+            const int c = __popc(__ballot_sync(0xffffffffu, lt));
+            const int nlo = c == 0 ? lo : lo + (c - 1) * stp + 1;
+            hi = min(hi, lo + c * stp);
+            lo = nlo;
+          }
+          const int p = lo + lane;
+          const bool lt = p < hi && (gs_smem ? S.gs[p] : cells.pos(h, p)) < idx;
+          lo += __popc(__ballot_sync(0xffffffffu, lt));
         }
         const int okind = is_vert ? 0 : 1;
         // crossing cells are sparse among the walked candidates: queue their
