@@ -310,6 +310,11 @@ struct SpinGuard {
   }
 };
 
+#ifndef LS_GREEDY_IDLE_SMSP
+#define LS_GREEDY_IDLE_SMSP 0  // measured: idling warps 4, 8, 12, 16 starves the crossing sums
+#endif
+constexpr bool g_idle_producer_smsp = LS_GREEDY_IDLE_SMSP != 0;
+
 template <typename Cells>
 __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
                                                                Picks P, int cap, Cells cells, int32_t *n_final,
@@ -575,6 +580,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       coverage[h] = cov < 1.0 ? cov : 1.0;
       approx_out[h] = j > 0 ? approx : 0.0;
     }
+  } else if ((warp & 3) == 0 && g_idle_producer_smsp) {
+    // the producer's scheduler (SM sub-partition) is left to the decision chain
   } else {
     // ================================================= crossing sums
     // (warps 4, 8, 12 share the producer's scheduler: they are consumers too;
