@@ -266,7 +266,7 @@ constexpr int WIN = 1024;            // staged lines per list
 constexpr int TAB_CAP = 16384;       // n_total up to which position tables live in shared memory
 constexpr int G_THREADS = 640;       // 20 warps
 constexpr int RING = 1024;           // pick slots between producer and finalizer
-constexpr int AHEAD = 256;           // the producer runs at most this far ahead of the finalizer: picks
+constexpr int AHEAD = 512;           // the producer runs at most this far ahead of the finalizer: picks
                                      // past the plan's end cost crossing sums for nothing
 constexpr int GS_CAP = 8192;         // sampled positions kept in shared memory
 
@@ -293,6 +293,7 @@ struct GreedySmem {
   int16_t rowof[TAB_CAP];    // position -> sampled row, or -1
   uint16_t inv[2][TAB_CAP];  // line index -> sorted position (clamped to 65535)
   int32_t hitq[G_THREADS / 32][64];  // per consumer warp: sampled rows of crossing cells awaiting a value
+  double fold_w[32], fold_m[32];     // producer: the round's R-side weights / max cells
 };
 
 __device__ __forceinline__ int vload(const volatile int *p) { return *p; }
@@ -391,7 +392,10 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         w = L.w[g]; mx = L.mx[g]; len = L.len[g]; ix = L.idx[g];
       }
     };
+    int rounds = 0;
+    long long ph[4] = {0, 0, 0, 0};  // diagnostics: producer phase cycles (dbg)
     while (go) {
+      ++rounds;
       if ((s_idx >= n_total && v_idx >= n_total) || n >= cap) break;
       stop_seen = __shfl_sync(0xffffffffu, lane == 0 ? stop_at : 0, 0);  // one read: the warp must agree
       if (n >= stop_seen) break;
@@ -413,6 +417,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       }
       if (__shfl_sync(0xffffffffu, stopped, 0)) break;
       fin_seen = __shfl_sync(0xffffffffu, fin_seen, 0);
+      const long long c0 = clock64();
       const int O = 1 - R;
       const int base_R = R ? v_idx : s_idx, base_O = R ? s_idx : v_idx;
       double wR, mxR, wO, mxO;
@@ -420,29 +425,38 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       head(R, base_R + lane, wR, mxR, lR, iR);
       head(O, base_O, wO, mxO, lO, iO);
       const double olR0 = R ? ol_v : ol_s, olO = R ? ol_s : ol_v;
+      const long long c1 = clock64() + (static_cast<long long>(wR + wO + mxR + mxO + lR + lO + iR + iO) & 0);
       // folds in reference order: state before R pick j (ol_R, approx)
       double my_ol = olR0, my_ap = approx, ol_run = olR0, ap_run = approx;
-      if (base_R + K <= win) {
-        // window in shared memory: broadcast loads (issued ahead of the fold)
-        // instead of shuffles; the fold itself is the same sequential fp64 chain
-        const double *wp = S.w[R] + base_R, *mp = S.mx[R] + base_R;
+      // the round's R-side values, lane j = entry base_R + j, staged for the fold
+      // (which every lane runs redundantly in the reference's sequential order)
+      S.fold_w[lane] = wR;
+      S.fold_m[lane] = mxR;
+      __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i < K) {
-            if (lane == i) { my_ol = ol_run; my_ap = ap_run; }
-            ap_run += wp[i] - olO;  // approx += w - ol_other (prefill.py:210, 216)
-            ol_run += mp[i];        // ol_R += max_cell (prefill.py:212, 218)
+      for (int c = 0; c < 32; c += 8) {
+        if (c < K) {
+          double wv[8], mv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {  // 16 broadcast loads in flight, then the chains
+            wv[u] = S.fold_w[c + u] - olO;
+            mv[u] = S.fold_m[c + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = c + u;
+            const bool take = lane == i;
+            my_ol = take ? ol_run : my_ol;
+            my_ap = take ? ap_run : my_ap;
+            if (i < K) {
+              ap_run += wv[u];  // approx += w - ol_other (prefill.py:210, 216)
+              ol_run += mv[u];  // ol_R += max_cell (prefill.py:212, 218)
+            }
           }
         }
-      } else {
-        for (int i = 0; i < K; ++i) {
-          if (lane == i) { my_ol = ol_run; my_ap = ap_run; }
-          const double wi = __shfl_sync(0xffffffffu, wR, i);
-          const double mi = __shfl_sync(0xffffffffu, mxR, i);
-          ap_run += wi - olO;  // approx += w - ol_other (prefill.py:210, 216)
-          ol_run += mi;        // ol_R += max_cell (prefill.py:212, 218)
-        }
       }
+      __syncwarp();
+      const long long c2 = clock64() + (static_cast<long long>(my_ol + my_ap + ol_run + ap_run) & 0);
       // decision at (j = lane) R picks taken
       const int sj = R ? s_idx : s_idx + lane, vj = R ? v_idx + lane : v_idx;
       const bool has_s = sj < n_total, has_v = vj < n_total;
@@ -473,6 +487,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         f = cap - n;
         chain_end = true;
       }
+      const long long c3 = clock64();
       if (lane < f) {  // publish the R picks
         const int slot = (n + lane) % RING;
         S.r_code[slot] = R ? (iR | static_cast<int32_t>(0x80000000u)) : iR;
@@ -519,6 +534,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       approx = ap;
       if (chain_end || np == 0) go = false;
       if (!(approx < target - EPS)) go = false;
+      if (lane == 0) {
+        const long long c4 = clock64();
+        ph[0] += c1 - c0;
+        ph[1] += c2 - c1;
+        ph[2] += c3 - c2;
+        ph[3] += c4 - c3;
+      }
       // next window: keep speculating on R while its runs are long
       if (f >= 2) {
         K = f >= K ? min(32, 2 * K) : max(4, min(32, 2 * f + 2));
@@ -534,39 +556,69 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         dbg[60000 + blockIdx.x * 8 + 0] = n;
         dbg[60000 + blockIdx.x * 8 + 2] = static_cast<int>(clock64() - t_start);
         dbg[60000 + blockIdx.x * 8 + 4] = static_cast<int>(wait_cycles);
+        dbg[60000 + blockIdx.x * 8 + 7] = rounds;
+        for (int k = 0; k < 4; ++k) dbg[61000 + blockIdx.x * 4 + k] = static_cast<int>(ph[k]);
       }
     }
   } else if (warp == 1) {
     // ================================================= finalizer
-    if (lane == 0) {
-      double exact = 0.0, approx = 0.0;
-      int j = 0;
-      long long fwait = 0;
+    // The whole warp: lanes test the readiness of picks j .. j+31 at once and
+    // load the ready prefix in parallel; the exact-mass chain and the dual
+    // termination test then run over it in selection order (every lane
+    // redundantly, values by shuffle) -- the reference's sequential fp64 order.
+    double exact = 0.0, approx = 0.0;
+    int j = 0;
+    long long fwait = 0;
+    const bool no_cross = dbg && dbg[69999] == 1;
+    while (true) {
+      const long long tw0 = clock64();
+      SpinGuard guard;
+      int m = 0;
+      bool done = false;
       while (true) {
-        const int slot = j % RING;
-        int ready;
-        const long long tw0 = clock64();
-        SpinGuard guard;
-        while ((ready = vload(S.r_seq + slot)) != j + 1) {
-          guard.tick();
-          if (prod_done) {
-            __threadfence_block();
-            if (j >= n_prod) break;
-          }
-          __nanosleep(32);
+        const int slot = (j + lane) % RING;
+        const bool ready = vload(S.r_seq + slot) == j + lane + 1;
+        const unsigned rb = __ballot_sync(0xffffffffu, ready);
+        m = rb == 0xffffffffu ? 32 : __ffs(~rb) - 1;  // contiguous ready prefix
+        if (m > 0) break;
+        int pd = prod_done, np = 0;
+        if (pd) {
+          __threadfence_block();
+          np = n_prod;
         }
-        fwait += clock64() - tw0;
-        if (ready != j + 1) break;  // every published pick consumed
-        exact += static_cast<const volatile double *>(S.r_w)[slot] - static_cast<const volatile double *>(S.r_cross)[slot];
-        P.code[pb + j] = static_cast<const volatile int32_t *>(S.r_code)[slot];
-        approx = static_cast<const volatile double *>(S.r_approx)[slot];
-        ++j;
-        fin_pos = j;
-        if (!(approx < target - EPS && (exact < target - EPS || (dbg && dbg[69999] == 1)))) {
-          stop_at = j;
+        if (__shfl_sync(0xffffffffu, pd && j >= np ? 1 : 0, 0)) {  // every published pick consumed
+          done = true;
+          break;
+        }
+        if (lane == 0) guard.tick();
+        __nanosleep(32);
+      }
+      fwait += clock64() - tw0;
+      if (done) break;
+      __threadfence_block();  // the ready picks' fields were written before their sequence numbers
+      const int slot = (j + lane) % RING;
+      double wc = 0.0, ap_l = 0.0;
+      if (lane < m) {
+        wc = static_cast<const volatile double *>(S.r_w)[slot] - static_cast<const volatile double *>(S.r_cross)[slot];
+        ap_l = static_cast<const volatile double *>(S.r_approx)[slot];
+        P.code[pb + j + lane] = static_cast<const volatile int32_t *>(S.r_code)[slot];
+      }
+      int took = m;
+      bool stop = false;
+      for (int k = 0; k < m; ++k) {
+        exact += __shfl_sync(0xffffffffu, wc, k);
+        approx = __shfl_sync(0xffffffffu, ap_l, k);
+        if (!(approx < target - EPS && (exact < target - EPS || no_cross))) {
+          took = k + 1;
+          stop = true;
           break;
         }
       }
+      j += took;
+      if (lane == 0) fin_pos = j;
+      if (stop) break;
+    }
+    if (lane == 0) {
       stop_at = j;
       if (dbg) {
         dbg[60000 + blockIdx.x * 8 + 1] = j;

@@ -29,4 +29,5 @@ for t, (ro, n_new) in enumerate([(0, 5000), (5000, 5128), (10128, 5128), (10128,
           f"({float(d[:, 2].max()) / max(1, int(d[int(d[:, 2].argmax()), 0])):.0f}/pick); "
           f"finalizer cycles max {int(d[:, 3].max())}; producer ring-full wait max {int(d[:, 4].max())}; "
           f"finalizer wait (slowest head) {int(d[int(d[:, 3].argmax()), 5])}; consumer busy/16 (slowest head) "
-          f"{int(d[int(d[:, 3].argmax()), 6])} -> x16/13 warps = {int(d[int(d[:, 3].argmax()), 6]) * 16 // 13} per warp")
+          f"{int(d[int(d[:, 3].argmax()), 6])}; producer rounds (slowest head) {int(d[int(d[:, 2].argmax()), 7])}; "
+          f"phases head/fold/decide/publish {dbg[61000:61000 + 128].view(32, 4)[int(d[:, 2].argmax())].tolist()}")
