@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       }
       if (__shfl_sync(0xffffffffu, stopped, 0)) break;
       fin_seen = __shfl_sync(0xffffffffu, fin_seen, 0);
-      const long long c0 = clock64();
+      const bool prof = dbg != nullptr;  // phase clocks only when profiling (ls_debug_set_buffer)
+      const long long c0 = prof ? clock64() : 0;
       const int O = 1 - R;
       const int base_R = R ? v_idx : s_idx, base_O = R ? s_idx : v_idx;
       double wR, mxR, wO, mxO;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       head(R, base_R + lane, wR, mxR, lR, iR);
       head(O, base_O, wO, mxO, lO, iO);
       const double olR0 = R ? ol_v : ol_s, olO = R ? ol_s : ol_v;
-      const long long c1 = clock64() + (static_cast<long long>(wR + wO + mxR + mxO + lR + lO + iR + iO) & 0);
+      const long long c1 = prof ? clock64() + (static_cast<long long>(wR + wO + mxR + mxO + lR + lO + iR + iO) & 0) : 0;
       // folds in reference order: state before R pick j (ol_R, approx)
       double my_ol = olR0, my_ap = approx, ol_run = olR0, ap_run = approx;
       // the round's R-side values, lane j = entry base_R + j, staged for the fold
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         }
       }
       __syncwarp();
-      const long long c2 = clock64() + (static_cast<long long>(my_ol + my_ap + ol_run + ap_run) & 0);
+      const long long c2 = prof ? clock64() + (static_cast<long long>(my_ol + my_ap + ol_run + ap_run) & 0) : 0;
       // decision at (j = lane) R picks taken
       const int sj = R ? s_idx : s_idx + lane, vj = R ? v_idx + lane : v_idx;
       const bool has_s = sj < n_total, has_v = vj < n_total;
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         f = cap - n;
         chain_end = true;
       }
-      const long long c3 = clock64();
+      const long long c3 = prof ? clock64() : 0;
       if (lane < f) {  // publish the R picks
         const int slot = (n + lane) % RING;
         S.r_code[slot] = R ? (iR | static_cast<int32_t>(0x80000000u)) : iR;
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       approx = ap;
       if (chain_end || np == 0) go = false;
       if (!(approx < target - EPS)) go = false;
-      if (lane == 0) {
+      if (prof && lane == 0) {
         const long long c4 = clock64();
         ph[0] += c1 - c0;
         ph[1] += c2 - c1;
