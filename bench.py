@@ -460,7 +460,10 @@ def roofline(per, cfg, eng, store, blocks, peaks):
     elif name.startswith("decode_graph_") and name != "decode_graph_event":
         kind = name[len("decode_graph_"):]
         cols = [c for k, c in eng.decode_log if k == kind]
-        bytes_ = 4.0 * d * sum(cols) / max(1, len(cols))  # bf16 K + V row per KV-head column, all layers
+        # bf16 K + V row per KV-head column, all layers, per launch (a launch is a
+        # graph of one or more steps)
+        bytes_ = 4.0 * d * sum(cols) / max(1, n)
+        extra = {"steps_per_launch": round(len(cols) / max(1, n), 3)}
         bound, unit, peak = "hbm", "GB/s", peaks["hbm"]
         achieved = bytes_ / (mean_ms * 1e-3) / 1e9 if bytes_ else None
         work = bytes_
@@ -473,6 +476,8 @@ def roofline(per, cfg, eng, store, blocks, peaks):
             "share_of_timed": None}
     res.update(extra)
     tr = NCU_TRAFFIC.get("ls_vs_attention" if name.startswith("ls_vs_attention") else name)
+    if tr is not None and "steps_per_launch" in extra:  # the capture is one step
+        tr = dict(tr, dram_bytes_per_launch=round(tr["dram_bytes_per_launch"] * extra["steps_per_launch"]))
     if tr:  # dram bytes per launch from the committed ncu --set full capture
         res["traffic"] = tr["dram_bytes_per_launch"]
         res["traffic_src"] = tr["source"]

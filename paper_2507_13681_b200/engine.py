@@ -347,6 +347,28 @@ class SessionEngine:
             graphs["event"] = self._graph(("event", sk, comp.budget, ev_len), "decode_graph_event",
                                           lambda: st.event(comp.budget, store.k, store.v, max_len=ev_len))
         compressed = False
+        if out_sink is None:
+            # no per-step host work: every run of steps between two events is one
+            # graph of that many steps (the kernels read the device counters, so
+            # a multi-step graph is the same launch sequence back to back)
+            n_o = 1
+            while n_o <= max_new:
+                if comp.event_at(n_o):
+                    graphs["event"].replay()
+                    compressed = True
+                nxt = n_o + 1
+                while nxt <= max_new and not comp.event_at(nxt):
+                    nxt += 1
+                n = nxt - n_o
+                kind, cols = ("comp", comp_cols) if compressed else ("dense", dense_cols)
+                g = self._graph((kind, sk, cols, n), f"decode_graph_{kind}",
+                                lambda n=n, c=compressed, cols=cols: [self._step(store, q_buf, out_buf, c, cols)
+                                                                      for _ in range(n)])
+                g.replay()
+                st.length += n
+                st.appended += n
+                n_o = nxt
+            return out_buf
         for n_o in range(1, max_new + 1):
             if comp.event_at(n_o):
                 graphs["event"].replay()
@@ -354,8 +376,7 @@ class SessionEngine:
             graphs["comp" if compressed else "dense"].replay()
             st.length += 1
             st.appended += 1
-            if out_sink is not None:
-                out_sink(n_o - 1, out_buf)
+            out_sink(n_o - 1, out_buf)
         return out_buf
 
     def turn_blocks(self, input_len: int, n_turns: int, max_new: int):

@@ -160,3 +160,20 @@ def test_prefill_layer_hooks(cuda_lib):
     for l in range(3):
         assert calls[2 * l + 1][2] == res.out[l].data_ptr()
         assert torch.equal(res.out[l], ref.out[l])
+
+
+def test_multistep_graphs_identical(cuda_lib):
+    """Without a per-step sink every run of steps between events is one graph
+    replay; the last step's outputs and the decode state equal the eager path."""
+    outs = []
+    for use_graphs in (False, True):
+        eng, store, n_new, max_new = _engine()
+        eng.prefill(store, 0, 0, n_new)
+        last = eng.decode(store, n_new, max_new, use_graphs=use_graphs)
+        torch.cuda.synchronize()
+        st = eng.stack
+        outs.append((last.float().cpu().clone(), st.step_t.cpu().clone(), st.sel_ids.cpu().clone(),
+                     st.n_a.cpu().clone(), (st.length, st.appended)))
+    (a, sa, sela, naa, ha), (b, sb, selb, nab, hb) = outs
+    assert torch.equal(a, b)
+    assert torch.equal(sa, sb) and torch.equal(sela, selb) and torch.equal(naa, nab) and ha == hb
