@@ -393,6 +393,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       }
     };
     int rounds = 0;
+    int pf_kind = -1, pf_base = -1;  // prefetched R-side window of the next round
+    double pf_w = 0.0, pf_mx = 0.0;
+    int pf_len = 0, pf_ix = 0;
     long long ph[4] = {0, 0, 0, 0};  // diagnostics: producer phase cycles (dbg)
     while (go) {
       ++rounds;
@@ -423,7 +426,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       const int base_R = R ? v_idx : s_idx, base_O = R ? s_idx : v_idx;
       double wR, mxR, wO, mxO;
       int lR, iR, lO, iO;
-      head(R, base_R + lane, wR, mxR, lR, iR);
+      if (pf_kind == R && pf_base == base_R) {  // the window loaded during the previous round
+        wR = pf_w; mxR = pf_mx; lR = pf_len; iR = pf_ix;
+      } else {
+        head(R, base_R + lane, wR, mxR, lR, iR);
+      }
       head(O, base_O, wO, mxO, lO, iO);
       const double olR0 = R ? ol_v : ol_s, olO = R ? ol_s : ol_v;
       const long long c1 = prof ? clock64() + (static_cast<long long>(wR + wO + mxR + mxO + lR + lO + iR + iO) & 0) : 0;
@@ -488,6 +495,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
         f = cap - n;
         chain_end = true;
       }
+      // the next round most likely continues this kind at base_R + f: start its
+      // window's loads now (L2 beyond the staged WIN entries) so they land while
+      // this round publishes
+      pf_kind = R;
+      pf_base = base_R + f;
+      head(R, pf_base + lane, pf_w, pf_mx, pf_len, pf_ix);
       const long long c3 = prof ? clock64() : 0;
       if (lane < f) {  // publish the R picks
         const int slot = (n + lane) % RING;
