@@ -51,7 +51,7 @@ constexpr int K7_SMEM_CAP = 24 * 1024;  // ids accumulated in shared memory (fp6
 constexpr int K7_CAND_CAP = 4096;       // touched ids listed in shared memory (radix + ranking over the list)
 constexpr int K7_BITONIC = 2048;        // candidate lists up to this size are ranked by one bitonic sort
 constexpr int K7_RB = 8, K7_PF = 2;     // rows fetched per round, columns per thread per row
-constexpr int K7_DMAX = 64, K7_DCH = 8;   // dense-window fast path: rows, rows loaded per batch
+constexpr int K7_DMAX = 64, K7_DCH = 16;  // dense-window fast path: rows, rows loaded per batch
 
 __device__ __forceinline__ int64_t head_row(const ls_decode_stack &S, int layer, int h) {
   return static_cast<int64_t>(layer) * S.n_heads + h;
