@@ -408,7 +408,11 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
         }
       }
     }
-    cta_sync_tc();
+    // P lives in generic-proxy shared memory only (the MMAs read Q and K): no
+    // proxy fence here, just the TMEM read -> next-MMA ordering around the barrier
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
     if (t + 1 < n_tiles && tid == 0) {
       tc::mbar_wait(&kfull[buf ^ 1], ((t + 1) >> 1) & 1);
       issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
