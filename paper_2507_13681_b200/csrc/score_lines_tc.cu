@@ -472,7 +472,8 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
         if (mx > 0.f) atomicMax(p.vmaxb + static_cast<int64_t>(h) * p.n_total + c, __float_as_uint(mx));
       }
     }
-    __syncthreads();  // Pf / colp reused by the next tile
+    // (no barrier here: every read of Pf precedes the barrier above, and the next
+    // tile writes colp / the slash accumulator only after its own first barrier)
   }
   if (smem_acc)
     for (int i = tid; i < width; i += LINES_THREADS) {
