@@ -348,21 +348,46 @@ __global__ void __launch_bounds__(PR_CHUNK) plan_scores_kernel(Params p, int n_r
 __global__ void __launch_bounds__(256) plan_norm_kernel(Params p, int n_rows, float *out, int64_t out_stride,
                                                         int64_t out_head_stride, const float2 *part, int n_chunks) {
   __shared__ float stats[2];
+  __shared__ float red[256 / 32];
   const int i = blockIdx.x, h = blockIdx.y;
   const int g = p.row_offset + p.n_new - n_rows + i;
   const float2 *pp = part + (static_cast<int64_t>(h) * n_rows + i) * n_chunks;
+  // the chunk partials combined by the whole block (fixed-order reductions:
+  // deterministic), not by one thread walking them serially
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float m = -INFINITY;
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) m = fmaxf(m, pp[c].x);
+  m = warp_max(m);
+  if (lane == 0) red[wid] = m;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    float M = -INFINITY, S = 0.f;
-    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, pp[c].x);
-    for (int c = 0; c < n_chunks; ++c)
-      if (pp[c].x != -INFINITY) S += pp[c].y * fast_exp2(pp[c].x - M);
+    float M = -INFINITY;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) M = fmaxf(M, red[w]);
     stats[0] = M;
+  }
+  __syncthreads();
+  const float Mb = stats[0];
+  float sacc = 0.f;
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
+    const float2 v = pp[c];
+    if (v.x != -INFINITY) sacc += v.y * fast_exp2(v.x - Mb);
+  }
+  sacc = warp_sum(sacc);
+  __syncthreads();  // red reused
+  if (lane == 0) red[wid] = sacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float S = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) S += red[w];
     stats[1] = S > 0.f ? 1.f / S : 0.f;
   }
   __syncthreads();
   const float M = stats[0], inv = stats[1];
   float *orow = out + static_cast<int64_t>(h) * out_head_stride + static_cast<int64_t>(i) * out_stride;
-  for (int c = threadIdx.x; c < p.n_total; c += blockDim.x) {
+  // this CTA's column slice (grid.z): every slice recomputes the row statistics
+  const int per = (p.n_total + gridDim.z - 1) / gridDim.z;
+  const int c_lo = blockIdx.z * per, c_hi = min(p.n_total, c_lo + per);
+  for (int c = c_lo + threadIdx.x; c < c_hi; c += blockDim.x) {
     if (M == -INFINITY) {
       orow[c] = (c == g) ? 1.f : 0.f;
     } else {
@@ -561,7 +586,8 @@ extern "C" int ls_plan_rows(const ls_layer_desc *L, int32_t n_rows, const uint16
   k5::plan_scores_kernel<<<dim3(n_chunks, n_rows, L->n_heads), k5::PR_CHUNK, 0, st>>>(p, n_rows, out, out_row_stride,
                                                                                      out_head_stride, part, n_chunks);
   LS_LAUNCH_CHECK("plan_scores_kernel");
-  k5::plan_norm_kernel<<<dim3(n_rows, L->n_heads), 256, 0, st>>>(p, n_rows, out, out_row_stride, out_head_stride, part,
+  k5::plan_norm_kernel<<<dim3(n_rows, L->n_heads, (L->n_total + 2047) / 2048), 256, 0, st>>>(
+      p, n_rows, out, out_row_stride, out_head_stride, part,
                                                                  n_chunks);
   LS_LAUNCH_CHECK("plan_norm_kernel");
   LS_CUDA(cudaFreeAsync(bits, st));
