@@ -26,6 +26,7 @@ h reads kv-head h // (n_q / n_kv). Outputs are token-major [n_new, n_q, d].
 from __future__ import annotations
 
 import math
+from contextlib import nullcontext as _nullcontext
 from dataclasses import dataclass, field
 
 import torch
@@ -211,6 +212,14 @@ class SessionEngine:
             cells_all.append(cells)
             self.cell_log.append(cells)
             self.score_log.append(plans.score_count)
+        if surv > 0 and p.mode != "dense":
+            # seed slots [n_seed - surv, n_seed) of every (layer, head): stored
+            # probabilities (sum 0 marks them), dense rows of n_total columns
+            first = n_seed - surv
+            with torch.cuda.stream(stream) if stream is not None else _nullcontext():
+                st.ring_ml[:, first:n_seed] = 0.0
+                st.ring_n[:, first:n_seed] = n_total
+                st.ring_dense[:, first:n_seed] = 1
         st.set_step(n_total, n_seed)
         return PrefillOut(outs, plans_all, cells_all, rows, n_new, n_total, n_seed)
 
@@ -234,9 +243,7 @@ class SessionEngine:
             plan_rows(qg, kg, plans.slash_ids, plans.vert_ids, plans.counts, n_new, n_total, n_kv, surv,
                       out=st.ring_s[hr, first:], out_row_stride=st.row_cap, out_head_stride=st.window * st.row_cap,
                       q_head_stride=qhs, stream=stream)
-            st.ring_ml[hr, first:n_seed] = 0.0
-            st.ring_n[hr, first:n_seed] = n_total
-            st.ring_dense[hr, first:n_seed] = 1
+            # (the seed slots' metadata is set once for every layer after the loop)
         return plans, out, cells, tiles
 
     def _layer_groups(self, l, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs, stream):
