@@ -280,6 +280,48 @@ int ls_decode_event(const ls_decode_stack *S, int32_t budget, int32_t max_len, c
                     const uint16_t *v_all, int32_t *retained_n, double *score_coverage, void *ws,
                     size_t ws_bytes, ls_stream_t stream);
 
+/* ------------------------------------------ reference-API decode pieces ---
+ * One call per reference function, for callers that keep the decode state in
+ * the reference's own types (numpy ids / rows) -- the drop-in patched onto
+ * loopserve.kvcompress / loopserve.model (paper_2507_13681_b200/dropin.py).
+ *
+ * accumulate_scores (kvcompress.py:67-83): rows r = 0..n_rows-1 oldest first,
+ * row r = ids/w[row_ptr[r] .. row_ptr[r+1]), ids distinct within a row and in
+ * [0, id_cap). acc[id] = 0.0 + w_0 + w_1 + ... in row order (fp64, the
+ * reference's order); touched[id] = 1 for every id some row holds (only those
+ * are candidates, kvcompress.py:73-83). LS_ERR_EMPTY_WINDOW for n_rows < 1. */
+int ls_accumulate_scores(int32_t n_rows, const int64_t *row_ptr, const int32_t *ids, const double *w,
+                         int32_t id_cap, double *acc, uint8_t *touched, ls_stream_t stream);
+/* _top_by_score (kvcompress.py:86-90): the budget highest of n (id, score)
+ * pairs by (score desc, id asc), written to out[0..budget) in ascending id
+ * order; ids distinct, inside [id_lo, id_lo + id_range). *n_out = ids written.
+ * Workspace: ls_top_by_score_workspace(id_range) bytes. */
+size_t ls_top_by_score_workspace(int32_t id_range);
+int ls_top_by_score(int32_t n, const int32_t *ids, const double *scores, int32_t budget, int32_t id_lo,
+                    int32_t id_range, int32_t *out, int32_t *n_out, void *ws, size_t ws_bytes, ls_stream_t stream);
+/* retained_union (kvcompress.py:126-130): sorted unique union of sel[0..n_sel)
+ * and [full_len - recent_window, full_len); ids in [0, cap). out capacity
+ * n_sel + recent_window; *n_out = its length. Workspace (cap + 31) / 32 * 4 bytes. */
+int ls_retained_union(int32_t n_sel, const int32_t *sel, int32_t recent_window, int32_t full_len, int32_t cap,
+                      int32_t *out, int32_t *n_out, void *ws, size_t ws_bytes, ls_stream_t stream);
+/* compact_cache's gather (kvcompress.py:133-147, K8): dst row r = the source
+ * row whose id (src_ids strictly increasing) equals keep_ids[r], for K rows of
+ * k_row_bytes and V rows of v_row_bytes (multiples of 16; 16-byte coalesced
+ * copies). *status = 0, or 1 + a keep index whose id is not in the source
+ * (-> InvalidIds). */
+int ls_kv_compact(int32_t n_src, const int32_t *src_ids, const void *src_k, const void *src_v, int32_t n_keep,
+                  const int32_t *keep_ids, int32_t k_row_bytes, int32_t v_row_bytes, void *dst_k, void *dst_v,
+                  int32_t *status, ls_stream_t stream);
+/* Working-set attention of one decode token for every head of a layer
+ * (forward_extend's working-set branch, model.py:232-241): head h attends to
+ * cols[col_ptr[h] .. col_ptr[h+1]) of kv-head h / (n_heads / n_kv_heads);
+ * bf16 q / K / V (q + h*q_head_stride, k / v + kv*kv_head_stride + pos*head_dim),
+ * fp64 arithmetic as the reference's branch. out[h][head_dim] = w . V[cols];
+ * w_out[col_ptr[h] + j] = softmax weight of column j (the observation row). */
+int ls_gather_attention(int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, const uint16_t *q,
+                        int64_t q_head_stride, const uint16_t *k, const uint16_t *v, int64_t kv_head_stride,
+                        const int64_t *col_ptr, const int32_t *cols, double *out, double *w_out, ls_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

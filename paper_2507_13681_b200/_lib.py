@@ -77,6 +77,12 @@ SIGNATURES = {
     "ls_decode_advance": (C.c_int, [DS, P]),
     "ls_decode_select_workspace": (SZ, [DS]),
     "ls_decode_event": (C.c_int, [DS, I32, I32, P, P, P, P, P, SZ, P]),
+    "ls_accumulate_scores": (C.c_int, [I32, P, P, P, I32, P, P, P]),
+    "ls_top_by_score_workspace": (SZ, [I32]),
+    "ls_top_by_score": (C.c_int, [I32, P, P, I32, I32, I32, P, P, P, SZ, P]),
+    "ls_retained_union": (C.c_int, [I32, P, I32, I32, I32, P, P, P, SZ, P]),
+    "ls_kv_compact": (C.c_int, [I32, P, P, P, I32, P, I32, I32, P, P, P, P]),
+    "ls_gather_attention": (C.c_int, [I32, I32, I32, P, I64, P, P, I64, P, P, P, P, P]),
 }
 
 
@@ -115,6 +121,8 @@ KERNELS_PER_CALL = {
     "ls_vs_attention": 3, "ls_vs_attention_ex": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
     "ls_plan_coverage": 7,
     "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
+    "ls_accumulate_scores": 1, "ls_top_by_score": 1, "ls_retained_union": 1, "ls_kv_compact": 1,
+    "ls_gather_attention": 1,
 }
 launch_count = 0
 entry_hook = None  # optional callable(name, phase) used by bench.py to time entries

@@ -107,13 +107,18 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_lines_kernel(const double *
 
 // K2 (device-wide): every (head, kind) list of a layer sorted at once by one
 // stable LSD radix sort over composite keys
-//   (segment << 50) | (2^50 - 1 - fixed point weight)
-// K1's line weights are exact multiples of 2^-40 below 2^10, so the 50-bit
-// fixed-point integer orders them exactly; ties keep index order (stable).
-// The whole GPU sorts, and n_total is not bounded by one SM's shared memory.
-constexpr int FIX_BITS = 50;
+//   (segment << fix_bits) | (2^fix_bits - 1 - fixed point weight)
+// K1's line weights are exact multiples of 2^-40 and at most n_s (every row
+// sums to 1), so a fix_bits = 40 + bits(n_s) integer orders them exactly;
+// ties keep index order (stable). The whole GPU sorts, and n_total is not
+// bounded by one SM's shared memory.
+inline int fix_bits_for(int n_s) {
+  int b = 0;
+  while ((1ll << b) <= static_cast<long long>(n_s)) ++b;
+  return 40 + b;
+}
 
-__global__ void sort_keys_kernel(const double *v_w, const double *s_w, int H, int n_total,
+__global__ void sort_keys_kernel(const double *v_w, const double *s_w, int H, int n_total, int FIX_BITS,
                                  unsigned long long *keys, int32_t *vals) {
   const int64_t n = static_cast<int64_t>(2) * H * n_total;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -128,14 +133,21 @@ __global__ void sort_keys_kernel(const double *v_w, const double *s_w, int H, in
   }
 }
 
+constexpr int kScatterShRows = 12 * 1024;  // 48 KB of positions: the default dynamic shared memory
+
 template <typename MaxT>
 __global__ void sort_scatter_kernel(const unsigned long long *keys_sorted, const int32_t *vals_sorted,
                                     const double *v_w, const MaxT *v_max, const double *s_w, const MaxT *s_max,
                                     const int32_t *rows, int n_s, int n_total, int row_offset, int H, Lists out) {
-  extern __shared__ int pos_sh[];  // sampled positions of this head
+  extern __shared__ int pos_sh[];  // sampled local rows of this head (when they fit in shared memory)
   const int h = blockIdx.y;
-  for (int r = threadIdx.x; r < n_s; r += blockDim.x) pos_sh[r] = row_offset + rows[static_cast<int64_t>(h) * n_s + r];
-  __syncthreads();
+  const int32_t *rows_h = rows + static_cast<int64_t>(h) * n_s;
+  const bool in_sh = n_s <= kScatterShRows;
+  if (in_sh) {
+    for (int r = threadIdx.x; r < n_s; r += blockDim.x) pos_sh[r] = rows_h[r];
+    __syncthreads();
+  }
+  const int32_t *pos = in_sh ? pos_sh : rows_h;
   for (int kind = 0; kind < 2; ++kind) {
     const int64_t base = (static_cast<int64_t>(h) * 2 + kind) * n_total;
     const double *w = (kind == 0 ? s_w : v_w) + static_cast<int64_t>(h) * n_total;
@@ -145,7 +157,8 @@ __global__ void sort_scatter_kernel(const unsigned long long *keys_sorted, const
       out.idx[base + o] = idx;
       out.w[base + o] = w[idx];
       out.mx[base + o] = static_cast<double>(mx[idx]);
-      out.len[base + o] = n_s - lower_bound_dev(pos_sh, n_s, idx);  // #{rows with g >= idx}, prefill.py:144,155
+      // #{rows with g >= idx}, prefill.py:144,155 (g = row_offset + local row)
+      out.len[base + o] = n_s - lower_bound_dev(pos, n_s, idx - row_offset);
       out.inv[base + idx] = o;
     }
   }
@@ -954,7 +967,11 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
                                double *approx, int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
                                ls_stream_t stream) {
   LS_REQUIRE(alpha >= 0.0 && alpha <= 1.0, LS_ERR_INVALID_ALPHA, "alpha=%g outside [0, 1]", alpha);
-  LS_REQUIRE(2 * L->n_heads < (1 << (64 - sel::FIX_BITS)), LS_ERR_UNSUPPORTED, "too many heads for the sort key");
+  const int fix_bits = sel::fix_bits_for(n_s);
+  int seg_bits = 1;
+  while ((1 << seg_bits) < 2 * L->n_heads) ++seg_bits;
+  LS_REQUIRE(fix_bits + seg_bits <= 64, LS_ERR_UNSUPPORTED, "sort key too wide (%d heads, %d sampled rows)",
+             L->n_heads, n_s);
   LS_REQUIRE(ws_bytes >= ls_select_lines_workspace(L, n_s), LS_ERR_WORKSPACE, "select_lines workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int H = L->n_heads, n_total = L->n_total;
@@ -963,14 +980,13 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   sel::SortWork sw = sel::carve_sort(c, H, n_total);
   {
     const int n = 2 * H * n_total;
-    int seg_bits = 1;
-    while ((1 << seg_bits) < 2 * H) ++seg_bits;
-    sel::sort_keys_kernel<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(v_w, s_w, H, n_total, sw.k_in, sw.v_in);
+    sel::sort_keys_kernel<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(v_w, s_w, H, n_total, fix_bits,
+                                                                                sw.k_in, sw.v_in);
     LS_LAUNCH_CHECK("sort_keys_kernel");
     size_t tb = sw.temp_bytes;
     LS_CUDA(cub::DeviceRadixSort::SortPairs(sw.temp, tb, sw.k_in, sw.k_out, sw.v_in, sw.v_out, n, 0,
-                                            sel::FIX_BITS + seg_bits, st));
-    const int smem_pos = n_s * 4;
+                                            fix_bits + seg_bits, st));
+    const int smem_pos = n_s <= sel::kScatterShRows ? n_s * 4 : 0;
     sel::sort_scatter_kernel<float><<<dim3(std::max(1, std::min(ceil_div(n_total, 256), 16)), H), 256, smem_pos, st>>>(
         sw.k_out, sw.v_out, v_w, v_max, s_w, s_max, rows, n_s, n_total, L->row_offset, H, w.lists);
     LS_LAUNCH_CHECK("sort_scatter_kernel");

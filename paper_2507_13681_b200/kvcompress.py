@@ -232,96 +232,180 @@ class DecodeStack:
         return self.ring_ids[hr, slot, :n].cpu().numpy().astype(np.intp), w
 
 
+def _i32_dev(x) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int32), device=_dev())
+
+
+def _f64_dev(x) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=_dev())
+
+
+def _check_id_range(ids: np.ndarray, what: str) -> None:
+    if len(ids) and (ids.min() < 0 or ids.max() >= 2 ** 31 - 1):
+        raise InvalidIds(f"{what}: ids must lie in [0, 2^31 - 1) on the device path")
+
+
 def retained_union(selected, recent_window: int, full_len: int) -> np.ndarray:
-    """kvcompress.py:126-130 (on the device)."""
+    """kvcompress.py:126-130 on the device (ls_retained_union: bitmap union,
+    ids emitted in ascending order)."""
+    sel = np.asarray(selected, dtype=np.int64).ravel()
+    _check_id_range(sel, "retained_union")
+    recent_window, full_len = int(recent_window), int(full_len)
+    cap = max(full_len, int(sel.max()) + 1 if len(sel) else 0, 1)
     dev = _dev()
-    sel = torch.as_tensor(np.asarray(selected, dtype=np.int64), device=dev)
-    recent = torch.arange(max(0, full_len - recent_window), full_len, device=dev, dtype=torch.int64)
-    return torch.unique(torch.cat([sel, recent])).cpu().numpy().astype(np.intp)
+    out = torch.empty(len(sel) + max(0, min(recent_window, full_len)) + 1, dtype=torch.int32, device=dev)
+    n_out = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = torch.empty((cap + 31) // 32 * 4, dtype=torch.uint8, device=dev)
+    sel_t = _i32_dev(sel) if len(sel) else torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("ls_retained_union", len(sel), sel_t.data_ptr(), recent_window, full_len, cap, out.data_ptr(),
+              n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    n = int(n_out.item())
+    return out[:n].cpu().numpy().astype(np.intp)
 
 
-def _rows_select(buffered_rows, budget: int):
-    """Run K7 on caller rows; returns (ids, scores, picked)."""
-    rows = list(buffered_rows)
-    if not rows:
-        raise EmptyWindow("need at least one observation row")
-    id_cap = max(int(np.max(ids)) + 1 if len(ids) else 1 for ids, _ in rows)
-    n_max = max(len(ids) for ids, _ in rows)
-    cap = max(id_cap, n_max) + 1
-    st = DecodeStack(1, 1, 1, 64, len(rows), max(1, budget), cap, 0, 0, sparse_cap=n_max)
-    for i, (ids, w) in enumerate(rows):
-        st.write_sparse_row(0, 0, i, np.asarray(ids), np.asarray(w))
-    st.set_step(id_cap, len(rows))
-    dummy = torch.zeros(8 * 64, dtype=torch.bfloat16, device=st.ring_s.device)
-    st.event(max(1, budget), dummy, dummy, max_len=id_cap)
-    # scores: host re-accumulation of the same fp32 weights in the same order
-    acc = np.zeros(id_cap)
-    touched = np.zeros(id_cap, dtype=bool)
+def _accumulate_device(rows):
+    """ls_accumulate_scores on (ids, weights) rows -> (acc, touched) numpy."""
+    ids_l, w_l = [], []
     for ids, w in rows:
-        np.add.at(acc, np.asarray(ids, dtype=np.intp), np.asarray(w, dtype=np.float32).astype(np.float64))
-        touched[np.asarray(ids, dtype=np.intp)] = True
-    ids = np.nonzero(touched)[0].astype(np.intp)
-    n = int(st.n_sel[0].item())
-    picked = st.sel_ids[0, :n].cpu().numpy().astype(np.intp)
-    return ids, acc[ids], picked
+        ids = np.asarray(ids, dtype=np.int64).ravel()
+        w = np.asarray(w, dtype=np.float64).ravel()
+        if len(w) < len(ids):
+            raise SizeMismatch("observation row has fewer weights than ids")
+        ids_l.append(ids)
+        w_l.append(w[:len(ids)])
+    if not ids_l:
+        raise EmptyWindow("need at least one observation row")
+    flat_ids = np.concatenate(ids_l) if ids_l else np.zeros(0, np.int64)
+    _check_id_range(flat_ids, "accumulate_scores")
+    flat_w = np.concatenate(w_l)
+    row_ptr = np.zeros(len(ids_l) + 1, dtype=np.int64)
+    row_ptr[1:] = np.cumsum([len(i) for i in ids_l])
+    id_cap = int(flat_ids.max()) + 1 if len(flat_ids) else 1
+    dev = _dev()
+    acc = torch.empty(id_cap, dtype=torch.float64, device=dev)
+    touched = torch.empty(id_cap, dtype=torch.uint8, device=dev)
+    ids_t = _i32_dev(flat_ids) if len(flat_ids) else torch.zeros(1, dtype=torch.int32, device=dev)
+    w_t = _f64_dev(flat_w) if len(flat_w) else torch.zeros(1, dtype=torch.float64, device=dev)
+    _lib.call("ls_accumulate_scores", len(ids_l), torch.as_tensor(row_ptr, device=dev).data_ptr(), ids_t.data_ptr(),
+              w_t.data_ptr(), id_cap, acc.data_ptr(), touched.data_ptr(), _lib.stream_ptr())
+    return acc.cpu().numpy(), touched.cpu().numpy().astype(bool)
 
 
 def accumulate_scores(buffered_rows):
-    """kvcompress.py:67-83 on the device (fp32 weights, fp64 sums)."""
-    ids, scores, _ = _rows_select(buffered_rows, 1)
-    return ids, scores
+    """kvcompress.py:67-83 on the device: fp64 sums in the reference's order
+    (rows oldest -> newest per id); only touched ids are candidates. Ids must
+    be distinct within a row (the reference's rows are working-set columns)."""
+    acc, touched = _accumulate_device(list(buffered_rows))
+    ids = np.nonzero(touched)[0].astype(np.intp)
+    return ids, acc[ids]
 
 
 def token_scores(window_rows) -> np.ndarray:
-    """kvcompress.py:58-64: dense rows -> column sums (device)."""
+    """kvcompress.py:58-64: dense rows -> column sums, added row by row on the
+    device (the order of numpy's axis-0 sum)."""
     rows = np.asarray(window_rows, dtype=np.float64)
     if rows.ndim != 2 or rows.shape[0] == 0:
         raise EmptyWindow("need at least one observation row")
-    dev = _dev()
-    return torch.as_tensor(rows, device=dev).sum(dim=0).cpu().numpy()
+    cols = np.arange(rows.shape[1])
+    acc, _ = _accumulate_device([(cols, r) for r in rows])
+    return acc[:rows.shape[1]]
 
 
 def _top_by_score(ids: np.ndarray, scores: np.ndarray, budget: int) -> np.ndarray:
-    """kvcompress.py:86-90 on the device via K7's radix select."""
-    ids = np.asarray(ids, dtype=np.intp)
-    scores = np.asarray(scores, dtype=np.float64)
-    if budget >= len(ids):
-        return np.sort(ids)
-    _, _, picked = _rows_select([(ids, scores)], budget)
-    return picked
+    """kvcompress.py:86-90 on the device (ls_top_by_score: radix select on
+    (score desc, id asc), ids emitted ascending). Ids must be distinct."""
+    ids = np.asarray(ids, dtype=np.int64).ravel()
+    scores = np.asarray(scores, dtype=np.float64).ravel()
+    if len(ids) != len(scores):
+        raise SizeMismatch("ids and scores differ in length")
+    if len(ids) == 0:
+        return np.zeros(0, dtype=np.intp)
+    _check_id_range(ids, "_top_by_score")
+    b = int(min(int(budget), len(ids)))
+    if b < 1:
+        return np.zeros(0, dtype=np.intp)
+    lo = int(ids.min())
+    rng = int(ids.max()) - lo + 1
+    dev = _dev()
+    out = torch.empty(b, dtype=torch.int32, device=dev)
+    n_out = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(_lib.lib().ls_top_by_score_workspace(rng)), dtype=torch.uint8, device=dev)
+    _lib.call("ls_top_by_score", len(ids), _i32_dev(ids).data_ptr(), _f64_dev(scores).data_ptr(), b, lo, rng,
+              out.data_ptr(), n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    if int(n_out.item()) != b:
+        raise InvalidIds("_top_by_score: ids must be distinct")
+    return out.cpu().numpy().astype(np.intp)
 
 
 def select_topB_obs(scores, budget: int, aggregate: str = "per_head", candidate_ids=None):
-    """kvcompress.py:93-109."""
+    """kvcompress.py:93-109 (summed_over_heads: the head sum runs on the device
+    in head order, as numpy's axis-0 sum)."""
     s = np.atleast_2d(np.asarray(scores, dtype=np.float64))
     ids = np.arange(s.shape[1]) if candidate_ids is None else np.asarray(candidate_ids)
     if len(ids) != s.shape[1]:
         raise SizeMismatch("candidate_ids length must match score columns")
     if aggregate == "summed_over_heads":
-        return _top_by_score(ids, s.sum(axis=0), budget)
+        return _top_by_score(ids, token_scores(s), budget)
     if aggregate == "per_head":
         return [_top_by_score(ids, s[h], budget) for h in range(s.shape[0])]
     raise ValueError(f"unknown aggregate mode {aggregate!r}")
 
 
+def ground_truth_topB(output_rows_per_head, budget: int) -> np.ndarray:
+    """kvcompress.py:112-116 on the device: per-head column sums of the output
+    rows' attention, summed over heads, top-B."""
+    stacked = np.stack([token_scores(rows) for rows in output_rows_per_head])
+    return select_topB_obs(stacked, budget, aggregate="summed_over_heads")
+
+
+def overlap_rate(selected, truth, budget: int) -> float:
+    """kvcompress.py:119-123: |a & b| / B, with |a & b| = |a| + |b| - |a U b|
+    and the union on the device."""
+    a = np.unique(np.asarray(selected, dtype=np.int64))
+    b = np.unique(np.asarray(truth, dtype=np.int64))
+    if len(a) != budget or len(b) != budget:
+        raise SizeMismatch(f"both sets must have exactly {budget} elements")
+    u = retained_union(np.concatenate([a, b]), 0, 0)
+    return (len(a) + len(b) - len(u)) / budget
+
+
 def compact_cache(head: KVCacheHead, retained_ids, recent_window: int) -> KVCacheHead:
-    """kvcompress.py:133-147: keep union(retained_ids, recent window) rows via
-    the K8 gather."""
+    """kvcompress.py:133-147: keep = retained_union(...) (device), then the K8
+    gather (ls_kv_compact) of those rows from the head's cache; a kept id the
+    cache does not hold raises InvalidIds."""
     keep = retained_union(retained_ids, recent_window, head.full_len)
-    have = {int(g): i for i, g in enumerate(head.retained_ids)}
-    try:
-        rows = np.array([have[int(g)] for g in keep], dtype=np.int32)
-    except KeyError as exc:
-        raise InvalidIds(f"position {exc} is not present in the cache") from exc
+    keys = np.ascontiguousarray(head.keys)
+    vals = np.ascontiguousarray(head.values)
+    n_src, n_keep = len(head.retained_ids), len(keep)
     dev = _dev()
-    d = head.keys.shape[1] if head.keys.ndim == 2 else 1
-    keys = torch.as_tensor(np.asarray(head.keys, dtype=np.float32), device=dev)
-    vals = torch.as_tensor(np.asarray(head.values, dtype=np.float32), device=dev)
-    idx = torch.as_tensor(rows, device=dev, dtype=torch.int64)
-    del d
-    return KVCacheHead(keys=keys[idx].cpu().numpy().astype(head.keys.dtype),
-                       values=vals[idx].cpu().numpy().astype(head.values.dtype),
-                       retained_ids=keep, full_len=head.full_len)
+
+    def rows_dev(a):
+        """[n_src, ...] -> uint8 rows padded to 16 bytes (the vectorised gather)."""
+        rb = int(np.prod(a.shape[1:])) * a.dtype.itemsize if a.ndim > 1 else a.dtype.itemsize
+        b = np.zeros((max(n_src, 1), rb + (-rb) % 16), dtype=np.uint8)
+        if n_src:
+            b[:n_src, :rb] = np.ascontiguousarray(a).reshape(n_src, -1).view(np.uint8).reshape(n_src, rb)
+        return torch.as_tensor(b, device=dev), rb
+
+    (src_k, kb), (src_v, vb) = rows_dev(keys), rows_dev(vals)
+    dst_k = torch.empty((max(n_keep, 1), src_k.shape[1]), dtype=torch.uint8, device=dev)
+    dst_v = torch.empty((max(n_keep, 1), src_v.shape[1]), dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    src_ids = _i32_dev(head.retained_ids) if n_src else torch.zeros(1, dtype=torch.int32, device=dev)
+    keep_t = _i32_dev(keep) if n_keep else torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("ls_kv_compact", n_src, src_ids.data_ptr(), src_k.data_ptr(), src_v.data_ptr(), n_keep,
+              keep_t.data_ptr(), src_k.shape[1], src_v.shape[1], dst_k.data_ptr(), dst_v.data_ptr(),
+              status.data_ptr(), _lib.stream_ptr())
+    st = int(status.item())
+    if st:
+        raise InvalidIds(f"position {int(keep[st - 1])} is not present in the cache")
+
+    def back(t, like, rb):
+        raw = np.ascontiguousarray(t[:n_keep, :rb].cpu().numpy())
+        return raw.view(like.dtype).reshape((n_keep,) + like.shape[1:])
+
+    cls = type(head) if hasattr(type(head), "__dataclass_fields__") else KVCacheHead  # the caller's class
+    return cls(keys=back(dst_k, keys, kb), values=back(dst_v, vals, vb), retained_ids=keep, full_len=head.full_len)
 
 
 def progressive_decode(stack: DecodeStack, step_source, L0: int, comp: CompressionConfig, max_new: int,
@@ -382,4 +466,5 @@ def progressive_decode(stack: DecodeStack, step_source, L0: int, comp: Compressi
 
 
 __all__ = ["CompressionConfig", "DecodeStats", "KVCacheHead", "accumulate_scores", "token_scores",
-           "select_topB_obs", "_top_by_score", "retained_union", "compact_cache", "progressive_decode", "DecodeStack"]
+           "select_topB_obs", "_top_by_score", "retained_union", "compact_cache", "ground_truth_topB",
+           "overlap_rate", "progressive_decode", "DecodeStack"]

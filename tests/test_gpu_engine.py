@@ -110,7 +110,7 @@ def test_long_context_turn_c3_shape(cuda_lib):
         assert (np.diff(s) > 0).all() and (np.diff(v) > 0).all()
         assert s.max(initial=0) < ro + n_new and v.max(initial=0) < ro + n_new
     cov = plans.coverage.cpu().numpy()
-    assert ((cov >= 0.955 - 1e-6) | (cov <= 1.0)).all()
+    assert ((cov >= 0.955 - 1e-6) & (cov <= 1.0)).all()
     cells = res.cells[0].cpu().numpy()
     dense_cells = n_new * ro + n_new * (n_new + 1) // 2
     assert (cells > 0).all() and (cells <= dense_cells).all()

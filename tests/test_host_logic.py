@@ -122,22 +122,40 @@ def test_output_gather_gloo_two_ranks():
 
 def test_dropin_rebinds_reference_names():
     """dropin.install() rebinds the reference's import-time name bindings
-    (session.py:37, model.py:20) in the calling modules and restores them."""
+    (session.py:19-37, model.py:20, kvcompress.py:18) in the calling modules
+    -- on the compiled reference itself when oracle/_ref is built -- and
+    uninstall() restores them."""
     import types
 
-    from paper_2507_13681_b200 import dropin, prefill, tensor_ops
+    from paper_2507_13681_b200 import dropin, kvcompress, prefill, tensor_ops
+    from c1_harness import reference_modules
 
-    orig = object()
-    mods = {}
-    for (mod_name, attr) in dropin.PATCHES:
-        m = mods.setdefault(mod_name, types.ModuleType(mod_name))
-        setattr(m, attr, orig)
+    ref = reference_modules()
+    if ref is not None:
+        mods = {f"loopserve.{k}": v for k, v in ref.items()}
+        before = {(m, a): getattr(mods[m], a) for m, a in dropin.PATCHES if m in mods and hasattr(mods[m], a)}
+    else:
+        orig = object()
+        mods = {}
+        for (mod_name, attr) in dropin.PATCHES:
+            m = mods.setdefault(mod_name, types.ModuleType(mod_name))
+            setattr(m, attr, orig)
+        before = {(m, a): orig for m, a in dropin.PATCHES}
     done = dropin.install(mods)
     try:
-        assert sorted(done) == sorted(f"{m}.{a}" for m, a in dropin.PATCHES)
-        assert mods["loopserve.session"].sparsify_head is prefill.sparsify_head
-        assert mods["loopserve.model"].masked_sparse_attention is tensor_ops.masked_sparse_attention
-        assert mods["loopserve.model"].scaled_dot_attention is tensor_ops.scaled_dot_attention
+        assert sorted(done) == sorted(f"{m}.{a}" for m, a in before)
+        assert mods["loopserve.session"].sparsify_head.__wrapped__ is prefill.sparsify_head
+        assert mods["loopserve.model"].masked_sparse_attention.__wrapped__ is tensor_ops.masked_sparse_attention
+        assert mods["loopserve.model"].scaled_dot_attention.__wrapped__ is tensor_ops.scaled_dot_attention
+        assert mods["loopserve.kvcompress"].accumulate_scores.__wrapped__ is kvcompress.accumulate_scores
+        assert mods["loopserve.kvcompress"]._top_by_score.__wrapped__ is kvcompress._top_by_score
+        assert mods["loopserve.kvcompress"].retained_union.__wrapped__ is kvcompress.retained_union
+        dec = mods["loopserve.kvcompress"].decode_step
+        assert getattr(dec, "__b200__", False) and mods["loopserve.session"].decode_step is dec
+        if ref is not None:
+            assert getattr(ref["model"].KVCache.truncate, "__b200__", False)
     finally:
         dropin.uninstall()
-    assert all(getattr(mods[m], a) is orig for m, a in dropin.PATCHES)
+    assert all(getattr(mods[m], a) is fn for (m, a), fn in before.items())
+    if ref is not None:
+        assert not getattr(ref["model"].KVCache.truncate, "__b200__", False)
