@@ -286,8 +286,9 @@ def _accumulate_device(rows):
     touched = torch.empty(id_cap, dtype=torch.uint8, device=dev)
     ids_t = _i32_dev(flat_ids) if len(flat_ids) else torch.zeros(1, dtype=torch.int32, device=dev)
     w_t = _f64_dev(flat_w) if len(flat_w) else torch.zeros(1, dtype=torch.float64, device=dev)
-    _lib.call("ls_accumulate_scores", len(ids_l), torch.as_tensor(row_ptr, device=dev).data_ptr(), ids_t.data_ptr(),
-              w_t.data_ptr(), id_cap, acc.data_ptr(), touched.data_ptr(), _lib.stream_ptr())
+    ptr_t = torch.as_tensor(row_ptr, device=dev)  # kept alive until the kernel has read it
+    _lib.call("ls_accumulate_scores", len(ids_l), ptr_t.data_ptr(), ids_t.data_ptr(), w_t.data_ptr(), id_cap,
+              acc.data_ptr(), touched.data_ptr(), _lib.stream_ptr())
     return acc.cpu().numpy(), touched.cpu().numpy().astype(bool)
 
 
@@ -330,8 +331,9 @@ def _top_by_score(ids: np.ndarray, scores: np.ndarray, budget: int) -> np.ndarra
     out = torch.empty(b, dtype=torch.int32, device=dev)
     n_out = torch.empty(1, dtype=torch.int32, device=dev)
     ws = torch.empty(int(_lib.lib().ls_top_by_score_workspace(rng)), dtype=torch.uint8, device=dev)
-    _lib.call("ls_top_by_score", len(ids), _i32_dev(ids).data_ptr(), _f64_dev(scores).data_ptr(), b, lo, rng,
-              out.data_ptr(), n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    ids_t, sc_t = _i32_dev(ids), _f64_dev(scores)  # named: a temporary's memory could be reused before the kernel runs
+    _lib.call("ls_top_by_score", len(ids), ids_t.data_ptr(), sc_t.data_ptr(), b, lo, rng, out.data_ptr(),
+              n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
     if int(n_out.item()) != b:
         raise InvalidIds("_top_by_score: ids must be distinct")
     return out.cpu().numpy().astype(np.intp)

@@ -36,13 +36,10 @@ N_TURNS, INPUT_LEN, MAX_NEW = 3, 1000, 32
 def reference_modules():
     """Import the compiled reference (`loopserve.*`) or return None."""
     sys.path.insert(0, REPO)
-    from oracle.build_ref import import_path
+    from oracle.build_ref import install_import
 
-    root = import_path()
-    if root is None:
+    if not install_import():
         return None
-    if root not in sys.path:
-        sys.path.insert(0, root)
     names = ("errors", "opcount", "tensor_ops", "prefill", "model", "kvcompress", "session")
     return {n: importlib.import_module(f"loopserve.{n}") for n in names}
 

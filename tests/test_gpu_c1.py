@@ -125,8 +125,12 @@ def _compare(gold, got, captured, report):
             soft((ge["step"], ge["head"]) == (de["step"], de["head"]), f"turn {t}: event order differs")
             if ge["retained_ids"] == de["retained_ids"]:
                 rep["events_identical"] += 1
-                soft(abs(de["score_coverage"] - ge["score_coverage"]) <= 1e-9,
-                     f"turn {t} event {ge['step']} {ge['head']}: score_coverage")
+                # the first event's buffer holds prefill seed rows: the K5 plan-row
+                # probabilities (fp32 on the device vs the reference's fp64)
+                dc = abs(de["score_coverage"] - ge["score_coverage"])
+                rep["max_score_coverage_diff"] = max(rep.get("max_score_coverage_diff", 0.0), dc)
+                soft(dc <= 1e-6, f"turn {t} event {ge['step']} {ge['head']}: score_coverage "
+                                 f"{de['score_coverage']} vs {ge['score_coverage']}")
             else:
                 rep["event_diffs"].append({"step": ge["step"], "head": ge["head"],
                                            "sym_diff": len(set(ge["retained_ids"]) ^ set(de["retained_ids"]))})
