@@ -137,13 +137,15 @@ def decode_head_step(k_arch, v_arch, q, cols):
 
 
 def progressive_decode_attn(k_arch, v_arch, kv_of_head, L0: int, obs_seed, comp: CompressionConfig,
-                            max_new: int, q_steps, counter=None):
+                            max_new: int, q_steps, counter=None, score_log=None):
     """kvcompress.py:167-240 at attention-only shapes.
 
     k_arch, v_arch: [n_kv, L0 + max_new, d] fp64; rows >= L0 are the decode
     steps' appended K/V (step t appends row L0 + t before attending).
     kv_of_head: q-head -> kv-head map.  obs_seed: per q-head list of (ids, w).
     q_steps: [max_new, n_heads, d].  Returns (outs [max_new, n_heads, d], stats).
+    score_log: if a list, each event appends (n_o, head, candidate ids, scores)
+    (the parity tests classify a differing retained set as a top-B near-tie).
     """
     comp.validate()
     n_heads = len(kv_of_head)
@@ -164,6 +166,8 @@ def progressive_decode_attn(k_arch, v_arch, kv_of_head, L0: int, obs_seed, comp:
         if comp.budget is not None and n_o >= comp.warmup and (n_o - comp.warmup) % comp.interval == 0:
             for h in heads:
                 ids, scores = accumulate_scores(obs_buf[h])
+                if score_log is not None:
+                    score_log.append((n_o, h, ids, scores))
                 picked = top_by_score(ids, scores, comp.budget)
                 selected[h] = picked
                 working[h] = retained_union(picked, window, length)

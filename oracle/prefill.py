@@ -54,7 +54,8 @@ class Plan:
     approx_sum: float
     total_weight: float
     n_total: int
-    picks: tuple = field(default=(), compare=False)  # ((kind, index, gain_s, gain_v), ...)
+    # ((kind, index, gain_s, gain_v, approx, exact, target) after each pick, ...)
+    picks: tuple = field(default=(), compare=False)
 
     def cost(self, n_new: int, n_total: int | None = None) -> int:
         n = self.n_total if n_total is None else n_total
@@ -160,14 +161,14 @@ def greedy(slashes, verticals, alpha: float, total_weight: float, view: BlockVie
             ol_s += s.max_cell
             sel_s.append(s.index)
             s_idx += 1
-            picks.append(("slash", s.index, gain_s, gain_v))
+            picks.append(("slash", s.index, gain_s, gain_v, approx, exact, target))
         else:
             approx += v.weight - ol_s
             exact += v.weight - sum(view.cell(d, v.index) for d in sel_s)
             ol_v += v.max_cell
             sel_v.append(v.index)
             v_idx += 1
-            picks.append(("vertical", v.index, gain_s, gain_v))
+            picks.append(("vertical", v.index, gain_s, gain_v, approx, exact, target))
     coverage = exact / total_weight if total_weight > 0 else 0.0
     return Plan(frozenset(sel_s), frozenset(sel_v), min(coverage, 1.0), approx,
                 total_weight, view.n_total, tuple(picks))

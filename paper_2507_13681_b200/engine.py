@@ -113,8 +113,10 @@ class SessionEngine:
     groups of layer l finish before layer l + 1 starts."""
 
     def __init__(self, shape: AttnShape, params: SessionParams, cap: int, device="cuda",
-                 out_dtype=torch.bfloat16, head_groups: int | None = None):
+                 out_dtype=torch.bfloat16, head_groups: int | None = None, keep_plans: bool = True):
         params.validate()
+        # the session's plan ledger (turn, layer) -> LayerPlans (session.py:153-154)
+        self.plan_ledger = {} if keep_plans else None
         self.shape, self.params, self.cap = shape, params, cap
         self.device = device
         self.out_dtype = out_dtype
@@ -210,6 +212,8 @@ class SessionEngine:
                 layer_done(l, out, main)
             plans_all.append(plans)
             cells_all.append(cells)
+            if self.plan_ledger is not None:
+                self.plan_ledger[(turn, l)] = plans  # session.py:153-154 (device plans, head order)
             self.cell_log.append(cells)
             self.score_log.append(plans.score_count)
         if surv > 0 and p.mode != "dense":
@@ -309,12 +313,23 @@ class SessionEngine:
             self._graphs[key] = g
         return g
 
-    def decode(self, store: QKVStore, L0: int, max_new: int, use_graphs: bool = True, out_sink=None):
+    def decode(self, store: QKVStore, L0: int, max_new: int, use_graphs: bool = True, out_sink=None,
+               events: list | None = None):
         """max_new decode steps (kvcompress.py:200-239) from cache length L0,
         after prefill() set the counters. Returns the last step's outputs
-        [L, n_q, d]; out_sink(step, out_buf) is called after every step."""
+        [L, n_q, d]; out_sink(step, out_buf) is called after every step.
+        events: if a list, every compression event appends a device snapshot
+        (step n_o, cache length, selected ids, score coverage) -- no host sync;
+        event_log() turns them into the reference's event records and
+        decode_op_counts() into its decode op counts."""
         p, sh = self.params, self.shape
         st = self.stack
+        self._last_decode = (L0, max_new, events)
+
+        def snap(n_o):
+            if events is not None:
+                events.append({"step": n_o, "length": st.length, "sel": st.sel_ids.clone(),
+                               "n_sel": st.n_sel.clone(), "cov": st.score_cov.clone()})
         comp = p.comp if p.mode == "loopserve" else CompressionConfig(budget=None)
         if p.mode == "dense":
             st.set_step(L0, 0)
@@ -338,6 +353,7 @@ class SessionEngine:
             for n_o in range(1, max_new + 1):
                 if comp.event_at(n_o):
                     st.event(comp.budget, store.k, store.v, max_len=ev_len)
+                    snap(n_o)
                     compressed = True
                 self._step(store, q_buf, out_buf, compressed, comp_cols if compressed else dense_cols)
                 if out_sink is not None:
@@ -362,6 +378,7 @@ class SessionEngine:
             while n_o <= max_new:
                 if comp.event_at(n_o):
                     graphs["event"].replay()
+                    snap(n_o)
                     compressed = True
                 nxt = n_o + 1
                 while nxt <= max_new and not comp.event_at(nxt):
@@ -379,12 +396,74 @@ class SessionEngine:
         for n_o in range(1, max_new + 1):
             if comp.event_at(n_o):
                 graphs["event"].replay()
+                snap(n_o)
                 compressed = True
             graphs["comp" if compressed else "dense"].replay()
             st.length += 1
             st.appended += 1
             out_sink(n_o - 1, out_buf)
         return out_buf
+
+    # ------------------------------------------------------- session records
+    def event_log(self, events: list, head_offset: int = 0) -> list[dict]:
+        """kvcompress.py:217-224 records {step, head "L{l}H{h}", retained_ids,
+        score_coverage} from decode(events=...) snapshots: retained_ids =
+        retained_union(selected, window, length) (kvcompress.py:214)."""
+        import numpy as np
+
+        sh, W = self.shape, self.window
+        out = []
+        for ev in events:
+            sel, n_sel, cov = ev["sel"].cpu().numpy(), ev["n_sel"].cpu().numpy(), ev["cov"].cpu().numpy()
+            L = ev["length"]
+            recent = np.arange(max(0, L - W), L)
+            for l in range(sh.n_layers):
+                for h in range(sh.n_q):
+                    hr = l * sh.n_q + h
+                    keep = np.union1d(sel[hr, :n_sel[hr]], recent)
+                    out.append({"step": ev["step"], "head": f"L{l}H{h + head_offset}",
+                                "retained_ids": [int(g) for g in keep], "score_coverage": float(cov[hr])})
+        return out
+
+    def decode_op_counts(self, events: list) -> dict:
+        """decode_scores / decode_steps of session.py:186-191 for the last
+        decode(): every step scores |working| + 1 cells per (layer, head)
+        (model.py:236-237), working = all positions before the first event,
+        retained_union(selected, W, length) after it (kvcompress.py:234-237)."""
+        import numpy as np
+
+        L0, max_new, _ = self._last_decode
+        sh, W = self.shape, self.window
+        by_step = {ev["step"]: ev for ev in events}
+        cur = None
+        total = 0
+        for n_o in range(1, max_new + 1):
+            length = L0 + n_o - 1  # cache length when token n_o is appended
+            if n_o in by_step:
+                ev = by_step[n_o]
+                cur = (ev["sel"].cpu().numpy(), ev["n_sel"].cpu().numpy())
+            if cur is None:
+                total += sh.n_layers * sh.n_q * (length + 1)
+            else:
+                sel, n_sel = cur
+                lo = max(0, length - W)
+                for hr in range(sh.n_layers * sh.n_q):
+                    s = sel[hr, :n_sel[hr]]
+                    total += int(n_sel[hr]) + (length - lo) - int(np.count_nonzero(s >= lo)) + 1
+        return {"decode_scores": total, "decode_steps": max(0, max_new - 1)}
+
+    def prefill_op_counts(self, res: "PrefillOut") -> dict:
+        """prefill_scores / prefill_dense_cells of session.py:186-189: sampled
+        scoring cells (prefill.py:388-389) + sparse attention cells
+        (tensor_ops.py:172-174), all layers and heads."""
+        sh = self.shape
+        scores = 0
+        for l in range(sh.n_layers):
+            if res.cells[l] is not None:
+                scores += int(res.cells[l].sum().item()) + int(res.plans[l].score_count.sum().item())
+            else:
+                scores += sh.n_q * sum(min(res.n_total, res.n_total - res.n_new + r + 1) for r in range(res.n_new))
+        return {"prefill_scores": scores, "prefill_dense_cells": sh.n_layers * sh.n_q * res.n_new * res.n_total}
 
     def turn_blocks(self, input_len: int, n_turns: int, max_new: int):
         """(row_offset, n_new) of each turn: block = previous answer + input
