@@ -35,14 +35,24 @@ namespace k1tc {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int CHUNK = 1024;        // key columns per CTA
+constexpr int CHUNK = 1024;        // key columns per statistics / slash-accumulator chunk
 constexpr int LDP = BN + 4;        // fp32 P row stride (16-B rows: conflict-free STS.128 / column LDS)
 constexpr int ACC_CAP = 3072;      // shared slash accumulator (diagonals per chunk)
 constexpr int RP_CAP = 2048;       // row-pointer table: first sampled row at or after a position
 constexpr int LINES_THREADS = 512; // 16 warps: 4 per TMEM lane quadrant
+constexpr int STATS_THREADS = 256; // two threads per sampled row (column halves)
 constexpr double FIX = 1099511627776.0;  // 2^40
 constexpr double UNFIX = 1.0 / 1099511627776.0;
 
+// Work decomposition (both passes, persistent CTAs). A row tile ("item") is
+// (head h, row tile rt): the n_s sampled rows of a head are split into n_rt =
+// ceil(n_s / 128) tiles of near-equal size (rows [rt*n_s/n_rt, (rt+1)*n_s/n_rt)),
+// and item i = h*n_rt + rt covers key tiles [0, ceil(c_end_i / 128)), c_end_i =
+// the causal end of its last row. The items' key tiles form one flat list
+// (prefix table `tstart`, written by k1_tiles_kernel); CTA b of G processes the
+// contiguous slice [T*b/G, T*(b+1)/G), so every SM gets the same number of
+// 128 x 128 score tiles and a CTA's setup (TMEM, barriers, Q gather) is paid
+// once per slice, not once per 1024-key chunk.
 struct Params {
   const uint16_t *q;
   const uint16_t *k;
@@ -50,18 +60,97 @@ struct Params {
   int n_heads, group, n_s, n_total, row_offset, n_rt, n_chunks;
   int64_t q_head_stride, kv_head_stride;
   float scale_log2;
-  float2 *pstats;  // [H][n_rt][n_chunks][BM]
+  const int32_t *tstart;            // [H*n_rt + 1] prefix of key tiles per item
+  float2 *pstats;                   // [H][n_chunks][n_s][2 slots][2 halves] (max, sum) per row
   unsigned long long *vfix, *sfix;  // [H][n_total]
   unsigned int *vmaxb, *smaxb;      // [H][n_total]
   float *row_stats;                 // [H][n_s][2]
 };
+
+__device__ __forceinline__ int rt_begin(const Params &p, int rt) {
+  return static_cast<int>((static_cast<long long>(rt) * p.n_s) / p.n_rt);
+}
+
+// key tiles of every item and their exclusive prefix (one CTA)
+__global__ void __launch_bounds__(1024) k1_tiles_kernel(Params p, int32_t *tstart) {
+  __shared__ int sh[32];
+  const int n_items = p.n_heads * p.n_rt;
+  int base = 0;
+  for (int i0 = 0; i0 < n_items; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    int nt = 0;
+    if (i < n_items) {
+      const int h = i / p.n_rt, rt = i - h * p.n_rt;
+      const int r_last = rt_begin(p, rt + 1) - 1;
+      const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
+      const int c_end = min(p.n_total, g_last + 1);
+      nt = (c_end + BN - 1) / BN;
+    }
+    // block exclusive scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh[wid] = incl;
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      if (w < wid) before += sh[w];
+      all += sh[w];
+    }
+    if (i < n_items) tstart[i] = base + before + incl - nt;
+    base += all;
+  }
+  if (threadIdx.x == 0) tstart[n_items] = base;
+}
+
+// Position in the flat tile list: item i, tile j of the item (columns [j*BN, +BN)).
+struct TileCursor {
+  int x, i, j, i_end_tile;  // global tile, item, local tile, first global tile of item i + 1
+  __device__ void seek(const int32_t *tstart, int n_items, int x_) {
+    x = x_;
+    int lo = 0, hi = n_items - 1;  // last item with tstart <= x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tstart[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    i = lo;
+    while (tstart[i + 1] <= x) ++i;  // skip empty items
+    j = x - tstart[i];
+    i_end_tile = tstart[i + 1];
+  }
+  __device__ void next(const int32_t *tstart) {
+    ++x;
+    ++j;
+    while (x >= i_end_tile) {  // next non-empty item
+      ++i;
+      j = x - tstart[i];
+      i_end_tile = tstart[i + 1];
+    }
+  }
+};
+
+// this CTA's slice [x0, x1) of the flat tile list; slices hold >= CHUNK / BN
+// tiles (fewer CTAs work on small problems) so a chunk spans at most two
+__device__ __forceinline__ bool tile_slice(const Params &p, int &x0, int &x1) {
+  const int T = p.tstart[p.n_heads * p.n_rt];
+  const int G = min(static_cast<int>(gridDim.x), max(1, T / (CHUNK / BN)));
+  if (static_cast<int>(blockIdx.x) >= G) return false;
+  x0 = static_cast<int>((static_cast<long long>(T) * blockIdx.x) / G);
+  x1 = static_cast<int>((static_cast<long long>(T) * (blockIdx.x + 1)) / G);
+  return x0 < x1;
+}
 
 template <int D>
 struct StatsSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = BM * D * 2;
   static constexpr int OFF_MISC = OFF_K + 2 * BN * D * 2;
-  static constexpr int TOTAL = OFF_MISC + 1024 + 64 + 1024 + 1024;  // (+ TMA / s_empty barriers, halves' (m, l))
+  static constexpr int TOTAL = OFF_MISC + 1024 + 1024;  // barriers, TMEM address, row positions
 };
 
 template <int D>
@@ -84,44 +173,24 @@ __device__ __forceinline__ unsigned long long to_fix(double x) {
   return static_cast<unsigned long long>(__double2ll_rn(x * FIX));
 }
 
-// shared prologue: TMEM, barriers, row positions, gathered Q tile
+// gather the Q rows of item (h, rt) into the swizzled Q tile (cp.async, all
+// threads) and their positions into gs[]; returns the item's row count
 template <int D>
-__device__ __forceinline__ void setup(const Params &p, unsigned char *smem, int off_misc, int h, int rt, int &nr,
-                                      int *gs, uint64_t *mbar, uint32_t *tmem_sh) {
-  const int tid = threadIdx.x;
-  const int r_begin = rt * BM;
-  nr = min(BM, p.n_s - r_begin);
-  if ((tid >> 5) == 0) tc::tmem_alloc(tmem_sh, 256);
-  if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-  }
-  const int32_t *rows_h = p.rows + static_cast<int64_t>(h) * p.n_s;
-  if (tid < BM) {
-    const int lr = tid < nr ? rows_h[r_begin + tid] : 0;
-    gs[tid] = tid < nr ? p.row_offset + lr : 0x7fffffff;
-    const uint16_t *qrow = p.q + static_cast<int64_t>(h) * p.q_head_stride + static_cast<int64_t>(lr) * D;
-    const uint32_t qs = tc::smem_u32(smem);
-#pragma unroll
-    for (int ch = 0; ch < D / 8; ++ch) zfill16(qs + tc::sw128_offset(tid, ch, BM), qrow + ch * 8, tid < nr);
-  }
-  tc::cp_async_commit();
-  (void)off_misc;
-}
-
-template <int D>
-__device__ __forceinline__ void load_k(const Params &p, unsigned char *smem, int off_k, const uint16_t *kbase, int c0,
-                                       int buf) {
-  // 128 key rows; threads >= 128 help when blockDim is 256
-  const uint32_t ks = tc::smem_u32(smem + off_k + buf * BN * D * 2);
+__device__ __forceinline__ int load_item_q(const Params &p, unsigned char *smem, int *gs, int h, int rt) {
+  const int r0 = rt_begin(p, rt), nr = rt_begin(p, rt + 1) - r0;
+  const int32_t *rows_h = p.rows + static_cast<int64_t>(h) * p.n_s + r0;
   constexpr int CH = D / 8;
-  for (int i = threadIdx.x; i < BN * CH; i += blockDim.x) {
-    const int r = i / CH, ch = i % CH;
-    const int c = c0 + r;
-    const bool ok = c < p.n_total;
-    zfill16(ks + tc::sw128_offset(r, ch, BN), kbase + static_cast<int64_t>(ok ? c : 0) * D + ch * 8, ok);
+  const uint32_t qs = tc::smem_u32(smem);
+  for (int idx = threadIdx.x; idx < BM * CH; idx += blockDim.x) {
+    const int r = idx / CH, ch = idx - r * CH;
+    const bool ok = r < nr;
+    const int lr = ok ? rows_h[r] : 0;
+    if (ch == 0) gs[r] = ok ? p.row_offset + lr : 0x7fffffff;
+    const uint16_t *qrow = p.q + static_cast<int64_t>(h) * p.q_head_stride + static_cast<int64_t>(lr) * D;
+    zfill16(qs + tc::sw128_offset(r, ch, BM), qrow + ch * 8, ok);
   }
   tc::cp_async_commit();
+  return nr;
 }
 
 // K rows [c0, c0 + 128) of kv head `kv` by TMA (rows past n_total read as zero)
@@ -148,90 +217,102 @@ __device__ __forceinline__ void issue_s(unsigned char *smem, int off_k, uint32_t
   tc::mma_commit(&mbar[buf]);
 }
 
-__device__ __forceinline__ void cta_sync_tc() {
+// cp.async-written Q visible to the tensor core, every thread past the barrier
+__device__ __forceinline__ void q_ready_sync() {
+  tc::cp_async_wait<0>();
   tc::fence_proxy_async();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
 }
 
+// Shared pipeline of both passes over the CTA's tile slice [x0, x1):
+//   thread 0 keeps the TMA of K two tiles ahead (stage t & 1) and issues
+//   S(t + 1) = Q K(t+1)^T into TMEM buffer (t + 1) & 1 before the CTA works on
+//   S(t); a TMEM buffer is reused once every thread has read it (the caller's
+//   s_empty arrivals or barrier). At an item boundary S(t + 1) needs the next
+//   item's Q: it is issued by on_item_switch() after the gather.
+struct Pipe {
+  uint64_t *s_full;   // [2] MMA -> threads
+  uint64_t *k_full;   // [2] TMA -> MMA
+  uint64_t *s_empty;  // [2] threads -> MMA (stats pass)
+  uint32_t tmem;
+};
+
 // ------------------------------------------------------------- pass 1
 // 256 threads, two per sampled row (TMEM lane = row, warps 0-3 columns 0-63,
 // warps 4-7 columns 64-127), each with its own online (max, sum) over its
-// half of every tile, merged once at the end. K tiles arrive by TMA (thread
-// 0), S = Qs K^T double-buffered in TMEM: S(t+1) is issued before the threads
-// process S(t), and a buffer is reused once all threads have read it
-// (s_empty, count 256) -- no CTA barrier per tile.
-constexpr int STATS_THREADS = 256;
+// half of every tile of a 1024-key chunk, written per (chunk, row, half) --
+// the consumer merges them in a fixed order, so no CTA barrier per tile.
 template <int D>
-__global__ void __launch_bounds__(STATS_THREADS) k1_stats_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
+__global__ void __launch_bounds__(STATS_THREADS, 2) k1_stats_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = StatsSmem<D>;
-  unsigned char *smem =
-      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);          // s_full[2] (setup)
-  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
-  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC + 1024);   // [2] TMA
-  uint64_t *s_empty = full + 2;                                             // [2] count STATS_THREADS
-  float2 *half = reinterpret_cast<float2 *>(smem + L::OFF_MISC + 1024 + 64);  // [128] second half's (m, l)
-  const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
+  unsigned char *smem = tc::align1024(smem_dyn);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);  // s_full[2] k_full[2] s_empty[2]
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 64);
+  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 1024);
+  const int n_items = p.n_heads * p.n_rt;
+  int x0, x1;
+  if (!tile_slice(p, x0, x1)) return;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int row = tid & (BM - 1), hc = tid >> 7;  // column half
-  float2 *ps = p.pstats + ((static_cast<int64_t>(h) * p.n_rt + rt) * p.n_chunks + ck) * BM;
-  // chunk bounds against this row tile's causal extent
-  const int r_last = min(p.n_s, (rt + 1) * BM) - 1;
-  const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
-  const int c_begin = ck * CHUNK;
-  if (c_begin > g_last) {
-    if (tid < BM) ps[tid] = make_float2(-INFINITY, 0.f);
-    return;
-  }
-  const int c_end = min(c_begin + CHUNK, g_last + 1);
-  const int kv = h / p.group;
-  const int n_tiles = (c_end - c_begin + BN - 1) / BN;
+  Pipe pp{bars, bars + 2, bars + 4, 0};
+  TileCursor cur, pre;  // consumer and TMA producer
+  cur.seek(p.tstart, n_items, x0);
+  if (warp == 0) tc::tmem_alloc(tmem_sh, 256);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&full[b], 1);
-      tc::mbar_init(&s_empty[b], STATS_THREADS);
+      tc::mbar_init(&pp.s_full[b], 1);
+      tc::mbar_init(&pp.k_full[b], 1);
+      tc::mbar_init(&pp.s_empty[b], STATS_THREADS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tc::prefetch_tmap(&tm_k);
-    for (int t = 0; t < 2 && t < n_tiles; ++t) tma_k<D>(&tm_k, smem, L::OFF_K, t, &full[t], c_begin + t * BN, kv);
+    pre = cur;
+    for (int t = 0; t < 2 && x0 + t < x1; ++t) {
+      tma_k<D>(&tm_k, smem, L::OFF_K, t, &pp.k_full[t], pre.j * BN, (pre.i / p.n_rt) / p.group);
+      if (x0 + t + 1 < x1) pre.next(p.tstart);
+    }
   }
-  int nr;
-  setup<D>(p, smem, L::OFF_MISC, h, rt, nr, gs, mbar, tmem_sh);  // Q rows (cp.async), TMEM, s_full barriers
-  tc::cp_async_wait<0>();
-  cta_sync_tc();
-  const uint32_t tmem = *tmem_sh;
+  int h = cur.i / p.n_rt, rt = cur.i - h * p.n_rt;
+  int nr = load_item_q<D>(p, smem, gs, h, rt);
+  q_ready_sync();
+  pp.tmem = *tmem_sh;
   if (tid == 0) {
-    tc::mbar_wait(&full[0], 0);
-    issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
+    tc::mbar_wait(&pp.k_full[0], 0);
+    issue_s<D>(smem, L::OFF_K, pp.tmem, 0, pp.s_full);
   }
-  const int my_g = gs[row];
-  const bool row_ok = row < nr;
+  int my_g = gs[row], r0 = rt_begin(p, rt);
+  bool row_ok = row < nr;
+  int c_end = min(p.n_total, gs[nr - 1] + 1);
   const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
   float m = -INFINITY, l = 0.f;
-  for (int t = 0; t < n_tiles; ++t) {
-    const int buf = t & 1;
-    const int c0 = c_begin + t * BN;
-    if (tid == 0 && t + 1 < n_tiles) {  // S(t+1) behind S(t): its buffer was read by every thread at t-1
-      tc::mbar_wait(&full[buf ^ 1], ((t + 1) >> 1) & 1);
-      if (t >= 1) tc::mbar_wait(&s_empty[buf ^ 1], ((t - 1) >> 1) & 1);
+  int seg_slot = (cur.j * BN) % CHUNK != 0 ? 1 : 0;
+  for (int x = x0; x < x1; ++x) {
+    const int t = x - x0, buf = t & 1;
+    const int c0 = cur.j * BN;
+    const bool last_in_item = x + 1 >= cur.i_end_tile;
+    const bool more = x + 1 < x1;
+    if (tid == 0 && more && !last_in_item) {  // S(t+1): its TMEM buffer was read by every thread at t-1
+      tc::mbar_wait(&pp.k_full[buf ^ 1], ((t + 1) >> 1) & 1);
+      if (t >= 1) tc::mbar_wait(&pp.s_empty[buf ^ 1], ((t - 1) >> 1) & 1);
       tc::fence_after_sync();
-      issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+      issue_s<D>(smem, L::OFF_K, pp.tmem, buf ^ 1, pp.s_full);
     }
-    tc::mbar_wait(&mbar[buf], (t >> 1) & 1);
+    tc::mbar_wait(&pp.s_full[buf], (t >> 1) & 1);
     tc::fence_after_sync();
-    if (tid == 0 && t + 2 < n_tiles)  // S(t) is done with K stage `buf`
-      tma_k<D>(&tm_k, smem, L::OFF_K, buf, &full[buf], c0 + 2 * BN, kv);
+    if (tid == 0 && x + 2 < x1) {  // S(t) is done with K stage `buf`
+      tma_k<D>(&tm_k, smem, L::OFF_K, buf, &pp.k_full[buf], pre.j * BN, (pre.i / p.n_rt) / p.group);
+      if (x + 3 < x1) pre.next(p.tstart);
+    }
     const int lim = min(my_g, c_end - 1) - c0 - 64 * hc;  // last valid column of this thread's 64
     float sv[64];
-    tc::tmem_ld32(tmem + buf * 128 + lane_base + 64 * hc, sv);
-    tc::tmem_ld32(tmem + buf * 128 + lane_base + 64 * hc + 32, sv + 32);
+    tc::tmem_ld32(pp.tmem + buf * 128 + lane_base + 64 * hc, sv);
+    tc::tmem_ld32(pp.tmem + buf * 128 + lane_base + 64 * hc + 32, sv + 32);
     tc::tmem_wait_ld();
     tc::fence_before_sync();
-    tc::mbar_arrive(&s_empty[buf]);
+    tc::mbar_arrive(&pp.s_empty[buf]);
     if (row_ok && lim >= 63) {  // whole half-tile causal: no masking
       float t4[4] = {sv[0], sv[1], sv[2], sv[3]};
 #pragma unroll
@@ -261,21 +342,41 @@ __global__ void __launch_bounds__(STATS_THREADS) k1_stats_kernel(const __grid_co
       l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + acc;
       m = mn;
     }
-  }
-  // merge the two column halves of each row (half 0 + half 1, fixed order)
-  if (hc == 1) half[row] = make_float2(m, l);
-  __syncthreads();
-  if (hc == 0) {
-    const float2 o = half[row];
-    const float mn = fmaxf(m, o.x);
-    float lt = 0.f;
-    if (m != -INFINITY) lt += l * fast_exp2(m - mn);
-    if (o.x != -INFINITY) lt += o.y * fast_exp2(o.x - mn);
-    ps[row] = make_float2(row_ok ? mn : -INFINITY, row_ok ? lt : 0.f);
+    if (last_in_item || ((c0 + BN) % CHUNK) == 0 || !more) {  // segment of a chunk done
+      // slot 0: the segment starting at the chunk's first tile; slot 1: the one a
+      // CTA slice starts with in mid-chunk (slices hold >= CHUNK / BN tiles, so a
+      // chunk has at most these two)
+      if (row_ok) {
+        const int ck = c0 / CHUNK;
+        p.pstats[(((static_cast<int64_t>(h) * p.n_chunks + ck) * p.n_s + r0 + row) * 2 + seg_slot) * 2 + hc] =
+            make_float2(m, l);
+      }
+      m = -INFINITY;
+      l = 0.f;
+      seg_slot = 0;
+    }
+    if (more) {
+      cur.next(p.tstart);
+      if (last_in_item) {  // next item: S(t) is complete and nothing else is in flight
+        h = cur.i / p.n_rt;
+        rt = cur.i - h * p.n_rt;
+        __syncthreads();  // every thread is done with gs / the TMEM reads of this item
+        nr = load_item_q<D>(p, smem, gs, h, rt);
+        q_ready_sync();
+        my_g = gs[row];
+        r0 = rt_begin(p, rt);
+        row_ok = row < nr;
+        c_end = min(p.n_total, gs[nr - 1] + 1);
+        if (tid == 0) {
+          tc::mbar_wait(&pp.k_full[buf ^ 1], ((t + 1) >> 1) & 1);
+          issue_s<D>(smem, L::OFF_K, pp.tmem, buf ^ 1, pp.s_full);
+        }
+      }
+    }
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+  if (warp == 0) tc::tmem_dealloc(pp.tmem, 256);
 }
 
 // ------------------------------------------------------------- pass 2
@@ -285,111 +386,145 @@ __global__ void __launch_bounds__(STATS_THREADS) k1_stats_kernel(const __grid_co
 // row order); slash partials by thread-owns-diagonal, rows ascending, with
 // the first contributing row read from a position -> row table instead of a
 // binary search; per-tile slash sums (<= ~13 cells) in fp32, accumulated per
-// chunk in fp64 shared memory.
+// 1024-key chunk in fp64 shared memory and flushed at the chunk's end.
 template <int D>
 __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = LinesSmem<D>;
-  unsigned char *smem =
-      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);
-  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 16);
+  unsigned char *smem = tc::align1024(smem_dyn);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);  // s_full[2] k_full[2]
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 48);
   int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);              // [128]
   float *m_sh = reinterpret_cast<float *>(smem + L::OFF_MISC + 64 + 512);  // [128]
   float *li_sh = m_sh + BM;                                                 // [128]
   double *colp = reinterpret_cast<double *>(smem + L::OFF_MISC + 2048);         // [4][128]
   float *colm = reinterpret_cast<float *>(smem + L::OFF_MISC + 2048 + 4096);    // [4][128]
+  int *rbase = reinterpret_cast<int *>(smem + L::OFF_MISC + 2048 + 4096 + 2048);  // [128] r * LDP + g_r
   float *Pf = reinterpret_cast<float *>(smem + L::OFF_P);
   double *acc = reinterpret_cast<double *>(smem + L::OFF_ACC);
   float *accm = reinterpret_cast<float *>(smem + L::OFF_ACCM);
   int *rp = reinterpret_cast<int *>(smem + L::OFF_RP);
-  const int ck = blockIdx.x, rt = blockIdx.y, h = blockIdx.z;
+  const int n_items = p.n_heads * p.n_rt;
+  int x0, x1;
+  if (!tile_slice(p, x0, x1)) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r_last = min(p.n_s, (rt + 1) * BM) - 1;
-  const int g_last = p.row_offset + p.rows[static_cast<int64_t>(h) * p.n_s + r_last];
-  const int c_begin = ck * CHUNK;
-  if (c_begin > g_last) return;
-  const int c_end = min(c_begin + CHUNK, g_last + 1);
-  int nr;
-  setup<D>(p, smem, L::OFF_MISC, h, rt, nr, gs, mbar, tmem_sh);
-  const uint16_t *kbase = p.k + static_cast<int64_t>(h / p.group) * p.kv_head_stride;
-  // combine the chunk statistics of this CTA's rows (chunk order: deterministic)
-  if (tid < BM) {
-    float m = -INFINITY, l = 0.f;
-    const float2 *ps = p.pstats + (static_cast<int64_t>(h) * p.n_rt + rt) * p.n_chunks * BM + tid;
-    for (int c = 0; c < p.n_chunks; ++c) {
-      const float2 v = ps[static_cast<int64_t>(c) * BM];
-      if (v.x == -INFINITY) continue;
-      const float mn = fmaxf(m, v.x);
-      l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
-      m = mn;
-    }
-    m_sh[tid] = m;
-    li_sh[tid] = l > 0.f ? 1.f / l : 0.f;
-    if (ck == 0 && tid < nr) {
-      float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + rt * BM + tid) * 2;
-      rs[0] = m;
-      rs[1] = l > 0.f ? 1.f / l : 0.f;
-    }
-  }
-  const int n_tiles = (c_end - c_begin + BN - 1) / BN;
-  uint64_t *kfull = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC + 32);  // [2] TMA K stages
-  const int kvh = h / p.group;
+  Pipe pp{bars, bars + 2, nullptr, 0};
+  TileCursor cur, pre;
+  cur.seek(p.tstart, n_items, x0);
+  if (warp == 0) tc::tmem_alloc(tmem_sh, 256);
   if (tid == 0) {
-    tc::mbar_init(&kfull[0], 1);
-    tc::mbar_init(&kfull[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&pp.s_full[b], 1);
+      tc::mbar_init(&pp.k_full[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tc::prefetch_tmap(&tm_k);
-    tma_k<D>(&tm_k, smem, L::OFF_K, 0, &kfull[0], c_begin, kvh);
+    pre = cur;  // K(t+1) is loaded one tile ahead, at the top of tile t
+    tma_k<D>(&tm_k, smem, L::OFF_K, 0, &pp.k_full[0], pre.j * BN, (pre.i / p.n_rt) / p.group);
+    if (x0 + 1 < x1) pre.next(p.tstart);
   }
-  (void)kbase;
-  tc::cp_async_wait<0>();
-  cta_sync_tc();
-  const uint32_t tmem = *tmem_sh;
-  if (tid == 0) {
-    tc::mbar_wait(&kfull[0], 0);
-    issue_s<D>(smem, L::OFF_K, tmem, 0, mbar);
-  }
-  const int g_first = gs[0];
-  const int g_hi = gs[nr - 1];
-  // position -> first sampled row at or after it, for positions [g_first, g_hi]
-  const int rp_span = g_hi - g_first + 1;
-  const bool use_rp = rp_span <= RP_CAP;
-  if (use_rp)
-    for (int x = tid; x < rp_span; x += LINES_THREADS) rp[x] = lower_bound_dev(gs, nr, g_first + x);
-  // slash accumulator window of the chunk: d in [d_base, d_base + width)
-  const int d_base = max(0, g_first - (c_end - 1));
-  const int width = g_hi - c_begin - d_base + 1;
-  const bool smem_acc = width <= ACC_CAP;
-  if (smem_acc)
-    for (int i = tid; i < width; i += LINES_THREADS) {
-      acc[i] = 0.0;
-      accm[i] = 0.f;
-    }
-  __syncthreads();
   // TMEM reads: warp w -> lanes 32*(w%4), columns [32*(w/4), +32)
   const int row = (warp & 3) * 32 + lane;
   const int cblk = (warp >> 2) * 32;
   const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-  const int my_g = gs[row];
-  const bool row_ok = row < nr;
-  // P = exp2(s * scale - m) / l = exp2(s * scale - (m + log2 l))
-  const float mr = li_sh[row] > 0.f ? m_sh[row] - __log2f(li_sh[row]) : INFINITY;
-  uint32_t ph0 = 0, ph1 = 0;
-  unsigned long long *sfix = p.sfix + static_cast<int64_t>(h) * p.n_total;
-  unsigned int *smaxb = p.smaxb + static_cast<int64_t>(h) * p.n_total;
-  for (int t = 0; t < n_tiles; ++t) {
-    const int buf = t & 1;
-    const int c0 = c_begin + t * BN;
-    if (t + 1 < n_tiles && tid == 0)  // stage buf^1 held K(t-1), consumed by S(t-1)
-      tma_k<D>(&tm_k, smem, L::OFF_K, buf ^ 1, &kfull[buf ^ 1], c0 + BN, kvh);
-    tc::mbar_wait(&mbar[buf], buf ? ph1 : ph0);
-    if (buf) ph1 ^= 1; else ph0 ^= 1;
+  unsigned long long *sfix = nullptr;
+  unsigned int *smaxb = nullptr;
+  int h = 0, rt = 0, nr = 0, my_g = 0, g_first = 0, g_hi = 0, c_end = 0, r0 = 0;
+  float mr = INFINITY;
+  bool row_ok = false, use_rp = false;
+  int d_base = 0, width = 0;
+  bool smem_acc = false;
+  bool first = true;
+  // per item: Q gather, the item rows' statistics (all chunks, fixed order),
+  // position -> row table; then S of the item's first tile
+  auto begin_item = [&](int t) {
+    h = cur.i / p.n_rt;
+    rt = cur.i - h * p.n_rt;
+    nr = load_item_q<D>(p, smem, gs, h, rt);
+    r0 = rt_begin(p, rt);
+    tc::cp_async_wait<0>();
+    __syncthreads();  // gs visible
+    if (tid < BM) {
+      float m = -INFINITY, l = 0.f;
+      if (tid < nr) {
+        const int n_ck = min(gs[tid], p.n_total - 1) / CHUNK + 1;  // chunks of this row's causal range
+        const float2 *ps = p.pstats + (static_cast<int64_t>(h) * p.n_chunks * p.n_s + r0 + tid) * 4;
+        for (int c = 0; c < n_ck; ++c) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {  // (slot, half) in a fixed order
+            const float2 v = ps[static_cast<int64_t>(c) * p.n_s * 4 + e];
+            if (v.y == 0.f) continue;  // empty (zeroed) or no causal column
+            const float mn = fmaxf(m, v.x);
+            l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
+            m = mn;
+          }
+        }
+        if (cur.j == 0) {  // the CTA holding the item's first tile publishes the row statistics
+          float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + r0 + tid) * 2;
+          rs[0] = m;
+          rs[1] = l > 0.f ? 1.f / l : 0.f;
+        }
+      }
+      m_sh[tid] = m;
+      li_sh[tid] = l > 0.f ? 1.f / l : 0.f;
+    }
+    if (tid < BM) rbase[tid] = tid * LDP + gs[tid];
+    g_first = gs[0];
+    g_hi = gs[nr - 1];
+    c_end = min(p.n_total, g_hi + 1);
+    const int rp_span = g_hi - g_first + 1;
+    use_rp = rp_span <= RP_CAP;
+    if (use_rp)
+      for (int xx = tid; xx < rp_span; xx += LINES_THREADS) rp[xx] = lower_bound_dev(gs, nr, g_first + xx);
+    sfix = p.sfix + static_cast<int64_t>(h) * p.n_total;
+    smaxb = p.smaxb + static_cast<int64_t>(h) * p.n_total;
+    q_ready_sync();
+    my_g = gs[row];
+    row_ok = row < nr;
+    mr = li_sh[row] > 0.f ? m_sh[row] - __log2f(li_sh[row]) : INFINITY;
+    if (tid == 0) {
+      tc::mbar_wait(&pp.k_full[t & 1], (t >> 1) & 1);
+      issue_s<D>(smem, L::OFF_K, pp.tmem, t & 1, pp.s_full);
+    }
+  };
+  // slash accumulator window of the chunk holding column c0: d in [d_base, d_base + width)
+  auto begin_chunk = [&](int c0) {
+    const int cb = (c0 / CHUNK) * CHUNK;
+    const int ce = min(cb + CHUNK, c_end);
+    d_base = max(0, g_first - (ce - 1));
+    width = g_hi - cb - d_base + 1;
+    smem_acc = width <= ACC_CAP;
+    if (smem_acc)
+      for (int i = tid; i < width; i += LINES_THREADS) {
+        acc[i] = 0.0;
+        accm[i] = 0.f;
+      }
+    // (ordered before the slash phase by the tile's first barrier)
+  };
+  __syncthreads();  // barrier init / TMEM address
+  pp.tmem = *tmem_sh;
+  for (int x = x0; x < x1; ++x) {
+    const int t = x - x0, buf = t & 1;
+    const int c0 = cur.j * BN;
+    const bool last_in_item = x + 1 >= cur.i_end_tile;
+    const bool more = x + 1 < x1;
+    if (first) {
+      begin_item(t);
+      begin_chunk(c0);
+      first = false;
+    } else if (c0 % CHUNK == 0) {
+      begin_chunk(c0);
+    }
+    if (more && tid == 0) {  // stage buf^1 held K(t-1), consumed by S(t-1)
+      tma_k<D>(&tm_k, smem, L::OFF_K, buf ^ 1, &pp.k_full[buf ^ 1], pre.j * BN, (pre.i / p.n_rt) / p.group);
+      if (x + 2 < x1) pre.next(p.tstart);
+    }
+    tc::mbar_wait(&pp.s_full[buf], (t >> 1) & 1);
     tc::fence_after_sync();
     {
       const int lim = min(my_g, c_end - 1) - c0 - cblk;  // last valid column of this thread's 32
       float sv[32];
-      tc::tmem_ld32(tmem + buf * 128 + lane_base + cblk, sv);
+      tc::tmem_ld32(pp.tmem + buf * 128 + lane_base + cblk, sv);
       tc::tmem_wait_ld();
       float4 *prow = reinterpret_cast<float4 *>(Pf + row * LDP + cblk);
       if (row_ok && lim >= 31) {
@@ -413,23 +548,25 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    if (t + 1 < n_tiles && tid == 0) {
-      tc::mbar_wait(&kfull[buf ^ 1], ((t + 1) >> 1) & 1);
-      issue_s<D>(smem, L::OFF_K, tmem, buf ^ 1, mbar);
+    if (more && !last_in_item && tid == 0) {
+      tc::mbar_wait(&pp.k_full[buf ^ 1], ((t + 1) >> 1) & 1);
+      issue_s<D>(smem, L::OFF_K, pp.tmem, buf ^ 1, pp.s_full);
     }
-    // vertical partials: four threads per column (32-row quarters)
+    // vertical partials: four threads per column (32-row quarters; rows past
+    // nr hold zeros): four fp32 partials of 8 rows each, combined in fp64
     {
       const int j = tid & (BN - 1), qq = tid >> 7;
-      double sw = 0.0;
-      float mx = 0.f;
-      const int r0 = qq * 32, r1 = min(nr, r0 + 32);
-      for (int r = r0; r < r1; ++r) {
-        const float v = Pf[r * LDP + j];
-        sw += static_cast<double>(v);
-        mx = fmaxf(mx, v);
+      const float *pc = Pf + qq * 32 * LDP + j;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f}, m4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const float v = pc[r * LDP];
+        s4[r & 3] += v;
+        m4[r & 3] = fmaxf(m4[r & 3], v);
       }
-      colp[qq * BN + j] = sw;
-      colm[qq * BN + j] = mx;
+      colp[qq * BN + j] = (static_cast<double>(s4[0]) + static_cast<double>(s4[1])) +
+                          (static_cast<double>(s4[2]) + static_cast<double>(s4[3]));
+      colm[qq * BN + j] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     }
     // slash partials: thread owns diagonal d, rows ascending
     {
@@ -446,10 +583,10 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
           r_end = lower_bound_dev(gs, nr, ghi + 1);
         }
         float sw = 0.f, mx = 0.f;
-        const float *pcol = Pf - dd - c0;
+        const float *pcol = Pf - dd - c0;  // cell (r, g_r - dd) at pcol[rb[r]]
 #pragma unroll 4
         for (; r < r_end; ++r) {
-          const float v = pcol[r * LDP + gs[r]];
+          const float v = pcol[rbase[r]];
           sw += v;
           mx = fmaxf(mx, v);
         }
@@ -472,17 +609,29 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
         if (mx > 0.f) atomicMax(p.vmaxb + static_cast<int64_t>(h) * p.n_total + c, __float_as_uint(mx));
       }
     }
-    // (no barrier here: every read of Pf precedes the barrier above, and the next
+    if (last_in_item || ((c0 + BN) % CHUNK) == 0 || !more) {  // chunk (or slice) done: flush the slash accumulator
+      if (smem_acc)
+        for (int i = tid; i < width; i += LINES_THREADS) {
+          if (acc[i] > 0.0) atomicAdd(sfix + d_base + i, to_fix(acc[i]));
+          if (accm[i] > 0.f) atomicMax(smaxb + d_base + i, __float_as_uint(accm[i]));
+        }
+    }
+    if (more) {
+      cur.next(p.tstart);
+      if (last_in_item) {
+        __syncthreads();  // flush / colp reads done before the next item rewrites smem
+        begin_item(t + 1);
+        begin_chunk(cur.j * BN);
+      } else if (((c0 + BN) % CHUNK) == 0) {
+        __syncthreads();  // flush reads done before the next chunk zeroes the accumulator
+      }
+    }
+    // (no barrier otherwise: every read of Pf precedes the barrier above, and the next
     // tile writes colp / the slash accumulator only after its own first barrier)
   }
-  if (smem_acc)
-    for (int i = tid; i < width; i += LINES_THREADS) {
-      if (acc[i] > 0.0) atomicAdd(sfix + d_base + i, to_fix(acc[i]));
-      if (accm[i] > 0.f) atomicMax(smaxb + d_base + i, __float_as_uint(accm[i]));
-    }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+  if (warp == 0) tc::tmem_dealloc(pp.tmem, 256);
 }
 
 // fixed point -> fp64 line weights; total = exact integer sum of the verticals.
@@ -554,19 +703,34 @@ __global__ void __launch_bounds__(FIN_THREADS) k1_finish_kernel(const unsigned l
 
 // per sampled row: merge the chunk statistics in chunk order (as k1_lines does)
 // into log2-sum-exp2 = m + log2(l) over all causal columns (ls_plan_coverage)
-__global__ void row_lse_kernel(const float2 *pstats, int n_s, int n_rt, int n_chunks, float *lse) {
+__global__ void row_lse_kernel(const float2 *pstats, const int32_t *rows, int n_s, int n_chunks, int row_offset,
+                               int n_total, float *lse) {
   const int h = blockIdx.y, r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_s) return;
-  const float2 *ps = pstats + (static_cast<int64_t>(h) * n_rt + r / BM) * n_chunks * BM + (r % BM);
+  const int g = row_offset + rows[static_cast<int64_t>(h) * n_s + r];
+  const int n_ck = min(g, n_total - 1) / CHUNK + 1;
+  const float2 *ps = pstats + (static_cast<int64_t>(h) * n_chunks * n_s + r) * 4;
   float m = -INFINITY, l = 0.f;
-  for (int c = 0; c < n_chunks; ++c) {
-    const float2 v = ps[static_cast<int64_t>(c) * BM];
-    if (v.x == -INFINITY) continue;
-    const float mn = fmaxf(m, v.x);
-    l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
-    m = mn;
-  }
+  for (int c = 0; c < n_ck; ++c)
+    for (int e = 0; e < 4; ++e) {
+      const float2 v = ps[static_cast<int64_t>(c) * n_s * 4 + e];
+      if (v.y == 0.f) continue;
+      const float mn = fmaxf(m, v.x);
+      l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
+      m = mn;
+    }
   lse[static_cast<int64_t>(h) * n_s + r] = l > 0.f ? m + __log2f(l) : -INFINITY;
+}
+
+inline int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 }  // namespace k1tc
@@ -575,14 +739,16 @@ size_t score_lines_tc_workspace(const ls_layer_desc *L, int32_t n_s) {
   const size_t n_rt = (n_s + k1tc::BM - 1) / k1tc::BM;
   const size_t n_ch = (L->n_total + k1tc::CHUNK - 1) / k1tc::CHUNK;
   const size_t H = L->n_heads;
-  return H * n_rt * n_ch * k1tc::BM * sizeof(float2) + H * L->n_total * (8 + 8 + 4 + 4) + H * 24 + 8 * 256 + 4096;
+  return H * n_ch * n_s * 4 * sizeof(float2) + H * L->n_total * (8 + 8 + 4 + 4) + H * 24 + (H * n_rt + 1) * 4 +
+         10 * 256 + 4096;
 }
 
-int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
-                   double *v_w, float *v_max, double *s_w, float *s_max, float *row_stats, double *total,
-                   int64_t *score_count, void *ws, size_t ws_bytes, cudaStream_t st) {
+namespace {
+int k1_prepare(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
+               float *row_stats, void *ws, size_t ws_bytes, k1tc::Params &p, unsigned long long **fin,
+               unsigned int **tick, bool accumulators, cudaStream_t st) {
   LS_REQUIRE(ws_bytes >= score_lines_tc_workspace(L, n_s), LS_ERR_WORKSPACE, "score_lines workspace too small");
-  k1tc::Params p;
+  p = k1tc::Params{};
   p.q = q;
   p.k = k;
   p.rows = rows;
@@ -599,43 +765,67 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
   p.row_stats = row_stats;
   Carver c(ws, ws_bytes);
   const size_t H = L->n_heads;
-  p.pstats = c.take<float2>(H * p.n_rt * p.n_chunks * k1tc::BM);
-  p.vfix = c.take<unsigned long long>(H * L->n_total);
-  p.sfix = c.take<unsigned long long>(H * L->n_total);
-  p.vmaxb = c.take<unsigned int>(H * L->n_total);
-  p.smaxb = c.take<unsigned int>(H * L->n_total);
-  unsigned long long *fin_tot = c.take<unsigned long long>(H);
-  unsigned long long *fin_cnt = c.take<unsigned long long>(H);
-  unsigned int *fin_tick = c.take<unsigned int>(H);
-  // line accumulators and finish counters are consecutive in the workspace (shared
-  // with other entries, so zeroed per call): one memset
-  LS_CUDA(cudaMemsetAsync(p.vfix, 0, reinterpret_cast<char *>(fin_tick + H) - reinterpret_cast<char *>(p.vfix), st));
-  dim3 grid(p.n_chunks, p.n_rt, L->n_heads);
-  CUtensorMap tmk;
-  int st_map = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride);
-  if (st_map) return st_map;
-  if (L->head_dim == 128) {
-    const int s1 = k1tc::StatsSmem<128>::TOTAL, s2 = k1tc::LinesSmem<128>::TOTAL;
-    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
-    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    k1tc::k1_stats_kernel<128><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
-    LS_LAUNCH_CHECK("k1_stats_kernel");
-    k1tc::k1_lines_kernel<128><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
-  } else {
-    const int s1 = k1tc::StatsSmem<64>::TOTAL, s2 = k1tc::LinesSmem<64>::TOTAL;
-    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
-    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    k1tc::k1_stats_kernel<64><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
-    LS_LAUNCH_CHECK("k1_stats_kernel");
-    k1tc::k1_lines_kernel<64><<<grid, k1tc::LINES_THREADS, s2, st>>>(tmk, p);
+  p.pstats = c.take<float2>(H * p.n_chunks * n_s * 4);
+  // every (chunk, row) has 2 segment slots x 2 column halves; unwritten ones stay (0, 0)
+  LS_CUDA(cudaMemsetAsync(p.pstats, 0, H * p.n_chunks * n_s * 4 * sizeof(float2), st));
+  int32_t *tstart = c.take<int32_t>(H * p.n_rt + 1);
+  p.tstart = tstart;
+  if (accumulators) {
+    p.vfix = c.take<unsigned long long>(H * L->n_total);
+    p.sfix = c.take<unsigned long long>(H * L->n_total);
+    p.vmaxb = c.take<unsigned int>(H * L->n_total);
+    p.smaxb = c.take<unsigned int>(H * L->n_total);
+    fin[0] = c.take<unsigned long long>(H);
+    fin[1] = c.take<unsigned long long>(H);
+    *tick = c.take<unsigned int>(H);
+    // line accumulators and finish counters are consecutive in the workspace (shared
+    // with other entries, so zeroed per call): one memset
+    LS_CUDA(cudaMemsetAsync(p.vfix, 0, reinterpret_cast<char *>(*tick + H) - reinterpret_cast<char *>(p.vfix), st));
   }
+  k1tc::k1_tiles_kernel<<<1, 1024, 0, st>>>(p, tstart);
+  LS_LAUNCH_CHECK("k1_tiles_kernel");
+  return LS_OK;
+}
+
+template <int D>
+int k1_stats_launch(const CUtensorMap &tmk, const k1tc::Params &p, cudaStream_t st) {
+  const int s1 = k1tc::StatsSmem<D>::TOTAL + 1024;
+  LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+  k1tc::k1_stats_kernel<D><<<2 * k1tc::sm_count(), k1tc::STATS_THREADS, s1, st>>>(tmk, p);
+  LS_LAUNCH_CHECK("k1_stats_kernel");
+  return LS_OK;
+}
+
+template <int D>
+int k1_lines_launch(const CUtensorMap &tmk, const k1tc::Params &p, cudaStream_t st) {
+  const int s2 = k1tc::LinesSmem<D>::TOTAL + 1024;
+  LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+  k1tc::k1_lines_kernel<D><<<k1tc::sm_count(), k1tc::LINES_THREADS, s2, st>>>(tmk, p);
   LS_LAUNCH_CHECK("k1_lines_kernel");
-  {
-    const dim3 fg((L->n_total + k1tc::FIN_CHUNK - 1) / k1tc::FIN_CHUNK, L->n_heads);
-    k1tc::k1_finish_kernel<<<fg, k1tc::FIN_THREADS, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
-                                                           L->row_offset, v_w, v_max, s_w, s_max, total, score_count,
-                                                           fin_tot, fin_cnt, fin_tick);
+  return LS_OK;
+}
+}  // namespace
+
+int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
+                   double *v_w, float *v_max, double *s_w, float *s_max, float *row_stats, double *total,
+                   int64_t *score_count, void *ws, size_t ws_bytes, cudaStream_t st) {
+  k1tc::Params p;
+  unsigned long long *fin[2];
+  unsigned int *tick = nullptr;
+  int s = k1_prepare(L, n_s, q, k, rows, row_stats, ws, ws_bytes, p, fin, &tick, true, st);
+  if (s) return s;
+  CUtensorMap tmk;
+  if ((s = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride)))
+    return s;
+  if (L->head_dim == 128) {
+    if ((s = k1_stats_launch<128>(tmk, p, st)) || (s = k1_lines_launch<128>(tmk, p, st))) return s;
+  } else {
+    if ((s = k1_stats_launch<64>(tmk, p, st)) || (s = k1_lines_launch<64>(tmk, p, st))) return s;
   }
+  const dim3 fg((L->n_total + k1tc::FIN_CHUNK - 1) / k1tc::FIN_CHUNK, L->n_heads);
+  k1tc::k1_finish_kernel<<<fg, k1tc::FIN_THREADS, 0, st>>>(p.vfix, p.vmaxb, p.sfix, p.smaxb, rows, n_s, L->n_total,
+                                                         L->row_offset, v_w, v_max, s_w, s_max, total, score_count,
+                                                         fin[0], fin[1], tick);
   LS_LAUNCH_CHECK("k1_finish_kernel");
   return LS_OK;
 }
@@ -644,38 +834,17 @@ int score_lines_tc(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const
 // causal columns (the dense softmax normaliser), [H][n_s]
 int score_row_lse(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uint16_t *k, const int32_t *rows,
                   float *lse, void *ws, size_t ws_bytes, cudaStream_t st) {
-  LS_REQUIRE(ws_bytes >= score_lines_tc_workspace(L, n_s), LS_ERR_WORKSPACE, "row_lse workspace too small");
-  k1tc::Params p{};
-  p.q = q;
-  p.k = k;
-  p.rows = rows;
-  p.n_heads = L->n_heads;
-  p.group = L->n_heads / L->n_kv_heads;
-  p.n_s = n_s;
-  p.n_total = L->n_total;
-  p.row_offset = L->row_offset;
-  p.n_rt = (n_s + k1tc::BM - 1) / k1tc::BM;
-  p.n_chunks = (L->n_total + k1tc::CHUNK - 1) / k1tc::CHUNK;
-  p.q_head_stride = L->q_head_stride;
-  p.kv_head_stride = L->kv_head_stride;
-  p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
-  Carver c(ws, ws_bytes);
-  p.pstats = c.take<float2>(static_cast<size_t>(L->n_heads) * p.n_rt * p.n_chunks * k1tc::BM);
-  dim3 grid(p.n_chunks, p.n_rt, L->n_heads);
+  k1tc::Params p;
+  unsigned long long *fin[2];
+  unsigned int *tick = nullptr;
+  int s = k1_prepare(L, n_s, q, k, rows, nullptr, ws, ws_bytes, p, fin, &tick, false, st);
+  if (s) return s;
   CUtensorMap tmk;
-  int st_map = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride);
-  if (st_map) return st_map;
-  if (L->head_dim == 128) {
-    const int s1 = k1tc::StatsSmem<128>::TOTAL;
-    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
-    k1tc::k1_stats_kernel<128><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
-  } else {
-    const int s1 = k1tc::StatsSmem<64>::TOTAL;
-    LS_CUDA(cudaFuncSetAttribute(k1tc::k1_stats_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
-    k1tc::k1_stats_kernel<64><<<grid, k1tc::STATS_THREADS, s1, st>>>(tmk, p);
-  }
-  LS_LAUNCH_CHECK("k1_stats_kernel");
-  k1tc::row_lse_kernel<<<dim3((n_s + 255) / 256, L->n_heads), 256, 0, st>>>(p.pstats, n_s, p.n_rt, p.n_chunks, lse);
+  if ((s = make_tmap_bf16_3d(&tmk, k, L->head_dim, L->n_total, L->n_kv_heads, L->head_dim, L->kv_head_stride)))
+    return s;
+  if ((s = L->head_dim == 128 ? k1_stats_launch<128>(tmk, p, st) : k1_stats_launch<64>(tmk, p, st))) return s;
+  k1tc::row_lse_kernel<<<dim3((n_s + 255) / 256, L->n_heads), 256, 0, st>>>(p.pstats, rows, n_s, p.n_chunks,
+                                                                           L->row_offset, L->n_total, lse);
   LS_LAUNCH_CHECK("row_lse_kernel");
   return LS_OK;
 }
