@@ -89,6 +89,24 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA / integer pipes (no MUFU): x = n + f, n = round(x) by the
+// 1.5 * 2^23 magic add, f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial
+// (max relative error 7.6e-5, far below the bf16 rounding of the P operand it
+// feeds); 2^n added to the exponent bits. x < -126 (incl. -inf) gives 0.
+// Used for part of the softmax exponentials so the MUFU pipe is not the only
+// exp2 unit (the FA4 split).
+__device__ __forceinline__ float poly_exp2(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float j = __fadd_rn(xc, 12582912.f);
+  const float n = __fsub_rn(j, 12582912.f);
+  const float f = xc - n;
+  float p = fmaf(f, 0.05517053f, 0.24260831f);
+  p = fmaf(p, f, 0.69326092f);
+  p = fmaf(p, f, 0.99992825f);
+  const int bits = __float_as_int(p) + (__float_as_int(j) << 23);
+  return x < -126.f ? 0.f : __int_as_float(bits);
+}
+
 // first index i in [0, n) with a[i] >= x (a sorted ascending)
 template <typename T>
 __device__ __forceinline__ int lower_bound_dev(const T *a, int n, T x) {
