@@ -315,19 +315,34 @@ def main():
 
     gather = shard.make_gather(cfg["d"]) if world > 1 else None
 
+    side = torch.cuda.Stream() if gather is not None else None
+    gathered = []
+
+    def layer_done(l, out, s):
+        # head-sharded prefill: layer l's output all-gather (the head concat
+        # before W_O) runs on a side stream while layer l + 1 computes
+        ev = torch.cuda.Event()
+        ev.record(s)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            gathered.append(gather.prefill(out))
+            out.record_stream(side)
+
     def dialogue(ev_log):
         for t, (ro, n_new) in enumerate(blocks):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e2 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res = eng.prefill(store, t, ro, n_new, turn_offset_heads=shard.q_begin)
+            gathered.clear()
+            res = eng.prefill(store, t, ro, n_new, turn_offset_heads=shard.q_begin,
+                              layer_done=layer_done if gather is not None else None)
             if gather is not None:
-                for l in range(cfg["n_layers"]):
-                    gather.prefill(res.out[l])
+                stream.wait_stream(side)
             e1.record(stream)
-            sink = (lambda t, ob: gather.decode(list(ob))) if gather is not None else None
-            eng.decode(store, ro + n_new, cfg["max_new"], out_sink=sink)
+            # decode: one all-gather per run of steps between events (multi-step graphs)
+            run_sink = (lambda s0, outs: gather.decode_run(outs)) if gather is not None else None
+            eng.decode(store, ro + n_new, cfg["max_new"], run_sink=run_sink)
             e2.record(stream)
             ev_log.append((e0, e1, e2))
             # rollback is implicit: the next block starts at ro + n_new (session.py:180)

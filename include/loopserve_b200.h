@@ -69,6 +69,13 @@ typedef struct ls_layer_desc {
 } ls_layer_desc;
 
 const char *ls_last_error(void);
+/* Device-side validation: kernels record the first reference error they find
+ * on the device (NonFiniteInput / AllMaskedRow in the sampled-row softmax of
+ * ls_score_lines, tensor_ops.py:34-38; EmptyPlan for a head with no selected
+ * line in ls_vs_attention, tensor_ops.py:165-166) in a device status word.
+ * ls_device_status synchronises `stream`, writes the code (0 = none) to
+ * *host_status and clears the word. */
+int ls_device_status(int32_t *host_status, ls_stream_t stream);
 int ls_version(void);
 /* Debugging: host-mapped int buffer where the pipelined kernels record the
  * progress of each role per CTA (NULL disables). */

@@ -48,6 +48,7 @@ DS = C.POINTER(DecodeStackDesc)
 SIGNATURES = {
     "ls_last_error": (C.c_char_p, []),
     "ls_version": (C.c_int, []),
+    "ls_device_status": (C.c_int, [C.POINTER(I32), P]),
     "ls_debug_set_buffer": (C.c_int, [P]),
     "ls_device_info": (C.c_int, [C.POINTER(C.c_int), C.c_char_p, C.c_int]),
     "ls_sample_size": (C.c_int, [I32, F64, I32, C.POINTER(I32)]),
@@ -171,6 +172,16 @@ class Captured:
         if entry_hook is not None:
             entry_hook(self.name, "end")
         launch_count += self.kernels
+
+
+def device_status(stream=None, what: str = "device") -> None:
+    """Raise the reference exception a kernel recorded on the device since the
+    last check (ls_device_status: synchronises the stream)."""
+    st = C.c_int32(0)
+    check(lib().ls_device_status(C.byref(st), stream_ptr(stream)), "ls_device_status")
+    if st.value:
+        exc = STATUS.get(int(st.value), NativeError)
+        raise exc(f"{what}: reported by the device (status {st.value})")
 
 
 def ptr(t) -> int | None:

@@ -13,6 +13,12 @@
 namespace ls {
 
 void set_error(const char *fmt, ...);
+int32_t *device_status_ptr();  // capi.cu: device validation status word (ls_device_status)
+
+// record a reference error found on the device (first one wins)
+__device__ __forceinline__ void report_status(int32_t *status, int32_t code) {
+  if (status) atomicCAS(status, 0, code);
+}
 int cuda_status(cudaError_t e, const char *where);
 
 #define LS_CUDA(call)                                          \

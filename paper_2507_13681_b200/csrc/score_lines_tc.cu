@@ -65,6 +65,7 @@ struct Params {
   unsigned long long *vfix, *sfix;  // [H][n_total]
   unsigned int *vmaxb, *smaxb;      // [H][n_total]
   float *row_stats;                 // [H][n_s][2]
+  int32_t *status;                  // device validation word (NonFiniteInput / AllMaskedRow)
 };
 
 __device__ __forceinline__ int rt_begin(const Params &p, int rt) {
@@ -134,14 +135,27 @@ struct TileCursor {
   }
 };
 
-// this CTA's slice [x0, x1) of the flat tile list; slices hold >= CHUNK / BN
-// tiles (fewer CTAs work on small problems) so a chunk spans at most two
+// first tile at or after global tile x that starts a 1024-key chunk of its item
+__device__ __forceinline__ int chunk_start_at_or_after(const int32_t *tstart, int n_items, int x, int T) {
+  if (x >= T) return T;
+  TileCursor c;
+  c.seek(tstart, n_items, x);
+  const int r = c.j % (CHUNK / BN);
+  if (r == 0) return x;
+  return min(x + (CHUNK / BN - r), c.i_end_tile);  // (the next item starts a chunk)
+}
+
+// this CTA's slice [x0, x1) of the flat tile list: balanced by tile count, with
+// both ends moved to chunk starts, so every 1024-key chunk is processed whole by
+// one CTA in tile order -- the results do not depend on the grid size or on
+// how many heads share the launch (head-sharded runs equal the unsharded one)
 __device__ __forceinline__ bool tile_slice(const Params &p, int &x0, int &x1) {
-  const int T = p.tstart[p.n_heads * p.n_rt];
-  const int G = min(static_cast<int>(gridDim.x), max(1, T / (CHUNK / BN)));
-  if (static_cast<int>(blockIdx.x) >= G) return false;
-  x0 = static_cast<int>((static_cast<long long>(T) * blockIdx.x) / G);
-  x1 = static_cast<int>((static_cast<long long>(T) * (blockIdx.x + 1)) / G);
+  const int n_items = p.n_heads * p.n_rt;
+  const int T = p.tstart[n_items];
+  const int G = gridDim.x;
+  x0 = chunk_start_at_or_after(p.tstart, n_items, static_cast<int>((static_cast<long long>(T) * blockIdx.x) / G), T);
+  x1 = chunk_start_at_or_after(p.tstart, n_items,
+                               static_cast<int>((static_cast<long long>(T) * (blockIdx.x + 1)) / G), T);
   return x0 < x1;
 }
 
@@ -463,6 +477,10 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
           float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + r0 + tid) * 2;
           rs[0] = m;
           rs[1] = l > 0.f ? 1.f / l : 0.f;
+          // softmax_rows' validation (tensor_ops.py:34-38): a NaN / +inf logit
+          // (NaN row max or sum), or a row whose every logit is -inf
+          if (isnan(m) || isnan(l) || isinf(l) || (isinf(m) && m > 0.f)) report_status(p.status, LS_ERR_NON_FINITE_INPUT);
+          else if (m == -INFINITY) report_status(p.status, LS_ERR_ALL_MASKED_ROW);
         }
       }
       m_sh[tid] = m;
@@ -763,6 +781,7 @@ int k1_prepare(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uin
   p.kv_head_stride = L->kv_head_stride;
   p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
   p.row_stats = row_stats;
+  p.status = device_status_ptr();
   Carver c(ws, ws_bytes);
   const size_t H = L->n_heads;
   p.pstats = c.take<float2>(H * p.n_chunks * n_s * 4);

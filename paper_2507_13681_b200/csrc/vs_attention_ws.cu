@@ -61,6 +61,7 @@ struct Params {
   long long *tiles;  // optional: tensor-core tiles executed per head (NULL: not counted)
   float *row_lse;    // optional [H][n_new]: log2-sum-exp2 of each row's plan cells (-inf: diagonal fallback)
   int *dbg;  // optional host-mapped progress record [CTA][16] (ls_debug_set_buffer)
+  int32_t *status;  // device validation word (EmptyPlan)
 };
 
 // progress note of a role (0 producer, 1 MMA, 2 softmax, 3 tile counts) before a wait
@@ -156,6 +157,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n_kb = g_hi / BN + 1;
   const int n_sl = p.dense ? 0 : p.counts[h * 2 + 0];
   const int n_vt = p.dense ? 0 : p.counts[h * 2 + 1];
+  // masked_sparse_attention raises EmptyPlan for a plan with no lines (tensor_ops.py:165-166)
+  if (!p.dense && qt == 0 && tid == 0 && n_sl == 0 && n_vt == 0) report_status(p.status, LS_ERR_EMPTY_PLAN);
   const int32_t *S = p.slash_ids + static_cast<int64_t>(h) * p.n_total;
   const int32_t *Vl = p.vert_ids + static_cast<int64_t>(h) * p.n_total;
   if (p.dense) {
@@ -1211,6 +1214,7 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   p.tiles = reinterpret_cast<long long *>(tiles);
   p.row_lse = row_lse;
   p.dbg = g_debug_buffer;
+  p.status = device_status_ptr();
   LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * H, st));
   if (tiles) LS_CUDA(cudaMemsetAsync(tiles, 0, sizeof(int64_t) * H, st));
   // the q-tile-pair ping-pong variant is opt-in (LS_K5_PP=1): measured slower

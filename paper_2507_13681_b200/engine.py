@@ -32,6 +32,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
+from .errors import EmptyPlan
 from .kvcompress import CompressionConfig, DecodeStack
 from .prefill import LayerPlans, Workspace, sample_rows_device, sample_size, sparsify_layer
 from .tensor_ops import attention_layer, dense_attention_layer, plan_rows
@@ -131,6 +132,7 @@ class SessionEngine:
         self._q_buf = torch.empty((shape.n_layers, shape.n_q, 1, shape.d), dtype=torch.bfloat16, device=device)
         self._out_buf = torch.empty((shape.n_layers, shape.n_q, shape.d), dtype=out_dtype, device=device)
         self._graphs = {}
+        self._ring = None
         if head_groups is None:
             import os
             head_groups = int(os.environ.get("LS_HEAD_GROUPS", "1"))
@@ -172,6 +174,10 @@ class SessionEngine:
         n_total = row_offset + n_new
         outs, plans_all, cells_all = [], [], []
         rows = None
+        if p.mode == "loopserve" and p.alpha <= 0.0:
+            # alpha = 0 selects no line for any head (prefill.py:188-195), and
+            # masked_sparse_attention rejects the empty plan (tensor_ops.py:165-166)
+            raise EmptyPlan("alpha = 0 selects no line: the sparse prefill has an empty plan")
         if p.mode == "loopserve":
             if p.alpha >= 1.0:  # session.py:136-137: every row
                 rows = torch.arange(n_new, dtype=torch.int32, device=self.device).expand(
@@ -314,14 +320,18 @@ class SessionEngine:
         return g
 
     def decode(self, store: QKVStore, L0: int, max_new: int, use_graphs: bool = True, out_sink=None,
-               events: list | None = None):
+               events: list | None = None, run_sink=None):
         """max_new decode steps (kvcompress.py:200-239) from cache length L0,
         after prefill() set the counters. Returns the last step's outputs
         [L, n_q, d]; out_sink(step, out_buf) is called after every step.
         events: if a list, every compression event appends a device snapshot
         (step n_o, cache length, selected ids, score coverage) -- no host sync;
         event_log() turns them into the reference's event records and
-        decode_op_counts() into its decode op counts."""
+        decode_op_counts() into its decode op counts.
+        run_sink(step0, outs): with multi-step graphs, called after each run of
+        steps between two events with that run's outputs [n, L, n_q, d] (one
+        call per run instead of one host round trip per step: e.g. the
+        head-sharded output all-gather)."""
         p, sh = self.params, self.shape
         st = self.stack
         self._last_decode = (L0, max_new, events)
@@ -359,7 +369,9 @@ class SessionEngine:
                 if out_sink is not None:
                     out_sink(n_o - 1, out_buf)
             return out_buf
-        sk = id(store)
+        # graphs bake in the store's K/V/Q pointers: key them on those, not on
+        # id(store) (a recycled id would replay a graph bound to freed memory)
+        sk = (store.q.data_ptr(), store.k.data_ptr(), store.v.data_ptr(), tuple(store.k.shape))
         graphs = {}
         if n_dense > 0:
             graphs["dense"] = self._graph(("dense", sk, dense_cols), "decode_graph_dense",
@@ -374,6 +386,13 @@ class SessionEngine:
             # no per-step host work: every run of steps between two events is one
             # graph of that many steps (the kernels read the device counters, so
             # a multi-step graph is the same launch sequence back to back)
+            ring = None
+            if run_sink is not None:
+                if self._ring is None or self._ring.shape[0] < max_new:
+                    self._ring = torch.empty((max_new,) + tuple(out_buf.shape), dtype=out_buf.dtype,
+                                             device=out_buf.device)
+                    self._graphs = {k: v for k, v in self._graphs.items() if k[-1] != "ring"}
+                ring = self._ring
             n_o = 1
             while n_o <= max_new:
                 if comp.event_at(n_o):
@@ -385,14 +404,21 @@ class SessionEngine:
                     nxt += 1
                 n = nxt - n_o
                 kind, cols = ("comp", comp_cols) if compressed else ("dense", dense_cols)
-                g = self._graph((kind, sk, cols, n), f"decode_graph_{kind}",
-                                lambda n=n, c=compressed, cols=cols: [self._step(store, q_buf, out_buf, c, cols)
-                                                                      for _ in range(n)])
+                if ring is None:
+                    g = self._graph((kind, sk, cols, n), f"decode_graph_{kind}",
+                                    lambda n=n, c=compressed, cols=cols: [self._step(store, q_buf, out_buf, c, cols)
+                                                                          for _ in range(n)])
+                else:  # step k of the run writes ring[k]
+                    g = self._graph((kind, sk, cols, n, "ring"), f"decode_graph_{kind}",
+                                    lambda n=n, c=compressed, cols=cols: [self._step(store, q_buf, ring[k], c, cols)
+                                                                          for k in range(n)])
                 g.replay()
                 st.length += n
                 st.appended += n
+                if ring is not None:
+                    run_sink(n_o - 1, ring[:n])
                 n_o = nxt
-            return out_buf
+            return ring[n - 1] if ring is not None else out_buf
         for n_o in range(1, max_new + 1):
             if comp.event_at(n_o):
                 graphs["event"].replay()
@@ -403,6 +429,14 @@ class SessionEngine:
             st.appended += 1
             out_sink(n_o - 1, out_buf)
         return out_buf
+
+    def check(self, stream=None) -> None:
+        """Synchronise and raise the reference exception any kernel of this
+        process recorded on the device since the last check (NonFiniteInput /
+        AllMaskedRow from the sampled-row softmax, EmptyPlan from the sparse
+        attention). prefill()/decode() stay asynchronous; call this where the
+        caller would read results anyway."""
+        _lib.device_status(stream, what="SessionEngine")
 
     # ------------------------------------------------------- session records
     def event_log(self, events: list, head_offset: int = 0) -> list[dict]:

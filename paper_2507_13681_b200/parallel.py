@@ -87,6 +87,13 @@ class OutputGather:
         buf = self._gather(local)  # [W, n_new, H_local, d]
         return buf.permute(1, 0, 2, 3).reshape(local.shape[0], self.shard.n_q, self.d)
 
+    def decode_run(self, outs):
+        """[n_steps, L, H_local, d] of a run of decode steps -> [n_steps, L, H, d]
+        in one collective (SessionEngine.decode(run_sink=...))."""
+        n, L = outs.shape[0], outs.shape[1]
+        buf = self._gather(outs)  # [W, n, L, H_local, d]
+        return buf.permute(1, 2, 0, 3, 4).reshape(n, L, self.shard.n_q, self.d)
+
     def decode(self, step_outs):
         """list over layers of [H_local, d] -> list of [H, d]"""
         import torch

@@ -331,6 +331,7 @@ def sparsify_head(Q_sampled, K_all, alpha: float, row_positions, counter: OpCoun
     block[local] = Qs[torch.from_numpy(order).to(K.device)]
     rows = local.to(torch.int32).reshape(1, -1).contiguous()
     plans = sparsify_layer(block.unsqueeze(0), K.unsqueeze(0), rows, alpha, n_new, n_total, 1)
+    _lib.device_status(what="sparsify_head")  # NonFiniteInput / AllMaskedRow (tensor_ops.py:34-38)
     if counter is not None:
         counter.add(int(plans.score_count[0].item()))
     return plans.to_host()[0]

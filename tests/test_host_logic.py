@@ -88,6 +88,15 @@ def _worker(rank, world, port, q):
     full = OutputGather(shard, d).prefill(local)
     step = [torch.full((shard.n_q_local, d), float(l * 100 + rank)) for l in range(2)]
     dec = OutputGather(shard, d).decode(step)
+    # a run of 3 decode steps of 2 layers in one collective (SessionEngine.decode(run_sink=...))
+    run = torch.stack([torch.stack([torch.stack([torch.full((d,), float(1000 * s + 100 * l + h))
+                                                 for h in shard.q_heads()]) for l in range(2)]) for s in range(3)])
+    run_full = OutputGather(shard, d).decode_run(run)
+    assert run_full.shape == (3, 2, 8, d)
+    for s_ in range(3):
+        for l in range(2):
+            for h in range(8):
+                assert torch.all(run_full[s_, l, h] == 1000 * s_ + 100 * l + h)
     # per-head sampling seeds depend on the GLOBAL head id only
     rows = [oseed.sample_rows(500, 0.1, 32, oseed.head_seed(0, 1, 0, h)) for h in shard.q_heads()]
     q.put((rank, full.numpy(), [x.numpy() for x in dec], [r.tolist() for r in rows]))
