@@ -329,6 +329,21 @@ int ls_gather_attention(int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, c
                         int64_t q_head_stride, const uint16_t *k, const uint16_t *v, int64_t kv_head_stride,
                         const int64_t *col_ptr, const int32_t *cols, double *out, double *w_out, ls_stream_t stream);
 
+/* ------------------------------------------------ obswindow baseline ---
+ * The observation-window (SnapKV-style) baseline's one-shot selection
+ * (session.py:204-230): scores[c] = sum over units u = 0..n_units-1 (every
+ * (layer, head), in order) of accumulate_scores of that unit's n_rows dense
+ * observation rows (rows + u*unit_stride + r*row_stride, fp32 probabilities,
+ * oldest first) -- the summed_over_heads input of select_topB_obs; fp64, the
+ * reference's addition order. */
+int ls_obs_window_scores(int32_t n_units, int32_t n_rows, const float *rows, int64_t unit_stride,
+                         int64_t row_stride, int32_t n_cols, double *scores, ls_stream_t stream);
+/* dst + s*dst_slice_bytes + r*row_bytes = src + s*src_slice_bytes + ids[r]*row_bytes
+ * for s < n_slices, r < n_ids (row_bytes a multiple of 16): the baseline's
+ * compaction of the shared working set for every (layer, kv-head) slice. */
+int ls_gather_rows(int32_t n_slices, int32_t n_ids, const int32_t *ids, const void *src, int64_t src_slice_bytes,
+                   void *dst, int64_t dst_slice_bytes, int32_t row_bytes, ls_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -199,3 +199,46 @@ def progressive_decode_attn(k_arch, v_arch, kv_of_head, L0: int, obs_seed, comp:
         stats.step_head_scores.append(max(pre_counts.values()))
         stats.step_retained.append(max(len(working[h]) for h in heads))
     return outs, stats
+
+
+def obswindow_select(obs_seed, budget, window: int, length: int):
+    """session.py:204-230 (the obswindow baseline's one-shot selection):
+    obs_seed: per (layer, head), in (layer, head) order, the list of buffered
+    (ids, w) rows. Each head's scores go into a dense length-`length` array,
+    the arrays are summed over all heads (numpy axis-0 order) and one top-B
+    (summed_over_heads) is taken; base = retained_union(picked, W, length)
+    is every head's working set. Returns (picked, base, summed)."""
+    if budget is None:
+        base = np.arange(length, dtype=np.intp)
+        return base, base, None
+    per_head = []
+    for rows in obs_seed:
+        ids, scores = accumulate_scores(rows)
+        full = np.zeros(length)
+        full[ids] = scores
+        per_head.append(full)
+    summed = np.stack(per_head).sum(axis=0)
+    picked = top_by_score(np.arange(length), summed, budget)
+    return picked, retained_union(picked, window, length), summed
+
+
+def obswindow_decode_attn(k_arch, v_arch, kv_of_head, L0: int, base, max_new: int, q_steps, counter=None):
+    """session.py:239-257 at attention-only shapes: every head attends to
+    working = base + every position appended since (no re-selection), plus the
+    new position (model.py:232-241). Returns outs [max_new, n_heads, d]."""
+    n_heads = len(kv_of_head)
+    working = np.asarray(base, dtype=np.intp)
+    outs = np.zeros((max_new, n_heads, np.asarray(v_arch).shape[2]))
+    length = L0
+    for t in range(max_new):
+        pos = length
+        length += 1
+        cols = np.append(working, pos)
+        for h in range(n_heads):
+            kv = kv_of_head[h]
+            out, _ = decode_head_step(k_arch[kv], v_arch[kv], q_steps[t][h], cols)
+            outs[t, h] = out
+            if counter is not None:
+                counter.add(len(cols))
+        working = np.append(working, pos)
+    return outs

@@ -84,6 +84,8 @@ SIGNATURES = {
     "ls_retained_union": (C.c_int, [I32, P, I32, I32, I32, P, P, P, SZ, P]),
     "ls_kv_compact": (C.c_int, [I32, P, P, P, I32, P, I32, I32, P, P, P, P]),
     "ls_gather_attention": (C.c_int, [I32, I32, I32, P, I64, P, P, I64, P, P, P, P, P]),
+    "ls_obs_window_scores": (C.c_int, [I32, I32, P, I64, I64, I32, P, P]),
+    "ls_gather_rows": (C.c_int, [I32, I32, P, P, I64, P, I64, I32, P]),
 }
 
 
@@ -123,7 +125,7 @@ KERNELS_PER_CALL = {
     "ls_plan_coverage": 7,
     "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
     "ls_accumulate_scores": 1, "ls_top_by_score": 1, "ls_retained_union": 1, "ls_kv_compact": 1,
-    "ls_gather_attention": 1,
+    "ls_gather_attention": 1, "ls_obs_window_scores": 1, "ls_gather_rows": 1,
 }
 launch_count = 0
 entry_hook = None  # optional callable(name, phase) used by bench.py to time entries

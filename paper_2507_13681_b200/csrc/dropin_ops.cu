@@ -322,10 +322,72 @@ __global__ void __launch_bounds__(kGaThreads) gather_attention_kernel(int d, con
   }
 }
 
+// ------------------------------------------------ obswindow selection
+// session.py:215-225: per (layer, head) unit, the buffered dense observation
+// rows accumulated in row order (accumulate_scores), then summed over the
+// units in unit order (numpy's axis-0 sum of the stacked per-head arrays).
+// Thread per column: ((s_0 + s_1) + s_2) + ..., s_u = ((0 + w_u0) + w_u1) + ...
+__global__ void obs_sum_kernel(int n_units, int n_rows, const float *rows, int64_t unit_stride, int64_t row_stride,
+                               int n_cols, double *scores) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  double acc = 0.0;
+  for (int u = 0; u < n_units; ++u) {
+    const float *ru = rows + u * unit_stride + c;
+    double su = 0.0;
+    for (int r = 0; r < n_rows; ++r) su += static_cast<double>(__ldg(ru + r * row_stride));
+    acc = u == 0 ? su : acc + su;
+  }
+  scores[c] = acc;
+}
+
+// dst[slice][r] = src[slice][ids[r]] for 16-byte-multiple rows (the obswindow
+// baseline's one-shot compaction of the shared working set)
+__global__ void gather_rows_kernel(int n_slices, int n_ids, const int32_t *ids, const uint8_t *src,
+                                   int64_t src_slice_bytes, uint8_t *dst, int64_t dst_slice_bytes, int row_bytes) {
+  const int vec = row_bytes / 16;
+  const int64_t per_slice = static_cast<int64_t>(n_ids) * vec;
+  const int64_t total = per_slice * n_slices;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int sl = static_cast<int>(t / per_slice);
+    const int64_t rem = t - sl * per_slice;
+    const int r = static_cast<int>(rem / vec), c = static_cast<int>(rem - static_cast<int64_t>(r) * vec);
+    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + sl * src_slice_bytes +
+                                                          static_cast<int64_t>(ids[r]) * row_bytes) + c);
+    reinterpret_cast<uint4 *>(dst + sl * dst_slice_bytes + static_cast<int64_t>(r) * row_bytes)[c] = v;
+  }
+}
+
 }  // namespace dropin
 }  // namespace ls
 
 using namespace ls;
+
+extern "C" int ls_obs_window_scores(int32_t n_units, int32_t n_rows, const float *rows, int64_t unit_stride,
+                                    int64_t row_stride, int32_t n_cols, double *scores, ls_stream_t stream) {
+  LS_REQUIRE(n_units >= 1 && n_rows >= 1, LS_ERR_EMPTY_WINDOW, "need at least one observation row");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dropin::obs_sum_kernel<<<ceil_div(n_cols, 256), 256, 0, st>>>(n_units, n_rows, rows, unit_stride, row_stride, n_cols,
+                                                               scores);
+  LS_LAUNCH_CHECK("obs_sum_kernel");
+  return LS_OK;
+}
+
+extern "C" int ls_gather_rows(int32_t n_slices, int32_t n_ids, const int32_t *ids, const void *src,
+                              int64_t src_slice_bytes, void *dst, int64_t dst_slice_bytes, int32_t row_bytes,
+                              ls_stream_t stream) {
+  LS_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0, LS_ERR_UNSUPPORTED, "row_bytes must be a multiple of 16");
+  if (n_ids == 0 || n_slices == 0) return LS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long total = static_cast<long long>(n_slices) * n_ids * (row_bytes / 16);
+  const int grid = static_cast<int>(std::min<long long>(ceil_div_ll(total, 256), 148 * 8));
+  dropin::gather_rows_kernel<<<grid, 256, 0, st>>>(n_slices, n_ids, ids, static_cast<const uint8_t *>(src),
+                                                   src_slice_bytes, static_cast<uint8_t *>(dst), dst_slice_bytes,
+                                                   row_bytes);
+  LS_LAUNCH_CHECK("gather_rows_kernel");
+  return LS_OK;
+}
 
 extern "C" int ls_accumulate_scores(int32_t n_rows, const int64_t *row_ptr, const int32_t *ids, const double *w,
                                     int32_t id_cap, double *acc, uint8_t *touched, ls_stream_t stream) {

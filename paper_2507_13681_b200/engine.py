@@ -37,7 +37,7 @@ from .kvcompress import CompressionConfig, DecodeStack
 from .prefill import LayerPlans, Workspace, sample_rows_device, sample_size, sparsify_layer
 from .tensor_ops import attention_layer, dense_attention_layer, plan_rows
 
-MODES = ("dense", "loopserve")
+MODES = ("dense", "loopserve", "obswindow")  # session.py:40
 GRAPH_BUCKET = 1024  # column-bound bucket of the captured decode graphs
 
 
@@ -133,6 +133,8 @@ class SessionEngine:
         self._out_buf = torch.empty((shape.n_layers, shape.n_q, shape.d), dtype=out_dtype, device=device)
         self._graphs = {}
         self._ring = None
+        self._obs = None  # obswindow baseline: (compact store, full-cache decode engine)
+        self._obs_nb = None
         if head_groups is None:
             import os
             head_groups = int(os.environ.get("LS_HEAD_GROUPS", "1"))
@@ -197,11 +199,20 @@ class SessionEngine:
                 layer_ready(l, main)
             qb = store.q[l, :, row_offset:n_total]
             kl, vl = store.k[l], store.v[l]
-            if p.mode == "dense":
+            if p.mode in ("dense", "obswindow"):
                 outs.append(dense_attention_layer(qb, kl, vl, n_new, n_total, sh.n_kv, out_dtype=self.out_dtype,
                                                   q_head_stride=store.q.stride(1), stream=stream))
                 plans_all.append(None)
                 cells_all.append(None)
+                if p.mode == "obswindow" and p.comp.budget is not None:
+                    # the baseline's observation rows: the last W rows of every head's
+                    # dense block (session.py:163, 89-95), into ring slots [0, n_seed)
+                    sl, vt, cn = self._all_lines(n_total)
+                    hr = slice(l * sh.n_q, (l + 1) * sh.n_q)
+                    plan_rows(qb, kl, sl, vt, cn, n_new, n_total, sh.n_kv, n_seed, out=self.stack.ring_s[hr, 0:],
+                              out_row_stride=self.stack.row_cap,
+                              out_head_stride=self.stack.window * self.stack.row_cap,
+                              q_head_stride=store.q.stride(1), stream=stream)
                 if layer_done is not None:
                     layer_done(l, outs[-1], main)
                 continue
@@ -232,6 +243,71 @@ class SessionEngine:
                 st.ring_dense[:, first:n_seed] = 1
         st.set_step(n_total, n_seed)
         return PrefillOut(outs, plans_all, cells_all, rows, n_new, n_total, n_seed)
+
+    def _all_lines(self, n_total: int):
+        """Every slash of every head: the plan whose cells are the whole causal block."""
+        key = ("all_lines", n_total)
+        if key not in self._graphs:
+            H = self.shape.n_q
+            sl = torch.arange(n_total, dtype=torch.int32, device=self.device).expand(H, n_total).contiguous()
+            cn = torch.tensor([[n_total, 0]] * H, dtype=torch.int32, device=self.device)
+            self._graphs[key] = (sl, torch.zeros_like(sl), cn)
+        return self._graphs[key]
+
+    def _decode_obswindow(self, store: QKVStore, L0: int, max_new: int, events, out_sink, run_sink):
+        """The observation-window baseline's decode (session.py:204-257): one
+        shared top-B over the prefill observation rows summed over every layer
+        and head (K7-style fp64 accumulation + radix select, all on the
+        device), base = retained_union(picked, W, L0) for every head, then
+        append-only decoding against base + the new positions: the base rows
+        are gathered once into a compact per-(layer, kv-head) store after which
+        the new tokens' rows follow, and the full-cache decode (K6 dense steps)
+        runs over it -- the same cells as the reference's working set."""
+        import ctypes
+
+        p, sh, st = self.params, self.shape, self.stack
+        W, B = self.window, p.comp.budget
+        dev = self.device
+        n_rows = min(st.appended, W)
+        scores = torch.empty(L0, dtype=torch.float64, device=dev)
+        _lib.call("ls_obs_window_scores", sh.n_layers * sh.n_q, n_rows, st.ring_s.data_ptr(), W * st.row_cap,
+                  st.row_cap, L0, scores.data_ptr(), _lib.stream_ptr())
+        b = min(B, L0)
+        ids = torch.arange(L0, dtype=torch.int32, device=dev)
+        picked = torch.empty(b, dtype=torch.int32, device=dev)
+        n_out = torch.empty(2, dtype=torch.int32, device=dev)
+        ws = torch.empty(int(_lib.lib().ls_top_by_score_workspace(L0)) + (L0 + 31) // 32 * 4 + 256,
+                         dtype=torch.uint8, device=dev)
+        _lib.call("ls_top_by_score", L0, ids.data_ptr(), scores.data_ptr(), b, 0, L0, picked.data_ptr(),
+                  n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        base = torch.empty(b + W + 1, dtype=torch.int32, device=dev)
+        _lib.call("ls_retained_union", b, picked.data_ptr(), W, L0, L0, base.data_ptr(), n_out[1:].data_ptr(),
+                  ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        nb = int(n_out[1].item())  # the compact store's length (one sync per turn)
+        base = base[:nb]
+        if events is not None:
+            events.append({"step": 0, "length": L0, "base": base})
+        cap_c = (B + W + 1) + max_new + 1
+        if self._obs is None or self._obs[0].cap < cap_c:
+            comp = CompressionConfig(budget=None, interval=p.comp.interval, warmup=p.comp.warmup,
+                                     obs_window=p.comp.obs_window)
+            inner = SessionEngine(sh, SessionParams(mode="dense", comp=comp, max_new=max_new), cap_c, device=dev,
+                                  out_dtype=self.out_dtype)
+            self._obs = (QKVStore(sh, cap_c, device=dev), inner)
+        sc, inner = self._obs
+        rows = torch.cat([base, torch.arange(L0, L0 + max_new, dtype=torch.int32, device=dev)])
+        d2 = sh.d * 2
+        for src, dst in ((store.k, sc.k), (store.v, sc.v)):
+            _lib.call("ls_gather_rows", sh.n_layers * sh.n_kv, rows.numel(), rows.data_ptr(), src.data_ptr(),
+                      store.cap * d2, dst.data_ptr(), sc.cap * d2, d2, _lib.stream_ptr())
+        qrows = rows[nb:]
+        _lib.call("ls_gather_rows", sh.n_layers * sh.n_q, max_new, qrows.data_ptr(), store.q.data_ptr(),
+                  store.cap * d2, sc.q.data_ptr() + nb * d2, sc.cap * d2, d2, _lib.stream_ptr())
+        inner.stack.set_step(nb, 0)
+        self._last_decode = (L0, max_new, events)
+        self._obs_nb = nb
+        del ctypes
+        return inner.decode(sc, nb, max_new, out_sink=out_sink, run_sink=run_sink)
 
     def _layer_group(self, l, h0, h1, kv0, kv1, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs, out, ws,
                      stream, on_scored=None, select_stream=None):
@@ -335,6 +411,9 @@ class SessionEngine:
         p, sh = self.params, self.shape
         st = self.stack
         self._last_decode = (L0, max_new, events)
+        self._obs_nb = None
+        if p.mode == "obswindow" and p.comp.budget is not None:
+            return self._decode_obswindow(store, L0, max_new, events, out_sink, run_sink)
 
         def snap(n_o):
             if events is not None:
@@ -448,6 +527,11 @@ class SessionEngine:
         sh, W = self.shape, self.window
         out = []
         for ev in events:
+            if "base" in ev:  # the obswindow baseline's one selection (session.py:226-234)
+                keep = [int(g) for g in ev["base"].cpu().numpy()]
+                out += [{"step": 0, "head": f"L{l}H{h + head_offset}", "retained_ids": list(keep),
+                         "score_coverage": 1.0} for l in range(sh.n_layers) for h in range(sh.n_q)]
+                continue
             sel, n_sel, cov = ev["sel"].cpu().numpy(), ev["n_sel"].cpu().numpy(), ev["cov"].cpu().numpy()
             L = ev["length"]
             recent = np.arange(max(0, L - W), L)
@@ -468,6 +552,10 @@ class SessionEngine:
 
         L0, max_new, _ = self._last_decode
         sh, W = self.shape, self.window
+        if self._obs_nb is not None:  # obswindow: base + the appended positions (session.py:243-253)
+            nb = self._obs_nb
+            return {"decode_scores": sh.n_layers * sh.n_q * sum(nb + t + 1 for t in range(max_new)),
+                    "decode_steps": max(0, max_new - 1)}
         by_step = {ev["step"]: ev for ev in events}
         cur = None
         total = 0

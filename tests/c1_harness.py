@@ -29,6 +29,7 @@ import numpy as np
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(REPO, "tests", "golden", "c1_run.json")
+GOLDEN_OBS = os.path.join(REPO, "tests", "golden", "c1_obswindow.json")  # mode="obswindow" (session.py:204-257)
 
 N_TURNS, INPUT_LEN, MAX_NEW = 3, 1000, 32
 
@@ -65,29 +66,30 @@ def install_bf16_projection(model_mod):
     return lambda: setattr(model_mod, "qkv_project", orig)
 
 
-def c1_inputs(mods):
+def c1_inputs(mods, mode: str = "loopserve"):
     m, kv, se = mods["model"], mods["kvcompress"], mods["session"]
     cfg = m.ModelConfig(1, 8, 512, 64, 64, 1000, max_seq_len=N_TURNS * INPUT_LEN + N_TURNS * MAX_NEW + 8)
     weights = m.init_weights(cfg, 0)
     rng = np.random.Generator(np.random.PCG64(123))
     turns = [rng.integers(0, cfg.vocab_size, size=INPUT_LEN).tolist() for _ in range(N_TURNS)]
-    params = se.SessionParams(alpha=0.9, comp=kv.CompressionConfig(budget=256, interval=16, warmup=16),
+    params = se.SessionParams(mode=mode, alpha=0.9, comp=kv.CompressionConfig(budget=256, interval=16, warmup=16),
                               sample_rate=0.1, sample_floor=32, max_new=MAX_NEW, seed=0)
     return weights, turns, params
 
 
-def run_c1(mods, record_argmax: bool = True, capture_sparsifier: list | None = None):
+def run_c1(mods, record_argmax: bool = True, capture_sparsifier: list | None = None, mode: str = "loopserve"):
     """Three run_turn calls; returns a JSON-able record of everything the
     parity test compares. record_argmax logs, for every greedy choice, the
     gap between the two largest logits (to classify an answer divergence as
     a near-tie). capture_sparsifier collects (turn, layer, head, Q_s, K, pos)."""
     m, se = mods["model"], mods["session"]
-    weights, turns, params = c1_inputs(mods)
+    weights, turns, params = c1_inputs(mods, mode)
     undo = install_bf16_projection(m)
     gaps = []
     orig_argmax = m.argmax_token
     kv_mod = mods["kvcompress"]
     orig_kv_argmax = kv_mod.argmax_token
+    orig_se_argmax = se.argmax_token
 
     def argmax_logged(logits):
         lg = np.asarray(logits, dtype=np.float64)
@@ -98,6 +100,7 @@ def run_c1(mods, record_argmax: bool = True, capture_sparsifier: list | None = N
     if record_argmax:
         m.argmax_token = argmax_logged
         kv_mod.argmax_token = argmax_logged
+        se.argmax_token = argmax_logged
     orig_sp = se.sparsify_head
     turn_box = [0]
     if capture_sparsifier is not None:
@@ -133,6 +136,7 @@ def run_c1(mods, record_argmax: bool = True, capture_sparsifier: list | None = N
         undo()
         m.argmax_token = orig_argmax
         kv_mod.argmax_token = orig_kv_argmax
+        se.argmax_token = orig_se_argmax
         se.sparsify_head = orig_sp
 
 
@@ -145,13 +149,13 @@ if __name__ == "__main__":
 
     build()
     mods = reference_modules()
-    t0 = time.time()
-    rec = run_c1(mods)
-    import numpy  # noqa: F401
-
-    meta = {"numpy": np.__version__, "seconds": round(time.time() - t0, 1),
-            "generator": "tests/c1_harness.py (pure reference, bf16-rounded projections)"}
-    with open(GOLDEN, "w") as fh:
-        json.dump({"meta": meta, "turns": rec}, fh, separators=(",", ":"))
-    print(f"wrote {GOLDEN} in {meta['seconds']} s:",
-          [(len(r["answer"]), len(r["events"]), r["op_counts"]) for r in rec])
+    for mode, path in (("loopserve", GOLDEN), ("obswindow", GOLDEN_OBS)):
+        if len(sys.argv) > 1 and mode not in sys.argv[1:]:
+            continue
+        t0 = time.time()
+        rec = run_c1(mods, mode=mode)
+        meta = {"numpy": np.__version__, "seconds": round(time.time() - t0, 1), "mode": mode,
+                "generator": "tests/c1_harness.py (pure reference, bf16-rounded projections)"}
+        with open(path, "w") as fh:
+            json.dump({"meta": meta, "turns": rec}, fh, separators=(",", ":"))
+        print(f"wrote {path} in {meta['seconds']} s:", [(len(r["answer"]), len(r["events"]), r["op_counts"]) for r in rec])

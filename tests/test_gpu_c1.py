@@ -16,7 +16,7 @@ import os
 import numpy as np
 import pytest
 
-from c1_harness import GOLDEN, reference_modules, run_c1
+from c1_harness import GOLDEN, GOLDEN_OBS, reference_modules, run_c1
 from parity import NEAR_TIE_REL, check_plan
 
 REPORT_DIR = os.environ.get("LS_REPORT_DIR", "gpurun_out")
@@ -51,26 +51,31 @@ def _oracle_classify(q_s, k_all, pos, dev_plan, log):
 
 
 @pytest.mark.gpu
-def test_c1_run_turn_dropin_matches_reference(cuda_lib):
+@pytest.mark.parametrize("mode", ["loopserve", "obswindow"])
+def test_c1_run_turn_dropin_matches_reference(cuda_lib, mode):
+    """mode="loopserve": sparse prefill + progressive decode; mode="obswindow":
+    the reference's observation-window baseline (dense prefill, one shared
+    top-B summed over heads, session.py:204-257) through the same drop-in."""
     from paper_2507_13681_b200 import dropin
 
     mods = reference_modules()
     assert mods is not None, "oracle/_ref is not built (python oracle/build_ref.py in a container with /root/reference)"
-    with open(GOLDEN) as fh:
+    with open(GOLDEN if mode == "loopserve" else GOLDEN_OBS) as fh:
         gold = json.load(fh)["turns"]
     patched = dropin.install({f"loopserve.{k}": v for k, v in mods.items()})
     assert "loopserve.kvcompress.decode_step" in patched and "loopserve.session.sparsify_head" in patched
     captured = []
     try:
-        got = run_c1(mods, capture_sparsifier=captured)
+        got = run_c1(mods, capture_sparsifier=captured, mode=mode)
     finally:
         dropin.uninstall()
-    report = {"near_tie_rel": NEAR_TIE_REL, "turns": [], "violations": []}
+    report = {"mode": mode, "near_tie_rel": NEAR_TIE_REL, "turns": [], "violations": []}
     try:
         _compare(gold, got, captured, report)
     finally:
         os.makedirs(REPORT_DIR, exist_ok=True)
-        with open(os.path.join(REPORT_DIR, "c1_parity_report.json"), "w") as fh:
+        name = "c1_parity_report.json" if mode == "loopserve" else "c1_obswindow_parity_report.json"
+        with open(os.path.join(REPORT_DIR, name), "w") as fh:
             json.dump(report, fh, indent=1)
     assert not report["violations"], report["violations"][:6]
 
