@@ -50,6 +50,16 @@ CONFIGS = {
                         "head-sharded over the ranks",
                n_layers=32, n_q=32, n_kv=8, d=128, input_len=8192, n_turns=4, max_new=256, alpha=0.955,
                budget=2048, interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),
+    "c4": dict(workload="C4: Qwen2.5-7B attention (28q/4kv, d=128, bf16), 28 layers, 64 independent 3-turn x 5000-token "
+                        "sessions sharded over 8 B200 (8 sessions per GPU, batched into every launch), 128 decoded "
+                        "tokens/turn, alpha=0.955, B=1024, n_d=16",
+               n_layers=28, n_q=28, n_kv=4, d=128, input_len=5000, n_turns=3, max_new=128, alpha=0.955,
+               budget=1024, interval=16, warmup=16, obs_window=None, rate=0.1, floor=32, sessions=8),
+    "c5": dict(workload="C5: Llama-3.1-70B attention (64q/8kv, d=128, bf16), 80 layers, 10 turns x 10000 tokens "
+                        "(~101K-token context), 128 decoded tokens/turn, alpha=0.955, B=1024, n_d=16, one KV-head "
+                        "group (8 q-heads) per GPU of 8 (each rank runs its shard; at N < 8 the first N shards)",
+               n_layers=80, n_q=64, n_kv=8, d=128, input_len=10000, n_turns=10, max_new=128, alpha=0.955,
+               budget=1024, interval=16, warmup=16, obs_window=None, rate=0.1, floor=32, kv_shards=8),
     "c1": dict(workload="C1: toy attention layer (8 heads MHA, d=64), 3 turns x 1000 tokens, alpha=0.9, B=256",
                n_layers=1, n_q=8, n_kv=8, d=64, input_len=1000, n_turns=3, max_new=32, alpha=0.9, budget=256,
                interval=16, warmup=16, obs_window=None, rate=0.1, floor=32),
@@ -283,15 +293,23 @@ def main():
     from paper_2507_13681_b200.kvcompress import CompressionConfig
     from paper_2507_13681_b200.parallel import HeadShard
 
-    shard = HeadShard(cfg["n_q"], cfg["n_kv"], world, rank)
-    shape = AttnShape(cfg["n_layers"], shard.n_q_local, shard.n_kv_local, cfg["d"])
+    n_sess = cfg.get("sessions", 1)
+    if n_sess > 1:  # C4: session sharding (no collective), n_sess sessions per GPU batched into every launch
+        shard = HeadShard(cfg["n_q"], cfg["n_kv"], 1, 0)
+        shape = AttnShape(cfg["n_layers"], n_sess * cfg["n_q"], n_sess * cfg["n_kv"], cfg["d"])
+        session_seeds = [rank * n_sess + s for s in range(n_sess)]  # global session ids as Session seeds
+        kv_offset = rank * n_sess * cfg["n_kv"]
+    else:  # head sharding over the ranks (C5: a fixed 8-way shard, rank r runs shard r)
+        shard = HeadShard(cfg["n_q"], cfg["n_kv"], cfg.get("kv_shards", world), rank % cfg.get("kv_shards", world))
+        shape = AttnShape(cfg["n_layers"], shard.n_q_local, shard.n_kv_local, cfg["d"])
+        session_seeds, kv_offset = None, shard.kv_begin
     comp = CompressionConfig(cfg["budget"], cfg["interval"], cfg["warmup"], cfg["obs_window"])
     params = SessionParams(alpha=cfg["alpha"], comp=comp, sample_rate=cfg["rate"], sample_floor=cfg["floor"],
                            max_new=cfg["max_new"], seed=0)
     blocks = turn_blocks(cfg["input_len"], cfg["n_turns"], cfg["max_new"])
     cap = cfg["n_turns"] * (cfg["input_len"] + cfg["max_new"])
-    store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1, kv_offset=shard.kv_begin)
-    eng = SessionEngine(shape, params, cap)
+    store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1, kv_offset=kv_offset)
+    eng = SessionEngine(shape, params, cap, session_seeds=session_seeds)
     stream = torch.cuda.current_stream()
 
     # per-entry CUDA-event timing (on the launching stream)
@@ -313,7 +331,7 @@ def main():
 
     _lib.entry_hook = hook
 
-    gather = shard.make_gather(cfg["d"]) if world > 1 else None
+    gather = shard.make_gather(cfg["d"]) if (world > 1 and n_sess == 1 and "kv_shards" not in cfg) else None
 
     side = torch.cuda.Stream() if gather is not None else None
     gathered = []
@@ -387,7 +405,8 @@ def main():
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     total_ms, prefill_ms, decode_ms = vals.tolist()
     ttft = prefill_ms / n_prefills
-    tok_s = args.steps * cfg["n_turns"] * cfg["max_new"] / (decode_ms / 1e3)
+    # every session (C4) decodes its own tokens; head-sharded ranks decode the same tokens
+    tok_s = n_sess * world ** (n_sess > 1) * args.steps * cfg["n_turns"] * cfg["max_new"] / (decode_ms / 1e3)
 
     # per-entry shares and the dominant kernel's roofline
     per = {}
@@ -412,6 +431,11 @@ def main():
             dec_roof["share_of_timed"] = round(sum(per[k]) / total_ms, 4)
             break
 
+    ev_roof = event_roofline(per, cfg, eng, shape, blocks, peaks)
+    k1_roof = k1_roofline(per, eng, cfg, clk)
+    if n_sess > 1 or "kv_shards" in cfg:
+        # the dense baseline, plan quality, end-to-end and CPU legs are measured on C2
+        args.no_dense = args.no_e2e = args.no_cpu_baseline = True
     dense = None if args.no_dense else dense_baseline(cfg, store, blocks, shard, ttft)
     quality = None if args.no_dense else plan_quality(cfg, eng, store, blocks, shard)
 
@@ -431,8 +455,14 @@ def main():
             "decode_tokens_per_s": round(tok_s, 2),
             "prefill_ms_per_turn": round(ttft, 3), "decode_ms_per_turn": round(decode_ms / n_prefills, 3),
             "stages_ms": stages, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-            "decode_roofline": dec_roof, "prefill_roofline": pre_roof, "dense_baseline": dense,
-            "plan_quality": quality}
+            "decode_roofline": dec_roof, "prefill_roofline": pre_roof, "event_roofline": ev_roof,
+            "k1_roofline": k1_roof, "dense_baseline": dense, "plan_quality": quality}
+    if n_sess > 1:
+        line["scaling"] = "weak"
+        line["config"]["parallelism"] = f"sessions: {n_sess} per GPU x {world} GPU(s), batched per launch"
+    if "kv_shards" in cfg:
+        line["scaling"] = "weak"
+        line["config"]["parallelism"] = f"kv-head group shard {rank % cfg['kv_shards']} of {cfg['kv_shards']} per GPU"
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -443,6 +473,63 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def event_roofline(per, cfg, eng, shape, blocks, peaks):
+    """Compression events (one graph: K7 select + K8 compaction, all layers)
+    against HBM. Algorithmic bytes of the turn's events:
+    K7 reads every buffered row once -- dense rows (prefill seeds, pre-event
+    steps) 4 B per column, compressed rows 8 B (logit + id) over B + W + 1
+    columns -- and K8 reads and writes every selected K and V row:
+    2 * 2 * B * d * 2 B per (layer, q-head)."""
+    name = "decode_graph_event"
+    if name not in per or not cfg.get("budget"):
+        return None
+    B, W, d = cfg["budget"], cfg["obs_window"] or cfg["interval"], cfg["d"]
+    units = shape.n_layers * shape.n_q
+    tot, n_ev = 0.0, 0
+    for ro, n_new in blocks:
+        L0 = ro + n_new
+        for n_o in range(cfg["warmup"], cfg["max_new"] + 1, cfg["interval"]):
+            L = L0 + n_o - 1
+            if n_o == cfg["warmup"]:  # seeds and dense steps: every column
+                k7 = sum(4.0 * (L0 + t) for t in range(max(0, n_o - W), n_o))
+            else:
+                k7 = W * 8.0 * (B + W + 1)
+            k8 = 2 * 2 * min(B, L) * d * 2.0
+            tot += units * (k7 + k8)
+            n_ev += 1
+    mean_ms = statistics.mean(per[name])
+    bytes_ = tot / max(1, n_ev)
+    ach = bytes_ / (mean_ms * 1e-3) / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": round(ach, 3), "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm"], 5), "mean_launch_ms": round(mean_ms, 4), "launches": len(per[name]),
+            "work_per_launch": bytes_, "peak_src": peaks["src"], "traffic": None}
+
+
+def k1_roofline(per, eng, cfg, clk):
+    """K1 (ls_score_lines: stats + lines passes over the causal sampled cells)
+    against max(tensor, MUFU): per pass 2*d FLOPs of QK^T and
+    one ex2 per cell, so 2 passes = 4*d FLOPs + 2 ex2 per cell. MUFU peak: 16
+    ex2 / clk / SM x 148 SMs at the sampled SM clock (B200_PROFILING.md)."""
+    name = "ls_score_lines"
+    if name not in per or not eng.score_log:
+        return None
+    n = len(per[name])
+    cells = float(sum(int(c.sum()) for c in eng.score_log)) / n
+    mean_ms = statistics.mean(per[name])
+    sm_ghz = ((clk or {}).get("sm_mhz") or 1965.0) / 1e3
+    mufu_peak = 16 * 148 * sm_ghz * 1e9  # ex2 / s
+    peaks = load_peaks()
+    tensor_peak = (peaks["tensor_sus"] or peaks["tensor"]) * 1e12
+    t_mufu = 2 * cells / mufu_peak * 1e3
+    t_tensor = 2 * 2 * cfg["d"] * cells / tensor_peak * 1e3
+    bound = "mufu" if t_mufu >= t_tensor else "tensor"
+    return {"kernel": name, "bound": bound, "cells_per_launch": cells, "bound_ms": round(max(t_mufu, t_tensor), 4),
+            "mufu_bound_ms": round(t_mufu, 4), "tensor_bound_ms": round(t_tensor, 4),
+            "mean_launch_ms": round(mean_ms, 4), "frac": round(max(t_mufu, t_tensor) / mean_ms, 4),
+            "achieved": round(2 * cells / (mean_ms * 1e-3) / 1e12, 4), "unit": "T ex2/s",
+            "peak": round(mufu_peak / 1e12, 4), "launches": n}
 
 
 def roofline(per, cfg, eng, store, blocks, peaks):

@@ -114,8 +114,21 @@ class SessionEngine:
     groups of layer l finish before layer l + 1 starts."""
 
     def __init__(self, shape: AttnShape, params: SessionParams, cap: int, device="cuda",
-                 out_dtype=torch.bfloat16, head_groups: int | None = None, keep_plans: bool = True):
+                 out_dtype=torch.bfloat16, head_groups: int | None = None, keep_plans: bool = True,
+                 session_seeds=None):
+        """session_seeds: run len(session_seeds) independent dialogue sessions
+        of identical turn geometry as ONE batch (config C4, session.py:71-86 /
+        cli.py:213-226): `shape` then counts the heads of all sessions, session
+        s owning q-heads [s*H_s, (s+1)*H_s) and kv-heads [s*KV_s, (s+1)*KV_s);
+        each session samples its rows with its own seed and head ids 0..H_s-1
+        (Session.head_seed), and every kernel launch covers all sessions'
+        heads (the decode moves n_sessions x the bytes per launch)."""
         params.validate()
+        self.session_seeds = list(session_seeds) if session_seeds is not None else None
+        if self.session_seeds is not None:
+            S = len(self.session_seeds)
+            if S < 1 or shape.n_q % S or shape.n_kv % S:
+                raise ValueError(f"{S} sessions do not divide {shape.n_q} q-heads / {shape.n_kv} kv-heads")
         # the session's plan ledger (turn, layer) -> LayerPlans (session.py:153-154)
         self.plan_ledger = {} if keep_plans else None
         self.shape, self.params, self.cap = shape, params, cap
@@ -184,6 +197,14 @@ class SessionEngine:
             if p.alpha >= 1.0:  # session.py:136-137: every row
                 rows = torch.arange(n_new, dtype=torch.int32, device=self.device).expand(
                     sh.n_layers, sh.n_q, n_new).contiguous()
+            elif self.session_seeds is not None:  # per-session seeds, per-session head ids
+                hs = sh.n_q // len(self.session_seeds)
+                parts = []
+                for sd in self.session_seeds:
+                    r_ = sample_rows_device(n_new, p.sample_rate, p.sample_floor, sd, turn, 0, 0, hs,
+                                            n_layers=sh.n_layers, stream=stream, ws=self.rows_ws)
+                    parts.append(r_.unsqueeze(0) if r_.dim() == 2 else r_.clone())
+                rows = torch.cat(parts, dim=1)
             else:
                 rows = sample_rows_device(n_new, p.sample_rate, p.sample_floor, p.seed, turn, 0,
                                           turn_offset_heads, sh.n_q, n_layers=sh.n_layers, stream=stream,
