@@ -1611,7 +1611,8 @@ static int decode_step_impl(const ls_decode_stack *S, int32_t layer, const uint1
 #define LS_ARGS q, q_head_stride, q_from_archive, k_layer, v_layer
   // dense steps: one unit per kv-head with its whole q-group (each K/V row read
   // once); LS_DECODE_DENSE_PER_HEAD=1 splits them per q-head (measured slower)
-  const bool per_head = compressed || getenv("LS_DECODE_DENSE_PER_HEAD") != nullptr;
+  static const bool env_dense_per_head = getenv("LS_DECODE_DENSE_PER_HEAD") != nullptr;  // read once
+  const bool per_head = compressed || env_dense_per_head;
   if (per_head) {
     r = S->head_dim == 128
             ? launch_k6<128, 1>(S->n_heads, max_cols, st, S, layer, LS_ARGS, compressed, sl, out, out_bf16, pdl)

@@ -3,9 +3,10 @@
 // Replaces the sort in _line_sums (reference prefill.py:168-169) and
 // _greedy (prefill.py:178-229).
 //
-// K2 sort: one CTA per (head, kind) sorts the n_total lines by
-//   (weight desc, index asc)  -- a stable LSD radix sort of ~bits(w_fp64)
-// (cub::BlockRadixSort, in-shared-memory, up to 16384 lines).
+// K2 sort: every (head, kind) list of a layer sorted at once by
+//   (weight desc, index asc) -- one device-wide stable LSD radix sort over
+// composite (segment, fixed-point weight) keys (sort_keys_kernel ->
+// cub::DeviceRadixSort -> sort_scatter_kernel).
 //
 // K3 greedy, split so the sequential part is tiny:
 //   (a) chain: the pick decisions of _greedy depend only on
@@ -29,7 +30,6 @@
 
 #include <algorithm>
 
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ls_common.cuh"
@@ -38,9 +38,6 @@ namespace ls {
 extern int *g_debug_buffer;
 namespace sel {
 
-constexpr int SORT_THREADS = 512;
-constexpr int SORT_ITEMS = 32;  // capacity 16384
-constexpr int SORT_CAP = SORT_THREADS * SORT_ITEMS;
 constexpr double EPS = 1e-12;   // prefill.py:188
 
 struct Lists {  // sorted lines, [H][2][n] (kind 0 = slash, 1 = vertical)
@@ -61,50 +58,6 @@ struct Picks {  // [H][cap]
 };
 
 // ---------------------------------------------------------------- K2 sort
-using BlockSort = cub::BlockRadixSort<unsigned long long, SORT_THREADS, SORT_ITEMS, int32_t>;
-
-template <typename MaxT>
-__global__ void __launch_bounds__(SORT_THREADS) sort_lines_kernel(const double *v_w, const MaxT *v_max,
-                                                                  const double *s_w, const MaxT *s_max,
-                                                                  const int32_t *rows, int n_s, int n_total,
-                                                                  int row_offset, Lists out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto &temp = *reinterpret_cast<typename BlockSort::TempStorage *>(smem_raw);
-  int *pos = reinterpret_cast<int *>(smem_raw + sizeof(typename BlockSort::TempStorage));
-  const int h = blockIdx.y, kind = blockIdx.x;  // 0 slash, 1 vertical
-  const double *w = (kind == 0 ? s_w : v_w) + static_cast<int64_t>(h) * n_total;
-  const MaxT *mx = (kind == 0 ? s_max : v_max) + static_cast<int64_t>(h) * n_total;
-  for (int r = threadIdx.x; r < n_s; r += blockDim.x) pos[r] = row_offset + rows[static_cast<int64_t>(h) * n_s + r];
-  unsigned long long keys[SORT_ITEMS];
-  int32_t vals[SORT_ITEMS];
-#pragma unroll
-  for (int i = 0; i < SORT_ITEMS; ++i) {
-    int idx = threadIdx.x * SORT_ITEMS + i;  // blocked arrangement = index order
-    if (idx < n_total) {
-      keys[i] = ~static_cast<unsigned long long>(__double_as_longlong(w[idx]));
-    } else {
-      keys[i] = ~0ull;
-    }
-    vals[i] = idx;
-  }
-  __syncthreads();
-  BlockSort(temp).Sort(keys, vals);  // ascending ~bits == descending weight, stable
-  __syncthreads();
-  const int64_t base = (static_cast<int64_t>(h) * 2 + kind) * n_total;
-#pragma unroll
-  for (int i = 0; i < SORT_ITEMS; ++i) {
-    int o = threadIdx.x * SORT_ITEMS + i;
-    if (o < n_total) {
-      int idx = vals[i];
-      out.idx[base + o] = idx;
-      out.w[base + o] = w[idx];
-      out.mx[base + o] = static_cast<double>(mx[idx]);
-      out.len[base + o] = n_s - lower_bound_dev(pos, n_s, idx);  // #{rows with g >= idx}, prefill.py:144,155
-      out.inv[base + idx] = o;
-    }
-  }
-}
-
 // K2 (device-wide): every (head, kind) list of a layer sorted at once by one
 // stable LSD radix sort over composite keys
 //   (segment << fix_bits) | (2^fix_bits - 1 - fixed point weight)
@@ -902,7 +855,6 @@ inline Work carve(Carver &c, int H, int n_total) {
   return w;
 }
 
-inline size_t sort_smem() { return sizeof(typename BlockSort::TempStorage) + 4 * 16384 + 64; }
 
 inline size_t radix_temp_bytes(int H, int n_total) {
   size_t bytes = 0;

@@ -562,492 +562,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
-// ---------------------------------------------------------------------------
-// K5 ping-pong variant: one CTA per (head, PAIR of 128-row q tiles A, B).
-// The two q tiles share every K/V tile load (the union of their tile lists,
-// each entry tagged with its owner tiles) and alternate on the tensor pipe:
-// while softmax warpgroup A works on S_A(t), the MMA thread runs PV_B / S_B,
-// and the other way round. Each softmax thread owns one full row (128
-// columns), so no per-tile max exchange is needed. TMEM: S_A | S_B | O_A | O_B
-// (P(t) bf16 over its own S buffer, PV as a TMEM-A MMA).
-constexpr int PP_THREADS = 320;        // 8 softmax warps (2 warpgroups) + producer + MMA
-constexpr int PP_MAX_KB = 1024;        // n_total <= 131072
-constexpr int PP_MAX_LIST = 4 * (PP_MAX_KB + 1);
-
-struct PPBars {
-  uint64_t full[2], empty[2], q_full;
-  uint64_t s_full[2], p_full[2], pv_done[2][2];  // [q tile] / [q tile][ordinal parity]
-};
-
-template <int D>
-struct PPSmem {
-  static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int KV_BYTES = BN * D * 2;
-  static constexpr int OFF_Q = 0;                        // A, B
-  static constexpr int OFF_K = 2 * Q_BYTES;              // 2 stages
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;     // 2 stages
-  static constexpr int OFF_MISC = OFF_V + 2 * KV_BYTES;
-  // misc: bars 256 | ints 256 | kb[2][32] 256 | gcols[2][128] 1024 | cm[2 X][2 stage][4] 64 (+pad)
-  //       | lx 1024 | blk_cnt[1024] 4096 | wins[2][1025] 8200 | list[4100] 16400
-  static constexpr int M_BARS = 0, M_INT = 256, M_KB = 512, M_GC = 768, M_CM = 1792, M_BLK = 2048,
-                       M_WIN = M_BLK + PP_MAX_KB * 4, M_LIST = M_WIN + 2 * (PP_MAX_KB + 1) * 4 + 16,
-                       M_END = M_LIST + PP_MAX_LIST * 4;
-  static constexpr int TOTAL = OFF_MISC + M_END + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(PP_THREADS, 1)
-    vs_attention_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
-                           const __grid_constant__ CUtensorMap tm_vc, Params p) {
-  extern __shared__ unsigned char smem_dyn[];
-  using L = PPSmem<D>;
-  unsigned char *smem = tc::align1024(smem_dyn);
-  unsigned char *misc = smem + L::OFF_MISC;
-  PPBars *bars = reinterpret_cast<PPBars *>(misc + L::M_BARS);
-  int *sh_int = reinterpret_cast<int *>(misc + L::M_INT);            // [64]
-  uint32_t *kbx = reinterpret_cast<uint32_t *>(misc + L::M_KB);      // [2][32] dense blocks of q tile X
-  int *gcols = reinterpret_cast<int *>(misc + L::M_GC);               // [2 stage][128]
-  uint32_t *cmx = reinterpret_cast<uint32_t *>(misc + L::M_CM);      // [2 X][2 stage][4]
-  int *blk_cnt = reinterpret_cast<int *>(misc + L::M_BLK);            // [PP_MAX_KB]
-  int *wins = reinterpret_cast<int *>(misc + L::M_WIN);               // [2][PP_MAX_KB + 1]
-  int *list = reinterpret_cast<int *>(misc + L::M_LIST);              // union tiles: code
-  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(misc + L::M_INT + 252);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = blockIdx.y, qp = blockIdx.x;
-  const int kv = h / p.group;
-  const uint32_t *vbits = p.vbits + static_cast<int64_t>(h) * (p.words + 8);
-  const uint32_t *rsbits = p.rsbits + static_cast<int64_t>(h) * (p.words + 8);
-  const int n_sl = p.counts[h * 2 + 0];
-  const int n_vt = p.counts[h * 2 + 1];
-  const int32_t *S = p.slash_ids + static_cast<int64_t>(h) * p.n_total;
-  const int32_t *Vl = p.vert_ids + static_cast<int64_t>(h) * p.n_total;
-  // geometry of q tile X
-  auto tile_r0 = [&](int X) { return qp * 2 * BM + X * BM; };
-  auto tile_nr = [&](int X) { return max(0, min(BM, p.n_new - tile_r0(X))); };
-
-  if (warp == 0) tc::tmem_alloc(tmem_sh, 512);
-  if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&bars->full[s], 1);
-      tc::mbar_init(&bars->empty[s], 1);
-      tc::mbar_init(&bars->s_full[s], 1);
-      tc::mbar_init(&bars->p_full[s], 1);
-      tc::mbar_init(&bars->pv_done[s][0], 1);
-      tc::mbar_init(&bars->pv_done[s][1], 1);
-    }
-    tc::mbar_init(&bars->q_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = tid; i < 64; i += PP_THREADS) kbx[i] = 0u;
-  __syncthreads();
-
-  // ---- per q tile: dense blocks, verticals <= g_hi, windows over isolated slashes
-  for (int X = 0; X < 2; ++X) {
-    const int nr = tile_nr(X);
-    if (nr == 0) {
-      if (tid == 0) { sh_int[4 * X + 0] = 0; sh_int[4 * X + 1] = 0; }
-      __syncthreads();
-      continue;
-    }
-    const int g0 = p.row_offset + tile_r0(X), g_hi = g0 + nr - 1;
-    const int n_kb = g_hi / BN + 1;
-    uint32_t *kb = kbx + 32 * X;
-    for (int i = tid; i < PP_MAX_KB; i += PP_THREADS) blk_cnt[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < n_sl; i += PP_THREADS) {
-      const int dd = S[i];
-      if (dd > g_hi) break;
-      const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
-      for (int b = c_lo / BN; b <= c_hi / BN; ++b) atomicAdd(&blk_cnt[b], 1);
-    }
-    __syncthreads();
-    for (int b = tid; b < n_kb; b += PP_THREADS)
-      if (blk_cnt[b] >= DENSE_SLASHES) atomicOr(&kb[b >> 5], 1u << (b & 31));
-    __syncthreads();
-    int32_t *sl = p.diag_ws + (static_cast<int64_t>(h) * p.n_qtiles + qp * 2 + X) * p.n_total;
-    int n_diag = 0;
-    for (int base = 0; base < n_sl; base += PP_THREADS) {
-      const int i = base + tid;
-      bool take = false;
-      int dd = 0;
-      if (i < n_sl) {
-        dd = S[i];
-        if (dd <= g_hi) {
-          const int c_lo = max(0, g0 - dd), c_hi = g_hi - dd;
-          for (int b = c_lo / BN; b <= c_hi / BN; ++b) take |= !bit_of(kb, b);
-        }
-      }
-      const unsigned ball = __ballot_sync(0xffffffffu, take);
-      __syncthreads();
-      if (lane == 0) sh_int[16 + warp] = __popc(ball);
-      __syncthreads();
-      int before = 0, tot = 0;
-      for (int w = 0; w < PP_THREADS / 32; ++w) {
-        if (w < warp) before += sh_int[16 + w];
-        tot += sh_int[16 + w];
-      }
-      if (take) sl[n_diag + before + __popc(ball & ((1u << lane) - 1u))] = dd;
-      n_diag += tot;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int n_win = 0, covered = -1;
-      int *wx = wins + X * (PP_MAX_KB + 1);
-      for (int i = n_diag - 1; i >= 0; --i) {
-        const int dd = sl[i];
-        const int lo = max(0, g0 - dd), hi = g_hi - dd;
-        if (hi <= covered) continue;
-        for (int w = max(lo, covered + 1); w <= hi && n_win <= PP_MAX_KB; w += BN) {
-          wx[n_win++] = w;
-          covered = w + BN - 1;
-        }
-      }
-      int lo = 0, hi2 = n_vt;  // verticals <= g_hi
-      while (lo < hi2) {
-        const int mid = (lo + hi2) >> 1;
-        if (Vl[mid] <= g_hi) lo = mid + 1; else hi2 = mid;
-      }
-      sh_int[4 * X + 0] = n_win;
-      sh_int[4 * X + 1] = (lo + BN - 1) / BN;  // gathered tiles
-      sh_int[4 * X + 2] = lo;                  // verticals <= g_hi
-    }
-    __syncthreads();
-  }
-  // ---- union list: code = start | kind << 28 | owner << 30 (start: key row or gathered tile)
-  if (tid == 0) {
-    int n = 0;
-    const int n_kb = (min(p.n_new, qp * 2 * BM + 2 * BM) - 1 + p.row_offset) / BN + 1;
-    for (int b = 0; b < n_kb; ++b) {
-      const int o = (bit_of(kbx, b) ? 1 : 0) | (bit_of(kbx + 32, b) ? 2 : 0);
-      if (o) list[n++] = b * BN | (0 << 28) | (o << 30);
-    }
-    const int ng = max(sh_int[1], sh_int[5]);
-    for (int k = 0; k < ng; ++k) list[n++] = k | (1 << 28) | (((k < sh_int[1]) ? 1 : 0) | ((k < sh_int[5]) ? 2 : 0)) << 30;
-    for (int X = 0; X < 2; ++X)
-      for (int i = 0; i < sh_int[4 * X]; ++i) list[n++] = wins[X * (PP_MAX_KB + 1) + i] | (2 << 28) | ((X + 1) << 30);
-    sh_int[12] = n;
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const int n_list = sh_int[12];
-  const uint32_t tmem = *tmem_sh;
-  auto l_start = [&](int c) { return c & 0x0fffffff; };
-  auto l_kind = [&](int c) { return (c >> 28) & 3; };
-  auto l_own = [&](int c) { return (static_cast<unsigned>(c) >> 30) & 3u; };
-
-  if (warp == 8) {
-    // =================================================== TMA producer
-    if (lane == 0) {
-      tc::prefetch_tmap(&tm_q);
-      tc::prefetch_tmap(&tm_k);
-      tc::prefetch_tmap(&tm_v);
-      tc::prefetch_tmap(&tm_kc);
-      tc::prefetch_tmap(&tm_vc);
-      tc::mbar_expect_tx(&bars->q_full, 2 * L::Q_BYTES);
-      for (int X = 0; X < 2; ++X)
-#pragma unroll
-        for (int a = 0; a < D / 64; ++a)
-          tc::tma_load_3d(tc::smem_u32(smem + L::OFF_Q + X * L::Q_BYTES + a * BM * 128), &tm_q, &bars->q_full, a * 64,
-                          tile_r0(X), h);
-    }
-    for (int t = 0; t < n_list; ++t) {
-      const int s = t & 1;
-      const int c = list[t];
-      if (lane == 0) tc::mbar_wait(&bars->empty[s], ((t >> 1) & 1) ^ 1);
-      __syncwarp();
-      if (l_kind(c) == 1) {  // gathered: stage this tile's vertical columns for the masks
-        for (int i = lane; i < BN; i += 32) {
-          const int idx = l_start(c) * BN + i;
-          gcols[s * BN + i] = idx < n_vt ? Vl[idx] : 0x7fffffff;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        tc::mbar_expect_tx(&bars->full[s], 2 * L::KV_BYTES);
-        const CUtensorMap *mk = &tm_k, *mv = &tm_v;
-        int row = l_start(c), hh = kv;
-        if (l_kind(c) == 1) mk = &tm_kc, mv = &tm_vc, row = l_start(c) * BN, hh = h;
-        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
-        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + s * L::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < D / 64; ++a) {
-          tc::tma_load_3d(ks + a * BN * 128, mk, &bars->full[s], a * 64, row, hh);
-          tc::tma_load_3d(vs + a * BN * 128, mv, &bars->full[s], a * 64, row, hh);
-        }
-      }
-    }
-  } else if (warp == 9) {
-    // =================================================== MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t IDESC_S = tc::make_idesc(BM, BN, false, false);
-      constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, false, true);
-      tc::mbar_wait(&bars->q_full, 0);
-      int ord[2] = {0, 0};      // tiles issued per q tile
-      int pend[2] = {-1, -1};   // list index whose PV is pending, per q tile
-      auto issue_pv = [&](int X) {
-        const int t = pend[X];
-        const int o = ord[X] - 1;  // ordinal of that tile for X
-        tc::mbar_wait(&bars->p_full[X], o & 1);
-        tc::fence_after_sync();
-        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (t & 1) * L::KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
-          tc::mma_bf16_ts(tmem + 256 + X * 128, tmem + X * 128 + kk * 8, bd, IDESC_O, (o > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(&bars->pv_done[X][o & 1]);
-        pend[X] = -1;
-      };
-      for (int t = 0; t < n_list; ++t) {
-        const int s = t & 1;
-        const unsigned own = l_own(list[t]);
-        tc::mbar_wait(&bars->full[s], (t >> 1) & 1);
-        tc::fence_after_sync();
-        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
-        for (int X = 0; X < 2; ++X) {
-          if (pend[X] >= 0) issue_pv(X);  // P_X(prev) consumed before S_X(t) overwrites its buffer
-          if (own & (1u << X)) {
-            const uint32_t qs = tc::smem_u32(smem + L::OFF_Q + X * L::Q_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t ad = tc::make_desc(qs + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
-              const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
-              tc::mma_bf16(tmem + X * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
-            }
-            tc::mma_commit(&bars->s_full[X]);
-            pend[X] = t;
-            ++ord[X];
-          }
-        }
-        // every PV of tile t-1 has been issued above: release its K/V stage
-        if (t > 0) tc::mma_commit(&bars->empty[(t - 1) & 1]);
-      }
-      for (int X = 0; X < 2; ++X)
-        if (pend[X] >= 0) issue_pv(X);
-      if (n_list > 0) tc::mma_commit(&bars->empty[(n_list - 1) & 1]);
-    }
-  } else {
-    // =================================================== softmax warpgroups
-    const int X = warp >> 2;                    // q tile of this warpgroup
-    const int row = (warp & 3) * 32 + lane;     // TMEM lane = row
-    const int nr = tile_nr(X);
-    const int r0 = tile_r0(X);
-    const int g0 = p.row_offset + r0;
-    const int my_g = g0 + row;
-    const bool row_ok = row < nr;
-    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t s_tm = tmem + X * 128 + lane_base, o_tm = tmem + 256 + X * 128 + lane_base;
-    const uint32_t *kb = kbx + 32 * X;
-    const int v_end = sh_int[4 * X + 2];
-    float m_ref = -INFINITY, l = 0.f;
-    long long my_cells = 0;
-    int o = 0;  // ordinal of this warpgroup's tiles
-    for (int t = 0; t < n_list; ++t) {
-      const int c = list[t];
-      if (!(l_own(c) & (1u << X))) continue;
-      const int s = t & 1;
-      uint32_t mk[4];
-      const int kind = l_kind(c);
-      if (kind == 1) {
-        // gathered: tile-wide mask of columns outside this q tile's dense blocks
-        // (the producer staged the columns before signalling `full`)
-        tc::mbar_wait(&bars->full[s], (t >> 1) & 1);
-        const int *gc = gcols + s * BN;
-        uint32_t *cm = cmx + (X * 2 + s) * 4;
-        {
-          const int cc = gc[row];
-          const unsigned b = __ballot_sync(0xffffffffu, cc != 0x7fffffff && !bit_of(kb, cc / BN));
-          if (lane == 0) cm[warp & 3] = b;
-        }
-        tc::named_sync(2 + X, 128);
-        int n_le;  // gathered columns <= my_g (sorted ascending)
-        if (gc[BN - 1] <= g0) {
-          n_le = BN;
-        } else {
-          int lo = 0, hi = BN;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (gc[mid] <= my_g) lo = mid + 1; else hi = mid;
-          }
-          n_le = lo;
-        }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int hi = n_le - 32 * w;
-          const uint32_t causal = hi >= 32 ? 0xffffffffu : (hi <= 0 ? 0u : ((1u << hi) - 1u));
-          mk[w] = row_ok ? (cm[w] & causal) : 0u;
-        }
-        (void)v_end;
-      } else if (!row_ok) {
-        mk[0] = mk[1] = mk[2] = mk[3] = 0u;
-      } else {
-        const int c0 = l_start(c);
-        uint32_t sw[4];
-        bit_window(rsbits, p.n_total - 1 - my_g + c0, sw, 2);
-        bit_window(rsbits, p.n_total - 1 - my_g + c0 + 64, sw + 2, 2);
-        if (kind == 0) {  // dense block: causal & (vbit | sbit)
-#pragma unroll
-          for (int w = 0; w < 4; ++w) mk[w] = ((c0 / 32 + w < p.words) ? __ldg(vbits + c0 / 32 + w) : 0u) | sw[w];
-        } else {  // window: slash cells outside dense blocks and verticals
-          uint32_t vw[4];
-          bit_window(vbits, c0, vw, 2);
-          bit_window(vbits, c0 + 64, vw + 2, 2);
-          const int b1 = c0 / BN, split = (b1 + 1) * BN - c0;  // columns [0, split) in block b1
-          const bool d1 = bit_of(kb, b1), d2 = b1 + 1 < PP_MAX_KB && bit_of(kb, b1 + 1);
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int lo_c = 32 * w;  // word covers columns [lo_c, lo_c + 32)
-            uint32_t in1;             // columns of this word inside block b1
-            const int k1 = split - lo_c;
-            in1 = k1 >= 32 ? 0xffffffffu : (k1 <= 0 ? 0u : ((1u << k1) - 1u));
-            const uint32_t dm = (d1 ? in1 : 0u) | (d2 ? ~in1 : 0u);
-            mk[w] = sw[w] & ~vw[w] & ~dm;
-          }
-        }
-        const int lim = my_g - c0;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int hi = lim - 32 * w;
-          mk[w] &= hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u));
-        }
-      }
-#pragma unroll
-      for (int w = 0; w < 4; ++w) my_cells += __popc(mk[w]);
-      tc::mbar_wait(&bars->s_full[X], o & 1);
-      tc::fence_after_sync();
-      float sv[128];
-      bool live[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {  // issue every load, then one wait (TMEM loads are .sync.aligned)
-        live[w] = __any_sync(0xffffffffu, mk[w] != 0u);
-        if (live[w]) tc::tmem_ld32(s_tm + 32 * w, sv + 32 * w);
-      }
-      tc::tmem_wait_ld();
-      float tm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        if (!live[w] || mk[w] != 0xffffffffu) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sv[32 * w + j] = ((mk[w] >> j) & 1u) ? sv[32 * w + j] : -INFINITY;
-        }
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          tm4[0] = fmaxf(tm4[0], sv[32 * w + j]);
-          tm4[1] = fmaxf(tm4[1], sv[32 * w + j + 1]);
-          tm4[2] = fmaxf(tm4[2], sv[32 * w + j + 2]);
-          tm4[3] = fmaxf(tm4[3], sv[32 * w + j + 3]);
-        }
-      }
-      const float tmax = fmaxf(fmaxf(tm4[0], tm4[1]), fmaxf(tm4[2], tm4[3]));
-      const float m_tile = tmax == -INFINITY ? -INFINITY : tmax * p.scale_log2;
-      const bool need = m_tile > m_ref + RESCALE_LOG2;
-      if (__any_sync(0xffffffffu, need && m_ref != -INFINITY && o > 0)) {
-        // O_X holds PV_X(o-1) once its commit lands; PV_X(o) waits for this tile's P
-        tc::mbar_wait(&bars->pv_done[X][(o - 1) & 1], ((o - 1) >> 1) & 1);
-        tc::fence_after_sync();
-        const float corr = (need && m_ref != -INFINITY) ? fast_exp2(m_ref - m_tile) : 1.f;
-#pragma unroll
-        for (int w = 0; w < D / 32; ++w) {
-          float ov[32];
-          tc::tmem_ld32(o_tm + 32 * w, ov);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) ov[j] *= corr;
-          tc::tmem_st32(o_tm + 32 * w, ov);
-        }
-        tc::tmem_wait_st();
-      }
-      if (need) {
-        if (m_ref != -INFINITY) l *= fast_exp2(m_ref - m_tile);
-        m_ref = m_tile;
-      }
-      float lsum = 0.f;
-      uint32_t pk[64];
-      if (m_ref != -INFINITY) {
-        const float nm = -m_ref;
-        float ls4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < 128; j += 2) {
-          const float a = fast_exp2(fmaf(sv[j], p.scale_log2, nm));
-          const float b = fast_exp2(fmaf(sv[j + 1], p.scale_log2, nm));
-          ls4[(j >> 1) & 3] += a + b;
-          pk[j >> 1] = tc::pack_bf16(a, b);
-        }
-        lsum = (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 64; ++j) pk[j] = 0u;
-      }
-      l += lsum;
-      // P(t) bf16 over this q tile's S buffer (all S reads of the tile are done)
-      tc::tmem_st32(s_tm, reinterpret_cast<const float *>(pk));
-      tc::tmem_st32(s_tm + 32, reinterpret_cast<const float *>(pk + 32));
-      tc::tmem_wait_st();
-      tc::fence_before_sync();
-      tc::named_sync(2 + X, 128);
-      if ((tid & 127) == 0) tc::mbar_arrive(&bars->p_full[X]);
-      ++o;
-    }
-    // ---- epilogue: O_X (TMEM) / l -> out
-    if (o > 0) {
-      tc::mbar_wait(&bars->pv_done[X][(o - 1) & 1], ((o - 1) >> 1) & 1);
-      tc::fence_after_sync();
-    }
-    // (TMEM loads are .sync.aligned: every lane of the warp loads each chunk)
-    const int64_t orow = static_cast<int64_t>(r0 + row) * p.out_row_stride + static_cast<int64_t>(h) * D;
-    const bool write_o = row_ok && l > 0.f;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll
-    for (int w = 0; w < D / 32; ++w) {
-      float ov[32];
-      if (o > 0) {
-        tc::tmem_ld32(o_tm + 32 * w, ov);
-        tc::tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) ov[j] = 0.f;
-      }
-      if (write_o) {
-        if (p.out_bf16) {
-          uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + orow + 32 * w;
-#pragma unroll
-          for (int j = 0; j < 32; j += 8)
-            *reinterpret_cast<uint4 *>(dst + j) =
-                make_uint4(tc::pack_bf16(ov[j] * inv, ov[j + 1] * inv), tc::pack_bf16(ov[j + 2] * inv, ov[j + 3] * inv),
-                           tc::pack_bf16(ov[j + 4] * inv, ov[j + 5] * inv), tc::pack_bf16(ov[j + 6] * inv, ov[j + 7] * inv));
-        } else {
-          float *dst = reinterpret_cast<float *>(p.out) + orow + 32 * w;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4 *>(dst + j) = make_float4(ov[j] * inv, ov[j + 1] * inv, ov[j + 2] * inv, ov[j + 3] * inv);
-        }
-      }
-    }
-    if (row_ok && !(l > 0.f)) {  // diagonal fallback (tensor_ops.py:136-137)
-      const uint16_t *vrow = p.v + static_cast<int64_t>(kv) * p.kv_head_stride + static_cast<int64_t>(my_g) * D;
-      for (int j = 0; j < D; ++j) {
-        const float val = bf2f(vrow[j]);
-        if (p.out_bf16)
-          reinterpret_cast<uint16_t *>(p.out)[orow + j] = f2bf(val);
-        else
-          reinterpret_cast<float *>(p.out)[orow + j] = val;
-      }
-      my_cells += 1;
-    }
-    const long long cs = warp_sum_ll(my_cells);
-    if (lane == 0 && cs)
-      atomicAdd(reinterpret_cast<unsigned long long *>(p.cells + h), static_cast<unsigned long long>(cs));
-    if ((tid & 127) == 0 && p.tiles && o)
-      atomicAdd(reinterpret_cast<unsigned long long *>(p.tiles + h), static_cast<unsigned long long>(o));
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
-}
-
 // compacted selected verticals: kc/vc[h][j] = K/V[kv(h)][vert_ids[h][j]], rows
 // [n_vt, round_up(n_vt, 128)) zeroed so that padded tile rows are finite
 __global__ void gather_verticals_kernel(const uint16_t *k, const uint16_t *v, const int32_t *vert_ids,
@@ -1217,23 +731,6 @@ int vs_attention_ws(const ls_layer_desc *L, const uint16_t *q, const uint16_t *k
   p.status = device_status_ptr();
   LS_CUDA(cudaMemsetAsync(cells, 0, sizeof(int64_t) * H, st));
   if (tiles) LS_CUDA(cudaMemsetAsync(tiles, 0, sizeof(int64_t) * H, st));
-  // the q-tile-pair ping-pong variant is opt-in (LS_K5_PP=1): measured slower
-  // than the single-tile kernel on C2 (one softmax warp per scheduler per tile)
-  const bool pp = !dense && !row_lse && (L->n_total + k5ws::BN - 1) / k5ws::BN <= k5ws::PP_MAX_KB && getenv("LS_K5_PP");
-  if (pp) {  // q-tile pairs sharing K/V tiles, ping-pong on the tensor pipe
-    dim3 grid((nqt + 1) / 2, H);
-    if (d == 128) {
-      const int smem = k5ws::PPSmem<128>::TOTAL;
-      LS_CUDA(cudaFuncSetAttribute(k5ws::vs_attention_pp_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k5ws::vs_attention_pp_kernel<128><<<grid, k5ws::PP_THREADS, smem, st>>>(tq, tk, tv, tkc, tvc, p);
-    } else {
-      const int smem = k5ws::PPSmem<64>::TOTAL;
-      LS_CUDA(cudaFuncSetAttribute(k5ws::vs_attention_pp_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k5ws::vs_attention_pp_kernel<64><<<grid, k5ws::PP_THREADS, smem, st>>>(tq, tk, tv, tkc, tvc, p);
-    }
-    LS_LAUNCH_CHECK("vs_attention_pp_kernel");
-    return LS_OK;
-  }
   dim3 grid(nqt, H);
   if (d == 128) {
     const int smem = k5ws::Smem<128>::TOTAL;
