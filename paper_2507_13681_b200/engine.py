@@ -32,7 +32,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
-from .errors import EmptyPlan
+from .errors import CacheCorrupt, DimensionMismatch, EmptyPlan, SequenceTooLong
 from .kvcompress import CompressionConfig, DecodeStack
 from .prefill import LayerPlans, Workspace, sample_rows_device, sample_size, sparsify_layer
 from .tensor_ops import attention_layer, dense_attention_layer, plan_rows
@@ -70,14 +70,59 @@ class AttnShape:
 
 
 class QKVStore:
-    """Q/K/V of every position of a dialogue, per layer, resident in HBM."""
+    """Q/K/V of every position of a dialogue, per layer, resident in HBM: the
+    append-only archive of the reference's KVCache (model.py:139-175; Q kept
+    too, since the attention-only path takes the projections as inputs).
+    `length` marks the filled prefix. A store built with `length=None` (the
+    default, e.g. QKVStore.synthetic) is preloaded: every position is present;
+    QKVStore.empty() starts at length 0 and grows with append()."""
 
-    def __init__(self, shape: AttnShape, cap: int, device="cuda", q=None, k=None, v=None):
+    def __init__(self, shape: AttnShape, cap: int, device="cuda", q=None, k=None, v=None, length: int | None = None):
         self.shape, self.cap = shape, cap
         L, d = shape.n_layers, shape.d
         self.q = q if q is not None else torch.empty((L, shape.n_q, cap, d), dtype=torch.bfloat16, device=device)
         self.k = k if k is not None else torch.empty((L, shape.n_kv, cap, d), dtype=torch.bfloat16, device=device)
         self.v = v if v is not None else torch.empty((L, shape.n_kv, cap, d), dtype=torch.bfloat16, device=device)
+        self.length = cap if length is None else int(length)
+        self.validate()
+
+    @staticmethod
+    def empty(shape: AttnShape, cap: int, device="cuda") -> "QKVStore":
+        return QKVStore(shape, cap, device=device, length=0)
+
+    def validate(self) -> None:
+        """KVCache.validate (model.py:157-168): length in range, layer/head shapes."""
+        sh = self.shape
+        if not (0 <= self.length <= self.cap):
+            raise CacheCorrupt(f"store length {self.length} outside [0, {self.cap}]")
+        want = {"q": (sh.n_layers, sh.n_q, self.cap, sh.d), "k": (sh.n_layers, sh.n_kv, self.cap, sh.d),
+                "v": (sh.n_layers, sh.n_kv, self.cap, sh.d)}
+        for name, shp in want.items():
+            if tuple(getattr(self, name).shape) != shp:
+                raise CacheCorrupt(f"{name} archive has a foreign shape {tuple(getattr(self, name).shape)} != {shp}")
+
+    def append(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> int:
+        """Write n new positions at [length, length + n) (forward_extend's cache
+        write, model.py:228-231): q [L, n_q, n, d], k / v [L, n_kv, n, d].
+        Returns the new length; SequenceTooLong past the capacity."""
+        n = int(k.shape[2])
+        if q.shape[2] != n or v.shape[2] != n:
+            raise DimensionMismatch("q, k, v must add the same number of positions")
+        if self.length + n > self.cap:
+            raise SequenceTooLong(f"{self.length + n} positions exceed the store capacity {self.cap}")
+        lo, hi = self.length, self.length + n
+        self.q[:, :, lo:hi].copy_(q, non_blocking=True)
+        self.k[:, :, lo:hi].copy_(k, non_blocking=True)
+        self.v[:, :, lo:hi].copy_(v, non_blocking=True)
+        self.length = hi
+        return hi
+
+    def truncate(self, length: int) -> None:
+        """KVCache.truncate (model.py:171-174): roll back to `length`, e.g. the
+        decode rows at the end of a turn (session.py:180)."""
+        if not (0 <= length <= self.length):
+            raise CacheCorrupt(f"cannot truncate length {self.length} to {length}")
+        self.length = int(length)
 
     @staticmethod
     def synthetic(shape: AttnShape, cap: int, n_ref: int | None = None, seed: int = 0, device="cuda",
@@ -187,6 +232,8 @@ class SessionEngine:
         next layer computes)."""
         p, sh = self.params, self.shape
         n_total = row_offset + n_new
+        if n_total > store.length:
+            raise CacheCorrupt(f"prefill of positions [{row_offset}, {n_total}) but the store holds {store.length}")
         outs, plans_all, cells_all = [], [], []
         rows = None
         if p.mode == "loopserve" and p.alpha <= 0.0:
@@ -431,6 +478,9 @@ class SessionEngine:
         head-sharded output all-gather)."""
         p, sh = self.params, self.shape
         st = self.stack
+        if L0 + max_new > store.length:
+            raise CacheCorrupt(f"decode of positions [{L0}, {L0 + max_new}) but the store holds {store.length} "
+                               "(append the decoded tokens' q / k / v first)")
         self._last_decode = (L0, max_new, events)
         self._obs_nb = None
         if p.mode == "obswindow" and p.comp.budget is not None:

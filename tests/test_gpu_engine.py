@@ -177,3 +177,39 @@ def test_multistep_graphs_identical(cuda_lib):
     (a, sa, sela, naa, ha), (b, sb, selb, nab, hb) = outs
     assert torch.equal(a, b)
     assert torch.equal(sa, sb) and torch.equal(sela, selb) and torch.equal(naa, nab) and ha == hb
+
+
+def test_multi_turn_session_with_archive_append_truncate(cuda_lib):
+    """A 3-turn session driven like run_turn (session.py:113-201) on an
+    append-only archive: append the block (previous answer + input), prefill,
+    append the decoded tokens' rows, decode, roll them back with truncate
+    (session.py:180) -- identical plans and outputs to the preloaded store, and
+    the plan ledger holds every (turn, layer)."""
+    from paper_2507_13681_b200.engine import AttnShape, QKVStore, SessionEngine, SessionParams
+    from paper_2507_13681_b200.kvcompress import CompressionConfig
+
+    shape = AttnShape(2, 4, 2, 128)
+    IN, MAX_NEW, T = 900, 24, 3
+    cap = T * (IN + MAX_NEW)
+    ref = QKVStore.synthetic(shape, cap, n_ref=cap, seed=8)
+    params = SessionParams(alpha=0.95, comp=CompressionConfig(128, 8, 8), max_new=MAX_NEW, seed=3)
+    e1, e2 = SessionEngine(shape, params, cap), SessionEngine(shape, params, cap)
+    st = QKVStore.empty(shape, cap)
+    for t, (ro, n_new) in enumerate(e1.turn_blocks(IN, T, MAX_NEW)):
+        hi = ro + n_new
+        st.truncate(ro)  # the previous turn's decode rows are re-prefilled as this block
+        st.append(ref.q[:, :, ro:hi], ref.k[:, :, ro:hi], ref.v[:, :, ro:hi])
+        a = e1.prefill(ref, t, ro, n_new)
+        b = e2.prefill(st, t, ro, n_new)
+        st.append(ref.q[:, :, hi:hi + MAX_NEW], ref.k[:, :, hi:hi + MAX_NEW], ref.v[:, :, hi:hi + MAX_NEW])
+        oa = e1.decode(ref, hi, MAX_NEW).clone()
+        ob = e2.decode(st, hi, MAX_NEW).clone()
+        torch.cuda.synchronize()
+        for l in range(2):
+            assert torch.equal(a.out[l], b.out[l])
+            assert torch.equal(a.plans[l].slash_ids, b.plans[l].slash_ids)
+        assert torch.equal(oa, ob)
+        st.truncate(hi)
+    assert sorted(e2.plan_ledger) == [(t, l) for t in range(T) for l in range(2)]
+    with pytest.raises(Exception):
+        e2.decode(st, st.length, MAX_NEW)  # decode rows not appended yet

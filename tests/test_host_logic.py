@@ -168,3 +168,31 @@ def test_dropin_rebinds_reference_names():
     assert all(getattr(mods[m], a) is fn for (m, a), fn in before.items())
     if ref is not None:
         assert not getattr(ref["model"].KVCache.truncate, "__b200__", False)
+
+
+def test_qkvstore_append_truncate_validate():
+    """QKVStore as the reference KVCache archive (model.py:139-175): append at
+    the filled prefix, roll back with truncate, CacheCorrupt / SequenceTooLong
+    as the reference raises them."""
+    import torch
+
+    from paper_2507_13681_b200.engine import AttnShape, QKVStore
+    from paper_2507_13681_b200.errors import CacheCorrupt, SequenceTooLong
+
+    sh = AttnShape(2, 4, 2, 8)
+    st = QKVStore.empty(sh, 10, device="cpu")
+    assert st.length == 0
+    blk = lambda n, h, x: torch.full((2, h, n, 8), float(x), dtype=torch.bfloat16)
+    assert st.append(blk(6, 4, 1), blk(6, 2, 2), blk(6, 2, 3)) == 6
+    assert torch.all(st.k[:, :, :6] == 2) and torch.all(st.v[:, :, :6] == 3)
+    st.truncate(4)  # decode rows rolled back (session.py:180)
+    assert st.append(blk(3, 4, 7), blk(3, 2, 8), blk(3, 2, 9)) == 7
+    assert torch.all(st.k[:, :, 4:7] == 8) and torch.all(st.k[:, :, :4] == 2)
+    with pytest.raises(SequenceTooLong):
+        st.append(blk(4, 4, 0), blk(4, 2, 0), blk(4, 2, 0))
+    with pytest.raises(CacheCorrupt):
+        st.truncate(8)
+    st.length = 11
+    with pytest.raises(CacheCorrupt):
+        st.validate()
+    assert QKVStore(sh, 10, device="cpu").length == 10  # preloaded by default
