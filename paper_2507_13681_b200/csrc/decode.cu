@@ -718,7 +718,9 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     // quad sum of the row's softmax denominator
     l_part += __shfl_xor_sync(0xffffffffu, l_part, 1);
     l_part += __shfl_xor_sync(0xffffffffu, l_part, 2);
-    __syncthreads();  // (A) every warp is done with the stage buffers
+    // (A) every consumer warp is done with the stage buffers (the producer warp
+    // issued its last TMA long before; every tile was waited on by a consumer)
+    tc::named_sync(1, 32 * KM_WARPS);
     float *wm = reinterpret_cast<float *>(sm);  // [W][8]
     float *wl = wm + KM_WARPS * 8;              // [W][8]
     float *wo = wl + KM_WARPS * 8;              // [W][8][D]
@@ -732,8 +734,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
         *reinterpret_cast<float2 *>(wo + (warp * 8 + g) * D + n * 8 + 2 * t4) = make_float2(o[n][0], o[n][1]);
     }
   }
-  if (warp == KM_WARPS) __syncthreads();  // (A) for the producer warp
-  __syncthreads();                        // (B) warp partials written
+  __syncthreads();  // (B) warp partials written
   // ---- this CTA's partial (M, L, O) per head, warps merged in order -> global
   {
     float *wm = reinterpret_cast<float *>(sm);
