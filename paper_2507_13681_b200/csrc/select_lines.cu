@@ -235,6 +235,7 @@ constexpr int RING = 1024;           // pick slots between producer and finalize
 constexpr int AHEAD = 512;           // the producer runs at most this far ahead of the finalizer: picks
                                      // past the plan's end cost crossing sums for nothing
 constexpr int GS_CAP = 8192;         // sampled positions kept in shared memory
+constexpr int BM_WORDS = TAB_CAP;    // bitmap words when n_total > TAB_CAP (the tables' space): n_total <= 2^19
 
 // gain_s >= gain_v with gain = num / den (prefill.py:206-208). Decided by
 // cross-multiplication unless the two sides are within 1e-13 relative, in
@@ -256,8 +257,16 @@ struct GreedySmem {
   double r_w[RING], r_approx[RING], r_cross[RING];
   int32_t r_code[RING], r_other[RING], r_seq[RING];
   int32_t gs[GS_CAP];
-  int16_t rowof[TAB_CAP];    // position -> sampled row, or -1
-  uint16_t inv[2][TAB_CAP];  // line index -> sorted position (clamped to 65535)
+  union {
+    struct {
+      int16_t rowof[TAB_CAP];    // position -> sampled row, or -1
+      uint16_t inv[2][TAB_CAP];  // line index -> sorted position (clamped to 65535)
+    } t;                         // n_total <= TAB_CAP
+    struct {
+      uint32_t bits[BM_WORDS];   // sampled positions (bit g)
+      int16_t rank[BM_WORDS];    // sampled positions before word w
+    } b;                         // larger n_total: position -> row by bitmap rank
+  } tab;
   int32_t hitq[G_THREADS / 32][64];  // per consumer warp: sampled rows of crossing cells awaiting a value
   double fold_w[32], fold_m[32];     // producer: the round's R-side weights / max cells
 };
@@ -313,15 +322,31 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
     for (int r = threadIdx.x; r < n_rows; r += blockDim.x) S.gs[r] = cells.pos(h, r);
   for (int i = threadIdx.x; i < RING; i += blockDim.x) S.r_seq[i] = 0;
   const bool tabs = n_total <= TAB_CAP && gs_smem;
+  const int bm_words = (n_total + 31) >> 5;
+  const bool bmap = !tabs && gs_smem && bm_words <= BM_WORDS;
   if (tabs) {
     for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
-      S.rowof[i] = -1;
-      S.inv[0][i] = static_cast<uint16_t>(min(L.inv[lb + i], 65535));
-      S.inv[1][i] = static_cast<uint16_t>(min(L.inv[lb + n_total + i], 65535));
+      S.tab.t.rowof[i] = -1;
+      S.tab.t.inv[0][i] = static_cast<uint16_t>(min(L.inv[lb + i], 65535));
+      S.tab.t.inv[1][i] = static_cast<uint16_t>(min(L.inv[lb + n_total + i], 65535));
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) S.rowof[S.gs[r]] = static_cast<int16_t>(r);
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) S.tab.t.rowof[S.gs[r]] = static_cast<int16_t>(r);
+  } else if (bmap) {
+    for (int w = threadIdx.x; w < bm_words; w += blockDim.x) S.tab.b.bits[w] = 0u;
+    __syncthreads();
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) atomicOr(&S.tab.b.bits[S.gs[r] >> 5], 1u << (S.gs[r] & 31));
+    __syncthreads();
+    // rank of word w = sampled rows before it = first row with position >= 32 w (rows are sorted)
+    for (int w = threadIdx.x; w < bm_words; w += blockDim.x)
+      S.tab.b.rank[w] = static_cast<int16_t>(lower_bound_dev(S.gs, n_rows, w << 5));
   }
+  // sampled row at position g (< n_total), or -1
+  auto row_at = [&](int g) -> int {
+    if (tabs) return S.tab.t.rowof[g];
+    const uint32_t wbits = S.tab.b.bits[g >> 5], bit = 1u << (g & 31);
+    return (wbits & bit) ? S.tab.b.rank[g >> 5] + __popc(wbits & (bit - 1u)) : -1;
+  };
   if (threadIdx.x == 0) {
     n_prod = 0;
     prod_done = 0;
@@ -707,30 +732,42 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
             __syncwarp();
           }
         };
-        if (tabs && n_other < n_rows - lo) {
+        if ((tabs || bmap) && n_other < n_rows - lo) {
           // walk the other kind's picked prefix: cell at g = idx + o if g is sampled
           for (int i0 = 0; i0 < n_other; i0 += 32) {
             const int i = i0 + lane;
             int o = -1;
             if (i < n_other) o = i < win ? S.idx[okind][i] : __ldg(L.idx + lb + static_cast<int64_t>(okind) * n_total + i);
             const int g = idx + o;
-            const int r = (o >= 0 && g < n_total) ? S.rowof[g] : -1;
+            const int r = (o >= 0 && g < n_total) ? row_at(g) : -1;
             push(r >= 0, r);
           }
         } else {
           // walk the sampled rows: the other line o = g - idx is picked iff its
           // sorted position is below the prefix length
           const int32_t *inv_o = is_vert ? inv_s : inv_v;
-          for (int r0 = lo; r0 < n_rows; r0 += 32) {
-            const int r = r0 + lane;
-            bool hit = false;
-            if (r < n_rows) {
-              const int g = gs_smem ? S.gs[r] : cells.pos(h, r);
-              const int o = g - idx;
-              const int pos = tabs ? static_cast<int>(S.inv[okind][o]) : __ldg(inv_o + o);
-              hit = pos < n_other;
+          if (tabs) {
+            for (int r0 = lo; r0 < n_rows; r0 += 32) {
+              const int r = r0 + lane;
+              bool hit = false;
+              if (r < n_rows) hit = static_cast<int>(S.tab.t.inv[okind][S.gs[r] - idx]) < n_other;
+              push(hit, r);
             }
-            push(hit, r);
+          } else {
+            // positions from L2: four independent loads per lane in flight
+            for (int r0 = lo; r0 < n_rows; r0 += 128) {
+              int pos[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int r = r0 + 32 * u + lane;
+                pos[u] = r < n_rows ? __ldg(inv_o + ((gs_smem ? S.gs[r] : cells.pos(h, r)) - idx)) : 0x7fffffff;
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (r0 + 32 * u >= n_rows) break;  // warp-uniform
+                push(pos[u] < n_other, r0 + 32 * u + lane);
+              }
+            }
           }
         }
         eval(qn);
