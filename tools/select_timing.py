@@ -1,5 +1,5 @@
 """K2/K3 device times at C2 turn 3 (4 layers) plus a
-plan digest so variants can be checked for identical output.
+plan digest so variants can be checked for identical output."""
 import hashlib
 import os
 import sys
