@@ -8,7 +8,9 @@
 // One CTA per (head, 128-row q tile), 10 warps:
 //   warp 8  (1 thread) TMA producer: every operand tile arrives by
 //           cp.async.bulk.tensor (128B swizzle, zero fill out of range) into a
-//           2-stage K/V ring; signals `full`, waits `empty`.
+//           3-stage K ring (a stage is free once S(i) has read it) and a
+//           2-stage V ring (free once PV(i) has read it); K runs one tile
+//           ahead of V, so S(i+1)'s operand is resident while P(i) is made.
 //   warp 9  (1 thread) MMA issuer: S(i) = Q K(i)^T into a double-buffered
 //           TMEM S, then O += P(i-1) V(i-1) into a TMEM O accumulator
 //           (tcgen05.mma kind::f16, bf16 -> fp32), commits to mbarriers.
@@ -41,10 +43,15 @@ namespace k5ws {
 
 constexpr int BM = 128, BN = 128;
 constexpr int N_SOFT = 256;           // softmax threads (8 warps)
-constexpr int THREADS = N_SOFT + 64;  // + producer warp + MMA warp
+constexpr int THREADS = N_SOFT + 128;  // + warpgroup 2: producer warp, MMA warp, two idle warps
+constexpr int REGS_SOFT = 224, REGS_CTRL = 56;  // setmaxnreg split: 8 x 232 + 4 x 40 warps' registers <= 64K
 constexpr int MAX_KB = 2048;
 constexpr int DENSE_SLASHES = 3;
 constexpr float RESCALE_LOG2 = 8.f;  // lazy rescale threshold (factor 256)
+constexpr int KST = 3, VST = 2;      // K / V ring stages
+#ifndef LS_K5_POLY
+#define LS_K5_POLY 0
+#endif
 
 struct Params {
   const int32_t *slash_ids, *vert_ids, *counts;
@@ -80,16 +87,16 @@ struct Smem {
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = Q_BYTES;                 // 2 stages
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;    // 2 stages
-  static constexpr int OFF_MISC = OFF_V + 2 * KV_BYTES;  // (P lives in TMEM, aliasing its S buffer)
+  static constexpr int OFF_K = Q_BYTES;                   // KST stages
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;    // VST stages
+  static constexpr int OFF_MISC = OFF_V + VST * KV_BYTES;  // (P lives in TMEM, aliasing its S buffer)
   // misc: barriers 256 | ints 256 | kb_bits 256 | pmax 1024 | pd 1024 | lx 512 | gcols 1024 | dense_list 4096 | blk_cnt 8192
   static constexpr int MISC_BYTES = 256 + 256 + 256 + 1024 + 1024 + 512 + 1024 + MAX_KB * 2 + MAX_KB * 4;
   static constexpr int TOTAL = OFF_MISC + MISC_BYTES + 1024;
 };
 
 struct Bars {
-  uint64_t full[2], empty[2], s_full[2], p_full[2], pv_done[2], q_full;
+  uint64_t kfull[KST], kempty[KST], vfull[VST], vempty[VST], s_full[2], p_full[2], pv_done[2], q_full;
 };
 
 __device__ __forceinline__ bool bit_of(const uint32_t *b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
@@ -102,6 +109,16 @@ __device__ __forceinline__ void bit_window(const uint32_t *bits, int s, uint32_t
 #pragma unroll
   for (int i = 0; i < 2; ++i) w[i] = __funnelshift_r(x[i], x[i + 1], sh);
   (void)n;
+}
+
+// 128 bits of `bits` starting at bit s (s >= 0)
+__device__ __forceinline__ void bit_window4(const uint32_t *bits, int s, uint32_t *w) {
+  const int w0 = s >> 5, sh = s & 31;
+  uint32_t x[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) x[i] = __ldg(bits + w0 + i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = __funnelshift_r(x[i], x[i + 1], sh);
 }
 
 template <int D>
@@ -119,7 +136,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t *kb_bits = reinterpret_cast<uint32_t *>(misc + 512);        // [64]
   float *pmax = reinterpret_cast<float *>(misc + 768);                 // [2][128]
   float *pd = reinterpret_cast<float *>(misc + 1792);                  // [2][128]
-  float *lx = reinterpret_cast<float *>(misc + 2816);                  // [128]
   int *gcols = reinterpret_cast<int *>(misc + 3328);                   // [2][128]
   int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 4352);      // [MAX_KB]
   int *blk_cnt = reinterpret_cast<int *>(misc + 4352 + MAX_KB * 2);   // [MAX_KB] slash counts, then window starts
@@ -139,11 +155,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) tc::tmem_alloc(tmem_sh, 512);
   if (tid == 0) {
+    for (int s = 0; s < KST; ++s) {
+      tc::mbar_init(&bars->kfull[s], 1);
+      tc::mbar_init(&bars->kempty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      tc::mbar_init(&bars->vfull[s], 1);
+      tc::mbar_init(&bars->vempty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&bars->full[s], 1);
-      tc::mbar_init(&bars->empty[s], 1);
       tc::mbar_init(&bars->s_full[s], 1);
-      tc::mbar_init(&bars->p_full[s], 1);
+      tc::mbar_init(&bars->p_full[s], 4);  // one arrival per softmax warp of the tile's warpgroup
       tc::mbar_init(&bars->pv_done[s], 1);
     }
     tc::mbar_init(&bars->q_full, 1);
@@ -258,6 +280,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_sh;
   const uint32_t tmem_o = tmem + 256;
 
+  if (warp >= 8) {
+  tc::setmaxnreg_dec<REGS_CTRL>();
   if (warp == 8) {
     // =================================================== TMA producer
     if (lane == 0) {
@@ -270,27 +294,33 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int a = 0; a < D / 64; ++a)
         tc::tma_load_3d(tc::smem_u32(smem + L::OFF_Q + a * BM * 128), &tm_q, &bars->q_full, a * 64, r0, h);
-      for (int t = 0; t < n_all; ++t) {
-        const int s = t & 1;
-        KDBG(0, t, 1);
-        tc::mbar_wait(&bars->empty[s], ((t >> 1) & 1) ^ 1);
-        tc::mbar_expect_tx(&bars->full[s], 2 * L::KV_BYTES);
-        const CUtensorMap *mk, *mv;
-        int row, hh;
+      // tile t's operand rows: (tensor map, row, head)
+      auto src = [&](int t, bool v, const CUtensorMap *&m, int &row, int &hh) {
         if (t < n_dense) {
-          mk = &tm_k, mv = &tm_v, row = dense_list[t] * BN, hh = kv;
+          m = v ? &tm_v : &tm_k, row = dense_list[t] * BN, hh = kv;
         } else if (t < n_tc) {
-          mk = &tm_kc, mv = &tm_vc, row = (t - n_dense) * BN, hh = h;
+          m = v ? &tm_vc : &tm_kc, row = (t - n_dense) * BN, hh = h;
         } else {  // window start (>= 0)
-          mk = &tm_k, mv = &tm_v, row = wins[t - n_tc], hh = kv;
+          m = v ? &tm_v : &tm_k, row = wins[t - n_tc], hh = kv;
         }
-        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
-        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + s * L::KV_BYTES);
+      };
+      auto load = [&](int t, bool v) {
+        const int st = v ? t % VST : t % KST, nst = v ? VST : KST;
+        uint64_t *fullb = v ? &bars->vfull[st] : &bars->kfull[st];
+        KDBG(0, t, v ? 11 : 1);
+        tc::mbar_wait(v ? &bars->vempty[st] : &bars->kempty[st], ((t / nst) & 1) ^ 1);
+        tc::mbar_expect_tx(fullb, L::KV_BYTES);
+        const CUtensorMap *m;
+        int row, hh;
+        src(t, v, m, row, hh);
+        const uint32_t dst = tc::smem_u32(smem + (v ? L::OFF_V : L::OFF_K) + st * L::KV_BYTES);
 #pragma unroll
-        for (int a = 0; a < D / 64; ++a) {
-          tc::tma_load_3d(ks + a * BN * 128, mk, &bars->full[s], a * 64, row, hh);
-          tc::tma_load_3d(vs + a * BN * 128, mv, &bars->full[s], a * 64, row, hh);
-        }
+        for (int a = 0; a < D / 64; ++a) tc::tma_load_3d(dst + a * BN * 128, m, fullb, a * 64, row, hh);
+      };
+      if (n_all > 0) load(0, false);
+      for (int t = 0; t < n_all; ++t) {
+        if (t + 1 < n_all) load(t + 1, false);  // K one tile ahead of V
+        load(t, true);
       }
     }
   } else if (warp == 9) {
@@ -304,25 +334,27 @@ __global__ void __launch_bounds__(THREADS, 1)
       auto issue_pv = [&](int j) {  // O += P(j) V(j), P(j) bf16 in TMEM over S(j)
         KDBG(1, j, 3);
         tc::mbar_wait(&bars->p_full[j & 1], (j >> 1) & 1);
+        tc::mbar_wait(&bars->vfull[j % VST], (j / VST) & 1);
         tc::fence_after_sync();
-        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (j & 1) * L::KV_BYTES);
+        const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (j % VST) * L::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
           const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
-          tc::mma_bf16_ts(tmem_o, tmem + (j & 1) * 128 + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_bf16_ts(tmem_o + (j & 1) * D, tmem + (j & 1) * 128 + kk * 8, bd, IDESC_O,
+                          (j > 1 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(&bars->pv_done[j & 1]);
-        tc::mma_commit(&bars->empty[j & 1]);
+        tc::mma_commit(&bars->vempty[j % VST]);
       };
       // S(i) may overwrite P(i-2) in its buffer: PV(i-2) was issued before it
       // and the tensor pipe executes one thread's MMAs in order
       for (int i = 0; i < n_all; ++i) {
         const int s = i & 1;
         KDBG(1, i, 4);
-        tc::mbar_wait(&bars->full[s], (i >> 1) & 1);
+        tc::mbar_wait(&bars->kfull[i % KST], (i / KST) & 1);
         KDBG(1, i, 5);
         tc::fence_after_sync();
-        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + s * L::KV_BYTES);
+        const uint32_t ks = tc::smem_u32(smem + L::OFF_K + (i % KST) * L::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint64_t ad = tc::make_desc(qs + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
@@ -330,59 +362,69 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::mma_bf16(tmem + s * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
         }
         tc::mma_commit(&bars->s_full[s]);
+        tc::mma_commit(&bars->kempty[i % KST]);
         if (i > 0) issue_pv(i - 1);
       }
       if (n_all > 0) issue_pv(n_all - 1);
     }
+  }
   } else {
+    tc::setmaxnreg_inc<REGS_SOFT>();
     // =================================================== softmax warps
+    // Warpgroup wg (warps 4 wg .. 4 wg + 3) owns the tiles i with i % 2 == wg:
+    // its own online softmax (m_ref, l) and its own TMEM O accumulator O_wg,
+    // one thread per row over all 128 columns of a tile. The two warpgroups
+    // work on consecutive tiles at the same time with no exchange per tile
+    // (the MMA warp interleaves their S and PV); the partial (m, l, O) pairs are
+    // merged once in the epilogue.
     const int wg = warp >> 2;
     const int row = (warp & 3) * 32 + lane;
     const int my_g = g0 + row;
     const bool row_ok = row < nr;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     float m_ref = -INFINITY, l = 0.f;
-    long long my_cells = 0;
-    for (int i = 0; i < n_all; ++i) {
-      const int s = i & 1;
+    int my_cells = 0;
+    for (int i = wg; i < n_all; i += 2) {
+      const int s = i & 1;  // == wg
       const bool gathered = i >= n_dense && i < n_tc;
-      uint32_t mk[2];
+      uint32_t mk[4];
       if (i >= n_tc) {  // window: slash cells outside dense blocks and verticals
-        const int c0 = wins[i - n_tc] + wg * 64;
+        const int c0 = wins[i - n_tc];
         if (!row_ok) {
-          mk[0] = mk[1] = 0u;
+          mk[0] = mk[1] = mk[2] = mk[3] = 0u;
         } else {
-          uint32_t sw[2], vw[2];
-          bit_window(rsbits, p.n_total - 1 - my_g + c0, sw, 2);
-          bit_window(vbits, c0, vw, 2);
-          // columns of this thread's 64 that fall in dense blocks
-          const int b1 = c0 / BN, split = (b1 + 1) * BN - c0;  // columns [0, split) in block b1
-          const uint64_t lo_mask = split >= 64 ? ~0ull : ((1ull << split) - 1ull);
-          uint64_t dm = 0ull;
-          if (bit_of(kb_bits, b1)) dm |= lo_mask;
-          if (split < 64 && b1 + 1 < MAX_KB && bit_of(kb_bits, b1 + 1)) dm |= ~lo_mask;
+          uint32_t sw[4], vw[4];
+          bit_window4(rsbits, p.n_total - 1 - my_g + c0, sw);
+          bit_window4(vbits, c0, vw);
+          // columns of the window in dense blocks: [0, split) in block b1, the rest in b1 + 1
+          const int b1 = c0 / BN, split = (b1 + 1) * BN - c0;
+          const bool d1 = bit_of(kb_bits, b1), d2 = split < BN && b1 + 1 < MAX_KB && bit_of(kb_bits, b1 + 1);
           const int lim = my_g - c0;
 #pragma unroll
-          for (int t = 0; t < 2; ++t) {
+          for (int t = 0; t < 4; ++t) {
+            const int sp = split - 32 * t;
+            const uint32_t below = sp >= 32 ? 0xffffffffu : (sp <= 0 ? 0u : ((1u << sp) - 1u));
+            const uint32_t dm = (d1 ? below : 0u) | (d2 ? ~below : 0u);
             const int hi = lim - 32 * t;
             const uint32_t causal = hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u));
-            mk[t] = sw[t] & ~vw[t] & ~static_cast<uint32_t>(dm >> (32 * t)) & causal;
+            mk[t] = sw[t] & ~vw[t] & ~dm & causal;
           }
         }
       } else if (gathered) {
         // stage this tile's 128 vertical columns (sorted ascending) and the
         // tile-wide mask of columns outside dense blocks; a row's causal part
         // is then a prefix: columns <= g
-        uint32_t *cm = reinterpret_cast<uint32_t *>(pd) + s * 4;
-        if (wg == 0) {
+        uint32_t *cm = reinterpret_cast<uint32_t *>(pd) + wg * 4;
+        int *gc = gcols + wg * BN;
+        tc::named_sync(2 + wg, 128);  // the previous gathered tile's reads are done
+        {
           const int idx = (i - n_dense) * BN + row;
           const int c = idx < v_end ? Vl[idx] : 0x7fffffff;
-          gcols[s * BN + row] = c;
+          gc[row] = c;
           const unsigned b = __ballot_sync(0xffffffffu, c != 0x7fffffff && !bit_of(kb_bits, c / BN));
           if (lane == 0) cm[warp & 3] = b;
         }
-        tc::named_sync(1, N_SOFT);
-        const int *gc = gcols + s * BN;
+        tc::named_sync(2 + wg, 128);
         int n_le;  // gathered columns <= my_g
         if (gc[BN - 1] <= g0) {
           n_le = BN;
@@ -395,42 +437,45 @@ __global__ void __launch_bounds__(THREADS, 1)
           n_le = lo;
         }
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int hi = n_le - (wg * 64 + t * 32);  // columns of this word below n_le
+        for (int t = 0; t < 4; ++t) {
+          const int hi = n_le - 32 * t;  // columns of this word below n_le
           const uint32_t causal = hi >= 32 ? 0xffffffffu : (hi <= 0 ? 0u : ((1u << hi) - 1u));
-          mk[t] = row_ok ? (cm[wg * 2 + t] & causal) : 0u;
+          mk[t] = row_ok ? (cm[t] & causal) : 0u;
         }
       } else {
-        const int c0 = dense_list[i] * BN + wg * 64;
+        const int c0 = dense_list[i] * BN;
         const int lim = my_g - c0;
         if (p.dense || !row_ok) {
-          mk[0] = mk[1] = 0xffffffffu;  // (rows past the block are cleared below)
+          mk[0] = mk[1] = mk[2] = mk[3] = 0xffffffffu;  // (rows past the block are cleared below)
         } else {
-          uint32_t sw[2];
-          bit_window(rsbits, p.n_total - 1 - my_g + c0, sw, 2);
+          uint32_t sw[4];
+          bit_window4(rsbits, p.n_total - 1 - my_g + c0, sw);
 #pragma unroll
-          for (int t = 0; t < 2; ++t) mk[t] = ((c0 / 32 + t < p.words) ? __ldg(vbits + c0 / 32 + t) : 0u) | sw[t];
+          for (int t = 0; t < 4; ++t) mk[t] = ((c0 / 32 + t < p.words) ? __ldg(vbits + c0 / 32 + t) : 0u) | sw[t];
         }
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < 4; ++t) {
           const int hi = lim - 32 * t;
           mk[t] &= (!row_ok) ? 0u : (hi >= 31 ? 0xffffffffu : (hi < 0 ? 0u : ((2u << hi) - 1u)));
         }
       }
-      my_cells += __popc(mk[0]) + __popc(mk[1]);
+      my_cells += __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
       if (tid == 0) KDBG(2, i, 6);
       tc::mbar_wait(&bars->s_full[s], (i >> 1) & 1);
       tc::fence_after_sync();
-      const uint32_t s_addr = tmem + s * 128 + lane_base + wg * 64;
-      float tmax = -INFINITY;
-      float sv[2][32];
-      bool live[2];
+      const uint32_t s_addr = tmem + s * 128 + lane_base;
+      float sv[4][32];
+      bool live[4];
 #pragma unroll
-      for (int cch = 0; cch < 2; ++cch) {
+      for (int cch = 0; cch < 4; ++cch) {
         live[cch] = __any_sync(0xffffffffu, mk[cch] != 0u);  // warp-uniform: TMEM loads are .sync.aligned
+        if (live[cch]) tc::tmem_ld32(s_addr + cch * 32, sv[cch]);
+      }
+      tc::tmem_wait_ld();
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int cch = 0; cch < 4; ++cch) {
         if (live[cch]) {
-          tc::tmem_ld32(s_addr + cch * 32, sv[cch]);
-          tc::tmem_wait_ld();
           // masked cells become -inf once; max and exp then run unmasked
           // (exp2(-inf) = 0); whole-chunk-valid rows skip the masking
           const uint32_t m = mk[cch];
@@ -442,86 +487,100 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, sv[cch][j]);
         }
       }
-      pmax[wg * BM + row] = tmax;
-      tc::named_sync(1, N_SOFT);
-      const float tm = fmaxf(pmax[row], pmax[BM + row]);
-      const float m_tile = tm == -INFINITY ? -INFINITY : tm * p.scale_log2;
+      const float m_tile = tmax == -INFINITY ? -INFINITY : tmax * p.scale_log2;
       const bool need = m_tile > m_ref + RESCALE_LOG2;
-      // TMEM ld/st are .sync.aligned: the whole warp rescales if any row needs it,
-      // after PV(i-1) has landed in O (PV(i) waits for this tile's p_full)
-      if (__any_sync(0xffffffffu, need && m_ref != -INFINITY && i > 0)) {
-        if (tid == 0) KDBG(2, i, 7);
-        tc::mbar_wait(&bars->pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
-        tc::fence_after_sync();
-        const float corr = (need && m_ref != -INFINITY) ? fast_exp2(m_ref - m_tile) : 1.f;
-#pragma unroll
-        for (int cch = 0; cch < DH / 32; ++cch) {
-          float ov[32];
-          tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) ov[j] *= corr;
-          tc::tmem_st32(tmem_o + lane_base + wg * DH + cch * 32, ov);
-        }
-        tc::tmem_wait_st();
-      }
-      if (need) {
-        if (m_ref != -INFINITY) l *= fast_exp2(m_ref - m_tile);
-        m_ref = m_tile;
-      }
+      const float m_old = m_ref;
+      if (need) m_ref = m_tile;
       float lsum = 0.f;
-      uint32_t pk[32];  // this thread's 64 bf16 of P(i): TMEM columns s*128 + wg*32 + [0, 32)
 #pragma unroll
-      for (int cch = 0; cch < 2; ++cch) {
+      for (int cch = 0; cch < 4; ++cch) {
+        uint32_t pk[16];  // P(i) columns [32 cch, +32) as bf16 pairs: TMEM columns s * 128 + 16 cch + [0, 16)
         // a row with no valid cell so far (m_ref = -inf) has P = 0 (and no NaN)
         if (live[cch] && m_ref != -INFINITY) {
           const float nm = -m_ref;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const float a = fast_exp2(fmaf(sv[cch][j], p.scale_log2, nm));
-            const float b = fast_exp2(fmaf(sv[cch][j + 1], p.scale_log2, nm));
+            // LS_K5_POLY: share of the exponentials on the FMA pipe (FA4 split)
+            const float xb = fmaf(sv[cch][j + 1], p.scale_log2, nm);
+            const float b = (LS_K5_POLY == 2 || (LS_K5_POLY == 1 && (j & 2))) ? poly_exp2(xb) : fast_exp2(xb);
             lsum += a + b;
-            pk[cch * 16 + (j >> 1)] = tc::pack_bf16(a, b);
+            pk[j >> 1] = tc::pack_bf16(a, b);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) pk[cch * 16 + j] = 0u;
+          for (int j = 0; j < 16; ++j) pk[j] = 0u;
         }
+        // (every S read of this tile finished at the wait::ld above)
+        tc::tmem_st16(s_addr + cch * 16, pk);
       }
-      // (every S read of this tile finished before the max exchange barrier)
-      tc::tmem_st32(tmem + s * 128 + lane_base + wg * 32, reinterpret_cast<const float *>(pk));
       tc::tmem_wait_st();
+      // O_wg relative to the new reference before PV(i) adds P(i) (P is already
+      // stored; TMEM ld/st are .sync.aligned: the whole warp rescales if any row
+      // needs it), after this warpgroup's previous PV (i - 2) has landed in O_wg
+      if (__any_sync(0xffffffffu, need && m_old != -INFINITY && i >= 2)) {
+        if (tid == 0) KDBG(2, i, 7);
+        tc::mbar_wait(&bars->pv_done[s], ((i - 2) >> 1) & 1);
+        tc::fence_after_sync();
+        const float corr = (need && m_old != -INFINITY) ? fast_exp2(m_old - m_tile) : 1.f;
+#pragma unroll
+        for (int cch = 0; cch < D / 32; ++cch) {
+          float ov[32];
+          tc::tmem_ld32(tmem_o + wg * D + lane_base + cch * 32, ov);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) ov[j] *= corr;
+          tc::tmem_st32(tmem_o + wg * D + lane_base + cch * 32, ov);
+        }
+        tc::tmem_wait_st();
+      }
+      if (need && m_old != -INFINITY) l *= fast_exp2(m_old - m_tile);
       l += lsum;
       tc::fence_before_sync();
-      tc::named_sync(1, N_SOFT);
-      if (tid == 0) tc::mbar_arrive(&bars->p_full[s]);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bars->p_full[s]);  // one arrival per warp of the group
     }
-    // O (TMEM) -> registers, relative to m_ref
+    // ---- epilogue: merge the two warpgroups' (m, l, O) per row
+    float *mx = pmax;  // [2][128]
+    float *lx2 = pd;   // [2][128] (the gathered-tile staging is done)
+    tc::named_sync(1, N_SOFT);  // every staging read of pd is done
+    mx[wg * BM + row] = m_ref;
+    lx2[wg * BM + row] = l;
+    // the last PV of each warpgroup has landed in its O
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int last = n_all - 1 - ((n_all - 1 - b) & 1);  // last tile i < n_all with i % 2 == b
+      if (last >= 0 && last % 2 == b) tc::mbar_wait(&bars->pv_done[b], (last >> 1) & 1);
+    }
+    tc::fence_after_sync();
+    tc::named_sync(1, N_SOFT);
+    const float m0 = mx[row], m1 = mx[BM + row];
+    const float mm = fmaxf(m0, m1);
+    const bool has0 = n_all > 0 && m0 != -INFINITY, has1 = n_all > 1 && m1 != -INFINITY;
+    const float f0 = has0 ? fast_exp2(m0 - mm) : 0.f, f1 = has1 ? fast_exp2(m1 - mm) : 0.f;
+    const float l_all = lx2[row] * f0 + lx2[BM + row] * f1;
+    // this thread writes output columns [wg * DH, wg * DH + DH) of its row
     float o[DH];
-    if (n_all > 0) {
-      if (tid == 0) KDBG(2, n_all, 8);
-      tc::mbar_wait(&bars->pv_done[(n_all - 1) & 1], ((n_all - 1) >> 1) & 1);
-      tc::fence_after_sync();
 #pragma unroll
-      for (int cch = 0; cch < DH / 32; ++cch) {
-        float ov[32];
-        tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
-        tc::tmem_wait_ld();
+    for (int j = 0; j < DH; ++j) o[j] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) o[cch * 32 + j] = ov[j];
+    for (int b = 0; b < 2; ++b) {
+      if (__any_sync(0xffffffffu, b == 0 ? has0 : has1)) {
+        const float f = b == 0 ? f0 : f1;
+#pragma unroll
+        for (int cch = 0; cch < DH / 32; ++cch) {
+          float ov[32];
+          tc::tmem_ld32(tmem_o + b * D + lane_base + wg * DH + cch * 32, ov);
+          tc::tmem_wait_ld();
+          if (f != 0.f) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[cch * 32 + j] = fmaf(ov[j], f, o[cch * 32 + j]);
+          }
+        }
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < DH; ++j) o[j] = 0.f;
     }
-    // ---- epilogue: both halves agree on m_ref; l = l(wg0) + l(wg1)
-    if (wg == 1) lx[row] = l;
-    tc::named_sync(1, N_SOFT);
-    if (wg == 0) lx[row] = l + lx[row];
-    tc::named_sync(1, N_SOFT);
-    const float l_all = lx[row];
     if (row_ok && wg == 0 && p.row_lse)  // plan-cell mass of the row on the log2 scale (ls_plan_coverage)
-      p.row_lse[static_cast<int64_t>(h) * p.n_new + r0 + row] = l_all > 0.f ? m_ref + __log2f(l_all) : -INFINITY;
+      p.row_lse[static_cast<int64_t>(h) * p.n_new + r0 + row] = l_all > 0.f ? mm + __log2f(l_all) : -INFINITY;
     if (row_ok) {
       const int64_t orow = static_cast<int64_t>(r0 + row) * p.out_row_stride + static_cast<int64_t>(h) * D + wg * DH;
       if (l_all > 0.f) {
@@ -551,7 +610,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (wg == 0) my_cells += 1;
       }
     }
-    const long long cs = warp_sum_ll(my_cells);
+    const long long cs = warp_sum_ll(static_cast<long long>(my_cells));
     if (lane == 0 && cs)
       atomicAdd(reinterpret_cast<unsigned long long *>(p.cells + h), static_cast<unsigned long long>(cs));
     if (tid == 0 && p.tiles && n_all)

@@ -17,15 +17,19 @@ if CFG == "c2":
 else:  # c3 turn 4
     shape, cap, ro, n_new, t = AttnShape(4, 32, 8, 128), 4 * 8448, 25088, 8448, 3
 store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1)
-eng = SessionEngine(shape, SessionParams(alpha=0.955, comp=CompressionConfig(1024, 16, 16), max_new=128), cap)
+mode = "dense" if os.environ.get("DENSE") else "loopserve"
+eng = SessionEngine(shape, SessionParams(mode=mode, alpha=0.955, comp=CompressionConfig(1024, 16, 16), max_new=128), cap)
 for _ in range(2):
     res = eng.prefill(store, t, ro, n_new)
 torch.cuda.synchronize()
 h = hashlib.sha1()
-for p in res.plans:
+for p in (x for x in res.plans if x is not None):
     h.update(p.counts.cpu().numpy().tobytes())
     h.update(p.slash_ids.cpu().numpy().tobytes())
     h.update(p.vert_ids.cpu().numpy().tobytes())
+ho = hashlib.sha1()
+for o in res.out:
+    ho.update(o.float().cpu().numpy().tobytes())
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     eng.prefill(store, t, ro, n_new)
     torch.cuda.synchronize()
@@ -33,7 +37,7 @@ agg = {}
 for e in prof.events():
     if e.device_type.name == "CUDA":
         agg.setdefault(e.name[:60], []).append(e.device_time_total)
-print(f"LS_K2_MODE={os.environ.get('LS_K2_MODE', '0')} {CFG} plans sha1 {h.hexdigest()[:16]}")
+print(f"{os.environ.get('LS_LIB_PATH', 'lib')} {CFG} {mode} plans sha1 {h.hexdigest()[:16]} out sha1 {ho.hexdigest()[:16]}")
 tot = 0.0
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))[:16]:
     print(f"  {sum(v) / 1e3 / shape.n_layers:8.3f} ms/layer {len(v):4d} x  {k}")
