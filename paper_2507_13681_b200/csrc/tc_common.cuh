@@ -90,16 +90,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
   return ok != 0;
 }
 
-// Waits for phase `parity` of an mbarrier; traps after ~10 s so a pipeline
-// bug surfaces as a launch error instead of a hung device.
+// Waits for phase `parity` of an mbarrier (try_wait suspends the thread for a
+// hardware time slice per probe, so the loop costs few issue slots). Debug
+// builds (-DLS_WATCHDOG=1) trap after ~10 s so a pipeline bug surfaces as a
+// launch error instead of a hung device; release builds carry no clock reads
+// in the spin loop (they cost issue slots the softmax warps need).
+#ifndef LS_WATCHDOG
+#define LS_WATCHDOG 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
   if (mbar_try_wait(a, parity)) return;
+#if LS_WATCHDOG
   const long long t0 = clock64();
   for (uint32_t k = 1;; ++k) {
     if (mbar_try_wait(a, parity)) return;
     if ((k & 255) == 0 && clock64() - t0 > 20000000000LL) __trap();
   }
+#else
+  while (!mbar_try_wait(a, parity)) {
+  }
+#endif
 }
 
 // ------------------------------------------------------------ TMEM
