@@ -30,6 +30,7 @@
 
 #include <algorithm>
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ls_common.cuh"
@@ -41,6 +42,8 @@ namespace sel {
 constexpr double EPS = 1e-12;   // prefill.py:188
 
 struct Lists {  // sorted lines, [H][2][n] (kind 0 = slash, 1 = vertical)
+  int32_t *sorted;    // [H][2] length of the sorted prefix (nullptr: every list fully sorted)
+  int32_t *overflow;  // [H] set by K3 when it needs a line past a sorted prefix
   int32_t *idx;
   int32_t *inv;     // line index -> position in its sorted list
   double *w;
@@ -117,6 +120,257 @@ __global__ void sort_scatter_kernel(const unsigned long long *keys_sorted, const
   }
   (void)keys_sorted;
   (void)H;
+}
+
+// K2 for lists of at most 16384 lines (every C2 / C4 turn): the greedy consumes
+// only a prefix of each sorted list (picks of one kind), so one CTA per
+// (kind, head) finds the PMIN..PCAP best lines by an MSD radix select on the
+// same fixed-point keys (2^fix_bits - 1 - w * 2^40: ascending = weight
+// descending), sorts just those by (key, index) -- the order of the full stable
+// sort -- and marks the rest unsorted (inv = INT_MAX, sorted[h][kind] = P). A
+// list with at most PCAP lines is sorted whole. K3 flags a head whose walk would
+// leave a sorted prefix; the fallback pair (sort_block_kernel + greedy on the
+// flagged heads only) then redoes that head on fully sorted lists, and exits at
+// once for every other head.
+constexpr int PCAP = 4096;   // prefix capacity (bitonic sort in shared memory)
+constexpr int PMIN = 3072;   // at least this many lines (or the whole list) in a prefix
+constexpr int PS_THREADS = 1024;
+constexpr int PS_ITEMS = 16;  // lines per thread in index order (n_total <= 16384)
+constexpr int PS_MAXN = PS_THREADS * PS_ITEMS;
+constexpr int PS_BINS = 4096;
+inline size_t prefix_sort_smem(int n_s) {
+  return PCAP * 12 + PS_BINS * 4 + 256 + (n_s <= kScatterShRows ? 4 * static_cast<size_t>(n_s) : 0);
+}
+
+// block exclusive scan of one int per thread (1024 threads); returns the total
+__device__ __forceinline__ int block_scan_excl(int v, int &excl, int *warp_sums) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  int before = 0, all = 0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+    const int x = warp_sums[w];
+    if (w < wid) before += x;
+    all += x;
+  }
+  excl = before + incl - v;
+  return all;
+}
+
+template <typename MaxT>
+__global__ void __launch_bounds__(PS_THREADS, 1)
+    sort_prefix_kernel(const double *v_w, const MaxT *v_max, const double *s_w, const MaxT *s_max,
+                       const int32_t *rows, int n_s, int n_total, int row_offset, int fix_bits, Lists out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long *skey = reinterpret_cast<unsigned long long *>(smem_raw);  // [PCAP]
+  int *sidx = reinterpret_cast<int *>(smem_raw + PCAP * 8);                     // [PCAP]
+  int *hist = reinterpret_cast<int *>(smem_raw + PCAP * 12);                    // [PS_BINS]
+  int *red = hist + PS_BINS;                                                     // [64] scan / select scratch
+  int *pos_sh = red + 64;
+  const int kind = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const double *w = (kind == 0 ? s_w : v_w) + static_cast<int64_t>(h) * n_total;
+  const MaxT *mx = (kind == 0 ? s_max : v_max) + static_cast<int64_t>(h) * n_total;
+  const int32_t *rows_h = rows + static_cast<int64_t>(h) * n_s;
+  const bool in_sh = n_s <= kScatterShRows;
+  if (in_sh)
+    for (int r = tid; r < n_s; r += PS_THREADS) pos_sh[r] = rows_h[r];
+  const int32_t *pos = in_sh ? pos_sh : rows_h;
+  if (kind == 0 && tid == 0) out.overflow[h] = 0;
+  // select / sort key: the inverted fp64 bits of the weight (weights are exact
+  // multiples of 2^-40, non-negative: bit order = value order = the fixed-point
+  // order of the full sort); ascending key = weight descending, ties by index
+  unsigned long long key[PS_ITEMS];
+#pragma unroll
+  for (int i = 0; i < PS_ITEMS; ++i) {
+    const int idx = tid * PS_ITEMS + i;
+    key[i] = idx < n_total ? ~static_cast<unsigned long long>(__double_as_longlong(w[idx])) : 0ull;
+  }
+  const int n_mine = max(0, min(PS_ITEMS, n_total - tid * PS_ITEMS));  // valid items of this thread
+  // ---- MSD radix select (12-bit digits, warp-aggregated histograms, block scans):
+  // selection = keys < thr, plus the first `take_eq` lines (index order) with key ==
+  // eq_key when a run of equal weights straddles the prefix end
+  unsigned long long thr = ~0ull, eq_key = 0ull;
+  bool sel_all = n_total <= PCAP;
+  int take_eq = 0;
+  if (!sel_all) {
+    unsigned long long hi_val = 0ull;  // the candidates' key bits above `hi`
+    int hi = 64, before = 0;
+    while (true) {
+      const int lo = max(0, hi - 12), nb = 1 << (hi - lo);
+      for (int b = tid; b < PS_BINS; b += PS_THREADS) hist[b] = 0;
+      __syncthreads();
+      const unsigned long long hmask = hi >= 64 ? 0ull : ~((1ull << hi) - 1ull);
+#pragma unroll
+      for (int i = 0; i < PS_ITEMS; ++i) {
+        const bool cand = i < n_mine && (key[i] & hmask) == (hi >= 64 ? 0ull : (hi_val << hi));
+        const int bin = cand ? static_cast<int>((key[i] >> lo) & static_cast<unsigned long long>(nb - 1)) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, bin);
+        if (cand && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&hist[bin], __popc(grp));
+      }
+      __syncthreads();
+      // first bin where the running count reaches PMIN (4 bins per thread, block scan)
+      int loc = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) loc += hist[tid * 4 + e];
+      int excl;
+      block_scan_excl(loc, excl, red);
+      int c = before + excl;
+      if (c < PMIN && c + loc >= PMIN) {
+        int b = tid * 4;
+        while (c + hist[b] < PMIN) c += hist[b++];
+        red[32] = b;
+        red[33] = c;
+      }
+      __syncthreads();
+      const int b = red[32];
+      c = red[33];
+      const int cnt = hist[b];
+      __syncthreads();
+      const unsigned long long binv = (hi_val << (hi - lo)) | static_cast<unsigned long long>(b);
+      if (c + cnt <= PCAP) {  // every candidate up to the end of bin b
+        const unsigned long long nxt = binv + 1ull;
+        if (lo > 0 ? (nxt >> (64 - lo)) != 0ull : nxt == 0ull)
+          sel_all = true;  // bin b ends the key space
+        else
+          thr = nxt << lo;
+        break;
+      }
+      if (lo == 0) {  // cnt lines of exactly this key: take the first PCAP - c of them
+        thr = binv;
+        eq_key = binv;
+        take_eq = PCAP - c;
+        break;
+      }
+      before = c;
+      hi_val = binv;
+      hi = lo;
+    }
+  }
+  // ---- compaction in index order
+  int mine = 0, mine_eq = 0;
+#pragma unroll
+  for (int i = 0; i < PS_ITEMS; ++i) {
+    mine += (i < n_mine && (sel_all || key[i] < thr)) ? 1 : 0;
+    mine_eq += (i < n_mine && take_eq > 0 && key[i] == eq_key) ? 1 : 0;
+  }
+  int off, off_eq = 0;
+  const int n_lt = block_scan_excl(mine, off, red);
+  if (take_eq > 0) block_scan_excl(mine_eq, off_eq, red);
+  const int P = take_eq > 0 ? PCAP : n_lt;
+#pragma unroll
+  for (int i = 0; i < PS_ITEMS; ++i) {
+    const int idx = tid * PS_ITEMS + i;
+    if (i >= n_mine) continue;
+    if (sel_all || key[i] < thr) {
+      skey[off] = key[i];
+      sidx[off] = idx;
+      ++off;
+    } else if (take_eq > 0 && key[i] == eq_key) {
+      if (off_eq < take_eq) {
+        skey[n_lt + off_eq] = key[i];
+        sidx[n_lt + off_eq] = idx;
+      }
+      ++off_eq;
+    }
+  }
+  int P2 = 1;
+  while (P2 < P) P2 <<= 1;
+  for (int i = P + tid; i < P2; i += PS_THREADS) {
+    skey[i] = ~0ull;
+    sidx[i] = 0x7fffffff;
+  }
+  // every line starts unsorted (K3 reads inv < picks-of-that-kind as "picked")
+  const int64_t base = (static_cast<int64_t>(h) * 2 + kind) * n_total;
+  for (int i = tid; i < n_total; i += PS_THREADS) out.inv[base + i] = 0x7fffffff;
+  __syncthreads();
+  // ---- bitonic sort of (key, index) ascending
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (P2 >> 1); t += PS_THREADS) {
+        const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1)), b2 = a | j;
+        const bool up = (a & k) == 0;
+        const unsigned long long ka = skey[a], kb = skey[b2];
+        const int ia = sidx[a], ib = sidx[b2];
+        const bool gt = ka > kb || (ka == kb && ia > ib);
+        if (gt == up) {
+          skey[a] = kb;
+          skey[b2] = ka;
+          sidx[a] = ib;
+          sidx[b2] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int o = tid; o < P; o += PS_THREADS) {
+    const int idx = sidx[o];
+    out.idx[base + o] = idx;
+    out.w[base + o] = w[idx];
+    out.mx[base + o] = static_cast<double>(mx[idx]);
+    // #{rows with g >= idx}, prefill.py:144,155 (g = row_offset + local row)
+    out.len[base + o] = n_s - lower_bound_dev(pos, n_s, idx - row_offset);
+    out.inv[base + idx] = o;
+  }
+  if (tid == 0) out.sorted[h * 2 + kind] = P;
+}
+
+// K2 fallback: the full stable sort of the lists of the heads K3 flagged (one
+// CTA per (kind, head) in shared memory); every other CTA exits at once.
+constexpr int BS_THREADS = 512;
+constexpr int BS_ITEMS = PS_MAXN / BS_THREADS;
+using BlockSort = cub::BlockRadixSort<unsigned long long, BS_THREADS, BS_ITEMS, int32_t, 6>;
+inline size_t block_sort_smem(int n_s) {
+  return sizeof(typename BlockSort::TempStorage) + (n_s <= kScatterShRows ? 4 * static_cast<size_t>(n_s) : 0) + 16;
+}
+
+template <typename MaxT>
+__global__ void __launch_bounds__(BS_THREADS, 1)
+    sort_block_kernel(const double *v_w, const MaxT *v_max, const double *s_w, const MaxT *s_max, const int32_t *rows,
+                      int n_s, int n_total, int row_offset, int fix_bits, Lists out) {
+  const int kind = blockIdx.x, h = blockIdx.y;
+  if (!out.overflow[h]) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto &temp = *reinterpret_cast<typename BlockSort::TempStorage *>(smem_raw);
+  int *pos_sh = reinterpret_cast<int *>(smem_raw + sizeof(typename BlockSort::TempStorage));
+  const double *w = (kind == 0 ? s_w : v_w) + static_cast<int64_t>(h) * n_total;
+  const MaxT *mx = (kind == 0 ? s_max : v_max) + static_cast<int64_t>(h) * n_total;
+  const int32_t *rows_h = rows + static_cast<int64_t>(h) * n_s;
+  const bool in_sh = n_s <= kScatterShRows;
+  if (in_sh)
+    for (int r = threadIdx.x; r < n_s; r += BS_THREADS) pos_sh[r] = rows_h[r];
+  const int32_t *pos = in_sh ? pos_sh : rows_h;
+  const unsigned long long top = (1ull << fix_bits) - 1ull;
+  unsigned long long keys[BS_ITEMS];
+  int32_t vals[BS_ITEMS];
+#pragma unroll
+  for (int i = 0; i < BS_ITEMS; ++i) {
+    const int idx = threadIdx.x * BS_ITEMS + i;  // blocked arrangement = index order (stability -> idx asc)
+    keys[i] = idx < n_total ? top - static_cast<unsigned long long>(w[idx] * 1099511627776.0) : top;
+    vals[i] = idx;
+  }
+  BlockSort(temp).Sort(keys, vals, 0, fix_bits);
+  __syncthreads();  // pos_sh (written before the sort) visible
+  const int64_t base = (static_cast<int64_t>(h) * 2 + kind) * n_total;
+#pragma unroll
+  for (int i = 0; i < BS_ITEMS; ++i) {
+    const int o = threadIdx.x * BS_ITEMS + i;
+    if (o < n_total) {
+      const int idx = vals[i];
+      out.idx[base + o] = idx;
+      out.w[base + o] = w[idx];
+      out.mx[base + o] = static_cast<double>(mx[idx]);
+      out.len[base + o] = n_s - lower_bound_dev(pos, n_s, idx - row_offset);
+      out.inv[base + idx] = o;
+    }
+  }
+  if (threadIdx.x == 0) out.sorted[h * 2 + kind] = n_total;
 }
 
 // ------------------------------------------------------- crossing cells
@@ -294,7 +548,8 @@ constexpr bool g_idle_producer_smsp = LS_GREEDY_IDLE_SMSP != 0;
 template <typename Cells>
 __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
                                                                Picks P, int cap, Cells cells, int32_t *n_final,
-                                                               double *coverage, double *approx_out, int *dbg) {
+                                                               double *coverage, double *approx_out, int *dbg,
+                                                               int only_overflowed) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const long long t_start = clock64();
   GreedySmem &S = *reinterpret_cast<GreedySmem *>(g_smem);
@@ -302,8 +557,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
   __shared__ int next_j;
   __shared__ unsigned long long busy_cyc;  // diagnostics: consumer cycles spent on crossing sums
   const int h = blockIdx.x;
+  // the K2 fallback pass re-runs only the heads whose walk left a sorted prefix
+  if (only_overflowed && !L.overflow[h]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double T = total[h];
+  // sorted prefix of each list (K2 prefix sort); a walk that would read past one
+  // stops and flags the head for the fallback pass
+  const int srt_s = L.sorted ? L.sorted[h * 2] : n_total, srt_v = L.sorted ? L.sorted[h * 2 + 1] : n_total;
   const double target = alpha * T;
   const int64_t lb = static_cast<int64_t>(h) * 2 * n_total;
   const int64_t pb = static_cast<int64_t>(h) * cap;
@@ -391,6 +651,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
     while (go) {
       ++rounds;
       if ((s_idx >= n_total && v_idx >= n_total) || n >= cap) break;
+      // a round reads at most 64 entries past either walk position (window + prefetch)
+      if ((srt_s < n_total && s_idx + 64 > srt_s) || (srt_v < n_total && v_idx + 64 > srt_v)) {
+        if (lane == 0) L.overflow[h] = 1;
+        break;
+      }
       stop_seen = __shfl_sync(0xffffffffu, lane == 0 ? stop_at : 0, 0);  // one read: the warp must agree
       if (n >= stop_seen) break;
       int stopped = 0;
@@ -787,11 +1052,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
 
 template <typename Cells>
 int launch_greedy(const Lists &lists, int H, int n_total, double alpha, const double *total, Picks &picks, int cap,
-                  const Cells &cells, int32_t *n_final, double *coverage, double *approx, cudaStream_t st) {
+                  const Cells &cells, int32_t *n_final, double *coverage, double *approx, cudaStream_t st,
+                  int only_overflowed = 0) {
   const int smem = static_cast<int>(sizeof(GreedySmem));
   LS_CUDA(cudaFuncSetAttribute(greedy_kernel<Cells>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   greedy_kernel<Cells><<<H, G_THREADS, smem, st>>>(lists, n_total, alpha, total, picks, cap, cells, n_final, coverage,
-                                                   approx, g_debug_buffer);
+                                                   approx, g_debug_buffer, only_overflowed);
   LS_LAUNCH_CHECK("greedy_kernel");
   return LS_OK;
 }
@@ -874,6 +1140,8 @@ inline Work carve(Carver &c, int H, int n_total) {
   const size_t nl = static_cast<size_t>(H) * 2 * n_total;
   w.cap = 2 * n_total;
   const size_t np = static_cast<size_t>(H) * w.cap;
+  w.lists.sorted = nullptr;  // set by the K2 prefix path
+  w.lists.overflow = c.take<int32_t>(static_cast<size_t>(H) * 3);
   w.lists.idx = c.take<int32_t>(nl);
   w.lists.inv = c.take<int32_t>(nl);
   w.lists.len = c.take<int32_t>(nl);
@@ -967,7 +1235,16 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   Carver c(ws, ws_bytes);
   sel::Work w = sel::carve(c, H, n_total);
   sel::SortWork sw = sel::carve_sort(c, H, n_total);
-  {
+  const bool prefix = n_total <= sel::PS_MAXN;
+  if (prefix) {
+    w.lists.sorted = w.lists.overflow + H;
+    const size_t smem = sel::prefix_sort_smem(n_s);
+    LS_CUDA(cudaFuncSetAttribute(sel::sort_prefix_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    sel::sort_prefix_kernel<float><<<dim3(2, H), sel::PS_THREADS, smem, st>>>(v_w, v_max, s_w, s_max, rows, n_s,
+                                                                            n_total, L->row_offset, fix_bits, w.lists);
+    LS_LAUNCH_CHECK("sort_prefix_kernel");
+  } else {
     const int n = 2 * H * n_total;
     sel::sort_keys_kernel<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(v_w, s_w, H, n_total, fix_bits,
                                                                                 sw.k_in, sw.v_in);
@@ -995,6 +1272,16 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   cells.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
   int s = sel::launch_greedy(w.lists, H, n_total, alpha, total, w.picks, w.cap, cells, w.n_final, coverage, approx,
                              st);
+  if (!s && prefix) {  // heads that left a sorted prefix: full sort + greedy again (no-op launches otherwise)
+    const size_t smem = sel::block_sort_smem(n_s);
+    LS_CUDA(cudaFuncSetAttribute(sel::sort_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    sel::sort_block_kernel<float><<<dim3(2, H), sel::BS_THREADS, smem, st>>>(v_w, v_max, s_w, s_max, rows, n_s,
+                                                                           n_total, L->row_offset, fix_bits, w.lists);
+    LS_LAUNCH_CHECK("sort_block_kernel");
+    s = sel::launch_greedy(w.lists, H, n_total, alpha, total, w.picks, w.cap, cells, w.n_final, coverage, approx, st,
+                           1);
+  }
   if (s) return s;
   return sel::run_tail(w, H, n_total, alpha, total, slash_ids, vert_ids, counts, coverage, approx, picks, n_picks,
                        st);
