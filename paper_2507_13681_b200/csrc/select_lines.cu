@@ -164,13 +164,65 @@ __device__ __forceinline__ int block_scan_excl(int v, int &excl, int *warp_sums)
   return all;
 }
 
+// Ascending bitonic sort of PCAP = 4096 distinct u64 keys with 1024 threads:
+// thread t holds keys [4t, 4t + 4) in registers; partners within a thread
+// (j < 4) by register exchange, within a warp (j < 128) by shuffles, across
+// warps through shared memory (15 of the 78 stages).
+__device__ void bitonic_sort_pcap(unsigned long long *skey) {
+  static_assert(PCAP == 4 * PS_THREADS, "4 entries per thread");
+  const int t = threadIdx.x;
+  unsigned long long k[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) k[r] = skey[4 * t + r];
+  for (int kk = 2; kk <= PCAP; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 4) {
+        unsigned long long pk[4];
+        if (j >= 128) {  // across warps
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < 4; ++r) skey[4 * t + r] = k[r];
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < 4; ++r) pk[r] = skey[(4 * t + r) ^ j];
+        } else {  // within a warp: partner lane = lane ^ (j / 4)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) pk[r] = __shfl_xor_sync(0xffffffffu, k[r], j >> 2);
+        }
+        // (e & kk) and (e & j) are the same for the four entries of a thread (j >= 4)
+        const bool keep_min = (((4 * t) & kk) == 0) == (((4 * t) & j) == 0);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) k[r] = keep_min ? (pk[r] < k[r] ? pk[r] : k[r]) : (pk[r] > k[r] ? pk[r] : k[r]);
+      } else {  // within the thread: pairs (r, r | j)
+        auto cas = [&](int r, int q) {
+          const bool up = ((4 * t + r) & kk) == 0;  // (kk = 2: the two pairs sort in opposite directions)
+          const unsigned long long a = k[r], b = k[q];
+          const bool sw = up ? (b < a) : (a < b);
+          k[r] = sw ? b : a;
+          k[q] = sw ? a : b;
+        };
+        if (j == 2) {
+          cas(0, 2);
+          cas(1, 3);
+        } else {
+          cas(0, 1);
+          cas(2, 3);
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) skey[4 * t + r] = k[r];
+  __syncthreads();
+}
+
 template <typename MaxT>
 __global__ void __launch_bounds__(PS_THREADS, 1)
     sort_prefix_kernel(const double *v_w, const MaxT *v_max, const double *s_w, const MaxT *s_max,
                        const int32_t *rows, int n_s, int n_total, int row_offset, int fix_bits, Lists out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long *skey = reinterpret_cast<unsigned long long *>(smem_raw);  // [PCAP]
-  int *sidx = reinterpret_cast<int *>(smem_raw + PCAP * 8);                     // [PCAP]
   int *hist = reinterpret_cast<int *>(smem_raw + PCAP * 12);                    // [PS_BINS]
   int *red = hist + PS_BINS;                                                     // [64] scan / select scratch
   int *pos_sh = red + 64;
@@ -264,53 +316,32 @@ __global__ void __launch_bounds__(PS_THREADS, 1)
   const int n_lt = block_scan_excl(mine, off, red);
   if (take_eq > 0) block_scan_excl(mine_eq, off_eq, red);
   const int P = take_eq > 0 ? PCAP : n_lt;
+  // sort keys: (2^fix_bits - 1 - w * 2^40) << 14 | index -- distinct, ascending =
+  // (weight desc, index asc); fix_bits <= 50 and n_total <= 2^14 (host-checked)
+  const unsigned long long top = (1ull << fix_bits) - 1ull;
+  auto packed = [&](int idx) {
+    return ((top - static_cast<unsigned long long>(w[idx] * 1099511627776.0)) << 14) |
+           static_cast<unsigned long long>(idx);
+  };
 #pragma unroll
   for (int i = 0; i < PS_ITEMS; ++i) {
     const int idx = tid * PS_ITEMS + i;
     if (i >= n_mine) continue;
     if (sel_all || key[i] < thr) {
-      skey[off] = key[i];
-      sidx[off] = idx;
-      ++off;
+      skey[off++] = packed(idx);
     } else if (take_eq > 0 && key[i] == eq_key) {
-      if (off_eq < take_eq) {
-        skey[n_lt + off_eq] = key[i];
-        sidx[n_lt + off_eq] = idx;
-      }
+      if (off_eq < take_eq) skey[n_lt + off_eq] = packed(idx);
       ++off_eq;
     }
   }
-  int P2 = 1;
-  while (P2 < P) P2 <<= 1;
-  for (int i = P + tid; i < P2; i += PS_THREADS) {
-    skey[i] = ~0ull;
-    sidx[i] = 0x7fffffff;
-  }
+  for (int i = P + tid; i < PCAP; i += PS_THREADS) skey[i] = ~0ull;
   // every line starts unsorted (K3 reads inv < picks-of-that-kind as "picked")
   const int64_t base = (static_cast<int64_t>(h) * 2 + kind) * n_total;
   for (int i = tid; i < n_total; i += PS_THREADS) out.inv[base + i] = 0x7fffffff;
   __syncthreads();
-  // ---- bitonic sort of (key, index) ascending
-  for (int k = 2; k <= P2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = tid; t < (P2 >> 1); t += PS_THREADS) {
-        const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1)), b2 = a | j;
-        const bool up = (a & k) == 0;
-        const unsigned long long ka = skey[a], kb = skey[b2];
-        const int ia = sidx[a], ib = sidx[b2];
-        const bool gt = ka > kb || (ka == kb && ia > ib);
-        if (gt == up) {
-          skey[a] = kb;
-          skey[b2] = ka;
-          sidx[a] = ib;
-          sidx[b2] = ia;
-        }
-      }
-      __syncthreads();
-    }
-  }
+  bitonic_sort_pcap(skey);
   for (int o = tid; o < P; o += PS_THREADS) {
-    const int idx = sidx[o];
+    const int idx = static_cast<int>(skey[o] & 16383ull);
     out.idx[base + o] = idx;
     out.w[base + o] = w[idx];
     out.mx[base + o] = static_cast<double>(mx[idx]);
@@ -1235,7 +1266,7 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   Carver c(ws, ws_bytes);
   sel::Work w = sel::carve(c, H, n_total);
   sel::SortWork sw = sel::carve_sort(c, H, n_total);
-  const bool prefix = n_total <= sel::PS_MAXN;
+  const bool prefix = n_total <= sel::PS_MAXN && fix_bits <= 50;  // packed (key, index) sort keys fit 64 bits
   if (prefix) {
     w.lists.sorted = w.lists.overflow + H;
     const size_t smem = sel::prefix_sort_smem(n_s);

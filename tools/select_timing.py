@@ -14,6 +14,8 @@ from paper_2507_13681_b200.kvcompress import CompressionConfig
 CFG = os.environ.get("CFG", "c2")
 if CFG == "c2":
     shape, cap, ro, n_new, t = AttnShape(4, 32, 8, 128), 3 * 5128, 10128, 5128, 2
+elif CFG == "c2t1":
+    shape, cap, ro, n_new, t = AttnShape(4, 32, 8, 128), 3 * 5128, 0, 5000, 0
 else:  # c3 turn 4
     shape, cap, ro, n_new, t = AttnShape(4, 32, 8, 128), 4 * 8448, 25088, 8448, 3
 store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1)
@@ -39,5 +41,5 @@ for e in prof.events():
         agg.setdefault(e.name[:60], []).append(e.device_time_total)
 print(f"{os.environ.get('LS_LIB_PATH', 'lib')} {CFG} {mode} plans sha1 {h.hexdigest()[:16]} out sha1 {ho.hexdigest()[:16]}")
 tot = 0.0
-for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))[:16]:
+for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))[:int(os.environ.get('TOP', '16'))]:
     print(f"  {sum(v) / 1e3 / shape.n_layers:8.3f} ms/layer {len(v):4d} x  {k}")
