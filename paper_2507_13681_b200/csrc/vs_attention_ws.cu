@@ -491,20 +491,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool need = m_tile > m_ref + RESCALE_LOG2;
       const float m_old = m_ref;
       if (need) m_ref = m_tile;
-      float lsum = 0.f;
+      float2 lsum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_ref, -m_ref);
 #pragma unroll
       for (int cch = 0; cch < 4; ++cch) {
         uint32_t pk[16];  // P(i) columns [32 cch, +32) as bf16 pairs: TMEM columns s * 128 + 16 cch + [0, 16)
         // a row with no valid cell so far (m_ref = -inf) has P = 0 (and no NaN)
         if (live[cch] && m_ref != -INFINITY) {
-          const float nm = -m_ref;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float a = fast_exp2(fmaf(sv[cch][j], p.scale_log2, nm));
-            // LS_K5_POLY: share of the exponentials on the FMA pipe (FA4 split)
-            const float xb = fmaf(sv[cch][j + 1], p.scale_log2, nm);
-            const float b = (LS_K5_POLY == 2 || (LS_K5_POLY == 1 && (j & 2))) ? poly_exp2(xb) : fast_exp2(xb);
-            lsum += a + b;
+            const float2 x = ffma2(make_float2(sv[cch][j], sv[cch][j + 1]), sc2, nm2);  // (s * scale - m) per pair
+            const float a = fast_exp2(x.x);
+            // LS_K5_POLY: share of the exponentials on the FMA pipe (FA4 split): 1 = every 8th, 2 = every 4th
+            const bool poly = (LS_K5_POLY == 1 && (j & 14) == 14) || (LS_K5_POLY == 2 && (j & 6) == 6);
+            const float b = poly ? poly_exp2(x.y) : fast_exp2(x.y);
+            lsum2 = fadd2(lsum2, make_float2(a, b));
             pk[j >> 1] = tc::pack_bf16(a, b);
           }
         } else {
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tmem_wait_st();
       }
       if (need && m_old != -INFINITY) l *= fast_exp2(m_old - m_tile);
-      l += lsum;
+      l += lsum2.x + lsum2.y;
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bars->p_full[s]);  // one arrival per warp of the group
