@@ -49,6 +49,7 @@ constexpr int MAX_KB = 2048;
 constexpr int DENSE_SLASHES = 3;
 constexpr float RESCALE_LOG2 = 8.f;  // lazy rescale threshold (factor 256)
 constexpr int KST = 3, VST = 2;      // K / V ring stages
+constexpr int NSB = 3;               // TMEM S / P buffers (+ one O accumulator: 512 columns)
 #ifndef LS_K5_POLY
 #define LS_K5_POLY 0
 #endif
@@ -96,7 +97,7 @@ struct Smem {
 };
 
 struct Bars {
-  uint64_t kfull[KST], kempty[KST], vfull[VST], vempty[VST], s_full[2], p_full[2], pv_done[2], q_full;
+  uint64_t kfull[KST], kempty[KST], vfull[VST], vempty[VST], s_full[NSB], p_full[NSB], pv_done[2], q_full;
 };
 
 __device__ __forceinline__ bool bit_of(const uint32_t *b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t *kb_bits = reinterpret_cast<uint32_t *>(misc + 512);        // [64]
   float *pmax = reinterpret_cast<float *>(misc + 768);                 // [2][128]
   float *pd = reinterpret_cast<float *>(misc + 1792);                  // [2][128]
+  float *lx = reinterpret_cast<float *>(misc + 2816);                  // [128]
   int *gcols = reinterpret_cast<int *>(misc + 3328);                   // [2][128]
   int16_t *dense_list = reinterpret_cast<int16_t *>(misc + 4352);      // [MAX_KB]
   int *blk_cnt = reinterpret_cast<int *>(misc + 4352 + MAX_KB * 2);   // [MAX_KB] slash counts, then window starts
@@ -163,9 +165,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(&bars->vfull[s], 1);
       tc::mbar_init(&bars->vempty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NSB; ++s) {
       tc::mbar_init(&bars->s_full[s], 1);
       tc::mbar_init(&bars->p_full[s], 4);  // one arrival per softmax warp of the tile's warpgroup
+    }
+    for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&bars->pv_done[s], 1);
     }
     tc::mbar_init(&bars->q_full, 1);
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_sh;
-  const uint32_t tmem_o = tmem + 256;
+  const uint32_t tmem_o = tmem + NSB * 128;  // S / P buffers in columns [0, 384), O after them
 
   if (warp >= 8) {
   tc::setmaxnreg_dec<REGS_CTRL>();
@@ -333,23 +337,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(&bars->q_full, 0);
       auto issue_pv = [&](int j) {  // O += P(j) V(j), P(j) bf16 in TMEM over S(j)
         KDBG(1, j, 3);
-        tc::mbar_wait(&bars->p_full[j & 1], (j >> 1) & 1);
+        tc::mbar_wait(&bars->p_full[j % NSB], (j / NSB) & 1);
         tc::mbar_wait(&bars->vfull[j % VST], (j / VST) & 1);
         tc::fence_after_sync();
         const uint32_t vs = tc::smem_u32(smem + L::OFF_V + (j % VST) * L::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
           const uint64_t bd = tc::make_desc(vs + kk * 2048, BN * 128, 1024);
-          tc::mma_bf16_ts(tmem_o + (j & 1) * D, tmem + (j & 1) * 128 + kk * 8, bd, IDESC_O,
-                          (j > 1 || kk > 0) ? 1u : 0u);
+          tc::mma_bf16_ts(tmem_o, tmem + (j % NSB) * 128 + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(&bars->pv_done[j & 1]);
         tc::mma_commit(&bars->vempty[j % VST]);
       };
-      // S(i) may overwrite P(i-2) in its buffer: PV(i-2) was issued before it
-      // and the tensor pipe executes one thread's MMAs in order
+      // order S(0) S(1) S(2) PV(0) S(3) PV(1) S(4) ...: S(i) overwrites P(i - 3),
+      // whose PV was issued before it (the tensor pipe executes one thread's MMAs
+      // in order), and a warpgroup's next S(i + 2) is issued before its PV(i)
       for (int i = 0; i < n_all; ++i) {
-        const int s = i & 1;
+        const int s = i % NSB;
         KDBG(1, i, 4);
         tc::mbar_wait(&bars->kfull[i % KST], (i / KST) & 1);
         KDBG(1, i, 5);
@@ -363,29 +367,35 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc::mma_commit(&bars->s_full[s]);
         tc::mma_commit(&bars->kempty[i % KST]);
-        if (i > 0) issue_pv(i - 1);
+        if (i >= 2) issue_pv(i - 2);
       }
-      if (n_all > 0) issue_pv(n_all - 1);
+      for (int j = max(0, n_all - 2); j < n_all; ++j) issue_pv(j);
     }
   }
   } else {
     tc::setmaxnreg_inc<REGS_SOFT>();
     // =================================================== softmax warps
-    // Warpgroup wg (warps 4 wg .. 4 wg + 3) owns the tiles i with i % 2 == wg:
-    // its own online softmax (m_ref, l) and its own TMEM O accumulator O_wg,
-    // one thread per row over all 128 columns of a tile. The two warpgroups
-    // work on consecutive tiles at the same time with no exchange per tile
-    // (the MMA warp interleaves their S and PV); the partial (m, l, O) pairs are
-    // merged once in the epilogue.
-    const int wg = warp >> 2;
-    const int row = (warp & 3) * 32 + lane;
+    // Warpgroup wg (warps 4 wg .. 4 wg + 3) works on the tiles i with i % 2 ==
+    // wg, one thread per row over all 128 columns, so the two groups overlap
+    // two tiles. S / P rotate through three TMEM buffers and PV(i) accumulates
+    // into one shared O, so a group's next S(i + 2) is issued before its PV(i)
+    // and is usually ready when P(i) is done. The lazy-rescale reference of a
+    // row (m_ref_sh) is decided tile by tile in tile order: the group of tile i
+    // takes the decision of tile i - 1 from the other group (a named barrier
+    // per TMEM lane quadrant), raises the reference if its tile max exceeds it
+    // by 2^8, and rescales O itself after PV(i - 1) has landed; each group keeps
+    // its row-sum partial relative to the last reference it used.
+    const int wg = warp >> 2, quad = warp & 3;
+    const int row = quad * 32 + lane;
     const int my_g = g0 + row;
     const bool row_ok = row < nr;
-    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    float m_ref = -INFINITY, l = 0.f;
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    float *m_ref_sh = lx;  // [128] the row's current reference (log2 units)
+    float m_seen = -INFINITY, l = 0.f;  // this group's row-sum partial, relative to m_seen
     int my_cells = 0;
+    auto dec_bar = [&](int dst_wg) { return static_cast<uint32_t>(4 + quad * 2 + dst_wg); };
     for (int i = wg; i < n_all; i += 2) {
-      const int s = i & 1;  // == wg
+      const int s = i % NSB;
       const bool gathered = i >= n_dense && i < n_tc;
       uint32_t mk[4];
       if (i >= n_tc) {  // window: slash cells outside dense blocks and verticals
@@ -461,7 +471,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       my_cells += __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
       if (tid == 0) KDBG(2, i, 6);
-      tc::mbar_wait(&bars->s_full[s], (i >> 1) & 1);
+      tc::mbar_wait(&bars->s_full[s], (i / NSB) & 1);
       tc::fence_after_sync();
       const uint32_t s_addr = tmem + s * 128 + lane_base;
       float sv[4][32];
@@ -488,9 +498,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       const float m_tile = tmax == -INFINITY ? -INFINITY : tmax * p.scale_log2;
-      const bool need = m_tile > m_ref + RESCALE_LOG2;
-      const float m_old = m_ref;
-      if (need) m_ref = m_tile;
+      // reference decision of tile i (after the other group's decision of tile i - 1)
+      if (i >= 1) tc::named_sync(dec_bar(wg), 64);
+      const float m_cur = i >= 1 ? m_ref_sh[row] : -INFINITY;
+      const bool need = m_tile > m_cur + RESCALE_LOG2;
+      const float m_ref = need ? m_tile : m_cur;
+      m_ref_sh[row] = m_ref;
+      if (i + 1 < n_all) asm volatile("bar.arrive %0, 64;" ::"r"(dec_bar(1 - wg)) : "memory");
+      if (m_ref != m_seen) {  // this group's partial sum follows the reference
+        if (m_seen != -INFINITY) l *= fast_exp2(m_seen - m_ref);
+        m_seen = m_ref;
+      }
       float2 lsum2 = make_float2(0.f, 0.f);
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_ref, -m_ref);
 #pragma unroll
@@ -516,69 +534,56 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tmem_st16(s_addr + cch * 16, pk);
       }
       tc::tmem_wait_st();
-      // O_wg relative to the new reference before PV(i) adds P(i) (P is already
-      // stored; TMEM ld/st are .sync.aligned: the whole warp rescales if any row
-      // needs it), after this warpgroup's previous PV (i - 2) has landed in O_wg
-      if (__any_sync(0xffffffffu, need && m_old != -INFINITY && i >= 2)) {
+      l += lsum2.x + lsum2.y;
+      // a raised reference: O (everything up to PV(i - 1)) to the new reference
+      // before PV(i) adds P(i) (TMEM ld/st are .sync.aligned: the whole warp
+      // rescales if any of its rows needs it)
+      if (__any_sync(0xffffffffu, need && m_cur != -INFINITY)) {
         if (tid == 0) KDBG(2, i, 7);
-        tc::mbar_wait(&bars->pv_done[s], ((i - 2) >> 1) & 1);
+        tc::mbar_wait(&bars->pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
         tc::fence_after_sync();
-        const float corr = (need && m_old != -INFINITY) ? fast_exp2(m_old - m_tile) : 1.f;
+        const float corr = (need && m_cur != -INFINITY) ? fast_exp2(m_cur - m_tile) : 1.f;
 #pragma unroll
         for (int cch = 0; cch < D / 32; ++cch) {
           float ov[32];
-          tc::tmem_ld32(tmem_o + wg * D + lane_base + cch * 32, ov);
+          tc::tmem_ld32(tmem_o + lane_base + cch * 32, ov);
           tc::tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) ov[j] *= corr;
-          tc::tmem_st32(tmem_o + wg * D + lane_base + cch * 32, ov);
+          tc::tmem_st32(tmem_o + lane_base + cch * 32, ov);
         }
         tc::tmem_wait_st();
       }
-      if (need && m_old != -INFINITY) l *= fast_exp2(m_old - m_tile);
-      l += lsum2.x + lsum2.y;
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bars->p_full[s]);  // one arrival per warp of the group
     }
-    // ---- epilogue: merge the two warpgroups' (m, l, O) per row
-    float *mx = pmax;  // [2][128]
-    float *lx2 = pd;   // [2][128] (the gathered-tile staging is done)
-    tc::named_sync(1, N_SOFT);  // every staging read of pd is done
-    mx[wg * BM + row] = m_ref;
-    lx2[wg * BM + row] = l;
-    // the last PV of each warpgroup has landed in its O
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int last = n_all - 1 - ((n_all - 1 - b) & 1);  // last tile i < n_all with i % 2 == b
-      if (last >= 0 && last % 2 == b) tc::mbar_wait(&bars->pv_done[b], (last >> 1) & 1);
-    }
+    // ---- epilogue: O is relative to the final reference; row sums of both groups
+    float *lx2 = pd;  // [2][128] (the gathered-tile staging is done)
+    tc::named_sync(1, N_SOFT);  // every decision and staging read is done
+    const float mm = n_all > 0 ? m_ref_sh[row] : -INFINITY;
+    lx2[wg * BM + row] = (m_seen == -INFINITY || mm == -INFINITY) ? 0.f : l * fast_exp2(m_seen - mm);
+    // the last PV has landed. (A parity wait on PV(j) needs PV(j - 2) complete: S(n_all - 1),
+    // seen complete by its group, follows PV(n_all - 4); PV(n_all - 2) then implies PV(n_all - 3).)
+    if (n_all > 1) tc::mbar_wait(&bars->pv_done[(n_all - 2) & 1], ((n_all - 2) >> 1) & 1);
+    if (n_all > 0) tc::mbar_wait(&bars->pv_done[(n_all - 1) & 1], ((n_all - 1) >> 1) & 1);
     tc::fence_after_sync();
     tc::named_sync(1, N_SOFT);
-    const float m0 = mx[row], m1 = mx[BM + row];
-    const float mm = fmaxf(m0, m1);
-    const bool has0 = n_all > 0 && m0 != -INFINITY, has1 = n_all > 1 && m1 != -INFINITY;
-    const float f0 = has0 ? fast_exp2(m0 - mm) : 0.f, f1 = has1 ? fast_exp2(m1 - mm) : 0.f;
-    const float l_all = lx2[row] * f0 + lx2[BM + row] * f1;
+    const float l_all = lx2[row] + lx2[BM + row];
     // this thread writes output columns [wg * DH, wg * DH + DH) of its row
     float o[DH];
+    if (n_all > 0) {
 #pragma unroll
-    for (int j = 0; j < DH; ++j) o[j] = 0.f;
+      for (int cch = 0; cch < DH / 32; ++cch) {
+        float ov[32];
+        tc::tmem_ld32(tmem_o + lane_base + wg * DH + cch * 32, ov);
+        tc::tmem_wait_ld();
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      if (__any_sync(0xffffffffu, b == 0 ? has0 : has1)) {
-        const float f = b == 0 ? f0 : f1;
-#pragma unroll
-        for (int cch = 0; cch < DH / 32; ++cch) {
-          float ov[32];
-          tc::tmem_ld32(tmem_o + b * D + lane_base + wg * DH + cch * 32, ov);
-          tc::tmem_wait_ld();
-          if (f != 0.f) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o[cch * 32 + j] = fmaf(ov[j], f, o[cch * 32 + j]);
-          }
-        }
+        for (int j = 0; j < 32; ++j) o[cch * 32 + j] = ov[j];
       }
+    } else {
+#pragma unroll
+      for (int j = 0; j < DH; ++j) o[j] = 0.f;
     }
     if (row_ok && wg == 0 && p.row_lse)  // plan-cell mass of the row on the log2 scale (ls_plan_coverage)
       p.row_lse[static_cast<int64_t>(h) * p.n_new + r0 + row] = l_all > 0.f ? mm + __log2f(l_all) : -INFINITY;
