@@ -434,10 +434,13 @@ def main():
     ev_roof = event_roofline(per, cfg, eng, shape, blocks, peaks)
     k1_roof = k1_roofline(per, eng, cfg, clk)
     if n_sess > 1 or "kv_shards" in cfg:
-        # the dense baseline, plan quality, end-to-end and CPU legs are measured on C2
-        args.no_dense = args.no_e2e = args.no_cpu_baseline = True
+        # plan quality, end-to-end and CPU legs are measured on C2; the dense
+        # baseline also runs at C5 (the long-context case), not for C4's batch
+        args.no_e2e = args.no_cpu_baseline = True
+        if n_sess > 1:
+            args.no_dense = True
     dense = None if args.no_dense else dense_baseline(cfg, store, blocks, shard, ttft)
-    quality = None if args.no_dense else plan_quality(cfg, eng, store, blocks, shard)
+    quality = None if args.no_dense or "kv_shards" in cfg else plan_quality(cfg, eng, store, blocks, shard)
 
     e2e = None
     if not args.no_e2e:

@@ -25,6 +25,7 @@
 #include "tc_common.cuh"
 
 namespace ls {
+extern int *g_debug_buffer;
 // bf16 [heads][rows][d] tensor map, box 64 columns x 128 rows, 128-B swizzle (vs_attention_ws.cu)
 int make_tmap_bf16_3d(CUtensorMap *m, const void *base, int d, int64_t rows, int heads, int64_t row_stride_el,
                       int64_t head_stride_el);
@@ -66,6 +67,7 @@ struct Params {
   unsigned int *vmaxb, *smaxb;      // [H][n_total]
   float *row_stats;                 // [H][n_s][2]
   int32_t *status;                  // device validation word (NonFiniteInput / AllMaskedRow)
+  int *dbg;                         // optional host-mapped phase clocks (ls_debug_set_buffer)
 };
 
 __device__ __forceinline__ int rt_begin(const Params &p, int rt) {
@@ -172,7 +174,7 @@ struct LinesSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = BM * D * 2;
   static constexpr int OFF_P = OFF_K + 2 * BN * D * 2;
-  static constexpr int OFF_ACC = OFF_P + BM * LDP * 4;         // double[ACC_CAP]
+  static constexpr int OFF_ACC = OFF_P + 16 + BM * LDP * 4;    // double[ACC_CAP] (P: 4 zero floats, then 128 rows)
   static constexpr int OFF_ACCM = OFF_ACC + ACC_CAP * 8;       // float[ACC_CAP]
   static constexpr int OFF_RP = OFF_ACCM + ACC_CAP * 4;        // int[RP_CAP] row pointer by position
   static constexpr int OFF_MISC = OFF_RP + RP_CAP * 4;  // barriers | gs | m | 1/l | colp [4][128] f64 | colm [4][128]
@@ -205,6 +207,54 @@ __device__ __forceinline__ int load_item_q(const Params &p, unsigned char *smem,
   }
   tc::cp_async_commit();
   return nr;
+}
+
+// the item's sampled positions into gs[] and its Q rows into TMEM (lane = row,
+// 32-bit columns = bf16 pairs: the A operand of S = Qs K^T), zeros past nr;
+// warp w writes lanes of quadrant w % 4, columns [16 (w / 4), +16)
+template <int D>
+__device__ __forceinline__ int load_item_q_tmem(const Params &p, int *gs, uint32_t tmem_q, int h, int rt) {
+  const int r0 = rt_begin(p, rt), nr = rt_begin(p, rt + 1) - r0;
+  const int32_t *rows_h = p.rows + static_cast<int64_t>(h) * p.n_s + r0;
+  for (int r = threadIdx.x; r < BM; r += blockDim.x) gs[r] = r < nr ? p.row_offset + rows_h[r] : 0x7fffffff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = (warp & 3) * 32 + lane, cb = (warp >> 2) * 16;
+  if (cb < D / 2) {
+    uint32_t v[16];
+    if (row < nr) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(p.q + static_cast<int64_t>(h) * p.q_head_stride +
+                                                         static_cast<int64_t>(rows_h[row]) * D + cb * 2);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint4 x = __ldg(src + u);
+        v[4 * u] = x.x;
+        v[4 * u + 1] = x.y;
+        v[4 * u + 2] = x.z;
+        v[4 * u + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = 0u;
+    }
+    tc::tmem_st16(tmem_q + (static_cast<uint32_t>((warp & 3) * 32) << 16) + cb, v);
+  }
+  tc::tmem_wait_st();
+  return nr;
+}
+
+// S(buf) = Qs K^T with Qs from TMEM (no shared-memory operand traffic for A:
+// the lines pass keeps shared memory busy with its reductions)
+template <int D>
+__device__ __forceinline__ void issue_s_tq(unsigned char *smem, int off_k, uint32_t tmem, uint32_t tmem_q, int buf,
+                                           uint64_t *mbar) {
+  constexpr uint32_t IDESC = tc::make_idesc(BM, BN, false, false);
+  const uint32_t ks = tc::smem_u32(smem + off_k + buf * BN * D * 2);
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+    tc::mma_bf16_ts(tmem + buf * 128, tmem_q + kk * 8, bd, IDESC, kk > 0);
+  }
+  tc::mma_commit(&mbar[buf]);
 }
 
 // K rows [c0, c0 + 128) of kv head `kv` by TMA (rows past n_total read as zero)
@@ -414,7 +464,10 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
   double *colp = reinterpret_cast<double *>(smem + L::OFF_MISC + 2048);         // [4][128]
   float *colm = reinterpret_cast<float *>(smem + L::OFF_MISC + 2048 + 4096);    // [4][128]
   int *rbase = reinterpret_cast<int *>(smem + L::OFF_MISC + 2048 + 4096 + 2048);  // [128] r * LDP + g_r
-  float *Pf = reinterpret_cast<float *>(smem + L::OFF_P);
+  // P rows at stride LDP; the pad columns [128, 132) of every row and the 4
+  // floats before row 0 stay zero, so a diagonal read up to 3 columns outside
+  // the tile (the slash quads below) reads 0
+  float *Pf = reinterpret_cast<float *>(smem + L::OFF_P + 16);
   double *acc = reinterpret_cast<double *>(smem + L::OFF_ACC);
   float *accm = reinterpret_cast<float *>(smem + L::OFF_ACCM);
   int *rp = reinterpret_cast<int *>(smem + L::OFF_RP);
@@ -425,7 +478,7 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
   Pipe pp{bars, bars + 2, nullptr, 0};
   TileCursor cur, pre;
   cur.seek(p.tstart, n_items, x0);
-  if (warp == 0) tc::tmem_alloc(tmem_sh, 256);
+  if (warp == 0) tc::tmem_alloc(tmem_sh, 512);  // S double buffer [0, 256), Qs [256, 256 + D / 2)
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&pp.s_full[b], 1);
@@ -433,9 +486,11 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tc::prefetch_tmap(&tm_k);
-    pre = cur;  // K(t+1) is loaded one tile ahead, at the top of tile t
-    tma_k<D>(&tm_k, smem, L::OFF_K, 0, &pp.k_full[0], pre.j * BN, (pre.i / p.n_rt) / p.group);
-    if (x0 + 1 < x1) pre.next(p.tstart);
+    pre = cur;  // K(t + 2) is loaded at the top of tile t (once S(t) has read stage t & 1)
+    for (int t = 0; t < 2 && x0 + t < x1; ++t) {
+      tma_k<D>(&tm_k, smem, L::OFF_K, t, &pp.k_full[t], pre.j * BN, (pre.i / p.n_rt) / p.group);
+      if (x0 + t + 1 < x1) pre.next(p.tstart);
+    }
   }
   // TMEM reads: warp w -> lanes 32*(w%4), columns [32*(w/4), +32)
   const int row = (warp & 3) * 32 + lane;
@@ -454,9 +509,8 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
   auto begin_item = [&](int t) {
     h = cur.i / p.n_rt;
     rt = cur.i - h * p.n_rt;
-    nr = load_item_q<D>(p, smem, gs, h, rt);
+    nr = load_item_q_tmem<D>(p, gs, pp.tmem + 256, h, rt);
     r0 = rt_begin(p, rt);
-    tc::cp_async_wait<0>();
     __syncthreads();  // gs visible
     if (tid < BM) {
       float m = -INFINITY, l = 0.f;
@@ -502,7 +556,7 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
     mr = li_sh[row] > 0.f ? m_sh[row] - __log2f(li_sh[row]) : INFINITY;
     if (tid == 0) {
       tc::mbar_wait(&pp.k_full[t & 1], (t >> 1) & 1);
-      issue_s<D>(smem, L::OFF_K, pp.tmem, t & 1, pp.s_full);
+      issue_s_tq<D>(smem, L::OFF_K, pp.tmem, pp.tmem + 256, t & 1, pp.s_full);
     }
   };
   // slash accumulator window of the chunk holding column c0: d in [d_base, d_base + width)
@@ -519,10 +573,20 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
       }
     // (ordered before the slash phase by the tile's first barrier)
   };
-  __syncthreads();  // barrier init / TMEM address
+  for (int i = tid; i < BM * 4 + 4; i += LINES_THREADS) {
+    if (i < BM * 4) Pf[(i >> 2) * LDP + BN + (i & 3)] = 0.f;
+    else Pf[i - BM * 4 - 4] = 0.f;
+  }
+  __syncthreads();  // barrier init / TMEM address / zero pads
   pp.tmem = *tmem_sh;
+  // diagnostics: per-tile phase clocks of CTA 0, threads 0 / 32 / 256, tiles < 64
+  int *rec = nullptr;
+  if (p.dbg && blockIdx.x == 0 && (tid == 0 || tid == 32 || tid == 256))
+    rec = p.dbg + 40000 + (tid == 0 ? 0 : tid == 32 ? 1 : 2) * 64 * 12;
+#define K1REC(k) do { if (rec && t < 64) rec[t * 12 + (k)] = static_cast<int>(clock64()); } while (0)
   for (int x = x0; x < x1; ++x) {
     const int t = x - x0, buf = t & 1;
+    K1REC(0);
     const int c0 = cur.j * BN;
     const bool last_in_item = x + 1 >= cur.i_end_tile;
     const bool more = x + 1 < x1;
@@ -533,12 +597,28 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
     } else if (c0 % CHUNK == 0) {
       begin_chunk(c0);
     }
-    if (more && tid == 0) {  // stage buf^1 held K(t-1), consumed by S(t-1)
-      tma_k<D>(&tm_k, smem, L::OFF_K, buf ^ 1, &pp.k_full[buf ^ 1], pre.j * BN, (pre.i / p.n_rt) / p.group);
-      if (x + 2 < x1) pre.next(p.tstart);
-    }
     tc::mbar_wait(&pp.s_full[buf], (t >> 1) & 1);
     tc::fence_after_sync();
+    K1REC(1);
+    if (tid == 0) {
+      // S(t) has read K stage buf: K(t + 2) into it; S(t + 1) into TMEM buffer buf ^ 1
+      // (read by the exp phase of tile t - 1, before its first barrier) so the MMA
+      // runs under this whole tile
+      if (x + 2 < x1) {
+        tma_k<D>(&tm_k, smem, L::OFF_K, buf, &pp.k_full[buf], pre.j * BN, (pre.i / p.n_rt) / p.group);
+        if (x + 3 < x1) pre.next(p.tstart);
+      }
+      if (more && !last_in_item) {
+        tc::mbar_wait(&pp.k_full[buf ^ 1], ((t + 1) >> 1) & 1);
+        K1REC(8);
+        issue_s_tq<D>(smem, L::OFF_K, pp.tmem, pp.tmem + 256, buf ^ 1, pp.s_full);
+        K1REC(9);
+#ifdef LS_K1_MMALAT  // diagnostics: S(t + 1) completion latency seen right after the issue
+        tc::mbar_wait(&pp.s_full[buf ^ 1], ((t + 1) >> 1) & 1);
+        K1REC(10);
+#endif
+      }
+    }
     {
       const int lim = min(my_g, c_end - 1) - c0 - cblk;  // last valid column of this thread's 32
       float sv[32];
@@ -563,13 +643,11 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
     }
     // P lives in generic-proxy shared memory only (the MMAs read Q and K): no
     // proxy fence here, just the TMEM read -> next-MMA ordering around the barrier
+    K1REC(2);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    if (more && !last_in_item && tid == 0) {
-      tc::mbar_wait(&pp.k_full[buf ^ 1], ((t + 1) >> 1) & 1);
-      issue_s<D>(smem, L::OFF_K, pp.tmem, buf ^ 1, pp.s_full);
-    }
+    K1REC(3);
     // vertical partials: four threads per column (32-row quarters; rows past
     // nr hold zeros): four fp32 partials of 8 rows each, combined in fp64
     {
@@ -586,12 +664,16 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
                           (static_cast<double>(s4[2]) + static_cast<double>(s4[3]));
       colm[qq * BN + j] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     }
-    // slash partials: thread owns diagonal d, rows ascending
+    K1REC(4);
+    // slash partials: a thread owns four consecutive diagonals dq .. dq + 3 and
+    // walks the rows of their union in ascending order (one row-base load per
+    // row for four cells; a cell outside a diagonal's own rows reads a zero pad,
+    // so each diagonal's fp32 sum is the same as summing its own rows alone)
     {
       const int d_lo = max(d_base, g_first - (c0 + BN - 1));
       const int d_hi = g_hi - c0;
-      for (int dd = d_lo + tid; dd <= d_hi; dd += LINES_THREADS) {
-        const int glo = c0 + dd, ghi = min(c0 + dd + BN - 1, g_hi);
+      for (int dq = d_lo + 4 * tid; dq <= d_hi; dq += 4 * LINES_THREADS) {
+        const int glo = c0 + dq, ghi = min(c0 + dq + 3 + BN - 1, g_hi);
         int r, r_end;
         if (use_rp) {
           r = rp[max(glo, g_first) - g_first];
@@ -600,24 +682,35 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
           r = lower_bound_dev(gs, nr, glo);
           r_end = lower_bound_dev(gs, nr, ghi + 1);
         }
-        float sw = 0.f, mx = 0.f;
-        const float *pcol = Pf - dd - c0;  // cell (r, g_r - dd) at pcol[rb[r]]
-#pragma unroll 4
+        float sw[4] = {0.f, 0.f, 0.f, 0.f}, mx[4] = {0.f, 0.f, 0.f, 0.f};
+        const float *pcol = Pf - dq - c0;  // cell (r, g_r - dq - k) at pcol[rbase[r] - k]
+#pragma unroll 2
         for (; r < r_end; ++r) {
-          const float v = pcol[rbase[r]];
-          sw += v;
-          mx = fmaxf(mx, v);
+          const float *pp = pcol + rbase[r];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float v = pp[-k];
+            sw[k] += v;
+            mx[k] = fmaxf(mx[k], v);
+          }
         }
-        if (smem_acc) {
-          acc[dd - d_base] += static_cast<double>(sw);
-          accm[dd - d_base] = fmaxf(accm[dd - d_base], mx);
-        } else if (sw > 0.f) {
-          atomicAdd(sfix + dd, to_fix(static_cast<double>(sw)));
-          atomicMax(smaxb + dd, __float_as_uint(mx));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int dd = dq + k;
+          if (dd > d_hi) break;
+          if (smem_acc) {
+            acc[dd - d_base] += static_cast<double>(sw[k]);
+            accm[dd - d_base] = fmaxf(accm[dd - d_base], mx[k]);
+          } else if (sw[k] > 0.f) {
+            atomicAdd(sfix + dd, to_fix(static_cast<double>(sw[k])));
+            atomicMax(smaxb + dd, __float_as_uint(mx[k]));
+          }
         }
       }
     }
+    K1REC(5);
     __syncthreads();
+    K1REC(6);
     if (tid < BN) {
       const int c = c0 + tid;
       if (c < c_end) {
@@ -646,10 +739,12 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
     }
     // (no barrier otherwise: every read of Pf precedes the barrier above, and the next
     // tile writes colp / the slash accumulator only after its own first barrier)
+    K1REC(7);
   }
+#undef K1REC
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(pp.tmem, 256);
+  if (warp == 0) tc::tmem_dealloc(pp.tmem, 512);
 }
 
 // fixed point -> fp64 line weights; total = exact integer sum of the verticals.
@@ -782,6 +877,7 @@ int k1_prepare(const ls_layer_desc *L, int32_t n_s, const uint16_t *q, const uin
   p.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
   p.row_stats = row_stats;
   p.status = device_status_ptr();
+  p.dbg = g_debug_buffer;
   Carver c(ws, ws_bytes);
   const size_t H = L->n_heads;
   p.pstats = c.take<float2>(H * p.n_chunks * n_s * 4);

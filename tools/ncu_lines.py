@@ -3,6 +3,7 @@
   python tools/ncu_lines.py gpurun_out/x.ncu-rep [N]
 """
 import csv
+import os
 import io
 import subprocess
 import sys
@@ -52,6 +53,7 @@ for r in rows:
         if v:
             a[2][h] = a[2].get(h, 0) + v
 print(f"total stall samples {tot_s:.0f}, warp instructions {tot_i:.0f}")
-for key, (s, ins, st) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+order = 1 if os.environ.get("BY_INSTR") else 0
+for key, (s, ins, st) in sorted(agg.items(), key=lambda x: -x[1][order])[:top]:
     reasons = ", ".join(f"{k[6:]}={v / max(s, 1):.0%}" for k, v in sorted(st.items(), key=lambda x: -x[1])[:3])
     print(f"{s / max(tot_s, 1):6.1%} {ins / max(tot_i, 1):6.1%}  {key[0]}:{key[1]:<4} {key[2]:<70} [{reasons}]")
