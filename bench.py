@@ -507,7 +507,9 @@ def event_roofline(per, cfg, eng, shape, blocks, peaks):
     ach = bytes_ / (mean_ms * 1e-3) / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": round(ach, 3), "peak": peaks["hbm"], "unit": "GB/s",
             "frac": round(ach / peaks["hbm"], 5), "mean_launch_ms": round(mean_ms, 4), "launches": len(per[name]),
-            "work_per_launch": bytes_, "peak_src": peaks["src"], "traffic": None}
+            "work_per_launch": bytes_, "peak_src": peaks["src"],
+            "traffic": (NCU_TRAFFIC.get(name) or {}).get("dram_bytes_per_launch"),
+            "traffic_src": (NCU_TRAFFIC.get(name) or {}).get("source")}
 
 
 def k1_roofline(per, eng, cfg, clk):
@@ -528,11 +530,14 @@ def k1_roofline(per, eng, cfg, clk):
     t_mufu = 2 * cells / mufu_peak * 1e3
     t_tensor = 2 * 2 * cfg["d"] * cells / tensor_peak * 1e3
     bound = "mufu" if t_mufu >= t_tensor else "tensor"
+    nc = NCU_TRAFFIC.get(name) or {}
     return {"kernel": name, "bound": bound, "cells_per_launch": cells, "bound_ms": round(max(t_mufu, t_tensor), 4),
             "mufu_bound_ms": round(t_mufu, 4), "tensor_bound_ms": round(t_tensor, 4),
             "mean_launch_ms": round(mean_ms, 4), "frac": round(max(t_mufu, t_tensor) / mean_ms, 4),
             "achieved": round(2 * cells / (mean_ms * 1e-3) / 1e12, 4), "unit": "T ex2/s",
-            "peak": round(mufu_peak / 1e12, 4), "launches": n}
+            "peak": round(mufu_peak / 1e12, 4), "launches": n, "traffic": nc.get("dram_bytes_per_launch"),
+            "ncu_xu_pct": {"lines": nc.get("lines_xu_pct"), "stats": nc.get("stats_xu_pct")},
+            "traffic_src": nc.get("source")}
 
 
 def roofline(per, cfg, eng, store, blocks, peaks):
@@ -557,7 +562,13 @@ def roofline(per, cfg, eng, store, blocks, peaks):
             ex = 4.0 * d * 128 * 128 * float(sum(int(t.sum()) for t in eng.tile_log)) / n
             extra = {"executed_tflops": round(ex / (mean_ms * 1e-3) / 1e12, 3),
                      "executed_frac": round(ex / (mean_ms * 1e-3) / 1e12 / peak, 5),
-                     "algorithmic_over_executed": round(work / ex, 4)}
+                     "algorithmic_over_executed": round(work / ex, 4),
+                     # the same executed work against the nominal 2.25 PF dense bf16 peak, beside
+                     # ncu's tensor-pipe activity of one captured launch (of nominal)
+                     "executed_frac_of_nominal": round(ex / (mean_ms * 1e-3) / 1e12 / 2250.0, 5)}
+            nc = NCU_TRAFFIC.get("ls_vs_attention") or {}
+            if "ncu_tensor_active_pct_of_nominal" in nc:
+                extra["ncu_tensor_active_of_nominal"] = round(nc["ncu_tensor_active_pct_of_nominal"] / 100.0, 5)
     elif name == "ls_score_lines" and eng.score_log:
         work = 2.0 * d * float(sum(int(c.sum()) for c in eng.score_log)) / n  # QK^T of the causal sampled cells
         bound, unit, peak = "tensor", "TFLOP/s", peaks["tensor_sus"] or peaks["tensor"]

@@ -196,13 +196,19 @@ class SessionEngine:
         if head_groups is None:
             import os
             head_groups = int(os.environ.get("LS_HEAD_GROUPS", "1"))
-        if head_groups < 1 or shape.n_kv % head_groups:
-            raise ValueError(f"head_groups={head_groups} must divide n_kv={shape.n_kv}")
-        self.head_groups = head_groups
-        kv_per = shape.n_kv // head_groups
         grp = shape.n_q // shape.n_kv
-        self._groups = [(g * kv_per * grp, (g + 1) * kv_per * grp, g * kv_per, (g + 1) * kv_per)
-                        for g in range(head_groups)]
+        if head_groups < 1 or (shape.n_kv % head_groups and (head_groups % shape.n_kv or grp % (head_groups // shape.n_kv))):
+            raise ValueError(f"head_groups={head_groups} must divide n_kv={shape.n_kv}, or split each KV head's "
+                             f"{grp} q-heads evenly")
+        self.head_groups = head_groups
+        if shape.n_kv % head_groups == 0:  # whole KV-head groups
+            kv_per = shape.n_kv // head_groups
+            self._groups = [(g * kv_per * grp, (g + 1) * kv_per * grp, g * kv_per, (g + 1) * kv_per)
+                            for g in range(head_groups)]
+        else:  # q-heads of one KV head split across groups (e.g. one C5 shard: 8 q-heads, 1 KV head)
+            q_per = shape.n_q // head_groups
+            self._groups = [(g * q_per, (g + 1) * q_per, (g * q_per) // grp, (g * q_per) // grp + 1)
+                            for g in range(head_groups)]
         if head_groups > 1 and str(device).startswith("cuda") and torch.cuda.is_available():
             # K1 / K5 on normal-priority streams; the selection chains (few CTAs,
             # latency-bound) on high-priority streams so their CTAs are

@@ -11,12 +11,16 @@ from paper_2507_13681_b200.kvcompress import CompressionConfig
 
 CFG = os.environ.get("CFG", "c2")
 L = int(os.environ.get("LAYERS", "32"))
+n_q, n_kv = 32, 8
 if CFG == "c2":
     blocks, budget = [(0, 5000), (5000, 5128), (10128, 5128)], 1024
+elif CFG == "c5":  # one KV-head group of Llama-70B (8 q-heads / 1 KV head), 10 turns x 10K
+    blocks = [(0, 10000)] + [(10000 + (t - 1) * 10128, 10128) for t in range(1, 10)]
+    budget, n_q, n_kv = 1024, 8, 1
 else:
     blocks, budget = [(0, 8192), (8192, 8448), (16640, 8448), (25088, 8448)], 2048
 cap = blocks[-1][0] + blocks[-1][1]
-shape = AttnShape(L, 32, 8, 128)
+shape = AttnShape(L, n_q, n_kv, 128)
 store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1)
 mode = "dense" if os.environ.get("DENSE") else "loopserve"
 eng = SessionEngine(shape, SessionParams(mode=mode, alpha=0.955, comp=CompressionConfig(budget, 16, 16), max_new=128),
