@@ -193,8 +193,38 @@ def _cpu_decode_unit(args):
     return (time.perf_counter() - t0) / reps
 
 
+def _cpu_event_unit(args):
+    """One compression event of one head on the oracle (kvcompress.py:210-214):
+    accumulate_scores over the W buffered rows, top-B, retained_union."""
+    import numpy as np
+
+    from oracle import kvcompress as okv
+
+    n_cols, window, budget, length, reps = args
+    rng = np.random.Generator(np.random.PCG64(0))
+    rows = [(np.sort(rng.choice(length, n_cols, replace=False)), rng.random(n_cols)) for _ in range(window)]
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ids, sc = okv.accumulate_scores(rows)
+        sel = okv.top_by_score(ids, sc, budget)
+        okv.retained_union(sel, window, length)
+    return (time.perf_counter() - t0) / reps
+
+
+def _cpu_worker_init():
+    """One BLAS thread per worker: `cores` is then the number of threads used."""
+    global _BLAS_LIMIT
+    from threadpoolctl import threadpool_limits
+
+    _BLAS_LIMIT = threadpool_limits(1)
+
+
+_BLAS_LIMIT = None
+
+
 def cpu_baseline(cfg, cores=None):
-    """Oracle port on `cores` host processes, bounded sample, extrapolated."""
+    """Oracle port on `cores` single-threaded host processes, bounded sample,
+    extrapolated."""
     import multiprocessing as mp
 
     import numpy as np
@@ -220,23 +250,27 @@ def cpu_baseline(cfg, cores=None):
     per_turn_heads = max(1, min(n_q_s, cores // n_t))
     work = [(t, h) for h in range(per_turn_heads) for t in range(n_t)]
     n_sample = len(work)
-    with ctx.Pool(min(cores, n_sample)) as pool:
+    W = cfg["obs_window"] or cfg["interval"]
+    with ctx.Pool(min(cores, n_sample), initializer=_cpu_worker_init) as pool:
         times = pool.map(_cpu_unit, work)
-        # decode: one head-step at the dense (pre-event) and compressed sizes
+        # decode: one head-step at the dense (pre-event) and compressed sizes, and one
+        # compression event of a head (its buffered rows over the working set)
         L_end = blocks[-1][0] + blocks[-1][1]
-        comp_cols = min(L_end, cfg["budget"] + (cfg["obs_window"] or cfg["interval"]) + 1)
+        comp_cols = min(L_end, cfg["budget"] + W + 1)
         dense_t, comp_t = pool.map(_cpu_decode_unit, [(L_end, 3), (comp_cols, 20)])
+        event_t = pool.map(_cpu_event_unit, [(comp_cols, W, cfg["budget"], L_end, 5)])[0] if cfg["budget"] else 0.0
     n_proc = min(cores, n_sample)
     # per-unit core time x units / cores in parallel = the turn's TTFT on this host
     per_turn_ms = [1e3 * statistics.mean(tt for (t, _), tt in zip(work, times) if t == turn) * units / n_proc
                    for turn in range(n_t)]
     n_dense = min(cfg["max_new"], cfg["warmup"] - 1 if cfg["budget"] is not None else cfg["max_new"])
-    step_s = (n_dense * dense_t + (cfg["max_new"] - n_dense) * comp_t) / cfg["max_new"]
+    n_events = len(range(cfg["warmup"], cfg["max_new"] + 1, cfg["interval"])) if cfg["budget"] else 0
+    step_s = (n_dense * dense_t + (cfg["max_new"] - n_dense) * comp_t + n_events * event_t) / cfg["max_new"]
     tok_s = 1.0 / (step_s * units / n_proc)
     sample = (f"oracle port (numpy fp64): {per_turn_heads} (layer 0, head) prefill units of each of the {n_t} turns "
               f"({n_sample} units in parallel on {n_proc} processes) + decode head-steps at {L_end} and "
-              f"{comp_cols} columns; per-unit core time extrapolated to {units} (layer, head) units on "
-              f"{n_proc} cores")
+              f"{comp_cols} columns + one compression event of a head; per-unit core time extrapolated to "
+              f"{units} (layer, head) units on {n_proc} single-threaded processes (BLAS threads limited to 1)")
     return dict(ttft_ms=statistics.mean(per_turn_ms), per_turn_ms=per_turn_ms, decode_tokens_per_s=tok_s,
                 cores=n_proc, sample=sample)
 

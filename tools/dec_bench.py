@@ -1,6 +1,6 @@
-"""Decode step time by kind (dense / compressed / event) at the C2 turn-3 state:
-CUDA-graph replays timed with events, so PDL overlap between layers counts
-as it does in bench.py. Diagnostics for the GPU box (launch-shape sweeps)."""
+"""Decode time of one C2 turn-3 decode (128 tokens, all 32 layers; CUDA events
+around SessionEngine.decode after an untimed re-prefill, best of REPS) --
+diagnostics for launch-shape sweeps (tools/sweep_dec.sh)."""
 import os
 import sys
 
@@ -12,36 +12,22 @@ from paper_2507_13681_b200.kvcompress import CompressionConfig
 
 L = int(os.environ.get("LAYERS", "32"))
 IN = int(os.environ.get("INPUT", "5000"))
-N = int(os.environ.get("REPS", "50"))
+N = int(os.environ.get("REPS", "5"))
 shape = AttnShape(L, 32, 8, 128)
 cap = 3 * (IN + 128)
 store = QKVStore.synthetic(shape, cap, n_ref=cap, seed=1)
 eng = SessionEngine(shape, SessionParams(alpha=0.955, comp=CompressionConfig(1024, 16, 16), max_new=128), cap)
 ro, n_new = 2 * (IN + 128) - 128, IN + 128
-eng.prefill(store, 2, ro, n_new)
-eng.decode(store, ro + n_new, 128)  # captures the graphs
-torch.cuda.synchronize()
-res = {}
-for kind, g in sorted(eng._graphs.items(), key=lambda kv: str(kv[0])):
-    name = kind[0]
+best = None
+for rep in range(N + 1):
     eng.prefill(store, 2, ro, n_new)
-    eng.decode(store, ro + n_new, 20)  # past the first event: compressed state valid
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(3):
-        g.replay()
     e0.record()
-    for _ in range(N):
-        g.replay()
+    eng.decode(store, ro + n_new, 128)
     e1.record()
     torch.cuda.synchronize()
-    res[name] = e0.elapsed_time(e1) / N
-eng.prefill(store, 2, ro, n_new)
-torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-eng.decode(store, ro + n_new, 128)
-e1.record()
-torch.cuda.synchronize()
-print(" ".join(f"{k}={v * 1e3:.1f}us/step" for k, v in res.items()), f"turn={e0.elapsed_time(e1):.2f}ms",
-      f"per_layer: " + " ".join(f"{k}={v * 1e3 / L:.2f}us" for k, v in res.items() if k != "event"))
+    ms = e0.elapsed_time(e1)
+    if rep > 0:
+        best = ms if best is None else min(best, ms)
+print(f"decode turn (128 tokens, {L} layers): {best:.3f} ms = {128 / best * 1e3:.0f} tokens/s")
