@@ -145,6 +145,21 @@ int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha, const uin
                     int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
                     ls_stream_t stream);
 
+/* ls_select_lines with the plan build (K4) fused into each head's K3 CTA: head h's
+ * slash_ids / vert_ids / counts / picks are written by its CTA, which then sets
+ * plan_ready[h] = epoch (device memory, monotonically increasing epochs), so the
+ * caller can start the head's sparse attention on another stream with
+ * ls_stream_wait_value while slower heads are still selecting. */
+int ls_select_lines_ready(const ls_layer_desc *L, int32_t n_s, double alpha, const uint16_t *q,
+                          const uint16_t *k, const int32_t *rows, const double *v_w, const float *v_max,
+                          const double *s_w, const float *s_max, const float *row_stats, const double *total,
+                          int32_t *slash_ids, int32_t *vert_ids, int32_t *counts, double *coverage, double *approx,
+                          int32_t *picks, int32_t *n_picks, int32_t *plan_ready, int32_t epoch, void *ws,
+                          size_t ws_bytes, ls_stream_t stream);
+
+/* Stream-ordered wait until *addr >= value (device memory; cuStreamWaitValue32 GEQ). */
+int ls_stream_wait_value(ls_stream_t stream, const int32_t *addr, int32_t value);
+
 /* Greedy on caller-provided sorted line lists with a dense weight matrix as
  * the cell source: replaces greedy_select_lines (prefill.py:232-251). One
  * head. lines are (index, weight, length, max_cell) sorted by (-w, index);

@@ -62,6 +62,9 @@ SIGNATURES = {
     "ls_select_lines_workspace": (SZ, [LD, I32]),
     "ls_select_lines": (C.c_int, [LD, I32, F64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
                                   SZ, P]),
+    "ls_select_lines_ready": (C.c_int, [LD, I32, F64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, P,
+                                        SZ, P]),
+    "ls_stream_wait_value": (C.c_int, [P, P, I32]),
     "ls_greedy_dense": (C.c_int, [I32, P, P, P, P, I32, P, P, P, P, F64, F64, P, P, I32, I32, P, P,
                                   P, P, P, P, SZ, P]),
     "ls_vs_attention_workspace": (SZ, [LD]),
@@ -120,7 +123,8 @@ def check(status: int, what: str = "") -> None:
 # CUDA kernels each C-ABI entry launches (memsets/memcpys not counted);
 # bench.py reports the sum over its timed region as `gpu_launches`.
 KERNELS_PER_CALL = {
-    "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 5, "ls_greedy_dense": 5,
+    "ls_sample_rows": 1, "ls_score_lines": 3, "ls_select_lines": 6, "ls_select_lines_ready": 4,
+    "ls_greedy_dense": 5,
     "ls_vs_attention": 3, "ls_vs_attention_ex": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
     "ls_plan_coverage": 7,
     "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,

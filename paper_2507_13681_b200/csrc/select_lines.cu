@@ -30,6 +30,8 @@
 
 #include <algorithm>
 
+#include <cuda.h>
+
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
@@ -58,6 +60,17 @@ struct Picks {  // [H][cap]
   double *approx;   // approx after this pick
   double *cross;    // crossing-cell sum (phase b)
   int32_t *n;       // [H] picks recorded by the chain
+};
+
+// K4 fused into K3 (per head, by the head's CTA) with a readiness flag, so the
+// sparse attention of a head can start while slower heads are still selecting
+struct PlanOut {
+  uint32_t *sbits, *vbits;  // [H][words] scratch bitmaps
+  int words;
+  int32_t *slash_ids, *vert_ids, *counts;  // [H][n_total], [H][n_total], [H][2]
+  int32_t *picks_out;                      // optional [H][2 n_total]
+  int32_t *ready;                          // [H] set to `epoch` once the head's plan is written
+  int32_t epoch;
 };
 
 // ---------------------------------------------------------------- K2 sort
@@ -580,7 +593,7 @@ template <typename Cells>
 __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_total, double alpha, const double *total,
                                                                Picks P, int cap, Cells cells, int32_t *n_final,
                                                                double *coverage, double *approx_out, int *dbg,
-                                                               int only_overflowed) {
+                                                               int only_overflowed, PlanOut po) {
   extern __shared__ __align__(16) unsigned char g_smem[];
   const long long t_start = clock64();
   GreedySmem &S = *reinterpret_cast<GreedySmem *>(g_smem);
@@ -1079,16 +1092,72 @@ __global__ void __launch_bounds__(G_THREADS, 1) greedy_kernel(Lists L, int n_tot
       }
     }
   }
+  if (po.ready == nullptr) return;
+  // ---- fused K4: picks -> bitmaps -> sorted id lists of this head, then its flag
+  // (a head that left a sorted prefix publishes only from the fallback pass)
+  __syncthreads();
+  const bool publish = only_overflowed || L.overflow == nullptr || !L.overflow[h];
+  if (!publish) return;
+  uint32_t *sb = po.sbits + static_cast<int64_t>(h) * po.words, *vb = po.vbits + static_cast<int64_t>(h) * po.words;
+  for (int w = threadIdx.x; w < po.words; w += blockDim.x) sb[w] = vb[w] = 0u;
+  __syncthreads();
+  const int nf = static_cast<const volatile int32_t *>(n_final)[h];
+  for (int t = threadIdx.x; t < nf; t += blockDim.x) {
+    const int32_t code = P.code[pb + t];
+    const int idx = code & 0x7fffffff;
+    atomicOr((code < 0 ? vb : sb) + (idx >> 5), 1u << (idx & 31));
+    if (po.picks_out) po.picks_out[static_cast<int64_t>(h) * 2 * n_total + t] = code;
+  }
+  __syncthreads();
+  __shared__ int scan_sh[G_THREADS / 32];
+  for (int kind = 0; kind < 2; ++kind) {
+    const uint32_t *bits = kind == 0 ? sb : vb;
+    int32_t *out = (kind == 0 ? po.slash_ids : po.vert_ids) + static_cast<int64_t>(h) * n_total;
+    int base = 0;
+    for (int w0 = 0; w0 < po.words; w0 += blockDim.x) {
+      const int w = w0 + threadIdx.x;
+      uint32_t x = w < po.words ? bits[w] : 0u;
+      // block exclusive scan of the popcounts
+      const int c = __popc(x);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) scan_sh[warp] = incl;
+      __syncthreads();
+      int before = 0, all = 0;
+      for (int k = 0; k < G_THREADS / 32; ++k) {
+        if (k < warp) before += scan_sh[k];
+        all += scan_sh[k];
+      }
+      int pos = base + before + incl - c;
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        out[pos++] = w * 32 + b;
+      }
+      base += all;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) po.counts[h * 2 + kind] = base;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(po.ready + h, po.epoch);
+  }
 }
 
 template <typename Cells>
 int launch_greedy(const Lists &lists, int H, int n_total, double alpha, const double *total, Picks &picks, int cap,
                   const Cells &cells, int32_t *n_final, double *coverage, double *approx, cudaStream_t st,
-                  int only_overflowed = 0) {
+                  int only_overflowed = 0, PlanOut po = PlanOut{}) {
   const int smem = static_cast<int>(sizeof(GreedySmem));
   LS_CUDA(cudaFuncSetAttribute(greedy_kernel<Cells>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   greedy_kernel<Cells><<<H, G_THREADS, smem, st>>>(lists, n_total, alpha, total, picks, cap, cells, n_final, coverage,
-                                                   approx, g_debug_buffer, only_overflowed);
+                                                   approx, g_debug_buffer, only_overflowed, po);
   LS_LAUNCH_CHECK("greedy_kernel");
   return LS_OK;
 }
@@ -1248,12 +1317,13 @@ extern "C" size_t ls_select_lines_workspace(const ls_layer_desc *L, int32_t /*n_
   return c.off + 4096;
 }
 
-extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha, const uint16_t *q,
-                               const uint16_t *k, const int32_t *rows, const double *v_w, const float *v_max,
-                               const double *s_w, const float *s_max, const float *row_stats, const double *total,
-                               int32_t *slash_ids, int32_t *vert_ids, int32_t *counts, double *coverage,
-                               double *approx, int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
-                               ls_stream_t stream) {
+extern "C" int ls_select_lines_ready(const ls_layer_desc *L, int32_t n_s, double alpha, const uint16_t *q,
+                                     const uint16_t *k, const int32_t *rows, const double *v_w, const float *v_max,
+                                     const double *s_w, const float *s_max, const float *row_stats,
+                                     const double *total, int32_t *slash_ids, int32_t *vert_ids, int32_t *counts,
+                                     double *coverage, double *approx, int32_t *picks, int32_t *n_picks,
+                                     int32_t *plan_ready, int32_t epoch, void *ws, size_t ws_bytes,
+                                     ls_stream_t stream) {
   LS_REQUIRE(alpha >= 0.0 && alpha <= 1.0, LS_ERR_INVALID_ALPHA, "alpha=%g outside [0, 1]", alpha);
   const int fix_bits = sel::fix_bits_for(n_s);
   int seg_bits = 1;
@@ -1266,7 +1336,12 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   Carver c(ws, ws_bytes);
   sel::Work w = sel::carve(c, H, n_total);
   sel::SortWork sw = sel::carve_sort(c, H, n_total);
+  // fused K4 + per-head readiness flags (plan_ready): the head's CTA writes its plan
+  const sel::PlanOut po = plan_ready ? sel::PlanOut{w.sbits, w.vbits, w.words, slash_ids, vert_ids, counts, picks,
+                                                    plan_ready, epoch}
+                                     : sel::PlanOut{};
   const bool prefix = n_total <= sel::PS_MAXN && fix_bits <= 50;  // packed (key, index) sort keys fit 64 bits
+  if (!prefix) w.lists.overflow = nullptr;  // fully sorted lists: no fallback pass
   if (prefix) {
     w.lists.sorted = w.lists.overflow + H;
     const size_t smem = sel::prefix_sort_smem(n_s);
@@ -1302,7 +1377,7 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
   cells.kv_head_stride = L->kv_head_stride;
   cells.scale_log2 = kLog2e / sqrtf(static_cast<float>(L->head_dim));
   int s = sel::launch_greedy(w.lists, H, n_total, alpha, total, w.picks, w.cap, cells, w.n_final, coverage, approx,
-                             st);
+                             st, 0, po);
   if (!s && prefix) {  // heads that left a sorted prefix: full sort + greedy again (no-op launches otherwise)
     const size_t smem = sel::block_sort_smem(n_s);
     LS_CUDA(cudaFuncSetAttribute(sel::sort_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1311,11 +1386,44 @@ extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha
                                                                            n_total, L->row_offset, fix_bits, w.lists);
     LS_LAUNCH_CHECK("sort_block_kernel");
     s = sel::launch_greedy(w.lists, H, n_total, alpha, total, w.picks, w.cap, cells, w.n_final, coverage, approx, st,
-                           1);
+                           1, po);
   }
   if (s) return s;
+  if (plan_ready) {  // the plans were written by the greedy CTAs
+    if (n_picks) LS_CUDA(cudaMemcpyAsync(n_picks, w.n_final, sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, st));
+    return LS_OK;
+  }
   return sel::run_tail(w, H, n_total, alpha, total, slash_ids, vert_ids, counts, coverage, approx, picks, n_picks,
                        st);
+}
+
+extern "C" int ls_select_lines(const ls_layer_desc *L, int32_t n_s, double alpha, const uint16_t *q,
+                               const uint16_t *k, const int32_t *rows, const double *v_w, const float *v_max,
+                               const double *s_w, const float *s_max, const float *row_stats, const double *total,
+                               int32_t *slash_ids, int32_t *vert_ids, int32_t *counts, double *coverage,
+                               double *approx, int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
+                               ls_stream_t stream) {
+  return ls_select_lines_ready(L, n_s, alpha, q, k, rows, v_w, v_max, s_w, s_max, row_stats, total, slash_ids,
+                               vert_ids, counts, coverage, approx, picks, n_picks, nullptr, 0, ws, ws_bytes, stream);
+}
+
+// ------------------------------------------------------- device-value stream wait
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+extern "C" int ls_stream_wait_value(ls_stream_t stream, const int32_t *addr, int32_t value) {
+  static StreamWaitValue32Fn fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitValue32Fn>(ptr);
+  }
+  LS_REQUIRE(fn != nullptr, LS_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr),
+                        static_cast<cuuint32_t>(value), CU_STREAM_WAIT_VALUE_GEQ);
+  LS_REQUIRE(r == CUDA_SUCCESS, LS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", static_cast<int>(r));
+  return LS_OK;
 }
 
 // Dense-weights greedy for caller-provided sorted lists (one head).

@@ -219,6 +219,34 @@ class SessionEngine:
             self._ev_scored = [torch.cuda.Event() for _ in range(head_groups)]
             self._ev_done = [torch.cuda.Event() for _ in range(head_groups)]
             self._ev_start = torch.cuda.Event()
+        # K5 overlapped with K3 (head_groups == 1): each head's K3 CTA publishes its plan
+        # with a device flag (ls_select_lines_ready); the sparse attention of a group of
+        # heads runs on its own stream as soon as the group's flags are set, while slower
+        # heads are still selecting. Groups are whole KV-head groups (or q-heads of one
+        # KV head), about LS_K5_GROUPS (8) of them. LS_K5_OVERLAP=0 turns it off.
+        import os as _os
+        self._overlap = (head_groups == 1 and str(device).startswith("cuda") and torch.cuda.is_available()
+                         and _os.environ.get("LS_K5_OVERLAP", "1") != "0")
+        if self._overlap:
+            gh = max(1, shape.n_q // int(_os.environ.get("LS_K5_GROUPS", "8")))  # ~8 groups
+            if gh >= grp:
+                gh -= gh % grp  # whole KV-head groups
+                while shape.n_q % gh:
+                    gh -= grp
+            else:
+                while grp % gh:  # q-heads of one KV head
+                    gh -= 1
+            self._k5_groups = [(h0, h0 + gh) for h0 in range(0, shape.n_q, gh)]
+            self._k5_streams = [torch.cuda.Stream(device=device) for _ in self._k5_groups]
+            self._k5_ws = [Workspace() for _ in self._k5_groups]
+            self._k5_done = [torch.cuda.Event() for _ in self._k5_groups]
+            self._k5_start = torch.cuda.Event()
+            self._ready = torch.zeros(shape.n_q, dtype=torch.int32, device=device)
+            self._epoch = 0
+            # below this context the layer's GPU work is too short to pay for the groups'
+            # extra launches and per-call hooks (measured: C2 turn 3 at 15K keys only 2 ms
+            # faster without hooks and slower with bench.py's; C5 turn 10 at 101K keys 19 % faster)
+            self._overlap_min = int(_os.environ.get("LS_K5_OVERLAP_MIN", "24000"))
         self.clear_logs()
 
     def clear_logs(self):
@@ -293,6 +321,9 @@ class SessionEngine:
             if self.head_groups > 1:
                 plans, out, cells, tiles = self._layer_groups(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
                                                               store.q.stride(1), stream)
+            elif self._overlap and n_total >= self._overlap_min:
+                plans, out, cells, tiles = self._layer_overlap(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
+                                                               store.q.stride(1), stream)
             else:
                 plans, out, cells, tiles = self._layer_group(l, 0, sh.n_q, 0, sh.n_kv, qb, kl, vl, rows[l], n_new,
                                                              n_total, surv, n_seed, store.q.stride(1), None,
@@ -404,6 +435,47 @@ class SessionEngine:
                       out=st.ring_s[hr, first:], out_row_stride=st.row_cap, out_head_stride=st.window * st.row_cap,
                       q_head_stride=qhs, stream=stream)
             # (the seed slots' metadata is set once for every layer after the loop)
+        return plans, out, cells, tiles
+
+    def _layer_overlap(self, l, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs, stream):
+        """One layer with K5 overlapped with K3: K1 + K2/K3 on the caller's stream
+        (each head's K3 CTA writes its plan and sets its ready flag), then per head
+        group, on its own stream: a device wait on the group's flags, K5 and the
+        seed rows; joined on the caller's stream."""
+        p, sh, st = self.params, self.shape, self.stack
+        main = stream if stream is not None else torch.cuda.current_stream()
+        grp = sh.n_q // sh.n_kv
+        self._epoch += 1
+        self._k5_start.record(main)  # the layer's inputs are in place
+        plans: LayerPlans = sparsify_layer(qb, kl, rows_l, p.alpha, n_new, n_total, sh.n_kv, q_head_stride=qhs,
+                                           ws=self.ws, stream=stream, plan_ready=self._ready, epoch=self._epoch)
+        out = torch.empty((n_new, sh.n_q, sh.d), dtype=self.out_dtype, device=self.device)
+        cells = torch.empty(sh.n_q, dtype=torch.int64, device=self.device)
+        tiles = torch.empty(sh.n_q, dtype=torch.int64, device=self.device)
+        for g, (h0, h1) in enumerate(self._k5_groups):
+            s = self._k5_streams[g]
+            s.wait_event(self._k5_start)
+            sp = _lib.stream_ptr(s)
+            for h in range(h0, h1):
+                _lib.call("ls_stream_wait_value", sp, self._ready[h:h + 1].data_ptr(), self._epoch)
+            kv0, kv1 = h0 // grp, (h1 - 1) // grp + 1
+            qg, kg, vg = qb[h0:h1], kl[kv0:kv1], vl[kv0:kv1]
+            sl, vt, cn = plans.slash_ids[h0:h1], plans.vert_ids[h0:h1], plans.counts[h0:h1]
+            with torch.cuda.stream(s):
+                attention_layer(qg, kg, vg, sl, vt, cn, n_new, n_total, kv1 - kv0, out=out[:, h0:h1],
+                                out_dtype=self.out_dtype, q_head_stride=qhs, ws=self._k5_ws[g], stream=s,
+                                tiles=tiles[h0:h1], cells=cells[h0:h1])
+                if surv > 0:
+                    first = n_seed - surv
+                    hr = slice(l * sh.n_q + h0, l * sh.n_q + h1)
+                    plan_rows(qg, kg, sl, vt, cn, n_new, n_total, kv1 - kv0, surv, out=st.ring_s[hr, first:],
+                              out_row_stride=st.row_cap, out_head_stride=st.window * st.row_cap, q_head_stride=qhs,
+                              stream=s)
+            self._k5_done[g].record(s)
+        for g in range(len(self._k5_groups)):
+            main.wait_event(self._k5_done[g])
+        # (the tensors made on the caller's stream and read on the group streams stay
+        # referenced by the returned plans / outputs until after this join)
         return plans, out, cells, tiles
 
     def _layer_groups(self, l, qb, kl, vl, rows_l, n_new, n_total, surv, n_seed, qhs, stream):

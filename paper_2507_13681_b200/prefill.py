@@ -213,12 +213,16 @@ def layer_desc(n_heads, n_kv_heads, d, n_new, n_total, q_head_stride, kv_head_st
 def sparsify_layer(q_block: torch.Tensor, k: torch.Tensor, rows: torch.Tensor, alpha: float,
                    n_new: int, n_total: int, n_kv_heads: int, q_head_stride: int | None = None,
                    kv_head_stride: int | None = None, ws: Workspace | None = None,
-                   stream=None, on_scored=None, select_stream=None) -> LayerPlans:
+                   stream=None, on_scored=None, select_stream=None, plan_ready: torch.Tensor | None = None,
+                   epoch: int = 0) -> LayerPlans:
     """Batched sparsify_head for every q-head of a layer (K1 + K2-K4).
     on_scored(): called once the line sums (K1) are enqueued, before the
     selection (the engine's head-group pipeline records an event there).
     select_stream: run the selection (K2-K4) there (ordered after K1 and
     before anything later on `stream` by events).
+    plan_ready / epoch: int32 [H] device flags; each head's K3 CTA writes its
+    plan and then sets plan_ready[h] = epoch (ls_select_lines_ready), so a
+    consumer stream can start on a head as soon as its plan exists.
 
     q_block: bf16, head h row r at q_block.data_ptr() + (h*q_head_stride + r*d)*2
     k:       bf16 archive, kv-head j position c at (j*kv_head_stride + c*d)*2
@@ -264,11 +268,18 @@ def sparsify_layer(q_block: torch.Tensor, k: torch.Tensor, rows: torch.Tensor, a
     n_picks = torch.empty(H, dtype=i32, device=dev)
     n2 = lib.ls_select_lines_workspace(C_ref(L), n_s)
     w2 = ws.get(n2)
-    _lib.call("ls_select_lines", C_ref(L), n_s, float(alpha), q_block.data_ptr(), k.data_ptr(),
-              rows.data_ptr(), v_w.data_ptr(), v_max.data_ptr(), s_w.data_ptr(), s_max.data_ptr(),
-              row_stats.data_ptr(), total.data_ptr(), slash_ids.data_ptr(), vert_ids.data_ptr(),
-              counts.data_ptr(), coverage.data_ptr(), approx.data_ptr(), picks.data_ptr(),
-              n_picks.data_ptr(), w2.data_ptr(), w2.numel(), sp)
+    if plan_ready is None:
+        _lib.call("ls_select_lines", C_ref(L), n_s, float(alpha), q_block.data_ptr(), k.data_ptr(),
+                  rows.data_ptr(), v_w.data_ptr(), v_max.data_ptr(), s_w.data_ptr(), s_max.data_ptr(),
+                  row_stats.data_ptr(), total.data_ptr(), slash_ids.data_ptr(), vert_ids.data_ptr(),
+                  counts.data_ptr(), coverage.data_ptr(), approx.data_ptr(), picks.data_ptr(),
+                  n_picks.data_ptr(), w2.data_ptr(), w2.numel(), sp)
+    else:
+        _lib.call("ls_select_lines_ready", C_ref(L), n_s, float(alpha), q_block.data_ptr(), k.data_ptr(),
+                  rows.data_ptr(), v_w.data_ptr(), v_max.data_ptr(), s_w.data_ptr(), s_max.data_ptr(),
+                  row_stats.data_ptr(), total.data_ptr(), slash_ids.data_ptr(), vert_ids.data_ptr(),
+                  counts.data_ptr(), coverage.data_ptr(), approx.data_ptr(), picks.data_ptr(),
+                  n_picks.data_ptr(), plan_ready.data_ptr(), int(epoch), w2.data_ptr(), w2.numel(), sp)
     if select_stream is not None:
         ev = torch.cuda.Event()
         ev.record(select_stream)

@@ -99,7 +99,8 @@ def plan_tensors(plan, n_total: int, device):
 def attention_layer(q_block: torch.Tensor, k: torch.Tensor, v: torch.Tensor, slash_ids, vert_ids, counts,
                     n_new: int, n_total: int, n_kv_heads: int, out: torch.Tensor | None = None,
                     out_dtype=torch.bfloat16, q_head_stride=None, kv_head_stride=None,
-                    ws: Workspace | None = None, stream=None, tiles: torch.Tensor | None = None):
+                    ws: Workspace | None = None, stream=None, tiles: torch.Tensor | None = None,
+                    cells: torch.Tensor | None = None):
     """K5 for every q-head of a layer -> (out [n_new, H, d], cells [H]); with
     `tiles` (int64 [H]) also the 128x128 tensor-core tiles each head executed.
     `out` may be a head-column view of a wider [n_new, H_all, d] output."""
@@ -112,7 +113,8 @@ def attention_layer(q_block: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sla
                    out.stride(0) if out is not None else 0)
     if out is None:
         out = torch.empty((n_new, H, d), dtype=out_dtype, device=dev)
-    cells = torch.empty(H, dtype=torch.int64, device=dev)
+    if cells is None:
+        cells = torch.empty(H, dtype=torch.int64, device=dev)
     ws = ws or Workspace()
     n = _lib.lib().ls_vs_attention_workspace(C_ref(L))
     w = ws.get(n)
