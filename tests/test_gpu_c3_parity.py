@@ -18,8 +18,10 @@ import pytest
 import torch
 
 from oracle import attention as oatt
+from oracle import kvcompress as okv
 from oracle import prefill as opf
-from parity import NEAR_TIE_REL, check_plan
+from oracle.session import seed_rows_for_plan
+from parity import NEAR_TIE_REL, check_plan, check_topb
 
 pytestmark = pytest.mark.gpu
 
@@ -73,3 +75,61 @@ def test_c3_turn4_plans_and_attention(cuda_lib):
                    "near_tie": len(ties), "ties": ties, "k5_max_abs_err": errs, "near_tie_rel": NEAR_TIE_REL}, fh,
                   indent=1)
     assert max(errs.values()) <= 2e-2, errs
+
+
+def test_c3_decode_events_match_oracle(cuda_lib):
+    """48 compressed decode steps after the C3 turn-4 prefill (B = 2048, W =
+    n_d = 16; events at n_o = 16, 32, 48): every event's retained ids vs the
+    oracle's progressive_decode restatement (identical or a top-B near-tie),
+    outputs within 2e-2, decode op counts exact."""
+    from paper_2507_13681_b200.engine import AttnShape, QKVStore, SessionEngine, SessionParams
+    from paper_2507_13681_b200.kvcompress import CompressionConfig
+
+    max_new, B, W = 48, 2048, 16
+    shape = AttnShape(1, 4, 1, 128)
+    store = QKVStore.synthetic(shape, N_TOTAL + max_new, n_ref=N_TOTAL + max_new, seed=43)
+    eng = SessionEngine(shape, SessionParams(alpha=ALPHA, comp=CompressionConfig(B, 16, 16), max_new=max_new,
+                                             seed=43), N_TOTAL + max_new)
+    res = eng.prefill(store, 3, RO, N_NEW)
+    outs, events = [], []
+    eng.decode(store, N_TOTAL, max_new, out_sink=lambda t, ob: outs.append(ob[0].float().cpu().numpy().copy()),
+               events=events)
+    torch.cuda.synchronize()
+    log = eng.event_log(events)
+    hp = res.plans[0].to_host()
+    K = store.k[0, 0, :N_TOTAL + max_new].double().cpu().numpy()
+    V = store.v[0, 0, :N_TOTAL + max_new].double().cpu().numpy()
+    Q = store.q[0].double().cpu().numpy()
+    seeds = [seed_rows_for_plan(Q[h, RO:N_TOTAL], K[:N_TOTAL], hp[h].selected_slashes, hp[h].selected_verticals,
+                                RO, W) for h in range(4)]
+    q_steps = np.stack([Q[:, N_TOTAL + t] for t in range(max_new)])
+    score_log = []
+
+    class Counter:
+        scores = 0
+
+        def add(self, n):
+            self.scores += int(n)
+
+    cnt = Counter()
+    o_outs, stats = okv.progressive_decode_attn(K[None], V[None], [0, 0, 0, 0], N_TOTAL, seeds,
+                                                okv.CompressionConfig(B, 16, 16), max_new, q_steps,
+                                                counter=cnt, score_log=score_log)
+    assert [e["step"] for e in log] == [e["step"] for e in stats.events]
+    ties = []
+    for i, (de, oe) in enumerate(zip(log, stats.events)):
+        if de["retained_ids"] == oe["retained_ids"]:
+            continue
+        n_o, h, ids, scores = score_log[i]
+        ev = events[i // 4]
+        dev_picked = ev["sel"][h, :int(ev["n_sel"][h])].cpu().numpy()
+        check_topb(ids, scores, okv.top_by_score(ids, scores, B), dev_picked, B)
+        ties.append({"event": i, "step": n_o, "head": h})
+    err = float(np.abs(np.stack(outs) - o_outs).max())
+    os.makedirs(os.path.dirname(REPORT), exist_ok=True)
+    doc = json.load(open(REPORT)) if os.path.exists(REPORT) else {}
+    doc["decode"] = {"events": len(log), "near_tie": len(ties), "ties": ties, "max_abs_err": err}
+    with open(REPORT, "w") as fh:
+        json.dump(doc, fh, indent=1)
+    assert err <= 2e-2, err
+    assert eng.decode_op_counts(events)["decode_scores"] == cnt.scores
