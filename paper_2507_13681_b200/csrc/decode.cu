@@ -565,6 +565,22 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   } else {
     // ---- consumers
+    const int wr0 = (warp % NW) * RPW, grp = warp / NW;
+    // the working-set ids of this warp's rows in its first tiles (written by the
+    // last compression event, not by the previous layer): loaded before the
+    // dependency wait, so the per-tile ring-id stores never wait on L2
+    constexpr int MAXPF = 4;
+    int id_pf[MAXPF];
+#pragma unroll
+    for (int k = 0; k < MAXPF; ++k) {
+      id_pf[k] = 0;
+      const int i = grp + k * NG;
+      if (compressed && i < n_my && lane < RPW) {
+        const KmTile x = km_tile<KM_TILE>(t_begin + i, t_a, geo);
+        if (wr0 + lane < x.valid)
+          id_pf[k] = x.seg_a ? __ldg(S.sel_ids + hr0 * S.budget_cap + x.row0 + wr0 + lane) : x.row0 + wr0 + lane;
+      }
+    }
     if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     const int g = lane >> 2, t4 = lane & 3;
     const bool hv = g < G;
@@ -580,16 +596,17 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
 #pragma unroll
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_run = -INFINITY, l_part = 0.f;
-    const int wr0 = (warp % NW) * RPW, grp = warp / NW;
     const int64_t hr_g = head_row(S, layer, h0 + (hv ? g : 0));
     float *ring_row = S.ring_s + (hr_g * S.window + slot) * S.row_cap;
     const int m8 = lane >> 3, r8 = lane & 7;
     for (int i = grp; i < n_my; i += NG) {
       const int st = i % NST;
       const KmTile x = km_tile<KM_TILE>(t_begin + i, t_a, geo);
-      // this tile's working-set ids (ring_ids of compressed rows), fetched before the data wait
-      int id = 0;
-      if (compressed && lane < RPW && wr0 + lane < x.valid)
+      // this tile's working-set ids (ring_ids of compressed rows): prefetched for the
+      // first MAXPF tiles, else fetched before the data wait
+      const int kt = (i - grp) / NG;
+      int id = kt == 0 ? id_pf[0] : kt == 1 ? id_pf[1] : kt == 2 ? id_pf[2] : id_pf[3];
+      if (kt >= MAXPF && compressed && lane < RPW && wr0 + lane < x.valid)
         id = x.seg_a ? __ldg(S.sel_ids + hr0 * S.budget_cap + x.row0 + wr0 + lane) : x.row0 + wr0 + lane;
       tc::mbar_wait(&full[st], (i / NST) & 1);
       if (rec && tid == 0 && i == 0) rec[2] = gtime();
