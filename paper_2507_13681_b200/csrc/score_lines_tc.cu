@@ -665,15 +665,17 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
       colm[qq * BN + j] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     }
     K1REC(4);
-    // slash partials: a thread owns four consecutive diagonals dq .. dq + 3 and
+    // slash partials: a thread owns NQ consecutive diagonals dq .. dq + NQ - 1 and
     // walks the rows of their union in ascending order (one row-base load per
-    // row for four cells; a cell outside a diagonal's own rows reads a zero pad,
-    // so each diagonal's fp32 sum is the same as summing its own rows alone)
+    // row for NQ cells; a cell outside a diagonal's own rows reads a zero pad,
+    // so each diagonal's fp32 sum is the same as summing its own rows alone).
+    // NQ = 3: a tile's ~1,400 diagonals are one task per thread
     {
+      constexpr int NQ = 3;
       const int d_lo = max(d_base, g_first - (c0 + BN - 1));
       const int d_hi = g_hi - c0;
-      for (int dq = d_lo + 4 * tid; dq <= d_hi; dq += 4 * LINES_THREADS) {
-        const int glo = c0 + dq, ghi = min(c0 + dq + 3 + BN - 1, g_hi);
+      for (int dq = d_lo + NQ * tid; dq <= d_hi; dq += NQ * LINES_THREADS) {
+        const int glo = c0 + dq, ghi = min(c0 + dq + NQ - 1 + BN - 1, g_hi);
         int r, r_end;
         if (use_rp) {
           r = rp[max(glo, g_first) - g_first];
@@ -682,20 +684,22 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
           r = lower_bound_dev(gs, nr, glo);
           r_end = lower_bound_dev(gs, nr, ghi + 1);
         }
-        float sw[4] = {0.f, 0.f, 0.f, 0.f}, mx[4] = {0.f, 0.f, 0.f, 0.f};
+        float sw[NQ], mx[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) sw[k] = mx[k] = 0.f;
         const float *pcol = Pf - dq - c0;  // cell (r, g_r - dq - k) at pcol[rbase[r] - k]
 #pragma unroll 2
         for (; r < r_end; ++r) {
           const float *pp = pcol + rbase[r];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < NQ; ++k) {
             const float v = pp[-k];
             sw[k] += v;
             mx[k] = fmaxf(mx[k], v);
           }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < NQ; ++k) {
           const int dd = dq + k;
           if (dd > d_hi) break;
           if (smem_acc) {
