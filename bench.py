@@ -791,10 +791,10 @@ def run_e2e(args, cfg, eng, store, blocks, shard, gather):
                 if it > 0:
                     h2d += src.numel() * 2
 
-            def sink(t, ob):  # every step's outputs of every layer back to the host
-                outs_host[t].copy_(ob, non_blocking=True)
+            def run_sink(t0, outs):  # every run's outputs (all steps, all layers) back to the host
+                outs_host[t0:t0 + outs.shape[0]].copy_(outs, non_blocking=True)
 
-            eng.decode(store, n_total, cfg["max_new"], out_sink=sink)
+            eng.decode(store, n_total, cfg["max_new"], run_sink=run_sink)
             if it > 0:
                 d2h += outs_host.numel() * 2
             e2.record(stream)
