@@ -38,6 +38,9 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int CHUNK = 1024;        // key columns per statistics / slash-accumulator chunk
 constexpr int LDP = BN + 4;        // fp32 P row stride (16-B rows: conflict-free STS.128 / column LDS)
+constexpr int P_PRE = 4;           // zero floats before each P buffer (slash reads reach 2 columns left of row 0)
+constexpr int PBUF = P_PRE + BM * LDP;  // floats per P buffer
+constexpr int SQ = 3;              // slash diagonals per lane (stride 3: lanes on one row hit distinct banks)
 constexpr int ACC_CAP = 3072;      // shared slash accumulator (diagonals per chunk)
 constexpr int RP_CAP = 2048;       // row-pointer table: first sampled row at or after a position
 constexpr int LINES_THREADS = 512; // 16 warps: 4 per TMEM lane quadrant
@@ -170,15 +173,14 @@ struct StatsSmem {
 };
 
 template <int D>
-struct LinesSmem {
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = BM * D * 2;
-  static constexpr int OFF_P = OFF_K + 2 * BN * D * 2;
-  static constexpr int OFF_ACC = OFF_P + 16 + BM * LDP * 4;    // double[ACC_CAP] (P: 4 zero floats, then 128 rows)
-  static constexpr int OFF_ACCM = OFF_ACC + ACC_CAP * 8;       // float[ACC_CAP]
-  static constexpr int OFF_RP = OFF_ACCM + ACC_CAP * 4;        // int[RP_CAP] row pointer by position
-  static constexpr int OFF_MISC = OFF_RP + RP_CAP * 4;  // barriers | gs | m | 1/l | colp [4][128] f64 | colm [4][128]
-  static constexpr int TOTAL = OFF_MISC + 2048 + 4096 + 2048 + 1024;
+struct LinesSmem {  // (Qs lives in TMEM)
+  static constexpr int OFF_K = 0;                                // one K stage
+  static constexpr int OFF_P = OFF_K + BN * D * 2;              // two fp32 P buffers [BM][LDP]
+  static constexpr int OFF_ACC = OFF_P + 2 * PBUF * 4;          // double[ACC_CAP]
+  static constexpr int OFF_ACCM = OFF_ACC + ACC_CAP * 8;        // float[ACC_CAP]
+  static constexpr int OFF_RP = OFF_ACCM + ACC_CAP * 4;         // int[RP_CAP] row pointer by position
+  static constexpr int OFF_MISC = OFF_RP + RP_CAP * 4;          // barriers | TMEM address | counters | gs | m | 1/l | row bases
+  static constexpr int TOTAL = OFF_MISC + 2560;
 };
 
 __device__ __forceinline__ void zfill16(uint32_t saddr, const void *g, bool ok) {
@@ -248,7 +250,7 @@ template <int D>
 __device__ __forceinline__ void issue_s_tq(unsigned char *smem, int off_k, uint32_t tmem, uint32_t tmem_q, int buf,
                                            uint64_t *mbar) {
   constexpr uint32_t IDESC = tc::make_idesc(BM, BN, false, false);
-  const uint32_t ks = tc::smem_u32(smem + off_k + buf * BN * D * 2);
+  const uint32_t ks = tc::smem_u32(smem + off_k);  // (one K stage)
 #pragma unroll
   for (int kk = 0; kk < D / 16; ++kk) {
     const uint64_t bd = tc::make_desc(ks + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
@@ -444,30 +446,36 @@ __global__ void __launch_bounds__(STATS_THREADS, 2) k1_stats_kernel(const __grid
 }
 
 // ------------------------------------------------------------- pass 2
-// 16 warps. Per 128-key tile: P = exp2(s - m) / l (fp32) from TMEM into
-// shared memory (warp w: TMEM lanes of quadrant w % 4, 32 columns of block
-// w / 4); vertical partials by 4 threads per column (32 rows each, fp64, in
-// row order); slash partials by thread-owns-diagonal, rows ascending, with
-// the first contributing row read from a position -> row table instead of a
-// binary search; per-tile slash sums (<= ~13 cells) in fp32, accumulated per
-// 1024-key chunk in fp64 shared memory and flushed at the chunk's end.
+// 16 compute warps + 1 producer warp, software-pipelined over two P buffers:
+// iteration t computes P(t + 1) = exp2(s - m) / l (fp32) from TMEM into
+// buffer (t + 1) & 1 (warp w: TMEM lanes of quadrant w % 4, 32 columns of
+// block w / 4) and then reduces P(t) from buffer t & 1, so the MUFU-bound
+// exponentials of one tile overlap the shared-memory-bound reductions of the
+// previous one across warps; one named barrier per tile. Reductions are warp
+// tasks handed out by a shared counter: vertical (32 columns x 128 rows; lane
+// = 32-row quarter x 4 columns, one 16-B load per row, fp32 partials of 8 rows
+// combined in fp64, quarters added in order through shuffles, straight to the
+// column's integer atomics) and slash (lane owns SQ = 3 consecutive diagonals
+// and walks the rows of their union in ascending order through a row-base
+// table, zero pads covering cells outside a diagonal; per-tile fp32 sums
+// accumulated per 1024-key chunk in fp64 shared memory and flushed at the
+// chunk's end). The producer warp keeps the K TMA (one stage: a second one does
+// not fit beside two P buffers) and the S = Qs K^T MMAs (Qs in TMEM as the A
+// operand, S double-buffered in TMEM) ahead of the compute warps.
 template <int D>
-__global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
+__global__ void __launch_bounds__(LINES_THREADS + 32, 1) k1_lines_kernel(const __grid_constant__ CUtensorMap tm_k, Params p) {
   extern __shared__ unsigned char smem_dyn[];
   using L = LinesSmem<D>;
   unsigned char *smem = tc::align1024(smem_dyn);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);  // s_full[2] k_full[2]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::OFF_MISC);
+  uint64_t *s_full = bars, *s_free = bars + 2, *k_full = bars + 4, *q_full = bars + 5;
   uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smem + L::OFF_MISC + 48);
-  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);              // [128]
-  float *m_sh = reinterpret_cast<float *>(smem + L::OFF_MISC + 64 + 512);  // [128]
-  float *li_sh = m_sh + BM;                                                 // [128]
-  double *colp = reinterpret_cast<double *>(smem + L::OFF_MISC + 2048);         // [4][128]
-  float *colm = reinterpret_cast<float *>(smem + L::OFF_MISC + 2048 + 4096);    // [4][128]
-  int *rbase = reinterpret_cast<int *>(smem + L::OFF_MISC + 2048 + 4096 + 2048);  // [128] r * LDP + g_r
-  // P rows at stride LDP; the pad columns [128, 132) of every row and the 4
-  // floats before row 0 stay zero, so a diagonal read up to 3 columns outside
-  // the tile (the slash quads below) reads 0
-  float *Pf = reinterpret_cast<float *>(smem + L::OFF_P + 16);
+  int *task_ctr = reinterpret_cast<int *>(smem + L::OFF_MISC + 56);             // [2]
+  int *gs = reinterpret_cast<int *>(smem + L::OFF_MISC + 64);                    // [BM + 4]
+  float *m_sh = reinterpret_cast<float *>(smem + L::OFF_MISC + 64 + 528);       // [BM]
+  float *li_sh = m_sh + BM;                                                      // [BM]
+  int *rbase = reinterpret_cast<int *>(li_sh + BM);                              // [BM] r * LDP + g_r
+  float *Pb0 = reinterpret_cast<float *>(smem + L::OFF_P) + P_PRE;  // P(t) at Pb0 + (t & 1) * PBUF, rows at stride LDP
   double *acc = reinterpret_cast<double *>(smem + L::OFF_ACC);
   float *accm = reinterpret_cast<float *>(smem + L::OFF_ACCM);
   int *rp = reinterpret_cast<int *>(smem + L::OFF_RP);
@@ -475,161 +483,157 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
   int x0, x1;
   if (!tile_slice(p, x0, x1)) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  Pipe pp{bars, bars + 2, nullptr, 0};
-  TileCursor cur, pre;
-  cur.seek(p.tstart, n_items, x0);
+  const int n_tiles = x1 - x0;
   if (warp == 0) tc::tmem_alloc(tmem_sh, 512);  // S double buffer [0, 256), Qs [256, 256 + D / 2)
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&pp.s_full[b], 1);
-      tc::mbar_init(&pp.k_full[b], 1);
+      tc::mbar_init(&s_full[b], 1);
+      tc::mbar_init(&s_free[b], LINES_THREADS / 32);
     }
+    tc::mbar_init(k_full, 1);
+    tc::mbar_init(q_full, LINES_THREADS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tc::prefetch_tmap(&tm_k);
-    pre = cur;  // K(t + 2) is loaded at the top of tile t (once S(t) has read stage t & 1)
-    for (int t = 0; t < 2 && x0 + t < x1; ++t) {
-      tma_k<D>(&tm_k, smem, L::OFF_K, t, &pp.k_full[t], pre.j * BN, (pre.i / p.n_rt) / p.group);
-      if (x0 + t + 1 < x1) pre.next(p.tstart);
-    }
+    task_ctr[0] = task_ctr[1] = 0;
   }
-  // TMEM reads: warp w -> lanes 32*(w%4), columns [32*(w/4), +32)
-  const int row = (warp & 3) * 32 + lane;
-  const int cblk = (warp >> 2) * 32;
-  const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-  unsigned long long *sfix = nullptr;
-  unsigned int *smaxb = nullptr;
-  int h = 0, rt = 0, nr = 0, my_g = 0, g_first = 0, g_hi = 0, c_end = 0, r0 = 0;
-  float mr = INFINITY;
-  bool row_ok = false, use_rp = false;
-  int d_base = 0, width = 0;
-  bool smem_acc = false;
-  bool first = true;
-  // per item: Q gather, the item rows' statistics (all chunks, fixed order),
-  // position -> row table; then S of the item's first tile
-  auto begin_item = [&](int t) {
-    h = cur.i / p.n_rt;
-    rt = cur.i - h * p.n_rt;
-    nr = load_item_q_tmem<D>(p, gs, pp.tmem + 256, h, rt);
-    r0 = rt_begin(p, rt);
-    __syncthreads();  // gs visible
-    if (tid < BM) {
-      float m = -INFINITY, l = 0.f;
-      if (tid < nr) {
-        const int n_ck = min(gs[tid], p.n_total - 1) / CHUNK + 1;  // chunks of this row's causal range
-        const float2 *ps = p.pstats + (static_cast<int64_t>(h) * p.n_chunks * p.n_s + r0 + tid) * 4;
-        for (int c = 0; c < n_ck; ++c) {
+  for (int i = tid; i < ACC_CAP; i += blockDim.x) {  // invariant: zero outside a chunk's use (the flush re-zeroes)
+    acc[i] = 0.0;
+    accm[i] = 0.f;
+  }
+  // zero pads of both P buffers: columns [BN, LDP) of every row and the P_PRE floats before row 0
+  for (int i = tid; i < 2 * (BM * 4 + P_PRE); i += blockDim.x) {
+    const int b = i / (BM * 4 + P_PRE), k = i - b * (BM * 4 + P_PRE);
+    float *base = Pb0 + b * PBUF;
+    if (k < BM * 4) base[(k >> 2) * LDP + BN + (k & 3)] = 0.f;
+    else base[k - BM * 4 - P_PRE] = 0.f;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_sh, tmem_q = tmem + 256;
+
+  if (warp == LINES_THREADS / 32) {  // ---------------- producer warp
+    if (lane == 0) {
+      TileCursor pre;
+      pre.seek(p.tstart, n_items, x0);
+      int item = -1, n_q = 0;
+      tma_k<D>(&tm_k, smem, L::OFF_K, 0, k_full, pre.j * BN, (pre.i / p.n_rt) / p.group);
+      for (int t = 0; t < n_tiles; ++t) {
+        if (pre.i != item) {  // the item's Qs written to TMEM by the compute warps
+          item = pre.i;
+          tc::mbar_wait(q_full, n_q & 1);
+          ++n_q;
+        }
+        if (t >= 2) tc::mbar_wait(&s_free[t & 1], ((t - 2) >> 1) & 1);  // P(t - 2) read S buffer t & 1
+        tc::mbar_wait(k_full, t & 1);
+        tc::fence_after_sync();
+        issue_s_tq<D>(smem, L::OFF_K, tmem, tmem_q, t & 1, s_full);
+        if (t + 1 < n_tiles) {
+          tc::mbar_wait(&s_full[t & 1], (t >> 1) & 1);  // S(t) has read the K stage
+          pre.next(p.tstart);
+          tma_k<D>(&tm_k, smem, L::OFF_K, 0, k_full, pre.j * BN, (pre.i / p.n_rt) / p.group);
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------------------------------- 16 compute warps
+    const int row = (warp & 3) * 32 + lane;
+    const int cblk = (warp >> 2) * 32;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    TileCursor cur;
+    cur.seek(p.tstart, n_items, x0);
+    unsigned long long *sfix = nullptr;
+    unsigned int *smaxb = nullptr;
+    int h = 0, rt = 0, nr = 0, my_g = 0, g_first = 0, g_hi = 0, c_end = 0;
+    float mr = INFINITY;
+    bool row_ok = false, use_rp = false;
+    int d_base = 0, width = 0;
+    bool smem_acc = false;
+    // diagnostics: per-tile phase clocks of CTA 0, threads 0 / 32 / 256, tiles < 64
+    int *rec = nullptr;
+    if (p.dbg && blockIdx.x == 0 && (tid == 0 || tid == 32 || tid == 256))
+      rec = p.dbg + 40000 + (tid == 0 ? 0 : tid == 32 ? 1 : 2) * 64 * 12;
+#define K1REC(tt, k) do { if (rec && (tt) < 64) rec[(tt) * 12 + (k)] = static_cast<int>(clock64()); } while (0)
+    // per item: positions, Qs into TMEM (-> producer), the rows' statistics
+    // (all chunks, fixed order), position -> row table
+    auto begin_item = [&]() {
+      h = cur.i / p.n_rt;
+      rt = cur.i - h * p.n_rt;
+      nr = load_item_q_tmem<D>(p, gs, tmem_q, h, rt);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(q_full);
+      if (tid < 4) gs[BM + tid] = 0x7fffffff;
+      const int r0 = rt_begin(p, rt);
+      tc::named_sync(1, LINES_THREADS);  // gs visible
+      if (tid < BM) {
+        float m = -INFINITY, l = 0.f;
+        if (tid < nr) {
+          const int n_ck = min(gs[tid], p.n_total - 1) / CHUNK + 1;  // chunks of this row's causal range
+          const float2 *ps = p.pstats + (static_cast<int64_t>(h) * p.n_chunks * p.n_s + r0 + tid) * 4;
+          for (int c = 0; c < n_ck; ++c) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {  // (slot, half) in a fixed order
-            const float2 v = ps[static_cast<int64_t>(c) * p.n_s * 4 + e];
-            if (v.y == 0.f) continue;  // empty (zeroed) or no causal column
-            const float mn = fmaxf(m, v.x);
-            l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
-            m = mn;
+            for (int e = 0; e < 4; ++e) {  // (slot, half) in a fixed order
+              const float2 v = ps[static_cast<int64_t>(c) * p.n_s * 4 + e];
+              if (v.y == 0.f) continue;  // empty (zeroed) or no causal column
+              const float mn = fmaxf(m, v.x);
+              l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + v.y * fast_exp2(v.x - mn);
+              m = mn;
+            }
+          }
+          if (cur.j == 0) {  // the CTA holding the item's first tile publishes the row statistics
+            float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + r0 + tid) * 2;
+            rs[0] = m;
+            rs[1] = l > 0.f ? 1.f / l : 0.f;
+            // softmax_rows' validation (tensor_ops.py:34-38): a NaN / +inf logit
+            // (NaN row max or sum), or a row whose every logit is -inf
+            if (isnan(m) || isnan(l) || isinf(l) || (isinf(m) && m > 0.f)) report_status(p.status, LS_ERR_NON_FINITE_INPUT);
+            else if (m == -INFINITY) report_status(p.status, LS_ERR_ALL_MASKED_ROW);
           }
         }
-        if (cur.j == 0) {  // the CTA holding the item's first tile publishes the row statistics
-          float *rs = p.row_stats + (static_cast<int64_t>(h) * p.n_s + r0 + tid) * 2;
-          rs[0] = m;
-          rs[1] = l > 0.f ? 1.f / l : 0.f;
-          // softmax_rows' validation (tensor_ops.py:34-38): a NaN / +inf logit
-          // (NaN row max or sum), or a row whose every logit is -inf
-          if (isnan(m) || isnan(l) || isinf(l) || (isinf(m) && m > 0.f)) report_status(p.status, LS_ERR_NON_FINITE_INPUT);
-          else if (m == -INFINITY) report_status(p.status, LS_ERR_ALL_MASKED_ROW);
-        }
+        m_sh[tid] = m;
+        li_sh[tid] = l > 0.f ? 1.f / l : 0.f;
       }
-      m_sh[tid] = m;
-      li_sh[tid] = l > 0.f ? 1.f / l : 0.f;
-    }
-    if (tid < BM) rbase[tid] = tid * LDP + gs[tid];
-    g_first = gs[0];
-    g_hi = gs[nr - 1];
-    c_end = min(p.n_total, g_hi + 1);
-    const int rp_span = g_hi - g_first + 1;
-    use_rp = rp_span <= RP_CAP;
-    if (use_rp)
-      for (int xx = tid; xx < rp_span; xx += LINES_THREADS) rp[xx] = lower_bound_dev(gs, nr, g_first + xx);
-    sfix = p.sfix + static_cast<int64_t>(h) * p.n_total;
-    smaxb = p.smaxb + static_cast<int64_t>(h) * p.n_total;
-    q_ready_sync();
-    my_g = gs[row];
-    row_ok = row < nr;
-    mr = li_sh[row] > 0.f ? m_sh[row] - __log2f(li_sh[row]) : INFINITY;
-    if (tid == 0) {
-      tc::mbar_wait(&pp.k_full[t & 1], (t >> 1) & 1);
-      issue_s_tq<D>(smem, L::OFF_K, pp.tmem, pp.tmem + 256, t & 1, pp.s_full);
-    }
-  };
-  // slash accumulator window of the chunk holding column c0: d in [d_base, d_base + width)
-  auto begin_chunk = [&](int c0) {
-    const int cb = (c0 / CHUNK) * CHUNK;
-    const int ce = min(cb + CHUNK, c_end);
-    d_base = max(0, g_first - (ce - 1));
-    width = g_hi - cb - d_base + 1;
-    smem_acc = width <= ACC_CAP;
-    if (smem_acc)
-      for (int i = tid; i < width; i += LINES_THREADS) {
-        acc[i] = 0.0;
-        accm[i] = 0.f;
-      }
-    // (ordered before the slash phase by the tile's first barrier)
-  };
-  for (int i = tid; i < BM * 4 + 4; i += LINES_THREADS) {
-    if (i < BM * 4) Pf[(i >> 2) * LDP + BN + (i & 3)] = 0.f;
-    else Pf[i - BM * 4 - 4] = 0.f;
-  }
-  __syncthreads();  // barrier init / TMEM address / zero pads
-  pp.tmem = *tmem_sh;
-  // diagnostics: per-tile phase clocks of CTA 0, threads 0 / 32 / 256, tiles < 64
-  int *rec = nullptr;
-  if (p.dbg && blockIdx.x == 0 && (tid == 0 || tid == 32 || tid == 256))
-    rec = p.dbg + 40000 + (tid == 0 ? 0 : tid == 32 ? 1 : 2) * 64 * 12;
-#define K1REC(k) do { if (rec && t < 64) rec[t * 12 + (k)] = static_cast<int>(clock64()); } while (0)
-  for (int x = x0; x < x1; ++x) {
-    const int t = x - x0, buf = t & 1;
-    K1REC(0);
-    const int c0 = cur.j * BN;
-    const bool last_in_item = x + 1 >= cur.i_end_tile;
-    const bool more = x + 1 < x1;
-    if (first) {
-      begin_item(t);
-      begin_chunk(c0);
-      first = false;
-    } else if (c0 % CHUNK == 0) {
-      begin_chunk(c0);
-    }
-    tc::mbar_wait(&pp.s_full[buf], (t >> 1) & 1);
-    tc::fence_after_sync();
-    K1REC(1);
-    if (tid == 0) {
-      // S(t) has read K stage buf: K(t + 2) into it; S(t + 1) into TMEM buffer buf ^ 1
-      // (read by the exp phase of tile t - 1, before its first barrier) so the MMA
-      // runs under this whole tile
-      if (x + 2 < x1) {
-        tma_k<D>(&tm_k, smem, L::OFF_K, buf, &pp.k_full[buf], pre.j * BN, (pre.i / p.n_rt) / p.group);
-        if (x + 3 < x1) pre.next(p.tstart);
-      }
-      if (more && !last_in_item) {
-        tc::mbar_wait(&pp.k_full[buf ^ 1], ((t + 1) >> 1) & 1);
-        K1REC(8);
-        issue_s_tq<D>(smem, L::OFF_K, pp.tmem, pp.tmem + 256, buf ^ 1, pp.s_full);
-        K1REC(9);
-#ifdef LS_K1_MMALAT  // diagnostics: S(t + 1) completion latency seen right after the issue
-        tc::mbar_wait(&pp.s_full[buf ^ 1], ((t + 1) >> 1) & 1);
-        K1REC(10);
-#endif
-      }
-    }
-    {
+      if (tid < BM) rbase[tid] = tid * LDP + gs[tid];
+      g_first = gs[0];
+      g_hi = gs[nr - 1];
+      c_end = min(p.n_total, g_hi + 1);
+      const int rp_span = g_hi - g_first + 1;
+      use_rp = rp_span <= RP_CAP;
+      if (use_rp)
+        for (int xx = tid; xx < rp_span; xx += LINES_THREADS) rp[xx] = lower_bound_dev(gs, nr, g_first + xx);
+      sfix = p.sfix + static_cast<int64_t>(h) * p.n_total;
+      smaxb = p.smaxb + static_cast<int64_t>(h) * p.n_total;
+      tc::named_sync(1, LINES_THREADS);  // statistics / table visible
+      my_g = gs[row];
+      row_ok = row < nr;
+      mr = li_sh[row] > 0.f ? m_sh[row] - __log2f(li_sh[row]) : INFINITY;
+    };
+    // slash accumulator window of the chunk holding column c0: d in [d_base, d_base + width)
+    auto begin_chunk = [&](int c0) {
+      const int cb = (c0 / CHUNK) * CHUNK;
+      const int ce = min(cb + CHUNK, c_end);
+      d_base = max(0, g_first - (ce - 1));
+      width = g_hi - cb - d_base + 1;
+      smem_acc = width <= ACC_CAP;
+    };
+    // P(t) of key tile c0 into buffer t & 1; releases S buffer t & 1 to the producer
+    auto exp_tile = [&](int t, int c0) {
+      tc::mbar_wait(&s_full[t & 1], (t >> 1) & 1);
+      tc::fence_after_sync();
       const int lim = min(my_g, c_end - 1) - c0 - cblk;  // last valid column of this thread's 32
       float sv[32];
-      tc::tmem_ld32(pp.tmem + buf * 128 + lane_base + cblk, sv);
+      tc::tmem_ld32(tmem + (t & 1) * 128 + lane_base + cblk, sv);
       tc::tmem_wait_ld();
-      float4 *prow = reinterpret_cast<float4 *>(Pf + row * LDP + cblk);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&s_free[t & 1]);
+      float4 *prow = reinterpret_cast<float4 *>(Pb0 + (t & 1) * PBUF + row * LDP + cblk);
       if (row_ok && lim >= 31) {
+#define K1E(u) fast_exp2(fmaf(sv[u], p.scale_log2, -mr))
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          prow[j / 4] = make_float4(fast_exp2(fmaf(sv[j], p.scale_log2, -mr)), fast_exp2(fmaf(sv[j + 1], p.scale_log2, -mr)),
-                                    fast_exp2(fmaf(sv[j + 2], p.scale_log2, -mr)), fast_exp2(fmaf(sv[j + 3], p.scale_log2, -mr)));
+        for (int j = 0; j < 32; j += 4) prow[j / 4] = make_float4(K1E(j), K1E(j + 1), K1E(j + 2), K1E(j + 3));
+#undef K1E
       } else {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
@@ -640,115 +644,154 @@ __global__ void __launch_bounds__(LINES_THREADS, 1) k1_lines_kernel(const __grid
           prow[j / 4] = make_float4(e[0], e[1], e[2], e[3]);
         }
       }
-    }
-    // P lives in generic-proxy shared memory only (the MMAs read Q and K): no
-    // proxy fence here, just the TMEM read -> next-MMA ordering around the barrier
-    K1REC(2);
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    K1REC(3);
-    // vertical partials: four threads per column (32-row quarters; rows past
-    // nr hold zeros): four fp32 partials of 8 rows each, combined in fp64
-    {
-      const int j = tid & (BN - 1), qq = tid >> 7;
-      const float *pc = Pf + qq * 32 * LDP + j;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f}, m4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const float v = pc[r * LDP];
-        s4[r & 3] += v;
-        m4[r & 3] = fmaxf(m4[r & 3], v);
-      }
-      colp[qq * BN + j] = (static_cast<double>(s4[0]) + static_cast<double>(s4[1])) +
-                          (static_cast<double>(s4[2]) + static_cast<double>(s4[3]));
-      colm[qq * BN + j] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-    }
-    K1REC(4);
-    // slash partials: a thread owns NQ consecutive diagonals dq .. dq + NQ - 1 and
-    // walks the rows of their union in ascending order (one row-base load per
-    // row for NQ cells; a cell outside a diagonal's own rows reads a zero pad,
-    // so each diagonal's fp32 sum is the same as summing its own rows alone).
-    // NQ = 3: a tile's ~1,400 diagonals are one task per thread
-    {
-      constexpr int NQ = 3;
+    };
+    // reductions of P(t) (key tile c0), warp tasks: [0, 4) vertical, [4, 4 + n_sl) slash
+    auto reduce_tile = [&](int t, int c0) {
+      const float *Pf = Pb0 + (t & 1) * PBUF;
       const int d_lo = max(d_base, g_first - (c0 + BN - 1));
       const int d_hi = g_hi - c0;
-      for (int dq = d_lo + NQ * tid; dq <= d_hi; dq += NQ * LINES_THREADS) {
-        const int glo = c0 + dq, ghi = min(c0 + dq + NQ - 1 + BN - 1, g_hi);
-        int r, r_end;
-        if (use_rp) {
-          r = rp[max(glo, g_first) - g_first];
-          r_end = ghi + 1 <= g_hi ? rp[ghi + 1 - g_first] : nr;
+      const int n_sl = d_hi >= d_lo ? (d_hi - d_lo) / (32 * SQ) + 1 : 0;
+      int *ctr = task_ctr + (t & 1);
+      if (tid == 0) task_ctr[(t & 1) ^ 1] = 0;  // the next tile's counter (last used before this tile's barrier)
+      for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(ctr, 1);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= 4 + n_sl) break;
+        if (task < 4) {
+          // vertical, 32 columns: lane = (32-row quarter qq, 4 consecutive
+          // columns), one 16-B load per row (rows past nr hold zeros); per
+          // column and quarter four fp32 partials of 8 rows, combined in fp64,
+          // quarters added in order through shuffles
+          const int qq = lane >> 3, j = task * 32 + (lane & 7) * 4;
+          const float *pc = Pf + qq * 32 * LDP + j;
+          float s4[4][4], m4[4][4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s4[c][u] = m4[c][u] = 0.f;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const float4 v = *reinterpret_cast<const float4 *>(pc + r * LDP);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              s4[c][r & 3] += vv[c];
+              m4[c][r & 3] = fmaxf(m4[c][r & 3], vv[c]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double sw = (static_cast<double>(s4[c][0]) + static_cast<double>(s4[c][1])) +
+                        (static_cast<double>(s4[c][2]) + static_cast<double>(s4[c][3]));
+            float mx = fmaxf(fmaxf(m4[c][0], m4[c][1]), fmaxf(m4[c][2], m4[c][3]));
+            const double q1 = __shfl_down_sync(0xffffffffu, sw, 8), q2 = __shfl_down_sync(0xffffffffu, sw, 16),
+                         q3 = __shfl_down_sync(0xffffffffu, sw, 24);
+            mx = fmaxf(mx, __shfl_down_sync(0xffffffffu, mx, 8));
+            mx = fmaxf(mx, __shfl_down_sync(0xffffffffu, mx, 16));
+            if (qq == 0) {
+              sw = ((sw + q1) + q2) + q3;
+              const int col = c0 + j + c;
+              if (col < c_end) {
+                if (sw > 0.0) atomicAdd(p.vfix + static_cast<int64_t>(h) * p.n_total + col, to_fix(sw));
+                if (mx > 0.f) atomicMax(p.vmaxb + static_cast<int64_t>(h) * p.n_total + col, __float_as_uint(mx));
+              }
+            }
+          }
         } else {
-          r = lower_bound_dev(gs, nr, glo);
-          r_end = lower_bound_dev(gs, nr, ghi + 1);
-        }
-        float sw[NQ], mx[NQ];
+          // slash: lane owns SQ consecutive diagonals dq .. dq + SQ - 1 and walks
+          // the rows of their union in ascending order (one row-base load per row
+          // for SQ cells; a cell outside a diagonal's own rows reads a zero pad,
+          // so each diagonal's fp32 sum is the same as summing its own rows alone)
+          const int dq = d_lo + 32 * SQ * (task - 4) + SQ * lane;
+          float sw[SQ], mx[SQ];
 #pragma unroll
-        for (int k = 0; k < NQ; ++k) sw[k] = mx[k] = 0.f;
-        const float *pcol = Pf - dq - c0;  // cell (r, g_r - dq - k) at pcol[rbase[r] - k]
+          for (int k = 0; k < SQ; ++k) sw[k] = mx[k] = 0.f;
+          if (dq <= d_hi) {
+            const int glo = c0 + dq, ghi = min(c0 + dq + SQ - 1 + BN - 1, g_hi);
+            int r, r_end;
+            if (use_rp) {
+              r = rp[max(glo, g_first) - g_first];
+              r_end = ghi + 1 <= g_hi ? rp[ghi + 1 - g_first] : nr;
+            } else {
+              r = lower_bound_dev(gs, nr, glo);
+              r_end = lower_bound_dev(gs, nr, ghi + 1);
+            }
+            const float *pcol = Pf - dq - c0;  // cell (r, g_r - dq - k) at pcol[rbase[r] - k]
 #pragma unroll 2
-        for (; r < r_end; ++r) {
-          const float *pp = pcol + rbase[r];
+            for (; r < r_end; ++r) {
+              const float *pp = pcol + rbase[r];
 #pragma unroll
-          for (int k = 0; k < NQ; ++k) {
-            const float v = pp[-k];
-            sw[k] += v;
-            mx[k] = fmaxf(mx[k], v);
+              for (int k = 0; k < SQ; ++k) {
+                const float v = pp[-k];
+                sw[k] += v;
+                mx[k] = fmaxf(mx[k], v);
+              }
+            }
           }
-        }
 #pragma unroll
-        for (int k = 0; k < NQ; ++k) {
-          const int dd = dq + k;
-          if (dd > d_hi) break;
-          if (smem_acc) {
-            acc[dd - d_base] += static_cast<double>(sw[k]);
-            accm[dd - d_base] = fmaxf(accm[dd - d_base], mx[k]);
-          } else if (sw[k] > 0.f) {
-            atomicAdd(sfix + dd, to_fix(static_cast<double>(sw[k])));
-            atomicMax(smaxb + dd, __float_as_uint(mx[k]));
+          for (int k = 0; k < SQ; ++k) {
+            const int dd = dq + k;
+            if (dd > d_hi) break;
+            if (smem_acc) {
+              acc[dd - d_base] += static_cast<double>(sw[k]);
+              accm[dd - d_base] = fmaxf(accm[dd - d_base], mx[k]);
+            } else if (sw[k] > 0.f) {
+              atomicAdd(sfix + dd, to_fix(static_cast<double>(sw[k])));
+              atomicMax(smaxb + dd, __float_as_uint(mx[k]));
+            }
           }
         }
       }
-    }
-    K1REC(5);
-    __syncthreads();
-    K1REC(6);
-    if (tid < BN) {
-      const int c = c0 + tid;
-      if (c < c_end) {
-        const double sw = ((colp[tid] + colp[BN + tid]) + colp[2 * BN + tid]) + colp[3 * BN + tid];
-        const float mx = fmaxf(fmaxf(colm[tid], colm[BN + tid]), fmaxf(colm[2 * BN + tid], colm[3 * BN + tid]));
-        if (sw > 0.0) atomicAdd(p.vfix + static_cast<int64_t>(h) * p.n_total + c, to_fix(sw));
-        if (mx > 0.f) atomicMax(p.vmaxb + static_cast<int64_t>(h) * p.n_total + c, __float_as_uint(mx));
-      }
-    }
-    if (last_in_item || ((c0 + BN) % CHUNK) == 0 || !more) {  // chunk (or slice) done: flush the slash accumulator
+    };
+    auto flush_chunk = [&]() {
       if (smem_acc)
         for (int i = tid; i < width; i += LINES_THREADS) {
           if (acc[i] > 0.0) atomicAdd(sfix + d_base + i, to_fix(acc[i]));
           if (accm[i] > 0.f) atomicMax(smaxb + d_base + i, __float_as_uint(accm[i]));
+          acc[i] = 0.0;
+          accm[i] = 0.f;
         }
-    }
-    if (more) {
-      cur.next(p.tstart);
-      if (last_in_item) {
-        __syncthreads();  // flush / colp reads done before the next item rewrites smem
-        begin_item(t + 1);
-        begin_chunk(cur.j * BN);
-      } else if (((c0 + BN) % CHUNK) == 0) {
-        __syncthreads();  // flush reads done before the next chunk zeroes the accumulator
+    };
+
+    begin_item();
+    begin_chunk(cur.j * BN);
+    exp_tile(0, cur.j * BN);
+    tc::named_sync(1, LINES_THREADS);
+    for (int t = 0; t < n_tiles; ++t) {
+      K1REC(t, 0);
+      const int c0 = cur.j * BN;
+      const bool last_in_item = x0 + t + 1 >= cur.i_end_tile;
+      const bool more = t + 1 < n_tiles;
+      const bool chunk_end = last_in_item || ((c0 + BN) % CHUNK) == 0 || !more;
+      if (more && !last_in_item) exp_tile(t + 1, c0 + BN);  // P(t + 1) while others reduce P(t)
+      K1REC(t, 1);
+      reduce_tile(t, c0);
+      K1REC(t, 2);
+      tc::named_sync(1, LINES_THREADS);  // P(t) reduced, P(t + 1) written
+      K1REC(t, 3);
+      if (chunk_end) {
+        flush_chunk();
+        tc::named_sync(1, LINES_THREADS);  // accumulator re-zeroed before the next chunk's tile
       }
+      if (more) {
+        cur.next(p.tstart);
+        if (last_in_item) {
+          begin_item();
+          begin_chunk(cur.j * BN);
+          exp_tile(t + 1, cur.j * BN);
+          tc::named_sync(1, LINES_THREADS);
+        } else if (chunk_end) {
+          begin_chunk(cur.j * BN);
+        }
+      }
+      K1REC(t, 4);
     }
-    // (no barrier otherwise: every read of Pf precedes the barrier above, and the next
-    // tile writes colp / the slash accumulator only after its own first barrier)
-    K1REC(7);
-  }
 #undef K1REC
+  }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(pp.tmem, 512);
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
 // fixed point -> fp64 line weights; total = exact integer sum of the verticals.
@@ -919,7 +962,7 @@ template <int D>
 int k1_lines_launch(const CUtensorMap &tmk, const k1tc::Params &p, cudaStream_t st) {
   const int s2 = k1tc::LinesSmem<D>::TOTAL + 1024;
   LS_CUDA(cudaFuncSetAttribute(k1tc::k1_lines_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-  k1tc::k1_lines_kernel<D><<<k1tc::sm_count(), k1tc::LINES_THREADS, s2, st>>>(tmk, p);
+  k1tc::k1_lines_kernel<D><<<k1tc::sm_count(), k1tc::LINES_THREADS + 32, s2, st>>>(tmk, p);
   LS_LAUNCH_CHECK("k1_lines_kernel");
   return LS_OK;
 }
