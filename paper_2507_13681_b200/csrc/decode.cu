@@ -759,7 +759,8 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     float *wo = wl + KM_WARPS * 8;
     float *part = S.partials + static_cast<int64_t>(unit) * n_split * G * (D + 2);
     float *gl = reinterpret_cast<float *>(sm + L::OFF_GATHER);  // rank 0's gather area (cluster mode)
-    float *dst = ccombine == 1 ? gl : part + split * G * (D + 2);  // rank 0 keeps its own partial locally
+    const bool solo = n_split == 1;  // the unit's only CTA: its merged partial is the result
+    float *dst = ccombine == 1 || solo ? gl : part + split * G * (D + 2);  // rank 0 keeps its own partial locally
     uint32_t rgl = 0, rbar = 0;
     if (ccombine == 1) {
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
@@ -802,7 +803,10 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     if (rec && tid == 0) rec[4] = gtime();
     int o_begin = 0, o_end = G * D;  // output elements this CTA writes
     bool write_meta = true;
-    if (ccombine == 1) {
+    if (solo) {
+      __syncthreads();  // no other split: combine straight from shared memory
+      part = gl;
+    } else if (ccombine == 1) {
       // the other splits' partials arrive by st.async on rank 0's mbarrier: no
       // cluster barrier (whose release would wait for every CTA's global stores)
       if (split != 0) return;
@@ -934,7 +938,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       S.ring_n[hr * S.window + slot] = geo.n_cols;
       S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
     }
-    if (ccombine == 0 && tid == 0) S.counters[unit] = 0;  // ticket re-armed for the next launch
+    if (ccombine == 0 && !solo && tid == 0) S.counters[unit] = 0;  // ticket re-armed for the next launch
     if (ccombine == 2) {
       // departures: the last CTA to leave re-arms both counters (every CTA has
       // stopped polling the arrival count by then)
@@ -1520,7 +1524,11 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 148;
   }
-  // splits: fill the resident CTA slots (2 per SM at this shared-memory size)
+  // splits: fill the resident CTA slots (2 per SM at this shared-memory size);
+  // compressed steps: ~3 tiles per split while the units leave slots free, one
+  // split per unit once they fill the GPU (C4: 8 sessions x 28 q-heads = 224
+  // units -> one CTA streams a head's whole working set, no combine; measured
+  // 3.25 -> 4.57 TB/s)
   static const int env_split_dense = getenv("LS_K6_SPLIT_DENSE") ? atoi(getenv("LS_K6_SPLIT_DENSE")) : 0;
   static const int env_split_comp = getenv("LS_K6_SPLIT_COMP") ? atoi(getenv("LS_K6_SPLIT_COMP")) : 0;
   static const int env_cta_mult = getenv("LS_K6_CTAS_PER_SM") ? atoi(getenv("LS_K6_CTAS_PER_SM")) : 1;
@@ -1529,7 +1537,7 @@ static int launch_decode_mma(int units, int max_cols, cudaStream_t st, const ls_
   const int tiles = ceil_div(max_cols, tile) + 1;  // + the segment boundary
   // dense: one CTA per SM; compressed: ~3 tiles per split (one cluster per unit)
   int n_split = env_split > 0 ? env_split
-                : compressed ? std::min(8, ceil_div(tiles, 3))
+                : compressed ? std::max(1, std::min({8, ceil_div(tiles, 3), 2 * n_sm / units}))
                              : std::max(1, env_cta_mult * n_sm / units);
   n_split = std::max(1, std::min({n_split, tiles, dec::KM_MAX_SPLIT}));
   // splits combine in rank 0's shared memory when they fit one portable cluster
