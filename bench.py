@@ -309,6 +309,8 @@ def run_reference(args, cfg):
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
+    if args.config != "c2":  # the committed ncu captures are of the C2 workload
+        NCU_TRAFFIC.clear()
     if args.impl == "reference":
         run_reference(args, cfg)
         return
