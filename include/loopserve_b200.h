@@ -238,7 +238,10 @@ int ls_plan_coverage(const ls_layer_desc *L, const uint16_t *q, const uint16_t *
  *   ring_ml  [hr][window][2]        fp32 (max, sum) of the row; sum == 0 means
  *                                   ring_s holds probabilities (prefill seeds)
  *   ring_ids [hr][window][sparse_cap] int32 ids of compressed rows
- *   ring_n, ring_dense [hr][window] int32
+ *   ring_n, ring_dense [hr][window] int32; ring_dense: 1 = dense row (ids 0..n-1),
+ *            0 = ids in ring_ids, LS_RING_WORKING_SET = the working set of the
+ *            current selection (ids: sel_ids[0, n_a) then lo, lo+1, ...; n_a and
+ *            lo in ring_ids[0..1]) -- valid until the next compression event
  *   sel_ids  [hr][budget_cap], n_sel [hr]      picked ids (kvcompress.py:212)
  *   ck, cv   [hr][budget_cap][head_dim] bf16   compacted K/V of sel_ids
  *   partials [ls_decode_partials_size() bytes] fp32 split-K partials of a decode step
@@ -285,6 +288,11 @@ int ls_decode_step(const ls_decode_stack *S, int32_t layer, const uint16_t *q, c
  * (its K/V tile prefetch overlaps that kernel's tail; q and all writes wait
  * for it, as the next layer of a full model would). */
 #define LS_DECODE_PDL 1
+/* compressed rows record (n_a, lo) and K7 derives their ids from the current
+ * selection (no per-column id writes): only when every buffered row is consumed
+ * before the selection changes again, i.e. interval >= obs_window */
+#define LS_DECODE_DERIVED_IDS 2
+#define LS_RING_WORKING_SET 2
 int ls_decode_step_archive(const ls_decode_stack *S, int32_t layer, const uint16_t *q_layer,
                            int64_t q_head_stride, const uint16_t *k_layer, const uint16_t *v_layer,
                            int32_t compressed, int32_t max_cols, void *out, int32_t out_bf16, int32_t flags,

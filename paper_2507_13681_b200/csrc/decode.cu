@@ -575,7 +575,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
     for (int k = 0; k < MAXPF; ++k) {
       id_pf[k] = 0;
       const int i = grp + k * NG;
-      if (compressed && i < n_my && lane < RPW) {
+      if (compressed == 1 && i < n_my && lane < RPW) {
         const KmTile x = km_tile<KM_TILE>(t_begin + i, t_a, geo);
         if (wr0 + lane < x.valid)
           id_pf[k] = x.seg_a ? __ldg(S.sel_ids + hr0 * S.budget_cap + x.row0 + wr0 + lane) : x.row0 + wr0 + lane;
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       // first MAXPF tiles, else fetched before the data wait
       const int kt = (i - grp) / NG;
       int id = kt == 0 ? id_pf[0] : kt == 1 ? id_pf[1] : kt == 2 ? id_pf[2] : id_pf[3];
-      if (kt >= MAXPF && compressed && lane < RPW && wr0 + lane < x.valid)
+      if (kt >= MAXPF && compressed == 1 && lane < RPW && wr0 + lane < x.valid)
         id = x.seg_a ? __ldg(S.sel_ids + hr0 * S.budget_cap + x.row0 + wr0 + lane) : x.row0 + wr0 + lane;
       tc::mbar_wait(&full[st], (i / NST) & 1);
       if (rec && tid == 0 && i == 0) rec[2] = gtime();
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
           if (r + 1 < x.valid) ring_row[x.j0 + r + 1] = xs[n][1];
         }
       }
-      if (compressed && lane < RPW && wr0 + lane < x.valid) {
+      if (compressed == 1 && lane < RPW && wr0 + lane < x.valid) {  // (2: ids derived by K7)
         const int r = wr0 + lane;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg)
@@ -936,7 +936,11 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       S.ring_ml[(hr * S.window + slot) * 2 + 0] = mg[tid];
       S.ring_ml[(hr * S.window + slot) * 2 + 1] = mg[8 + tid];
       S.ring_n[hr * S.window + slot] = geo.n_cols;
-      S.ring_dense[hr * S.window + slot] = compressed ? 0 : 1;
+      S.ring_dense[hr * S.window + slot] = compressed == 2 ? LS_RING_WORKING_SET : compressed ? 0 : 1;
+      if (compressed == 2) {  // the row's ids follow from the current selection: n_a and the window start
+        S.ring_ids[(hr * S.window + slot) * S.sparse_cap + 0] = geo.n_a;
+        S.ring_ids[(hr * S.window + slot) * S.sparse_cap + 1] = geo.lo;
+      }
     }
     if (ccombine == 0 && !solo && tid == 0) S.counters[unit] = 0;  // ticket re-armed for the next launch
     if (ccombine == 2) {
@@ -1046,6 +1050,12 @@ __device__ __forceinline__ int gtime32() {
   return static_cast<int>(t & 0x7fffffffull);
 }
 
+// id of working-set column j of a LS_RING_WORKING_SET row (decode_mma_kernel's
+// column order): the first n_a picked ids, then the archive window from lo
+__device__ __forceinline__ int working_id(const ls_decode_stack &S, int64_t hr, int na, int lo, int j) {
+  return j < na ? __ldg(S.sel_ids + hr * S.budget_cap + j) : lo + (j - na);
+}
+
 __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, int budget, double *acc_ws,
                                                             uint32_t *touched_ws, int use_smem, int32_t *retained_n,
                                                             double *score_cov, int *dbg) {
@@ -1081,7 +1091,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   // owned by one thread, which adds the rows in order from registers -- all of
   // a chunk's row values are loaded at once and no block barrier runs per row
   __shared__ int64_t d_so[K7_DMAX];
-  __shared__ int d_n[K7_DMAX], d_dense[K7_DMAX];
+  __shared__ int d_n[K7_DMAX], d_dense[K7_DMAX], d_na[K7_DMAX], d_lo[K7_DMAX];
   __shared__ float d_m[K7_DMAX], d_l[K7_DMAX], d_inv[K7_DMAX];
   __shared__ int d_all;
   if (threadIdx.x == 0) d_all = n_rows <= K7_DMAX;
@@ -1094,7 +1104,11 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     d_l[threadIdx.x] = S.ring_ml[so * 2 + 1];
     d_inv[threadIdx.x] = d_l[threadIdx.x] > 0.f ? 1.f / d_l[threadIdx.x] : 0.f;
     d_dense[threadIdx.x] = S.ring_dense[so];
-    if (!d_dense[threadIdx.x]) d_all = 0;
+    if (d_dense[threadIdx.x] == LS_RING_WORKING_SET) {
+      d_na[threadIdx.x] = S.ring_ids[so * S.sparse_cap + 0];
+      d_lo[threadIdx.x] = S.ring_ids[so * S.sparse_cap + 1];
+    }
+    if (d_dense[threadIdx.x] != 1) d_all = 0;
   }
   __syncthreads();
   const bool all_dense = d_all != 0;
@@ -1129,7 +1143,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
     const int nr = min(K7_RB, n_rows - r0);
     // row metadata of the round (one round trip: slots are always valid indices)
     int64_t so_r[K7_RB];
-    int n_r[K7_RB], dense_r[K7_RB];
+    int n_r[K7_RB], dense_r[K7_RB], na_r[K7_RB], lo_r[K7_RB];
     float m_r[K7_RB], l_r[K7_RB];
     int nmax = 0;
 #pragma unroll
@@ -1139,12 +1153,16 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
         so_r[rr] = d_so[R];
         n_r[rr] = d_n[R];
         dense_r[rr] = d_dense[R];
+        na_r[rr] = d_na[R];
+        lo_r[rr] = d_lo[R];
         m_r[rr] = d_m[R];
         l_r[rr] = d_l[R];
       } else {
         so_r[rr] = hr * S.window + (appended - n_rows + R) % S.window;
         n_r[rr] = __ldg(S.ring_n + so_r[rr]);
         dense_r[rr] = __ldg(S.ring_dense + so_r[rr]);
+        na_r[rr] = __ldg(S.ring_ids + so_r[rr] * S.sparse_cap + 0);
+        lo_r[rr] = __ldg(S.ring_ids + so_r[rr] * S.sparse_cap + 1);
         m_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2);
         l_r[rr] = __ldg(S.ring_ml + so_r[rr] * 2 + 1);
       }
@@ -1165,7 +1183,10 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
         for (int e = 0; e < K7_PF; ++e) {
           const int j = threadIdx.x + e * blockDim.x;
           const bool ok = j < n_r[rr];
-          iv[rr][e] = !ok ? -1 : dense_r[rr] ? j : __ldg(S.ring_ids + so_r[rr] * S.sparse_cap + j);
+          iv[rr][e] = !ok                                   ? -1
+                      : dense_r[rr] == 1                    ? j
+                      : dense_r[rr] == LS_RING_WORKING_SET  ? working_id(S, hr, na_r[rr], lo_r[rr], j)
+                                                            : __ldg(S.ring_ids + so_r[rr] * S.sparse_cap + j);
           sv_r[rr][e] = ok ? __ldg(S.ring_s + so_r[rr] * S.row_cap + j) : 0.f;
         }
       if (rec && r0 == 0) rec[9] = gtime32() + 0 * __float_as_int(sv_r[0][0]) + 0 * iv[0][0];
@@ -1193,8 +1214,9 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
         const float inv = Lr > 0.f ? 1.f / Lr : 0.f;
         const float *sr = S.ring_s + so * S.row_cap;
         const int32_t *ids = S.ring_ids + so * S.sparse_cap;
+        const int na = ids[0], lo = ids[1];
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
-          const int id = dense ? j : ids[j];
+          const int id = dense == 1 ? j : dense == LS_RING_WORKING_SET ? working_id(S, hr, na, lo, j) : ids[j];
           acc[id] += static_cast<double>(row_weight(sr[j], M, Lr, inv));
           atomicOr(touched + (id >> 5), 1u << (id & 31));
         }
@@ -1678,7 +1700,9 @@ extern "C" int ls_decode_step_archive(const ls_decode_stack *S, int32_t layer, c
                                       int64_t q_head_stride, const uint16_t *k_layer, const uint16_t *v_layer,
                                       int32_t compressed, int32_t max_cols, void *out, int32_t out_bf16,
                                       int32_t flags, ls_stream_t stream) {
-  return decode_step_impl(S, layer, q_layer, q_head_stride, 1, k_layer, v_layer, compressed, max_cols, out, out_bf16,
+  // LS_DECODE_DERIVED_IDS: compressed rows record (n_a, lo) instead of their ids
+  const int32_t kind = compressed && (flags & LS_DECODE_DERIVED_IDS) ? 2 : compressed ? 1 : 0;
+  return decode_step_impl(S, layer, q_layer, q_head_stride, 1, k_layer, v_layer, kind, max_cols, out, out_bf16,
                           (flags & LS_DECODE_PDL) ? 1 : 0, stream);
 }
 

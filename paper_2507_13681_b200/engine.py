@@ -187,6 +187,11 @@ class SessionEngine:
         self.ws = Workspace()
         self.rows_ws = Workspace()
         self.stack.event_workspace(self.stack.row_cap)  # fixed before any graph captures it
+        # observation rows of compressed steps carry (n_a, lo) instead of their ids when
+        # each row is consumed by one event only (interval >= window, kvcompress.py:196)
+        import os as _os
+        self.stack.derived_ids = (comp.budget is not None and comp.interval >= self.window
+                                  and _os.environ.get("LS_DERIVED_IDS", "1") != "0")
         self._q_buf = torch.empty((shape.n_layers, shape.n_q, 1, shape.d), dtype=torch.bfloat16, device=device)
         self._out_buf = torch.empty((shape.n_layers, shape.n_q, shape.d), dtype=out_dtype, device=device)
         self._graphs = {}

@@ -92,6 +92,9 @@ class KVCacheHead:
             raise InvalidIds("row count does not match retained_ids")
 
 
+RING_WORKING_SET = 2  # ring_dense kind: ids derived from the selection (LS_RING_WORKING_SET)
+
+
 class DecodeStack:
     """Device decode state of every layer of one session (ls_decode_stack):
     observation ring (the deque of kvcompress.py:196) per (layer, q-head),
@@ -131,6 +134,11 @@ class DecodeStack:
         self.partials = torch.zeros(max(1, n_part), dtype=f32, device=dev)
         self.desc.partials = self.partials.data_ptr()
         self.ws = Workspace()
+        # compressed steps record (n_a, lo) per observation row instead of its ids
+        # (K7 derives them from the selection): only valid when every buffered
+        # row is consumed before the next selection, i.e. interval >= window;
+        # the owner (SessionEngine) sets it from its CompressionConfig
+        self.derived_ids = False
         self.set_step(0, 0)
 
     # ---------------------------------------------------------------- counters
@@ -198,9 +206,10 @@ class DecodeStack:
         """K6 for one layer with q read from the layer's Q archive [H, cap, d]
         at the current cache length (no per-step q gather); pdl: programmatic
         dependent launch after the previous kernel on the stream."""
+        flags = (1 if pdl else 0) | (2 if self.derived_ids else 0)  # LS_DECODE_PDL, LS_DECODE_DERIVED_IDS
         _lib.call("ls_decode_step_archive", ctypes.byref(self.desc), int(layer), q_layer.data_ptr(),
                   int(q_layer.stride(0)), k_layer.data_ptr(), v_layer.data_ptr(), int(bool(compressed)),
-                  int(max_cols), out.data_ptr(), int(out.dtype == torch.bfloat16), 1 if pdl else 0,
+                  int(max_cols), out.data_ptr(), int(out.dtype == torch.bfloat16), flags,
                   _lib.stream_ptr(stream))
 
     def advance(self, stream=None):
@@ -227,8 +236,13 @@ class DecodeStack:
         s = self.ring_s[hr, slot, :n].double().cpu().numpy()
         M, Ls = (float(x) for x in self.ring_ml[hr, slot].cpu().numpy())
         w = s if Ls == 0.0 else np.exp2(s - M) / Ls
-        if int(self.ring_dense[hr, slot].item()):
+        kind = int(self.ring_dense[hr, slot].item())
+        if kind == 1:
             return np.arange(n), w
+        if kind == RING_WORKING_SET:  # ids from the current selection: sel_ids[:n_a] then lo, lo + 1, ...
+            n_a, lo = (int(x) for x in self.ring_ids[hr, slot, :2].cpu().numpy())
+            sel = self.sel_ids[hr, :n_a].cpu().numpy().astype(np.intp)
+            return np.concatenate([sel, lo + np.arange(n - n_a)]), w
         return self.ring_ids[hr, slot, :n].cpu().numpy().astype(np.intp), w
 
 
