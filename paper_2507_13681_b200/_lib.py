@@ -127,7 +127,7 @@ KERNELS_PER_CALL = {
     "ls_greedy_dense": 5,
     "ls_vs_attention": 3, "ls_vs_attention_ex": 3, "ls_vs_attention_simt": 3, "ls_plan_rows": 4, "ls_dense_attention": 1,
     "ls_plan_coverage": 7,
-    "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 2,
+    "ls_decode_step": 1, "ls_decode_step_archive": 1, "ls_decode_advance": 1, "ls_decode_event": 3,
     "ls_accumulate_scores": 1, "ls_top_by_score": 1, "ls_retained_union": 1, "ls_kv_compact": 1,
     "ls_gather_attention": 1, "ls_obs_window_scores": 1, "ls_gather_rows": 1,
 }

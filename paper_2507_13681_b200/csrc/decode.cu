@@ -1050,6 +1050,55 @@ __device__ __forceinline__ int gtime32() {
   return static_cast<int>(t & 0x7fffffffull);
 }
 
+// ------------------------------------------------------------------ K7, working-set events
+// Every event after the first one buffers only rows that decode_mma_kernel wrote
+// as LS_RING_WORKING_SET (interval >= window): row r covers the current picks
+// below its window start, sel_ids[0, na_r), then the positions [lo_r, L_r]. The
+// touched ids are then known without a bitmap: candidates c < n0 (= na of the
+// oldest row) are sel_ids[c], the rest are the positions lo_0 + (c - n0) up to
+// the newest row's end, and every one of them is touched (the windows overlap).
+// A CTA (256 threads, ~cap * 12 B of shared memory) owns candidates, adds the
+// rows' weights oldest -> newest in fp64 (the reference's order,
+// kvcompress.py:75-79), finds the B-th (score desc, id asc) key by a radix select and
+// writes the picks as select_kernel does (same scores and picks; the coverage
+// masses summed over another thread partition). A (layer, head) whose rows are not all
+// working-set rows, or with more than `cap` candidates, is left to
+// select_kernel, which skips the heads handled here.
+struct WsEvent {
+  bool ok;
+  int n_rows, n0, lo0, n_cand;
+};
+// called by every thread of the block (thread r reads row r's record; one round trip)
+__device__ WsEvent ws_event(const ls_decode_stack &S, int64_t hr, int cap) {
+  __shared__ int w_first[2], w_last_end;
+  WsEvent e;
+  const int appended = S.step[1];
+  e.n_rows = min(S.window, appended);
+  const int r = threadIdx.x;
+  bool mine = true;
+  if (r < e.n_rows) {
+    const int64_t so = hr * S.window + (appended - e.n_rows + r) % S.window;
+    const int kind = __ldg(S.ring_dense + so);
+    const int na = __ldg(S.ring_ids + so * S.sparse_cap), lo = __ldg(S.ring_ids + so * S.sparse_cap + 1);
+    const int n = __ldg(S.ring_n + so);
+    mine = kind == LS_RING_WORKING_SET;
+    if (r == 0) {
+      w_first[0] = na;
+      w_first[1] = lo;
+    }
+    if (r == e.n_rows - 1) w_last_end = lo + (n - na) - 1;  // the newest row's last position
+  }
+  e.ok = __syncthreads_and(mine) && e.n_rows > 0 && e.n_rows <= K7_DMAX;
+  if (e.ok) {
+    e.n0 = w_first[0];
+    e.lo0 = w_first[1];
+    e.n_cand = e.n0 + (w_last_end - e.lo0 + 1);
+    e.ok = e.n_cand <= cap;
+  }
+  __syncthreads();  // the records may be reused by the next call
+  return e;
+}
+
 // id of working-set column j of a LS_RING_WORKING_SET row (decode_mma_kernel's
 // column order): the first n_a picked ids, then the archive window from lo
 __device__ __forceinline__ int working_id(const ls_decode_stack &S, int64_t hr, int na, int lo, int j) {
@@ -1058,7 +1107,7 @@ __device__ __forceinline__ int working_id(const ls_decode_stack &S, int64_t hr, 
 
 __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, int budget, double *acc_ws,
                                                             uint32_t *touched_ws, int use_smem, int32_t *retained_n,
-                                                            double *score_cov, int *dbg) {
+                                                            double *score_cov, int *dbg, int ws_cap) {
   extern __shared__ __align__(16) unsigned char smem7[];
   __shared__ int hist[256];
   __shared__ int shi[32];
@@ -1066,6 +1115,7 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   __shared__ int s_digit, s_above;
   const int h = blockIdx.x, layer = blockIdx.y;
   const int64_t hr = head_row(S, layer, h);
+  if (ws_cap > 0 && ws_event(S, hr, ws_cap).ok) return;  // handled by select_ws_kernel (same test)
   const int length = S.step[0];
   const int appended = S.step[1];
   const int n_rows = min(S.window, appended);
@@ -1407,6 +1457,167 @@ __global__ void __launch_bounds__(K7_THREADS) select_kernel(ls_decode_stack S, i
   if (rec) rec[6] = gtime32();
 }
 
+constexpr int K7W_THREADS = 256;  // small CTAs: four per SM keep the sort's barriers overlapped
+__global__ void __launch_bounds__(K7W_THREADS) select_ws_kernel(ls_decode_stack S, int budget, int cap,
+                                                               int32_t *retained_n, double *score_cov) {
+  extern __shared__ __align__(16) unsigned char smws[];
+  __shared__ int shi[32];
+  __shared__ double shd[32];
+  __shared__ int hist[256];
+  __shared__ int s_digit, s_above;
+  __shared__ int64_t r_so[K7_DMAX];
+  __shared__ int r_na[K7_DMAX], r_lo[K7_DMAX], r_end[K7_DMAX];
+  __shared__ float r_m[K7_DMAX], r_inv[K7_DMAX];
+  const int h = blockIdx.x, layer = blockIdx.y;
+  const int64_t hr = head_row(S, layer, h);
+  const WsEvent e = ws_event(S, hr, cap);
+  if (!e.ok) return;
+  const int n_rows = e.n_rows, n0 = e.n0, lo0 = e.lo0, n_cand = e.n_cand;
+  const int length = S.step[0], appended = S.step[1];
+  double *acc = reinterpret_cast<double *>(smws);          // [cap] scores
+  int32_t *cid = reinterpret_cast<int32_t *>(acc + cap);   // [cap] candidate ids
+  int32_t *srank = cid + cap;                              // [window + 1] pick index of a position
+  const int32_t *sel_in = S.sel_ids + hr * S.budget_cap;
+  if (threadIdx.x < n_rows) {
+    const int r = threadIdx.x;
+    const int64_t so = hr * S.window + (appended - n_rows + r) % S.window;
+    r_so[r] = so;
+    r_na[r] = S.ring_ids[so * S.sparse_cap];
+    r_lo[r] = S.ring_ids[so * S.sparse_cap + 1];
+    r_end[r] = r_lo[r] + (S.ring_n[so] - r_na[r]) - 1;
+    r_m[r] = S.ring_ml[so * 2];
+    const float l = S.ring_ml[so * 2 + 1];
+    r_inv[r] = l > 0.f ? 1.f / l : 0.f;  // (select_kernel's row weight)
+  }
+  __syncthreads();
+  // positions below a later row's window start appear in it only if picked:
+  // srank[p - lo0] = the pick's column there (its index in sel_ids), or -1
+  const int span = r_lo[n_rows - 1] - lo0;
+  for (int p = threadIdx.x; p < span; p += blockDim.x) srank[p] = -1;
+  __syncthreads();
+  for (int k = n0 + threadIdx.x; k < r_na[n_rows - 1]; k += blockDim.x) srank[sel_in[k] - lo0] = k;
+  __syncthreads();
+  // scores: one thread per candidate, rows oldest -> newest in fp64
+  for (int c = threadIdx.x; c < n_cand; c += blockDim.x) {
+    const int p = c < n0 ? -1 : lo0 + (c - n0);
+    cid[c] = c < n0 ? sel_in[c] : p;
+    double a = 0.0;
+    for (int r0 = 0; r0 < n_rows; r0 += K7_RB) {
+      float v[K7_RB];
+      bool in[K7_RB];
+#pragma unroll
+      for (int u = 0; u < K7_RB; ++u) {  // the round's loads first
+        const int r = r0 + u;
+        int j = -1;
+        if (r < n_rows) {
+          if (c < n0) j = c;
+          else if (p >= r_lo[r]) j = p <= r_end[r] ? r_na[r] + (p - r_lo[r]) : -1;
+          else j = srank[p - lo0];
+        }
+        in[u] = j >= 0;
+        v[u] = in[u] ? __ldg(S.ring_s + r_so[r] * S.row_cap + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < K7_RB; ++u)
+        if (in[u]) a += static_cast<double>(fast_exp2(v[u] - r_m[r0 + u]) * r_inv[r0 + u]);
+    }
+    acc[c] = a;
+  }
+  __syncthreads();
+  const bool take_all = budget >= n_cand;
+  // the B-th key of (score desc, id asc) by an MSD radix select over the
+  // candidates (8-bit digits of the monotone fp64 key): picks are keys above
+  // it plus the lowest-id `need` of the keys equal to it (candidate order is id order)
+  unsigned long long prefix = 0ull, pmask = 0ull;
+  int need = budget;
+  if (!take_all) {
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int k = threadIdx.x; k < n_cand; k += blockDim.x) {
+        const unsigned long long key = dkey(acc[k]);
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {  // warp scan from the top digit down
+        const int lane = threadIdx.x;
+        int cnt[8], loc = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          cnt[t] = hist[255 - (lane * 8 + t)];
+          loc += cnt[t];
+        }
+        int incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int excl = incl - loc;
+        const unsigned hb = __ballot_sync(0xffffffffu, excl < need && incl >= need);
+        if (lane == __ffs(hb) - 1) {
+          int above = excl;
+          for (int t = 0; t < 8; ++t) {
+            if (above + cnt[t] >= need) {
+              s_digit = 255 - (lane * 8 + t);
+              s_above = above;
+              break;
+            }
+            above += cnt[t];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= static_cast<unsigned long long>(s_digit) << shift;
+      pmask |= 0xffull << shift;
+      need -= s_above;
+      __syncthreads();
+    }
+  }
+  // picks in id order + the event-log fields, as select_kernel (the coverage
+  // masses are fp64 sums over a different thread partition: equal up to rounding)
+  int32_t *sel = S.sel_ids + hr * S.budget_cap;
+  int base = 0, eq_seen = 0;
+  double tot_mass = 0.0, kept_mass = 0.0;
+  int in_window_picked = 0;
+  const int lo = max(0, length - S.window);
+  for (int i0 = 0; i0 < n_cand; i0 += blockDim.x) {
+    const int k = i0 + threadIdx.x;
+    const int is_t = k < n_cand;
+    const int id = is_t ? cid[k] : length;
+    const double scv = is_t ? acc[k] : 0.0;
+    const unsigned long long key = dkey(scv);
+    const int is_gt = is_t && !take_all && key > prefix, is_eq = is_t && !take_all && key == prefix;
+    int eq_tot;
+    const int eq_rank = block_rank(is_eq, shi, &eq_tot);
+    const int pick = take_all ? is_t : (is_gt || (is_eq && eq_seen + eq_rank < need));
+    eq_seen += eq_tot;
+    int pick_tot;
+    const int rank = block_rank(pick, shi, &pick_tot);
+    if (pick) sel[base + rank] = id;
+    if (is_t) {
+      tot_mass += scv;
+      if (pick || id >= lo) kept_mass += scv;  // kvcompress.py:215 (working = picked U recent)
+    }
+    if (pick && id >= lo) in_window_picked += 1;
+    base += pick_tot;
+  }
+  const double T = block_sum_double(tot_mass, shd);
+  const double Kp = block_sum_double(kept_mass, shd);
+  const int iw = block_sum_int(in_window_picked, shi);
+  {
+    int below = 0;
+    for (int j = threadIdx.x; j < base; j += blockDim.x) below += sel[j] < lo ? 1 : 0;
+    below = block_sum_int(below, shi);
+    if (threadIdx.x == 0) S.n_a[hr] = below;
+  }
+  if (threadIdx.x == 0) {
+    S.n_sel[hr] = base;
+    if (retained_n) retained_n[hr] = base + (length - lo) - iw;
+    if (score_cov) score_cov[hr] = T > 0 ? Kp / T : 1.0;
+  }
+}
+
 // ------------------------------------------------------------------ K8
 __global__ void compact_kernel(ls_decode_stack S, const uint16_t *k, const uint16_t *v) {
   const int h = blockIdx.y, layer = blockIdx.z;
@@ -1738,8 +1949,24 @@ extern "C" int ls_decode_event(const ls_decode_stack *S, int32_t budget, int32_t
       smem ? static_cast<size_t>(dec::K7_SMEM_CAP) * 8 + dec::K7_SMEM_CAP / 8 + 64 + dec::K7_CAND_CAP * 4 : 0;
   if (dyn > 48 * 1024)
     LS_CUDA(cudaFuncSetAttribute(dec::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+  // working-set events (all buffered rows LS_RING_WORKING_SET, <= ws_cap candidates:
+  // budget + 2 window) first; select_kernel takes the other heads
+  int ws_cap = 1;
+  while (ws_cap < budget + 2 * S->window + 2) ws_cap <<= 1;
+  static const bool env_no_ws = getenv("LS_K7_NO_WS") != nullptr;  // (A/B: select_kernel for every head)
+  if (ws_cap > 4096 || S->window >= dec::K7_DMAX || env_no_ws) ws_cap = 0;
+  if (ws_cap > 0) {
+    const size_t dyn_ws = static_cast<size_t>(ws_cap) * 12 + static_cast<size_t>(S->window + 2) * 4;
+    if (dyn_ws > 48 * 1024)
+      LS_CUDA(cudaFuncSetAttribute(dec::select_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(dyn_ws)));
+    dec::select_ws_kernel<<<dim3(S->n_heads, S->n_layers), dec::K7W_THREADS, dyn_ws, st>>>(*S, budget, ws_cap,
+                                                                                          retained_n, score_coverage);
+    LS_LAUNCH_CHECK("select_ws_kernel");
+  }
   dec::select_kernel<<<dim3(S->n_heads, S->n_layers), dec::K7_THREADS, dyn, st>>>(*S, budget, acc, touched, smem ? 1 : 0,
-                                                                                   retained_n, score_coverage, g_debug_buffer);
+                                                                                   retained_n, score_coverage, g_debug_buffer,
+                                                                                   ws_cap);
   LS_LAUNCH_CHECK("select_kernel");
   dec::compact_kernel<<<dim3(16, S->n_heads, S->n_layers), 256, 0, st>>>(*S, k_all, v_all);
   LS_LAUNCH_CHECK("compact_kernel");
