@@ -518,9 +518,10 @@ def event_roofline(per, cfg, eng, shape, blocks, peaks):
     """Compression events (one graph: K7 select + K8 compaction, all layers)
     against HBM. Algorithmic bytes of the turn's events:
     K7 reads every buffered row once -- dense rows (prefill seeds, pre-event
-    steps) 4 B per column, compressed rows 8 B (logit + id) over B + W + 1
-    columns -- and K8 reads and writes every selected K and V row:
-    2 * 2 * B * d * 2 B per (layer, q-head)."""
+    steps) 4 B per column; compressed rows 4 B per logit over B + W + 1 columns
+    plus the B picked ids once (the rows' ids derive from the selection when
+    interval >= window, else 4 B more per column) -- and K8 reads and writes
+    every selected K and V row: 2 * 2 * B * d * 2 B per (layer, q-head)."""
     name = "decode_graph_event"
     if name not in per or not cfg.get("budget"):
         return None
@@ -533,6 +534,8 @@ def event_roofline(per, cfg, eng, shape, blocks, peaks):
             L = L0 + n_o - 1
             if n_o == cfg["warmup"]:  # seeds and dense steps: every column
                 k7 = sum(4.0 * (L0 + t) for t in range(max(0, n_o - W), n_o))
+            elif cfg["interval"] >= W:  # working-set rows (LS_RING_WORKING_SET)
+                k7 = W * 4.0 * (B + W + 1) + 4.0 * B
             else:
                 k7 = W * 8.0 * (B + W + 1)
             k8 = 2 * 2 * min(B, L) * d * 2.0

@@ -6,7 +6,7 @@ set -u
 OUT=gpurun_out; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
 python -c 'import __graft_entry__ as g; g.build()' > $OUT/build.log 2>&1 || { tail -30 $OUT/build.log; exit 1; }
-OURS='^(sample_rows|k1_|sort_prefix|sort_block|greedy|plan_bits|compact_bits|gather_vert|vert_bits|reverse_bits|vs_attention|plan_scores|plan_norm|decode_mma|advance_kernel|select_kernel|compact_kernel|set_bits)'
+OURS='^(sample_rows|k1_|sort_prefix|sort_block|greedy|plan_bits|compact_bits|gather_vert|vert_bits|reverse_bits|vs_attention|plan_scores|plan_norm|decode_mma|advance_kernel|select_kernel|select_ws_kernel|compact_kernel|set_bits)'
 for s in ${STAGES:-tests smoke bench ref launches full}; do
   case $s in
     tests) timeout 1500 python -m pytest tests -m gpu -q > $OUT/tests_gpu.log 2>&1; echo "tests rc=$?"; tail -2 $OUT/tests_gpu.log;;
@@ -17,7 +17,7 @@ for s in ${STAGES:-tests smoke bench ref launches full}; do
                 --log-file $OUT/launches.csv python tools/one_turn.py > $OUT/launches.log 2>&1; echo "launches rc=$?";;
     full)
       for ks in "vs_attention_ws_kernel 8" "k1_lines_kernel 8" "k1_stats_kernel 8" "greedy_kernel 16" "sort_prefix_kernel 8" \
-                "decode_mma_kernel 200" "decode_mma_kernel 1500" "select_kernel 2" "compact_kernel 2"; do
+                "decode_mma_kernel 200" "decode_mma_kernel 1500" "select_ws_kernel 2" "select_kernel 2" "compact_kernel 2"; do
         set -- $ks
         timeout 600 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
           -o $OUT/full_${1}_$2 -f python tools/one_turn.py > $OUT/full_${1}_$2.log 2>&1; echo "full $1 $2 rc=$?"

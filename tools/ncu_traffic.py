@@ -66,10 +66,15 @@ def main():
         "source": f"{kl['source']} + {ks['source']} (C2 turn 3, layer 8)"}
     sel = metrics(f"{g}/full_select_kernel_2.ncu-rep", BASE)
     cmp_ = metrics(f"{g}/full_compact_kernel_2.ncu-rep", BASE)
-    out["decode_graph_event"] = {"dram_bytes_per_launch": round(sel["dram_bytes"] + cmp_["dram_bytes"]),
+    ws_path = f"{g}/full_select_ws_kernel_2.ncu-rep"  # working-set events (K7 fast path)
+    ws = metrics(ws_path, BASE) if os.path.exists(ws_path) else {"dram_bytes": 0.0, "gpu__time_duration.sum": 0.0,
+                                                                  "source": "-"}
+    out["decode_graph_event"] = {"dram_bytes_per_launch": round(ws["dram_bytes"] + sel["dram_bytes"] + cmp_["dram_bytes"]),
+                                 "select_ws_us": round(ws["gpu__time_duration.sum"] * 1e6, 3),
                                  "select_us": round(sel["gpu__time_duration.sum"] * 1e6, 3),
                                  "compact_us": round(cmp_["gpu__time_duration.sum"] * 1e6, 3),
-                                 "source": f"{sel['source']} + {cmp_['source']} (3rd event of the C2 turn-3 decode)"}
+                                 "source": f"{ws['source']} + {sel['source']} + {cmp_['source']} "
+                                           "(3rd event of the C2 turn-3 decode)"}
     with open(os.path.join("profiles", "ncu_traffic.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print(json.dumps(out, indent=1))
