@@ -437,6 +437,15 @@ __device__ __forceinline__ void mma_16816(float *d, uint32_t a0, uint32_t a2, ui
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+// D += A B, m16n8k16 bf16 -> fp32, all four A registers
+__device__ __forceinline__ void mma_16816_a4(float *d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                             uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t *>(&h);
@@ -503,6 +512,7 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
   using L = KmSmem<D, NST, NW, NG, RPW>;
   constexpr int KM_TILE = L::TILE, KM_WARPS = NW * NG, KM_THREADS = (NW * NG + 1) * 32;
   constexpr int NT = D / 8;  // n-tiles of 8 dims in O
+  constexpr bool SWAP = G == 1 && RPW == 16;  // one q-head: K / V as the A operands (see the tile loop)
   extern __shared__ unsigned char km_dyn[];
   unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(km_dyn) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + L::OFF_BAR);
@@ -621,6 +631,72 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
         tc::fence_proxy_async();  // the stage is refilled by TMA (async proxy) later
         __syncwarp();
       }
+      if constexpr (SWAP) {
+        // one q-head: the K / V tiles are the A operands and q / P the B
+        // column (n = 0), halving the MMAs of the m16 q-row form (15 of whose 16
+        // A rows are zero). S^T = K q^T: C rows = this warp's 16 key rows;
+        // column 0 (lanes t4 == 0) holds rows g (c0) and g + 8 (c2). The
+        // B-operand ldmatrix fragments of the q-row form are the A fragments
+        // here with the middle pair swapped; k-steps in the same two chains.
+        uint32_t fb[D / 16][4];
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          ldsm_x4(fb[kk], ks + km_off<KM_TILE>(wr0 + (m8 >> 1) * 8 + r8, 2 * kk + (m8 & 1)));
+        float cs[4] = {0.f, 0.f, 0.f, 0.f}, cd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < D / 16; kk += 2) {
+          mma_16816_a4(cs, fb[kk][0], fb[kk][2], fb[kk][1], fb[kk][3], qa[kk][0], qa[kk][1]);
+          mma_16816_a4(cd, fb[kk + 1][0], fb[kk + 1][2], fb[kk + 1][1], fb[kk + 1][3], qa[kk + 1][0], qa[kk + 1][1]);
+        }
+        cs[0] += cd[0];
+        cs[2] += cd[2];
+        // V^T fragments (ldmatrix.trans; A = dims x rows) in flight while the softmax runs
+#pragma unroll
+        for (int np = 0; np < D / 16; ++np)
+          ldsm_x4_t(fb[np], vs + km_off<KM_TILE>(wr0 + (m8 & 1) * 8 + r8, 2 * np + (m8 >> 1)));
+        const bool col0 = t4 == 0;
+        const int ra = wr0 + g, rb = wr0 + g + 8;
+        const float xa = col0 && ra < x.valid ? cs[0] * scale_log2 : -INFINITY;
+        const float xb = col0 && rb < x.valid ? cs[2] * scale_log2 : -INFINITY;
+        if (col0) {  // raw logits to the ring (columns j0 + r)
+          if (ra < x.valid) ring_row[x.j0 + ra] = xa;
+          if (rb < x.valid) ring_row[x.j0 + rb] = xb;
+        }
+        if (compressed == 1 && lane < RPW && wr0 + lane < x.valid)
+          S.ring_ids[(head_row(S, layer, h0) * S.window + slot) * S.sparse_cap + x.j0 + wr0 + lane] = id;
+        float tmax = fmaxf(xa, xb);
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+        const float m_new = fmaxf(m_run, tmax);
+        float pa = 0.f, pb = 0.f, corr = 1.f;
+        if (m_new != -INFINITY) {
+          corr = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
+          pa = xa == -INFINITY ? 0.f : fast_exp2(xa - m_new);
+          pb = xb == -INFINITY ? 0.f : fast_exp2(xb - m_new);
+          m_run = m_new;
+        }
+        l_part = l_part * corr + (pa + pb);
+        if (corr != 1.f) {  // (uniform over the warp)
+#pragma unroll
+          for (int mt = 0; mt < D / 16; ++mt) {
+            o[mt][0] *= corr;
+            o[mt][2] *= corr;
+          }
+        }
+        // P^T as the B column: lane t4 of row group 0 takes rows 2t4, 2t4+1 (b0)
+        // and 8+2t4, 9+2t4 (b1) from the lanes 8 t4 and 8 t4 + 4 that hold them
+        const float va = __shfl_sync(0xffffffffu, pa, 8 * t4), vb = __shfl_sync(0xffffffffu, pa, 8 * t4 + 4);
+        const float vc = __shfl_sync(0xffffffffu, pb, 8 * t4), vd = __shfl_sync(0xffffffffu, pb, 8 * t4 + 4);
+        const uint32_t b0 = g == 0 ? pack_bf16(va, vb) : 0u, b1 = g == 0 ? pack_bf16(vc, vd) : 0u;
+        // O^T += V^T P^T: m-tile mt = dims [16 mt, +16); column 0 in lanes t4 == 0
+#pragma unroll
+        for (int mt = 0; mt < D / 16; ++mt) mma_16816_a4(o[mt], fb[mt][0], fb[mt][2], fb[mt][1], fb[mt][3], b0, b1);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[st]);
+        if (rec && tid == 0 && i < 4) rec[11 + i] = gtime();
+        continue;
+      }
       // S = Q K^T over this warp's rows (n-tile n = rows wr0 + 8n .. +7)
       // (all fragment loads first, then the MMAs in two independent chains per n-tile)
       uint32_t fb[D / 16][4];
@@ -732,16 +808,34 @@ __global__ void __launch_bounds__((NW * NG + 1) * 32) decode_mma_kernel(const __
       rec[3] = gtime();
       rec[5] = n_my;
     }
-    // quad sum of the row's softmax denominator
-    l_part += __shfl_xor_sync(0xffffffffu, l_part, 1);
-    l_part += __shfl_xor_sync(0xffffffffu, l_part, 2);
+    // quad sum of the row's softmax denominator (swapped form: the column-0 lanes)
+    if constexpr (SWAP) {
+      l_part += __shfl_xor_sync(0xffffffffu, l_part, 4);
+      l_part += __shfl_xor_sync(0xffffffffu, l_part, 8);
+      l_part += __shfl_xor_sync(0xffffffffu, l_part, 16);
+    } else {
+      l_part += __shfl_xor_sync(0xffffffffu, l_part, 1);
+      l_part += __shfl_xor_sync(0xffffffffu, l_part, 2);
+    }
     // (A) every consumer warp is done with the stage buffers (the producer warp
     // issued its last TMA long before; every tile was waited on by a consumer)
     tc::named_sync(1, 32 * KM_WARPS);
     float *wm = reinterpret_cast<float *>(sm);  // [W][8]
     float *wl = wm + KM_WARPS * 8;              // [W][8]
     float *wo = wl + KM_WARPS * 8;              // [W][8][D]
-    if (hv) {
+    if constexpr (SWAP) {  // O^T column 0: lane 4g holds dims 16 mt + g (c0) and 16 mt + 8 + g (c2)
+      if (lane == 0) {
+        wm[warp * 8] = m_run;
+        wl[warp * 8] = l_part;
+      }
+      if (t4 == 0) {
+#pragma unroll
+        for (int mt = 0; mt < D / 16; ++mt) {
+          wo[warp * 8 * D + 16 * mt + g] = o[mt][0];
+          wo[warp * 8 * D + 16 * mt + 8 + g] = o[mt][2];
+        }
+      }
+    } else if (hv) {
       if (t4 == 0) {
         wm[warp * 8 + g] = m_run;
         wl[warp * 8 + g] = l_part;
