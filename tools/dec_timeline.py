@@ -53,10 +53,7 @@ def show(kind):
               f"(max {rel(3).max():5.2f}) | partial {np.median(rel(4)):5.2f} (max {rel(4).max():5.2f}) | "
               f"fence1 {np.median(rel(8)):5.2f} (max {rel(8).max():5.2f}) | ticket {np.median(rel(9)):5.2f} (max {rel(9).max():5.2f}) | "
               f"fence2 {((last[:, 10] - t0) / 1e3).max() if len(last) else float('nan'):5.2f} | "
-              f"tiles@ {' '.join(f'{np.median((r[r[:, 11 + k] != 0][:, 11 + k] - t0) / 1e3):5.2f}' for k in range(3))} "
-              f"t0 phases wait->S {np.median((r[:, 11] - r[:, 2]) / 1e3):5.2f} S->P {np.median((r[:, 12] - r[:, 11]) / 1e3):5.2f} "
-              f"P->PV {np.median((r[:, 13] - r[:, 12]) / 1e3):5.2f} PV->end {np.median((r[:, 14] - r[:, 13]) / 1e3):5.2f} "
-              f"t1 {np.median((r[:, 15] - r[:, 14]) / 1e3):5.2f} | "
+              f"tiles@ {' '.join(f'{np.median((r[r[:, 11 + k] != 0][:, 11 + k] - t0) / 1e3):5.2f}' for k in range(3))} | "
               f"staged {stg.max():5.2f} | combined {((last[:, 6] - t0) / 1e3).max() if len(last) else float('nan'):5.2f} | tiles {r[:, 5].min()}-{r[:, 5].max()} "
               f"| SMs used {int((sms > 0).sum())}, max CTAs/SM {int(sms.max())}")
 
