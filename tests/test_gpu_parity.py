@@ -263,8 +263,12 @@ DECODE = ["decode_small", "decode_window_gt_interval", "decode_warmup_lt_window"
           "decode_huge_budget", "decode_gqa7", "decode_gqa8", "decode_long"]
 
 
+@pytest.mark.parametrize("archive", [False, True])
 @pytest.mark.parametrize("name", DECODE)
-def test_progressive_decode_matches_reference(cuda_lib, golden, name):
+def test_progressive_decode_matches_reference(cuda_lib, golden, name, archive):
+    """archive=True: the engine's step path (q read from the Q archive at the
+    device length; with interval >= window the observation rows record
+    (n_a, lo) and events take K7's working-set path, select_ws_kernel)."""
     c = golden.case(name)
     spec = SynthSpec(**c["spec"])
     Q, K, V = layer_qkv_numpy(spec, layer=0)
@@ -285,6 +289,11 @@ def test_progressive_decode_matches_reference(cuda_lib, golden, name):
 
     def source(t, length):
         return [(qd[:, length].contiguous(), kd, vd)]
+
+    if archive:
+        stack.derived_ids = c["budget"] is not None and c["interval"] >= W
+        stack.step = lambda li, q, k, v, compressed, max_cols, out, stream=None: stack.step_archive(
+            li, qd, k, v, compressed, max_cols, out, pdl=False, stream=stream)
 
     from paper_2507_13681_b200.opcount import OpCounter
 
