@@ -249,9 +249,10 @@ class SessionEngine:
             self._ready = torch.zeros(shape.n_q, dtype=torch.int32, device=device)
             self._epoch = 0
             # below this context the layer's GPU work is too short to pay for the groups'
-            # extra launches and per-call hooks (measured: C2 turn 3 at 15K keys only 2 ms
-            # faster without hooks and slower with bench.py's; C5 turn 10 at 101K keys 19 % faster)
-            self._overlap_min = int(_os.environ.get("LS_K5_OVERLAP_MIN", "24000"))
+            # extra launches (measured: C2 turn 1 at 5K keys 16 -> 36 ms, turn 2 at 10K
+            # neutral, turn 3 at 15K 49.5 -> 47.0 ms; C3 turn 2 at 16.6K 71.2 -> 66.6 ms;
+            # C5 turn 10 at 101K keys 19 % faster)
+            self._overlap_min = int(_os.environ.get("LS_K5_OVERLAP_MIN", "12000"))
         self.clear_logs()
 
     def clear_logs(self):
