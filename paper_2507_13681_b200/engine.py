@@ -327,7 +327,10 @@ class SessionEngine:
             if self.head_groups > 1:
                 plans, out, cells, tiles = self._layer_groups(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
                                                               store.q.stride(1), stream)
-            elif self._overlap and n_total >= self._overlap_min:
+            elif self._overlap and n_total >= self._overlap_min and (layer_ready is None or n_total >= 2 * self._overlap_min):
+                # (with per-layer host inputs streaming in, layer_ready, the head groups'
+                # streams contend with the copies: kept for the longest contexts only --
+                # measured C2 turn 3 end to end 54 -> 63 ms with them)
                 plans, out, cells, tiles = self._layer_overlap(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
                                                                store.q.stride(1), stream)
             else:
