@@ -130,6 +130,25 @@ __device__ __forceinline__ float poly_exp2(float x) {
   return x < -126.f ? 0.f : __int_as_float(bits);
 }
 
+// 2^x on the FMA / integer pipes at fp32 accuracy: the same range reduction as
+// poly_exp2, 2^f on [-0.5, 0.5] by a degree-6 near-minimax polynomial (max
+// relative error 1.0e-7 with fp32 Horner, within ex2.approx's 2^-22 bound).
+// Lets a share of the exponentials bypass the MUFU / MIO path.
+__device__ __forceinline__ float poly6_exp2(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float j = __fadd_rn(xc, 12582912.f);
+  const float n = __fsub_rn(j, 12582912.f);
+  const float f = xc - n;
+  float p = fmaf(f, 1.5345795e-4f, 1.3399932e-3f);
+  p = fmaf(p, f, 9.6184891e-3f);
+  p = fmaf(p, f, 5.5503286e-2f);
+  p = fmaf(p, f, 2.4022646e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.0f);
+  const int bits = __float_as_int(p) + (__float_as_int(j) << 23);
+  return x < -126.f ? 0.f : __int_as_float(bits);
+}
+
 // first index i in [0, n) with a[i] >= x (a sorted ascending)
 template <typename T>
 __device__ __forceinline__ int lower_bound_dev(const T *a, int n, T x) {
