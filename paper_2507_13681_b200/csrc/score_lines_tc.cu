@@ -630,14 +630,16 @@ __global__ void __launch_bounds__(LINES_THREADS + 32, 1) k1_lines_kernel(const _
       if (lane == 0) tc::mbar_arrive(&s_free[t & 1]);
       float4 *prow = reinterpret_cast<float4 *>(Pb0 + (t & 1) * PBUF + row * LDP + cblk);
       if (row_ok && lim >= 31) {
-        // every fourth exponential on the FMA pipe (poly6_exp2, fp32 accuracy): the
+        // every eighth exponential on the FMA pipe (poly6_exp2, fp32 accuracy): the
         // MUFU ex2, the P stores and the TMEM loads share the MIO queue, the phase's
-        // top stall (0.427 -> 0.419 ms/layer at C2 turn 3, identical plans; half
-        // the exponentials there measured slower, 0.449)
+        // top stall (C2 turn 3: 0.427 -> 0.414 ms/layer, C5 turn 10: 1.341 -> 1.318 ms,
+        // identical plans; a quarter 0.419 / 1.341, three eighths 0.427 / 1.359, half 0.449)
 #define K1E(u) fast_exp2(fmaf(sv[u], p.scale_log2, -mr))
 #define K1F(u) poly6_exp2(fmaf(sv[u], p.scale_log2, -mr))
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) prow[j / 4] = make_float4(K1E(j), K1E(j + 1), K1E(j + 2), K1F(j + 3));
+        for (int j = 0; j < 32; j += 4)
+          prow[j / 4] = (j & 4) ? make_float4(K1E(j), K1E(j + 1), K1E(j + 2), K1F(j + 3))
+                                : make_float4(K1E(j), K1E(j + 1), K1E(j + 2), K1E(j + 3));
 #undef K1E
 #undef K1F
       } else {
