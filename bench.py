@@ -437,15 +437,15 @@ def main():
     # K3/K5 head-group overlap so every kernel's time is its own
     recs.clear()
     eng.clear_logs()
-    overlap_min = getattr(eng, "_overlap_min", None)
+    overlap_min = getattr(eng, "overlap_min", None)
     if overlap_min is not None:
-        eng._overlap_min = 1 << 30
+        eng.overlap_min = 1 << 30
     timing["on"] = True
     dialogue([])
     torch.cuda.synchronize()
     timing["on"] = False
     if overlap_min is not None:
-        eng._overlap_min = overlap_min
+        eng.overlap_min = overlap_min
     if world > 1:
         dist.barrier()
     dialogue_ms = total_ms / args.steps  # the breakdown pass covers one dialogue

@@ -252,7 +252,8 @@ class SessionEngine:
             # extra launches (measured: C2 turn 1 at 5K keys 16 -> 36 ms, turn 2 at 10K
             # neutral, turn 3 at 15K 49.5 -> 47.0 ms; C3 turn 2 at 16.6K 71.2 -> 66.6 ms;
             # C5 turn 10 at 101K keys 19 % faster)
-            self._overlap_min = int(_os.environ.get("LS_K5_OVERLAP_MIN", "12000"))
+            # (public: contexts of at least this many keys use the head-group overlap)
+            self.overlap_min = int(_os.environ.get("LS_K5_OVERLAP_MIN", "12000"))
         self.clear_logs()
 
     def clear_logs(self):
@@ -327,7 +328,7 @@ class SessionEngine:
             if self.head_groups > 1:
                 plans, out, cells, tiles = self._layer_groups(l, qb, kl, vl, rows[l], n_new, n_total, surv, n_seed,
                                                               store.q.stride(1), stream)
-            elif self._overlap and n_total >= self._overlap_min and (layer_ready is None or n_total >= 2 * self._overlap_min):
+            elif self._overlap and n_total >= self.overlap_min and (layer_ready is None or n_total >= 2 * self.overlap_min):
                 # (with per-layer host inputs streaming in, layer_ready, the head groups'
                 # streams contend with the copies: kept for the longest contexts only --
                 # measured C2 turn 3 end to end 54 -> 63 ms with them)
