@@ -818,10 +818,18 @@ def run_e2e(args, cfg, eng, store, blocks, shard, gather):
                 if it > 0:
                     h2d += src.numel() * 2
 
-            def run_sink(t0, outs):  # every run's outputs (all steps, all layers) back to the host
-                outs_host[t0:t0 + outs.shape[0]].copy_(outs, non_blocking=True)
+            def run_sink(t0, outs):
+                # every run's outputs (all steps, all layers) back to the host on the
+                # copy stream while the next run computes (each run writes its own
+                # slots of the engine's output ring; the turn waits for the copies)
+                ev_run = torch.cuda.Event()
+                ev_run.record(stream)
+                d2h_s.wait_event(ev_run)
+                with torch.cuda.stream(d2h_s):
+                    outs_host[t0:t0 + outs.shape[0]].copy_(outs, non_blocking=True)
 
             eng.decode(store, n_total, cfg["max_new"], run_sink=run_sink)
+            stream.wait_stream(d2h_s)  # every step's output is on the host
             if it > 0:
                 d2h += outs_host.numel() * 2
             e2.record(stream)
